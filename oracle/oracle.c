@@ -1,0 +1,265 @@
+/*
+ * MAPA CPU oracle in plain C -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  It shares no code with the
+ * CUDA path (paper_2110_03214_b200/csrc): it is the same plain definition as
+ * oracle/mapa_oracle.py, written in C so that the large configurations finish.
+ *
+ * Definition followed (PAPER.md / SPEC.md citations):
+ *   - matches: every injective map V(P)->F is an embedding because the hardware
+ *     graph is complete; matches are deduplicated by
+ *     (device set, used-edge set) (reading A2);
+ *   - Eq. 1 AggBW = sum of w over used edges;
+ *   - census (x,y,z) over used edges, 25 and 20 both count toward y
+ *     (reading A5);
+ *   - Eq. 2 predicted EffBW with Table 4 theta, double;
+ *   - Eq. 3 PreservedBW = sum of w over pairs of free devices not in S
+ *     (reading A6), direct double loop;
+ *   - selection: strict '>' over matches in lex order of (sorted device tuple,
+ *     sorted used-edge list) = Alg. 1 first-wins loop + SPEC tie-break
+ *     (SPEC S:349).
+ *
+ * Parallelism: pthreads over the index a of the first device S[0] = F[a] of
+ * each lexicographic k-subset; per-a results are combined in increasing a,
+ * strict '>', so the result is identical for every thread count.
+ */
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+    int32_t status;        /* 0 ok, 1 no capacity, <0 error */
+    int32_t k;
+    uint32_t device_mask;  /* bit d = device d (0-based) */
+    int8_t mapping[8];     /* mapping[i] = device of pattern vertex i */
+    int32_t m;
+    int32_t used[28][2];   /* sorted used edges (lo, hi) */
+    int32_t x, y, z, agg_bw, preserved_bw;
+    int32_t pad;
+    double pred_effbw;
+    double score;
+    uint64_t raw, distinct;
+} oracle_result;
+
+/* Table 4 */
+static const double THETA[14] = {16.396, 4.536, 1.556, -20.694, -9.467, 7.615, -7.973,
+                                 12.733, -4.195, -8.413, 62.851, 27.418, -5.114, -46.973};
+
+double oracle_eq2(int x, int y, int z) {
+    const double *t = THETA;
+    double X = x, Y = y, Z = z;
+    return t[0] * X + t[1] * Y + t[2] * Z + t[3] / (X + 1) + t[4] / (Y + 1) + t[5] / (Z + 1) +
+           t[6] * X * Y + t[7] * Y * Z + t[8] * Z * X + t[9] / (X * Y + 1) + t[10] / (Y * Z + 1) +
+           t[11] / (Z * X + 1) + t[12] * X * Y * Z + t[13] / (X * Y * Z + 1);
+}
+
+typedef struct {
+    int n, k, m, selector, sensitive;
+    const int32_t *w;     /* n*n weights */
+    const int32_t *pe;    /* 2m pattern edges */
+    int nf;
+    int F[64];
+} ctx_t;
+
+typedef struct {
+    int found;
+    double score;
+    int S[8];
+    int pi[8];
+    int E[28][2];
+    int agg, x, y, z, pres;
+    double eff;
+    uint64_t raw, distinct;
+} unit_t;
+
+typedef struct {
+    uint16_t code[28];
+    int8_t pi[8];
+    int32_t idx;
+    int m;
+} entry_t;
+
+static int cmp_entry(const void *a, const void *b) {
+    const entry_t *p = (const entry_t *)a, *q = (const entry_t *)b;
+    for (int i = 0; i < p->m; i++) {
+        if (p->code[i] != q->code[i]) return p->code[i] < q->code[i] ? -1 : 1;
+    }
+    return p->idx < q->idx ? -1 : (p->idx > q->idx);
+}
+
+/* std::next_permutation on a small int array; returns 0 after the last. */
+static int next_perm(int *a, int n) {
+    int i = n - 2;
+    while (i >= 0 && a[i] >= a[i + 1]) i--;
+    if (i < 0) return 0;
+    int j = n - 1;
+    while (a[j] <= a[i]) j--;
+    int t = a[i]; a[i] = a[j]; a[j] = t;
+    for (int l = i + 1, r = n - 1; l < r; l++, r--) { t = a[l]; a[l] = a[r]; a[r] = t; }
+    return 1;
+}
+
+static void score_match(const ctx_t *c, const int *S, const entry_t *e, unit_t *u) {
+    int n = c->n;
+    int agg = 0, x = 0, y = 0, z = 0;
+    for (int i = 0; i < c->m; i++) {
+        int lo = e->code[i] >> 6, hi = e->code[i] & 63;
+        int b = c->w[lo * n + hi];
+        agg += b;                                   /* Eq. 1 */
+        if (b == 50) x++;                           /* census */
+        else if (b == 25 || b == 20) y++;
+        else z++;
+    }
+    double eff = oracle_eq2(x, y, z);               /* Eq. 2 */
+    int inS[64] = {0};
+    for (int i = 0; i < c->k; i++) inS[S[i]] = 1;
+    int pres = 0;                                   /* Eq. 3 */
+    for (int i = 0; i < c->nf; i++) {
+        if (inS[c->F[i]]) continue;
+        for (int j = i + 1; j < c->nf; j++) {
+            if (inS[c->F[j]]) continue;
+            pres += c->w[c->F[i] * n + c->F[j]];
+        }
+    }
+    double s;
+    if (c->selector == 0) s = agg;
+    else if (c->selector == 1) s = c->sensitive ? eff : pres;
+    else s = 0.0;
+    if (!u->found || s > u->score) {
+        u->found = 1;
+        u->score = s;
+        for (int i = 0; i < c->k; i++) { u->S[i] = S[i]; u->pi[i] = e->pi[i]; }
+        for (int i = 0; i < c->m; i++) { u->E[i][0] = e->code[i] >> 6; u->E[i][1] = e->code[i] & 63; }
+        u->agg = agg; u->x = x; u->y = y; u->z = z; u->pres = pres; u->eff = eff;
+    }
+}
+
+static void process_subset(const ctx_t *c, const int *S, entry_t *ent, unit_t *u) {
+    int k = c->k, m = c->m;
+    int perm[8];
+    memcpy(perm, S, sizeof(int) * k);
+    int cnt = 0;
+    do {                                            /* permutations in lex order */
+        u->raw++;
+        entry_t *e = &ent[cnt];
+        e->m = m;
+        e->idx = cnt;
+        for (int i = 0; i < k; i++) e->pi[i] = (int8_t)perm[i];
+        for (int i = 0; i < m; i++) {
+            int a = perm[c->pe[2 * i]], b = perm[c->pe[2 * i + 1]];
+            int lo = a < b ? a : b, hi = a < b ? b : a;
+            uint16_t code = (uint16_t)(lo * 64 + hi);
+            int j = i;                              /* insertion sort */
+            while (j > 0 && e->code[j - 1] > code) { e->code[j] = e->code[j - 1]; j--; }
+            e->code[j] = code;
+        }
+        cnt++;
+    } while (next_perm(perm, k));
+    qsort(ent, cnt, sizeof(entry_t), cmp_entry);    /* sorted(seen), first pi kept */
+    for (int i = 0; i < cnt; i++) {
+        if (i > 0 && memcmp(ent[i].code, ent[i - 1].code, sizeof(uint16_t) * m) == 0) continue;
+        u->distinct++;
+        score_match(c, S, &ent[i], u);
+    }
+}
+
+static void process_unit(const ctx_t *c, int a, entry_t *ent, unit_t *u) {
+    memset(u, 0, sizeof(*u));
+    int k = c->k, nf = c->nf;
+    int idx[8];
+    int S[8];
+    idx[0] = a;
+    for (int i = 1; i < k; i++) idx[i] = a + i;
+    if (k > 0 && idx[k - 1] >= nf) return;
+    for (;;) {
+        for (int i = 0; i < k; i++) S[i] = c->F[idx[i]];
+        process_subset(c, S, ent, u);
+        int i = k - 1;                              /* next combination, idx[0] fixed */
+        while (i >= 1 && idx[i] == nf - k + i) i--;
+        if (i < 1) break;
+        idx[i]++;
+        for (int j = i + 1; j < k; j++) idx[j] = idx[j - 1] + 1;
+    }
+}
+
+typedef struct {
+    const ctx_t *c;
+    unit_t *units;
+    int lo, hi;
+    int next;
+    pthread_mutex_t mu;
+} pool_t;
+
+static size_t fact(int k) { size_t f = 1; for (int i = 2; i <= k; i++) f *= i; return f; }
+
+static void *worker(void *arg) {
+    pool_t *p = (pool_t *)arg;
+    entry_t *ent = (entry_t *)malloc(sizeof(entry_t) * fact(p->c->k));
+    for (;;) {
+        pthread_mutex_lock(&p->mu);
+        int a = p->next++;
+        pthread_mutex_unlock(&p->mu);
+        if (a >= p->hi) break;
+        process_unit(p->c, a, ent, &p->units[a - p->lo]);
+    }
+    free(ent);
+    return NULL;
+}
+
+/* Brute-force allocation.  w: n*n weights (GB/s, diagonal ignored); busy: bit d
+ * busy; pe: 2m pattern edges (0-based); selector 0 GREEDY, 1 PRESERVE, 2 BASELINE.
+ * a_lo/a_hi restrict S[0] to F[a_lo..a_hi) (bounded samples); a_hi < 0 = all.
+ * Returns 0, or <0 on invalid arguments. */
+int oracle_allocate(int n, const int32_t *w, uint32_t busy, int k, int m, const int32_t *pe,
+                    int selector, int sensitive, int nthreads, int a_lo, int a_hi,
+                    oracle_result *out) {
+    memset(out, 0, sizeof(*out));
+    if (n < 1 || n > 32 || k < 1 || k > 8 || m < 0 || m > 28) return -1;
+    ctx_t c;
+    c.n = n; c.k = k; c.m = m; c.selector = selector; c.sensitive = sensitive; c.w = w; c.pe = pe;
+    c.nf = 0;
+    for (int d = 0; d < n; d++)
+        if (!((busy >> d) & 1u)) c.F[c.nf++] = d;
+    out->k = k;
+    out->m = m;
+    if (k > c.nf) { out->status = 1; return 0; }
+    int lo = a_lo < 0 ? 0 : a_lo;
+    int hi = a_hi < 0 ? c.nf - k + 1 : a_hi;
+    if (hi > c.nf - k + 1) hi = c.nf - k + 1;
+    if (lo >= hi) { out->status = 1; return 0; }
+    pool_t p;
+    p.c = &c; p.lo = lo; p.hi = hi; p.next = lo;
+    p.units = (unit_t *)calloc(hi - lo, sizeof(unit_t));
+    pthread_mutex_init(&p.mu, NULL);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; t++) pthread_create(&th[t], NULL, worker, &p);
+    for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+    pthread_mutex_destroy(&p.mu);
+    unit_t best;
+    memset(&best, 0, sizeof(best));
+    uint64_t raw = 0, distinct = 0;
+    for (int a = lo; a < hi; a++) {                 /* combine in lex order, strict '>' */
+        unit_t *u = &p.units[a - lo];
+        raw += u->raw;
+        distinct += u->distinct;
+        if (u->found && (!best.found || u->score > best.score)) best = *u;
+    }
+    free(p.units);
+    out->raw = raw;
+    out->distinct = distinct;
+    out->status = 0;
+    out->score = best.score;
+    out->device_mask = 0;
+    for (int i = 0; i < k; i++) {
+        out->device_mask |= 1u << best.S[i];
+        out->mapping[i] = (int8_t)best.pi[i];
+    }
+    for (int i = 0; i < m; i++) { out->used[i][0] = best.E[i][0]; out->used[i][1] = best.E[i][1]; }
+    out->x = best.x; out->y = best.y; out->z = best.z;
+    out->agg_bw = best.agg; out->preserved_bw = best.pres; out->pred_effbw = best.eff;
+    return 0;
+}
