@@ -1,0 +1,246 @@
+/*
+ * mapa.h — C-ABI of libmapa.so, the B200-native MAPA hot path
+ * (Multi-Accelerator Pattern Allocation, SC'21, arXiv 2110.03214).
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n
+ * (section / equation / algorithm named beside each).  Device ids are 0-based
+ * here (the paper's and SPEC's 1-based id minus 1; lexicographic order is
+ * unchanged).  No C++ exception ever crosses this ABI; every entry point
+ * returns a mapa_status and leaves outputs and state untouched on error
+ * (S:74).  The message of the last error on the calling thread is available
+ * from mapa_last_error().
+ *
+ * What the hot path computes:
+ *   enumerate every injective map f: V(P) -> F of the pattern P into the free
+ *   devices F of the hardware graph G (complete; subgraph matching
+ *   §3.3), score it (Eq. 1 AggBW P:575-577, Eq. 2 predicted EffBW
+ *   P:605-612 over the link census P:602, Eq. 3 PreservedBW P:714-716) and
+ *   return the policy's argmax (Greedy P:777, Preserve Alg. 1)
+ *   under SPEC's tie-break: lex-smallest sorted device tuple, then
+ *   lex-smallest sorted used-edge list.  The reported mapping
+ *   is the lex-first mapping of the winning (device set, edge set) match.
+ *
+ * Two enumeration modes (flags):
+ *   default        canonical: one leaf per Aut(P)-orbit (lex-leader symmetry
+ *                  breaking) = SPEC's deduplicated matches;
+ *                  leaves scored = distinct matches = P(|F|,k)/|Aut(P)|.
+ *   MAPA_F_RAW     every injective map is scored; leaves = P(|F|,k).
+ * Both modes return the identical decision.
+ *
+ * Memory: every device pointer is caller-owned (e.g. a torch CUDA tensor);
+ * streams are cudaStream_t passed as void*.  Device-side entry points are
+ * asynchronous on that stream and never synchronise.
+ */
+#ifndef MAPA_H
+#define MAPA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t mapa_status;
+#define MAPA_OK 0
+#define MAPA_NO_CAPACITY 1      /* signal, not an error: |F| < k */
+#define MAPA_E_INVALID_ARG (-1)
+#define MAPA_E_PARSE (-2)       /* topology text: message names line/field */
+#define MAPA_E_ALREADY_BUSY (-3) /* claim of a busy device, state unchanged */
+#define MAPA_E_NOT_BUSY (-4)    /* release of a free device */
+#define MAPA_E_ID_RANGE (-5)    /* device id out of range */
+#define MAPA_E_UNSUPPORTED (-6) /* N > 32, k > 8, or key budget 15+W+C(k,2) > 63 */
+#define MAPA_E_CUDA (-7)        /* CUDA runtime error (message has the CUDA string) */
+#define MAPA_E_DISCONNECTED (-8) /* disconnected pattern, k > 1 */
+#define MAPA_E_INTERNAL (-10)   /* self-check failed (decoded key inconsistent) */
+
+/* Selectors (P:777 Greedy; Alg. 1 P:681-706 Preserve; P:777 Baseline). */
+enum { MAPA_SEL_GREEDY = 0, MAPA_SEL_PRESERVE = 1, MAPA_SEL_BASELINE = 2 };
+
+/* Flags. */
+enum {
+    MAPA_F_COMMIT = 1,              /* mapa_allocate: mark the chosen devices busy (§3.6) */
+    MAPA_F_RAW = 2,                 /* score every injective map (no symmetry breaking) */
+    MAPA_F_ALLOW_DISCONNECTED = 4   /* mapa_load_pattern: accept disconnected patterns */
+};
+
+/* Pattern shapes of Fig. 4 as constructed by SPEC make_pattern. */
+enum { MAPA_SHAPE_RING = 0, MAPA_SHAPE_TREE = 1, MAPA_SHAPE_RINGTREE = 2,
+       MAPA_SHAPE_FULL = 3, MAPA_SHAPE_EDGELESS = 4 };
+
+typedef struct mapa_topology mapa_topology; /* immutable graph + mutable busy mask */
+typedef struct mapa_pattern mapa_pattern;   /* immutable compiled pattern descriptor */
+
+/* A decision (SPEC AllocationDecision S:322-325), host memory. */
+typedef struct {
+    int32_t status;          /* MAPA_OK or MAPA_NO_CAPACITY */
+    int32_t k;               /* pattern vertices */
+    uint32_t device_mask;    /* bit d = device d allocated */
+    int8_t mapping[8];       /* mapping[i] = device of pattern vertex i (lex-first of the match) */
+    int32_t m;               /* pattern edges */
+    int32_t used[28][2];     /* sorted used edges (lo, hi) = E(P) ∩ E(M) realised */
+    int32_t x, y, z;         /* link census: double / single(25|20) / PCIe used edges */
+    int32_t agg_bw;          /* Eq. 1, GB/s */
+    int32_t preserved_bw;    /* Eq. 3, GB/s */
+    int32_t score;           /* selector score as packed in the key (AggBW, Eq. 2 rank, PreservedBW, 0) */
+    double pred_effbw;       /* Eq. 2, double */
+    uint64_t raw_embeddings;   /* P(|F|,k) injective maps (counted in RAW mode) */
+    uint64_t distinct_matches; /* P(|F|,k)/|Aut(P)| (counted in canonical mode) */
+    uint64_t leaves_scored;    /* leaves the kernel actually scored */
+    uint64_t key;            /* packed argmax key (see mapa_record) */
+} mapa_decision;
+
+/* Device-side query, 16 bytes (coalesced uint4 load). */
+typedef struct {
+    uint32_t busy;       /* bit d = device d busy */
+    uint32_t pattern;    /* index into the pattern array of the call */
+    int32_t selector;    /* MAPA_SEL_* */
+    int32_t sensitive;   /* PRESERVE: 1 = bandwidth sensitive (Alg. 1) */
+} mapa_query;
+
+/* Device-side result record, 32 bytes.
+ *   key = score << (W + C(k,2)) | brev_W(S) << C(k,2) | ecode, where W is the
+ *   topology width (8/16/32), brev_W(S) sets bit W-1-d for every chosen
+ *   device d (larger = lex-smaller device tuple) and ecode sets bit
+ *   C(k,2)-1-p for every used edge whose endpoint ranks inside S form the
+ *   p-th pair in lex order (larger = lex-smaller used-edge list).  key 0 =
+ *   no match (no capacity).  Max over keys = the policy's choice. */
+typedef struct {
+    uint64_t key;
+    uint64_t leaves;     /* leaves scored */
+    uint32_t ctr;        /* work-item counter (scratch, zeroed by the launch) */
+    uint32_t status;     /* 0 ok; nonzero = device-side argument error */
+    uint64_t reserved;
+} mapa_record;
+
+/* Trace op (C2 replay): op 0 = ALLOC job, 1 = RELEASE job. */
+typedef struct {
+    int32_t op;
+    int32_t job;
+} mapa_trace_op;
+
+/* ---------------------------------------------------------------- topology */
+
+/* Builtin name (dgx1v, dgx1p, summit, torus2d16, cubemesh16: S:43-51,
+ * S:105-110) when is_text == 0, else the topology text format of DESIGN.md
+ * (fields of S:115: name, devices, sockets, link a b class; 1-based ids;
+ * unlisted pairs are PCIe).  N <= 32.  *out owned by the caller,
+ * freed with mapa_free_topology.  Errors: PARSE (message names the line),
+ * ID_RANGE, UNSUPPORTED (N > 32), INVALID_ARG. */
+mapa_status mapa_load_topology(const char *builtin_or_text, int32_t is_text, mapa_topology **out);
+void mapa_free_topology(mapa_topology *t);
+
+/* N, padded width W (8, 16 or 32), link bandwidth matrix bw[N*N] (GB/s,
+ * diagonal 0; may be NULL) and the busy mask. */
+mapa_status mapa_topology_info(const mapa_topology *t, int32_t *n, int32_t *width, int32_t *bw,
+                               uint32_t *busy);
+
+/* State management (§3.6; SPEC allocate_devices S:70-78,
+ * release_devices S:79-87).  claim: ALREADY_BUSY / ID_RANGE with state
+ * unchanged; release: NOT_BUSY / ID_RANGE. set_busy replaces the mask
+ * (checkpoint/restore). */
+mapa_status mapa_claim(mapa_topology *t, uint32_t device_mask);
+mapa_status mapa_release(mapa_topology *t, uint32_t device_mask);
+mapa_status mapa_set_busy(mapa_topology *t, uint32_t busy);
+
+/* ---------------------------------------------------------------- patterns */
+
+/* Pattern from an edge list (2*m ints, 0-based vertex ids < k).  1 <= k <= 8,
+ * 0 <= m <= C(k,2).  Duplicate edges and self loops: INVALID_ARG.
+ * Disconnected with k > 1: DISCONNECTED unless MAPA_F_ALLOW_DISCONNECTED
+ * (S:210).  Compiles Aut(P) (brute force over k!), the lex-leader symmetry
+ * constraints and the Eq. 2 rank table for m. */
+mapa_status mapa_load_pattern(int32_t k, int32_t m, const int32_t *edges, uint32_t flags,
+                              mapa_pattern **out);
+/* SPEC make_pattern: Ring (k=2: one edge; k=1: INVALID_ARG),
+ * Tree (children of i are 2i+1, 2i+2), RingTree (union), Full, Edgeless. */
+mapa_status mapa_make_pattern(int32_t shape, int32_t k, mapa_pattern **out);
+void mapa_free_pattern(mapa_pattern *p);
+
+typedef struct {
+    int32_t k, m;
+    int32_t aut_order;       /* |Aut(P)| */
+    uint8_t back[8];         /* back[j] bit i: edge (i,j), i < j */
+    uint8_t lex_src[8];      /* lex_src[u] bit i: canonical mode requires f(i) < f(u) */
+    int32_t edges[28][2];    /* normalised (a<b), sorted */
+} mapa_pattern_info;
+mapa_status mapa_get_pattern_info(const mapa_pattern *p, mapa_pattern_info *out);
+
+/* Eq. 2 with Table 4 theta, double. */
+double mapa_pred_effbw(int32_t x, int32_t y, int32_t z);
+/* Dense rank of Eq. 2 over the censuses with x+y+z = m: out[x*(m+1)+y]
+ * (entries with x+y > m are 0).  m <= 28. */
+mapa_status mapa_effbw_rank_table(int32_t m, uint16_t *out);
+
+/* ---------------------------------------------------------- single query */
+
+/* One allocation end to end, host buffers: stages the query (16 B) to the
+ * device from pinned memory, launches the enumerate-score-argmax kernel on
+ * cuda_stream (NULL = default stream), reads the 32-B record back, decodes it
+ * on the host and, with MAPA_F_COMMIT, marks the devices busy.  Blocks until
+ * the stream reaches the copy.  Returns MAPA_OK, MAPA_NO_CAPACITY (out->status
+ * too) or an error. Not thread-safe per topology handle. */
+mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selector,
+                          int32_t bw_sensitive, uint32_t flags, void *cuda_stream,
+                          mapa_decision *out);
+
+/* Device-resident launch of one query's shard: zeroes d_record and
+ * enumerates the work items i with i % world == rank of the query whose busy
+ * mask is read from d_query->busy on the device (the other d_query fields are
+ * ignored; p, selector and sensitive choose the kernel).  rank = 0, world = 1
+ * for the whole query.  Asynchronous on cuda_stream.  Records of the R shards
+ * combine by max(key), sum(leaves) (mapa_reduce_records or an NCCL
+ * MAX/SUM all-reduce), then mapa_decode gives the same decision for every R
+ * (S:369).  busy_hint: the busy mask if the host knows it (sizes the grid),
+ * else 0xFFFFFFFF. */
+mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
+                              int32_t sensitive, const mapa_query *d_query, mapa_record *d_record,
+                              uint32_t flags, int32_t rank, int32_t world, uint32_t busy_hint,
+                              void *cuda_stream);
+
+/* Host: combine n shard records (max key, sum leaves). */
+mapa_status mapa_reduce_records(const mapa_record *records, int32_t n, mapa_record *out);
+
+/* Host: decode a (combined) record into a decision for (busy, selector,
+ * sensitive, flags).  Recomputes census, AggBW, PreservedBW and Eq. 2 from
+ * the decoded (S, mapping) and checks them against the key's score. */
+mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint32_t busy,
+                        int32_t selector, int32_t bw_sensitive, uint32_t flags,
+                        const mapa_record *record, mapa_decision *out);
+
+/* ---------------------------------------------------------------- batches */
+
+/* nq independent queries (never committed; each carries its own busy mask),
+ * d_queries[nq] -> d_results[nq] records.  pats[npats] (npats <= 16, every
+ * pattern k <= 8 and sum of (m+1)^2 rank-table entries <= 4096).
+ * d_scratch: >= 64 bytes of device memory, used for the work counter.
+ * Asynchronous on cuda_stream.  A query with a bad pattern index or an
+ * unsupported key budget gets record.status = 1 and key 0. */
+mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *const *pats,
+                                int32_t npats, int64_t nq, const mapa_query *d_queries,
+                                mapa_record *d_results, void *d_scratch, uint32_t flags,
+                                void *cuda_stream);
+
+/* ----------------------------------------------------------- trace replay */
+
+/* C2: ntraces independent FIFO traces replayed entirely on the device, one
+ * CTA per trace.  Trace t has nops ops d_ops[t*nops ...] and njobs jobs
+ * d_jobs[t*njobs ...] (mapa_query with busy ignored, pattern/selector/
+ * sensitive per job).  ALLOC j: the kernel enumerates, scores and selects on
+ * the trace's current busy mask, stores the winning key in
+ * d_keys[t*njobs + j] and marks the devices busy; RELEASE j frees them
+ * (§3.6).  An ALLOC without capacity stores key 0 and leaves the state.
+ * Asynchronous. */
+mapa_status mapa_trace_replay(const mapa_topology *t, const mapa_pattern *const *pats,
+                              int32_t npats, int32_t ntraces, int32_t nops,
+                              const mapa_trace_op *d_ops, int32_t njobs, const mapa_query *d_jobs,
+                              uint64_t *d_keys, uint32_t flags, void *cuda_stream);
+
+/* Thread-local message of the last failing call on this thread. */
+const char *mapa_last_error(void);
+/* Library version string. */
+const char *mapa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MAPA_H */

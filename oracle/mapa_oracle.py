@@ -319,11 +319,13 @@ def device_mask(devs) -> int:
     return m
 
 
-def replay_trace(topo: Topology, jobs, ops, patterns, policy: str):
+def replay_trace(topo: Topology, jobs, ops, patterns, policy: str, allocate_fn=None):
     """Replays an ALLOC/RELEASE op list (workloads.fifo_ops) with MAPA state
     management (§3.6): allocate removes the chosen devices, release
     adds them back.  policy 'preserve' uses each job's sensitivity (Alg. 1);
-    'greedy' uses AggBW.  Returns {job: decision}."""
+    'greedy' uses AggBW.  allocate_fn defaults to allocate() (the C oracle's
+    coracle.allocate has the same signature).  Returns {job: decision}."""
+    alloc = allocate_fn or allocate
     busy = 0
     held = {}
     out = {}
@@ -332,9 +334,9 @@ def replay_trace(topo: Topology, jobs, ops, patterns, policy: str):
             job = jobs[j]
             k, pe = patterns[(job["shape"], job["k"])]
             if policy == "preserve":
-                d = allocate(topo, busy, k, pe, PRESERVE, bool(job["sensitive"]))
+                d = alloc(topo, busy, k, pe, PRESERVE, bool(job["sensitive"]))
             else:
-                d = allocate(topo, busy, k, pe, GREEDY, False)
+                d = alloc(topo, busy, k, pe, GREEDY, False)
             if d["status"] != "ok":
                 raise RuntimeError("trace admitted a job without capacity")
             m = device_mask(d["devices"])

@@ -1,0 +1,304 @@
+"""Thin Python binding of libmapa.so (include/mapa.h) — argument marshalling only.
+
+Every step of the hot path (enumerate, score, argmax) runs in the sm_100a
+kernels of ``csrc/esa.cu``; the host pieces (topology encode, pattern compile,
+key decode) are C++ in ``csrc/mapa_host.cpp``.  There is no Python or CPU
+fallback: if ``libmapa.so`` is missing the import fails loudly.  PyTorch is
+used only for device memory, streams and ``torch.distributed`` (see
+``dist.py``).
+
+Names follow the C-ABI (``mapa_allocate`` -> ``allocate`` etc.).  Device ids
+are 0-based (the paper's 1-based id - 1).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmapa.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(the MAPA hot path has no CPU fallback)")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+OK, NO_CAPACITY = 0, 1
+E_INVALID_ARG, E_PARSE, E_ALREADY_BUSY, E_NOT_BUSY, E_ID_RANGE = -1, -2, -3, -4, -5
+E_UNSUPPORTED, E_CUDA, E_DISCONNECTED, E_INTERNAL = -6, -7, -8, -10
+SEL_GREEDY, SEL_PRESERVE, SEL_BASELINE = 0, 1, 2
+F_COMMIT, F_RAW, F_ALLOW_DISCONNECTED = 1, 2, 4
+SHAPES = {"ring": 0, "tree": 1, "ringtree": 2, "full": 3, "edgeless": 4}
+
+
+class MapaError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"mapa status {status}: {msg}")
+        self.status = status
+
+
+class Decision(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("k", ctypes.c_int32), ("device_mask", ctypes.c_uint32),
+                ("mapping", ctypes.c_int8 * 8), ("m", ctypes.c_int32), ("used", (ctypes.c_int32 * 2) * 28),
+                ("x", ctypes.c_int32), ("y", ctypes.c_int32), ("z", ctypes.c_int32),
+                ("agg_bw", ctypes.c_int32), ("preserved_bw", ctypes.c_int32), ("score", ctypes.c_int32),
+                ("pred_effbw", ctypes.c_double), ("raw_embeddings", ctypes.c_uint64),
+                ("distinct_matches", ctypes.c_uint64), ("leaves_scored", ctypes.c_uint64),
+                ("key", ctypes.c_uint64)]
+
+
+class Query(ctypes.Structure):
+    _fields_ = [("busy", ctypes.c_uint32), ("pattern", ctypes.c_uint32), ("selector", ctypes.c_int32),
+                ("sensitive", ctypes.c_int32)]
+
+
+class Record(ctypes.Structure):
+    _fields_ = [("key", ctypes.c_uint64), ("leaves", ctypes.c_uint64), ("ctr", ctypes.c_uint32),
+                ("status", ctypes.c_uint32), ("reserved", ctypes.c_uint64)]
+
+
+class PatternInfo(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("m", ctypes.c_int32), ("aut_order", ctypes.c_int32),
+                ("back", ctypes.c_uint8 * 8), ("lex_src", ctypes.c_uint8 * 8),
+                ("edges", (ctypes.c_int32 * 2) * 28)]
+
+
+assert ctypes.sizeof(Query) == 16 and ctypes.sizeof(Record) == 32
+
+_vp = ctypes.c_void_p
+_S = ctypes.c_int32
+_SIGS = {
+    "mapa_load_topology": (_S, [ctypes.c_char_p, ctypes.c_int32, ctypes.POINTER(_vp)]),
+    "mapa_free_topology": (None, [_vp]),
+    "mapa_topology_info": (_S, [_vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_uint32)]),
+    "mapa_claim": (_S, [_vp, ctypes.c_uint32]),
+    "mapa_release": (_S, [_vp, ctypes.c_uint32]),
+    "mapa_set_busy": (_S, [_vp, ctypes.c_uint32]),
+    "mapa_load_pattern": (_S, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_uint32,
+                               ctypes.POINTER(_vp)]),
+    "mapa_make_pattern": (_S, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_vp)]),
+    "mapa_free_pattern": (None, [_vp]),
+    "mapa_get_pattern_info": (_S, [_vp, ctypes.POINTER(PatternInfo)]),
+    "mapa_pred_effbw": (ctypes.c_double, [ctypes.c_int32] * 3),
+    "mapa_effbw_rank_table": (_S, [ctypes.c_int32, ctypes.POINTER(ctypes.c_uint16)]),
+    "mapa_allocate": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, _vp,
+                           ctypes.POINTER(Decision)]),
+    "mapa_launch_query": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.c_uint32,
+                               ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, _vp]),
+    "mapa_reduce_records": (_S, [ctypes.POINTER(Record), ctypes.c_int32, ctypes.POINTER(Record)]),
+    "mapa_decode": (_S, [_vp, _vp, ctypes.c_uint32, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
+                         ctypes.POINTER(Record), ctypes.POINTER(Decision)]),
+    "mapa_allocate_batch": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int64, _vp, _vp, _vp,
+                                 ctypes.c_uint32, _vp]),
+    "mapa_trace_replay": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp,
+                               ctypes.c_int32, _vp, _vp, ctypes.c_uint32, _vp]),
+    "mapa_last_error": (ctypes.c_char_p, []),
+    "mapa_version": (ctypes.c_char_p, []),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTS = tuple(_SIGS)
+
+
+def _check(st: int, allow_no_capacity: bool = False) -> int:
+    if st == OK or (allow_no_capacity and st == NO_CAPACITY):
+        return st
+    raise MapaError(st, _lib.mapa_last_error().decode())
+
+
+def last_error() -> str:
+    return _lib.mapa_last_error().decode()
+
+
+def version() -> str:
+    return _lib.mapa_version().decode()
+
+
+def pred_effbw(x: int, y: int, z: int) -> float:
+    """Eq. 2 with Table 4 theta."""
+    return _lib.mapa_pred_effbw(x, y, z)
+
+
+def effbw_rank_table(m: int) -> list[int]:
+    buf = (ctypes.c_uint16 * ((m + 1) * (m + 1)))()
+    _check(_lib.mapa_effbw_rank_table(m, buf))
+    return list(buf)
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.cuda.current_stream().cuda_stream
+        except Exception:  # pragma: no cover
+            pass
+        return None
+    return getattr(stream, "cuda_stream", stream)
+
+
+class Topology:
+    """mapa_topology handle (hardware graph + busy mask, §3.2 / §3.6)."""
+
+    def __init__(self, builtin: str | None = None, text: str | None = None):
+        h = _vp()
+        if text is not None:
+            _check(_lib.mapa_load_topology(text.encode(), 1, ctypes.byref(h)))
+        else:
+            _check(_lib.mapa_load_topology(builtin.encode(), 0, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.mapa_free_topology(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        n, w, busy = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_uint32()
+        _check(_lib.mapa_topology_info(self._h, ctypes.byref(n), ctypes.byref(w), None, ctypes.byref(busy)))
+        bw = (ctypes.c_int32 * (n.value * n.value))()
+        _check(_lib.mapa_topology_info(self._h, None, None, bw, None))
+        mat = [[bw[u * n.value + v] for v in range(n.value)] for u in range(n.value)]
+        return dict(n=n.value, width=w.value, busy=busy.value, bw=mat)
+
+    @property
+    def n(self) -> int:
+        return self.info()["n"]
+
+    @property
+    def width(self) -> int:
+        return self.info()["width"]
+
+    @property
+    def busy(self) -> int:
+        return self.info()["busy"]
+
+    def claim(self, mask: int):
+        _check(_lib.mapa_claim(self._h, mask))
+
+    def release(self, mask: int):
+        _check(_lib.mapa_release(self._h, mask))
+
+    def set_busy(self, mask: int):
+        _check(_lib.mapa_set_busy(self._h, mask))
+
+
+class Pattern:
+    """mapa_pattern handle (application graph, §3.1 / Fig. 4)."""
+
+    def __init__(self, k: int, edges=None, shape: str | None = None, allow_disconnected: bool = False):
+        h = _vp()
+        if shape is not None:
+            _check(_lib.mapa_make_pattern(SHAPES[shape], k, ctypes.byref(h)))
+        else:
+            edges = list(edges or [])
+            flat = (ctypes.c_int32 * max(1, 2 * len(edges)))(*[c for e in edges for c in e])
+            _check(_lib.mapa_load_pattern(k, len(edges), flat,
+                                          F_ALLOW_DISCONNECTED if allow_disconnected else 0, ctypes.byref(h)))
+        self._h = h
+
+    @classmethod
+    def make(cls, shape: str, k: int) -> "Pattern":
+        return cls(k, shape=shape)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.mapa_free_pattern(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self) -> dict:
+        pi = PatternInfo()
+        _check(_lib.mapa_get_pattern_info(self._h, ctypes.byref(pi)))
+        return dict(k=pi.k, m=pi.m, aut=pi.aut_order, back=list(pi.back)[:pi.k],
+                    lex_src=list(pi.lex_src)[:pi.k], edges=[(pi.edges[i][0], pi.edges[i][1]) for i in range(pi.m)])
+
+
+def decision_dict(d: Decision) -> dict:
+    if d.status == NO_CAPACITY:
+        return dict(status="no_capacity", raw=0, distinct=0, leaves=0, key=0)
+    devs = tuple(i for i in range(32) if (d.device_mask >> i) & 1)
+    return dict(status="ok", devices=devs, mapping=tuple(d.mapping[i] for i in range(d.k)),
+                used_edges=[(d.used[i][0], d.used[i][1]) for i in range(d.m)],
+                x=d.x, y=d.y, z=d.z, agg_bw=d.agg_bw, preserved_bw=d.preserved_bw,
+                pred_effbw=d.pred_effbw, score=d.score, raw=int(d.raw_embeddings),
+                distinct=int(d.distinct_matches), leaves=int(d.leaves_scored), key=int(d.key))
+
+
+def allocate(topo: Topology, pat: Pattern, selector: int, sensitive: bool = False, raw: bool = False,
+             commit: bool = False, stream=None) -> dict:
+    """mapa_allocate: one allocation end to end from host buffers (H2D query,
+    kernel, D2H record, host decode)."""
+    d = Decision()
+    flags = (F_RAW if raw else 0) | (F_COMMIT if commit else 0)
+    _check(_lib.mapa_allocate(topo.handle, pat.handle, selector, int(bool(sensitive)), flags,
+                              _stream_ptr(stream), ctypes.byref(d)), allow_no_capacity=True)
+    return decision_dict(d)
+
+
+def launch_query(topo: Topology, pat: Pattern, selector: int, sensitive: bool, d_query_ptr: int,
+                 d_record_ptr: int, raw: bool = False, rank: int = 0, world: int = 1,
+                 busy_hint: int = 0xFFFFFFFF, stream=None):
+    """mapa_launch_query: device-resident launch (asynchronous)."""
+    _check(_lib.mapa_launch_query(topo.handle, pat.handle, selector, int(bool(sensitive)), d_query_ptr,
+                                  d_record_ptr, F_RAW if raw else 0, rank, world, busy_hint,
+                                  _stream_ptr(stream)))
+
+
+def record_from_bytes(b: bytes) -> Record:
+    return Record.from_buffer_copy(b)
+
+
+def reduce_records(records) -> Record:
+    arr = (Record * len(records))(*records)
+    out = Record()
+    _check(_lib.mapa_reduce_records(arr, len(records), ctypes.byref(out)))
+    return out
+
+
+def decode(topo: Topology, pat: Pattern, busy: int, selector: int, sensitive: bool, record: Record,
+           raw: bool = False) -> dict:
+    d = Decision()
+    _check(_lib.mapa_decode(topo.handle, pat.handle, busy, selector, int(bool(sensitive)),
+                            F_RAW if raw else 0, ctypes.byref(record), ctypes.byref(d)), allow_no_capacity=True)
+    return decision_dict(d)
+
+
+def allocate_batch(topo: Topology, pats, nq: int, d_queries_ptr: int, d_results_ptr: int, d_scratch_ptr: int,
+                   raw: bool = False, stream=None):
+    arr = (_vp * len(pats))(*[p.handle for p in pats])
+    _check(_lib.mapa_allocate_batch(topo.handle, arr, len(pats), nq, d_queries_ptr, d_results_ptr,
+                                    d_scratch_ptr, F_RAW if raw else 0, _stream_ptr(stream)))
+
+
+def trace_replay(topo: Topology, pats, ntraces: int, nops: int, d_ops_ptr: int, njobs: int, d_jobs_ptr: int,
+                 d_keys_ptr: int, raw: bool = False, stream=None):
+    arr = (_vp * len(pats))(*[p.handle for p in pats])
+    _check(_lib.mapa_trace_replay(topo.handle, arr, len(pats), ntraces, nops, d_ops_ptr, njobs, d_jobs_ptr,
+                                  d_keys_ptr, F_RAW if raw else 0, _stream_ptr(stream)))
+
+
+def key_layout(topo_width: int, k: int):
+    """(score_shift, set_shift) of the packed key (include/mapa.h)."""
+    eb = k * (k - 1) // 2
+    return topo_width + eb, eb
+
+
+def key_device_mask(key: int, topo_width: int, k: int) -> int:
+    """Device set S encoded in a key (brev_W)."""
+    eb = k * (k - 1) // 2
+    sb = (key >> eb) & ((1 << topo_width) - 1)
+    return sum(1 << d for d in range(topo_width) if (sb >> (topo_width - 1 - d)) & 1)

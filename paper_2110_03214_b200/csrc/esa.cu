@@ -1,0 +1,698 @@
+// esa.cu — Enumerate-Score-Argmax kernels for sm_100a (B200).
+//
+// One pass = SURVEY.md §8(a) S3-S6 fused in registers / shared memory:
+//   S3 occupancy prep   F = ~busy; inc_F(v), T_F (Eq. 3 support)
+//   S4 enumeration      DFS over injective maps f: V(P) -> F (§3.3 P:496-501;
+//                       G complete, so every injective map embeds).
+//                       Lanes = candidate devices of the LAST pattern vertex;
+//                       groups of W lanes (W = 8/16/32 = padded N) each run an
+//                       independent prefix, so small topologies fill the warp.
+//                       Canonical mode adds lex-leader lower bounds (one leaf
+//                       per Aut(P)-orbit = SPEC dedup S:209).
+//   S5 scoring          integer only.  For a device set X not containing v,
+//                       sum_{u in X} w(u,v) = 12|X| + 38 popc(c0&X)
+//                       + 13 popc(c1&X) + 8 popc(c2&X) with v's class masks.
+//                         Eq. 1 AggBW: X = devices of the back-
+//                         neighbours of the vertex being placed.
+//                         Eq. 3 PreservedBW: T_F - sum inc_F(S)
+//                         + inside(S), X = all previously placed devices.
+//                         Eq. 2: census x = popc(c0&X), y =
+//                         popc((c1|c2)&X) accumulated, score = dense rank of
+//                         Eq. 2 among censuses with x+y+z = m (host table).
+//   S6 argmax           per-lane running max of a packed 64-bit key
+//                       (score | brev(S) | edge code) computed lazily (only
+//                       when score >= lane best), warp shuffle max, block max,
+//                       atomicMax in HBM.  Max is order independent, so the
+//                       result is identical for every grid size / rank count.
+// There is no dense contraction anywhere, so no tensor cores (tcgen05) are
+// used: the bound is integer issue.
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace mapa {
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+constexpr int kMaxDecode = 4;
+
+enum { SEL_LIN = 0, SEL_SENS = 1 };
+
+struct Ctx {
+    uint32_t F;
+    int nF;
+    int b;                          // lane's device id (lane % W)
+    uint32_t cm0, cm1, cm2, cm12;   // lane's class masks
+    int leafC;                      // leaf constant: w12*n12(K-1) + lane constant
+    int w0, w1, w2, w12;
+    int useU;                       // 1: X = all placed devices (Eq. 3), 0: back neighbours (Eq. 1/2)
+    int acc0;                       // accumulator at the root (T_F for Eq. 3)
+    const uint4 *cm;                // class masks of every device (smem)
+    const int *inc;                 // inc_F(v) (smem)
+    const uint16_t *lut;            // Eq. 2 rank table (smem)
+    int mp1;                        // m + 1
+    uint64_t fb, fs, db;            // bytes: fwd_back, fwd_src, dback
+    int clique, eb, m;
+    const uint8_t *edge;            // pattern edges a | b<<4
+};
+
+template <int K>
+struct St {
+    uint32_t U;       // placed devices
+    int acc;          // LIN: partial score; SENS: x
+    int acc2;         // SENS: y
+    uint32_t f[K];    // f(i) for placed vertices
+    uint32_t bm[K];   // bm[u]: devices of the placed back-neighbours of u
+    uint32_t al[K];   // al[u]: devices allowed for u by lex-leader constraints
+};
+
+struct Best {
+    unsigned long long key;
+    uint32_t bs;
+    uint32_t cnt;
+};
+
+__device__ __forceinline__ unsigned long long *u64p(uint64_t *p) {
+    return reinterpret_cast<unsigned long long *>(p);
+}
+
+__device__ __forceinline__ uint32_t nth_set(uint32_t m, uint32_t n) {
+    // position of the n-th (0-based) set bit of m (popc binary search)
+    uint32_t pos = 0, c;
+    c = __popc(m & 0xFFFFu); if (n >= c) { n -= c; m >>= 16; pos += 16; }
+    c = __popc(m & 0xFFu);   if (n >= c) { n -= c; m >>= 8;  pos += 8; }
+    c = __popc(m & 0xFu);    if (n >= c) { n -= c; m >>= 4;  pos += 4; }
+    c = __popc(m & 0x3u);    if (n >= c) { n -= c; m >>= 2;  pos += 2; }
+    c = m & 1u;              if (n >= c) { pos += 1; }
+    return pos;
+}
+
+// Packed argmax key: score | brev_W(S) | edge code.  Only
+// evaluated on the slow path (score >= the lane's best score), so it is kept
+// out of line; arguments by value so the DFS state stays in registers.
+//   fpack: f(0..K-2) one byte each; b: device of vertex K-1.
+template <int W, int K>
+__device__ __noinline__ unsigned long long make_key(uint32_t U, unsigned long long fpack, uint32_t b,
+                                                    uint32_t s, int clique, int eb, int m,
+                                                    const uint8_t *edge) {
+    const uint32_t S = U | (1u << b);
+    const uint32_t sb = __brev(S) >> (32 - W);
+    uint32_t ecode;
+    if (clique) {
+        ecode = (1u << eb) - 1u;  // eb <= 28
+    } else {
+        uint32_t R = 0;  // rank of f(i) inside S, 4 bits per pattern vertex
+#pragma unroll
+        for (int i = 0; i < K - 1; ++i) {
+            const uint32_t fi = (uint32_t)(fpack >> (8 * i)) & 0xFFu;
+            R |= (uint32_t)__popc(S & ((1u << fi) - 1u)) << (4 * i);
+        }
+        R |= (uint32_t)__popc(S & ((1u << b) - 1u)) << (4 * (K - 1));
+        ecode = 0;
+        for (int e = 0; e < m; ++e) {
+            const uint32_t ed = edge[e];
+            const uint32_t ra = (R >> (4 * (ed & 15u))) & 15u;
+            const uint32_t rb = (R >> (4 * (ed >> 4))) & 15u;
+            const uint32_t lo = min(ra, rb), hi = max(ra, rb);
+            const uint32_t p = lo * (2u * K - lo - 1u) / 2u + (hi - lo - 1u);
+            ecode |= 1u << (eb - 1 - (int)p);
+        }
+    }
+    return ((unsigned long long)s << (W + eb)) | ((unsigned long long)sb << eb) | ecode;
+}
+
+template <int K, int SEL, int J>
+__device__ __forceinline__ St<K> push(const Ctx &c, const St<K> &st, uint32_t v) {
+    St<K> s = st;
+    const uint32_t vb = 1u << v;
+    const uint4 t = c.cm[v];
+    if constexpr (SEL == SEL_LIN) {
+        const uint32_t X = c.useU ? st.U : st.bm[J];
+        const int n12 = c.useU ? J : (int)((c.db >> (8 * J)) & 0xFFu);
+        const int incv = c.useU ? c.inc[v] : 0;
+        s.acc = st.acc + c.w12 * n12 - incv + c.w0 * __popc(t.x & X) + c.w1 * __popc(t.y & X) +
+                c.w2 * __popc(t.z & X);
+    } else {
+        const uint32_t X = st.bm[J];
+        s.acc = st.acc + __popc(t.x & X);
+        s.acc2 = st.acc2 + __popc((t.y | t.z) & X);
+    }
+    s.U = st.U | vb;
+    s.f[J] = v;
+    const uint32_t fbJ = (uint32_t)(c.fb >> (8 * J)) & 0xFFu;
+    const uint32_t fsJ = (uint32_t)(c.fs >> (8 * J)) & 0xFFu;
+    const uint32_t above = 0xFFFFFFFEu << v;
+#pragma unroll
+    for (int u = J + 1; u < K; ++u) {
+        if ((fbJ >> u) & 1u) s.bm[u] |= vb;
+        if ((fsJ >> u) & 1u) s.al[u] &= above;
+    }
+    return s;
+}
+
+template <int W, int K, int SEL>
+__device__ __forceinline__ void leaf(const Ctx &c, const St<K> &st, Best &bst) {
+    const uint32_t lc = c.F & ~st.U & st.al[K - 1];
+    const bool act = (lc >> c.b) & 1u;
+    int s;
+    if constexpr (SEL == SEL_LIN) {
+        const uint32_t X = c.useU ? st.U : st.bm[K - 1];
+        s = st.acc + c.leafC + c.w0 * __popc(c.cm0 & X) + c.w1 * __popc(c.cm1 & X) +
+            c.w2 * __popc(c.cm2 & X);
+    } else {
+        const uint32_t X = st.bm[K - 1];
+        const int x = st.acc + __popc(c.cm0 & X);
+        const int y = st.acc2 + __popc(c.cm12 & X);
+        s = act ? (int)c.lut[x * c.mp1 + y] : 0;
+    }
+    bst.cnt += act ? 1u : 0u;
+    if (act && (uint32_t)s >= bst.bs) {
+        unsigned long long fpack = 0;
+#pragma unroll
+        for (int i = 0; i < K - 1; ++i) fpack |= (unsigned long long)st.f[i] << (8 * i);
+        const unsigned long long key =
+            make_key<W, K>(st.U, fpack, (uint32_t)c.b, (uint32_t)s, c.clique, c.eb, c.m, c.edge);
+        if (key > bst.key) {
+            bst.key = key;
+            bst.bs = (uint32_t)s;
+        }
+    }
+}
+
+template <int W, int K, int SEL, int J>
+__device__ __forceinline__ void level(const Ctx &c, const St<K> &st, Best &bst) {
+    if constexpr (J == K - 1) {
+        leaf<W, K, SEL>(c, st, bst);
+    } else {
+        uint32_t cand = c.F & ~st.U & st.al[J];
+        while (cand) {
+            const uint32_t v = __ffs(cand) - 1;
+            cand &= cand - 1u;
+            level<W, K, SEL, J + 1>(c, push<K, SEL, J>(c, st, v), bst);
+        }
+    }
+}
+
+// Decode levels [0, D) from the item digits, then run the DFS from level D.
+// Levels < DMIN are always decoded, levels >= DMAX never.
+template <int W, int K, int SEL, int J, int DMIN, int DMAX>
+__device__ __forceinline__ void descend(const Ctx &c, const St<K> &st, const uint32_t (&dg)[kMaxDecode],
+                                        int D, Best &bst) {
+    if constexpr (J >= DMAX || J >= K - 1) {
+        level<W, K, SEL, J>(c, st, bst);
+    } else {
+        if (J < DMIN || J < D) {
+            const uint32_t v = nth_set(c.F & ~st.U, dg[J]);
+            if (!((st.al[J] >> v) & 1u)) return;  // prefix violates a lex-leader bound
+            descend<W, K, SEL, J + 1, DMIN, DMAX>(c, push<K, SEL, J>(c, st, v), dg, D, bst);
+        } else {
+            level<W, K, SEL, J>(c, st, bst);
+        }
+    }
+}
+
+template <int K>
+__device__ __forceinline__ St<K> root(const Ctx &c) {
+    St<K> st;
+    st.U = 0;
+    st.acc = c.acc0;
+    st.acc2 = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        st.f[i] = 0;
+        st.bm[i] = 0;
+        st.al[i] = kFull;
+    }
+    return st;
+}
+
+// item -> mixed-radix digits (radix nF - j at level j); false if item >= P(nF, D)
+__device__ __forceinline__ bool digits(uint32_t item, int nF, int D, const uint32_t *magic,
+                                       uint32_t (&dg)[kMaxDecode]) {
+    uint32_t it = item;
+#pragma unroll
+    for (int j = kMaxDecode - 1; j >= 0; --j) {
+        if (j < D) {
+            const uint32_t r = (uint32_t)(nF - j);
+            const uint32_t q = __umulhi(it, magic[r]);
+            dg[j] = it - q * r;
+            it = q;
+        } else {
+            dg[j] = 0;
+        }
+    }
+    return it == 0;
+}
+
+__device__ __forceinline__ uint32_t perm_count(int n, int d) {
+    uint32_t p = 1;
+    for (int j = 0; j < d; ++j) p *= (uint32_t)(n - j);
+    return p;
+}
+
+// Per-query context.  Must be called by the whole warp (uses shuffles).
+// inc: per-warp (or per-CTA) smem table, written by lanes < W of group 0.
+template <int W>
+__device__ __forceinline__ Ctx make_ctx(const DevTopo &topo, const uint4 *s_cm, int *s_inc,
+                                        const uint16_t *s_lut, const DevPattern &P, uint32_t busy,
+                                        int selector, int sensitive) {
+    const int lane = threadIdx.x & 31;
+    Ctx c;
+    const uint32_t nmask = topo.n >= 32 ? kFull : ((1u << topo.n) - 1u);
+    c.F = ~busy & nmask;
+    c.nF = __popc(c.F);
+    c.b = lane & (W - 1);
+    const uint4 mine = s_cm[c.b];
+    c.cm0 = mine.x;
+    c.cm1 = mine.y;
+    c.cm2 = mine.z;
+    c.cm12 = mine.y | mine.z;
+    // inc_F(b) = sum_{u in F, u != b} w(u,b)
+    const int inFb = (c.F >> c.b) & 1u;
+    int incb = 12 * (c.nF - inFb) + 38 * __popc(mine.x & c.F) + 13 * __popc(mine.y & c.F) +
+               8 * __popc(mine.z & c.F);
+    if (c.b >= topo.n) incb = 0;
+    if (lane < W) s_inc[c.b] = incb;
+    // T_F = 1/2 sum_{v in F} inc_F(v)  (reduce within the W-lane group)
+    int t = inFb ? incb : 0;
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o, W);
+    const int TF = t / 2;
+    const int K = P.k;
+    c.fb = *reinterpret_cast<const uint64_t *>(P.fwd_back);
+    c.fs = *reinterpret_cast<const uint64_t *>(P.fwd_src);
+    c.db = *reinterpret_cast<const uint64_t *>(P.dback);
+    c.clique = P.clique;
+    c.eb = P.eb;
+    c.m = P.m;
+    c.edge = P.edge;
+    c.mp1 = P.m + 1;
+    c.cm = s_cm;
+    c.inc = s_inc;
+    c.lut = s_lut;
+    int laneC = 0;
+    if (selector == MAPA_SEL_BASELINE) {
+        c.w0 = c.w1 = c.w2 = c.w12 = 0;
+        c.useU = 0;
+        c.acc0 = 0;
+    } else if (selector == MAPA_SEL_PRESERVE && !sensitive) {  // Eq. 3
+        c.w0 = 38; c.w1 = 13; c.w2 = 8; c.w12 = 12;
+        c.useU = 1;
+        c.acc0 = TF;
+        laneC = -incb;
+    } else {  // Eq. 1 (or Eq. 2 census for the sensitive kernel)
+        c.w0 = 38; c.w1 = 13; c.w2 = 8; c.w12 = 12;
+        c.useU = 0;
+        c.acc0 = 0;
+    }
+    const int n12 = c.useU ? (K - 1) : (int)P.dback[K - 1];
+    c.leafC = c.w12 * n12 + laneC;
+    __syncwarp();
+    return c;
+}
+
+template <int W, int K, int SEL, int DMIN, int DMAX>
+__device__ __forceinline__ void run_item(const Ctx &c, uint32_t item, int D, const uint32_t *magic,
+                                         Best &bst) {
+    uint32_t dg[kMaxDecode];
+    if (!digits(item, c.nF, D, magic, dg)) return;
+    descend<W, K, SEL, 0, DMIN, DMAX>(c, root<K>(c), dg, D, bst);
+}
+
+__device__ __forceinline__ void warp_reduce(unsigned long long &key, unsigned long long &cnt) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long k2 = __shfl_xor_sync(kFull, key, o);
+        const unsigned long long c2 = __shfl_xor_sync(kFull, cnt, o);
+        key = k2 > key ? k2 : key;
+        cnt += c2;
+    }
+}
+
+__device__ __forceinline__ void load_topo(const DevTopo &topo, uint4 *s_cm, uint32_t *s_magic) {
+    const int tid = threadIdx.x;
+    if (tid < kMaxN) s_cm[tid] = make_uint4(topo.cm[tid][0], topo.cm[tid][1], topo.cm[tid][2], topo.cm[tid][3]);
+    if (tid <= kMaxN) s_magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
+}
+
+// ---------------------------------------------------------------- single query
+template <int W, int K, int SEL>
+__global__ void __launch_bounds__(kBlock, 2)
+esa_single(const __grid_constant__ SingleTables tb, int selector, int sensitive,
+           const mapa_query *__restrict__ dq, mapa_record *__restrict__ rec, int D, int rank,
+           int world, int chunk) {
+    constexpr int G = 32 / W;
+    constexpr int DMAX = (K - 1) < kMaxDecode ? (K - 1) : kMaxDecode;
+    __shared__ uint4 s_cm[kMaxN];
+    __shared__ uint32_t s_magic[kMaxN + 1];
+    __shared__ int s_inc[kMaxN];
+    __shared__ uint16_t s_lut[kLutCapSingle];
+    __shared__ uint8_t s_edge[28];
+    __shared__ unsigned long long s_key[kWarps], s_cnt[kWarps];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const DevPattern &P = tb.pat[0];
+    load_topo(tb.topo, s_cm, s_magic);
+    const int lutn = (P.m + 1) * (P.m + 1);
+    for (int i = tid; i < lutn; i += kBlock) s_lut[i] = tb.lut[P.lut_off + i];
+    if (tid < 28) s_edge[tid] = P.edge[tid];
+    const uint32_t busy = dq->busy;
+    __syncthreads();
+
+    Ctx c = make_ctx<W>(tb.topo, s_cm, s_inc, s_lut, P, busy, selector, sensitive);
+    c.edge = s_edge;
+    __syncthreads();  // s_inc written by every warp with identical values
+
+    const uint32_t nItems = (K <= c.nF) ? perm_count(c.nF, D) : 0u;
+    const uint32_t nLocal = nItems > (uint32_t)rank ? (nItems - (uint32_t)rank + (uint32_t)world - 1u) / (uint32_t)world : 0u;
+    Best bst{0ull, 0u, 0u};
+    const uint32_t g = (uint32_t)(lane / W);
+    for (;;) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&rec->ctr, (uint32_t)chunk);
+        base = __shfl_sync(kFull, base, 0);
+        if (base >= nLocal) break;
+        const uint32_t end = min(base + (uint32_t)chunk, nLocal);
+        for (uint32_t j = base + g; j < end; j += G) {
+            run_item<W, K, SEL, 0, DMAX>(c, j * (uint32_t)world + (uint32_t)rank, D, s_magic, bst);
+        }
+        __syncwarp();
+    }
+    unsigned long long key = bst.key, cnt = bst.cnt;
+    warp_reduce(key, cnt);
+    if (lane == 0) {
+        s_key[warp] = key;
+        s_cnt[warp] = cnt;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        key = lane < kWarps ? s_key[lane] : 0ull;
+        cnt = lane < kWarps ? s_cnt[lane] : 0ull;
+        warp_reduce(key, cnt);
+        if (lane == 0) {
+            if (key) atomicMax(u64p(&rec->key), key);
+            if (cnt) atomicAdd(u64p(&rec->leaves), cnt);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- batches
+// W slots per query; slot j = the j-th free device as f(0) (D = 1); K = 1
+// queries use slot 0 only (D = 0).
+template <int W, int K, int SEL>
+__device__ __forceinline__ void batch_item(const Ctx &c, uint32_t j, const uint32_t *magic, Best &bst) {
+    if constexpr (K == 1) {
+        if (j == 0) run_item<W, 1, SEL, 0, 0>(c, 0u, 0, magic, bst);
+    } else {
+        if (j < (uint32_t)c.nF) run_item<W, K, SEL, 1, 1>(c, j, 1, magic, bst);
+    }
+}
+
+template <int W, int SEL>
+__device__ __forceinline__ void batch_dispatch_k(int K, const Ctx &c, uint32_t j, const uint32_t *magic,
+                                                 Best &bst) {
+    switch (K) {
+        case 1: batch_item<W, 1, SEL>(c, j, magic, bst); break;
+        case 2: batch_item<W, 2, SEL>(c, j, magic, bst); break;
+        case 3: batch_item<W, 3, SEL>(c, j, magic, bst); break;
+        case 4: batch_item<W, 4, SEL>(c, j, magic, bst); break;
+        case 5: batch_item<W, 5, SEL>(c, j, magic, bst); break;
+        case 6: batch_item<W, 6, SEL>(c, j, magic, bst); break;
+        case 7: batch_item<W, 7, SEL>(c, j, magic, bst); break;
+        case 8: batch_item<W, 8, SEL>(c, j, magic, bst); break;
+        default: break;
+    }
+}
+
+__device__ __forceinline__ bool key_fits(int W, const DevPattern &P) { return 15 + W + P.eb <= 63; }
+
+template <int W>
+__global__ void __launch_bounds__(kBlock, 2)
+esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query *__restrict__ qs,
+          mapa_record *__restrict__ res, uint32_t *__restrict__ ctr) {
+    constexpr int G = 32 / W;
+    __shared__ uint4 s_cm[kMaxN];
+    __shared__ uint32_t s_magic[kMaxN + 1];
+    __shared__ int s_inc[kWarps][kMaxN];
+    __shared__ uint16_t s_lut[kLutCapMulti];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    load_topo(tb.topo, s_cm, s_magic);
+    int lutn = 0;
+    for (int p = 0; p < tb.npats; ++p) {
+        const int e = tb.pat[p].lut_off + (tb.pat[p].m + 1) * (tb.pat[p].m + 1);
+        lutn = e > lutn ? e : lutn;
+    }
+    for (int i = tid; i < lutn; i += kBlock) s_lut[i] = tb.lut[i];
+    __syncthreads();
+
+    const unsigned long long nslots = (unsigned long long)nq * W;
+    const uint32_t g = (uint32_t)(lane / W);
+    for (;;) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long *>(ctr), (unsigned long long)G);
+        base = __shfl_sync(kFull, base, 0);
+        if (base >= nslots) break;
+        const unsigned long long q = base / W;  // G | W: every group of the warp has the same query
+        const mapa_query qu = qs[q];
+        const uint32_t pid = qu.pattern;
+        if (pid >= (uint32_t)tb.npats || !key_fits(W, tb.pat[pid < (uint32_t)tb.npats ? pid : 0])) {
+            if (lane == 0 && (base % W) == 0) atomicExch(&res[q].status, 1u);
+            continue;
+        }
+        const DevPattern &P = tb.pat[pid];
+        Ctx c = make_ctx<W>(tb.topo, s_cm, s_inc[warp], s_lut + P.lut_off, P, qu.busy, qu.selector,
+                            qu.sensitive);
+        if (P.k > c.nF) continue;
+        const uint32_t j = (uint32_t)(base % W) + g;
+        Best bst{0ull, 0u, 0u};
+        const bool sens = qu.selector == MAPA_SEL_PRESERVE && qu.sensitive;
+        if (sens) batch_dispatch_k<W, SEL_SENS>(P.k, c, j, s_magic, bst);
+        else batch_dispatch_k<W, SEL_LIN>(P.k, c, j, s_magic, bst);
+        __syncwarp();
+        unsigned long long key = bst.key, cnt = bst.cnt;
+        warp_reduce(key, cnt);
+        if (lane == 0) {
+            if (key) atomicMax(u64p(&res[q].key), key);
+            if (cnt) atomicAdd(u64p(&res[q].leaves), cnt);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- trace replay
+template <int W, int K, int SEL>
+__device__ __forceinline__ void trace_items(const Ctx &c, int D, uint32_t nItems, uint32_t gid,
+                                            uint32_t ngroups, const uint32_t *magic, Best &bst) {
+    constexpr int DMAX = (K - 1) < 2 ? (K - 1) : 2;
+    for (uint32_t it = gid; it < nItems; it += ngroups) run_item<W, K, SEL, 0, DMAX>(c, it, D, magic, bst);
+}
+
+template <int W, int SEL>
+__device__ __forceinline__ void trace_dispatch_k(int K, const Ctx &c, int D, uint32_t nItems, uint32_t gid,
+                                                 uint32_t ngroups, const uint32_t *magic, Best &bst) {
+    switch (K) {
+        case 1: trace_items<W, 1, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
+        case 2: trace_items<W, 2, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
+        case 3: trace_items<W, 3, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
+        case 4: trace_items<W, 4, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
+        case 5: trace_items<W, 5, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
+        case 6: trace_items<W, 6, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
+        case 7: trace_items<W, 7, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
+        case 8: trace_items<W, 8, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
+        default: break;
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(kBlock, 1)
+esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op *__restrict__ ops, int njobs,
+          const mapa_query *__restrict__ jobs, unsigned long long *__restrict__ keys) {
+    constexpr int G = 32 / W;
+    __shared__ uint4 s_cm[kMaxN];
+    __shared__ uint32_t s_magic[kMaxN + 1];
+    __shared__ int s_inc[kWarps][kMaxN];
+    __shared__ uint16_t s_lut[kLutCapMulti];
+    __shared__ unsigned long long s_key[kWarps], s_cnt[kWarps];
+    __shared__ uint32_t s_busy;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int t = blockIdx.x;
+    load_topo(tb.topo, s_cm, s_magic);
+    int lutn = 0;
+    for (int p = 0; p < tb.npats; ++p) {
+        const int e = tb.pat[p].lut_off + (tb.pat[p].m + 1) * (tb.pat[p].m + 1);
+        lutn = e > lutn ? e : lutn;
+    }
+    for (int i = tid; i < lutn; i += kBlock) s_lut[i] = tb.lut[i];
+    if (tid == 0) s_busy = 0u;
+    __syncthreads();
+    const mapa_trace_op *op = ops + (long long)t * nops;
+    const mapa_query *jb = jobs + (long long)t * njobs;
+    unsigned long long *ky = keys + (long long)t * njobs;
+    const uint32_t gid = (uint32_t)(warp * G + lane / W);
+    for (int o = 0; o < nops; ++o) {
+        const mapa_trace_op cur = op[o];
+        const mapa_query qu = jb[cur.job];
+        const uint32_t pid = qu.pattern;
+        const bool okp = pid < (uint32_t)tb.npats && key_fits(W, tb.pat[pid < (uint32_t)tb.npats ? pid : 0]);
+        const DevPattern &P = tb.pat[okp ? pid : 0];
+        if (cur.op == 0) {
+            const uint32_t busy = s_busy;
+            Ctx c = make_ctx<W>(tb.topo, s_cm, s_inc[warp], s_lut + P.lut_off, P, busy, qu.selector,
+                                qu.sensitive);
+            Best bst{0ull, 0u, 0u};
+            if (okp && P.k <= c.nF) {
+                const int D = (P.k - 1) < 2 ? (P.k - 1) : 2;
+                const uint32_t nItems = perm_count(c.nF, D);
+                const bool sens = qu.selector == MAPA_SEL_PRESERVE && qu.sensitive;
+                if (sens) trace_dispatch_k<W, SEL_SENS>(P.k, c, D, nItems, gid, kWarps * G, s_magic, bst);
+                else trace_dispatch_k<W, SEL_LIN>(P.k, c, D, nItems, gid, kWarps * G, s_magic, bst);
+            }
+            __syncwarp();
+            unsigned long long key = bst.key, cnt = bst.cnt;
+            warp_reduce(key, cnt);
+            if (lane == 0) s_key[warp] = key;
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long best = 0;
+                for (int w = 0; w < kWarps; ++w) best = s_key[w] > best ? s_key[w] : best;
+                ky[cur.job] = best;
+                if (best) {
+                    const uint32_t sb = (uint32_t)(best >> P.eb) & (W >= 32 ? kFull : ((1u << W) - 1u));
+                    s_busy = busy | (__brev(sb) >> (32 - W));
+                }
+            }
+        } else {
+            if (tid == 0) {
+                const unsigned long long kk = ky[cur.job];
+                const uint32_t sb = (uint32_t)(kk >> P.eb) & (W >= 32 ? kFull : ((1u << W) - 1u));
+                s_busy &= ~(__brev(sb) >> (32 - W));
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- dispatch tables
+template <int W, int K, int SEL>
+int do_launch_single(const SingleTables &tb, int selector, int sensitive, const mapa_query *dq,
+                     mapa_record *rec, int D, int rank, int world, int chunk, int grid, cudaStream_t st) {
+    esa_single<W, K, SEL><<<grid, kBlock, 0, st>>>(tb, selector, sensitive, dq, rec, D, rank, world, chunk);
+    return (int)cudaGetLastError();
+}
+
+using SingleFn = int (*)(const SingleTables &, int, int, const mapa_query *, mapa_record *, int, int, int,
+                         int, int, cudaStream_t);
+
+template <int W, int SEL>
+SingleFn pick_k(int K) {
+    switch (K) {
+        case 1: return do_launch_single<W, 1, SEL>;
+        case 2: return do_launch_single<W, 2, SEL>;
+        case 3: return do_launch_single<W, 3, SEL>;
+        case 4: return do_launch_single<W, 4, SEL>;
+        case 5: return do_launch_single<W, 5, SEL>;
+        case 6: return do_launch_single<W, 6, SEL>;
+        case 7: return do_launch_single<W, 7, SEL>;
+        case 8: return do_launch_single<W, 8, SEL>;
+    }
+    return nullptr;
+}
+
+template <int W>
+SingleFn pick_sel(int K, int sens) {
+    return sens ? pick_k<W, SEL_SENS>(K) : pick_k<W, SEL_LIN>(K);
+}
+
+SingleFn pick_single(int W, int K, int sens) {
+    if (W == 8) return pick_sel<8>(K, sens);
+    if (W == 16) return pick_sel<16>(K, sens);
+    if (W == 32) return pick_sel<32>(K, sens);
+    return nullptr;
+}
+
+template <int W, int K, int SEL>
+const void *single_ptr() { return (const void *)esa_single<W, K, SEL>; }
+
+}  // namespace
+
+int launch_single(const SingleTables &tb, int selector, int sensitive, const mapa_query *d_query,
+                  mapa_record *d_record, int depth, int rank, int world, int chunk, int grid, void *stream) {
+    const int sensk = (selector == MAPA_SEL_PRESERVE && sensitive) ? 1 : 0;
+    SingleFn fn = pick_single(tb.topo.width, tb.pat[0].k, sensk);
+    if (!fn) return (int)cudaErrorInvalidValue;
+    return fn(tb, selector, sensitive, d_query, d_record, depth, rank, world, chunk, grid,
+              (cudaStream_t)stream);
+}
+
+int launch_batch(const MultiTables &tb, int64_t nq, const mapa_query *d_queries, mapa_record *d_results,
+                 uint32_t *d_ctr, int grid, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (tb.topo.width) {
+        case 8: esa_batch<8><<<grid, kBlock, 0, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr); break;
+        case 16: esa_batch<16><<<grid, kBlock, 0, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr); break;
+        case 32: esa_batch<32><<<grid, kBlock, 0, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr); break;
+        default: return (int)cudaErrorInvalidValue;
+    }
+    return (int)cudaGetLastError();
+}
+
+int launch_trace(const MultiTables &tb, int ntraces, int nops, const mapa_trace_op *d_ops, int njobs,
+                 const mapa_query *d_jobs, uint64_t *d_keys, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long *k = reinterpret_cast<unsigned long long *>(d_keys);
+    switch (tb.topo.width) {
+        case 8: esa_trace<8><<<ntraces, kBlock, 0, st>>>(tb, nops, d_ops, njobs, d_jobs, k); break;
+        case 16: esa_trace<16><<<ntraces, kBlock, 0, st>>>(tb, nops, d_ops, njobs, d_jobs, k); break;
+        case 32: esa_trace<32><<<ntraces, kBlock, 0, st>>>(tb, nops, d_ops, njobs, d_jobs, k); break;
+        default: return (int)cudaErrorInvalidValue;
+    }
+    return (int)cudaGetLastError();
+}
+
+int device_sm_count() {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    return n;
+}
+
+namespace {
+template <int W>
+int occ_single(int K, int sens) {
+    const void *f = nullptr;
+#define MAPA_OCC_CASE(KK)                                                        \
+    case KK:                                                                     \
+        f = sens ? single_ptr<W, KK, SEL_SENS>() : single_ptr<W, KK, SEL_LIN>(); \
+        break;
+    switch (K) {
+        MAPA_OCC_CASE(1) MAPA_OCC_CASE(2) MAPA_OCC_CASE(3) MAPA_OCC_CASE(4)
+        MAPA_OCC_CASE(5) MAPA_OCC_CASE(6) MAPA_OCC_CASE(7) MAPA_OCC_CASE(8)
+    }
+#undef MAPA_OCC_CASE
+    int nb = 0;
+    if (!f || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kBlock, 0) != cudaSuccess) return 1;
+    return nb > 0 ? nb : 1;
+}
+}  // namespace
+
+int max_blocks_per_sm_single(int width, int k, int sens) {
+    if (width == 8) return occ_single<8>(k, sens);
+    if (width == 16) return occ_single<16>(k, sens);
+    return occ_single<32>(k, sens);
+}
+
+int max_blocks_per_sm_batch(int width) {
+    int nb = 0;
+    cudaError_t e = cudaErrorInvalidValue;
+    if (width == 8) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, esa_batch<8>, kBlock, 0);
+    if (width == 16) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, esa_batch<16>, kBlock, 0);
+    if (width == 32) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, esa_batch<32>, kBlock, 0);
+    return (e == cudaSuccess && nb > 0) ? nb : 1;
+}
+
+const char *cuda_error_string(int err) { return cudaGetErrorString((cudaError_t)err); }
+
+}  // namespace mapa

@@ -1,0 +1,77 @@
+// internal.h — structs shared by the host side (mapa_host.cpp) and the
+// sm_100a kernels (esa.cu) of libmapa.  Not part of the C-ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/mapa.h"
+
+namespace mapa {
+
+constexpr int kMaxK = 8;
+constexpr int kMaxN = 32;
+constexpr int kMaxPats = 16;      // patterns per batch / trace launch
+constexpr int kLutCapSingle = 1024;  // (m+1)^2 <= 841 for m <= 28
+constexpr int kLutCapMulti = 4096;
+
+// Link class codes (Table 1): 0 = DoubleNVLink2 50, 1 = SingleNVLink2 25,
+// 2 = SingleNVLink1 20, 3 = PCIe 12 (also the fallback for unlinked pairs).
+constexpr int kClassBw[4] = {50, 25, 20, 12};
+
+// Device view of a topology: per device v the class masks
+//   cm[v].x = {u : class(u,v) == 0}, .y = class 1, .z = class 2, .w = class 3
+// (u != v, u < n).  The masks of a device partition the other devices, so
+//   sum_{u in X} w(u,v) = 12|X| + 38 popc(x&X) + 13 popc(y&X) + 8 popc(z&X)
+// for any X not containing v (weights 50,25,20,12 = 12 + {38,13,8,0}).
+struct DevTopo {
+    uint32_t cm[kMaxN][4];
+    int32_t n;
+    int32_t width;  // 8, 16 or 32 lanes per group
+};
+
+// Device view of a compiled pattern.  Vertex order = pattern index order
+// (the order of the mapping tuple whose lex-min the canonical mode keeps).
+struct DevPattern {
+    uint8_t k, m, clique, eb;   // eb = C(k,2)
+    uint8_t fwd_back[8];        // fwd_back[j] bit u (u > j): pattern edge (j,u)
+    uint8_t fwd_src[8];         // fwd_src[j] bit u (u > j): lex-leader f(j) < f(u)
+    uint8_t dback[8];           // |{i < j : (i,j) in E}|
+    uint8_t edge[28];           // a | b << 4, a < b
+    uint16_t lut_off;           // offset of the Eq. 2 rank table in the LUT pool
+    uint16_t aut;               // |Aut(P)|
+};
+
+template <int MAXP, int LUTCAP>
+struct Tables {
+    DevTopo topo;
+    int32_t npats;
+    int32_t pad[3];
+    DevPattern pat[MAXP];
+    uint16_t lut[LUTCAP];
+};
+using SingleTables = Tables<1, kLutCapSingle>;
+using MultiTables = Tables<kMaxPats, kLutCapMulti>;
+
+// Canonical-mode patterns get fwd_src from the lex-leader constraints; RAW
+// mode zeroes fwd_src (no symmetry breaking).
+struct LaunchCfg {
+    int grid;
+    int block;
+    int depth;      // decoded prefix depth D
+    int chunk;      // items per counter grab
+};
+
+// Kernel launchers (esa.cu).  Return cudaError_t as int.
+int launch_single(const SingleTables &tb, int selector, int sensitive, const mapa_query *d_query, mapa_record *d_record,
+                  int depth, int rank, int world, int chunk, int grid, void *stream);
+int launch_batch(const MultiTables &tb, int64_t nq, const mapa_query *d_queries,
+                 mapa_record *d_results, uint32_t *d_ctr, int grid, void *stream);
+int launch_trace(const MultiTables &tb, int ntraces, int nops, const mapa_trace_op *d_ops, int njobs,
+                 const mapa_query *d_jobs, uint64_t *d_keys, void *stream);
+int device_sm_count();
+int max_blocks_per_sm_single(int width, int k, int sens);
+int max_blocks_per_sm_batch(int width);
+const char *cuda_error_string(int err);
+
+}  // namespace mapa

@@ -1,0 +1,713 @@
+// mapa_host.cpp — host side of libmapa: topology encode (S1), pattern compile
+// (S2), Eq. 2 rank tables, launch planning, key decode (S8) and the C-ABI.
+// Nothing here enumerates or scores embeddings: that is esa.cu.  The decode
+// recomputes the winner's census / scores from (S, mapping) only to report
+// them and to self-check the key.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <new>
+#include <sstream>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "internal.h"
+
+using namespace mapa;
+
+struct mapa_topology {
+    std::string name;
+    int n = 0;
+    int width = 8;
+    uint8_t cls[kMaxN][kMaxN];   // class code 0..3, diagonal 0xFF
+    std::vector<std::vector<int>> sockets;
+    uint32_t busy = 0;
+    void *d_stage = nullptr;      // device: query (16 B) + record (32 B)
+    void *h_stage = nullptr;      // pinned host mirror
+};
+
+struct mapa_pattern {
+    int k = 0, m = 0;
+    std::vector<std::pair<int, int>> edges;  // a < b, sorted
+    uint8_t adj[kMaxK][kMaxK];
+    uint8_t back[kMaxK];
+    uint8_t src[kMaxK];
+    int aut = 1;
+    std::vector<uint16_t> lut;   // (m+1)^2
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+mapa_status fail(mapa_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+
+// ------------------------------------------------------------------ topology
+// Link classes, Table 1.
+const char *kClassNames[4] = {"nv2x2", "nv2x1", "nv1x1", "pcie"};
+
+void topo_init(mapa_topology *t, const std::string &name, int n) {
+    t->name = name;
+    t->n = n;
+    t->width = n <= 8 ? 8 : (n <= 16 ? 16 : 32);
+    for (int u = 0; u < kMaxN; ++u)
+        for (int v = 0; v < kMaxN; ++v) t->cls[u][v] = (u == v) ? 0xFF : 3;  // PCIe fallback
+}
+
+void topo_link(mapa_topology *t, int a1, int b1, int c) {  // 1-based ids
+    t->cls[a1 - 1][b1 - 1] = (uint8_t)c;
+    t->cls[b1 - 1][a1 - 1] = (uint8_t)c;
+}
+
+// DGX-1 hybrid cube-mesh wiring, SPEC S:46 (classes fixed by P:261 and the
+// §2.2 worked examples P:294).
+const int kCubeDouble[8][2] = {{1, 4}, {1, 5}, {2, 3}, {2, 6}, {3, 4}, {5, 8}, {6, 7}, {7, 8}};
+const int kCubeSingle[8][2] = {{1, 2}, {1, 3}, {2, 4}, {3, 7}, {4, 8}, {5, 6}, {5, 7}, {6, 8}};
+
+bool build_builtin(const std::string &name, mapa_topology *t) {
+    if (name == "dgx1v" || name == "dgx1p") {
+        topo_init(t, name, 8);
+        const bool p100 = name == "dgx1p";
+        for (auto &e : kCubeDouble) topo_link(t, e[0], e[1], p100 ? 2 : 0);
+        for (auto &e : kCubeSingle) topo_link(t, e[0], e[1], p100 ? 2 : 1);
+        t->sockets = {{0, 1, 2, 3}, {4, 5, 6, 7}};
+        return true;
+    }
+    if (name == "summit") {
+        topo_init(t, name, 6);
+        for (int s = 0; s < 2; ++s)
+            for (int a = 1; a <= 3; ++a)
+                for (int b = a + 1; b <= 3; ++b) topo_link(t, 3 * s + a, 3 * s + b, 0);
+        t->sockets = {{0, 1, 2}, {3, 4, 5}};
+        return true;
+    }
+    if (name == "torus2d16") {  // rows DoubleNVLink2, columns SingleNVLink2
+        topo_init(t, name, 16);
+        for (int r = 0; r < 4; ++r)
+            for (int c = 0; c < 4; ++c) {
+                const int u = 4 * r + c + 1;
+                topo_link(t, u, 4 * r + (c + 1) % 4 + 1, 0);
+                topo_link(t, u, 4 * ((r + 1) % 4) + c + 1, 1);
+            }
+        t->sockets = {{0, 1, 2, 3, 4, 5, 6, 7}, {8, 9, 10, 11, 12, 13, 14, 15}};
+        return true;
+    }
+    if (name == "cubemesh16") {
+        topo_init(t, name, 16);
+        for (int o = 0; o <= 8; o += 8) {
+            for (auto &e : kCubeDouble) topo_link(t, e[0] + o, e[1] + o, 0);
+            for (auto &e : kCubeSingle) topo_link(t, e[0] + o, e[1] + o, 1);
+        }
+        const int br[4][2] = {{1, 9}, {4, 12}, {5, 13}, {8, 16}};
+        for (auto &e : br) topo_link(t, e[0], e[1], 1);
+        t->sockets = {{0, 1, 2, 3, 4, 5, 6, 7}, {8, 9, 10, 11, 12, 13, 14, 15}};
+        return true;
+    }
+    return false;
+}
+
+mapa_status parse_topology_text(const char *text, mapa_topology *t) {
+    std::istringstream in(text);
+    std::string line;
+    int ln = 0, n = -1;
+    std::string name = "topology";
+    std::vector<std::vector<int>> sockets;
+    struct L { int a, b, c, line; };
+    std::vector<L> links;
+    while (std::getline(in, line)) {
+        ++ln;
+        const size_t hash = line.find('#');
+        if (hash != std::string::npos) line = line.substr(0, hash);
+        std::istringstream ls(line);
+        std::string f;
+        if (!(ls >> f)) continue;
+        if (f == "name") {
+            if (!(ls >> name)) return fail(MAPA_E_PARSE, "line " + std::to_string(ln) + ": name: missing value");
+        } else if (f == "devices") {
+            if (!(ls >> n) || n < 1) return fail(MAPA_E_PARSE, "line " + std::to_string(ln) + ": devices: bad count");
+            if (n > kMaxN) return fail(MAPA_E_UNSUPPORTED, "line " + std::to_string(ln) + ": devices > 32 unsupported");
+        } else if (f == "sockets") {
+            std::string grp;
+            while (ls >> grp) {
+                std::vector<int> s;
+                std::istringstream gs(grp);
+                std::string id;
+                while (std::getline(gs, id, ',')) {
+                    char *end = nullptr;
+                    const long v = std::strtol(id.c_str(), &end, 10);
+                    if (id.empty() || *end) return fail(MAPA_E_PARSE, "line " + std::to_string(ln) + ": sockets: bad id '" + id + "'");
+                    s.push_back((int)v - 1);
+                }
+                sockets.push_back(s);
+            }
+        } else if (f == "link") {
+            int a, b;
+            std::string c;
+            if (!(ls >> a >> b >> c)) return fail(MAPA_E_PARSE, "line " + std::to_string(ln) + ": link: expected 'link a b class'");
+            int code = -1;
+            for (int i = 0; i < 4; ++i)
+                if (c == kClassNames[i]) code = i;
+            if (code < 0) return fail(MAPA_E_PARSE, "line " + std::to_string(ln) + ": link: unknown class '" + c + "'");
+            links.push_back({a, b, code, ln});
+        } else {
+            return fail(MAPA_E_PARSE, "line " + std::to_string(ln) + ": unknown field '" + f + "'");
+        }
+    }
+    if (n < 1) return fail(MAPA_E_PARSE, "missing 'devices'");
+    topo_init(t, name, n);
+    bool seen[kMaxN][kMaxN] = {};
+    for (const L &l : links) {
+        if (l.a == l.b) return fail(MAPA_E_PARSE, "line " + std::to_string(l.line) + ": link: self loop");
+        if (l.a < 1 || l.b < 1 || l.a > n || l.b > n)
+            return fail(MAPA_E_ID_RANGE, "line " + std::to_string(l.line) + ": link: id out of range");
+        if (seen[l.a - 1][l.b - 1]) return fail(MAPA_E_PARSE, "line " + std::to_string(l.line) + ": link: duplicate edge");
+        seen[l.a - 1][l.b - 1] = seen[l.b - 1][l.a - 1] = true;
+        topo_link(t, l.a, l.b, l.c);
+    }
+    if (sockets.empty()) {
+        std::vector<int> all;
+        for (int i = 0; i < n; ++i) all.push_back(i);
+        sockets.push_back(all);
+    }
+    std::vector<int> cover(n, 0);
+    for (auto &s : sockets)
+        for (int d : s) {
+            if (d < 0 || d >= n) return fail(MAPA_E_ID_RANGE, "sockets: id out of range");
+            cover[d]++;
+        }
+    for (int d = 0; d < n; ++d)
+        if (cover[d] != 1) return fail(MAPA_E_PARSE, "sockets: groups must be disjoint and cover every device");
+    t->sockets = sockets;
+    return MAPA_OK;
+}
+
+void fill_devtopo(const mapa_topology *t, DevTopo &dt) {
+    std::memset(&dt, 0, sizeof(dt));
+    dt.n = t->n;
+    dt.width = t->width;
+    for (int v = 0; v < t->n; ++v)
+        for (int u = 0; u < t->n; ++u)
+            if (u != v) dt.cm[v][t->cls[u][v]] |= 1u << u;
+}
+
+int bw_of(const mapa_topology *t, int u, int v) { return kClassBw[t->cls[u][v]]; }
+
+uint32_t nmask_of(int n) { return n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u); }
+
+// ---------------------------------------------------------------- Eq. 2
+// Predicted effective bandwidth, Eq. 2, Table 4.
+const double kTheta[14] = {16.396, 4.536, 1.556, -20.694, -9.467, 7.615, -7.973,
+                           12.733, -4.195, -8.413, 62.851, 27.418, -5.114, -46.973};
+
+double eq2(int xi, int yi, int zi) {
+    const double x = xi, y = yi, z = zi;
+    const double lin = kTheta[0] * x + kTheta[1] * y + kTheta[2] * z;
+    const double inv = kTheta[3] / (x + 1.0) + kTheta[4] / (y + 1.0) + kTheta[5] / (z + 1.0);
+    const double pair = kTheta[6] * x * y + kTheta[7] * y * z + kTheta[8] * z * x;
+    const double ipair = kTheta[9] / (x * y + 1.0) + kTheta[10] / (y * z + 1.0) + kTheta[11] / (z * x + 1.0);
+    const double trip = kTheta[12] * x * y * z + kTheta[13] / (x * y * z + 1.0);
+    return lin + inv + pair + ipair + trip;
+}
+
+// Dense rank of Eq. 2 over the censuses with x+y+z = m (reading A9: distinct
+// censuses never tie and are separated by >= 7.8e-4, so double order is exact).
+std::vector<uint16_t> rank_table(int m) {
+    std::vector<std::pair<double, int>> v;
+    for (int x = 0; x <= m; ++x)
+        for (int y = 0; x + y <= m; ++y) v.push_back({eq2(x, y, m - x - y), x * (m + 1) + y});
+    std::sort(v.begin(), v.end());
+    std::vector<uint16_t> lut((size_t)(m + 1) * (m + 1), 0);
+    int r = 0;
+    for (size_t i = 0; i < v.size(); ++i) {
+        if (i > 0 && v[i].first != v[i - 1].first) ++r;
+        lut[v[i].second] = (uint16_t)r;
+    }
+    return lut;
+}
+
+// ---------------------------------------------------------------- patterns
+mapa_status compile_pattern(int k, const std::vector<std::pair<int, int>> &raw, uint32_t flags,
+                            mapa_pattern **out) {
+    if (k < 1 || k > kMaxK) return fail(MAPA_E_UNSUPPORTED, "pattern: need 1 <= k <= 8");
+    mapa_pattern *p = new (std::nothrow) mapa_pattern();
+    if (!p) return fail(MAPA_E_INVALID_ARG, "out of memory");
+    p->k = k;
+    std::memset(p->adj, 0, sizeof(p->adj));
+    for (auto e : raw) {
+        int a = e.first, b = e.second;
+        if (a < 0 || b < 0 || a >= k || b >= k) { delete p; return fail(MAPA_E_INVALID_ARG, "pattern: vertex id out of range"); }
+        if (a == b) { delete p; return fail(MAPA_E_INVALID_ARG, "pattern: self loop"); }
+        if (a > b) std::swap(a, b);
+        if (p->adj[a][b]) { delete p; return fail(MAPA_E_INVALID_ARG, "pattern: duplicate edge"); }
+        p->adj[a][b] = p->adj[b][a] = 1;
+        p->edges.push_back({a, b});
+    }
+    std::sort(p->edges.begin(), p->edges.end());
+    p->m = (int)p->edges.size();
+    if (k > 1 && !(flags & MAPA_F_ALLOW_DISCONNECTED)) {
+        int seen = 1, stack[kMaxK], sp = 0, vis = 1;
+        stack[sp++] = 0;
+        while (sp) {
+            const int u = stack[--sp];
+            for (int v = 0; v < k; ++v)
+                if (p->adj[u][v] && !((vis >> v) & 1)) { vis |= 1 << v; ++seen; stack[sp++] = v; }
+        }
+        if (seen != k) { delete p; return fail(MAPA_E_DISCONNECTED, "pattern: disconnected (k > 1)"); }
+    }
+    for (int j = 0; j < k; ++j) {
+        p->back[j] = 0;
+        for (int i = 0; i < j; ++i)
+            if (p->adj[i][j]) p->back[j] |= (uint8_t)(1u << i);
+    }
+    // Aut(P) by brute force (k! <= 40320), then lex-leader constraints along
+    // the point-stabiliser chain: for every vertex i, every u != i in the orbit
+    // of i under the stabiliser of 0..i-1 gets the constraint f(i) < f(u).
+    // This keeps exactly the lex-min mapping of every Aut-orbit.
+    std::vector<std::vector<int>> aut;
+    std::vector<int> s(k);
+    for (int i = 0; i < k; ++i) s[i] = i;
+    do {
+        bool ok = true;
+        for (auto &e : p->edges)
+            if (!p->adj[s[e.first]][s[e.second]]) { ok = false; break; }
+        if (ok) aut.push_back(s);
+    } while (std::next_permutation(s.begin(), s.end()));
+    p->aut = (int)aut.size();
+    std::memset(p->src, 0, sizeof(p->src));
+    for (int i = 0; i < k; ++i) {
+        for (auto &a : aut) {
+            bool fixes = true;
+            for (int j = 0; j < i; ++j)
+                if (a[j] != j) { fixes = false; break; }
+            if (fixes && a[i] != i) p->src[a[i]] |= (uint8_t)(1u << i);
+        }
+    }
+    p->lut = rank_table(p->m);
+    *out = p;
+    return MAPA_OK;
+}
+
+void fill_devpattern(const mapa_pattern *p, bool raw, uint16_t lut_off, DevPattern &dp) {
+    std::memset(&dp, 0, sizeof(dp));
+    dp.k = (uint8_t)p->k;
+    dp.m = (uint8_t)p->m;
+    dp.eb = (uint8_t)(p->k * (p->k - 1) / 2);
+    dp.clique = p->m == dp.eb;
+    for (int j = 0; j < p->k; ++j) {
+        for (int u = j + 1; u < p->k; ++u) {
+            if (p->adj[j][u]) dp.fwd_back[j] |= (uint8_t)(1u << u);
+            if (!raw && ((p->src[u] >> j) & 1)) dp.fwd_src[j] |= (uint8_t)(1u << u);
+        }
+        dp.dback[j] = (uint8_t)__builtin_popcount(p->back[j]);
+    }
+    for (int e = 0; e < p->m; ++e) dp.edge[e] = (uint8_t)(p->edges[e].first | (p->edges[e].second << 4));
+    dp.lut_off = lut_off;
+    dp.aut = (uint16_t)p->aut;
+}
+
+bool key_fits(const mapa_topology *t, const mapa_pattern *p) {
+    return 15 + t->width + p->k * (p->k - 1) / 2 <= 63;
+}
+
+uint64_t perm_count(int n, int d) {
+    uint64_t r = 1;
+    for (int j = 0; j < d; ++j) r *= (uint64_t)(n - j);
+    return r;
+}
+
+mapa_status cuda_fail(int err, const char *what) {
+    return fail(MAPA_E_CUDA, std::string(what) + ": " + cuda_error_string(err));
+}
+
+struct Plan {
+    int depth, chunk, grid;
+    uint64_t nlocal;
+};
+
+Plan plan_single(const mapa_topology *t, const mapa_pattern *p, int sensk, int nF, int world) {
+    Plan pl{};
+    const int W = t->width, G = 32 / W, k = p->k;
+    int sm = device_sm_count();
+    if (sm <= 0) sm = 148;
+    const int occ = max_blocks_per_sm_single(W, k, sensk);
+    const uint64_t resident_warps = (uint64_t)sm * occ * 8;
+    const uint64_t target = 32ull * resident_warps * G * (uint64_t)world;
+    int dmax = k <= 1 ? 0 : std::max(1, std::min(k - 2, 4));
+    int d = k <= 1 ? 0 : 1;
+    while (d < dmax && perm_count(nF, d) < target) ++d;
+    pl.depth = d;
+    const uint64_t items = nF >= k ? perm_count(nF, d) : 0;
+    pl.nlocal = (items + world - 1) / world;
+    uint64_t chunk = pl.nlocal / (resident_warps * 16);
+    chunk = std::max<uint64_t>(chunk, 1);
+    chunk = ((chunk + G - 1) / G) * G;
+    pl.chunk = (int)std::min<uint64_t>(chunk, 1u << 20);
+    const uint64_t warps_needed = (pl.nlocal + pl.chunk - 1) / pl.chunk;
+    const uint64_t blocks = std::max<uint64_t>(1, (warps_needed + 7) / 8);
+    pl.grid = (int)std::min<uint64_t>(blocks, (uint64_t)sm * occ);
+    return pl;
+}
+
+mapa_status decode_record(const mapa_topology *t, const mapa_pattern *p, uint32_t busy, int selector,
+                          int sens, uint32_t flags, const mapa_record *rec, mapa_decision *out) {
+    mapa_decision d;
+    std::memset(&d, 0, sizeof(d));
+    d.k = p->k;
+    d.m = p->m;
+    d.key = rec->key;
+    d.leaves_scored = rec->leaves;
+    const bool raw = (flags & MAPA_F_RAW) != 0;
+    if (raw) {
+        d.raw_embeddings = rec->leaves;
+        d.distinct_matches = rec->leaves / (uint64_t)p->aut;
+    } else {
+        d.distinct_matches = rec->leaves;
+        d.raw_embeddings = rec->leaves * (uint64_t)p->aut;
+    }
+    const uint32_t F = ~busy & nmask_of(t->n);
+    if (rec->status != 0) return fail(MAPA_E_INVALID_ARG, "device reported a bad query");
+    if (rec->key == 0) {
+        d.status = MAPA_NO_CAPACITY;
+        *out = d;
+        return MAPA_NO_CAPACITY;
+    }
+    const int W = t->width, eb = p->k * (p->k - 1) / 2, k = p->k;
+    const uint64_t key = rec->key;
+    const uint32_t score = (uint32_t)(key >> (W + eb));
+    const uint32_t sb = (uint32_t)((key >> eb) & (W >= 32 ? 0xFFFFFFFFull : ((1ull << W) - 1)));
+    const uint32_t ecode = (uint32_t)(key & ((1ull << eb) - 1));
+    uint32_t S = 0;
+    for (int dv = 0; dv < W; ++dv)
+        if ((sb >> (W - 1 - dv)) & 1u) S |= 1u << dv;
+    if (__builtin_popcount(S) != k || (S & ~F)) return fail(MAPA_E_INTERNAL, "decoded device set inconsistent");
+    std::vector<int> ds;
+    for (int dv = 0; dv < t->n; ++dv)
+        if ((S >> dv) & 1u) ds.push_back(dv);
+    // used-edge set from the edge code (pair p in lex order of rank pairs)
+    std::vector<std::pair<int, int>> E;
+    int pidx = 0;
+    for (int a = 0; a < k; ++a)
+        for (int b = a + 1; b < k; ++b, ++pidx)
+            if ((ecode >> (eb - 1 - pidx)) & 1u) E.push_back({ds[a], ds[b]});
+    if ((int)E.size() != p->m) return fail(MAPA_E_INTERNAL, "decoded edge set has wrong size");
+    std::sort(E.begin(), E.end());
+    // lex-first mapping of S producing E
+    std::vector<int> pi = ds;
+    bool found = false;
+    do {
+        std::vector<std::pair<int, int>> img;
+        for (auto &e : p->edges) {
+            int a = pi[e.first], b = pi[e.second];
+            img.push_back({std::min(a, b), std::max(a, b)});
+        }
+        std::sort(img.begin(), img.end());
+        if (img == E) { found = true; break; }
+    } while (std::next_permutation(pi.begin(), pi.end()));
+    if (!found) return fail(MAPA_E_INTERNAL, "no mapping of the decoded set yields the decoded edges");
+    int agg = 0, x = 0, y = 0, z = 0;
+    for (auto &e : E) {
+        const int c = t->cls[e.first][e.second];
+        agg += kClassBw[c];
+        if (c == 0) ++x;
+        else if (c == 3) ++z;
+        else ++y;
+    }
+    int pres = 0;
+    for (int u = 0; u < t->n; ++u)
+        for (int v = u + 1; v < t->n; ++v)
+            if (((F >> u) & (F >> v) & 1u) && !((S >> u) & 1u) && !((S >> v) & 1u)) pres += bw_of(t, u, v);
+    uint32_t expect = 0;
+    if (selector == MAPA_SEL_GREEDY) expect = (uint32_t)agg;
+    else if (selector == MAPA_SEL_PRESERVE) expect = sens ? p->lut[x * (p->m + 1) + y] : (uint32_t)pres;
+    if (expect != score) return fail(MAPA_E_INTERNAL, "key score does not match the decoded match");
+    d.status = MAPA_OK;
+    d.device_mask = S;
+    for (int i = 0; i < k; ++i) d.mapping[i] = (int8_t)pi[i];
+    for (size_t i = 0; i < E.size(); ++i) { d.used[i][0] = E[i].first; d.used[i][1] = E[i].second; }
+    d.x = x; d.y = y; d.z = z;
+    d.agg_bw = agg;
+    d.preserved_bw = pres;
+    d.score = (int32_t)score;
+    d.pred_effbw = eq2(x, y, z);
+    *out = d;
+    return MAPA_OK;
+}
+
+mapa_status build_multi(const mapa_topology *t, const mapa_pattern *const *pats, int npats, uint32_t flags,
+                        MultiTables *tb) {
+    if (npats < 1 || npats > kMaxPats) return fail(MAPA_E_INVALID_ARG, "npats must be 1..16");
+    std::memset(tb, 0, sizeof(*tb));
+    fill_devtopo(t, tb->topo);
+    tb->npats = npats;
+    int off = 0;
+    for (int i = 0; i < npats; ++i) {
+        if (!pats[i]) return fail(MAPA_E_INVALID_ARG, "null pattern");
+        const int n = (int)pats[i]->lut.size();
+        if (off + n > kLutCapMulti) return fail(MAPA_E_UNSUPPORTED, "rank tables exceed 4096 entries");
+        fill_devpattern(pats[i], (flags & MAPA_F_RAW) != 0, (uint16_t)off, tb->pat[i]);
+        std::memcpy(tb->lut + off, pats[i]->lut.data(), n * sizeof(uint16_t));
+        off += n;
+    }
+    return MAPA_OK;
+}
+
+}  // namespace
+
+// =================================================================== C-ABI
+extern "C" {
+
+const char *mapa_last_error(void) { return g_err.c_str(); }
+const char *mapa_version(void) { return "mapa-b200 0.1 (sm_100a)"; }
+
+mapa_status mapa_load_topology(const char *spec, int32_t is_text, mapa_topology **out) {
+    if (!spec || !out) return fail(MAPA_E_INVALID_ARG, "null argument");
+    mapa_topology *t = new (std::nothrow) mapa_topology();
+    if (!t) return fail(MAPA_E_INVALID_ARG, "out of memory");
+    if (!is_text) {
+        if (!build_builtin(spec, t)) {
+            delete t;
+            return fail(MAPA_E_INVALID_ARG, std::string("unknown builtin '") + spec +
+                                                "'; valid: dgx1v dgx1p summit torus2d16 cubemesh16");
+        }
+    } else {
+        mapa_status st = parse_topology_text(spec, t);
+        if (st != MAPA_OK) { delete t; return st; }
+    }
+    *out = t;
+    return MAPA_OK;
+}
+
+void mapa_free_topology(mapa_topology *t) {
+    if (!t) return;
+    if (t->d_stage) cudaFree(t->d_stage);
+    if (t->h_stage) cudaFreeHost(t->h_stage);
+    delete t;
+}
+
+mapa_status mapa_topology_info(const mapa_topology *t, int32_t *n, int32_t *width, int32_t *bw, uint32_t *busy) {
+    if (!t) return fail(MAPA_E_INVALID_ARG, "null topology");
+    if (n) *n = t->n;
+    if (width) *width = t->width;
+    if (busy) *busy = t->busy;
+    if (bw)
+        for (int u = 0; u < t->n; ++u)
+            for (int v = 0; v < t->n; ++v) bw[u * t->n + v] = u == v ? 0 : bw_of(t, u, v);
+    return MAPA_OK;
+}
+
+mapa_status mapa_claim(mapa_topology *t, uint32_t mask) {
+    if (!t) return fail(MAPA_E_INVALID_ARG, "null topology");
+    if (mask & ~nmask_of(t->n)) return fail(MAPA_E_ID_RANGE, "device id out of range");
+    if (mask & t->busy) return fail(MAPA_E_ALREADY_BUSY, "device already busy");
+    t->busy |= mask;
+    return MAPA_OK;
+}
+
+mapa_status mapa_release(mapa_topology *t, uint32_t mask) {
+    if (!t) return fail(MAPA_E_INVALID_ARG, "null topology");
+    if (mask & ~nmask_of(t->n)) return fail(MAPA_E_ID_RANGE, "device id out of range");
+    if (mask & ~t->busy) return fail(MAPA_E_NOT_BUSY, "releasing a device that is not busy");
+    t->busy &= ~mask;
+    return MAPA_OK;
+}
+
+mapa_status mapa_set_busy(mapa_topology *t, uint32_t busy) {
+    if (!t) return fail(MAPA_E_INVALID_ARG, "null topology");
+    if (busy & ~nmask_of(t->n)) return fail(MAPA_E_ID_RANGE, "device id out of range");
+    t->busy = busy;
+    return MAPA_OK;
+}
+
+mapa_status mapa_load_pattern(int32_t k, int32_t m, const int32_t *edges, uint32_t flags, mapa_pattern **out) {
+    if (!out || m < 0 || (m > 0 && !edges)) return fail(MAPA_E_INVALID_ARG, "bad pattern arguments");
+    if (k < 1 || k > kMaxK) return fail(MAPA_E_UNSUPPORTED, "pattern: need 1 <= k <= 8");
+    if (m > k * (k - 1) / 2) return fail(MAPA_E_INVALID_ARG, "pattern: more edges than vertex pairs");
+    std::vector<std::pair<int, int>> e;
+    for (int i = 0; i < m; ++i) e.push_back({edges[2 * i], edges[2 * i + 1]});
+    return compile_pattern(k, e, flags, out);
+}
+
+mapa_status mapa_make_pattern(int32_t shape, int32_t k, mapa_pattern **out) {
+    if (!out) return fail(MAPA_E_INVALID_ARG, "null out");
+    if (k < 1 || k > kMaxK) return fail(MAPA_E_UNSUPPORTED, "pattern: need 1 <= k <= 8");
+    std::vector<std::pair<int, int>> e;
+    const bool ring = shape == MAPA_SHAPE_RING || shape == MAPA_SHAPE_RINGTREE;
+    const bool tree = shape == MAPA_SHAPE_TREE || shape == MAPA_SHAPE_RINGTREE;
+    if (shape == MAPA_SHAPE_RING && k == 1) return fail(MAPA_E_INVALID_ARG, "Ring requires k >= 2");
+    if (shape < 0 || shape > MAPA_SHAPE_EDGELESS) return fail(MAPA_E_INVALID_ARG, "unknown shape");
+    std::map<std::pair<int, int>, int> set;
+    if (ring) {
+        if (k == 2) set[{0, 1}] = 1;
+        if (k >= 3)
+            for (int i = 0; i < k; ++i) set[{std::min(i, (i + 1) % k), std::max(i, (i + 1) % k)}] = 1;
+    }
+    if (tree)
+        for (int i = 0; i < k; ++i)
+            for (int c = 2 * i + 1; c <= 2 * i + 2; ++c)
+                if (c < k) set[{i, c}] = 1;
+    if (shape == MAPA_SHAPE_FULL)
+        for (int a = 0; a < k; ++a)
+            for (int b = a + 1; b < k; ++b) set[{a, b}] = 1;
+    for (auto &kv : set) e.push_back(kv.first);
+    return compile_pattern(k, e, shape == MAPA_SHAPE_EDGELESS ? MAPA_F_ALLOW_DISCONNECTED : 0, out);
+}
+
+void mapa_free_pattern(mapa_pattern *p) { delete p; }
+
+mapa_status mapa_get_pattern_info(const mapa_pattern *p, mapa_pattern_info *out) {
+    if (!p || !out) return fail(MAPA_E_INVALID_ARG, "null argument");
+    std::memset(out, 0, sizeof(*out));
+    out->k = p->k;
+    out->m = p->m;
+    out->aut_order = p->aut;
+    for (int j = 0; j < p->k; ++j) { out->back[j] = p->back[j]; out->lex_src[j] = p->src[j]; }
+    for (int e = 0; e < p->m; ++e) { out->edges[e][0] = p->edges[e].first; out->edges[e][1] = p->edges[e].second; }
+    return MAPA_OK;
+}
+
+double mapa_pred_effbw(int32_t x, int32_t y, int32_t z) { return eq2(x, y, z); }
+
+mapa_status mapa_effbw_rank_table(int32_t m, uint16_t *out) {
+    if (m < 0 || m > 28 || !out) return fail(MAPA_E_INVALID_ARG, "m must be 0..28");
+    std::vector<uint16_t> l = rank_table(m);
+    std::memcpy(out, l.data(), l.size() * sizeof(uint16_t));
+    return MAPA_OK;
+}
+
+mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
+                                  int32_t sensitive, const mapa_query *d_query, mapa_record *d_record,
+                                  uint32_t flags, int32_t rank, int32_t world, uint32_t busy_hint,
+                                  void *stream) {
+    if (!t || !p || !d_query || !d_record) return fail(MAPA_E_INVALID_ARG, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) return fail(MAPA_E_INVALID_ARG, "bad rank/world");
+    if (selector < 0 || selector > 2) return fail(MAPA_E_INVALID_ARG, "bad selector");
+    if (!key_fits(t, p)) return fail(MAPA_E_UNSUPPORTED, "key budget 15 + W + C(k,2) > 63");
+    const int nF = busy_hint == 0xFFFFFFFFu ? t->n : __builtin_popcount(~busy_hint & nmask_of(t->n));
+    const int sensk = (selector == MAPA_SEL_PRESERVE && sensitive) ? 1 : 0;
+    Plan pl = plan_single(t, p, sensk, nF, world);
+    if (pl.nlocal >= (1ull << 27)) return fail(MAPA_E_UNSUPPORTED, "too many work items");
+    static_assert(sizeof(SingleTables) < 32000, "kernel parameter block too large");
+    SingleTables tb;
+    std::memset(&tb, 0, sizeof(tb));
+    fill_devtopo(t, tb.topo);
+    tb.npats = 1;
+    fill_devpattern(p, (flags & MAPA_F_RAW) != 0, 0, tb.pat[0]);
+    std::memcpy(tb.lut, p->lut.data(), p->lut.size() * sizeof(uint16_t));
+    int err = (int)cudaMemsetAsync(d_record, 0, sizeof(mapa_record), (cudaStream_t)stream);
+    if (err) return cuda_fail(err, "cudaMemsetAsync");
+    err = launch_single(tb, selector, sensitive, d_query, d_record, pl.depth, rank, world, pl.chunk, pl.grid, stream);
+    if (err) return cuda_fail(err, "esa_single launch");
+    return MAPA_OK;
+}
+
+mapa_status mapa_reduce_records(const mapa_record *records, int32_t n, mapa_record *out) {
+    if (!records || !out || n < 1) return fail(MAPA_E_INVALID_ARG, "bad records");
+    mapa_record r;
+    std::memset(&r, 0, sizeof(r));
+    for (int i = 0; i < n; ++i) {
+        r.key = std::max(r.key, records[i].key);
+        r.leaves += records[i].leaves;
+        r.status |= records[i].status;
+    }
+    *out = r;
+    return MAPA_OK;
+}
+
+mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint32_t busy, int32_t selector,
+                        int32_t sens, uint32_t flags, const mapa_record *record, mapa_decision *out) {
+    if (!t || !p || !record || !out) return fail(MAPA_E_INVALID_ARG, "null argument");
+    return decode_record(t, p, busy, selector, sens, flags, record, out);
+}
+
+mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selector, int32_t sens,
+                          uint32_t flags, void *stream, mapa_decision *out) {
+    if (!t || !p || !out) return fail(MAPA_E_INVALID_ARG, "null argument");
+    if (selector < 0 || selector > 2) return fail(MAPA_E_INVALID_ARG, "bad selector");
+    if (!key_fits(t, p)) return fail(MAPA_E_UNSUPPORTED, "key budget 15 + W + C(k,2) > 63");
+    const uint32_t F = ~t->busy & nmask_of(t->n);
+    if (p->k > __builtin_popcount(F)) {
+        std::memset(out, 0, sizeof(*out));
+        out->status = MAPA_NO_CAPACITY;
+        out->k = p->k;
+        out->m = p->m;
+        return MAPA_NO_CAPACITY;
+    }
+    int err;
+    if (!t->d_stage) {
+        if ((err = (int)cudaMalloc(&t->d_stage, 64))) return cuda_fail(err, "cudaMalloc");
+    }
+    if (!t->h_stage) {
+        if ((err = (int)cudaMallocHost(&t->h_stage, 64))) return cuda_fail(err, "cudaMallocHost");
+    }
+    mapa_query *hq = (mapa_query *)t->h_stage;
+    mapa_record *hr = (mapa_record *)((char *)t->h_stage + 32);
+    mapa_query *dq = (mapa_query *)t->d_stage;
+    mapa_record *dr = (mapa_record *)((char *)t->d_stage + 32);
+    hq->busy = t->busy;
+    hq->pattern = 0;
+    hq->selector = selector;
+    hq->sensitive = sens;
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((err = (int)cudaMemcpyAsync(dq, hq, sizeof(mapa_query), cudaMemcpyHostToDevice, st)))
+        return cuda_fail(err, "H2D query");
+    mapa_status s = mapa_launch_query(t, p, selector, sens, dq, dr, flags, 0, 1, t->busy, stream);
+    if (s != MAPA_OK) return s;
+    if ((err = (int)cudaMemcpyAsync(hr, dr, sizeof(mapa_record), cudaMemcpyDeviceToHost, st)))
+        return cuda_fail(err, "D2H record");
+    if ((err = (int)cudaStreamSynchronize(st))) return cuda_fail(err, "cudaStreamSynchronize");
+    mapa_decision d;
+    s = decode_record(t, p, t->busy, selector, sens, flags, hr, &d);
+    if (s < 0) return s;
+    if (s == MAPA_OK && (flags & MAPA_F_COMMIT)) t->busy |= d.device_mask;
+    *out = d;
+    return s;
+}
+
+mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *const *pats, int32_t npats,
+                                int64_t nq, const mapa_query *d_queries, mapa_record *d_results,
+                                void *d_scratch, uint32_t flags, void *stream) {
+    if (!t || !pats || (nq > 0 && (!d_queries || !d_results || !d_scratch)) || nq < 0)
+        return fail(MAPA_E_INVALID_ARG, "null argument");
+    static thread_local MultiTables *tbp = nullptr;  // ~10 KB: keep off the stack
+    if (!tbp) tbp = new MultiTables();
+    mapa_status s = build_multi(t, pats, npats, flags, tbp);
+    if (s != MAPA_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    int err;
+    if (nq == 0) return MAPA_OK;
+    if ((err = (int)cudaMemsetAsync(d_results, 0, (size_t)nq * sizeof(mapa_record), st))) return cuda_fail(err, "memset");
+    if ((err = (int)cudaMemsetAsync(d_scratch, 0, 64, st))) return cuda_fail(err, "memset");
+    int sm = device_sm_count();
+    if (sm <= 0) sm = 148;
+    const int grid = sm * max_blocks_per_sm_batch(t->width);
+    err = launch_batch(*tbp, nq, d_queries, d_results, (uint32_t *)d_scratch, grid, stream);
+    if (err) return cuda_fail(err, "esa_batch launch");
+    return MAPA_OK;
+}
+
+mapa_status mapa_trace_replay(const mapa_topology *t, const mapa_pattern *const *pats, int32_t npats,
+                              int32_t ntraces, int32_t nops, const mapa_trace_op *d_ops, int32_t njobs,
+                              const mapa_query *d_jobs, uint64_t *d_keys, uint32_t flags, void *stream) {
+    if (!t || !pats || ntraces < 0 || nops < 0 || njobs < 0) return fail(MAPA_E_INVALID_ARG, "bad argument");
+    if (ntraces == 0) return MAPA_OK;
+    if (!d_ops || !d_jobs || !d_keys) return fail(MAPA_E_INVALID_ARG, "null device buffer");
+    static thread_local MultiTables *tbp = nullptr;
+    if (!tbp) tbp = new MultiTables();
+    mapa_status s = build_multi(t, pats, npats, flags, tbp);
+    if (s != MAPA_OK) return s;
+    int err = (int)cudaMemsetAsync(d_keys, 0, (size_t)ntraces * njobs * sizeof(uint64_t), (cudaStream_t)stream);
+    if (err) return cuda_fail(err, "memset");
+    err = launch_trace(*tbp, ntraces, nops, d_ops, njobs, d_jobs, d_keys, stream);
+    if (err) return cuda_fail(err, "esa_trace launch");
+    return MAPA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,304 @@
+"""GPU parity: the sm_100a path through the C-ABI vs the CPU oracle, element by
+element on the same seeded inputs (decision fields and counts bit-exact,
+Eq. 2 double within 1e-6 relative — north_star tolerance)."""
+import itertools
+import json
+import math
+import os
+import random
+
+import pytest
+
+import workloads as W
+from oracle import coracle as co
+from oracle import mapa_oracle as mo
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2110_03214_b200 as mp  # noqa: E402
+from paper_2110_03214_b200 import dist as md  # noqa: E402
+
+FIELDS = ("devices", "mapping", "used_edges", "x", "y", "z", "agg_bw", "preserved_bw", "raw", "distinct")
+SELS = [(0, False), (1, True), (1, False), (2, False)]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    torch.cuda.init()
+
+
+def same(o, g, ctx=""):
+    assert o["status"] == g["status"], (ctx, o, g)
+    if o["status"] != "ok":
+        return
+    for f in FIELDS:
+        assert o[f] == g[f], (ctx, f, o[f], g[f])
+    assert abs(o["pred_effbw"] - g["pred_effbw"]) <= 1e-6 * max(1.0, abs(o["pred_effbw"])), ctx
+
+
+def gpu(topo: mp.Topology, busy, shape, k, sel, sens, raw):
+    topo.set_busy(busy)
+    return mp.allocate(topo, mp.Pattern.make(shape, k), sel, sens, raw=raw)
+
+
+def oracle(o, busy, shape, k, sel, sens, use_c=False):
+    kk, e = mo.make_pattern(shape, k)
+    if use_c:
+        return co.allocate(o, busy, kk, e, sel, sens)
+    return mo.allocate(o, busy, kk, e, sel, sens)
+
+
+def test_c1_expected_answer():
+    """C1: dgx1v ring-3 all free -> {1,3,4} (1-based), (2,1,0), 125, 311,
+    57.857167; raw 336 / distinct 56 in both modes."""
+    t = mp.Topology("dgx1v")
+    o = mo.builtin("dgx1v")
+    for sel, sens in SELS:
+        for raw in (False, True):
+            g = gpu(t, 0, "ring", 3, sel, sens, raw)
+            same(oracle(o, 0, "ring", 3, sel, sens), g, (sel, sens, raw))
+            assert g["leaves"] == (336 if raw else 56)
+            if sel != 2:
+                assert g["devices"] == (0, 2, 3)
+
+
+@pytest.mark.parametrize("name", ["dgx1v", "dgx1p", "summit", "torus2d16", "cubemesh16"])
+def test_random_small_vs_oracle(name):
+    o = mo.builtin(name)
+    t = mp.Topology(name)
+    rng = random.Random(sum(map(ord, name)) * 7)
+    ntr = 60 if o.n <= 8 else 40
+    for trial in range(ntr):
+        shape = rng.choice(["ring", "tree", "ringtree", "full"])
+        k = rng.randint(2 if shape == "ring" else 1, 6 if o.n <= 8 else 5)
+        busy = rng.randrange(0, 1 << o.n)
+        if o.n > 8:  # keep the python-free C oracle fast
+            busy |= (1 << rng.randint(0, 3)) - 1
+        sel, sens = rng.choice(SELS)
+        raw = bool(trial & 1)
+        g = gpu(t, busy, shape, k, sel, sens, raw)
+        ob = oracle(o, busy, shape, k, sel, sens, use_c=True)
+        same(ob, g, (name, trial, shape, k, hex(busy), sel, sens, raw))
+        if ob["status"] == "ok":
+            assert g["leaves"] == (ob["raw"] if raw else ob["distinct"])
+
+
+def test_text_topologies_vs_oracle():
+    rng = random.Random(1234)
+    for text in (W.rand_text(8, 3), W.rand_text(13, 4), W.rand_text(21, 5), W.het32_text(),
+                 W.rand_text(32, W.MASTER_SEED)):
+        o = mo.parse_topology(text)
+        t = mp.Topology(text=text)
+        for trial in range(12):
+            shape = rng.choice(["ring", "tree", "ringtree", "full"])
+            k = rng.randint(2, 4 if o.n > 16 else 5)
+            nb = max(0, o.n - rng.randint(k, min(o.n, 12)))
+            busy = sum(1 << d for d in rng.sample(range(o.n), nb))
+            sel, sens = rng.choice(SELS)
+            raw = bool(trial & 1)
+            same(oracle(o, busy, shape, k, sel, sens, use_c=True), gpu(t, busy, shape, k, sel, sens, raw),
+                 (o.name, trial, shape, k, hex(busy), sel, sens, raw))
+
+
+def test_large_k_vs_oracle():
+    """k = 7, 8 (key budget holds for W <= 16), ragged free sets."""
+    rng = random.Random(77)
+    for name in ("dgx1v", "cubemesh16", "torus2d16"):
+        o = mo.builtin(name)
+        t = mp.Topology(name)
+        for k in (7, 8):
+            for shape in ("ring", "tree", "full"):
+                nf = min(o.n, k + rng.randint(0, 1))
+                busy = sum(1 << d for d in rng.sample(range(o.n), o.n - nf))
+                sel, sens = rng.choice(SELS[:3])
+                for raw in (False, True):
+                    same(oracle(o, busy, shape, k, sel, sens, use_c=True), gpu(t, busy, shape, k, sel, sens, raw),
+                         (name, k, shape, hex(busy), sel, sens, raw))
+
+
+def test_edge_cases():
+    o = mo.builtin("dgx1v")
+    t = mp.Topology("dgx1v")
+    # no capacity
+    assert gpu(t, 0b11111110, "ring", 2, 0, False, False)["status"] == "no_capacity"
+    assert gpu(t, 0xFF, "full", 1, 0, False, True)["status"] == "no_capacity"
+    # k == |F|, k = 1, empty pattern on many devices
+    for busy in (0b00001111, 0b10100101, 0):
+        for shape, k in (("full", 4), ("tree", 4), ("full", 1), ("edgeless", 3)):
+            for sel, sens in SELS:
+                for raw in (False, True):
+                    same(oracle(o, busy, shape, k, sel, sens), gpu(t, busy, shape, k, sel, sens, raw),
+                         (hex(busy), shape, k, sel, sens, raw))
+    # N = 32 with the top device free / busy
+    text = W.het32_text()
+    o32, t32 = mo.parse_topology(text), mp.Topology(text=text)
+    for busy in (0x7FFFFFF0 ^ 0x00F0F000, 0xFFFFFF00 ^ 0x80000000, 0x0FFFFFFF):
+        for sel, sens in SELS:
+            same(oracle(o32, busy, "ring", 3, sel, sens, use_c=True), gpu(t32, busy, "ring", 3, sel, sens, True))
+
+
+def test_unsupported_key_budget():
+    t = mp.Topology(text=W.het32_text())
+    with pytest.raises(mp.MapaError) as e:
+        mp.allocate(t, mp.Pattern.make("ring", 8), 0, False)
+    assert e.value.status == mp.E_UNSUPPORTED
+
+
+def test_commit_and_release_roundtrip():
+    t = mp.Topology("dgx1v")
+    p = mp.Pattern.make("ring", 3)
+    d1 = mp.allocate(t, p, 0, False, commit=True)
+    assert t.busy == sum(1 << d for d in d1["devices"])
+    d2 = mp.allocate(t, p, 0, False, commit=True)
+    assert d2["devices"] == (4, 6, 7)  # S:354 analogue: next best triangle {5,7,8}
+    t.release(sum(1 << d for d in d1["devices"]))
+    assert t.busy == sum(1 << d for d in d2["devices"])
+
+
+def test_sharded_virtual_ranks_equal_unsharded():
+    """Sharding by work item (rank = i % world) + max/sum combine gives the
+    unsharded record for every world size (S:369 determinism)."""
+    text = W.rand_text(32, W.MASTER_SEED)
+    t = mp.Topology(text=text)
+    for shape, k, busy in (("full", 5, 0), ("ring", 5, 0x0000FF00), ("tree", 6, 0xF0F0F0F0)):
+        pat = mp.Pattern.make(shape, k)
+        for sel, sens in SELS[:3]:
+            for raw in (True, False):
+                ref, _ = md.run_query(t, pat, sel, sens, busy, raw=raw)
+                torch.cuda.synchronize()
+                ref = md.records_from_tensor(ref)[0]
+                for world in (2, 3, 8):
+                    recs = []
+                    for r in range(world):
+                        rt, _ = md.run_query(t, pat, sel, sens, busy, raw=raw, rank=r, world=world)
+                        torch.cuda.synchronize()
+                        recs.append(md.records_from_tensor(rt)[0])
+                    comb = mp.reduce_records(recs)
+                    assert comb.key == ref.key and comb.leaves == ref.leaves, (shape, k, world, raw)
+                d = mp.decode(t, pat, busy, sel, sens, ref, raw=raw)
+                nf = 32 - bin(busy).count("1")
+                assert d["raw"] == math.perm(nf, k)
+
+
+def test_determinism_repeat():
+    t = mp.Topology(text=W.het32_text())
+    pat = mp.Pattern.make("tree", 5)
+    keys = {mp.allocate(t, pat, 1, False, raw=True)["key"] for _ in range(5)}
+    assert len(keys) == 1
+
+
+def test_c4_full_size_golden(golden_dir):
+    """C4 at full size in the bench launch configuration: het32 / rand32,
+    full-6, all free, RAW mode (652,458,240 embeddings) vs the oracle's
+    decisions (tests/golden/make_golden.py, oracle/ only)."""
+    gold = json.load(open(os.path.join(golden_dir, "c4_expected.json")))
+    tops = {"het32": W.het32_text(), "rand32_2110": W.rand_text(32, W.MASTER_SEED)}
+    sel_of = {"greedy": (0, False), "sensitive": (1, True), "insensitive": (1, False)}
+    pat = mp.Pattern.make("full", 6)
+    for case in gold["cases"]:
+        t = mp.Topology(text=tops[case["topology"]])
+        sel, sens = sel_of[case["selector"]]
+        for raw in (True, False):
+            g = mp.allocate(t, pat, sel, sens, raw=raw)
+            exp = dict(case)
+            exp["devices"] = tuple(exp["devices"])
+            exp["mapping"] = tuple(exp["mapping"])
+            exp["used_edges"] = [tuple(e) for e in exp["used_edges"]]
+            same(exp, g, (case["topology"], case["selector"], raw))
+            assert g["leaves"] == (652458240 if raw else 906192)
+
+
+def test_batch_vs_oracle_and_counts():
+    """C5-shaped batch: every query's leaf count equals the closed form, a
+    sample of decisions equals the oracle."""
+    for name, text in (("cubemesh16", None), ("het32", W.het32_text())):
+        o = mo.builtin(name) if text is None else mo.parse_topology(text)
+        t = mp.Topology(name) if text is None else mp.Topology(text=text)
+        qs = W.c5_queries(o.n, count=2000, seed=99)
+        shapes = [(s, k) for s in ("ring", "tree", "full") for k in range(2, 6)]
+        pats = [mp.Pattern.make(s, k) for s, k in shapes]
+        auts = [p.info()["aut"] for p in pats]
+        pid = {sk: i for i, sk in enumerate(shapes)}
+        rows = [(q["busy"], pid[(q["shape"], q["k"])], q["selector"], q["sensitive"]) for q in qs]
+        for raw in (True, False):
+            res = md.run_batch(t, pats, md.queries_tensor(rows), raw=raw)
+            torch.cuda.synchronize()
+            recs = md.records_from_tensor(res)
+            for i, (q, r) in enumerate(zip(qs, recs)):
+                nf = o.n - bin(q["busy"]).count("1")
+                p = math.perm(nf, q["k"])
+                assert r.leaves == (p if raw else p // auts[rows[i][1]]), (name, i)
+                assert r.status == 0
+            rng = random.Random(5)
+            for i in rng.sample(range(len(qs)), 25):
+                q = qs[i]
+                d = mp.decode(t, pats[rows[i][1]], q["busy"], q["selector"], q["sensitive"], recs[i], raw=raw)
+                same(oracle(o, q["busy"], q["shape"], q["k"], q["selector"], q["sensitive"], use_c=True), d,
+                     (name, i, raw))
+
+
+def _trace_inputs(topo_name, seed, policy):
+    jobs = W.c2_jobs(seed, 1000)
+    n = mo.builtin(topo_name).n
+    ops = W.fifo_ops(jobs, n)
+    shapes = [(s, k) for s in ("ring", "tree", "full") for k in range(2, 6)]
+    pid = {sk: i for i, sk in enumerate(shapes)}
+    jrows = []
+    for j in jobs:
+        if policy == "preserve":
+            jrows.append([0, pid[(j["shape"], j["k"])], 1, j["sensitive"]])
+        else:
+            jrows.append([0, pid[(j["shape"], j["k"])], 0, 0])
+    return jobs, ops, shapes, jrows
+
+
+@pytest.mark.parametrize("topo_name", ["dgx1p", "summit"])
+@pytest.mark.parametrize("policy", ["preserve", "greedy"])
+def test_c2_trace_replay_vs_oracle(topo_name, policy):
+    """C2: 1000-job FIFO trace replayed entirely on the device; every
+    allocation must equal the oracle's replay (§3.6 state management)."""
+    jobs, ops, shapes, jrows = _trace_inputs(topo_name, 2110 + len(topo_name), policy)
+    t = mp.Topology(topo_name)
+    pats = [mp.Pattern.make(s, k) for s, k in shapes]
+    dops = torch.tensor([[o, j] for o, j in ops], dtype=torch.int32, device="cuda").reshape(1, -1, 2)
+    djobs = torch.tensor(jrows, dtype=torch.int32, device="cuda").reshape(1, -1, 4)
+    for raw in (False, True):
+        keys = md.run_trace(t, pats, dops, djobs, raw=raw)
+        torch.cuda.synchronize()
+        keys = keys.cpu().tolist()[0]
+        o = mo.builtin(topo_name)
+        patd = {(s, k): mo.make_pattern(s, k) for s, k in shapes}
+
+        def alloc(topo, busy, k, pe, sel, sens):
+            return co.allocate(topo, busy, k, pe, sel, sens, nthreads=1)
+
+        exp = mo.replay_trace(o, jobs, ops, patd, policy, allocate_fn=alloc)
+        W8 = t.width
+        for j, d in exp.items():
+            k = jobs[j]["k"]
+            got = mp.key_device_mask(keys[j] & ((1 << 64) - 1), W8, k)
+            assert got == mo.device_mask(d["devices"]), (topo_name, policy, j)
+
+
+def test_c3_sampled_vs_oracle():
+    """C3: cubemesh16, {ring,tree,full} x k in {4,6,8}, random busy; sampled
+    queries in the single-query launch configuration vs the C oracle."""
+    o = mo.builtin("cubemesh16")
+    t = mp.Topology("cubemesh16")
+    qs = W.c3_queries(per_case=1000)
+    rng = random.Random(3)
+    picked = 0
+    for i in rng.sample(range(len(qs)), 400):
+        q = qs[i]
+        nf = 16 - bin(q["busy"]).count("1")
+        if q["k"] <= nf and math.perm(nf, q["k"]) > 3e6:  # keep the CPU oracle within seconds
+            continue
+        for raw in (True, False):
+            same(oracle(o, q["busy"], q["shape"], q["k"], q["selector"], q["sensitive"], use_c=True),
+                 gpu(t, q["busy"], q["shape"], q["k"], q["selector"], q["sensitive"], raw), (i, q, raw))
+        picked += 1
+        if picked >= 40:
+            break
+    assert picked >= 20
