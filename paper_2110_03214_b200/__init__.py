@@ -155,9 +155,12 @@ class Topology:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.mapa_free_topology(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib.mapa_free_topology(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     @property
     def handle(self):
@@ -212,9 +215,12 @@ class Pattern:
         return cls(k, shape=shape)
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.mapa_free_pattern(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                _lib.mapa_free_pattern(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     @property
     def handle(self):

@@ -32,15 +32,18 @@ struct DevTopo {
 
 // Device view of a compiled pattern.  Vertex order = pattern index order
 // (the order of the mapping tuple whose lex-min the canonical mode keeps).
-struct DevPattern {
-    uint8_t k, m, clique, eb;   // eb = C(k,2)
+// The three byte arrays are read as one 64-bit word each: keep them 8-aligned.
+struct alignas(8) DevPattern {
     uint8_t fwd_back[8];        // fwd_back[j] bit u (u > j): pattern edge (j,u)
     uint8_t fwd_src[8];         // fwd_src[j] bit u (u > j): lex-leader f(j) < f(u)
     uint8_t dback[8];           // |{i < j : (i,j) in E}|
-    uint8_t edge[28];           // a | b << 4, a < b
+    uint8_t k, m, clique, eb;   // eb = C(k,2)
     uint16_t lut_off;           // offset of the Eq. 2 rank table in the LUT pool
     uint16_t aut;               // |Aut(P)|
+    uint8_t edge[28];           // a | b << 4, a < b
+    uint8_t pad[4];
 };
+static_assert(sizeof(DevPattern) == 64, "DevPattern layout");
 
 template <int MAXP, int LUTCAP>
 struct Tables {
