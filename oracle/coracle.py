@@ -42,14 +42,15 @@ def lib():
         _lib.oracle_allocate.argtypes = [
             ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_uint32, ctypes.c_int,
             ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_int, ctypes.c_int,
-            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(OracleResult)]
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(OracleResult)]
         _lib.oracle_eq2.restype = ctypes.c_double
         _lib.oracle_eq2.argtypes = [ctypes.c_int] * 3
     return _lib
 
 
 def allocate(topo: mo.Topology, busy: int, k: int, pedges, selector: int, sensitive: bool,
-             nthreads: int | None = None, a_lo: int = -1, a_hi: int = -1) -> dict:
+             nthreads: int | None = None, a_lo: int = -1, a_hi: int = -1, b_lo: int = -1,
+             b_hi: int = -1) -> dict:
     """Same result dict as mapa_oracle.allocate (without the exact Fraction)."""
     n = topo.n
     w = (ctypes.c_int32 * (n * n))(*[topo.w[u][v] for u in range(n) for v in range(n)])
@@ -58,7 +59,7 @@ def allocate(topo: mo.Topology, busy: int, k: int, pedges, selector: int, sensit
     r = OracleResult()
     nt = nthreads or os.cpu_count() or 1
     rc = lib().oracle_allocate(n, w, busy, k, len(pedges), pe, selector, int(bool(sensitive)),
-                               nt, a_lo, a_hi, ctypes.byref(r))
+                               nt, a_lo, a_hi, b_lo, b_hi, ctypes.byref(r))
     if rc != 0:
         raise ValueError(f"oracle_allocate rc={rc}")
     if r.status == 1:

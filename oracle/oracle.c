@@ -165,20 +165,25 @@ static void process_subset(const ctx_t *c, const int *S, entry_t *ent, unit_t *u
     }
 }
 
-static void process_unit(const ctx_t *c, int a, entry_t *ent, unit_t *u) {
+/* One work unit = every k-subset whose first two elements are F[a], F[b]
+ * (b < 0 when k == 1: the single subset {F[a]}), in lex order. */
+static void process_unit(const ctx_t *c, int a, int b, entry_t *ent, unit_t *u) {
     memset(u, 0, sizeof(*u));
     int k = c->k, nf = c->nf;
     int idx[8];
     int S[8];
     idx[0] = a;
-    for (int i = 1; i < k; i++) idx[i] = a + i;
-    if (k > 0 && idx[k - 1] >= nf) return;
+    if (k > 1) {
+        idx[1] = b;
+        for (int i = 2; i < k; i++) idx[i] = b + i - 1;
+    }
+    if (idx[k - 1] >= nf) return;
     for (;;) {
         for (int i = 0; i < k; i++) S[i] = c->F[idx[i]];
         process_subset(c, S, ent, u);
-        int i = k - 1;                              /* next combination, idx[0] fixed */
-        while (i >= 1 && idx[i] == nf - k + i) i--;
-        if (i < 1) break;
+        int i = k - 1;                              /* next combination, idx[0..1] fixed */
+        while (i >= 2 && idx[i] == nf - k + i) i--;
+        if (i < 2) break;
         idx[i]++;
         for (int j = i + 1; j < k; j++) idx[j] = idx[j - 1] + 1;
     }
@@ -187,7 +192,8 @@ static void process_unit(const ctx_t *c, int a, entry_t *ent, unit_t *u) {
 typedef struct {
     const ctx_t *c;
     unit_t *units;
-    int lo, hi;
+    int (*ab)[2];
+    int nunits;
     int next;
     pthread_mutex_t mu;
 } pool_t;
@@ -199,10 +205,10 @@ static void *worker(void *arg) {
     entry_t *ent = (entry_t *)malloc(sizeof(entry_t) * fact(p->c->k));
     for (;;) {
         pthread_mutex_lock(&p->mu);
-        int a = p->next++;
+        int i = p->next++;
         pthread_mutex_unlock(&p->mu);
-        if (a >= p->hi) break;
-        process_unit(p->c, a, ent, &p->units[a - p->lo]);
+        if (i >= p->nunits) break;
+        process_unit(p->c, p->ab[i][0], p->ab[i][1], ent, &p->units[i]);
     }
     free(ent);
     return NULL;
@@ -210,11 +216,13 @@ static void *worker(void *arg) {
 
 /* Brute-force allocation.  w: n*n weights (GB/s, diagonal ignored); busy: bit d
  * busy; pe: 2m pattern edges (0-based); selector 0 GREEDY, 1 PRESERVE, 2 BASELINE.
- * a_lo/a_hi restrict S[0] to F[a_lo..a_hi) (bounded samples); a_hi < 0 = all.
- * Returns 0, or <0 on invalid arguments. */
+ * a_lo/a_hi restrict S[0] to F[a_lo..a_hi) and b_lo/b_hi restrict S[1] to
+ * F[b_lo..b_hi) (bounded samples); a negative bound = unrestricted.  Work units
+ * are the (S[0], S[1]) pairs, combined in lex order, so the result does not
+ * depend on the thread count.  Returns 0, or <0 on invalid arguments. */
 int oracle_allocate(int n, const int32_t *w, uint32_t busy, int k, int m, const int32_t *pe,
-                    int selector, int sensitive, int nthreads, int a_lo, int a_hi,
-                    oracle_result *out) {
+                    int selector, int sensitive, int nthreads, int a_lo, int a_hi, int b_lo,
+                    int b_hi, oracle_result *out) {
     memset(out, 0, sizeof(*out));
     if (n < 1 || n > 32 || k < 1 || k > 8 || m < 0 || m > 28) return -1;
     ctx_t c;
@@ -229,9 +237,20 @@ int oracle_allocate(int n, const int32_t *w, uint32_t busy, int k, int m, const 
     int hi = a_hi < 0 ? c.nf - k + 1 : a_hi;
     if (hi > c.nf - k + 1) hi = c.nf - k + 1;
     if (lo >= hi) { out->status = 1; return 0; }
+    int bmax = c.nf - k + 2;
+    int blo = b_lo < 0 ? 0 : b_lo, bhi = b_hi < 0 ? bmax : (b_hi < bmax ? b_hi : bmax);
     pool_t p;
-    p.c = &c; p.lo = lo; p.hi = hi; p.next = lo;
-    p.units = (unit_t *)calloc(hi - lo, sizeof(unit_t));
+    p.c = &c;
+    p.ab = (int (*)[2])malloc(sizeof(int[2]) * (size_t)(hi - lo) * (k > 1 ? c.nf : 1));
+    p.nunits = 0;
+    for (int a = lo; a < hi; a++) {
+        if (k == 1) { p.ab[p.nunits][0] = a; p.ab[p.nunits][1] = -1; p.nunits++; continue; }
+        for (int b = (a + 1 > blo ? a + 1 : blo); b < bhi; b++) {
+            p.ab[p.nunits][0] = a; p.ab[p.nunits][1] = b; p.nunits++;
+        }
+    }
+    p.next = 0;
+    p.units = (unit_t *)calloc(p.nunits > 0 ? p.nunits : 1, sizeof(unit_t));
     pthread_mutex_init(&p.mu, NULL);
     if (nthreads < 1) nthreads = 1;
     if (nthreads > 256) nthreads = 256;
@@ -242,16 +261,18 @@ int oracle_allocate(int n, const int32_t *w, uint32_t busy, int k, int m, const 
     unit_t best;
     memset(&best, 0, sizeof(best));
     uint64_t raw = 0, distinct = 0;
-    for (int a = lo; a < hi; a++) {                 /* combine in lex order, strict '>' */
-        unit_t *u = &p.units[a - lo];
+    for (int i = 0; i < p.nunits; i++) {            /* combine in lex order, strict '>' */
+        unit_t *u = &p.units[i];
         raw += u->raw;
         distinct += u->distinct;
         if (u->found && (!best.found || u->score > best.score)) best = *u;
     }
     free(p.units);
+    free(p.ab);
     out->raw = raw;
     out->distinct = distinct;
-    out->status = 0;
+    out->status = best.found ? 0 : 1;
+    if (!best.found) return 0;
     out->score = best.score;
     out->device_mask = 0;
     for (int i = 0; i < k; i++) {

@@ -4,28 +4,38 @@
 //   S3 occupancy prep   F = ~busy; inc_F(v), T_F (Eq. 3 support)
 //   S4 enumeration      DFS over injective maps f: V(P) -> F (§3.3 P:496-501;
 //                       G complete, so every injective map embeds).
-//                       Lanes = candidate devices of the LAST pattern vertex;
-//                       groups of W lanes (W = 8/16/32 = padded N) each run an
-//                       independent prefix, so small topologies fill the warp.
+//                       Lanes = devices of the LAST pattern vertex k-1; the
+//                       inner loop walks the devices v of vertex k-2.  Groups
+//                       of W lanes (W = 8/16/32 = padded N) each run their own
+//                       prefix, so small topologies still fill the warp.
 //                       Canonical mode adds lex-leader lower bounds (one leaf
 //                       per Aut(P)-orbit = SPEC dedup S:209).
-//   S5 scoring          integer only.  For a device set X not containing v,
-//                       sum_{u in X} w(u,v) = 12|X| + 38 popc(c0&X)
-//                       + 13 popc(c1&X) + 8 popc(c2&X) with v's class masks.
-//                         Eq. 1 AggBW: X = devices of the back-
-//                         neighbours of the vertex being placed.
+//   S5 scoring          integer only.  With v's class masks c0..c2 and any
+//                       device set X not containing v:
+//                         sum_{u in X} w(u,v) = 12|X| + 38 popc(c0&X)
+//                                               + 13 popc(c1&X) + 8 popc(c2&X)
+//                       Outer DFS levels use that (popc, lane-uniform); the
+//                       inner loop uses no popc at all: per prefix the lanes
+//                       precompute in parallel (a) the score increment of
+//                       placing vertex k-2 on their device (broadcast through
+//                       a 32-entry smem list) and (b) their own leaf partial
+//                       over vertices 0..k-3; each inner iteration then adds
+//                       one list entry and one 32x32 weight-table byte.
+//                         Eq. 1 AggBW: X = back-neighbour devices.
 //                         Eq. 3 PreservedBW: T_F - sum inc_F(S)
-//                         + inside(S), X = all previously placed devices.
-//                         Eq. 2: census x = popc(c0&X), y =
-//                         popc((c1|c2)&X) accumulated, score = dense rank of
-//                         Eq. 2 among censuses with x+y+z = m (host table).
-//   S6 argmax           per-lane running max of a packed 64-bit key
-//                       (score | brev(S) | edge code) computed lazily (only
-//                       when score >= lane best), warp shuffle max, block max,
-//                       atomicMax in HBM.  Max is order independent, so the
-//                       result is identical for every grid size / rank count.
-// There is no dense contraction anywhere, so no tensor cores (tcgen05) are
-// used: the bound is integer issue.
+//                         + inside(S), X = all placed devices.
+//                         Eq. 2: census (x, y) accumulated as a
+//                         table index x*(m+1)+y; score = dense rank of Eq. 2
+//                         among the censuses with x+y+z = m (host table).
+//   S6 argmax           per-lane running max of a packed 64-bit key (score |
+//                       brev(S) | edge code), built out of line only when the
+//                       score reaches the lane's best; warp shuffle max, block
+//                       max, atomicMax in HBM.  Max is order independent, so
+//                       the result is identical for every grid / rank count.
+// Work items: the prefixes of depth D (mixed radix over the free devices),
+// handed out as contiguous chunks; a chunk is walked as a DFS range, so only
+// the first item of a run is decoded.  No dense contraction exists, so no
+// tensor cores are used; the bound is integer issue.
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -44,14 +54,20 @@ struct Ctx {
     uint32_t F;
     int nF;
     int b;                          // lane's device id (lane % W)
+    uint32_t gmask;                 // lanes of this lane's group
     uint32_t cm0, cm1, cm2, cm12;   // lane's class masks
-    int leafC;                      // leaf constant: w12*n12(K-1) + lane constant
-    int w0, w1, w2, w12;
-    int useU;                       // 1: X = all placed devices (Eq. 3), 0: back neighbours (Eq. 1/2)
+    int incb;                       // inc_F(b)
+    int laneC;                      // lane constant of the score (Eq. 3: -inc_F(b))
+    int leafC;                      // k = 1 leaf constant
+    int w0, w1, w2, w12;            // 38, 13, 8, 12 (0 for Baseline)
+    int useU;                       // 1: X = all placed devices (Eq. 3), 0: back neighbours
     int acc0;                       // accumulator at the root (T_F for Eq. 3)
     const uint4 *cm;                // class masks of every device (smem)
     const int *inc;                 // inc_F(v) (smem)
     const uint16_t *lut;            // Eq. 2 rank table (smem)
+    const uint8_t *wt;              // w(v, b) at [v*32 + b] (smem)
+    const uint8_t *ct;              // census bits of (v, b): 1 = double, 2 = single (smem)
+    int2 *list;                     // this group's inner-loop candidate list (smem, W entries)
     int mp1;                        // m + 1
     uint64_t fb, fs, db;            // bytes: fwd_back, fwd_src, dback
     int clique, eb, m;
@@ -94,10 +110,9 @@ __device__ __forceinline__ uint32_t nth_set(uint32_t m, uint32_t n) {
 // out of line; arguments by value so the DFS state stays in registers.
 //   fpack: f(0..K-2) one byte each; b: device of vertex K-1.
 template <int W, int K>
-__device__ __noinline__ unsigned long long make_key(uint32_t U, unsigned long long fpack, uint32_t b,
+__device__ __noinline__ unsigned long long make_key(uint32_t S, unsigned long long fpack, uint32_t b,
                                                     uint32_t s, int clique, int eb, int m,
                                                     const uint8_t *edge) {
-    const uint32_t S = U | (1u << b);
     const uint32_t sb = __brev(S) >> (32 - W);
     uint32_t ecode;
     if (clique) {
@@ -121,6 +136,16 @@ __device__ __noinline__ unsigned long long make_key(uint32_t U, unsigned long lo
         }
     }
     return ((unsigned long long)s << (W + eb)) | ((unsigned long long)sb << eb) | ecode;
+}
+
+template <int W, int K>
+__device__ __forceinline__ void consider(const Ctx &c, Best &bst, uint32_t S, unsigned long long fpack,
+                                         uint32_t s) {
+    const unsigned long long key = make_key<W, K>(S, fpack, (uint32_t)c.b, s, c.clique, c.eb, c.m, c.edge);
+    if (key > bst.key) {
+        bst.key = key;
+        bst.bs = s;
+    }
 }
 
 template <int K, int SEL, int J>
@@ -152,63 +177,110 @@ __device__ __forceinline__ St<K> push(const Ctx &c, const St<K> &st, uint32_t v)
     return s;
 }
 
-template <int W, int K, int SEL>
-__device__ __forceinline__ void leaf(const Ctx &c, const St<K> &st, Best &bst) {
-    const uint32_t lc = c.F & ~st.U & st.al[K - 1];
-    const bool act = (lc >> c.b) & 1u;
-    int s;
-    if constexpr (SEL == SEL_LIN) {
-        const uint32_t X = c.useU ? st.U : st.bm[K - 1];
-        s = st.acc + c.leafC + c.w0 * __popc(c.cm0 & X) + c.w1 * __popc(c.cm1 & X) +
-            c.w2 * __popc(c.cm2 & X);
-    } else {
-        const uint32_t X = st.bm[K - 1];
-        const int x = st.acc + __popc(c.cm0 & X);
-        const int y = st.acc2 + __popc(c.cm12 & X);
-        s = act ? (int)c.lut[x * c.mp1 + y] : 0;
-    }
-    bst.cnt += act ? 1u : 0u;
-    if (act && (uint32_t)s >= bst.bs) {
-        unsigned long long fpack = 0;
+template <int K>
+__device__ __forceinline__ unsigned long long pack_f(const St<K> &st) {
+    unsigned long long fpack = 0;
 #pragma unroll
-        for (int i = 0; i < K - 1; ++i) fpack |= (unsigned long long)st.f[i] << (8 * i);
-        const unsigned long long key =
-            make_key<W, K>(st.U, fpack, (uint32_t)c.b, (uint32_t)s, c.clique, c.eb, c.m, c.edge);
-        if (key > bst.key) {
-            bst.key = key;
-            bst.bs = (uint32_t)s;
+    for (int i = 0; i < K - 1; ++i) fpack |= (unsigned long long)st.f[i] << (8 * i);
+    return fpack;
+}
+
+// k = 1: a single level, the lanes are the devices of vertex 0.
+template <int W, int SEL>
+__device__ __forceinline__ void leaf_k1(const Ctx &c, Best &bst) {
+    const bool act = (c.F >> c.b) & 1u;
+    const int s = (SEL == SEL_LIN) ? c.acc0 + c.leafC : (int)c.lut[0];
+    bst.cnt += act ? 1u : 0u;
+    if (act && (uint32_t)s >= bst.bs) consider<W, 1>(c, bst, 1u << c.b, 0ull, (uint32_t)s);
+}
+
+// The two innermost levels: vertex K-2 walks the devices of `cand`
+// (uniform loop), vertex K-1 sits on the lanes.  Vertices 0..K-3 are placed.
+template <int W, int K, int SEL>
+__device__ __forceinline__ void inner(const Ctx &c, const St<K> &st, uint32_t cand, Best &bst) {
+    constexpr int J = K - 2;
+    const uint32_t b = (uint32_t)c.b;
+    const uint32_t fbJ = (uint32_t)(c.fb >> (8 * J)) & 0xFFu;
+    const uint32_t fsJ = (uint32_t)(c.fs >> (8 * J)) & 0xFFu;
+    const bool eK = (fbJ >> (K - 1)) & 1u;   // pattern edge (K-2, K-1)
+    const bool dep = (fsJ >> (K - 1)) & 1u;  // lex-leader f(K-2) < f(K-1)
+    int t2, lp, A;
+    bool eW;
+    const uint8_t *col;
+    if constexpr (SEL == SEL_LIN) {
+        const uint32_t X2 = c.useU ? st.U : st.bm[J];
+        const uint32_t X1 = c.useU ? st.U : st.bm[K - 1];
+        const int n2 = c.useU ? J : (int)((c.db >> (8 * J)) & 0xFFu);
+        // (a) increment of placing vertex K-2 on this lane's device
+        t2 = c.w12 * n2 - (c.useU ? c.incb : 0) + c.w0 * __popc(c.cm0 & X2) + c.w1 * __popc(c.cm1 & X2) +
+             c.w2 * __popc(c.cm2 & X2);
+        // (b) this lane's leaf partial over vertices 0..K-3
+        lp = c.laneC + c.w12 * __popc(X1) + c.w0 * __popc(c.cm0 & X1) + c.w1 * __popc(c.cm1 & X1) +
+             c.w2 * __popc(c.cm2 & X1);
+        A = st.acc;
+        eW = c.w12 != 0 && (c.useU || eK);
+        col = c.wt + b;
+    } else {
+        const uint32_t X2 = st.bm[J], X1 = st.bm[K - 1];
+        t2 = __popc(c.cm0 & X2) * c.mp1 + __popc(c.cm12 & X2);
+        lp = __popc(c.cm0 & X1) * c.mp1 + __popc(c.cm12 & X1);
+        A = st.acc * c.mp1 + st.acc2;
+        eW = eK;
+        col = c.ct + b;
+    }
+    // Candidate list of this group, in increasing device order: entry i =
+    // (i-th device v of cand, increment of placing vertex K-2 on v).
+    const uint32_t n = (uint32_t)__popc(cand);
+    __syncwarp(c.gmask);  // previous readers of the list are done
+    if ((cand >> b) & 1u) c.list[__popc(cand & ((1u << b) - 1u))] = make_int2((int)b, t2);
+    __syncwarp(c.gmask);
+    // act(v) = bit v of M: vertex K-1 may sit on b once K-2 sits on v
+    const uint32_t lowb = (1u << b) - 1u;
+    const uint32_t M = (((c.F & ~st.U & st.al[K - 1]) >> b) & 1u) ? (dep ? lowb : ~(1u << b)) : 0u;
+    bst.cnt += (uint32_t)__popc(M & cand);
+    // Within this call the lane's leaves differ only in v, and for equal
+    // scores the smaller v is the lex-smaller device set (larger key): keep
+    // (max score, min v) branch-free and build the full key once afterwards.
+    const int Alp = A + lp;
+    int best = -1;
+    uint32_t bestv = 0;
+    for (int i = (int)n - 1; i >= 0; --i) {
+        const int2 e = c.list[i];
+        const uint32_t v = (uint32_t)e.x;
+        int s;
+        if constexpr (SEL == SEL_LIN) {
+            s = Alp + e.y + (eW ? (int)col[v * 32] : 0);
+        } else {
+            int idx = Alp + e.y;
+            if (eW) {
+                const uint32_t cb = col[v * 32];
+                idx += (int)(cb & 1u) * c.mp1 + (int)(cb >> 1);
+            }
+            s = (int)c.lut[idx];
         }
+        const bool take = ((M >> v) & 1u) && s >= best;
+        best = take ? s : best;
+        bestv = take ? v : bestv;
+    }
+    if (best >= 0 && (uint32_t)best >= bst.bs) {
+        unsigned long long fpack = pack_f<K>(st);
+        fpack |= (unsigned long long)bestv << (8 * J);
+        consider<W, K>(c, bst, st.U | (1u << bestv) | (1u << b), fpack, (uint32_t)best);
     }
 }
 
 template <int W, int K, int SEL, int J>
 __device__ __forceinline__ void level(const Ctx &c, const St<K> &st, Best &bst) {
-    if constexpr (J == K - 1) {
-        leaf<W, K, SEL>(c, st, bst);
+    if constexpr (K == 1) {
+        leaf_k1<W, SEL>(c, bst);
+    } else if constexpr (J == K - 2) {
+        inner<W, K, SEL>(c, st, c.F & ~st.U & st.al[J], bst);
     } else {
         uint32_t cand = c.F & ~st.U & st.al[J];
         while (cand) {
             const uint32_t v = __ffs(cand) - 1;
             cand &= cand - 1u;
             level<W, K, SEL, J + 1>(c, push<K, SEL, J>(c, st, v), bst);
-        }
-    }
-}
-
-// Decode levels [0, D) from the item digits, then run the DFS from level D.
-// Levels < DMIN are always decoded, levels >= DMAX never.
-template <int W, int K, int SEL, int J, int DMIN, int DMAX>
-__device__ __forceinline__ void descend(const Ctx &c, const St<K> &st, const uint32_t (&dg)[kMaxDecode],
-                                        int D, Best &bst) {
-    if constexpr (J >= DMAX || J >= K - 1) {
-        level<W, K, SEL, J>(c, st, bst);
-    } else {
-        if (J < DMIN || J < D) {
-            const uint32_t v = nth_set(c.F & ~st.U, dg[J]);
-            if (!((st.al[J] >> v) & 1u)) return;  // prefix violates a lex-leader bound
-            descend<W, K, SEL, J + 1, DMIN, DMAX>(c, push<K, SEL, J>(c, st, v), dg, D, bst);
-        } else {
-            level<W, K, SEL, J>(c, st, bst);
         }
     }
 }
@@ -252,18 +324,85 @@ __device__ __forceinline__ uint32_t perm_count(int n, int d) {
     return p;
 }
 
+// Walk up to maxn consecutive items starting at the item whose digits are dg.
+// Levels < D-1 are decoded from the digits; level D-1 iterates its (raw-order)
+// candidates from digit dg[D-1] on.  Returns the number of items consumed
+// (>= 1); a prefix that violates a lex-leader bound skips its whole subtree.
+template <int W, int K, int SEL, int J, int DMAX>
+__device__ __forceinline__ uint32_t descend_range(const Ctx &c, const St<K> &st, const uint32_t (&dg)[kMaxDecode],
+                                                  int D, uint32_t maxn, Best &bst) {
+    if constexpr (J >= DMAX || J > K - 2) {
+        return maxn;  // unreachable: D <= DMAX <= K-1
+    } else {
+        if (J < D - 1) {
+            const uint32_t v = nth_set(c.F & ~st.U, dg[J]);
+            if (!((st.al[J] >> v) & 1u)) {
+                uint32_t prod = 1, off = 0;
+#pragma unroll
+                for (int l = kMaxDecode - 1; l > J; --l) {
+                    if (l < D) {
+                        off += dg[l] * prod;
+                        prod *= (uint32_t)(c.nF - l);
+                    }
+                }
+                return min(maxn, prod - off);
+            }
+            return descend_range<W, K, SEL, J + 1, DMAX>(c, push<K, SEL, J>(c, st, v), dg, D, maxn, bst);
+        } else {
+            uint32_t cand = c.F & ~st.U;
+            const uint32_t p = nth_set(cand, dg[J]);
+            cand &= ~((1u << p) - 1u);  // raw candidates from the current item on
+            uint32_t n = (uint32_t)__popc(cand);
+            if (maxn < n) {
+                cand &= (1u << nth_set(cand, maxn)) - 1u;
+                n = maxn;
+            }
+            cand &= st.al[J];
+            if constexpr (J == K - 2) {
+                inner<W, K, SEL>(c, st, cand, bst);
+            } else {
+                while (cand) {
+                    const uint32_t v = __ffs(cand) - 1;
+                    cand &= cand - 1u;
+                    level<W, K, SEL, J + 1>(c, push<K, SEL, J>(c, st, v), bst);
+                }
+            }
+            return n;
+        }
+    }
+}
+
+// Items [lo, hi) of depth D (D = 0 only for K = 1).
+template <int W, int K, int SEL, int DMAX>
+__device__ __forceinline__ void run_range(const Ctx &c, uint32_t lo, uint32_t hi, int D, const uint32_t *magic,
+                                          Best &bst) {
+    if constexpr (K == 1) {
+        if (lo == 0 && hi > 0) leaf_k1<W, SEL>(c, bst);
+    } else {
+        uint32_t i = lo;
+        while (i < hi) {
+            uint32_t dg[kMaxDecode];
+            if (!digits(i, c.nF, D, magic, dg)) break;
+            i += descend_range<W, K, SEL, 0, DMAX>(c, root<K>(c), dg, D, hi - i, bst);
+        }
+    }
+}
+
 // Per-query context.  Must be called by the whole warp (uses shuffles).
-// inc: per-warp (or per-CTA) smem table, written by lanes < W of group 0.
+// s_inc: per-warp (or per-CTA) smem table of inc_F, written by group 0.
 template <int W>
 __device__ __forceinline__ Ctx make_ctx(const DevTopo &topo, const uint4 *s_cm, int *s_inc,
-                                        const uint16_t *s_lut, const DevPattern &P, uint32_t busy,
-                                        int selector, int sensitive) {
+                                        const uint16_t *s_lut, const uint8_t *s_wt, const uint8_t *s_ct,
+                                        int2 *s_list, const DevPattern &P, uint32_t busy, int selector,
+                                        int sensitive) {
     const int lane = threadIdx.x & 31;
     Ctx c;
     const uint32_t nmask = topo.n >= 32 ? kFull : ((1u << topo.n) - 1u);
     c.F = ~busy & nmask;
     c.nF = __popc(c.F);
     c.b = lane & (W - 1);
+    const int g = lane / W;
+    c.gmask = W == 32 ? kFull : (((1u << W) - 1u) << (g * W));
     const uint4 mine = s_cm[c.b];
     c.cm0 = mine.x;
     c.cm1 = mine.y;
@@ -275,6 +414,7 @@ __device__ __forceinline__ Ctx make_ctx(const DevTopo &topo, const uint4 *s_cm, 
                8 * __popc(mine.z & c.F);
     if (c.b >= topo.n) incb = 0;
     if (lane < W) s_inc[c.b] = incb;
+    c.incb = incb;
     // T_F = 1/2 sum_{v in F} inc_F(v)  (reduce within the W-lane group)
     int t = inFb ? incb : 0;
 #pragma unroll
@@ -292,7 +432,10 @@ __device__ __forceinline__ Ctx make_ctx(const DevTopo &topo, const uint4 *s_cm, 
     c.cm = s_cm;
     c.inc = s_inc;
     c.lut = s_lut;
-    int laneC = 0;
+    c.wt = s_wt;
+    c.ct = s_ct;
+    c.list = s_list + g * W;
+    c.laneC = 0;
     if (selector == MAPA_SEL_BASELINE) {
         c.w0 = c.w1 = c.w2 = c.w12 = 0;
         c.useU = 0;
@@ -301,24 +444,16 @@ __device__ __forceinline__ Ctx make_ctx(const DevTopo &topo, const uint4 *s_cm, 
         c.w0 = 38; c.w1 = 13; c.w2 = 8; c.w12 = 12;
         c.useU = 1;
         c.acc0 = TF;
-        laneC = -incb;
+        c.laneC = -incb;
     } else {  // Eq. 1 (or Eq. 2 census for the sensitive kernel)
         c.w0 = 38; c.w1 = 13; c.w2 = 8; c.w12 = 12;
         c.useU = 0;
         c.acc0 = 0;
     }
     const int n12 = c.useU ? (K - 1) : (int)P.dback[K - 1];
-    c.leafC = c.w12 * n12 + laneC;
+    c.leafC = c.w12 * n12 + c.laneC;
     __syncwarp();
     return c;
-}
-
-template <int W, int K, int SEL, int DMIN, int DMAX>
-__device__ __forceinline__ void run_item(const Ctx &c, uint32_t item, int D, const uint32_t *magic,
-                                         Best &bst) {
-    uint32_t dg[kMaxDecode];
-    if (!digits(item, c.nF, D, magic, dg)) return;
-    descend<W, K, SEL, 0, DMIN, DMAX>(c, root<K>(c), dg, D, bst);
 }
 
 __device__ __forceinline__ void warp_reduce(unsigned long long &key, unsigned long long &cnt) {
@@ -331,13 +466,31 @@ __device__ __forceinline__ void warp_reduce(unsigned long long &key, unsigned lo
     }
 }
 
-__device__ __forceinline__ void load_topo(const DevTopo &topo, uint4 *s_cm, uint32_t *s_magic) {
+// Topology tables in shared memory: class masks, weight and census tables,
+// magic reciprocals for the item decode.  Caller syncs.
+__device__ __forceinline__ void load_topo(const DevTopo &topo, uint4 *s_cm, uint32_t *s_magic, uint8_t *s_wt,
+                                          uint8_t *s_ct) {
     const int tid = threadIdx.x;
     if (tid < kMaxN) s_cm[tid] = make_uint4(topo.cm[tid][0], topo.cm[tid][1], topo.cm[tid][2], topo.cm[tid][3]);
     if (tid <= kMaxN) s_magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
+    for (int i = tid; i < kMaxN * kMaxN; i += blockDim.x) {
+        const int v = i >> 5, b = i & 31;
+        uint8_t w = 0, cb = 0;
+        if (v != b && v < topo.n && b < topo.n) {
+            if ((topo.cm[b][0] >> v) & 1u) { w = 50; cb = 1; }
+            else if ((topo.cm[b][1] >> v) & 1u) { w = 25; cb = 2; }
+            else if ((topo.cm[b][2] >> v) & 1u) { w = 20; cb = 2; }
+            else w = 12;
+        }
+        s_wt[i] = w;
+        s_ct[i] = cb;
+    }
 }
 
 // ---------------------------------------------------------------- single query
+// Items = prefixes of depth D, in chunks of `chunk` consecutive items; local
+// chunk q of rank r is global chunk q*world + r.  Group g of a warp walks the
+// g-th slice of the chunk.
 template <int W, int K, int SEL>
 __global__ void __launch_bounds__(kBlock, 2)
 esa_single(const __grid_constant__ SingleTables tb, int selector, int sensitive,
@@ -350,34 +503,38 @@ esa_single(const __grid_constant__ SingleTables tb, int selector, int sensitive,
     __shared__ int s_inc[kMaxN];
     __shared__ uint16_t s_lut[kLutCapSingle];
     __shared__ uint8_t s_edge[28];
+    __shared__ __align__(16) uint8_t s_wt[kMaxN * kMaxN];
+    __shared__ __align__(16) uint8_t s_ct[kMaxN * kMaxN];
+    __shared__ int2 s_list[kWarps][32];
     __shared__ unsigned long long s_key[kWarps], s_cnt[kWarps];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const DevPattern &P = tb.pat[0];
-    load_topo(tb.topo, s_cm, s_magic);
+    load_topo(tb.topo, s_cm, s_magic, s_wt, s_ct);
     const int lutn = (P.m + 1) * (P.m + 1);
     for (int i = tid; i < lutn; i += kBlock) s_lut[i] = tb.lut[P.lut_off + i];
     if (tid < 28) s_edge[tid] = P.edge[tid];
     const uint32_t busy = dq->busy;
     __syncthreads();
 
-    Ctx c = make_ctx<W>(tb.topo, s_cm, s_inc, s_lut, P, busy, selector, sensitive);
+    Ctx c = make_ctx<W>(tb.topo, s_cm, s_inc, s_lut, s_wt, s_ct, s_list[warp], P, busy, selector, sensitive);
     c.edge = s_edge;
     __syncthreads();  // s_inc written by every warp with identical values
 
     const uint32_t nItems = (K <= c.nF) ? perm_count(c.nF, D) : 0u;
-    const uint32_t nLocal = nItems > (uint32_t)rank ? (nItems - (uint32_t)rank + (uint32_t)world - 1u) / (uint32_t)world : 0u;
+    const uint32_t nChunks = (nItems + (uint32_t)chunk - 1u) / (uint32_t)chunk;
+    const uint32_t per = (uint32_t)chunk / G;  // host makes chunk a multiple of G
     Best bst{0ull, 0u, 0u};
     const uint32_t g = (uint32_t)(lane / W);
     for (;;) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&rec->ctr, (uint32_t)chunk);
-        base = __shfl_sync(kFull, base, 0);
-        if (base >= nLocal) break;
-        const uint32_t end = min(base + (uint32_t)chunk, nLocal);
-        for (uint32_t j = base + g; j < end; j += G) {
-            run_item<W, K, SEL, 0, DMAX>(c, j * (uint32_t)world + (uint32_t)rank, D, s_magic, bst);
-        }
+        uint32_t q = 0;
+        if (lane == 0) q = atomicAdd(&rec->ctr, 1u);
+        q = __shfl_sync(kFull, q, 0);
+        const uint32_t gq = q * (uint32_t)world + (uint32_t)rank;
+        if (gq >= nChunks) break;
+        const uint32_t lo = gq * (uint32_t)chunk + g * per;
+        const uint32_t hi = min(lo + per, nItems);
+        if (lo < hi) run_range<W, K, SEL, DMAX>(c, lo, hi, D, s_magic, bst);
         __syncwarp();
     }
     unsigned long long key = bst.key, cnt = bst.cnt;
@@ -399,14 +556,14 @@ esa_single(const __grid_constant__ SingleTables tb, int selector, int sensitive,
 }
 
 // ---------------------------------------------------------------- batches
-// W slots per query; slot j = the j-th free device as f(0) (D = 1); K = 1
-// queries use slot 0 only (D = 0).
+// W slots per query; slot j = the j-th free device as f(0) (items of depth 1);
+// K = 1 queries use slot 0 only (depth 0).
 template <int W, int K, int SEL>
 __device__ __forceinline__ void batch_item(const Ctx &c, uint32_t j, const uint32_t *magic, Best &bst) {
     if constexpr (K == 1) {
-        if (j == 0) run_item<W, 1, SEL, 0, 0>(c, 0u, 0, magic, bst);
+        if (j == 0) leaf_k1<W, SEL>(c, bst);
     } else {
-        if (j < (uint32_t)c.nF) run_item<W, K, SEL, 1, 1>(c, j, 1, magic, bst);
+        if (j < (uint32_t)c.nF) run_range<W, K, SEL, 1>(c, j, j + 1, 1, magic, bst);
     }
 }
 
@@ -437,9 +594,12 @@ esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query
     __shared__ uint32_t s_magic[kMaxN + 1];
     __shared__ int s_inc[kWarps][kMaxN];
     __shared__ uint16_t s_lut[kLutCapMulti];
+    __shared__ __align__(16) uint8_t s_wt[kMaxN * kMaxN];
+    __shared__ __align__(16) uint8_t s_ct[kMaxN * kMaxN];
+    __shared__ int2 s_list[kWarps][32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    load_topo(tb.topo, s_cm, s_magic);
+    load_topo(tb.topo, s_cm, s_magic, s_wt, s_ct);
     int lutn = 0;
     for (int p = 0; p < tb.npats; ++p) {
         const int e = tb.pat[p].lut_off + (tb.pat[p].m + 1) * (tb.pat[p].m + 1);
@@ -463,8 +623,8 @@ esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query
             continue;
         }
         const DevPattern &P = tb.pat[pid];
-        Ctx c = make_ctx<W>(tb.topo, s_cm, s_inc[warp], s_lut + P.lut_off, P, qu.busy, qu.selector,
-                            qu.sensitive);
+        Ctx c = make_ctx<W>(tb.topo, s_cm, s_inc[warp], s_lut + P.lut_off, s_wt, s_ct, s_list[warp], P, qu.busy,
+                            qu.selector, qu.sensitive);
         if (P.k > c.nF) continue;
         const uint32_t j = (uint32_t)(base % W) + g;
         Best bst{0ull, 0u, 0u};
@@ -483,10 +643,12 @@ esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query
 
 // ---------------------------------------------------------------- trace replay
 template <int W, int K, int SEL>
-__device__ __forceinline__ void trace_items(const Ctx &c, int D, uint32_t nItems, uint32_t gid,
-                                            uint32_t ngroups, const uint32_t *magic, Best &bst) {
+__device__ __forceinline__ void trace_items(const Ctx &c, int D, uint32_t nItems, uint32_t gid, uint32_t ngroups,
+                                            const uint32_t *magic, Best &bst) {
     constexpr int DMAX = (K - 1) < 2 ? (K - 1) : 2;
-    for (uint32_t it = gid; it < nItems; it += ngroups) run_item<W, K, SEL, 0, DMAX>(c, it, D, magic, bst);
+    const uint32_t per = (nItems + ngroups - 1u) / ngroups;
+    const uint32_t lo = gid * per, hi = min(lo + per, nItems);
+    if (lo < hi) run_range<W, K, SEL, DMAX>(c, lo, hi, D, magic, bst);
 }
 
 template <int W, int SEL>
@@ -505,6 +667,8 @@ __device__ __forceinline__ void trace_dispatch_k(int K, const Ctx &c, int D, uin
     }
 }
 
+// One CTA per trace; ALLOC / RELEASE ops in order; the busy mask lives in
+// shared memory (§3.6 state management), decisions go to HBM as keys.
 template <int W>
 __global__ void __launch_bounds__(kBlock, 1)
 esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op *__restrict__ ops, int njobs,
@@ -514,12 +678,15 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
     __shared__ uint32_t s_magic[kMaxN + 1];
     __shared__ int s_inc[kWarps][kMaxN];
     __shared__ uint16_t s_lut[kLutCapMulti];
-    __shared__ unsigned long long s_key[kWarps], s_cnt[kWarps];
+    __shared__ __align__(16) uint8_t s_wt[kMaxN * kMaxN];
+    __shared__ __align__(16) uint8_t s_ct[kMaxN * kMaxN];
+    __shared__ int2 s_list[kWarps][32];
+    __shared__ unsigned long long s_key[kWarps];
     __shared__ uint32_t s_busy;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int t = blockIdx.x;
-    load_topo(tb.topo, s_cm, s_magic);
+    load_topo(tb.topo, s_cm, s_magic, s_wt, s_ct);
     int lutn = 0;
     for (int p = 0; p < tb.npats; ++p) {
         const int e = tb.pat[p].lut_off + (tb.pat[p].m + 1) * (tb.pat[p].m + 1);
@@ -532,6 +699,7 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
     const mapa_query *jb = jobs + (long long)t * njobs;
     unsigned long long *ky = keys + (long long)t * njobs;
     const uint32_t gid = (uint32_t)(warp * G + lane / W);
+    const uint32_t wmask = W >= 32 ? kFull : ((1u << W) - 1u);
     for (int o = 0; o < nops; ++o) {
         const mapa_trace_op cur = op[o];
         const mapa_query qu = jb[cur.job];
@@ -540,8 +708,8 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
         const DevPattern &P = tb.pat[okp ? pid : 0];
         if (cur.op == 0) {
             const uint32_t busy = s_busy;
-            Ctx c = make_ctx<W>(tb.topo, s_cm, s_inc[warp], s_lut + P.lut_off, P, busy, qu.selector,
-                                qu.sensitive);
+            Ctx c = make_ctx<W>(tb.topo, s_cm, s_inc[warp], s_lut + P.lut_off, s_wt, s_ct, s_list[warp], P, busy,
+                                qu.selector, qu.sensitive);
             Best bst{0ull, 0u, 0u};
             if (okp && P.k <= c.nF) {
                 const int D = (P.k - 1) < 2 ? (P.k - 1) : 2;
@@ -559,16 +727,12 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
                 unsigned long long best = 0;
                 for (int w = 0; w < kWarps; ++w) best = s_key[w] > best ? s_key[w] : best;
                 ky[cur.job] = best;
-                if (best) {
-                    const uint32_t sb = (uint32_t)(best >> P.eb) & (W >= 32 ? kFull : ((1u << W) - 1u));
-                    s_busy = busy | (__brev(sb) >> (32 - W));
-                }
+                if (best) s_busy = busy | (__brev((uint32_t)(best >> P.eb) & wmask) >> (32 - W));
             }
         } else {
             if (tid == 0) {
                 const unsigned long long kk = ky[cur.job];
-                const uint32_t sb = (uint32_t)(kk >> P.eb) & (W >= 32 ? kFull : ((1u << W) - 1u));
-                s_busy &= ~(__brev(sb) >> (32 - W));
+                s_busy &= ~(__brev((uint32_t)(kk >> P.eb) & wmask) >> (32 - W));
             }
         }
         __syncthreads();

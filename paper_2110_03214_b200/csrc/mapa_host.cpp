@@ -345,13 +345,16 @@ Plan plan_single(const mapa_topology *t, const mapa_pattern *p, int sensk, int n
     while (d < dmax && perm_count(nF, d) < target) ++d;
     pl.depth = d;
     const uint64_t items = nF >= k ? perm_count(nF, d) : 0;
-    pl.nlocal = (items + world - 1) / world;
-    uint64_t chunk = pl.nlocal / (resident_warps * 16);
-    chunk = std::max<uint64_t>(chunk, 1);
+    pl.nlocal = items;
+    // ~16 counter grabs per resident warp; a grab = `chunk` consecutive items
+    // (a multiple of G: each W-lane group walks chunk/G of them as a DFS range)
+    uint64_t chunk = (items + resident_warps * 16 * world - 1) / (resident_warps * 16 * world);
+    chunk = std::max<uint64_t>(chunk, (uint64_t)G);
     chunk = ((chunk + G - 1) / G) * G;
     pl.chunk = (int)std::min<uint64_t>(chunk, 1u << 20);
-    const uint64_t warps_needed = (pl.nlocal + pl.chunk - 1) / pl.chunk;
-    const uint64_t blocks = std::max<uint64_t>(1, (warps_needed + 7) / 8);
+    const uint64_t nchunks = (items + pl.chunk - 1) / pl.chunk;
+    const uint64_t local = (nchunks + world - 1) / world;
+    const uint64_t blocks = std::max<uint64_t>(1, (local + 7) / 8);
     pl.grid = (int)std::min<uint64_t>(blocks, (uint64_t)sm * occ);
     return pl;
 }
