@@ -7,9 +7,10 @@ topology), 6-vertex all-to-all pattern (m = 15), all devices free, RAW mode:
 every one of the P(32,6) = 652,458,240 injective embeddings is scored.  One
 step = one allocation per selector (Greedy / Preserve-sensitive /
 Preserve-insensitive): 3 x 652,458,240 = 1,957,374,720 embeddings.  With N
-GPUs (torchrun, one process per GPU) each query is sharded by work item
-(item i -> rank i % N) and the per-rank 32-B records are combined with one
-all_gather over NCCL: the total work per step is fixed ("strong" scaling).
+GPUs (torchrun, one process per GPU) each query is sharded by work chunk
+(global chunk q*N + r -> rank r) and the per-rank 32-B records are combined
+with one all_gather over NCCL: the total work per step is fixed ("strong"
+scaling).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 

@@ -68,8 +68,13 @@ def combine_records(rec: torch.Tensor, group=None) -> Record:
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return records_from_tensor(rec)[0]
-    out = torch.empty((world, 4), dtype=torch.int64, device=rec.device)
-    dist.all_gather_into_tensor(out, rec.reshape(4), group=group)
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((world, 4), dtype=torch.int64, device=rec.device)
+        dist.all_gather_into_tensor(out, rec.reshape(4), group=group)
+    else:  # gloo (CPU tests of the multi-rank path)
+        parts = [torch.empty(4, dtype=torch.int64, device=rec.device) for _ in range(world)]
+        dist.all_gather(parts, rec.reshape(4), group=group)
+        out = torch.stack(parts)
     return reduce_records(records_from_tensor(out))
 
 
