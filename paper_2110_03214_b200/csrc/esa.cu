@@ -64,10 +64,11 @@ struct Ctx {
     int acc0;                       // accumulator at the root (T_F for Eq. 3)
     const uint4 *cm;                // class masks of every device (smem)
     const int *inc;                 // inc_F(v) (smem)
-    const uint16_t *lut;            // Eq. 2 rank table (smem)
-    const uint8_t *wt;              // w(v, b) at [v*32 + b] (smem)
-    const uint8_t *ct;              // census bits of (v, b): 1 = double, 2 = single (smem)
-    int2 *list;                     // this group's inner-loop candidate list (smem, W entries)
+    const uint16_t *lut;            // Eq. 2 table: (rank + 1) * 32 at [x * xs + y] (smem)
+    const int *tw, *tz, *twd, *tzd; // inner-loop tables [v*32 + b] (smem, see SmemTopo)
+    const int *tdl;                 // census index delta of edge (v, b) (smem)
+    int4 *list;                     // this group's inner-loop candidate list (smem, W entries)
+    int xs;                         // row stride of the Eq. 2 table (16 or 32)
     int mp1;                        // m + 1
     uint64_t fb, fs, db;            // bytes: fwd_back, fwd_src, dback
     int clique, eb, m;
@@ -88,6 +89,23 @@ struct Best {
     unsigned long long key;
     uint32_t bs;
     uint32_t cnt;
+};
+
+// Inner-loop leaves are ranked by one int: (score + 1) * 32 + (31 - v).  Its
+// max is the max score with ties to the smallest v.  Invalid leaves (vertex
+// K-1 on the device of K-2, or a lex-leader violation) get kNeg added.
+constexpr int kNeg = -(1 << 28);
+
+// Per-CTA topology tables (shared memory), all indexed [v * 32 + b]:
+//   tw  = 32 * w(v,b), kNeg when v == b or either is not a device
+//   tz  = 0,           kNeg likewise
+//   twd / tzd = the same with kNeg also where v >= b (canonical f(K-2) < f(K-1))
+//   tdl = census index delta of the edge (v,b): xs * [double] + [single]
+struct SmemTopo {
+    uint4 cm[kMaxN];
+    uint32_t magic[kMaxN + 1];
+    int tw[kMaxN * kMaxN], tz[kMaxN * kMaxN], twd[kMaxN * kMaxN], tzd[kMaxN * kMaxN];
+    int tdl[kMaxN * kMaxN];
 };
 
 __device__ __forceinline__ unsigned long long *u64p(uint64_t *p) {
@@ -189,7 +207,7 @@ __device__ __forceinline__ unsigned long long pack_f(const St<K> &st) {
 template <int W, int SEL>
 __device__ __forceinline__ void leaf_k1(const Ctx &c, Best &bst) {
     const bool act = (c.F >> c.b) & 1u;
-    const int s = (SEL == SEL_LIN) ? c.acc0 + c.leafC : (int)c.lut[0];
+    const int s = (SEL == SEL_LIN) ? c.acc0 + c.leafC : 0;  // m = 0: census (0,0,0) has rank 0
     bst.cnt += act ? 1u : 0u;
     if (act && (uint32_t)s >= bst.bs) consider<W, 1>(c, bst, 1u << c.b, 0ull, (uint32_t)s);
 }
@@ -204,68 +222,74 @@ __device__ __forceinline__ void inner(const Ctx &c, const St<K> &st, uint32_t ca
     const uint32_t fsJ = (uint32_t)(c.fs >> (8 * J)) & 0xFFu;
     const bool eK = (fbJ >> (K - 1)) & 1u;   // pattern edge (K-2, K-1)
     const bool dep = (fsJ >> (K - 1)) & 1u;  // lex-leader f(K-2) < f(K-1)
-    int t2, lp, A;
-    bool eW;
-    const uint8_t *col;
+    // (a) t2: increment of placing vertex K-2 on this lane's device;
+    // (b) lp: this lane's leaf partial over vertices 0..K-3.
+    int t2, base;
     if constexpr (SEL == SEL_LIN) {
         const uint32_t X2 = c.useU ? st.U : st.bm[J];
         const uint32_t X1 = c.useU ? st.U : st.bm[K - 1];
         const int n2 = c.useU ? J : (int)((c.db >> (8 * J)) & 0xFFu);
-        // (a) increment of placing vertex K-2 on this lane's device
         t2 = c.w12 * n2 - (c.useU ? c.incb : 0) + c.w0 * __popc(c.cm0 & X2) + c.w1 * __popc(c.cm1 & X2) +
              c.w2 * __popc(c.cm2 & X2);
-        // (b) this lane's leaf partial over vertices 0..K-3
-        lp = c.laneC + c.w12 * __popc(X1) + c.w0 * __popc(c.cm0 & X1) + c.w1 * __popc(c.cm1 & X1) +
-             c.w2 * __popc(c.cm2 & X1);
-        A = st.acc;
-        eW = c.w12 != 0 && (c.useU || eK);
-        col = c.wt + b;
+        const int lp = c.laneC + c.w12 * __popc(X1) + c.w0 * __popc(c.cm0 & X1) + c.w1 * __popc(c.cm1 & X1) +
+                       c.w2 * __popc(c.cm2 & X1);
+        base = (st.acc + lp + 1) * 32;
     } else {
         const uint32_t X2 = st.bm[J], X1 = st.bm[K - 1];
-        t2 = __popc(c.cm0 & X2) * c.mp1 + __popc(c.cm12 & X2);
-        lp = __popc(c.cm0 & X1) * c.mp1 + __popc(c.cm12 & X1);
-        A = st.acc * c.mp1 + st.acc2;
-        eW = eK;
-        col = c.ct + b;
+        t2 = __popc(c.cm0 & X2) * c.xs + __popc(c.cm12 & X2);
+        base = (st.acc + __popc(c.cm0 & X1)) * c.xs + st.acc2 + __popc(c.cm12 & X1);  // census index
     }
     // Candidate list of this group, in increasing device order: entry i =
-    // (i-th device v of cand, increment of placing vertex K-2 on v).
+    // (byte offset of table row v, LIN rank increment 32*t2 + 31 - v,
+    //  SENS census-index increment t2, 31 - v).
     const uint32_t n = (uint32_t)__popc(cand);
     __syncwarp(c.gmask);  // previous readers of the list are done
-    if ((cand >> b) & 1u) c.list[__popc(cand & ((1u << b) - 1u))] = make_int2((int)b, t2);
+    if ((cand >> b) & 1u)
+        c.list[__popc(cand & ((1u << b) - 1u))] = make_int4((int)b * 128, t2 * 32 + 31 - (int)b, t2, 31 - (int)b);
     __syncwarp(c.gmask);
-    // act(v) = bit v of M: vertex K-1 may sit on b once K-2 sits on v
-    const uint32_t lowb = (1u << b) - 1u;
-    const uint32_t M = (((c.F & ~st.U & st.al[K - 1]) >> b) & 1u) ? (dep ? lowb : ~(1u << b)) : 0u;
+    const bool laneok = ((c.F & ~st.U & st.al[K - 1]) >> b) & 1u;
+    // leaves counted: v in cand with v != b (and v < b if canonical-ordered)
+    const uint32_t M = laneok ? (dep ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
     bst.cnt += (uint32_t)__popc(M & cand);
     // Within this call the lane's leaves differ only in v, and for equal
-    // scores the smaller v is the lex-smaller device set (larger key): keep
-    // (max score, min v) branch-free and build the full key once afterwards.
-    const int Alp = A + lp;
-    int best = -1;
-    uint32_t bestv = 0;
-    for (int i = (int)n - 1; i >= 0; --i) {
-        const int2 e = c.list[i];
-        const uint32_t v = (uint32_t)e.x;
-        int s;
-        if constexpr (SEL == SEL_LIN) {
-            s = Alp + e.y + (eW ? (int)col[v * 32] : 0);
-        } else {
-            int idx = Alp + e.y;
-            if (eW) {
-                const uint32_t cb = col[v * 32];
-                idx += (int)(cb & 1u) * c.mp1 + (int)(cb >> 1);
-            }
-            s = (int)c.lut[idx];
+    // scores the smaller v is the lex-smaller device set (larger key): the
+    // packed rank (score+1)*32 + 31-v is maxed branch-free and the full key
+    // is built once afterwards.
+    int best = 0;
+    if constexpr (SEL == SEL_LIN) {
+        const bool eW = c.w12 != 0 && (c.useU || eK);
+        const char *tb = reinterpret_cast<const char *>((eW ? (dep ? c.twd : c.tw) : (dep ? c.tzd : c.tz)) + b);
+#pragma unroll 4
+        for (uint32_t i = 0; i < n; ++i) {
+            const int4 e = c.list[i];
+            best = max(best, base + e.y + *reinterpret_cast<const int *>(tb + e.x));
         }
-        const bool take = ((M >> v) & 1u) && s >= best;
-        best = take ? s : best;
-        bestv = take ? v : bestv;
+    } else {
+        const char *tz = reinterpret_cast<const char *>((dep ? c.tzd : c.tz) + b);
+        if (eK) {
+            const char *td = reinterpret_cast<const char *>(c.tdl + b);
+#pragma unroll 4
+            for (uint32_t i = 0; i < n; ++i) {
+                const int4 e = c.list[i];
+                const int idx = base + e.z + *reinterpret_cast<const int *>(td + e.x);
+                best = max(best, (int)c.lut[idx] + e.w + *reinterpret_cast<const int *>(tz + e.x));
+            }
+        } else {
+#pragma unroll 4
+            for (uint32_t i = 0; i < n; ++i) {
+                const int4 e = c.list[i];
+                best = max(best, (int)c.lut[base + e.z] + e.w + *reinterpret_cast<const int *>(tz + e.x));
+            }
+        }
     }
-    if (best >= 0 && (uint32_t)best >= bst.bs) {
-        unsigned long long fpack = pack_f<K>(st);
-        fpack |= (unsigned long long)bestv << (8 * J);
-        consider<W, K>(c, bst, st.U | (1u << bestv) | (1u << b), fpack, (uint32_t)best);
+    if (laneok && best >= 32) {
+        const uint32_t s = (uint32_t)(best >> 5) - 1u;
+        if (s >= bst.bs) {
+            const uint32_t bestv = 31u - (uint32_t)(best & 31);
+            unsigned long long fpack = pack_f<K>(st);
+            fpack |= (unsigned long long)bestv << (8 * J);
+            consider<W, K>(c, bst, st.U | (1u << bestv) | (1u << b), fpack, s);
+        }
     }
 }
 
@@ -391,10 +415,10 @@ __device__ __forceinline__ void run_range(const Ctx &c, uint32_t lo, uint32_t hi
 // Per-query context.  Must be called by the whole warp (uses shuffles).
 // s_inc: per-warp (or per-CTA) smem table of inc_F, written by group 0.
 template <int W>
-__device__ __forceinline__ Ctx make_ctx(const DevTopo &topo, const uint4 *s_cm, int *s_inc,
-                                        const uint16_t *s_lut, const uint8_t *s_wt, const uint8_t *s_ct,
-                                        int2 *s_list, const DevPattern &P, uint32_t busy, int selector,
-                                        int sensitive) {
+__device__ __forceinline__ Ctx make_ctx(const DevTopo &topo, const SmemTopo &sm, int *s_inc,
+                                        const uint16_t *s_lut, int xs, int4 *s_list, const DevPattern &P,
+                                        uint32_t busy, int selector, int sensitive) {
+    const uint4 *s_cm = sm.cm;
     const int lane = threadIdx.x & 31;
     Ctx c;
     const uint32_t nmask = topo.n >= 32 ? kFull : ((1u << topo.n) - 1u);
@@ -432,8 +456,12 @@ __device__ __forceinline__ Ctx make_ctx(const DevTopo &topo, const uint4 *s_cm, 
     c.cm = s_cm;
     c.inc = s_inc;
     c.lut = s_lut;
-    c.wt = s_wt;
-    c.ct = s_ct;
+    c.xs = xs;
+    c.tw = sm.tw;
+    c.tz = sm.tz;
+    c.twd = sm.twd;
+    c.tzd = sm.tzd;
+    c.tdl = sm.tdl;
     c.list = s_list + g * W;
     c.laneC = 0;
     if (selector == MAPA_SEL_BASELINE) {
@@ -466,24 +494,37 @@ __device__ __forceinline__ void warp_reduce(unsigned long long &key, unsigned lo
     }
 }
 
-// Topology tables in shared memory: class masks, weight and census tables,
-// magic reciprocals for the item decode.  Caller syncs.
-__device__ __forceinline__ void load_topo(const DevTopo &topo, uint4 *s_cm, uint32_t *s_magic, uint8_t *s_wt,
-                                          uint8_t *s_ct) {
+// Topology tables in shared memory (SmemTopo) for Eq. 2 table stride xs.
+// Caller syncs.
+__device__ __forceinline__ void load_topo(const DevTopo &topo, SmemTopo &sm, int xs) {
     const int tid = threadIdx.x;
-    if (tid < kMaxN) s_cm[tid] = make_uint4(topo.cm[tid][0], topo.cm[tid][1], topo.cm[tid][2], topo.cm[tid][3]);
-    if (tid <= kMaxN) s_magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
+    if (tid < kMaxN) sm.cm[tid] = make_uint4(topo.cm[tid][0], topo.cm[tid][1], topo.cm[tid][2], topo.cm[tid][3]);
+    if (tid <= kMaxN) sm.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
     for (int i = tid; i < kMaxN * kMaxN; i += blockDim.x) {
         const int v = i >> 5, b = i & 31;
-        uint8_t w = 0, cb = 0;
+        int w = kNeg, d = 0;
         if (v != b && v < topo.n && b < topo.n) {
-            if ((topo.cm[b][0] >> v) & 1u) { w = 50; cb = 1; }
-            else if ((topo.cm[b][1] >> v) & 1u) { w = 25; cb = 2; }
-            else if ((topo.cm[b][2] >> v) & 1u) { w = 20; cb = 2; }
+            if ((topo.cm[b][0] >> v) & 1u) { w = 50; d = xs; }
+            else if ((topo.cm[b][1] >> v) & 1u) { w = 25; d = 1; }
+            else if ((topo.cm[b][2] >> v) & 1u) { w = 20; d = 1; }
             else w = 12;
         }
-        s_wt[i] = w;
-        s_ct[i] = cb;
+        const int z = w == kNeg ? kNeg : 0;
+        const int wv = w == kNeg ? kNeg : 32 * w;
+        sm.tw[i] = wv;
+        sm.tz[i] = z;
+        sm.twd[i] = v >= b ? kNeg : wv;
+        sm.tzd[i] = v >= b ? kNeg : z;
+        sm.tdl[i] = d;
+    }
+}
+
+// Eq. 2 table for the kernels: out[x*xs + y] = (rank(x,y) + 1) * 32 from the
+// host's dense rank table rank[x*(m+1) + y] (x + y <= m); other entries 0.
+__device__ __forceinline__ void load_lut(const uint16_t *rank, int m, int xs, uint16_t *out) {
+    for (int i = threadIdx.x; i < xs * xs; i += blockDim.x) {
+        const int x = i / xs, y = i % xs;
+        out[i] = (x + y <= m) ? (uint16_t)((rank[x * (m + 1) + y] + 1) * 32) : (uint16_t)0;
     }
 }
 
@@ -498,26 +539,24 @@ esa_single(const __grid_constant__ SingleTables tb, int selector, int sensitive,
            int world, int chunk) {
     constexpr int G = 32 / W;
     constexpr int DMAX = (K - 1) < kMaxDecode ? (K - 1) : kMaxDecode;
-    __shared__ uint4 s_cm[kMaxN];
-    __shared__ uint32_t s_magic[kMaxN + 1];
+    __shared__ SmemTopo s_topo;
     __shared__ int s_inc[kMaxN];
     __shared__ uint16_t s_lut[kLutCapSingle];
     __shared__ uint8_t s_edge[28];
-    __shared__ __align__(16) uint8_t s_wt[kMaxN * kMaxN];
-    __shared__ __align__(16) uint8_t s_ct[kMaxN * kMaxN];
-    __shared__ int2 s_list[kWarps][32];
+    __shared__ int4 s_list[kWarps][32];
     __shared__ unsigned long long s_key[kWarps], s_cnt[kWarps];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const DevPattern &P = tb.pat[0];
-    load_topo(tb.topo, s_cm, s_magic, s_wt, s_ct);
-    const int lutn = (P.m + 1) * (P.m + 1);
-    for (int i = tid; i < lutn; i += kBlock) s_lut[i] = tb.lut[P.lut_off + i];
+    const int xs = P.m <= 15 ? 16 : 32;
+    load_topo(tb.topo, s_topo, xs);
+    load_lut(tb.lut + P.lut_off, P.m, xs, s_lut);
     if (tid < 28) s_edge[tid] = P.edge[tid];
+    const uint32_t *s_magic = s_topo.magic;
     const uint32_t busy = dq->busy;
     __syncthreads();
 
-    Ctx c = make_ctx<W>(tb.topo, s_cm, s_inc, s_lut, s_wt, s_ct, s_list[warp], P, busy, selector, sensitive);
+    Ctx c = make_ctx<W>(tb.topo, s_topo, s_inc, s_lut, xs, s_list[warp], P, busy, selector, sensitive);
     c.edge = s_edge;
     __syncthreads();  // s_inc written by every warp with identical values
 
@@ -590,22 +629,16 @@ __global__ void __launch_bounds__(kBlock, 2)
 esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query *__restrict__ qs,
           mapa_record *__restrict__ res, uint32_t *__restrict__ ctr) {
     constexpr int G = 32 / W;
-    __shared__ uint4 s_cm[kMaxN];
-    __shared__ uint32_t s_magic[kMaxN + 1];
+    __shared__ SmemTopo s_topo;
     __shared__ int s_inc[kWarps][kMaxN];
-    __shared__ uint16_t s_lut[kLutCapMulti];
-    __shared__ __align__(16) uint8_t s_wt[kMaxN * kMaxN];
-    __shared__ __align__(16) uint8_t s_ct[kMaxN * kMaxN];
-    __shared__ int2 s_list[kWarps][32];
+    __shared__ int4 s_list[kWarps][32];
+    extern __shared__ uint16_t s_lut[];  // npats * xs * xs Eq. 2 tables (dynamic)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    load_topo(tb.topo, s_cm, s_magic, s_wt, s_ct);
-    int lutn = 0;
-    for (int p = 0; p < tb.npats; ++p) {
-        const int e = tb.pat[p].lut_off + (tb.pat[p].m + 1) * (tb.pat[p].m + 1);
-        lutn = e > lutn ? e : lutn;
-    }
-    for (int i = tid; i < lutn; i += kBlock) s_lut[i] = tb.lut[i];
+    const int xs = tb.xs;
+    load_topo(tb.topo, s_topo, xs);
+    for (int p = 0; p < tb.npats; ++p) load_lut(tb.lut + tb.pat[p].lut_off, tb.pat[p].m, xs, s_lut + p * xs * xs);
+    const uint32_t *s_magic = s_topo.magic;
     __syncthreads();
 
     const unsigned long long nslots = (unsigned long long)nq * W;
@@ -623,7 +656,7 @@ esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query
             continue;
         }
         const DevPattern &P = tb.pat[pid];
-        Ctx c = make_ctx<W>(tb.topo, s_cm, s_inc[warp], s_lut + P.lut_off, s_wt, s_ct, s_list[warp], P, qu.busy,
+        Ctx c = make_ctx<W>(tb.topo, s_topo, s_inc[warp], s_lut + pid * xs * xs, xs, s_list[warp], P, qu.busy,
                             qu.selector, qu.sensitive);
         if (P.k > c.nF) continue;
         const uint32_t j = (uint32_t)(base % W) + g;
@@ -674,25 +707,19 @@ __global__ void __launch_bounds__(kBlock, 1)
 esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op *__restrict__ ops, int njobs,
           const mapa_query *__restrict__ jobs, unsigned long long *__restrict__ keys) {
     constexpr int G = 32 / W;
-    __shared__ uint4 s_cm[kMaxN];
-    __shared__ uint32_t s_magic[kMaxN + 1];
+    __shared__ SmemTopo s_topo;
     __shared__ int s_inc[kWarps][kMaxN];
-    __shared__ uint16_t s_lut[kLutCapMulti];
-    __shared__ __align__(16) uint8_t s_wt[kMaxN * kMaxN];
-    __shared__ __align__(16) uint8_t s_ct[kMaxN * kMaxN];
-    __shared__ int2 s_list[kWarps][32];
+    __shared__ int4 s_list[kWarps][32];
     __shared__ unsigned long long s_key[kWarps];
     __shared__ uint32_t s_busy;
+    extern __shared__ uint16_t s_lut[];  // npats * xs * xs Eq. 2 tables (dynamic)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int t = blockIdx.x;
-    load_topo(tb.topo, s_cm, s_magic, s_wt, s_ct);
-    int lutn = 0;
-    for (int p = 0; p < tb.npats; ++p) {
-        const int e = tb.pat[p].lut_off + (tb.pat[p].m + 1) * (tb.pat[p].m + 1);
-        lutn = e > lutn ? e : lutn;
-    }
-    for (int i = tid; i < lutn; i += kBlock) s_lut[i] = tb.lut[i];
+    const int xs = tb.xs;
+    load_topo(tb.topo, s_topo, xs);
+    for (int p = 0; p < tb.npats; ++p) load_lut(tb.lut + tb.pat[p].lut_off, tb.pat[p].m, xs, s_lut + p * xs * xs);
+    const uint32_t *s_magic = s_topo.magic;
     if (tid == 0) s_busy = 0u;
     __syncthreads();
     const mapa_trace_op *op = ops + (long long)t * nops;
@@ -708,8 +735,8 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
         const DevPattern &P = tb.pat[okp ? pid : 0];
         if (cur.op == 0) {
             const uint32_t busy = s_busy;
-            Ctx c = make_ctx<W>(tb.topo, s_cm, s_inc[warp], s_lut + P.lut_off, s_wt, s_ct, s_list[warp], P, busy,
-                                qu.selector, qu.sensitive);
+            Ctx c = make_ctx<W>(tb.topo, s_topo, s_inc[warp], s_lut + (okp ? pid : 0) * xs * xs, xs, s_list[warp], P,
+                                busy, qu.selector, qu.sensitive);
             Best bst{0ull, 0u, 0u};
             if (okp && P.k <= c.nF) {
                 const int D = (P.k - 1) < 2 ? (P.k - 1) : 2;
@@ -794,10 +821,11 @@ int launch_single(const SingleTables &tb, int selector, int sensitive, const map
 int launch_batch(const MultiTables &tb, int64_t nq, const mapa_query *d_queries, mapa_record *d_results,
                  uint32_t *d_ctr, int grid, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
+    const int dyn = tb.npats * tb.xs * tb.xs * (int)sizeof(uint16_t);
     switch (tb.topo.width) {
-        case 8: esa_batch<8><<<grid, kBlock, 0, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr); break;
-        case 16: esa_batch<16><<<grid, kBlock, 0, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr); break;
-        case 32: esa_batch<32><<<grid, kBlock, 0, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr); break;
+        case 8: esa_batch<8><<<grid, kBlock, dyn, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr); break;
+        case 16: esa_batch<16><<<grid, kBlock, dyn, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr); break;
+        case 32: esa_batch<32><<<grid, kBlock, dyn, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr); break;
         default: return (int)cudaErrorInvalidValue;
     }
     return (int)cudaGetLastError();
@@ -807,10 +835,11 @@ int launch_trace(const MultiTables &tb, int ntraces, int nops, const mapa_trace_
                  const mapa_query *d_jobs, uint64_t *d_keys, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     unsigned long long *k = reinterpret_cast<unsigned long long *>(d_keys);
+    const int dyn = tb.npats * tb.xs * tb.xs * (int)sizeof(uint16_t);
     switch (tb.topo.width) {
-        case 8: esa_trace<8><<<ntraces, kBlock, 0, st>>>(tb, nops, d_ops, njobs, d_jobs, k); break;
-        case 16: esa_trace<16><<<ntraces, kBlock, 0, st>>>(tb, nops, d_ops, njobs, d_jobs, k); break;
-        case 32: esa_trace<32><<<ntraces, kBlock, 0, st>>>(tb, nops, d_ops, njobs, d_jobs, k); break;
+        case 8: esa_trace<8><<<ntraces, kBlock, dyn, st>>>(tb, nops, d_ops, njobs, d_jobs, k); break;
+        case 16: esa_trace<16><<<ntraces, kBlock, dyn, st>>>(tb, nops, d_ops, njobs, d_jobs, k); break;
+        case 32: esa_trace<32><<<ntraces, kBlock, dyn, st>>>(tb, nops, d_ops, njobs, d_jobs, k); break;
         default: return (int)cudaErrorInvalidValue;
     }
     return (int)cudaGetLastError();
@@ -848,13 +877,24 @@ int max_blocks_per_sm_single(int width, int k, int sens) {
     return occ_single<32>(k, sens);
 }
 
-int max_blocks_per_sm_batch(int width) {
+int max_blocks_per_sm_batch(int width, int dyn_smem) {
     int nb = 0;
     cudaError_t e = cudaErrorInvalidValue;
-    if (width == 8) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, esa_batch<8>, kBlock, 0);
-    if (width == 16) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, esa_batch<16>, kBlock, 0);
-    if (width == 32) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, esa_batch<32>, kBlock, 0);
+    if (width == 8) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, esa_batch<8>, kBlock, dyn_smem);
+    if (width == 16) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, esa_batch<16>, kBlock, dyn_smem);
+    if (width == 32) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, esa_batch<32>, kBlock, dyn_smem);
     return (e == cudaSuccess && nb > 0) ? nb : 1;
+}
+
+int set_dynamic_smem(int bytes) {
+    // batch / trace kernels keep npats Eq. 2 tables in dynamic shared memory
+    const void *fs[6] = {(const void *)esa_batch<8>, (const void *)esa_batch<16>, (const void *)esa_batch<32>,
+                         (const void *)esa_trace<8>, (const void *)esa_trace<16>, (const void *)esa_trace<32>};
+    for (const void *f : fs) {
+        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+        if (e != cudaSuccess) return (int)e;
+    }
+    return 0;
 }
 
 const char *cuda_error_string(int err) { return cudaGetErrorString((cudaError_t)err); }

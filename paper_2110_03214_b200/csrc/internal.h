@@ -49,7 +49,8 @@ template <int MAXP, int LUTCAP>
 struct Tables {
     DevTopo topo;
     int32_t npats;
-    int32_t pad[3];
+    int32_t xs;      // row stride of the Eq. 2 tables on the device (16 if every m <= 15, else 32)
+    int32_t pad[2];
     DevPattern pat[MAXP];
     uint16_t lut[LUTCAP];
 };
@@ -74,7 +75,8 @@ int launch_trace(const MultiTables &tb, int ntraces, int nops, const mapa_trace_
                  const mapa_query *d_jobs, uint64_t *d_keys, void *stream);
 int device_sm_count();
 int max_blocks_per_sm_single(int width, int k, int sens);
-int max_blocks_per_sm_batch(int width);
+int max_blocks_per_sm_batch(int width, int dyn_smem);
+int set_dynamic_smem(int bytes);
 const char *cuda_error_string(int err);
 
 }  // namespace mapa

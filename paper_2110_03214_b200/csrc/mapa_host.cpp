@@ -450,6 +450,9 @@ mapa_status build_multi(const mapa_topology *t, const mapa_pattern *const *pats,
     std::memset(tb, 0, sizeof(*tb));
     fill_devtopo(t, tb->topo);
     tb->npats = npats;
+    tb->xs = 16;
+    for (int i = 0; i < npats; ++i)
+        if (pats[i] && pats[i]->m > 15) tb->xs = 32;
     int off = 0;
     for (int i = 0; i < npats; ++i) {
         if (!pats[i]) return fail(MAPA_E_INVALID_ARG, "null pattern");
@@ -688,9 +691,11 @@ mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *cons
     if (nq == 0) return MAPA_OK;
     if ((err = (int)cudaMemsetAsync(d_results, 0, (size_t)nq * sizeof(mapa_record), st))) return cuda_fail(err, "memset");
     if ((err = (int)cudaMemsetAsync(d_scratch, 0, 64, st))) return cuda_fail(err, "memset");
+    const int dyn = tbp->npats * tbp->xs * tbp->xs * 2;
+    if ((err = set_dynamic_smem(dyn))) return cuda_fail(err, "cudaFuncSetAttribute");
     int sm = device_sm_count();
     if (sm <= 0) sm = 148;
-    const int grid = sm * max_blocks_per_sm_batch(t->width);
+    const int grid = sm * max_blocks_per_sm_batch(t->width, dyn);
     err = launch_batch(*tbp, nq, d_queries, d_results, (uint32_t *)d_scratch, grid, stream);
     if (err) return cuda_fail(err, "esa_batch launch");
     return MAPA_OK;
@@ -706,7 +711,9 @@ mapa_status mapa_trace_replay(const mapa_topology *t, const mapa_pattern *const 
     if (!tbp) tbp = new MultiTables();
     mapa_status s = build_multi(t, pats, npats, flags, tbp);
     if (s != MAPA_OK) return s;
-    int err = (int)cudaMemsetAsync(d_keys, 0, (size_t)ntraces * njobs * sizeof(uint64_t), (cudaStream_t)stream);
+    int err = set_dynamic_smem(tbp->npats * tbp->xs * tbp->xs * 2);
+    if (err) return cuda_fail(err, "cudaFuncSetAttribute");
+    err = (int)cudaMemsetAsync(d_keys, 0, (size_t)ntraces * njobs * sizeof(uint64_t), (cudaStream_t)stream);
     if (err) return cuda_fail(err, "memset");
     err = launch_trace(*tbp, ntraces, nops, d_ops, njobs, d_jobs, d_keys, stream);
     if (err) return cuda_fail(err, "esa_trace launch");
