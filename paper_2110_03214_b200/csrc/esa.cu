@@ -5,37 +5,42 @@
 //   S4 enumeration      DFS over injective maps f: V(P) -> F (§3.3 P:496-501;
 //                       G complete, so every injective map embeds).
 //                       Lanes = devices of the LAST pattern vertex k-1; the
-//                       inner loop walks the devices v of vertex k-2.  Groups
-//                       of W lanes (W = 8/16/32 = padded N) each run their own
-//                       prefix, so small topologies still fill the warp.
+//                       two levels above it (k-3, k-2) walk per-group smem
+//                       candidate lists; outer levels are a uniform DFS.
+//                       Groups of W lanes (W = 8/16/32 = padded N) each run
+//                       their own prefix, so small topologies fill the warp.
 //                       Canonical mode adds lex-leader lower bounds (one leaf
 //                       per Aut(P)-orbit = SPEC dedup S:209).
 //   S5 scoring          integer only.  With v's class masks c0..c2 and any
 //                       device set X not containing v:
 //                         sum_{u in X} w(u,v) = 12|X| + 38 popc(c0&X)
 //                                               + 13 popc(c1&X) + 8 popc(c2&X)
-//                       Outer DFS levels use that (popc, lane-uniform); the
-//                       inner loop uses no popc at all: per prefix the lanes
-//                       precompute in parallel (a) the score increment of
-//                       placing vertex k-2 on their device (broadcast through
-//                       a 32-entry smem list) and (b) their own leaf partial
-//                       over vertices 0..k-3; each inner iteration then adds
-//                       one list entry and one 32x32 weight-table byte.
+//                       (popc on the outer levels only).  For the inner levels
+//                       the lanes precompute in parallel the increment of
+//                       placing vertex k-3 / k-2 on their device (broadcast
+//                       through the lists) and their own leaf partial; a
+//                       k-3 step then costs one weight lookup per lane, a
+//                       k-2 step one list read + one table read + one fused
+//                       add-max per leaf.
 //                         Eq. 1 AggBW: X = back-neighbour devices.
 //                         Eq. 3 PreservedBW: T_F - sum inc_F(S)
 //                         + inside(S), X = all placed devices.
 //                         Eq. 2: census (x, y) accumulated as a
-//                         table index x*(m+1)+y; score = dense rank of Eq. 2
+//                         table index x*xs + y; score = dense rank of Eq. 2
 //                         among the censuses with x+y+z = m (host table).
-//   S6 argmax           per-lane running max of a packed 64-bit key (score |
-//                       brev(S) | edge code), built out of line only when the
-//                       score reaches the lane's best; warp shuffle max, block
-//                       max, atomicMax in HBM.  Max is order independent, so
-//                       the result is identical for every grid / rank count.
+//   S6 argmax           leaves of one k-2 scan are ranked by (score+1)*32 +
+//                       (31 - v) (ties -> smaller v = lex-smaller device set);
+//                       the packed 64-bit key (score | brev(S) | edge code) is
+//                       built out of line only when a scan's best reaches the
+//                       lane's best score; warp shuffle max, block max,
+//                       atomicMax in HBM.  Max is order independent, so the
+//                       result is identical for every grid size / rank count.
 // Work items: the prefixes of depth D (mixed radix over the free devices),
 // handed out as contiguous chunks; a chunk is walked as a DFS range, so only
-// the first item of a run is decoded.  No dense contraction exists, so no
-// tensor cores are used; the bound is integer issue.
+// the first item of a run is decoded.  All tables live in one dynamic
+// shared-memory block (Shared below) addressed by offset, so the per-query
+// context holds no pointers.  No dense contraction exists, so no tensor cores
+// are used; the bound is integer issue / LSU.
 #include <cuda_runtime.h>
 
 #include "internal.h"
@@ -47,13 +52,54 @@ constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int kBlock = 256;
 constexpr int kWarps = kBlock / 32;
 constexpr int kMaxDecode = 4;
+constexpr int kNN = kMaxN * kMaxN;
 
 enum { SEL_LIN = 0, SEL_SENS = 1 };
 
+// Leaves of a k-2 scan are ranked by one int: (score + 1) * 32 + (31 - v).
+// Invalid leaves (vertex k-1 on the device of k-2, a lex-leader violation,
+// a padding lane) get kNeg added through the tables.
+constexpr int kNeg = -(1 << 28);
+
+// Per-warp candidate lists of the innermost DFS levels (G groups x W).
+struct WarpLists {
+    int dense[32];  // level k-2: per device, increment of placing k-2 there (or a sentinel)
+    int2 l3[32];    // level k-3: (v, increment of placing k-3 on v)
+};
+
+// One dynamic shared-memory block per CTA.  Tables are indexed [v*32 + b]:
+//   tw  = 32 w(v,b), kNeg when v == b or either is not a device
+//   tz  = 0,         kNeg likewise
+//   twd / tzd = the same with kNeg also where v >= b (canonical f(k-2) < f(k-1))
+//   twp = w(v,b) (0 when invalid), tdl = census delta xs [double] + [single]
+//   tse / tsed = tdl + kSent when invalid (/ v >= b); ts0 / ts0d = 0 + kSent
+//     (kSent = xs*xs moves the Eq. 2 index into a region of kNeg entries)
+// followed by npats Eq. 2 tables of 3 xs^2 ints: [x*xs + y] = (rank+1)*32,
+// [xs^2, 3 xs^2) = kNeg (an index carries at most two kSent offsets).
+struct Shared {
+    uint4 cm[kMaxN];
+    uint32_t magic[kMaxN + 4];
+    int tw[kNN], tz[kNN], twd[kNN], tzd[kNN], twp[kNN], tdl[kNN];
+    int tse[kNN], tsed[kNN], ts0[kNN], ts0d[kNN];
+    int inc[kWarps][kMaxN];
+    WarpLists wl[kWarps];
+    unsigned long long key[kWarps], cnt[kWarps];
+    uint8_t edge[kMaxPats][28];
+    uint32_t busy;
+    uint32_t pad[3];
+};
+
+extern __shared__ __align__(16) unsigned char g_smem[];
+__device__ __forceinline__ Shared &sh() { return *reinterpret_cast<Shared *>(g_smem); }
+__device__ __forceinline__ int *sh_lut() { return reinterpret_cast<int *>(g_smem + sizeof(Shared)); }
+
+template <int W>
 struct Ctx {
     uint32_t F;
     int nF;
     int b;                          // lane's device id (lane % W)
+    int g;                          // lane's group in the warp
+    int warp;
     uint32_t gmask;                 // lanes of this lane's group
     uint32_t cm0, cm1, cm2, cm12;   // lane's class masks
     int incb;                       // inc_F(b)
@@ -62,17 +108,12 @@ struct Ctx {
     int w0, w1, w2, w12;            // 38, 13, 8, 12 (0 for Baseline)
     int useU;                       // 1: X = all placed devices (Eq. 3), 0: back neighbours
     int acc0;                       // accumulator at the root (T_F for Eq. 3)
-    const uint4 *cm;                // class masks of every device (smem)
-    const int *inc;                 // inc_F(v) (smem)
-    const uint16_t *lut;            // Eq. 2 table: (rank + 1) * 32 at [x * xs + y] (smem)
-    const int *tw, *tz, *twd, *tzd; // inner-loop tables [v*32 + b] (smem, see SmemTopo)
-    const int *tdl;                 // census index delta of edge (v, b) (smem)
-    int4 *list;                     // this group's inner-loop candidate list (smem, W entries)
-    int xs;                         // row stride of the Eq. 2 table (16 or 32)
-    int mp1;                        // m + 1
+    int xs;                         // Eq. 2 table row stride (16 or 32)
+    int lut;                        // this pattern's Eq. 2 table offset (ints) in sh_lut()
+    int pid;                        // pattern index (edge list in smem)
     uint64_t fb, fs, db;            // bytes: fwd_back, fwd_src, dback
     int clique, eb, m;
-    const uint8_t *edge;            // pattern edges a | b<<4
+    int col[W];                     // lane's inner-scan column (see lane_column)
 };
 
 template <int K>
@@ -91,25 +132,12 @@ struct Best {
     uint32_t cnt;
 };
 
-// Inner-loop leaves are ranked by one int: (score + 1) * 32 + (31 - v).  Its
-// max is the max score with ties to the smallest v.  Invalid leaves (vertex
-// K-1 on the device of K-2, or a lex-leader violation) get kNeg added.
-constexpr int kNeg = -(1 << 28);
-
-// Per-CTA topology tables (shared memory), all indexed [v * 32 + b]:
-//   tw  = 32 * w(v,b), kNeg when v == b or either is not a device
-//   tz  = 0,           kNeg likewise
-//   twd / tzd = the same with kNeg also where v >= b (canonical f(K-2) < f(K-1))
-//   tdl = census index delta of the edge (v,b): xs * [double] + [single]
-struct SmemTopo {
-    uint4 cm[kMaxN];
-    uint32_t magic[kMaxN + 1];
-    int tw[kMaxN * kMaxN], tz[kMaxN * kMaxN], twd[kMaxN * kMaxN], tzd[kMaxN * kMaxN];
-    int tdl[kMaxN * kMaxN];
-};
-
 __device__ __forceinline__ unsigned long long *u64p(uint64_t *p) {
     return reinterpret_cast<unsigned long long *>(p);
+}
+
+__device__ __forceinline__ int lds_off(const int *base, int byte_off) {
+    return *reinterpret_cast<const int *>(reinterpret_cast<const char *>(base) + byte_off);
 }
 
 __device__ __forceinline__ uint32_t nth_set(uint32_t m, uint32_t n) {
@@ -123,14 +151,12 @@ __device__ __forceinline__ uint32_t nth_set(uint32_t m, uint32_t n) {
     return pos;
 }
 
-// Packed argmax key: score | brev_W(S) | edge code.  Only
-// evaluated on the slow path (score >= the lane's best score), so it is kept
-// out of line; arguments by value so the DFS state stays in registers.
+// Packed argmax key: score | brev_W(S) | edge code, built
+// out of line on the slow path; arguments by value.
 //   fpack: f(0..K-2) one byte each; b: device of vertex K-1.
 template <int W, int K>
 __device__ __noinline__ unsigned long long make_key(uint32_t S, unsigned long long fpack, uint32_t b,
-                                                    uint32_t s, int clique, int eb, int m,
-                                                    const uint8_t *edge) {
+                                                    uint32_t s, int clique, int eb, int m, int pid) {
     const uint32_t sb = __brev(S) >> (32 - W);
     uint32_t ecode;
     if (clique) {
@@ -144,6 +170,7 @@ __device__ __noinline__ unsigned long long make_key(uint32_t S, unsigned long lo
         }
         R |= (uint32_t)__popc(S & ((1u << b) - 1u)) << (4 * (K - 1));
         ecode = 0;
+        const uint8_t *edge = sh().edge[pid];
         for (int e = 0; e < m; ++e) {
             const uint32_t ed = edge[e];
             const uint32_t ra = (R >> (4 * (ed & 15u))) & 15u;
@@ -157,25 +184,30 @@ __device__ __noinline__ unsigned long long make_key(uint32_t S, unsigned long lo
 }
 
 template <int W, int K>
-__device__ __forceinline__ void consider(const Ctx &c, Best &bst, uint32_t S, unsigned long long fpack,
+__device__ __forceinline__ void consider(const Ctx<W> &c, Best &bst, uint32_t S, unsigned long long fpack,
                                          uint32_t s) {
-    const unsigned long long key = make_key<W, K>(S, fpack, (uint32_t)c.b, s, c.clique, c.eb, c.m, c.edge);
+    if (s == bst.bs && bst.key) {
+        // equal score: the device-set field decides unless the sets are equal
+        const uint32_t sb_new = __brev(S) >> (32 - W);
+        const uint32_t sb_old = (uint32_t)(bst.key >> c.eb) & (W >= 32 ? kFull : ((1u << W) - 1u));
+        if (sb_new < sb_old) return;
+    }
+    const unsigned long long key = make_key<W, K>(S, fpack, (uint32_t)c.b, s, c.clique, c.eb, c.m, c.pid);
     if (key > bst.key) {
         bst.key = key;
         bst.bs = s;
     }
 }
 
-template <int K, int SEL, int J>
-__device__ __forceinline__ St<K> push(const Ctx &c, const St<K> &st, uint32_t v) {
+template <int W, int K, int SEL, int J>
+__device__ __forceinline__ St<K> push(const Ctx<W> &c, const St<K> &st, uint32_t v) {
     St<K> s = st;
     const uint32_t vb = 1u << v;
-    const uint4 t = c.cm[v];
+    const uint4 t = sh().cm[v];
     if constexpr (SEL == SEL_LIN) {
         const uint32_t X = c.useU ? st.U : st.bm[J];
-        const int n12 = c.useU ? J : (int)((c.db >> (8 * J)) & 0xFFu);
-        const int incv = c.useU ? c.inc[v] : 0;
-        s.acc = st.acc + c.w12 * n12 - incv + c.w0 * __popc(t.x & X) + c.w1 * __popc(t.y & X) +
+        const int incv = c.useU ? sh().inc[c.warp][v] : 0;
+        s.acc = st.acc + c.w12 * __popc(X) - incv + c.w0 * __popc(t.x & X) + c.w1 * __popc(t.y & X) +
                 c.w2 * __popc(t.z & X);
     } else {
         const uint32_t X = st.bm[J];
@@ -205,31 +237,76 @@ __device__ __forceinline__ unsigned long long pack_f(const St<K> &st) {
 
 // k = 1: a single level, the lanes are the devices of vertex 0.
 template <int W, int SEL>
-__device__ __forceinline__ void leaf_k1(const Ctx &c, Best &bst) {
+__device__ __forceinline__ void leaf_k1(const Ctx<W> &c, Best &bst) {
     const bool act = (c.F >> c.b) & 1u;
     const int s = (SEL == SEL_LIN) ? c.acc0 + c.leafC : 0;  // m = 0: census (0,0,0) has rank 0
     bst.cnt += act ? 1u : 0u;
     if (act && (uint32_t)s >= bst.bs) consider<W, 1>(c, bst, 1u << c.b, 0ull, (uint32_t)s);
 }
 
-// The two innermost levels: vertex K-2 walks the devices of `cand`
-// (uniform loop), vertex K-1 sits on the lanes.  Vertices 0..K-3 are placed.
+// Level k-2 scan, dense over the W devices of the group.  Lane b writes its
+// entry (increment of placing vertex k-2 on b, or a sentinel when b is not a
+// candidate) into the group's table; then every lane (device of vertex k-1)
+// ranks all W leaves (v, b) with its register column c.col (fully unrolled,
+// compile-time indices) and keeps the max.  Within one scan a lane's leaves
+// differ only in v, and among equal scores the smaller v is the lex-smaller
+// device set (larger key), so the packed rank (score+1)*32 + (31-v) decides
+// and the full key is built once, later.  Returns < 32 when no valid leaf.
+//   LIN:  rank = base + tab[v] + col[v],     tab = 32 t2 | kNeg, col = T[v][b] + 31 - v
+//   SENS: rank = lut[base + tab[v] + col[v]] + 31 - v,  tab = t2 | kSent, col = D[v][b]
+template <int W, int SEL>
+__device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2, int base) {
+    const uint32_t b = (uint32_t)c.b;
+    int *tab = sh().wl[c.warp].dense + c.g * W;
+    const bool mine = (cand >> b) & 1u;
+    __syncwarp(c.gmask);  // previous readers of the table are done
+    if constexpr (SEL == SEL_LIN) tab[b] = mine ? t2 * 32 : kNeg;
+    else tab[b] = mine ? t2 : c.xs * c.xs;
+    __syncwarp(c.gmask);
+    const int4 *t4 = reinterpret_cast<const int4 *>(tab);
+    int best = 0;
+    if constexpr (SEL == SEL_LIN) {
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q) {
+            const int4 e = t4[q];
+            const int r0 = base + e.x + c.col[4 * q + 0];
+            const int r1 = base + e.y + c.col[4 * q + 1];
+            const int r2 = base + e.z + c.col[4 * q + 2];
+            const int r3 = base + e.w + c.col[4 * q + 3];
+            best = max(best, max(r0, r1));
+            best = max(best, max(r2, r3));
+        }
+    } else {
+        const int *lut = sh_lut() + c.lut;
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q) {
+            const int4 e = t4[q];
+            const int r0 = lut[base + e.x + c.col[4 * q + 0]] + (31 - (4 * q + 0));
+            const int r1 = lut[base + e.y + c.col[4 * q + 1]] + (31 - (4 * q + 1));
+            const int r2 = lut[base + e.z + c.col[4 * q + 2]] + (31 - (4 * q + 2));
+            const int r3 = lut[base + e.w + c.col[4 * q + 3]] + (31 - (4 * q + 3));
+            best = max(best, max(r0, r1));
+            best = max(best, max(r2, r3));
+        }
+    }
+    return best;
+}
+
+// The two innermost levels: vertex k-2 walks the devices of `cand`, vertex
+// k-1 sits on the lanes.  Vertices 0..k-3 are placed.
 template <int W, int K, int SEL>
-__device__ __forceinline__ void inner(const Ctx &c, const St<K> &st, uint32_t cand, Best &bst) {
+__device__ __forceinline__ void inner(const Ctx<W> &c, const St<K> &st, uint32_t cand, Best &bst) {
     constexpr int J = K - 2;
     const uint32_t b = (uint32_t)c.b;
     const uint32_t fbJ = (uint32_t)(c.fb >> (8 * J)) & 0xFFu;
     const uint32_t fsJ = (uint32_t)(c.fs >> (8 * J)) & 0xFFu;
-    const bool eK = (fbJ >> (K - 1)) & 1u;   // pattern edge (K-2, K-1)
-    const bool dep = (fsJ >> (K - 1)) & 1u;  // lex-leader f(K-2) < f(K-1)
-    // (a) t2: increment of placing vertex K-2 on this lane's device;
-    // (b) lp: this lane's leaf partial over vertices 0..K-3.
+    const bool eK = (fbJ >> (K - 1)) & 1u;   // pattern edge (k-2, k-1)
+    const bool dep = (fsJ >> (K - 1)) & 1u;  // lex-leader f(k-2) < f(k-1)
     int t2, base;
     if constexpr (SEL == SEL_LIN) {
         const uint32_t X2 = c.useU ? st.U : st.bm[J];
         const uint32_t X1 = c.useU ? st.U : st.bm[K - 1];
-        const int n2 = c.useU ? J : (int)((c.db >> (8 * J)) & 0xFFu);
-        t2 = c.w12 * n2 - (c.useU ? c.incb : 0) + c.w0 * __popc(c.cm0 & X2) + c.w1 * __popc(c.cm1 & X2) +
+        t2 = c.w12 * __popc(X2) - (c.useU ? c.incb : 0) + c.w0 * __popc(c.cm0 & X2) + c.w1 * __popc(c.cm1 & X2) +
              c.w2 * __popc(c.cm2 & X2);
         const int lp = c.laneC + c.w12 * __popc(X1) + c.w0 * __popc(c.cm0 & X1) + c.w1 * __popc(c.cm1 & X1) +
                        c.w2 * __popc(c.cm2 & X1);
@@ -239,49 +316,11 @@ __device__ __forceinline__ void inner(const Ctx &c, const St<K> &st, uint32_t ca
         t2 = __popc(c.cm0 & X2) * c.xs + __popc(c.cm12 & X2);
         base = (st.acc + __popc(c.cm0 & X1)) * c.xs + st.acc2 + __popc(c.cm12 & X1);  // census index
     }
-    // Candidate list of this group, in increasing device order: entry i =
-    // (byte offset of table row v, LIN rank increment 32*t2 + 31 - v,
-    //  SENS census-index increment t2, 31 - v).
-    const uint32_t n = (uint32_t)__popc(cand);
-    __syncwarp(c.gmask);  // previous readers of the list are done
-    if ((cand >> b) & 1u)
-        c.list[__popc(cand & ((1u << b) - 1u))] = make_int4((int)b * 128, t2 * 32 + 31 - (int)b, t2, 31 - (int)b);
-    __syncwarp(c.gmask);
     const bool laneok = ((c.F & ~st.U & st.al[K - 1]) >> b) & 1u;
     // leaves counted: v in cand with v != b (and v < b if canonical-ordered)
     const uint32_t M = laneok ? (dep ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
     bst.cnt += (uint32_t)__popc(M & cand);
-    // Within this call the lane's leaves differ only in v, and for equal
-    // scores the smaller v is the lex-smaller device set (larger key): the
-    // packed rank (score+1)*32 + 31-v is maxed branch-free and the full key
-    // is built once afterwards.
-    int best = 0;
-    if constexpr (SEL == SEL_LIN) {
-        const bool eW = c.w12 != 0 && (c.useU || eK);
-        const char *tb = reinterpret_cast<const char *>((eW ? (dep ? c.twd : c.tw) : (dep ? c.tzd : c.tz)) + b);
-#pragma unroll 4
-        for (uint32_t i = 0; i < n; ++i) {
-            const int4 e = c.list[i];
-            best = max(best, base + e.y + *reinterpret_cast<const int *>(tb + e.x));
-        }
-    } else {
-        const char *tz = reinterpret_cast<const char *>((dep ? c.tzd : c.tz) + b);
-        if (eK) {
-            const char *td = reinterpret_cast<const char *>(c.tdl + b);
-#pragma unroll 4
-            for (uint32_t i = 0; i < n; ++i) {
-                const int4 e = c.list[i];
-                const int idx = base + e.z + *reinterpret_cast<const int *>(td + e.x);
-                best = max(best, (int)c.lut[idx] + e.w + *reinterpret_cast<const int *>(tz + e.x));
-            }
-        } else {
-#pragma unroll 4
-            for (uint32_t i = 0; i < n; ++i) {
-                const int4 e = c.list[i];
-                best = max(best, (int)c.lut[base + e.z] + e.w + *reinterpret_cast<const int *>(tz + e.x));
-            }
-        }
-    }
+    const int best = scan_dense<W, SEL>(c, cand, t2, base);
     if (laneok && best >= 32) {
         const uint32_t s = (uint32_t)(best >> 5) - 1u;
         if (s >= bst.bs) {
@@ -293,24 +332,100 @@ __device__ __forceinline__ void inner(const Ctx &c, const St<K> &st, uint32_t ca
     }
 }
 
+// The three innermost levels: vertex k-3 walks `cand3` (uniform loop over a
+// per-group list of (v3, increment of placing k-3 on v3) built lane-parallel);
+// for every v3 the lane values are updated by ONE table lookup (w(v3,b) or the
+// census delta) and the k-2 list scan runs.  Vertices 0..k-4 are placed.
+template <int W, int K, int SEL>
+__device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_t cand3, Best &bst) {
+    constexpr int J3 = K - 3, J2 = K - 2, J1 = K - 1;
+    const uint32_t b = (uint32_t)c.b;
+    const uint32_t fb3 = (uint32_t)(c.fb >> (8 * J3)) & 0xFFu, fs3 = (uint32_t)(c.fs >> (8 * J3)) & 0xFFu;
+    const uint32_t fb2 = (uint32_t)(c.fb >> (8 * J2)) & 0xFFu, fs2 = (uint32_t)(c.fs >> (8 * J2)) & 0xFFu;
+    const bool e32 = (fb3 >> J2) & 1u, e31 = (fb3 >> J1) & 1u, e21 = (fb2 >> J1) & 1u;
+    const bool d32 = (fs3 >> J2) & 1u, d31 = (fs3 >> J1) & 1u, d21 = (fs2 >> J1) & 1u;
+    // lane values over the placed vertices 0..k-4:
+    //   t3 = increment of placing k-3 on b, t2b = of placing k-2 on b,
+    //   lpb = leaf partial of k-1 on b; v3 then adds m32 w3, m31 w3.
+    int t3, t2b, lpb, m32, m31, A;
+    const int *wcol;
+    if constexpr (SEL == SEL_LIN) {
+        const uint32_t X3 = c.useU ? st.U : st.bm[J3];
+        const uint32_t X2 = c.useU ? st.U : st.bm[J2];
+        const uint32_t X1 = c.useU ? st.U : st.bm[J1];
+        const int inc = c.useU ? c.incb : 0;
+        t3 = c.w12 * __popc(X3) - inc + c.w0 * __popc(c.cm0 & X3) + c.w1 * __popc(c.cm1 & X3) +
+             c.w2 * __popc(c.cm2 & X3);
+        t2b = c.w12 * __popc(X2) - inc + c.w0 * __popc(c.cm0 & X2) + c.w1 * __popc(c.cm1 & X2) +
+              c.w2 * __popc(c.cm2 & X2);
+        lpb = c.laneC + c.w12 * __popc(X1) + c.w0 * __popc(c.cm0 & X1) + c.w1 * __popc(c.cm1 & X1) +
+              c.w2 * __popc(c.cm2 & X1);
+        m32 = (c.w12 != 0 && (c.useU || e32)) ? 1 : 0;
+        m31 = (c.w12 != 0 && (c.useU || e31)) ? 1 : 0;
+        A = st.acc;
+        wcol = sh().twp + b;
+    } else {
+        const uint32_t X3 = st.bm[J3], X2 = st.bm[J2], X1 = st.bm[J1];
+        t3 = __popc(c.cm0 & X3) * c.xs + __popc(c.cm12 & X3);
+        t2b = __popc(c.cm0 & X2) * c.xs + __popc(c.cm12 & X2);
+        lpb = __popc(c.cm0 & X1) * c.xs + __popc(c.cm12 & X1);
+        m32 = e32 ? 1 : 0;
+        m31 = e31 ? 1 : 0;
+        A = st.acc * c.xs + st.acc2;
+        wcol = sh().tdl + b;
+    }
+    int2 *L3 = sh().wl[c.warp].l3 + c.g * W;
+    const uint32_t n3 = (uint32_t)__popc(cand3);
+    __syncwarp(c.gmask);  // previous readers of the k-3 list are done
+    if ((cand3 >> b) & 1u) L3[__popc(cand3 & ((1u << b) - 1u))] = make_int2((int)b, t3);
+    __syncwarp(c.gmask);
+    const bool okb = ((c.F & ~st.U & st.al[J1]) >> b) & 1u;
+    const uint32_t cand2b = c.F & ~st.U & st.al[J2];
+    const unsigned long long fbase = pack_f<K>(st);
+    for (uint32_t i = 0; i < n3; ++i) {
+        const int2 e3 = L3[i];
+        const uint32_t v3 = (uint32_t)e3.x;
+        const int w3 = wcol[v3 * 32];
+        const int t2 = t2b + m32 * w3;
+        const int lp = lpb + m31 * w3;
+        const uint32_t cand2 = cand2b & ~(1u << v3) & (d32 ? (0xFFFFFFFEu << v3) : kFull);
+        const bool laneok = okb && b != v3 && (!d31 || b > v3);
+        const uint32_t M = laneok ? (d21 ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
+        bst.cnt += (uint32_t)__popc(M & cand2);
+        const int base = (SEL == SEL_LIN) ? (A + e3.y + lp + 1) * 32 : A + e3.y + lp;
+        const int best = scan_dense<W, SEL>(c, cand2, t2, base);
+        if (laneok && best >= 32) {
+            const uint32_t s = (uint32_t)(best >> 5) - 1u;
+            if (s >= bst.bs) {
+                const uint32_t bestv = 31u - (uint32_t)(best & 31);
+                const unsigned long long fpack =
+                    fbase | ((unsigned long long)v3 << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
+                consider<W, K>(c, bst, st.U | (1u << v3) | (1u << bestv) | (1u << b), fpack, s);
+            }
+        }
+    }
+}
+
 template <int W, int K, int SEL, int J>
-__device__ __forceinline__ void level(const Ctx &c, const St<K> &st, Best &bst) {
+__device__ __forceinline__ void level(const Ctx<W> &c, const St<K> &st, Best &bst) {
     if constexpr (K == 1) {
         leaf_k1<W, SEL>(c, bst);
     } else if constexpr (J == K - 2) {
         inner<W, K, SEL>(c, st, c.F & ~st.U & st.al[J], bst);
+    } else if constexpr (J == K - 3) {
+        inner3<W, K, SEL>(c, st, c.F & ~st.U & st.al[J], bst);
     } else {
         uint32_t cand = c.F & ~st.U & st.al[J];
         while (cand) {
             const uint32_t v = __ffs(cand) - 1;
             cand &= cand - 1u;
-            level<W, K, SEL, J + 1>(c, push<K, SEL, J>(c, st, v), bst);
+            level<W, K, SEL, J + 1>(c, push<W, K, SEL, J>(c, st, v), bst);
         }
     }
 }
 
-template <int K>
-__device__ __forceinline__ St<K> root(const Ctx &c) {
+template <int W, int K>
+__device__ __forceinline__ St<K> root(const Ctx<W> &c) {
     St<K> st;
     st.U = 0;
     st.acc = c.acc0;
@@ -325,14 +440,13 @@ __device__ __forceinline__ St<K> root(const Ctx &c) {
 }
 
 // item -> mixed-radix digits (radix nF - j at level j); false if item >= P(nF, D)
-__device__ __forceinline__ bool digits(uint32_t item, int nF, int D, const uint32_t *magic,
-                                       uint32_t (&dg)[kMaxDecode]) {
+__device__ __forceinline__ bool digits(uint32_t item, int nF, int D, uint32_t (&dg)[kMaxDecode]) {
     uint32_t it = item;
 #pragma unroll
     for (int j = kMaxDecode - 1; j >= 0; --j) {
         if (j < D) {
             const uint32_t r = (uint32_t)(nF - j);
-            const uint32_t q = __umulhi(it, magic[r]);
+            const uint32_t q = __umulhi(it, sh().magic[r]);
             dg[j] = it - q * r;
             it = q;
         } else {
@@ -353,7 +467,7 @@ __device__ __forceinline__ uint32_t perm_count(int n, int d) {
 // candidates from digit dg[D-1] on.  Returns the number of items consumed
 // (>= 1); a prefix that violates a lex-leader bound skips its whole subtree.
 template <int W, int K, int SEL, int J, int DMAX>
-__device__ __forceinline__ uint32_t descend_range(const Ctx &c, const St<K> &st, const uint32_t (&dg)[kMaxDecode],
+__device__ __forceinline__ uint32_t descend_range(const Ctx<W> &c, const St<K> &st, const uint32_t (&dg)[kMaxDecode],
                                                   int D, uint32_t maxn, Best &bst) {
     if constexpr (J >= DMAX || J > K - 2) {
         return maxn;  // unreachable: D <= DMAX <= K-1
@@ -371,7 +485,7 @@ __device__ __forceinline__ uint32_t descend_range(const Ctx &c, const St<K> &st,
                 }
                 return min(maxn, prod - off);
             }
-            return descend_range<W, K, SEL, J + 1, DMAX>(c, push<K, SEL, J>(c, st, v), dg, D, maxn, bst);
+            return descend_range<W, K, SEL, J + 1, DMAX>(c, push<W, K, SEL, J>(c, st, v), dg, D, maxn, bst);
         } else {
             uint32_t cand = c.F & ~st.U;
             const uint32_t p = nth_set(cand, dg[J]);
@@ -384,11 +498,13 @@ __device__ __forceinline__ uint32_t descend_range(const Ctx &c, const St<K> &st,
             cand &= st.al[J];
             if constexpr (J == K - 2) {
                 inner<W, K, SEL>(c, st, cand, bst);
+            } else if constexpr (J == K - 3) {
+                inner3<W, K, SEL>(c, st, cand, bst);
             } else {
                 while (cand) {
                     const uint32_t v = __ffs(cand) - 1;
                     cand &= cand - 1u;
-                    level<W, K, SEL, J + 1>(c, push<K, SEL, J>(c, st, v), bst);
+                    level<W, K, SEL, J + 1>(c, push<W, K, SEL, J>(c, st, v), bst);
                 }
             }
             return n;
@@ -398,36 +514,34 @@ __device__ __forceinline__ uint32_t descend_range(const Ctx &c, const St<K> &st,
 
 // Items [lo, hi) of depth D (D = 0 only for K = 1).
 template <int W, int K, int SEL, int DMAX>
-__device__ __forceinline__ void run_range(const Ctx &c, uint32_t lo, uint32_t hi, int D, const uint32_t *magic,
-                                          Best &bst) {
+__device__ __forceinline__ void run_range(const Ctx<W> &c, uint32_t lo, uint32_t hi, int D, Best &bst) {
     if constexpr (K == 1) {
         if (lo == 0 && hi > 0) leaf_k1<W, SEL>(c, bst);
     } else {
         uint32_t i = lo;
         while (i < hi) {
             uint32_t dg[kMaxDecode];
-            if (!digits(i, c.nF, D, magic, dg)) break;
-            i += descend_range<W, K, SEL, 0, DMAX>(c, root<K>(c), dg, D, hi - i, bst);
+            if (!digits(i, c.nF, D, dg)) break;
+            i += descend_range<W, K, SEL, 0, DMAX>(c, root<W, K>(c), dg, D, hi - i, bst);
         }
     }
 }
 
-// Per-query context.  Must be called by the whole warp (uses shuffles).
-// s_inc: per-warp (or per-CTA) smem table of inc_F, written by group 0.
+// Per-query context.  Must be called by the whole warp (uses shuffles); it
+// writes this warp's inc_F table.
 template <int W>
-__device__ __forceinline__ Ctx make_ctx(const DevTopo &topo, const SmemTopo &sm, int *s_inc,
-                                        const uint16_t *s_lut, int xs, int4 *s_list, const DevPattern &P,
-                                        uint32_t busy, int selector, int sensitive) {
-    const uint4 *s_cm = sm.cm;
+__device__ __forceinline__ Ctx<W> make_ctx(const DevTopo &topo, const DevPattern &P, int pid, int xs, uint32_t busy,
+                                        int selector, int sensitive) {
     const int lane = threadIdx.x & 31;
-    Ctx c;
+    Ctx<W> c;
     const uint32_t nmask = topo.n >= 32 ? kFull : ((1u << topo.n) - 1u);
     c.F = ~busy & nmask;
     c.nF = __popc(c.F);
     c.b = lane & (W - 1);
-    const int g = lane / W;
-    c.gmask = W == 32 ? kFull : (((1u << W) - 1u) << (g * W));
-    const uint4 mine = s_cm[c.b];
+    c.g = lane / W;
+    c.warp = (int)(threadIdx.x >> 5);
+    c.gmask = W == 32 ? kFull : (((1u << W) - 1u) << (c.g * W));
+    const uint4 mine = sh().cm[c.b];
     c.cm0 = mine.x;
     c.cm1 = mine.y;
     c.cm2 = mine.z;
@@ -437,7 +551,7 @@ __device__ __forceinline__ Ctx make_ctx(const DevTopo &topo, const SmemTopo &sm,
     int incb = 12 * (c.nF - inFb) + 38 * __popc(mine.x & c.F) + 13 * __popc(mine.y & c.F) +
                8 * __popc(mine.z & c.F);
     if (c.b >= topo.n) incb = 0;
-    if (lane < W) s_inc[c.b] = incb;
+    if (lane < W) sh().inc[c.warp][c.b] = incb;
     c.incb = incb;
     // T_F = 1/2 sum_{v in F} inc_F(v)  (reduce within the W-lane group)
     int t = inFb ? incb : 0;
@@ -451,18 +565,9 @@ __device__ __forceinline__ Ctx make_ctx(const DevTopo &topo, const SmemTopo &sm,
     c.clique = P.clique;
     c.eb = P.eb;
     c.m = P.m;
-    c.edge = P.edge;
-    c.mp1 = P.m + 1;
-    c.cm = s_cm;
-    c.inc = s_inc;
-    c.lut = s_lut;
+    c.pid = pid;
     c.xs = xs;
-    c.tw = sm.tw;
-    c.tz = sm.tz;
-    c.twd = sm.twd;
-    c.tzd = sm.tzd;
-    c.tdl = sm.tdl;
-    c.list = s_list + g * W;
+    c.lut = pid * 3 * xs * xs;
     c.laneC = 0;
     if (selector == MAPA_SEL_BASELINE) {
         c.w0 = c.w1 = c.w2 = c.w12 = 0;
@@ -480,6 +585,18 @@ __device__ __forceinline__ Ctx make_ctx(const DevTopo &topo, const SmemTopo &sm,
     }
     const int n12 = c.useU ? (K - 1) : (int)P.dback[K - 1];
     c.leafC = c.w12 * n12 + c.laneC;
+    // inner-scan column of this lane (vertex k-1 on device b, vertex k-2 on v):
+    //   LIN  col[v] = T[v][b] + 31 - v, T = 32 w (edge k-2~k-1 scored) or 0, kNeg invalid
+    //   SENS col[v] = D[v][b], D = census delta (edge k-2~k-1) or 0, + kSent invalid
+    const int sh2 = K >= 2 ? 8 * (K - 2) : 0;
+    const bool eK = K >= 2 && ((((uint32_t)(c.fb >> sh2)) >> (K - 1)) & 1u);
+    const bool dep = K >= 2 && ((((uint32_t)(c.fs >> sh2)) >> (K - 1)) & 1u);
+    const bool sens = selector == MAPA_SEL_PRESERVE && sensitive;
+    const bool eW = c.w12 != 0 && (c.useU || eK);
+    const int *T = sens ? (eK ? (dep ? sh().tsed : sh().tse) : (dep ? sh().ts0d : sh().ts0))
+                        : (eW ? (dep ? sh().twd : sh().tw) : (dep ? sh().tzd : sh().tz));
+#pragma unroll
+    for (int v = 0; v < W; ++v) c.col[v] = T[v * 32 + c.b] + (sens ? 0 : 31 - v);
     __syncwarp();
     return c;
 }
@@ -494,13 +611,17 @@ __device__ __forceinline__ void warp_reduce(unsigned long long &key, unsigned lo
     }
 }
 
-// Topology tables in shared memory (SmemTopo) for Eq. 2 table stride xs.
+// Shared tables for Eq. 2 row stride xs + npats Eq. 2 tables + edge lists.
 // Caller syncs.
-__device__ __forceinline__ void load_topo(const DevTopo &topo, SmemTopo &sm, int xs) {
+template <int MAXP, int LUTCAP>
+__device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int xs) {
+    Shared &s = sh();
+    const DevTopo &topo = tb.topo;
     const int tid = threadIdx.x;
-    if (tid < kMaxN) sm.cm[tid] = make_uint4(topo.cm[tid][0], topo.cm[tid][1], topo.cm[tid][2], topo.cm[tid][3]);
-    if (tid <= kMaxN) sm.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
-    for (int i = tid; i < kMaxN * kMaxN; i += blockDim.x) {
+    if (tid < kMaxN) s.cm[tid] = make_uint4(topo.cm[tid][0], topo.cm[tid][1], topo.cm[tid][2], topo.cm[tid][3]);
+    if (tid <= kMaxN) s.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
+    const int sent = xs * xs;
+    for (int i = tid; i < kNN; i += blockDim.x) {
         const int v = i >> 5, b = i & 31;
         int w = kNeg, d = 0;
         if (v != b && v < topo.n && b < topo.n) {
@@ -509,22 +630,30 @@ __device__ __forceinline__ void load_topo(const DevTopo &topo, SmemTopo &sm, int
             else if ((topo.cm[b][2] >> v) & 1u) { w = 20; d = 1; }
             else w = 12;
         }
-        const int z = w == kNeg ? kNeg : 0;
-        const int wv = w == kNeg ? kNeg : 32 * w;
-        sm.tw[i] = wv;
-        sm.tz[i] = z;
-        sm.twd[i] = v >= b ? kNeg : wv;
-        sm.tzd[i] = v >= b ? kNeg : z;
-        sm.tdl[i] = d;
+        const bool bad = w == kNeg, badd = bad || v >= b;
+        s.tw[i] = bad ? kNeg : 32 * w;
+        s.tz[i] = bad ? kNeg : 0;
+        s.twd[i] = badd ? kNeg : 32 * w;
+        s.tzd[i] = badd ? kNeg : 0;
+        s.twp[i] = bad ? 0 : w;
+        s.tdl[i] = d;
+        s.tse[i] = d + (bad ? sent : 0);
+        s.tsed[i] = d + (badd ? sent : 0);
+        s.ts0[i] = bad ? sent : 0;
+        s.ts0d[i] = badd ? sent : 0;
     }
-}
-
-// Eq. 2 table for the kernels: out[x*xs + y] = (rank(x,y) + 1) * 32 from the
-// host's dense rank table rank[x*(m+1) + y] (x + y <= m); other entries 0.
-__device__ __forceinline__ void load_lut(const uint16_t *rank, int m, int xs, uint16_t *out) {
-    for (int i = threadIdx.x; i < xs * xs; i += blockDim.x) {
-        const int x = i / xs, y = i % xs;
-        out[i] = (x + y <= m) ? (uint16_t)((rank[x * (m + 1) + y] + 1) * 32) : (uint16_t)0;
+    int *lut = sh_lut();
+    for (int p = 0; p < tb.npats; ++p) {
+        const DevPattern &P = tb.pat[p];
+        const uint16_t *rank = tb.lut + P.lut_off;
+        const int m = P.m;
+        for (int i = tid; i < 3 * xs * xs; i += blockDim.x) {
+            const int x = i / xs, y = i % xs;
+            int v = kNeg;
+            if (i < xs * xs) v = (x + y <= m) ? ((int)rank[x * (m + 1) + y] + 1) * 32 : 0;
+            lut[p * 3 * xs * xs + i] = v;
+        }
+        if (tid < 28) s.edge[p][tid] = P.edge[tid];
     }
 }
 
@@ -539,26 +668,13 @@ esa_single(const __grid_constant__ SingleTables tb, int selector, int sensitive,
            int world, int chunk) {
     constexpr int G = 32 / W;
     constexpr int DMAX = (K - 1) < kMaxDecode ? (K - 1) : kMaxDecode;
-    __shared__ SmemTopo s_topo;
-    __shared__ int s_inc[kMaxN];
-    __shared__ uint16_t s_lut[kLutCapSingle];
-    __shared__ uint8_t s_edge[28];
-    __shared__ int4 s_list[kWarps][32];
-    __shared__ unsigned long long s_key[kWarps], s_cnt[kWarps];
-
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const DevPattern &P = tb.pat[0];
-    const int xs = P.m <= 15 ? 16 : 32;
-    load_topo(tb.topo, s_topo, xs);
-    load_lut(tb.lut + P.lut_off, P.m, xs, s_lut);
-    if (tid < 28) s_edge[tid] = P.edge[tid];
-    const uint32_t *s_magic = s_topo.magic;
+    const int xs = tb.xs;
+    load_shared(tb, xs);
     const uint32_t busy = dq->busy;
     __syncthreads();
 
-    Ctx c = make_ctx<W>(tb.topo, s_topo, s_inc, s_lut, xs, s_list[warp], P, busy, selector, sensitive);
-    c.edge = s_edge;
-    __syncthreads();  // s_inc written by every warp with identical values
+    Ctx<W> c = make_ctx<W>(tb.topo, tb.pat[0], 0, xs, busy, selector, sensitive);
 
     const uint32_t nItems = (K <= c.nF) ? perm_count(c.nF, D) : 0u;
     const uint32_t nChunks = (nItems + (uint32_t)chunk - 1u) / (uint32_t)chunk;
@@ -573,19 +689,19 @@ esa_single(const __grid_constant__ SingleTables tb, int selector, int sensitive,
         if (gq >= nChunks) break;
         const uint32_t lo = gq * (uint32_t)chunk + g * per;
         const uint32_t hi = min(lo + per, nItems);
-        if (lo < hi) run_range<W, K, SEL, DMAX>(c, lo, hi, D, s_magic, bst);
+        if (lo < hi) run_range<W, K, SEL, DMAX>(c, lo, hi, D, bst);
         __syncwarp();
     }
     unsigned long long key = bst.key, cnt = bst.cnt;
     warp_reduce(key, cnt);
     if (lane == 0) {
-        s_key[warp] = key;
-        s_cnt[warp] = cnt;
+        sh().key[warp] = key;
+        sh().cnt[warp] = cnt;
     }
     __syncthreads();
     if (warp == 0) {
-        key = lane < kWarps ? s_key[lane] : 0ull;
-        cnt = lane < kWarps ? s_cnt[lane] : 0ull;
+        key = lane < kWarps ? sh().key[lane] : 0ull;
+        cnt = lane < kWarps ? sh().cnt[lane] : 0ull;
         warp_reduce(key, cnt);
         if (lane == 0) {
             if (key) atomicMax(u64p(&rec->key), key);
@@ -598,26 +714,25 @@ esa_single(const __grid_constant__ SingleTables tb, int selector, int sensitive,
 // W slots per query; slot j = the j-th free device as f(0) (items of depth 1);
 // K = 1 queries use slot 0 only (depth 0).
 template <int W, int K, int SEL>
-__device__ __forceinline__ void batch_item(const Ctx &c, uint32_t j, const uint32_t *magic, Best &bst) {
+__device__ __forceinline__ void batch_item(const Ctx<W> &c, uint32_t j, Best &bst) {
     if constexpr (K == 1) {
         if (j == 0) leaf_k1<W, SEL>(c, bst);
     } else {
-        if (j < (uint32_t)c.nF) run_range<W, K, SEL, 1>(c, j, j + 1, 1, magic, bst);
+        if (j < (uint32_t)c.nF) run_range<W, K, SEL, 1>(c, j, j + 1, 1, bst);
     }
 }
 
 template <int W, int SEL>
-__device__ __forceinline__ void batch_dispatch_k(int K, const Ctx &c, uint32_t j, const uint32_t *magic,
-                                                 Best &bst) {
+__device__ __forceinline__ void batch_dispatch_k(int K, const Ctx<W> &c, uint32_t j, Best &bst) {
     switch (K) {
-        case 1: batch_item<W, 1, SEL>(c, j, magic, bst); break;
-        case 2: batch_item<W, 2, SEL>(c, j, magic, bst); break;
-        case 3: batch_item<W, 3, SEL>(c, j, magic, bst); break;
-        case 4: batch_item<W, 4, SEL>(c, j, magic, bst); break;
-        case 5: batch_item<W, 5, SEL>(c, j, magic, bst); break;
-        case 6: batch_item<W, 6, SEL>(c, j, magic, bst); break;
-        case 7: batch_item<W, 7, SEL>(c, j, magic, bst); break;
-        case 8: batch_item<W, 8, SEL>(c, j, magic, bst); break;
+        case 1: batch_item<W, 1, SEL>(c, j, bst); break;
+        case 2: batch_item<W, 2, SEL>(c, j, bst); break;
+        case 3: batch_item<W, 3, SEL>(c, j, bst); break;
+        case 4: batch_item<W, 4, SEL>(c, j, bst); break;
+        case 5: batch_item<W, 5, SEL>(c, j, bst); break;
+        case 6: batch_item<W, 6, SEL>(c, j, bst); break;
+        case 7: batch_item<W, 7, SEL>(c, j, bst); break;
+        case 8: batch_item<W, 8, SEL>(c, j, bst); break;
         default: break;
     }
 }
@@ -629,16 +744,9 @@ __global__ void __launch_bounds__(kBlock, 2)
 esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query *__restrict__ qs,
           mapa_record *__restrict__ res, uint32_t *__restrict__ ctr) {
     constexpr int G = 32 / W;
-    __shared__ SmemTopo s_topo;
-    __shared__ int s_inc[kWarps][kMaxN];
-    __shared__ int4 s_list[kWarps][32];
-    extern __shared__ uint16_t s_lut[];  // npats * xs * xs Eq. 2 tables (dynamic)
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lane = threadIdx.x & 31;
     const int xs = tb.xs;
-    load_topo(tb.topo, s_topo, xs);
-    for (int p = 0; p < tb.npats; ++p) load_lut(tb.lut + tb.pat[p].lut_off, tb.pat[p].m, xs, s_lut + p * xs * xs);
-    const uint32_t *s_magic = s_topo.magic;
+    load_shared(tb, xs);
     __syncthreads();
 
     const unsigned long long nslots = (unsigned long long)nq * W;
@@ -656,14 +764,13 @@ esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query
             continue;
         }
         const DevPattern &P = tb.pat[pid];
-        Ctx c = make_ctx<W>(tb.topo, s_topo, s_inc[warp], s_lut + pid * xs * xs, xs, s_list[warp], P, qu.busy,
-                            qu.selector, qu.sensitive);
+        Ctx<W> c = make_ctx<W>(tb.topo, P, (int)pid, xs, qu.busy, qu.selector, qu.sensitive);
         if (P.k > c.nF) continue;
         const uint32_t j = (uint32_t)(base % W) + g;
         Best bst{0ull, 0u, 0u};
         const bool sens = qu.selector == MAPA_SEL_PRESERVE && qu.sensitive;
-        if (sens) batch_dispatch_k<W, SEL_SENS>(P.k, c, j, s_magic, bst);
-        else batch_dispatch_k<W, SEL_LIN>(P.k, c, j, s_magic, bst);
+        if (sens) batch_dispatch_k<W, SEL_SENS>(P.k, c, j, bst);
+        else batch_dispatch_k<W, SEL_LIN>(P.k, c, j, bst);
         __syncwarp();
         unsigned long long key = bst.key, cnt = bst.cnt;
         warp_reduce(key, cnt);
@@ -676,26 +783,26 @@ esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query
 
 // ---------------------------------------------------------------- trace replay
 template <int W, int K, int SEL>
-__device__ __forceinline__ void trace_items(const Ctx &c, int D, uint32_t nItems, uint32_t gid, uint32_t ngroups,
-                                            const uint32_t *magic, Best &bst) {
+__device__ __forceinline__ void trace_items(const Ctx<W> &c, int D, uint32_t nItems, uint32_t gid, uint32_t ngroups,
+                                            Best &bst) {
     constexpr int DMAX = (K - 1) < 2 ? (K - 1) : 2;
     const uint32_t per = (nItems + ngroups - 1u) / ngroups;
     const uint32_t lo = gid * per, hi = min(lo + per, nItems);
-    if (lo < hi) run_range<W, K, SEL, DMAX>(c, lo, hi, D, magic, bst);
+    if (lo < hi) run_range<W, K, SEL, DMAX>(c, lo, hi, D, bst);
 }
 
 template <int W, int SEL>
-__device__ __forceinline__ void trace_dispatch_k(int K, const Ctx &c, int D, uint32_t nItems, uint32_t gid,
-                                                 uint32_t ngroups, const uint32_t *magic, Best &bst) {
+__device__ __forceinline__ void trace_dispatch_k(int K, const Ctx<W> &c, int D, uint32_t nItems, uint32_t gid,
+                                                 uint32_t ngroups, Best &bst) {
     switch (K) {
-        case 1: trace_items<W, 1, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
-        case 2: trace_items<W, 2, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
-        case 3: trace_items<W, 3, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
-        case 4: trace_items<W, 4, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
-        case 5: trace_items<W, 5, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
-        case 6: trace_items<W, 6, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
-        case 7: trace_items<W, 7, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
-        case 8: trace_items<W, 8, SEL>(c, D, nItems, gid, ngroups, magic, bst); break;
+        case 1: trace_items<W, 1, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 2: trace_items<W, 2, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 3: trace_items<W, 3, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 4: trace_items<W, 4, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 5: trace_items<W, 5, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 6: trace_items<W, 6, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 7: trace_items<W, 7, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 8: trace_items<W, 8, SEL>(c, D, nItems, gid, ngroups, bst); break;
         default: break;
     }
 }
@@ -707,20 +814,11 @@ __global__ void __launch_bounds__(kBlock, 1)
 esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op *__restrict__ ops, int njobs,
           const mapa_query *__restrict__ jobs, unsigned long long *__restrict__ keys) {
     constexpr int G = 32 / W;
-    __shared__ SmemTopo s_topo;
-    __shared__ int s_inc[kWarps][kMaxN];
-    __shared__ int4 s_list[kWarps][32];
-    __shared__ unsigned long long s_key[kWarps];
-    __shared__ uint32_t s_busy;
-    extern __shared__ uint16_t s_lut[];  // npats * xs * xs Eq. 2 tables (dynamic)
-
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int t = blockIdx.x;
     const int xs = tb.xs;
-    load_topo(tb.topo, s_topo, xs);
-    for (int p = 0; p < tb.npats; ++p) load_lut(tb.lut + tb.pat[p].lut_off, tb.pat[p].m, xs, s_lut + p * xs * xs);
-    const uint32_t *s_magic = s_topo.magic;
-    if (tid == 0) s_busy = 0u;
+    load_shared(tb, xs);
+    if (tid == 0) sh().busy = 0u;
     __syncthreads();
     const mapa_trace_op *op = ops + (long long)t * nops;
     const mapa_query *jb = jobs + (long long)t * njobs;
@@ -732,34 +830,34 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
         const mapa_query qu = jb[cur.job];
         const uint32_t pid = qu.pattern;
         const bool okp = pid < (uint32_t)tb.npats && key_fits(W, tb.pat[pid < (uint32_t)tb.npats ? pid : 0]);
-        const DevPattern &P = tb.pat[okp ? pid : 0];
+        const int ep = okp ? (int)pid : 0;
+        const DevPattern &P = tb.pat[ep];
         if (cur.op == 0) {
-            const uint32_t busy = s_busy;
-            Ctx c = make_ctx<W>(tb.topo, s_topo, s_inc[warp], s_lut + (okp ? pid : 0) * xs * xs, xs, s_list[warp], P,
-                                busy, qu.selector, qu.sensitive);
+            const uint32_t busy = sh().busy;
+            Ctx<W> c = make_ctx<W>(tb.topo, P, ep, xs, busy, qu.selector, qu.sensitive);
             Best bst{0ull, 0u, 0u};
             if (okp && P.k <= c.nF) {
                 const int D = (P.k - 1) < 2 ? (P.k - 1) : 2;
                 const uint32_t nItems = perm_count(c.nF, D);
                 const bool sens = qu.selector == MAPA_SEL_PRESERVE && qu.sensitive;
-                if (sens) trace_dispatch_k<W, SEL_SENS>(P.k, c, D, nItems, gid, kWarps * G, s_magic, bst);
-                else trace_dispatch_k<W, SEL_LIN>(P.k, c, D, nItems, gid, kWarps * G, s_magic, bst);
+                if (sens) trace_dispatch_k<W, SEL_SENS>(P.k, c, D, nItems, gid, kWarps * G, bst);
+                else trace_dispatch_k<W, SEL_LIN>(P.k, c, D, nItems, gid, kWarps * G, bst);
             }
             __syncwarp();
             unsigned long long key = bst.key, cnt = bst.cnt;
             warp_reduce(key, cnt);
-            if (lane == 0) s_key[warp] = key;
+            if (lane == 0) sh().key[warp] = key;
             __syncthreads();
             if (tid == 0) {
                 unsigned long long best = 0;
-                for (int w = 0; w < kWarps; ++w) best = s_key[w] > best ? s_key[w] : best;
+                for (int w = 0; w < kWarps; ++w) best = sh().key[w] > best ? sh().key[w] : best;
                 ky[cur.job] = best;
-                if (best) s_busy = busy | (__brev((uint32_t)(best >> P.eb) & wmask) >> (32 - W));
+                if (best) sh().busy = busy | (__brev((uint32_t)(best >> P.eb) & wmask) >> (32 - W));
             }
         } else {
             if (tid == 0) {
                 const unsigned long long kk = ky[cur.job];
-                s_busy &= ~(__brev((uint32_t)(kk >> P.eb) & wmask) >> (32 - W));
+                sh().busy &= ~(__brev((uint32_t)(kk >> P.eb) & wmask) >> (32 - W));
             }
         }
         __syncthreads();
@@ -767,10 +865,23 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
 }
 
 // ---------------------------------------------------------------- dispatch tables
+template <int MAXP, int LUTCAP>
+int smem_bytes(const Tables<MAXP, LUTCAP> &tb) {
+    return (int)sizeof(Shared) + tb.npats * 3 * tb.xs * tb.xs * (int)sizeof(int);
+}
+
 template <int W, int K, int SEL>
 int do_launch_single(const SingleTables &tb, int selector, int sensitive, const mapa_query *dq,
                      mapa_record *rec, int D, int rank, int world, int chunk, int grid, cudaStream_t st) {
-    esa_single<W, K, SEL><<<grid, kBlock, 0, st>>>(tb, selector, sensitive, dq, rec, D, rank, world, chunk);
+    const int smem = smem_bytes(tb);
+    static int configured = 0;
+    if (configured < smem) {
+        cudaError_t e = cudaFuncSetAttribute((const void *)esa_single<W, K, SEL>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return (int)e;
+        configured = smem;
+    }
+    esa_single<W, K, SEL><<<grid, kBlock, smem, st>>>(tb, selector, sensitive, dq, rec, D, rank, world, chunk);
     return (int)cudaGetLastError();
 }
 
@@ -807,6 +918,10 @@ SingleFn pick_single(int W, int K, int sens) {
 template <int W, int K, int SEL>
 const void *single_ptr() { return (const void *)esa_single<W, K, SEL>; }
 
+int set_smem(const void *f, int bytes) {
+    return (int)cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
 }  // namespace
 
 int launch_single(const SingleTables &tb, int selector, int sensitive, const mapa_query *d_query,
@@ -821,11 +936,21 @@ int launch_single(const SingleTables &tb, int selector, int sensitive, const map
 int launch_batch(const MultiTables &tb, int64_t nq, const mapa_query *d_queries, mapa_record *d_results,
                  uint32_t *d_ctr, int grid, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
-    const int dyn = tb.npats * tb.xs * tb.xs * (int)sizeof(uint16_t);
+    const int smem = smem_bytes(tb);
+    int err = 0;
     switch (tb.topo.width) {
-        case 8: esa_batch<8><<<grid, kBlock, dyn, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr); break;
-        case 16: esa_batch<16><<<grid, kBlock, dyn, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr); break;
-        case 32: esa_batch<32><<<grid, kBlock, dyn, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr); break;
+        case 8:
+            if ((err = set_smem((const void *)esa_batch<8>, smem))) return err;
+            esa_batch<8><<<grid, kBlock, smem, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr);
+            break;
+        case 16:
+            if ((err = set_smem((const void *)esa_batch<16>, smem))) return err;
+            esa_batch<16><<<grid, kBlock, smem, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr);
+            break;
+        case 32:
+            if ((err = set_smem((const void *)esa_batch<32>, smem))) return err;
+            esa_batch<32><<<grid, kBlock, smem, st>>>(tb, (long long)nq, d_queries, d_results, d_ctr);
+            break;
         default: return (int)cudaErrorInvalidValue;
     }
     return (int)cudaGetLastError();
@@ -835,11 +960,21 @@ int launch_trace(const MultiTables &tb, int ntraces, int nops, const mapa_trace_
                  const mapa_query *d_jobs, uint64_t *d_keys, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     unsigned long long *k = reinterpret_cast<unsigned long long *>(d_keys);
-    const int dyn = tb.npats * tb.xs * tb.xs * (int)sizeof(uint16_t);
+    const int smem = smem_bytes(tb);
+    int err = 0;
     switch (tb.topo.width) {
-        case 8: esa_trace<8><<<ntraces, kBlock, dyn, st>>>(tb, nops, d_ops, njobs, d_jobs, k); break;
-        case 16: esa_trace<16><<<ntraces, kBlock, dyn, st>>>(tb, nops, d_ops, njobs, d_jobs, k); break;
-        case 32: esa_trace<32><<<ntraces, kBlock, dyn, st>>>(tb, nops, d_ops, njobs, d_jobs, k); break;
+        case 8:
+            if ((err = set_smem((const void *)esa_trace<8>, smem))) return err;
+            esa_trace<8><<<ntraces, kBlock, smem, st>>>(tb, nops, d_ops, njobs, d_jobs, k);
+            break;
+        case 16:
+            if ((err = set_smem((const void *)esa_trace<16>, smem))) return err;
+            esa_trace<16><<<ntraces, kBlock, smem, st>>>(tb, nops, d_ops, njobs, d_jobs, k);
+            break;
+        case 32:
+            if ((err = set_smem((const void *)esa_trace<32>, smem))) return err;
+            esa_trace<32><<<ntraces, kBlock, smem, st>>>(tb, nops, d_ops, njobs, d_jobs, k);
+            break;
         default: return (int)cudaErrorInvalidValue;
     }
     return (int)cudaGetLastError();
@@ -854,7 +989,7 @@ int device_sm_count() {
 
 namespace {
 template <int W>
-int occ_single(int K, int sens) {
+int occ_single(int K, int sens, int smem) {
     const void *f = nullptr;
 #define MAPA_OCC_CASE(KK)                                                        \
     case KK:                                                                     \
@@ -866,35 +1001,27 @@ int occ_single(int K, int sens) {
     }
 #undef MAPA_OCC_CASE
     int nb = 0;
-    if (!f || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kBlock, 0) != cudaSuccess) return 1;
+    if (!f || set_smem(f, smem) != 0) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kBlock, smem) != cudaSuccess) return 1;
     return nb > 0 ? nb : 1;
 }
 }  // namespace
 
-int max_blocks_per_sm_single(int width, int k, int sens) {
-    if (width == 8) return occ_single<8>(k, sens);
-    if (width == 16) return occ_single<16>(k, sens);
-    return occ_single<32>(k, sens);
+int max_blocks_per_sm_single(int width, int k, int sens, int xs) {
+    const int smem = (int)sizeof(Shared) + 3 * xs * xs * (int)sizeof(int);
+    if (width == 8) return occ_single<8>(k, sens, smem);
+    if (width == 16) return occ_single<16>(k, sens, smem);
+    return occ_single<32>(k, sens, smem);
 }
 
-int max_blocks_per_sm_batch(int width, int dyn_smem) {
+int max_blocks_per_sm_batch(int width, int npats, int xs) {
+    const int smem = (int)sizeof(Shared) + npats * 3 * xs * xs * (int)sizeof(int);
+    const void *f = width == 8 ? (const void *)esa_batch<8>
+                  : width == 16 ? (const void *)esa_batch<16> : (const void *)esa_batch<32>;
     int nb = 0;
-    cudaError_t e = cudaErrorInvalidValue;
-    if (width == 8) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, esa_batch<8>, kBlock, dyn_smem);
-    if (width == 16) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, esa_batch<16>, kBlock, dyn_smem);
-    if (width == 32) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, esa_batch<32>, kBlock, dyn_smem);
-    return (e == cudaSuccess && nb > 0) ? nb : 1;
-}
-
-int set_dynamic_smem(int bytes) {
-    // batch / trace kernels keep npats Eq. 2 tables in dynamic shared memory
-    const void *fs[6] = {(const void *)esa_batch<8>, (const void *)esa_batch<16>, (const void *)esa_batch<32>,
-                         (const void *)esa_trace<8>, (const void *)esa_trace<16>, (const void *)esa_trace<32>};
-    for (const void *f : fs) {
-        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-        if (e != cudaSuccess) return (int)e;
-    }
-    return 0;
+    if (set_smem(f, smem) != 0) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kBlock, smem) != cudaSuccess) return 1;
+    return nb > 0 ? nb : 1;
 }
 
 const char *cuda_error_string(int err) { return cudaGetErrorString((cudaError_t)err); }

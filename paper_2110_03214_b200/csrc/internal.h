@@ -74,9 +74,8 @@ int launch_batch(const MultiTables &tb, int64_t nq, const mapa_query *d_queries,
 int launch_trace(const MultiTables &tb, int ntraces, int nops, const mapa_trace_op *d_ops, int njobs,
                  const mapa_query *d_jobs, uint64_t *d_keys, void *stream);
 int device_sm_count();
-int max_blocks_per_sm_single(int width, int k, int sens);
-int max_blocks_per_sm_batch(int width, int dyn_smem);
-int set_dynamic_smem(int bytes);
+int max_blocks_per_sm_single(int width, int k, int sens, int xs);
+int max_blocks_per_sm_batch(int width, int npats, int xs);
 const char *cuda_error_string(int err);
 
 }  // namespace mapa

@@ -337,7 +337,7 @@ Plan plan_single(const mapa_topology *t, const mapa_pattern *p, int sensk, int n
     const int W = t->width, G = 32 / W, k = p->k;
     int sm = device_sm_count();
     if (sm <= 0) sm = 148;
-    const int occ = max_blocks_per_sm_single(W, k, sensk);
+    const int occ = max_blocks_per_sm_single(W, k, sensk, p->m <= 15 ? 16 : 32);
     const uint64_t resident_warps = (uint64_t)sm * occ * 8;
     const uint64_t target = 32ull * resident_warps * G * (uint64_t)world;
     int dmax = k <= 1 ? 0 : std::max(1, std::min(k - 2, 4));
@@ -605,6 +605,7 @@ mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int
     std::memset(&tb, 0, sizeof(tb));
     fill_devtopo(t, tb.topo);
     tb.npats = 1;
+    tb.xs = p->m <= 15 ? 16 : 32;
     fill_devpattern(p, (flags & MAPA_F_RAW) != 0, 0, tb.pat[0]);
     std::memcpy(tb.lut, p->lut.data(), p->lut.size() * sizeof(uint16_t));
     int err = (int)cudaMemsetAsync(d_record, 0, sizeof(mapa_record), (cudaStream_t)stream);
@@ -691,11 +692,9 @@ mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *cons
     if (nq == 0) return MAPA_OK;
     if ((err = (int)cudaMemsetAsync(d_results, 0, (size_t)nq * sizeof(mapa_record), st))) return cuda_fail(err, "memset");
     if ((err = (int)cudaMemsetAsync(d_scratch, 0, 64, st))) return cuda_fail(err, "memset");
-    const int dyn = tbp->npats * tbp->xs * tbp->xs * 2;
-    if ((err = set_dynamic_smem(dyn))) return cuda_fail(err, "cudaFuncSetAttribute");
     int sm = device_sm_count();
     if (sm <= 0) sm = 148;
-    const int grid = sm * max_blocks_per_sm_batch(t->width, dyn);
+    const int grid = sm * max_blocks_per_sm_batch(t->width, tbp->npats, tbp->xs);
     err = launch_batch(*tbp, nq, d_queries, d_results, (uint32_t *)d_scratch, grid, stream);
     if (err) return cuda_fail(err, "esa_batch launch");
     return MAPA_OK;
@@ -711,9 +710,7 @@ mapa_status mapa_trace_replay(const mapa_topology *t, const mapa_pattern *const 
     if (!tbp) tbp = new MultiTables();
     mapa_status s = build_multi(t, pats, npats, flags, tbp);
     if (s != MAPA_OK) return s;
-    int err = set_dynamic_smem(tbp->npats * tbp->xs * tbp->xs * 2);
-    if (err) return cuda_fail(err, "cudaFuncSetAttribute");
-    err = (int)cudaMemsetAsync(d_keys, 0, (size_t)ntraces * njobs * sizeof(uint64_t), (cudaStream_t)stream);
+    int err = (int)cudaMemsetAsync(d_keys, 0, (size_t)ntraces * njobs * sizeof(uint64_t), (cudaStream_t)stream);
     if (err) return cuda_fail(err, "memset");
     err = launch_trace(*tbp, ntraces, nops, d_ops, njobs, d_jobs, d_keys, stream);
     if (err) return cuda_fail(err, "esa_trace launch");
