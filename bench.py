@@ -41,15 +41,14 @@ METRIC = "candidate embeddings scored/sec and allocations/sec at 1/2/4/8 B200"
 K_PAT, M_PAT = 6, 15
 RAW_PER_QUERY = math.perm(32, K_PAT)                    # 652,458,240
 SELECTORS = ((0, False, "greedy"), (1, True, "preserve_sensitive"), (1, False, "preserve_insensitive"))
-# Algorithmic integer work per scored embedding: the
-# incremental leaf work of any DFS enumerator, whose prefix (vertices 0..k-2)
-# is shared by its leaves: the d edges from the last vertex to the prefix
-# (d = |back(k-1)| = 5 for full-6; Eq. 3 uses all k-1 = 5 placed devices)
-# cost d weight/class lookups + d adds, then 1 compare + 1 select for the
-# argmax; Eq. 2 adds the rank-table lookup.  (The unamortised SURVEY 8(d)
-# figure, ~2m = 30 ops, is reported beside it as "ops_unamortised".)
-D_LAST = K_PAT - 1
-ALG_OPS = {"greedy": 2 * D_LAST + 2, "preserve_sensitive": 2 * D_LAST + 3, "preserve_insensitive": 2 * D_LAST + 2}
+# Algorithmic integer work per scored embedding: with
+# the enumeration tree sharing every partial sum of an embedding's prefix, what
+# remains per embedding is to complete its score from two shared partials (1
+# add) and compare it (1 max); Eq. 2 also reads the rank table (+1).  The
+# kernel fuses add+max (VIADDMNMX), so these counts are reachable.  SURVEY
+# 8(d)'s unamortised figure (~2m = 30-43 ops: every edge weight re-read) is
+# reported beside it as "ops_unamortised" for context.
+ALG_OPS = {"greedy": 2, "preserve_sensitive": 3, "preserve_insensitive": 2}
 ALG_OPS_UNAMORTISED = {"greedy": 2 * M_PAT, "preserve_sensitive": 2 * M_PAT + 2,
                        "preserve_insensitive": 2 * (K_PAT * (K_PAT - 1) // 2 + K_PAT) + 1}
 # Reference-arm / cpu_baseline sample: the C4 subsets whose smallest device is
@@ -321,8 +320,9 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "Gop/s", "frac": achieved / peak,
                          "traffic": traffic,
                          "ops_per_embedding": ALG_OPS[dom], "ops_unamortised": ALG_OPS_UNAMORTISED[dom],
-                         "note": f"incremental leaf work {ALG_OPS[dom]} int ops/embedding (DESIGN.md Roofline); peak = "
-                                 f"148 SM x 128 int32 lane-ops/clk (issue) x {max_mhz:.0f} MHz (measured max SM clock)"},
+                         "note": f"{ALG_OPS[dom]} int ops per embedding (complete score from shared partials + compare; "
+                                 f"DESIGN.md Roofline); peak = 148 SM x 128 int32 lane-ops/clk (issue) x {max_mhz:.0f} MHz "
+                                 f"(measured max SM clock)"},
             "cpu_baseline": cpu,
             "e2e": {"value": emb_step * e2e_steps / e2e_s, "unit": "embeddings/s",
                     "h2d_bytes_per_step": 16 * len(SELECTORS),

@@ -89,6 +89,9 @@ struct Shared {
     uint32_t pad[3];
 };
 
+// Single-query kernels: Shared + one Eq. 2 table of 3 xs^2 ints, xs <= 40.
+constexpr int kSmemSingleMax = (int)sizeof(Shared) + 3 * 40 * 40 * (int)sizeof(int);
+
 extern __shared__ __align__(16) unsigned char g_smem[];
 __device__ __forceinline__ Shared &sh() { return *reinterpret_cast<Shared *>(g_smem); }
 __device__ __forceinline__ int *sh_lut() { return reinterpret_cast<int *>(g_smem + sizeof(Shared)); }
@@ -191,6 +194,7 @@ __device__ __forceinline__ void consider(const Ctx<W> &c, Best &bst, uint32_t S,
         const uint32_t sb_new = __brev(S) >> (32 - W);
         const uint32_t sb_old = (uint32_t)(bst.key >> c.eb) & (W >= 32 ? kFull : ((1u << W) - 1u));
         if (sb_new < sb_old) return;
+        if (sb_new == sb_old && c.clique) return;  // same set, clique: identical key
     }
     const unsigned long long key = make_key<W, K>(S, fpack, (uint32_t)c.b, s, c.clique, c.eb, c.m, c.pid);
     if (key > bst.key) {
@@ -266,16 +270,17 @@ __device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2
     const int4 *t4 = reinterpret_cast<const int4 *>(tab);
     int best = 0;
     if constexpr (SEL == SEL_LIN) {
+        // four independent fused add-max chains (VIADDMNMX), base added once
+        int b0 = kNeg, b1 = kNeg, b2 = kNeg, b3 = kNeg;
 #pragma unroll
         for (int q = 0; q < W / 4; ++q) {
             const int4 e = t4[q];
-            const int r0 = base + e.x + c.col[4 * q + 0];
-            const int r1 = base + e.y + c.col[4 * q + 1];
-            const int r2 = base + e.z + c.col[4 * q + 2];
-            const int r3 = base + e.w + c.col[4 * q + 3];
-            best = max(best, max(r0, r1));
-            best = max(best, max(r2, r3));
+            b0 = max(b0, e.x + c.col[4 * q + 0]);
+            b1 = max(b1, e.y + c.col[4 * q + 1]);
+            b2 = max(b2, e.z + c.col[4 * q + 2]);
+            b3 = max(b3, e.w + c.col[4 * q + 3]);
         }
+        best = max(0, max(max(b0, b1), max(b2, b3)) + base);
     } else {
         const int *lut = sh_lut() + c.lut;
 #pragma unroll
@@ -874,13 +879,16 @@ template <int W, int K, int SEL>
 int do_launch_single(const SingleTables &tb, int selector, int sensitive, const mapa_query *dq,
                      mapa_record *rec, int D, int rank, int world, int chunk, int grid, cudaStream_t st) {
     const int smem = smem_bytes(tb);
-    static int configured = 0;
-    if (configured < smem) {
+    // the attribute is always set to the fixed upper bound (see kSmemSingleMax),
+    // so the occupancy query and every launch agree
+    static bool configured = false;
+    if (!configured) {
         cudaError_t e = cudaFuncSetAttribute((const void *)esa_single<W, K, SEL>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSingleMax);
         if (e != cudaSuccess) return (int)e;
-        configured = smem;
+        configured = true;
     }
+    if (smem > kSmemSingleMax) return (int)cudaErrorInvalidValue;
     esa_single<W, K, SEL><<<grid, kBlock, smem, st>>>(tb, selector, sensitive, dq, rec, D, rank, world, chunk);
     return (int)cudaGetLastError();
 }
@@ -981,9 +989,13 @@ int launch_trace(const MultiTables &tb, int ntraces, int nops, const mapa_trace_
 }
 
 int device_sm_count() {
+    // cached per device (host launch path latency: no attribute query per call)
+    static int cached[64] = {0};
     int dev = 0, n = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (dev >= 0 && dev < 64 && cached[dev]) return cached[dev];
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    if (dev >= 0 && dev < 64) cached[dev] = n;
     return n;
 }
 
@@ -1001,17 +1013,25 @@ int occ_single(int K, int sens, int smem) {
     }
 #undef MAPA_OCC_CASE
     int nb = 0;
-    if (!f || set_smem(f, smem) != 0) return 1;
+    if (!f || set_smem(f, kSmemSingleMax) != 0) return 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kBlock, smem) != cudaSuccess) return 1;
     return nb > 0 ? nb : 1;
 }
 }  // namespace
 
 int max_blocks_per_sm_single(int width, int k, int sens, int xs) {
+    // cached: (width, k, sens, xs) -> blocks per SM (same device model per process)
+    static int cache[3][9][2][48] = {};
+    const int wi = width == 8 ? 0 : (width == 16 ? 1 : 2), xi = xs < 48 ? xs : 0;
+    int &slot = cache[wi][k >= 1 && k <= 8 ? k : 0][sens ? 1 : 0][xi];
+    if (slot) return slot;
     const int smem = (int)sizeof(Shared) + 3 * xs * xs * (int)sizeof(int);
-    if (width == 8) return occ_single<8>(k, sens, smem);
-    if (width == 16) return occ_single<16>(k, sens, smem);
-    return occ_single<32>(k, sens, smem);
+    int r;
+    if (width == 8) r = occ_single<8>(k, sens, smem);
+    else if (width == 16) r = occ_single<16>(k, sens, smem);
+    else r = occ_single<32>(k, sens, smem);
+    slot = r;
+    return r;
 }
 
 int max_blocks_per_sm_batch(int width, int npats, int xs) {

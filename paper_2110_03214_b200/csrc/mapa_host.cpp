@@ -323,6 +323,22 @@ uint64_t perm_count(int n, int d) {
     return r;
 }
 
+// Row stride of the device Eq. 2 table (index x*xs + y, x, y <= m): the
+// smallest xs >= m+1 such that lanes whose census differs by a small
+// (dx, dy) rarely hit the same shared-memory bank (32 banks of 4 B):
+// minimises #{(dx, dy) != 0, |dx|,|dy| <= 5 : 32 | xs*dx + dy}.
+int pick_xs(int m) {
+    int best = m + 1, bestc = 1 << 30;
+    for (int xs = m + 1; xs <= std::max(m + 1, 40); ++xs) {
+        int cnt = 0;
+        for (int dx = -5; dx <= 5; ++dx)
+            for (int dy = -5; dy <= 5; ++dy)
+                if ((dx || dy) && ((xs * dx + dy) % 32 + 32) % 32 == 0) ++cnt;
+        if (cnt < bestc) { bestc = cnt; best = xs; }
+    }
+    return best;
+}
+
 mapa_status cuda_fail(int err, const char *what) {
     return fail(MAPA_E_CUDA, std::string(what) + ": " + cuda_error_string(err));
 }
@@ -337,7 +353,7 @@ Plan plan_single(const mapa_topology *t, const mapa_pattern *p, int sensk, int n
     const int W = t->width, G = 32 / W, k = p->k;
     int sm = device_sm_count();
     if (sm <= 0) sm = 148;
-    const int occ = max_blocks_per_sm_single(W, k, sensk, p->m <= 15 ? 16 : 32);
+    const int occ = max_blocks_per_sm_single(W, k, sensk, pick_xs(p->m));
     const uint64_t resident_warps = (uint64_t)sm * occ * 8;
     const uint64_t target = 32ull * resident_warps * G * (uint64_t)world;
     int dmax = k <= 1 ? 0 : std::max(1, std::min(k - 2, 4));
@@ -450,9 +466,10 @@ mapa_status build_multi(const mapa_topology *t, const mapa_pattern *const *pats,
     std::memset(tb, 0, sizeof(*tb));
     fill_devtopo(t, tb->topo);
     tb->npats = npats;
-    tb->xs = 16;
+    int mmax = 0;
     for (int i = 0; i < npats; ++i)
-        if (pats[i] && pats[i]->m > 15) tb->xs = 32;
+        if (pats[i]) mmax = std::max(mmax, pats[i]->m);
+    tb->xs = pick_xs(mmax);
     int off = 0;
     for (int i = 0; i < npats; ++i) {
         if (!pats[i]) return fail(MAPA_E_INVALID_ARG, "null pattern");
@@ -605,7 +622,7 @@ mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int
     std::memset(&tb, 0, sizeof(tb));
     fill_devtopo(t, tb.topo);
     tb.npats = 1;
-    tb.xs = p->m <= 15 ? 16 : 32;
+    tb.xs = pick_xs(p->m);
     fill_devpattern(p, (flags & MAPA_F_RAW) != 0, 0, tb.pat[0]);
     std::memcpy(tb.lut, p->lut.data(), p->lut.size() * sizeof(uint16_t));
     int err = (int)cudaMemsetAsync(d_record, 0, sizeof(mapa_record), (cudaStream_t)stream);
