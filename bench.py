@@ -180,6 +180,8 @@ def main():
     ap.add_argument("--impl", default="mapa", choices=["mapa", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--config", default="c4", choices=["c4", "c1", "c2", "c3", "c5"],
+                    help="c4 = the headline workload (default); c1/c2/c3/c5 measure the other SURVEY 8(d) configs")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "mapa" and not args.no_cpu_baseline:
         args.warmup = 3
@@ -194,12 +196,43 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    # MAPA_BENCH_BACKEND=gloo lets several ranks share one GPU (tests of this
+    # script's multi-rank logic); production runs use NCCL over NVLink.
+    backend = os.environ.get("MAPA_BENCH_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
+
+    def all_gather_dev(out, inp):
+        if backend == "nccl":
+            dist.all_gather_into_tensor(out, inp)
+        else:
+            parts = [torch.empty_like(inp, device="cpu") for _ in range(world)]
+            dist.all_gather(parts, inp.cpu())
+            out.copy_(torch.cat(parts).view_as(out))
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    if args.config != "c4":
+        from bench_configs import run_config
+        line = run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks)
+        if rank == 0 and line is not None:
+            print(json.dumps(line), flush=True)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
 
     topo = mp.Topology(text=W.het32_text())
     pat = mp.Pattern.make("full", K_PAT)
@@ -222,7 +255,7 @@ def main():
                 b.record(stream)
                 kev[name].append((a, b))
         if world > 1:
-            dist.all_gather_into_tensor(gath.view(world, -1), recs.view(-1))
+            all_gather_dev(gath.view(world, -1), recs.view(-1))
 
     for _ in range(args.warmup):
         step(False)
@@ -257,10 +290,7 @@ def main():
     sampler.mark("t1")
     dev_ms = sum(a.elapsed_time(b) for a, b in steps_ev)
     kern_ms = {n: sum(a.elapsed_time(b) for a, b in v) / len(v) for n, v in kev.items()}
-    t = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_ms = float(t.item())
+    dev_ms = max_over_ranks(dev_ms)
 
     # ---- e2e through the public API (host buffers, copies inside the region)
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 20))
@@ -276,10 +306,7 @@ def main():
                 d = md.allocate_sharded(topo, pat, sel, sens, busy, raw=True)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - w0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_s = float(te.item())
+    e2e_s = max_over_ranks(e2e_s)
     sampler.stop()
 
     if rank == 0:

@@ -71,9 +71,9 @@ def combine_records(rec: torch.Tensor, group=None) -> Record:
     if dist.get_backend(group) == "nccl":
         out = torch.empty((world, 4), dtype=torch.int64, device=rec.device)
         dist.all_gather_into_tensor(out, rec.reshape(4), group=group)
-    else:  # gloo (CPU tests of the multi-rank path)
-        parts = [torch.empty(4, dtype=torch.int64, device=rec.device) for _ in range(world)]
-        dist.all_gather(parts, rec.reshape(4), group=group)
+    else:  # gloo (CPU tests of the multi-rank path): host tensors
+        parts = [torch.empty(4, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(parts, rec.reshape(4).cpu(), group=group)
         out = torch.stack(parts)
     return reduce_records(records_from_tensor(out))
 

@@ -61,7 +61,7 @@ def launches(path):
         name = r[hdr.index("Kernel Name")]
         unit = r[hdr.index("Metric Unit")]
         v = float(r[hdr.index("Metric Value")].replace(",", ""))
-        v_us = v / 1e3 if unit == "nsecond" else (v * 1e3 if unit == "msecond" else v)
+        v_us = v / 1e3 if unit in ("nsecond", "ns") else (v * 1e3 if unit in ("msecond", "ms") else v)
         a = agg.setdefault(name, [0, 0.0])
         a[0] += 1
         a[1] += v_us
