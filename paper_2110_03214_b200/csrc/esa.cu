@@ -131,8 +131,9 @@ struct St {
 
 struct Best {
     unsigned long long key;
-    uint32_t bs;
-    uint32_t cnt;
+    uint32_t bs;   // score of key
+    uint32_t cnt;  // leaves scored
+    int thr;       // (bs + 1) * 32: a scan's packed rank must reach this to matter
 };
 
 __device__ __forceinline__ unsigned long long *u64p(uint64_t *p) {
@@ -200,6 +201,7 @@ __device__ __forceinline__ void consider(const Ctx<W> &c, Best &bst, uint32_t S,
     if (key > bst.key) {
         bst.key = key;
         bst.bs = s;
+        bst.thr = ((int)s + 1) * 32;
     }
 }
 
@@ -326,9 +328,9 @@ __device__ __forceinline__ void inner(const Ctx<W> &c, const St<K> &st, uint32_t
     const uint32_t M = laneok ? (dep ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
     bst.cnt += (uint32_t)__popc(M & cand);
     const int best = scan_dense<W, SEL>(c, cand, t2, base);
-    if (laneok && best >= 32) {
+    if (laneok && best >= bst.thr) {  // best >= 32 and its score >= the lane's best score
         const uint32_t s = (uint32_t)(best >> 5) - 1u;
-        if (s >= bst.bs) {
+        {
             const uint32_t bestv = 31u - (uint32_t)(best & 31);
             unsigned long long fpack = pack_f<K>(st);
             fpack |= (unsigned long long)bestv << (8 * J);
@@ -399,9 +401,9 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
         bst.cnt += (uint32_t)__popc(M & cand2);
         const int base = (SEL == SEL_LIN) ? (A + e3.y + lp + 1) * 32 : A + e3.y + lp;
         const int best = scan_dense<W, SEL>(c, cand2, t2, base);
-        if (laneok && best >= 32) {
+        if (laneok && best >= bst.thr) {  // best >= 32 and its score >= the lane's best score
             const uint32_t s = (uint32_t)(best >> 5) - 1u;
-            if (s >= bst.bs) {
+            {
                 const uint32_t bestv = 31u - (uint32_t)(best & 31);
                 const unsigned long long fpack =
                     fbase | ((unsigned long long)v3 << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
@@ -670,7 +672,7 @@ template <int W, int K, int SEL>
 __global__ void __launch_bounds__(kBlock, 2)
 esa_single(const __grid_constant__ SingleTables tb, int selector, int sensitive,
            const mapa_query *__restrict__ dq, mapa_record *__restrict__ rec, int D, int rank,
-           int world, int chunk) {
+           int world, int stripe) {
     constexpr int G = 32 / W;
     constexpr int DMAX = (K - 1) < kMaxDecode ? (K - 1) : kMaxDecode;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -681,20 +683,42 @@ esa_single(const __grid_constant__ SingleTables tb, int selector, int sensitive,
 
     Ctx<W> c = make_ctx<W>(tb.topo, tb.pat[0], 0, xs, busy, selector, sensitive);
 
-    const uint32_t nItems = (K <= c.nF) ? perm_count(c.nF, D) : 0u;
-    const uint32_t nChunks = (nItems + (uint32_t)chunk - 1u) / (uint32_t)chunk;
-    const uint32_t per = (uint32_t)chunk / G;  // host makes chunk a multiple of G
-    Best bst{0ull, 0u, 0u};
+    // Rank r owns the stripes s = r, r + world, ... of `stripe` consecutive
+    // items; its local item space is their concatenation.  Warps grab local
+    // chunks by guided self-scheduling (size = remaining / (2 x warps), at
+    // least 2G), so few chunks are decoded and the tail stays short.
+    const uint32_t N = (K <= c.nF) ? perm_count(c.nF, D) : 0u;
+    const uint32_t L = (uint32_t)stripe;
+    const uint32_t nS = (N + L - 1u) / L;
+    const uint32_t myS = nS > (uint32_t)rank ? (nS - (uint32_t)rank + (uint32_t)world - 1u) / (uint32_t)world : 0u;
+    const bool ownLast = nS > 0 && ((nS - 1u) % (uint32_t)world) == (uint32_t)rank;
+    const uint32_t Nloc = myS == 0 ? 0u : (ownLast ? (myS - 1u) * L + (N - (nS - 1u) * L) : myS * L);
+    const uint32_t P = gridDim.x * (uint32_t)kWarps;
+    Best bst{0ull, 0u, 0u, 32};
     const uint32_t g = (uint32_t)(lane / W);
     for (;;) {
-        uint32_t q = 0;
-        if (lane == 0) q = atomicAdd(&rec->ctr, 1u);
-        q = __shfl_sync(kFull, q, 0);
-        const uint32_t gq = q * (uint32_t)world + (uint32_t)rank;
-        if (gq >= nChunks) break;
-        const uint32_t lo = gq * (uint32_t)chunk + g * per;
-        const uint32_t hi = min(lo + per, nItems);
-        if (lo < hi) run_range<W, K, SEL, DMAX>(c, lo, hi, D, bst);
+        uint32_t start = 0, sz = 0;
+        if (lane == 0) {
+            const uint32_t cur = *reinterpret_cast<volatile uint32_t *>(&rec->ctr);
+            const uint32_t rem = cur < Nloc ? Nloc - cur : 0u;
+            sz = max(2u * G, rem / (2u * P));
+            sz = (sz + G - 1u) / G * G;
+            start = atomicAdd(&rec->ctr, sz);
+        }
+        start = __shfl_sync(kFull, start, 0);
+        sz = __shfl_sync(kFull, sz, 0);
+        if (start >= Nloc) break;
+        const uint32_t end = min(start + sz, Nloc);
+        const uint32_t per = (end - start + G - 1u) / G;
+        uint32_t j0 = start + g * per;
+        const uint32_t j1 = min(j0 + per, end);
+        while (j0 < j1) {  // split at stripe boundaries
+            const uint32_t sl = j0 / L;
+            const uint32_t seg = min(j1, (sl + 1u) * L);
+            const uint32_t lo = (sl * (uint32_t)world + (uint32_t)rank) * L + (j0 - sl * L);
+            run_range<W, K, SEL, DMAX>(c, lo, lo + (seg - j0), D, bst);
+            j0 = seg;
+        }
         __syncwarp();
     }
     unsigned long long key = bst.key, cnt = bst.cnt;
@@ -772,7 +796,7 @@ esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query
         Ctx<W> c = make_ctx<W>(tb.topo, P, (int)pid, xs, qu.busy, qu.selector, qu.sensitive);
         if (P.k > c.nF) continue;
         const uint32_t j = (uint32_t)(base % W) + g;
-        Best bst{0ull, 0u, 0u};
+        Best bst{0ull, 0u, 0u, 32};
         const bool sens = qu.selector == MAPA_SEL_PRESERVE && qu.sensitive;
         if (sens) batch_dispatch_k<W, SEL_SENS>(P.k, c, j, bst);
         else batch_dispatch_k<W, SEL_LIN>(P.k, c, j, bst);
@@ -840,7 +864,7 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
         if (cur.op == 0) {
             const uint32_t busy = sh().busy;
             Ctx<W> c = make_ctx<W>(tb.topo, P, ep, xs, busy, qu.selector, qu.sensitive);
-            Best bst{0ull, 0u, 0u};
+            Best bst{0ull, 0u, 0u, 32};
             if (okp && P.k <= c.nF) {
                 const int D = (P.k - 1) < 2 ? (P.k - 1) : 2;
                 const uint32_t nItems = perm_count(c.nF, D);

@@ -355,22 +355,24 @@ Plan plan_single(const mapa_topology *t, const mapa_pattern *p, int sensk, int n
     if (sm <= 0) sm = 148;
     const int occ = max_blocks_per_sm_single(W, k, sensk, pick_xs(p->m));
     const uint64_t resident_warps = (uint64_t)sm * occ * 8;
-    const uint64_t target = 32ull * resident_warps * G * (uint64_t)world;
+    // Items = prefixes of depth D; guided self-scheduling balances ~8 items
+    // per resident W-lane group, and D = k-3 (one inner3 call per item) is
+    // reached whenever that gives enough items.
+    const uint64_t target = 8ull * resident_warps * G * (uint64_t)world;
     int dmax = k <= 1 ? 0 : std::max(1, std::min(k - 2, 4));
     int d = k <= 1 ? 0 : 1;
     while (d < dmax && perm_count(nF, d) < target) ++d;
     pl.depth = d;
     const uint64_t items = nF >= k ? perm_count(nF, d) : 0;
     pl.nlocal = items;
-    // ~16 counter grabs per resident warp; a grab = `chunk` consecutive items
-    // (a multiple of G: each W-lane group walks chunk/G of them as a DFS range)
-    uint64_t chunk = (items + resident_warps * 16 * world - 1) / (resident_warps * 16 * world);
-    chunk = std::max<uint64_t>(chunk, (uint64_t)G);
-    chunk = ((chunk + G - 1) / G) * G;
-    pl.chunk = (int)std::min<uint64_t>(chunk, 1u << 20);
-    const uint64_t nchunks = (items + pl.chunk - 1) / pl.chunk;
-    const uint64_t local = (nchunks + world - 1) / world;
-    const uint64_t blocks = std::max<uint64_t>(1, (local + 7) / 8);
+    // Sharding: `chunk` is the stripe length; rank r owns stripes r, r+world, ...
+    // (64 stripes per rank keep canonical-mode work balanced).  Inside a rank
+    // the kernel hands out chunks by guided self-scheduling.
+    uint64_t stripe = world == 1 ? std::max<uint64_t>(1, items)
+                                 : std::max<uint64_t>(1, (items + 64ull * world - 1) / (64ull * world));
+    pl.chunk = (int)std::min<uint64_t>(stripe, 1u << 30);
+    const uint64_t local = (items + world - 1) / world;
+    const uint64_t blocks = std::max<uint64_t>(1, (local + 8 * 2 * G - 1) / (8 * 2 * G));
     pl.grid = (int)std::min<uint64_t>(blocks, (uint64_t)sm * occ);
     return pl;
 }
