@@ -267,7 +267,7 @@ __device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2
     const bool mine = (cand >> b) & 1u;
     __syncwarp(c.gmask);  // previous readers of the table are done
     if constexpr (SEL == SEL_LIN) tab[b] = mine ? t2 * 32 : kNeg;
-    else tab[b] = mine ? t2 : c.xs * c.xs;
+    else tab[b] = 4 * (mine ? t2 : c.xs * c.xs);  // byte offsets into the Eq. 2 table
     __syncwarp(c.gmask);
     const int4 *t4 = reinterpret_cast<const int4 *>(tab);
     int best = 0;
@@ -284,14 +284,16 @@ __device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2
         }
         best = max(0, max(max(b0, b1), max(b2, b3)) + base);
     } else {
+        // table, column and base are byte offsets: one IADD3 gives the address
         const int *lut = sh_lut() + c.lut;
+        const int b4 = 4 * base;
 #pragma unroll
         for (int q = 0; q < W / 4; ++q) {
             const int4 e = t4[q];
-            const int r0 = lut[base + e.x + c.col[4 * q + 0]] + (31 - (4 * q + 0));
-            const int r1 = lut[base + e.y + c.col[4 * q + 1]] + (31 - (4 * q + 1));
-            const int r2 = lut[base + e.z + c.col[4 * q + 2]] + (31 - (4 * q + 2));
-            const int r3 = lut[base + e.w + c.col[4 * q + 3]] + (31 - (4 * q + 3));
+            const int r0 = lds_off(lut, b4 + e.x + c.col[4 * q + 0]) + (31 - (4 * q + 0));
+            const int r1 = lds_off(lut, b4 + e.y + c.col[4 * q + 1]) + (31 - (4 * q + 1));
+            const int r2 = lds_off(lut, b4 + e.z + c.col[4 * q + 2]) + (31 - (4 * q + 2));
+            const int r3 = lds_off(lut, b4 + e.w + c.col[4 * q + 3]) + (31 - (4 * q + 3));
             best = max(best, max(r0, r1));
             best = max(best, max(r2, r3));
         }
@@ -603,7 +605,7 @@ __device__ __forceinline__ Ctx<W> make_ctx(const DevTopo &topo, const DevPattern
     const int *T = sens ? (eK ? (dep ? sh().tsed : sh().tse) : (dep ? sh().ts0d : sh().ts0))
                         : (eW ? (dep ? sh().twd : sh().tw) : (dep ? sh().tzd : sh().tz));
 #pragma unroll
-    for (int v = 0; v < W; ++v) c.col[v] = T[v * 32 + c.b] + (sens ? 0 : 31 - v);
+    for (int v = 0; v < W; ++v) c.col[v] = sens ? 4 * T[v * 32 + c.b] : T[v * 32 + c.b] + 31 - v;
     __syncwarp();
     return c;
 }
