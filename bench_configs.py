@@ -41,6 +41,26 @@ def _timed(torch, stream, fn, steps, warmup):
     return tot  # ms
 
 
+PEAK_GOPS = 148 * 128 * 1965e6 / 1e9   # int32 issue roofline, measured max SM clock
+OPS_MIX = (2 + 3 + 2) / 3              # ops/embedding, selectors U{Greedy, Sensitive, Insensitive}
+
+
+def _roof(emb_per_s, kernel, note=""):
+    ach = OPS_MIX * emb_per_s / 1e9
+    return {"bound": "alu", "kernel": kernel, "achieved": ach, "peak": PEAK_GOPS, "unit": "Gop/s",
+            "frac": ach / PEAK_GOPS, "traffic": None, "ops_per_embedding": OPS_MIX, "note": note}
+
+
+def _cpu(fn, what):
+    """Time the CPU oracle (oracle/, all host threads) on a bounded sample."""
+    import os
+    t0 = time.perf_counter()
+    n_emb, n_alloc = fn()
+    dt = time.perf_counter() - t0
+    return {"value": n_emb / dt, "unit": "embeddings/s", "allocations_per_s": n_alloc / dt,
+            "cores": os.cpu_count(), "kind": "oracle", "sample": what}
+
+
 def _base(cfg, world, steps, warmup):
     return {"config_id": cfg, "n_gpus": world, "steps": steps, "warmup": warmup, "higher_is_better": True,
             "dtype": "int32", "data": "synthetic"}
@@ -70,6 +90,18 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
         ms = max_over_ranks(ms)
         allocs = B * steps * world / (ms / 1e3)
         line = _base("c1", world, steps, warmup)
+        if rank == 0:
+            from oracle import coracle as co
+            from oracle import mapa_oracle as mo
+            o = mo.builtin("dgx1v")
+            kk, ee = mo.make_pattern("ring", 3)
+
+            def c1_cpu():
+                for i in range(600):
+                    co.allocate(o, 0, kk, ee, [0, 1, 1][i % 3], [0, 1, 0][i % 3], nthreads=1)
+                return 600 * 336, 600
+            line["cpu_baseline"] = _cpu(c1_cpu, "600 C1 allocations, C oracle, 1 thread each")
+        line["roofline"] = _roof(allocs * 336, "esa_batch<8> (C1 queries)")
         line.update(metric="allocations/sec (C1: dgx1v ring-3, all free)", value=allocs, unit="allocations/s",
                     embeddings_per_s=allocs * 336, batch=B, e2e_latency_us_median=lat,
                     config={"workload": "C1 dgx1v ring-3 all free; 1e5 identical queries per batch launch "
@@ -113,6 +145,27 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
                 total_ms += per
         total_ms = max_over_ranks(total_ms)
         line = _base("c2", world, max(1, steps // 10), warmup)
+        if rank == 0:
+            from oracle import coracle as co
+            from oracle import mapa_oracle as mo
+
+            def c2_cpu():
+                jobs = W.c2_jobs(2110, 1000)
+                ops = W.fifo_ops(jobs, 8)
+                patd = {(s_, k_): mo.make_pattern(s_, k_) for s_, k_ in SHAPE_K}
+                emb, free = 0, 8
+                for o_, j in ops:
+                    if o_ == W.OP_ALLOC:
+                        emb += math.perm(free, jobs[j]["k"])
+                        free -= jobs[j]["k"]
+                    else:
+                        free += jobs[j]["k"]
+                mo.replay_trace(mo.builtin("dgx1p"), jobs, ops, patd, "preserve",
+                                allocate_fn=lambda t_, b_, k_, e_, s_, x_: co.allocate(t_, b_, k_, e_, s_, x_, nthreads=1))
+                return emb, 1000
+            line["cpu_baseline"] = _cpu(c2_cpu, "one dgx1p Preserve 1000-job trace replayed by the C oracle")
+        line["roofline"] = _roof(total_emb * world / (total_ms / 1e3), "esa_trace<8> / esa_trace<8> (summit)",
+                                 "dependent ALLOC/RELEASE chain per CTA: latency-bound, not issue-bound")
         line.update(metric="allocations/sec (C2: 1000-job FIFO traces replayed on device)",
                     value=total_allocs * world / (total_ms / 1e3), unit="allocations/s",
                     embeddings_per_s=total_emb * world / (total_ms / 1e3), per_case=res, replicas_per_case=R,
@@ -140,6 +193,21 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
         ms = _timed(torch, stream, run, max(1, steps // 10), warmup)
         ms = max_over_ranks(ms / max(1, steps // 10))
         line = _base("c3", world, max(1, steps // 10), warmup)
+        if rank == 0:
+            from oracle import coracle as co
+            from oracle import mapa_oracle as mo
+            o = mo.builtin("cubemesh16")
+            sample = [q for q in qs if q["k"] <= 6][:24]
+
+            def c3_cpu():
+                emb_ = 0
+                for q in sample:
+                    kk, ee = mo.make_pattern(q["shape"], q["k"])
+                    r = co.allocate(o, q["busy"], kk, ee, q["selector"], q["sensitive"])
+                    emb_ += r["raw"]
+                return emb_, len(sample)
+            line["cpu_baseline"] = _cpu(c3_cpu, f"{len(sample)} C3 queries with k <= 6, C oracle, all host threads")
+        line["roofline"] = _roof(emb * world / (ms / 1e3), "esa_single<16,K,*> (C3 queries)")
         line.update(metric="embeddings/sec (C3: cubemesh16, k in {4,6,8}, random busy)", value=emb * world / (ms / 1e3),
                     unit="embeddings/s", allocations_per_s=len(qs) * world / (ms / 1e3), queries=len(qs) * world,
                     scaling="weak",
@@ -169,6 +237,21 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
             tot_ms += ms
         tot_ms = max_over_ranks(tot_ms)
         line = _base("c5", world, max(1, steps // 10), warmup)
+        if rank == 0:
+            from oracle import coracle as co
+            from oracle import mapa_oracle as mo
+            o32 = mo.parse_topology(W.het32_text())
+            sample = W.c5_queries(32, count=100_000)[:40]
+
+            def c5_cpu():
+                emb_ = 0
+                for q in sample:
+                    kk, ee = mo.make_pattern(q["shape"], q["k"])
+                    r = co.allocate(o32, q["busy"], kk, ee, q["selector"], q["sensitive"])
+                    emb_ += r["raw"]
+                return emb_, len(sample)
+            line["cpu_baseline"] = _cpu(c5_cpu, "first 40 het32 C5 queries, C oracle, all host threads")
+        line["roofline"] = _roof(tot_emb * world / (tot_ms / 1e3), "esa_batch<32> + esa_batch<16>")
         line.update(metric="embeddings/sec (C5: 1e5 batched random queries per topology)",
                     value=tot_emb * world / (tot_ms / 1e3), unit="embeddings/s",
                     allocations_per_s=tot_q * world / (tot_ms / 1e3), per_topology=res, scaling="weak",
