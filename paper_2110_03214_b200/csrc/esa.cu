@@ -54,7 +54,15 @@ constexpr int kWarps = kBlock / 32;
 constexpr int kMaxDecode = 4;
 constexpr int kNN = kMaxN * kMaxN;
 
-enum { SEL_LIN = 0, SEL_SENS = 1 };
+// Compile-time selector: Greedy (Eq. 1), Preserve-insensitive (Eq. 3),
+// Preserve-sensitive (Eq. 2 rank), Baseline (constant score).
+template <int SEL>
+struct SelT {
+    static constexpr bool lin = SEL != SEL_SENS;      // additive score (Eq. 1 / Eq. 3 / 0)
+    static constexpr bool useU = SEL == SEL_INSENS;   // Eq. 3 sums over every placed device
+    static constexpr int wt = SEL == SEL_BASE ? 0 : 1;
+    static constexpr int w0 = 38 * wt, w1 = 13 * wt, w2 = 8 * wt, w12 = 12 * wt;
+};
 
 // Leaves of a k-2 scan are ranked by one int: (score + 1) * 32 + (31 - v).
 // Invalid leaves (vertex k-1 on the device of k-2, a lex-leader violation,
@@ -108,8 +116,6 @@ struct Ctx {
     int incb;                       // inc_F(b)
     int laneC;                      // lane constant of the score (Eq. 3: -inc_F(b))
     int leafC;                      // k = 1 leaf constant
-    int w0, w1, w2, w12;            // 38, 13, 8, 12 (0 for Baseline)
-    int useU;                       // 1: X = all placed devices (Eq. 3), 0: back neighbours
     int acc0;                       // accumulator at the root (T_F for Eq. 3)
     int xs;                         // Eq. 2 table row stride (16 or 32)
     int lut;                        // this pattern's Eq. 2 table offset (ints) in sh_lut()
@@ -210,11 +216,11 @@ __device__ __forceinline__ St<K> push(const Ctx<W> &c, const St<K> &st, uint32_t
     St<K> s = st;
     const uint32_t vb = 1u << v;
     const uint4 t = sh().cm[v];
-    if constexpr (SEL == SEL_LIN) {
-        const uint32_t X = c.useU ? st.U : st.bm[J];
-        const int incv = c.useU ? sh().inc[c.warp][v] : 0;
-        s.acc = st.acc + c.w12 * __popc(X) - incv + c.w0 * __popc(t.x & X) + c.w1 * __popc(t.y & X) +
-                c.w2 * __popc(t.z & X);
+    if constexpr (SelT<SEL>::lin) {
+        const uint32_t X = SelT<SEL>::useU ? st.U : st.bm[J];
+        const int incv = SelT<SEL>::useU ? sh().inc[c.warp][v] : 0;
+        s.acc = st.acc + SelT<SEL>::w12 * __popc(X) - incv + SelT<SEL>::w0 * __popc(t.x & X) + SelT<SEL>::w1 * __popc(t.y & X) +
+                SelT<SEL>::w2 * __popc(t.z & X);
     } else {
         const uint32_t X = st.bm[J];
         s.acc = st.acc + __popc(t.x & X);
@@ -245,7 +251,7 @@ __device__ __forceinline__ unsigned long long pack_f(const St<K> &st) {
 template <int W, int SEL>
 __device__ __forceinline__ void leaf_k1(const Ctx<W> &c, Best &bst) {
     const bool act = (c.F >> c.b) & 1u;
-    const int s = (SEL == SEL_LIN) ? c.acc0 + c.leafC : 0;  // m = 0: census (0,0,0) has rank 0
+    const int s = (SelT<SEL>::lin) ? c.acc0 + c.leafC : 0;  // m = 0: census (0,0,0) has rank 0
     bst.cnt += act ? 1u : 0u;
     if (act && (uint32_t)s >= bst.bs) consider<W, 1>(c, bst, 1u << c.b, 0ull, (uint32_t)s);
 }
@@ -266,12 +272,12 @@ __device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2
     int *tab = sh().wl[c.warp].dense + c.g * W;
     const bool mine = (cand >> b) & 1u;
     __syncwarp(c.gmask);  // previous readers of the table are done
-    if constexpr (SEL == SEL_LIN) tab[b] = mine ? t2 * 32 : kNeg;
+    if constexpr (SelT<SEL>::lin) tab[b] = mine ? t2 * 32 : kNeg;
     else tab[b] = 4 * (mine ? t2 : c.xs * c.xs);  // byte offsets into the Eq. 2 table
     __syncwarp(c.gmask);
     const int4 *t4 = reinterpret_cast<const int4 *>(tab);
     int best = 0;
-    if constexpr (SEL == SEL_LIN) {
+    if constexpr (SelT<SEL>::lin) {
         // four independent fused add-max chains (VIADDMNMX), base added once
         int b0 = kNeg, b1 = kNeg, b2 = kNeg, b3 = kNeg;
 #pragma unroll
@@ -285,6 +291,7 @@ __device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2
         best = max(0, max(max(b0, b1), max(b2, b3)) + base);
     } else {
         // table, column and base are byte offsets: one IADD3 gives the address
+        // table, column and base are byte offsets into the Eq. 2 table
         const int *lut = sh_lut() + c.lut;
         const int b4 = 4 * base;
 #pragma unroll
@@ -312,13 +319,13 @@ __device__ __forceinline__ void inner(const Ctx<W> &c, const St<K> &st, uint32_t
     const bool eK = (fbJ >> (K - 1)) & 1u;   // pattern edge (k-2, k-1)
     const bool dep = (fsJ >> (K - 1)) & 1u;  // lex-leader f(k-2) < f(k-1)
     int t2, base;
-    if constexpr (SEL == SEL_LIN) {
-        const uint32_t X2 = c.useU ? st.U : st.bm[J];
-        const uint32_t X1 = c.useU ? st.U : st.bm[K - 1];
-        t2 = c.w12 * __popc(X2) - (c.useU ? c.incb : 0) + c.w0 * __popc(c.cm0 & X2) + c.w1 * __popc(c.cm1 & X2) +
-             c.w2 * __popc(c.cm2 & X2);
-        const int lp = c.laneC + c.w12 * __popc(X1) + c.w0 * __popc(c.cm0 & X1) + c.w1 * __popc(c.cm1 & X1) +
-                       c.w2 * __popc(c.cm2 & X1);
+    if constexpr (SelT<SEL>::lin) {
+        const uint32_t X2 = SelT<SEL>::useU ? st.U : st.bm[J];
+        const uint32_t X1 = SelT<SEL>::useU ? st.U : st.bm[K - 1];
+        t2 = SelT<SEL>::w12 * __popc(X2) - (SelT<SEL>::useU ? c.incb : 0) + SelT<SEL>::w0 * __popc(c.cm0 & X2) + SelT<SEL>::w1 * __popc(c.cm1 & X2) +
+             SelT<SEL>::w2 * __popc(c.cm2 & X2);
+        const int lp = c.laneC + SelT<SEL>::w12 * __popc(X1) + SelT<SEL>::w0 * __popc(c.cm0 & X1) + SelT<SEL>::w1 * __popc(c.cm1 & X1) +
+                       SelT<SEL>::w2 * __popc(c.cm2 & X1);
         base = (st.acc + lp + 1) * 32;
     } else {
         const uint32_t X2 = st.bm[J], X1 = st.bm[K - 1];
@@ -358,19 +365,19 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
     //   lpb = leaf partial of k-1 on b; v3 then adds m32 w3, m31 w3.
     int t3, t2b, lpb, m32, m31, A;
     const int *wcol;
-    if constexpr (SEL == SEL_LIN) {
-        const uint32_t X3 = c.useU ? st.U : st.bm[J3];
-        const uint32_t X2 = c.useU ? st.U : st.bm[J2];
-        const uint32_t X1 = c.useU ? st.U : st.bm[J1];
-        const int inc = c.useU ? c.incb : 0;
-        t3 = c.w12 * __popc(X3) - inc + c.w0 * __popc(c.cm0 & X3) + c.w1 * __popc(c.cm1 & X3) +
-             c.w2 * __popc(c.cm2 & X3);
-        t2b = c.w12 * __popc(X2) - inc + c.w0 * __popc(c.cm0 & X2) + c.w1 * __popc(c.cm1 & X2) +
-              c.w2 * __popc(c.cm2 & X2);
-        lpb = c.laneC + c.w12 * __popc(X1) + c.w0 * __popc(c.cm0 & X1) + c.w1 * __popc(c.cm1 & X1) +
-              c.w2 * __popc(c.cm2 & X1);
-        m32 = (c.w12 != 0 && (c.useU || e32)) ? 1 : 0;
-        m31 = (c.w12 != 0 && (c.useU || e31)) ? 1 : 0;
+    if constexpr (SelT<SEL>::lin) {
+        const uint32_t X3 = SelT<SEL>::useU ? st.U : st.bm[J3];
+        const uint32_t X2 = SelT<SEL>::useU ? st.U : st.bm[J2];
+        const uint32_t X1 = SelT<SEL>::useU ? st.U : st.bm[J1];
+        const int inc = SelT<SEL>::useU ? c.incb : 0;
+        t3 = SelT<SEL>::w12 * __popc(X3) - inc + SelT<SEL>::w0 * __popc(c.cm0 & X3) + SelT<SEL>::w1 * __popc(c.cm1 & X3) +
+             SelT<SEL>::w2 * __popc(c.cm2 & X3);
+        t2b = SelT<SEL>::w12 * __popc(X2) - inc + SelT<SEL>::w0 * __popc(c.cm0 & X2) + SelT<SEL>::w1 * __popc(c.cm1 & X2) +
+              SelT<SEL>::w2 * __popc(c.cm2 & X2);
+        lpb = c.laneC + SelT<SEL>::w12 * __popc(X1) + SelT<SEL>::w0 * __popc(c.cm0 & X1) + SelT<SEL>::w1 * __popc(c.cm1 & X1) +
+              SelT<SEL>::w2 * __popc(c.cm2 & X1);
+        m32 = (SelT<SEL>::w12 != 0 && (SelT<SEL>::useU || e32)) ? 1 : 0;
+        m31 = (SelT<SEL>::w12 != 0 && (SelT<SEL>::useU || e31)) ? 1 : 0;
         A = st.acc;
         wcol = sh().twp + b;
     } else {
@@ -401,7 +408,7 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
         const bool laneok = okb && b != v3 && (!d31 || b > v3);
         const uint32_t M = laneok ? (d21 ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
         bst.cnt += (uint32_t)__popc(M & cand2);
-        const int base = (SEL == SEL_LIN) ? (A + e3.y + lp + 1) * 32 : A + e3.y + lp;
+        const int base = (SelT<SEL>::lin) ? (A + e3.y + lp + 1) * 32 : A + e3.y + lp;
         const int best = scan_dense<W, SEL>(c, cand2, t2, base);
         if (laneok && best >= bst.thr) {  // best >= 32 and its score >= the lane's best score
             const uint32_t s = (uint32_t)(best >> 5) - 1u;
@@ -577,31 +584,21 @@ __device__ __forceinline__ Ctx<W> make_ctx(const DevTopo &topo, const DevPattern
     c.pid = pid;
     c.xs = xs;
     c.lut = pid * 3 * xs * xs;
-    c.laneC = 0;
-    if (selector == MAPA_SEL_BASELINE) {
-        c.w0 = c.w1 = c.w2 = c.w12 = 0;
-        c.useU = 0;
-        c.acc0 = 0;
-    } else if (selector == MAPA_SEL_PRESERVE && !sensitive) {  // Eq. 3
-        c.w0 = 38; c.w1 = 13; c.w2 = 8; c.w12 = 12;
-        c.useU = 1;
-        c.acc0 = TF;
-        c.laneC = -incb;
-    } else {  // Eq. 1 (or Eq. 2 census for the sensitive kernel)
-        c.w0 = 38; c.w1 = 13; c.w2 = 8; c.w12 = 12;
-        c.useU = 0;
-        c.acc0 = 0;
-    }
-    const int n12 = c.useU ? (K - 1) : (int)P.dback[K - 1];
-    c.leafC = c.w12 * n12 + c.laneC;
+    const int sc = sel_code(selector, sensitive);
+    const bool useU = sc == SEL_INSENS;
+    const int w12 = sc == SEL_BASE ? 0 : 12;
+    c.laneC = useU ? -incb : 0;
+    c.acc0 = useU ? TF : 0;
+    const int n12 = useU ? (K - 1) : (int)P.dback[K - 1];
+    c.leafC = w12 * n12 + c.laneC;
     // inner-scan column of this lane (vertex k-1 on device b, vertex k-2 on v):
     //   LIN  col[v] = T[v][b] + 31 - v, T = 32 w (edge k-2~k-1 scored) or 0, kNeg invalid
     //   SENS col[v] = D[v][b], D = census delta (edge k-2~k-1) or 0, + kSent invalid
     const int sh2 = K >= 2 ? 8 * (K - 2) : 0;
     const bool eK = K >= 2 && ((((uint32_t)(c.fb >> sh2)) >> (K - 1)) & 1u);
     const bool dep = K >= 2 && ((((uint32_t)(c.fs >> sh2)) >> (K - 1)) & 1u);
-    const bool sens = selector == MAPA_SEL_PRESERVE && sensitive;
-    const bool eW = c.w12 != 0 && (c.useU || eK);
+    const bool sens = sc == SEL_SENS;
+    const bool eW = w12 != 0 && (useU || eK);
     const int *T = sens ? (eK ? (dep ? sh().tsed : sh().tse) : (dep ? sh().ts0d : sh().ts0))
                         : (eW ? (dep ? sh().twd : sh().tw) : (dep ? sh().tzd : sh().tz));
 #pragma unroll
@@ -799,9 +796,12 @@ esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query
         if (P.k > c.nF) continue;
         const uint32_t j = (uint32_t)(base % W) + g;
         Best bst{0ull, 0u, 0u, 32};
-        const bool sens = qu.selector == MAPA_SEL_PRESERVE && qu.sensitive;
-        if (sens) batch_dispatch_k<W, SEL_SENS>(P.k, c, j, bst);
-        else batch_dispatch_k<W, SEL_LIN>(P.k, c, j, bst);
+        switch (sel_code(qu.selector, qu.sensitive)) {
+            case SEL_GREEDY: batch_dispatch_k<W, SEL_GREEDY>(P.k, c, j, bst); break;
+            case SEL_INSENS: batch_dispatch_k<W, SEL_INSENS>(P.k, c, j, bst); break;
+            case SEL_SENS: batch_dispatch_k<W, SEL_SENS>(P.k, c, j, bst); break;
+            default: batch_dispatch_k<W, SEL_BASE>(P.k, c, j, bst); break;
+        }
         __syncwarp();
         unsigned long long key = bst.key, cnt = bst.cnt;
         warp_reduce(key, cnt);
@@ -870,9 +870,12 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
             if (okp && P.k <= c.nF) {
                 const int D = (P.k - 1) < 2 ? (P.k - 1) : 2;
                 const uint32_t nItems = perm_count(c.nF, D);
-                const bool sens = qu.selector == MAPA_SEL_PRESERVE && qu.sensitive;
-                if (sens) trace_dispatch_k<W, SEL_SENS>(P.k, c, D, nItems, gid, kWarps * G, bst);
-                else trace_dispatch_k<W, SEL_LIN>(P.k, c, D, nItems, gid, kWarps * G, bst);
+                switch (sel_code(qu.selector, qu.sensitive)) {
+                    case SEL_GREEDY: trace_dispatch_k<W, SEL_GREEDY>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
+                    case SEL_INSENS: trace_dispatch_k<W, SEL_INSENS>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
+                    case SEL_SENS: trace_dispatch_k<W, SEL_SENS>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
+                    default: trace_dispatch_k<W, SEL_BASE>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
+                }
             }
             __syncwarp();
             unsigned long long key = bst.key, cnt = bst.cnt;
@@ -938,8 +941,13 @@ SingleFn pick_k(int K) {
 }
 
 template <int W>
-SingleFn pick_sel(int K, int sens) {
-    return sens ? pick_k<W, SEL_SENS>(K) : pick_k<W, SEL_LIN>(K);
+SingleFn pick_sel(int K, int sc) {
+    switch (sc) {
+        case SEL_GREEDY: return pick_k<W, SEL_GREEDY>(K);
+        case SEL_INSENS: return pick_k<W, SEL_INSENS>(K);
+        case SEL_SENS: return pick_k<W, SEL_SENS>(K);
+        default: return pick_k<W, SEL_BASE>(K);
+    }
 }
 
 SingleFn pick_single(int W, int K, int sens) {
@@ -960,8 +968,7 @@ int set_smem(const void *f, int bytes) {
 
 int launch_single(const SingleTables &tb, int selector, int sensitive, const mapa_query *d_query,
                   mapa_record *d_record, int depth, int rank, int world, int chunk, int grid, void *stream) {
-    const int sensk = (selector == MAPA_SEL_PRESERVE && sensitive) ? 1 : 0;
-    SingleFn fn = pick_single(tb.topo.width, tb.pat[0].k, sensk);
+    SingleFn fn = pick_single(tb.topo.width, tb.pat[0].k, sel_code(selector, sensitive));
     if (!fn) return (int)cudaErrorInvalidValue;
     return fn(tb, selector, sensitive, d_query, d_record, depth, rank, world, chunk, grid,
               (cudaStream_t)stream);
@@ -1027,11 +1034,14 @@ int device_sm_count() {
 
 namespace {
 template <int W>
-int occ_single(int K, int sens, int smem) {
+int occ_single(int K, int sc, int smem) {
     const void *f = nullptr;
 #define MAPA_OCC_CASE(KK)                                                        \
     case KK:                                                                     \
-        f = sens ? single_ptr<W, KK, SEL_SENS>() : single_ptr<W, KK, SEL_LIN>(); \
+        f = sc == SEL_GREEDY ? single_ptr<W, KK, SEL_GREEDY>()                   \
+          : sc == SEL_INSENS ? single_ptr<W, KK, SEL_INSENS>()                   \
+          : sc == SEL_SENS ? single_ptr<W, KK, SEL_SENS>()                       \
+                           : single_ptr<W, KK, SEL_BASE>();                      \
         break;
     switch (K) {
         MAPA_OCC_CASE(1) MAPA_OCC_CASE(2) MAPA_OCC_CASE(3) MAPA_OCC_CASE(4)
@@ -1045,17 +1055,17 @@ int occ_single(int K, int sens, int smem) {
 }
 }  // namespace
 
-int max_blocks_per_sm_single(int width, int k, int sens, int xs) {
+int max_blocks_per_sm_single(int width, int k, int sc, int xs) {
     // cached: (width, k, sens, xs) -> blocks per SM (same device model per process)
-    static int cache[3][9][2][48] = {};
+    static int cache[3][9][4][48] = {};
     const int wi = width == 8 ? 0 : (width == 16 ? 1 : 2), xi = xs < 48 ? xs : 0;
-    int &slot = cache[wi][k >= 1 && k <= 8 ? k : 0][sens ? 1 : 0][xi];
+    int &slot = cache[wi][k >= 1 && k <= 8 ? k : 0][sc & 3][xi];
     if (slot) return slot;
     const int smem = (int)sizeof(Shared) + 3 * xs * xs * (int)sizeof(int);
     int r;
-    if (width == 8) r = occ_single<8>(k, sens, smem);
-    else if (width == 16) r = occ_single<16>(k, sens, smem);
-    else r = occ_single<32>(k, sens, smem);
+    if (width == 8) r = occ_single<8>(k, sc, smem);
+    else if (width == 16) r = occ_single<16>(k, sc, smem);
+    else r = occ_single<32>(k, sc, smem);
     slot = r;
     return r;
 }

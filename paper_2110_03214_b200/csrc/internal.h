@@ -5,6 +5,11 @@
 #include <cstdint>
 #include <string>
 
+#ifndef __CUDACC__
+#define __host__
+#define __device__
+#endif
+
 #include "../../include/mapa.h"
 
 namespace mapa {
@@ -57,6 +62,14 @@ struct Tables {
 using SingleTables = Tables<1, kLutCapSingle>;
 using MultiTables = Tables<kMaxPats, kLutCapMulti>;
 
+// Kernel selector codes: Greedy (Eq. 1), Preserve-insensitive (Eq. 3),
+// Preserve-sensitive (Eq. 2 rank), Baseline (constant score).
+enum { SEL_GREEDY = 0, SEL_INSENS = 1, SEL_SENS = 2, SEL_BASE = 3 };
+inline __host__ __device__ int sel_code(int selector, int sensitive) {
+    return selector == MAPA_SEL_BASELINE ? SEL_BASE
+         : selector == MAPA_SEL_PRESERVE ? (sensitive ? SEL_SENS : SEL_INSENS) : SEL_GREEDY;
+}
+
 // Canonical-mode patterns get fwd_src from the lex-leader constraints; RAW
 // mode zeroes fwd_src (no symmetry breaking).
 struct LaunchCfg {
@@ -74,7 +87,7 @@ int launch_batch(const MultiTables &tb, int64_t nq, const mapa_query *d_queries,
 int launch_trace(const MultiTables &tb, int ntraces, int nops, const mapa_trace_op *d_ops, int njobs,
                  const mapa_query *d_jobs, uint64_t *d_keys, void *stream);
 int device_sm_count();
-int max_blocks_per_sm_single(int width, int k, int sens, int xs);
+int max_blocks_per_sm_single(int width, int k, int sc, int xs);
 int max_blocks_per_sm_batch(int width, int npats, int xs);
 const char *cuda_error_string(int err);
 

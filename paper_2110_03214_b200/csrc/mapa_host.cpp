@@ -616,7 +616,7 @@ mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int
     if (selector < 0 || selector > 2) return fail(MAPA_E_INVALID_ARG, "bad selector");
     if (!key_fits(t, p)) return fail(MAPA_E_UNSUPPORTED, "key budget 15 + W + C(k,2) > 63");
     const int nF = busy_hint == 0xFFFFFFFFu ? t->n : __builtin_popcount(~busy_hint & nmask_of(t->n));
-    const int sensk = (selector == MAPA_SEL_PRESERVE && sensitive) ? 1 : 0;
+    const int sensk = sel_code(selector, sensitive);
     Plan pl = plan_single(t, p, sensk, nF, world);
     if (pl.nlocal >= (1ull << 27)) return fail(MAPA_E_UNSUPPORTED, "too many work items");
     static_assert(sizeof(SingleTables) < 32000, "kernel parameter block too large");
