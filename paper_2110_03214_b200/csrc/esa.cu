@@ -398,6 +398,12 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
     const bool okb = ((c.F & ~st.U & st.al[J1]) >> b) & 1u;
     const uint32_t cand2b = c.F & ~st.U & st.al[J2];
     const unsigned long long fbase = pack_f<K>(st);
+    const bool dep = d32 || d31 || d21;
+    if (!dep && okb) {
+        // leaves of this lane: every (v3, v) with v3 in cand3, v in cand2b, v3, v, b distinct
+        const uint32_t nb = ~(1u << b);
+        bst.cnt += (uint32_t)(__popc(cand3 & nb) * __popc(cand2b & nb) - __popc(cand3 & cand2b & nb));
+    }
     for (uint32_t i = 0; i < n3; ++i) {
         const int2 e3 = L3[i];
         const uint32_t v3 = (uint32_t)e3.x;
@@ -406,8 +412,10 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
         const int lp = lpb + m31 * w3;
         const uint32_t cand2 = cand2b & ~(1u << v3) & (d32 ? (0xFFFFFFFEu << v3) : kFull);
         const bool laneok = okb && b != v3 && (!d31 || b > v3);
-        const uint32_t M = laneok ? (d21 ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
-        bst.cnt += (uint32_t)__popc(M & cand2);
+        if (dep) {
+            const uint32_t M = laneok ? (d21 ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
+            bst.cnt += (uint32_t)__popc(M & cand2);
+        }
         const int base = (SelT<SEL>::lin) ? (A + e3.y + lp + 1) * 32 : A + e3.y + lp;
         const int best = scan_dense<W, SEL>(c, cand2, t2, base);
         if (laneok && best >= bst.thr) {  // best >= 32 and its score >= the lane's best score
