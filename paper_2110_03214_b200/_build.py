@@ -3,16 +3,20 @@ from __future__ import annotations
 
 import os
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmapa.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("esa.cu", "mapa_host.cpp")]
-HEADERS = [os.path.join(CSRC, "internal.h"), os.path.join(os.path.dirname(HERE), "include", "mapa.h")]
+# one translation unit per topology width W, compiled in parallel
+SOURCES = [os.path.join(CSRC, f) for f in ("esa_w32.cu", "esa_w16.cu", "esa_w8.cu", "esa.cu", "mapa_host.cpp")]
+HEADERS = [os.path.join(CSRC, f) for f in ("internal.h", "esa_kernels.cuh", "esa_w.cuh")] + \
+    [os.path.join(os.path.dirname(HERE), "include", "mapa.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-         "-Xcompiler", "-fPIC", "-shared", "-cudart", "static", "-Xptxas", "-v"]
+         "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+LINK = ["-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC", "-shared", "-cudart", "static"]
 
 
 def stale() -> bool:
@@ -24,15 +28,27 @@ def stale() -> bool:
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
-        cmd = [NVCC] + FLAGS + ["-o", LIB + ".tmp"] + SOURCES
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        objdir = os.path.join(HERE, "build_obj")
+        os.makedirs(objdir, exist_ok=True)
+        objs = [os.path.join(objdir, os.path.basename(src) + ".o") for src in SOURCES]
+
+        def compile_one(i):
+            return subprocess.run([NVCC] + FLAGS + ["-c", "-o", objs[i], SOURCES[i]], capture_output=True, text=True)
+
+        with ThreadPoolExecutor(len(SOURCES)) as ex:
+            results = list(ex.map(compile_one, range(len(SOURCES))))
+        log = "".join(r.stderr for r in results)
+        for r in results:
+            if r.returncode != 0:
+                raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+        r = subprocess.run([NVCC] + LINK + ["-o", LIB + ".tmp"] + objs, capture_output=True, text=True)
         if r.returncode != 0:
-            raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+            raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
         with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
-            f.write(r.stderr)
+            f.write(log)
         os.replace(LIB + ".tmp", LIB)
         if verbose:
-            print(r.stderr)
+            print(log)
     return LIB
 
 

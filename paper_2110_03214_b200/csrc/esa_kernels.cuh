@@ -1,0 +1,928 @@
+// esa_kernels.cuh — Enumerate-Score-Argmax kernels for sm_100a (B200).
+// Template code; instantiated per topology width W by esa_w8.cu / esa_w16.cu /
+// esa_w32.cu (compiled in parallel) and dispatched by esa.cu.
+//
+// One pass = SURVEY.md §8(a) S3-S6 fused in registers / shared memory:
+//   S3 occupancy prep   F = ~busy; inc_F(v), T_F (Eq. 3 support)
+//   S4 enumeration      DFS over injective maps f: V(P) -> F (§3.3 P:496-501;
+//                       G complete, so every injective map embeds).
+//                       Lanes = devices of the LAST pattern vertex k-1; the
+//                       two levels above it (k-3, k-2) walk per-group smem
+//                       candidate lists; outer levels are a uniform DFS.
+//                       Groups of W lanes (W = 8/16/32 = padded N) each run
+//                       their own prefix, so small topologies fill the warp.
+//                       Canonical mode adds lex-leader lower bounds (one leaf
+//                       per Aut(P)-orbit = SPEC dedup S:209).
+//   S5 scoring          integer only.  With v's class masks c0..c2 and any
+//                       device set X not containing v:
+//                         sum_{u in X} w(u,v) = 12|X| + 38 popc(c0&X)
+//                                               + 13 popc(c1&X) + 8 popc(c2&X)
+//                       (popc on the outer levels only).  For the inner levels
+//                       the lanes precompute in parallel the increment of
+//                       placing vertex k-3 / k-2 on their device (broadcast
+//                       through the lists) and their own leaf partial; a
+//                       k-3 step then costs one weight lookup per lane, a
+//                       k-2 step one list read + one table read + one fused
+//                       add-max per leaf.
+//                         Eq. 1 AggBW: X = back-neighbour devices.
+//                         Eq. 3 PreservedBW: T_F - sum inc_F(S)
+//                         + inside(S), X = all placed devices.
+//                         Eq. 2: census (x, y) accumulated as a
+//                         table index x*xs + y; score = dense rank of Eq. 2
+//                         among the censuses with x+y+z = m (host table).
+//   S6 argmax           leaves of one k-2 scan are ranked by (score+1)*32 +
+//                       (31 - v) (ties -> smaller v = lex-smaller device set);
+//                       the packed 64-bit key (score | brev(S) | edge code) is
+//                       built out of line only when a scan's best reaches the
+//                       lane's best score; warp shuffle max, block max,
+//                       atomicMax in HBM.  Max is order independent, so the
+//                       result is identical for every grid size / rank count.
+// Work items: the prefixes of depth D (mixed radix over the free devices),
+// handed out as contiguous chunks; a chunk is walked as a DFS range, so only
+// the first item of a run is decoded.  All tables live in one dynamic
+// shared-memory block (Shared below) addressed by offset, so the per-query
+// context holds no pointers.  No dense contraction exists, so no tensor cores
+// are used; the bound is integer issue / LSU.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace mapa {
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kBlock = 256;
+constexpr int kWarps = kBlock / 32;
+constexpr int kMaxDecode = 4;
+constexpr int kNN = kMaxN * kMaxN;
+
+// Compile-time selector: Greedy (Eq. 1), Preserve-insensitive (Eq. 3),
+// Preserve-sensitive (Eq. 2 rank), Baseline (constant score).
+// Bit 2 of the code = canonical mode (lex-leader constraints live); RAW-mode
+// instantiations compile every constraint test away.
+template <int SEL>
+struct SelT {
+    static constexpr int base = SEL & 3;
+    static constexpr bool canon = (SEL & 4) != 0;
+    static constexpr bool lin = base != SEL_SENS;      // additive score (Eq. 1 / Eq. 3 / 0)
+    static constexpr bool useU = base == SEL_INSENS;   // Eq. 3 sums over every placed device
+    static constexpr int wt = base == SEL_BASE ? 0 : 1;
+    static constexpr int w0 = 38 * wt, w1 = 13 * wt, w2 = 8 * wt, w12 = 12 * wt;
+};
+
+// Leaves of a k-2 scan are ranked by one int: (score + 1) * 32 + (31 - v).
+// Invalid leaves (vertex k-1 on the device of k-2, a lex-leader violation,
+// a padding lane) get kNeg added through the tables.
+constexpr int kNeg = -(1 << 28);
+
+// Per-warp candidate lists of the innermost DFS levels (G groups x W).
+struct WarpLists {
+    int dense[32];  // level k-2: per device, increment of placing k-2 there (or a sentinel)
+    int2 l3[32];    // level k-3: (v, increment of placing k-3 on v)
+};
+
+// One dynamic shared-memory block per CTA.  Tables are indexed [v*32 + b]:
+//   tw  = 32 w(v,b), kNeg when v == b or either is not a device
+//   tz  = 0,         kNeg likewise
+//   twd / tzd = the same with kNeg also where v >= b (canonical f(k-2) < f(k-1))
+//   twp = w(v,b) (0 when invalid), tdl = census delta xs [double] + [single]
+//   tse / tsed = tdl + kSent when invalid (/ v >= b); ts0 / ts0d = 0 + kSent
+//     (kSent = xs*xs moves the Eq. 2 index into a region of kNeg entries)
+// followed by npats Eq. 2 tables of 3 xs^2 ints: [x*xs + y] = (rank+1)*32,
+// [xs^2, 3 xs^2) = kNeg (an index carries at most two kSent offsets).
+struct Shared {
+    uint4 cm[kMaxN];
+    uint32_t magic[kMaxN + 4];
+    int tw[kNN], tz[kNN], twd[kNN], tzd[kNN], twp[kNN], tdl[kNN];
+    int tse[kNN], tsed[kNN], ts0[kNN], ts0d[kNN];
+    int inc[kWarps][kMaxN];
+    WarpLists wl[kWarps];
+    unsigned long long key[kWarps], cnt[kWarps];
+    uint8_t edge[kMaxPats][28];
+    uint32_t busy;
+    uint32_t pad[3];
+};
+
+// Single-query kernels: Shared + one Eq. 2 table of 3 xs^2 ints, xs <= 40.
+constexpr int kSmemSingleMax = (int)sizeof(Shared) + 3 * 40 * 40 * (int)sizeof(int);
+
+extern __shared__ __align__(16) unsigned char g_smem[];
+__device__ __forceinline__ Shared &sh() { return *reinterpret_cast<Shared *>(g_smem); }
+__device__ __forceinline__ int *sh_lut() { return reinterpret_cast<int *>(g_smem + sizeof(Shared)); }
+
+template <int W>
+struct Ctx {
+    uint32_t F;
+    int nF;
+    int b;                          // lane's device id (lane % W)
+    int g;                          // lane's group in the warp
+    int warp;
+    uint32_t gmask;                 // lanes of this lane's group
+    uint32_t cm0, cm1, cm2, cm12;   // lane's class masks
+    int incb;                       // inc_F(b)
+    int laneC;                      // lane constant of the score (Eq. 3: -inc_F(b))
+    int leafC;                      // k = 1 leaf constant
+    int acc0;                       // accumulator at the root (T_F for Eq. 3)
+    int xs;                         // Eq. 2 table row stride (16 or 32)
+    int lut;                        // this pattern's Eq. 2 table offset (ints) in sh_lut()
+    int pid;                        // pattern index (edge list in smem)
+    uint64_t fb, fs, db;            // bytes: fwd_back, fwd_src, dback
+    int clique, eb, m;
+    int col[W];                     // lane's inner-scan column (see lane_column)
+};
+
+template <int K>
+struct St {
+    uint32_t U;       // placed devices
+    int acc;          // LIN: partial score; SENS: x
+    int acc2;         // SENS: y
+    uint32_t f[K];    // f(i) for placed vertices
+    uint32_t bm[K];   // bm[u]: devices of the placed back-neighbours of u
+    uint32_t al[K];   // al[u]: devices allowed for u by lex-leader constraints
+};
+
+struct Best {
+    unsigned long long key;
+    uint32_t bs;   // score of key
+    uint32_t cnt;  // leaves scored
+    int thr;       // (bs + 1) * 32: a scan's packed rank must reach this to matter
+};
+
+template <int SEL>
+__device__ __forceinline__ uint32_t alw(uint32_t al) { return SelT<SEL>::canon ? al : 0xFFFFFFFFu; }
+
+__device__ __forceinline__ unsigned long long *u64p(uint64_t *p) {
+    return reinterpret_cast<unsigned long long *>(p);
+}
+
+__device__ __forceinline__ int lds_off(const int *base, int byte_off) {
+    return *reinterpret_cast<const int *>(reinterpret_cast<const char *>(base) + byte_off);
+}
+
+__device__ __forceinline__ uint32_t nth_set(uint32_t m, uint32_t n) {
+    // position of the n-th (0-based) set bit of m (popc binary search)
+    uint32_t pos = 0, c;
+    c = __popc(m & 0xFFFFu); if (n >= c) { n -= c; m >>= 16; pos += 16; }
+    c = __popc(m & 0xFFu);   if (n >= c) { n -= c; m >>= 8;  pos += 8; }
+    c = __popc(m & 0xFu);    if (n >= c) { n -= c; m >>= 4;  pos += 4; }
+    c = __popc(m & 0x3u);    if (n >= c) { n -= c; m >>= 2;  pos += 2; }
+    c = m & 1u;              if (n >= c) { pos += 1; }
+    return pos;
+}
+
+// Packed argmax key: score | brev_W(S) | edge code, built
+// out of line on the slow path; arguments by value.
+//   fpack: f(0..K-2) one byte each; b: device of vertex K-1.
+template <int W, int K>
+__device__ __noinline__ unsigned long long make_key(uint32_t S, unsigned long long fpack, uint32_t b,
+                                                    uint32_t s, int clique, int eb, int m, int pid) {
+    const uint32_t sb = __brev(S) >> (32 - W);
+    uint32_t ecode;
+    if (clique) {
+        ecode = (1u << eb) - 1u;  // eb <= 28
+    } else {
+        uint32_t R = 0;  // rank of f(i) inside S, 4 bits per pattern vertex
+#pragma unroll
+        for (int i = 0; i < K - 1; ++i) {
+            const uint32_t fi = (uint32_t)(fpack >> (8 * i)) & 0xFFu;
+            R |= (uint32_t)__popc(S & ((1u << fi) - 1u)) << (4 * i);
+        }
+        R |= (uint32_t)__popc(S & ((1u << b) - 1u)) << (4 * (K - 1));
+        ecode = 0;
+        const uint8_t *edge = sh().edge[pid];
+        for (int e = 0; e < m; ++e) {
+            const uint32_t ed = edge[e];
+            const uint32_t ra = (R >> (4 * (ed & 15u))) & 15u;
+            const uint32_t rb = (R >> (4 * (ed >> 4))) & 15u;
+            const uint32_t lo = min(ra, rb), hi = max(ra, rb);
+            const uint32_t p = lo * (2u * K - lo - 1u) / 2u + (hi - lo - 1u);
+            ecode |= 1u << (eb - 1 - (int)p);
+        }
+    }
+    return ((unsigned long long)s << (W + eb)) | ((unsigned long long)sb << eb) | ecode;
+}
+
+template <int W, int K>
+__device__ __forceinline__ void consider(const Ctx<W> &c, Best &bst, uint32_t S, unsigned long long fpack,
+                                         uint32_t s) {
+    if (s == bst.bs && bst.key) {
+        // equal score: the device-set field decides unless the sets are equal
+        const uint32_t sb_new = __brev(S) >> (32 - W);
+        const uint32_t sb_old = (uint32_t)(bst.key >> c.eb) & (W >= 32 ? kFull : ((1u << W) - 1u));
+        if (sb_new < sb_old) return;
+        if (sb_new == sb_old && c.clique) return;  // same set, clique: identical key
+    }
+    const unsigned long long key = make_key<W, K>(S, fpack, (uint32_t)c.b, s, c.clique, c.eb, c.m, c.pid);
+    if (key > bst.key) {
+        bst.key = key;
+        bst.bs = s;
+        bst.thr = ((int)s + 1) * 32;
+    }
+}
+
+template <int W, int K, int SEL, int J>
+__device__ __forceinline__ St<K> push(const Ctx<W> &c, const St<K> &st, uint32_t v) {
+    St<K> s = st;
+    const uint32_t vb = 1u << v;
+    const uint4 t = sh().cm[v];
+    if constexpr (SelT<SEL>::lin) {
+        const uint32_t X = SelT<SEL>::useU ? st.U : st.bm[J];
+        const int incv = SelT<SEL>::useU ? sh().inc[c.warp][v] : 0;
+        s.acc = st.acc + SelT<SEL>::w12 * __popc(X) - incv + SelT<SEL>::w0 * __popc(t.x & X) + SelT<SEL>::w1 * __popc(t.y & X) +
+                SelT<SEL>::w2 * __popc(t.z & X);
+    } else {
+        const uint32_t X = st.bm[J];
+        s.acc = st.acc + __popc(t.x & X);
+        s.acc2 = st.acc2 + __popc((t.y | t.z) & X);
+    }
+    s.U = st.U | vb;
+    s.f[J] = v;
+    const uint32_t fbJ = (uint32_t)(c.fb >> (8 * J)) & 0xFFu;
+    const uint32_t fsJ = (uint32_t)(SelT<SEL>::canon ? c.fs >> (8 * J) : 0ull) & 0xFFu;
+    const uint32_t above = 0xFFFFFFFEu << v;
+#pragma unroll
+    for (int u = J + 1; u < K; ++u) {
+        if ((fbJ >> u) & 1u) s.bm[u] |= vb;
+        if ((fsJ >> u) & 1u) s.al[u] &= above;
+    }
+    return s;
+}
+
+template <int K>
+__device__ __forceinline__ unsigned long long pack_f(const St<K> &st) {
+    unsigned long long fpack = 0;
+#pragma unroll
+    for (int i = 0; i < K - 1; ++i) fpack |= (unsigned long long)st.f[i] << (8 * i);
+    return fpack;
+}
+
+// k = 1: a single level, the lanes are the devices of vertex 0.
+template <int W, int SEL>
+__device__ __forceinline__ void leaf_k1(const Ctx<W> &c, Best &bst) {
+    const bool act = (c.F >> c.b) & 1u;
+    const int s = (SelT<SEL>::lin) ? c.acc0 + c.leafC : 0;  // m = 0: census (0,0,0) has rank 0
+    bst.cnt += act ? 1u : 0u;
+    if (act && (uint32_t)s >= bst.bs) consider<W, 1>(c, bst, 1u << c.b, 0ull, (uint32_t)s);
+}
+
+// Level k-2 scan, dense over the W devices of the group.  Lane b writes its
+// entry (increment of placing vertex k-2 on b, or a sentinel when b is not a
+// candidate) into the group's table; then every lane (device of vertex k-1)
+// ranks all W leaves (v, b) with its register column c.col (fully unrolled,
+// compile-time indices) and keeps the max.  Within one scan a lane's leaves
+// differ only in v, and among equal scores the smaller v is the lex-smaller
+// device set (larger key), so the packed rank (score+1)*32 + (31-v) decides
+// and the full key is built once, later.  Returns < 32 when no valid leaf.
+//   LIN:  rank = base + tab[v] + col[v],     tab = 32 t2 | kNeg, col = T[v][b] + 31 - v
+//   SENS: rank = lut[base + tab[v] + col[v]] + 31 - v,  tab = t2 | kSent, col = D[v][b]
+template <int W, int SEL>
+__device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2, int base) {
+    const uint32_t b = (uint32_t)c.b;
+    int *tab = sh().wl[c.warp].dense + c.g * W;
+    const bool mine = (cand >> b) & 1u;
+    __syncwarp(c.gmask);  // previous readers of the table are done
+    if constexpr (SelT<SEL>::lin) tab[b] = mine ? t2 * 32 : kNeg;
+    else tab[b] = 4 * (mine ? t2 : c.xs * c.xs);  // byte offsets into the Eq. 2 table
+    __syncwarp(c.gmask);
+    const int4 *t4 = reinterpret_cast<const int4 *>(tab);
+    int best = 0;
+    if constexpr (SelT<SEL>::lin) {
+        // four independent fused add-max chains (VIADDMNMX), base added once
+        int b0 = kNeg, b1 = kNeg, b2 = kNeg, b3 = kNeg;
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q) {
+            const int4 e = t4[q];
+            b0 = max(b0, e.x + c.col[4 * q + 0]);
+            b1 = max(b1, e.y + c.col[4 * q + 1]);
+            b2 = max(b2, e.z + c.col[4 * q + 2]);
+            b3 = max(b3, e.w + c.col[4 * q + 3]);
+        }
+        best = max(0, max(max(b0, b1), max(b2, b3)) + base);
+    } else {
+        // table, column and base are byte offsets: one IADD3 gives the address
+        // table, column and base are byte offsets into the Eq. 2 table
+        const int *lut = sh_lut() + c.lut;
+        const int b4 = 4 * base;
+#pragma unroll
+        for (int q = 0; q < W / 4; ++q) {
+            const int4 e = t4[q];
+            const int r0 = lds_off(lut, b4 + e.x + c.col[4 * q + 0]) + (31 - (4 * q + 0));
+            const int r1 = lds_off(lut, b4 + e.y + c.col[4 * q + 1]) + (31 - (4 * q + 1));
+            const int r2 = lds_off(lut, b4 + e.z + c.col[4 * q + 2]) + (31 - (4 * q + 2));
+            const int r3 = lds_off(lut, b4 + e.w + c.col[4 * q + 3]) + (31 - (4 * q + 3));
+            best = max(best, max(r0, r1));
+            best = max(best, max(r2, r3));
+        }
+    }
+    return best;
+}
+
+// The two innermost levels: vertex k-2 walks the devices of `cand`, vertex
+// k-1 sits on the lanes.  Vertices 0..k-3 are placed.
+template <int W, int K, int SEL>
+__device__ __forceinline__ void inner(const Ctx<W> &c, const St<K> &st, uint32_t cand, Best &bst) {
+    constexpr int J = K - 2;
+    const uint32_t b = (uint32_t)c.b;
+    const uint32_t fbJ = (uint32_t)(c.fb >> (8 * J)) & 0xFFu;
+    const uint32_t fsJ = (uint32_t)(SelT<SEL>::canon ? c.fs >> (8 * J) : 0ull) & 0xFFu;
+    const bool eK = (fbJ >> (K - 1)) & 1u;   // pattern edge (k-2, k-1)
+    const bool dep = (fsJ >> (K - 1)) & 1u;  // lex-leader f(k-2) < f(k-1)
+    int t2, base;
+    if constexpr (SelT<SEL>::lin) {
+        const uint32_t X2 = SelT<SEL>::useU ? st.U : st.bm[J];
+        const uint32_t X1 = SelT<SEL>::useU ? st.U : st.bm[K - 1];
+        t2 = SelT<SEL>::w12 * __popc(X2) - (SelT<SEL>::useU ? c.incb : 0) + SelT<SEL>::w0 * __popc(c.cm0 & X2) + SelT<SEL>::w1 * __popc(c.cm1 & X2) +
+             SelT<SEL>::w2 * __popc(c.cm2 & X2);
+        const int lp = c.laneC + SelT<SEL>::w12 * __popc(X1) + SelT<SEL>::w0 * __popc(c.cm0 & X1) + SelT<SEL>::w1 * __popc(c.cm1 & X1) +
+                       SelT<SEL>::w2 * __popc(c.cm2 & X1);
+        base = (st.acc + lp + 1) * 32;
+    } else {
+        const uint32_t X2 = st.bm[J], X1 = st.bm[K - 1];
+        t2 = __popc(c.cm0 & X2) * c.xs + __popc(c.cm12 & X2);
+        base = (st.acc + __popc(c.cm0 & X1)) * c.xs + st.acc2 + __popc(c.cm12 & X1);  // census index
+    }
+    const bool laneok = ((c.F & ~st.U & alw<SEL>(st.al[K - 1])) >> b) & 1u;
+    // leaves counted: v in cand with v != b (and v < b if canonical-ordered)
+    const uint32_t M = laneok ? (dep ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
+    bst.cnt += (uint32_t)__popc(M & cand);
+    const int best = scan_dense<W, SEL>(c, cand, t2, base);
+    if (laneok && best >= bst.thr) {  // best >= 32 and its score >= the lane's best score
+        const uint32_t s = (uint32_t)(best >> 5) - 1u;
+        {
+            const uint32_t bestv = 31u - (uint32_t)(best & 31);
+            unsigned long long fpack = pack_f<K>(st);
+            fpack |= (unsigned long long)bestv << (8 * J);
+            consider<W, K>(c, bst, st.U | (1u << bestv) | (1u << b), fpack, s);
+        }
+    }
+}
+
+// The three innermost levels: vertex k-3 walks `cand3` (uniform loop over a
+// per-group list of (v3, increment of placing k-3 on v3) built lane-parallel);
+// for every v3 the lane values are updated by ONE table lookup (w(v3,b) or the
+// census delta) and the k-2 list scan runs.  Vertices 0..k-4 are placed.
+template <int W, int K, int SEL>
+__device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_t cand3, Best &bst) {
+    constexpr int J3 = K - 3, J2 = K - 2, J1 = K - 1;
+    const uint32_t b = (uint32_t)c.b;
+    const uint32_t fb3 = (uint32_t)(c.fb >> (8 * J3)) & 0xFFu, fs3 = (uint32_t)(SelT<SEL>::canon ? c.fs >> (8 * J3) : 0ull) & 0xFFu;
+    const uint32_t fb2 = (uint32_t)(c.fb >> (8 * J2)) & 0xFFu, fs2 = (uint32_t)(SelT<SEL>::canon ? c.fs >> (8 * J2) : 0ull) & 0xFFu;
+    const bool e32 = (fb3 >> J2) & 1u, e31 = (fb3 >> J1) & 1u, e21 = (fb2 >> J1) & 1u;
+    const bool d32 = (fs3 >> J2) & 1u, d31 = (fs3 >> J1) & 1u, d21 = (fs2 >> J1) & 1u;
+    // lane values over the placed vertices 0..k-4:
+    //   t3 = increment of placing k-3 on b, t2b = of placing k-2 on b,
+    //   lpb = leaf partial of k-1 on b; v3 then adds m32 w3, m31 w3.
+    int t3, t2b, lpb, m32, m31, A;
+    const int *wcol;
+    if constexpr (SelT<SEL>::lin) {
+        const uint32_t X3 = SelT<SEL>::useU ? st.U : st.bm[J3];
+        const uint32_t X2 = SelT<SEL>::useU ? st.U : st.bm[J2];
+        const uint32_t X1 = SelT<SEL>::useU ? st.U : st.bm[J1];
+        const int inc = SelT<SEL>::useU ? c.incb : 0;
+        t3 = SelT<SEL>::w12 * __popc(X3) - inc + SelT<SEL>::w0 * __popc(c.cm0 & X3) + SelT<SEL>::w1 * __popc(c.cm1 & X3) +
+             SelT<SEL>::w2 * __popc(c.cm2 & X3);
+        t2b = SelT<SEL>::w12 * __popc(X2) - inc + SelT<SEL>::w0 * __popc(c.cm0 & X2) + SelT<SEL>::w1 * __popc(c.cm1 & X2) +
+              SelT<SEL>::w2 * __popc(c.cm2 & X2);
+        lpb = c.laneC + SelT<SEL>::w12 * __popc(X1) + SelT<SEL>::w0 * __popc(c.cm0 & X1) + SelT<SEL>::w1 * __popc(c.cm1 & X1) +
+              SelT<SEL>::w2 * __popc(c.cm2 & X1);
+        m32 = (SelT<SEL>::w12 != 0 && (SelT<SEL>::useU || e32)) ? 1 : 0;
+        m31 = (SelT<SEL>::w12 != 0 && (SelT<SEL>::useU || e31)) ? 1 : 0;
+        A = st.acc;
+        wcol = sh().twp + b;
+    } else {
+        const uint32_t X3 = st.bm[J3], X2 = st.bm[J2], X1 = st.bm[J1];
+        t3 = __popc(c.cm0 & X3) * c.xs + __popc(c.cm12 & X3);
+        t2b = __popc(c.cm0 & X2) * c.xs + __popc(c.cm12 & X2);
+        lpb = __popc(c.cm0 & X1) * c.xs + __popc(c.cm12 & X1);
+        m32 = e32 ? 1 : 0;
+        m31 = e31 ? 1 : 0;
+        A = st.acc * c.xs + st.acc2;
+        wcol = sh().tdl + b;
+    }
+    int2 *L3 = sh().wl[c.warp].l3 + c.g * W;
+    const uint32_t n3 = (uint32_t)__popc(cand3);
+    __syncwarp(c.gmask);  // previous readers of the k-3 list are done
+    if ((cand3 >> b) & 1u) L3[__popc(cand3 & ((1u << b) - 1u))] = make_int2((int)b, t3);
+    __syncwarp(c.gmask);
+    const bool okb = ((c.F & ~st.U & alw<SEL>(st.al[J1])) >> b) & 1u;
+    const uint32_t cand2b = c.F & ~st.U & alw<SEL>(st.al[J2]);
+    const unsigned long long fbase = pack_f<K>(st);
+    const bool dep = d32 || d31 || d21;
+    if (!dep && okb) {
+        // leaves of this lane: every (v3, v) with v3 in cand3, v in cand2b, v3, v, b distinct
+        const uint32_t nb = ~(1u << b);
+        bst.cnt += (uint32_t)(__popc(cand3 & nb) * __popc(cand2b & nb) - __popc(cand3 & cand2b & nb));
+    }
+    for (uint32_t i = 0; i < n3; ++i) {
+        const int2 e3 = L3[i];
+        const uint32_t v3 = (uint32_t)e3.x;
+        const int w3 = wcol[v3 * 32];
+        const int t2 = t2b + m32 * w3;
+        const int lp = lpb + m31 * w3;
+        const uint32_t cand2 = cand2b & ~(1u << v3) & (d32 ? (0xFFFFFFFEu << v3) : kFull);
+        const bool laneok = okb && b != v3 && (!d31 || b > v3);
+        if (dep) {
+            const uint32_t M = laneok ? (d21 ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
+            bst.cnt += (uint32_t)__popc(M & cand2);
+        }
+        const int base = (SelT<SEL>::lin) ? (A + e3.y + lp + 1) * 32 : A + e3.y + lp;
+        const int best = scan_dense<W, SEL>(c, cand2, t2, base);
+        if (laneok && best >= bst.thr) {  // best >= 32 and its score >= the lane's best score
+            const uint32_t s = (uint32_t)(best >> 5) - 1u;
+            {
+                const uint32_t bestv = 31u - (uint32_t)(best & 31);
+                const unsigned long long fpack =
+                    fbase | ((unsigned long long)v3 << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
+                consider<W, K>(c, bst, st.U | (1u << v3) | (1u << bestv) | (1u << b), fpack, s);
+            }
+        }
+    }
+}
+
+template <int W, int K, int SEL, int J>
+__device__ __forceinline__ void level(const Ctx<W> &c, const St<K> &st, Best &bst) {
+    if constexpr (K == 1) {
+        leaf_k1<W, SEL>(c, bst);
+    } else if constexpr (J == K - 2) {
+        inner<W, K, SEL>(c, st, c.F & ~st.U & alw<SEL>(st.al[J]), bst);
+    } else if constexpr (J == K - 3) {
+        inner3<W, K, SEL>(c, st, c.F & ~st.U & alw<SEL>(st.al[J]), bst);
+    } else {
+        uint32_t cand = c.F & ~st.U & alw<SEL>(st.al[J]);
+        while (cand) {
+            const uint32_t v = __ffs(cand) - 1;
+            cand &= cand - 1u;
+            level<W, K, SEL, J + 1>(c, push<W, K, SEL, J>(c, st, v), bst);
+        }
+    }
+}
+
+template <int W, int K>
+__device__ __forceinline__ St<K> root(const Ctx<W> &c) {
+    St<K> st;
+    st.U = 0;
+    st.acc = c.acc0;
+    st.acc2 = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        st.f[i] = 0;
+        st.bm[i] = 0;
+        st.al[i] = kFull;
+    }
+    return st;
+}
+
+// item -> mixed-radix digits (radix nF - j at level j); false if item >= P(nF, D)
+__device__ __forceinline__ bool digits(uint32_t item, int nF, int D, uint32_t (&dg)[kMaxDecode]) {
+    uint32_t it = item;
+#pragma unroll
+    for (int j = kMaxDecode - 1; j >= 0; --j) {
+        if (j < D) {
+            const uint32_t r = (uint32_t)(nF - j);
+            const uint32_t q = __umulhi(it, sh().magic[r]);
+            dg[j] = it - q * r;
+            it = q;
+        } else {
+            dg[j] = 0;
+        }
+    }
+    return it == 0;
+}
+
+__device__ __forceinline__ uint32_t perm_count(int n, int d) {
+    uint32_t p = 1;
+    for (int j = 0; j < d; ++j) p *= (uint32_t)(n - j);
+    return p;
+}
+
+// Walk up to maxn consecutive items starting at the item whose digits are dg.
+// Levels < D-1 are decoded from the digits; level D-1 iterates its (raw-order)
+// candidates from digit dg[D-1] on.  Returns the number of items consumed
+// (>= 1); a prefix that violates a lex-leader bound skips its whole subtree.
+template <int W, int K, int SEL, int J, int DMAX>
+__device__ __forceinline__ uint32_t descend_range(const Ctx<W> &c, const St<K> &st, const uint32_t (&dg)[kMaxDecode],
+                                                  int D, uint32_t maxn, Best &bst) {
+    if constexpr (J >= DMAX || J > K - 2) {
+        return maxn;  // unreachable: D <= DMAX <= K-1
+    } else {
+        if (J < D - 1) {
+            const uint32_t v = nth_set(c.F & ~st.U, dg[J]);
+            if (SelT<SEL>::canon && !((st.al[J] >> v) & 1u)) {
+                uint32_t prod = 1, off = 0;
+#pragma unroll
+                for (int l = kMaxDecode - 1; l > J; --l) {
+                    if (l < D) {
+                        off += dg[l] * prod;
+                        prod *= (uint32_t)(c.nF - l);
+                    }
+                }
+                return min(maxn, prod - off);
+            }
+            return descend_range<W, K, SEL, J + 1, DMAX>(c, push<W, K, SEL, J>(c, st, v), dg, D, maxn, bst);
+        } else {
+            uint32_t cand = c.F & ~st.U;
+            const uint32_t p = nth_set(cand, dg[J]);
+            cand &= ~((1u << p) - 1u);  // raw candidates from the current item on
+            uint32_t n = (uint32_t)__popc(cand);
+            if (maxn < n) {
+                cand &= (1u << nth_set(cand, maxn)) - 1u;
+                n = maxn;
+            }
+            cand &= alw<SEL>(st.al[J]);
+            if constexpr (J == K - 2) {
+                inner<W, K, SEL>(c, st, cand, bst);
+            } else if constexpr (J == K - 3) {
+                inner3<W, K, SEL>(c, st, cand, bst);
+            } else {
+                while (cand) {
+                    const uint32_t v = __ffs(cand) - 1;
+                    cand &= cand - 1u;
+                    level<W, K, SEL, J + 1>(c, push<W, K, SEL, J>(c, st, v), bst);
+                }
+            }
+            return n;
+        }
+    }
+}
+
+// Items [lo, hi) of depth D (D = 0 only for K = 1).
+template <int W, int K, int SEL, int DMAX>
+__device__ __forceinline__ void run_range(const Ctx<W> &c, uint32_t lo, uint32_t hi, int D, Best &bst) {
+    if constexpr (K == 1) {
+        if (lo == 0 && hi > 0) leaf_k1<W, SEL>(c, bst);
+    } else {
+        uint32_t i = lo;
+        while (i < hi) {
+            uint32_t dg[kMaxDecode];
+            if (!digits(i, c.nF, D, dg)) break;
+            i += descend_range<W, K, SEL, 0, DMAX>(c, root<W, K>(c), dg, D, hi - i, bst);
+        }
+    }
+}
+
+// Per-query context.  Must be called by the whole warp (uses shuffles); it
+// writes this warp's inc_F table.
+template <int W>
+__device__ __forceinline__ Ctx<W> make_ctx(const DevTopo &topo, const DevPattern &P, int pid, int xs, uint32_t busy,
+                                           int sc) {
+    const int lane = threadIdx.x & 31;
+    Ctx<W> c;
+    const uint32_t nmask = topo.n >= 32 ? kFull : ((1u << topo.n) - 1u);
+    c.F = ~busy & nmask;
+    c.nF = __popc(c.F);
+    c.b = lane & (W - 1);
+    c.g = lane / W;
+    c.warp = (int)(threadIdx.x >> 5);
+    c.gmask = W == 32 ? kFull : (((1u << W) - 1u) << (c.g * W));
+    const uint4 mine = sh().cm[c.b];
+    c.cm0 = mine.x;
+    c.cm1 = mine.y;
+    c.cm2 = mine.z;
+    c.cm12 = mine.y | mine.z;
+    // inc_F(b) = sum_{u in F, u != b} w(u,b)
+    const int inFb = (c.F >> c.b) & 1u;
+    int incb = 12 * (c.nF - inFb) + 38 * __popc(mine.x & c.F) + 13 * __popc(mine.y & c.F) +
+               8 * __popc(mine.z & c.F);
+    if (c.b >= topo.n) incb = 0;
+    if (lane < W) sh().inc[c.warp][c.b] = incb;
+    c.incb = incb;
+    // T_F = 1/2 sum_{v in F} inc_F(v)  (reduce within the W-lane group)
+    int t = inFb ? incb : 0;
+#pragma unroll
+    for (int o = W / 2; o > 0; o >>= 1) t += __shfl_xor_sync(kFull, t, o, W);
+    const int TF = t / 2;
+    const int K = P.k;
+    c.fb = *reinterpret_cast<const uint64_t *>(P.fwd_back);
+    c.fs = *reinterpret_cast<const uint64_t *>(P.fwd_src);
+    c.db = *reinterpret_cast<const uint64_t *>(P.dback);
+    c.clique = P.clique;
+    c.eb = P.eb;
+    c.m = P.m;
+    c.pid = pid;
+    c.xs = xs;
+    c.lut = pid * 3 * xs * xs;
+    sc &= 3;
+    const bool useU = sc == SEL_INSENS;
+    const int w12 = sc == SEL_BASE ? 0 : 12;
+    c.laneC = useU ? -incb : 0;
+    c.acc0 = useU ? TF : 0;
+    const int n12 = useU ? (K - 1) : (int)P.dback[K - 1];
+    c.leafC = w12 * n12 + c.laneC;
+    // inner-scan column of this lane (vertex k-1 on device b, vertex k-2 on v):
+    //   LIN  col[v] = T[v][b] + 31 - v, T = 32 w (edge k-2~k-1 scored) or 0, kNeg invalid
+    //   SENS col[v] = D[v][b], D = census delta (edge k-2~k-1) or 0, + kSent invalid
+    const int sh2 = K >= 2 ? 8 * (K - 2) : 0;
+    const bool eK = K >= 2 && ((((uint32_t)(c.fb >> sh2)) >> (K - 1)) & 1u);
+    const bool dep = K >= 2 && ((((uint32_t)(c.fs >> sh2)) >> (K - 1)) & 1u);
+    const bool sens = sc == SEL_SENS;
+    const bool eW = w12 != 0 && (useU || eK);
+    const int *T = sens ? (eK ? (dep ? sh().tsed : sh().tse) : (dep ? sh().ts0d : sh().ts0))
+                        : (eW ? (dep ? sh().twd : sh().tw) : (dep ? sh().tzd : sh().tz));
+#pragma unroll
+    for (int v = 0; v < W; ++v) c.col[v] = sens ? 4 * T[v * 32 + c.b] : T[v * 32 + c.b] + 31 - v;
+    __syncwarp();
+    return c;
+}
+
+__device__ __forceinline__ void warp_reduce(unsigned long long &key, unsigned long long &cnt) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long k2 = __shfl_xor_sync(kFull, key, o);
+        const unsigned long long c2 = __shfl_xor_sync(kFull, cnt, o);
+        key = k2 > key ? k2 : key;
+        cnt += c2;
+    }
+}
+
+// Shared tables for Eq. 2 row stride xs + npats Eq. 2 tables + edge lists.
+// Caller syncs.
+template <int MAXP, int LUTCAP>
+__device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int xs) {
+    Shared &s = sh();
+    const DevTopo &topo = tb.topo;
+    const int tid = threadIdx.x;
+    if (tid < kMaxN) s.cm[tid] = make_uint4(topo.cm[tid][0], topo.cm[tid][1], topo.cm[tid][2], topo.cm[tid][3]);
+    if (tid <= kMaxN) s.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
+    const int sent = xs * xs;
+    for (int i = tid; i < kNN; i += blockDim.x) {
+        const int v = i >> 5, b = i & 31;
+        int w = kNeg, d = 0;
+        if (v != b && v < topo.n && b < topo.n) {
+            if ((topo.cm[b][0] >> v) & 1u) { w = 50; d = xs; }
+            else if ((topo.cm[b][1] >> v) & 1u) { w = 25; d = 1; }
+            else if ((topo.cm[b][2] >> v) & 1u) { w = 20; d = 1; }
+            else w = 12;
+        }
+        const bool bad = w == kNeg, badd = bad || v >= b;
+        s.tw[i] = bad ? kNeg : 32 * w;
+        s.tz[i] = bad ? kNeg : 0;
+        s.twd[i] = badd ? kNeg : 32 * w;
+        s.tzd[i] = badd ? kNeg : 0;
+        s.twp[i] = bad ? 0 : w;
+        s.tdl[i] = d;
+        s.tse[i] = d + (bad ? sent : 0);
+        s.tsed[i] = d + (badd ? sent : 0);
+        s.ts0[i] = bad ? sent : 0;
+        s.ts0d[i] = badd ? sent : 0;
+    }
+    int *lut = sh_lut();
+    for (int p = 0; p < tb.npats; ++p) {
+        const DevPattern &P = tb.pat[p];
+        const uint16_t *rank = tb.lut + P.lut_off;
+        const int m = P.m;
+        for (int i = tid; i < 3 * xs * xs; i += blockDim.x) {
+            const int x = i / xs, y = i % xs;
+            int v = kNeg;
+            if (i < xs * xs) v = (x + y <= m) ? ((int)rank[x * (m + 1) + y] + 1) * 32 : 0;
+            lut[p * 3 * xs * xs + i] = v;
+        }
+        if (tid < 28) s.edge[p][tid] = P.edge[tid];
+    }
+}
+
+// ---------------------------------------------------------------- single query
+// Items = prefixes of depth D, in chunks of `chunk` consecutive items; local
+// chunk q of rank r is global chunk q*world + r.  Group g of a warp walks the
+// g-th slice of the chunk.
+template <int W, int K, int SEL>
+__global__ void __launch_bounds__(kBlock, 2)
+esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict__ dq,
+           mapa_record *__restrict__ rec, int D, int rank, int world, int stripe) {
+    constexpr int G = 32 / W;
+    constexpr int DMAX = (K - 1) < kMaxDecode ? (K - 1) : kMaxDecode;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int xs = tb.xs;
+    load_shared(tb, xs);
+    const uint32_t busy = dq->busy;
+    __syncthreads();
+
+    Ctx<W> c = make_ctx<W>(tb.topo, tb.pat[0], 0, xs, busy, SEL & 3);
+
+    // Rank r owns the stripes s = r, r + world, ... of `stripe` consecutive
+    // items; its local item space is their concatenation.  Warps grab local
+    // chunks by guided self-scheduling (size = remaining / (2 x warps), at
+    // least 2G), so few chunks are decoded and the tail stays short.
+    const uint32_t N = (K <= c.nF) ? perm_count(c.nF, D) : 0u;
+    const uint32_t L = (uint32_t)stripe;
+    const uint32_t nS = (N + L - 1u) / L;
+    const uint32_t myS = nS > (uint32_t)rank ? (nS - (uint32_t)rank + (uint32_t)world - 1u) / (uint32_t)world : 0u;
+    const bool ownLast = nS > 0 && ((nS - 1u) % (uint32_t)world) == (uint32_t)rank;
+    const uint32_t Nloc = myS == 0 ? 0u : (ownLast ? (myS - 1u) * L + (N - (nS - 1u) * L) : myS * L);
+    const uint32_t P = gridDim.x * (uint32_t)kWarps;
+    Best bst{0ull, 0u, 0u, 32};
+    const uint32_t g = (uint32_t)(lane / W);
+    for (;;) {
+        uint32_t start = 0, sz = 0;
+        if (lane == 0) {
+            const uint32_t cur = *reinterpret_cast<volatile uint32_t *>(&rec->ctr);
+            const uint32_t rem = cur < Nloc ? Nloc - cur : 0u;
+            sz = max(2u * G, rem / (2u * P));
+            sz = (sz + G - 1u) / G * G;
+            start = atomicAdd(&rec->ctr, sz);
+        }
+        start = __shfl_sync(kFull, start, 0);
+        sz = __shfl_sync(kFull, sz, 0);
+        if (start >= Nloc) break;
+        const uint32_t end = min(start + sz, Nloc);
+        const uint32_t per = (end - start + G - 1u) / G;
+        uint32_t j0 = start + g * per;
+        const uint32_t j1 = min(j0 + per, end);
+        while (j0 < j1) {  // split at stripe boundaries
+            const uint32_t sl = j0 / L;
+            const uint32_t seg = min(j1, (sl + 1u) * L);
+            const uint32_t lo = (sl * (uint32_t)world + (uint32_t)rank) * L + (j0 - sl * L);
+            run_range<W, K, SEL, DMAX>(c, lo, lo + (seg - j0), D, bst);
+            j0 = seg;
+        }
+        __syncwarp();
+    }
+    unsigned long long key = bst.key, cnt = bst.cnt;
+    warp_reduce(key, cnt);
+    if (lane == 0) {
+        sh().key[warp] = key;
+        sh().cnt[warp] = cnt;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        key = lane < kWarps ? sh().key[lane] : 0ull;
+        cnt = lane < kWarps ? sh().cnt[lane] : 0ull;
+        warp_reduce(key, cnt);
+        if (lane == 0) {
+            if (key) atomicMax(u64p(&rec->key), key);
+            if (cnt) atomicAdd(u64p(&rec->leaves), cnt);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- batches
+// W slots per query; slot j = the j-th free device as f(0) (items of depth 1);
+// K = 1 queries use slot 0 only (depth 0).
+template <int W, int K, int SEL>
+__device__ __forceinline__ void batch_item(const Ctx<W> &c, uint32_t j, Best &bst) {
+    if constexpr (K == 1) {
+        if (j == 0) leaf_k1<W, SEL>(c, bst);
+    } else {
+        if (j < (uint32_t)c.nF) run_range<W, K, SEL, 1>(c, j, j + 1, 1, bst);
+    }
+}
+
+template <int W, int SEL>
+__device__ __forceinline__ void batch_dispatch_k(int K, const Ctx<W> &c, uint32_t j, Best &bst) {
+    switch (K) {
+        case 1: batch_item<W, 1, SEL>(c, j, bst); break;
+        case 2: batch_item<W, 2, SEL>(c, j, bst); break;
+        case 3: batch_item<W, 3, SEL>(c, j, bst); break;
+        case 4: batch_item<W, 4, SEL>(c, j, bst); break;
+        case 5: batch_item<W, 5, SEL>(c, j, bst); break;
+        case 6: batch_item<W, 6, SEL>(c, j, bst); break;
+        case 7: batch_item<W, 7, SEL>(c, j, bst); break;
+        case 8: batch_item<W, 8, SEL>(c, j, bst); break;
+        default: break;
+    }
+}
+
+__device__ __forceinline__ bool key_fits(int W, const DevPattern &P) { return 15 + W + P.eb <= 63; }
+
+template <int W, int CANON>
+__global__ void __launch_bounds__(kBlock, 2)
+esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query *__restrict__ qs,
+          mapa_record *__restrict__ res, uint32_t *__restrict__ ctr) {
+    constexpr int G = 32 / W;
+    const int lane = threadIdx.x & 31;
+    const int xs = tb.xs;
+    load_shared(tb, xs);
+    __syncthreads();
+
+    const unsigned long long nslots = (unsigned long long)nq * W;
+    const uint32_t g = (uint32_t)(lane / W);
+    for (;;) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long *>(ctr), (unsigned long long)G);
+        base = __shfl_sync(kFull, base, 0);
+        if (base >= nslots) break;
+        const unsigned long long q = base / W;  // G | W: every group of the warp has the same query
+        const mapa_query qu = qs[q];
+        const uint32_t pid = qu.pattern;
+        if (pid >= (uint32_t)tb.npats || !key_fits(W, tb.pat[pid < (uint32_t)tb.npats ? pid : 0])) {
+            if (lane == 0 && (base % W) == 0) atomicExch(&res[q].status, 1u);
+            continue;
+        }
+        const DevPattern &P = tb.pat[pid];
+        Ctx<W> c = make_ctx<W>(tb.topo, P, (int)pid, xs, qu.busy, sel_code(qu.selector, qu.sensitive));
+        if (P.k > c.nF) continue;
+        const uint32_t j = (uint32_t)(base % W) + g;
+        Best bst{0ull, 0u, 0u, 32};
+        switch (sel_code(qu.selector, qu.sensitive)) {
+            case SEL_GREEDY: batch_dispatch_k<W, SEL_GREEDY | 4 * CANON>(P.k, c, j, bst); break;
+            case SEL_INSENS: batch_dispatch_k<W, SEL_INSENS | 4 * CANON>(P.k, c, j, bst); break;
+            case SEL_SENS: batch_dispatch_k<W, SEL_SENS | 4 * CANON>(P.k, c, j, bst); break;
+            default: batch_dispatch_k<W, SEL_BASE | 4 * CANON>(P.k, c, j, bst); break;
+        }
+        __syncwarp();
+        unsigned long long key = bst.key, cnt = bst.cnt;
+        warp_reduce(key, cnt);
+        if (lane == 0) {
+            if (key) atomicMax(u64p(&res[q].key), key);
+            if (cnt) atomicAdd(u64p(&res[q].leaves), cnt);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- trace replay
+template <int W, int K, int SEL>
+__device__ __forceinline__ void trace_items(const Ctx<W> &c, int D, uint32_t nItems, uint32_t gid, uint32_t ngroups,
+                                            Best &bst) {
+    constexpr int DMAX = (K - 1) < 2 ? (K - 1) : 2;
+    const uint32_t per = (nItems + ngroups - 1u) / ngroups;
+    const uint32_t lo = gid * per, hi = min(lo + per, nItems);
+    if (lo < hi) run_range<W, K, SEL, DMAX>(c, lo, hi, D, bst);
+}
+
+template <int W, int SEL>
+__device__ __forceinline__ void trace_dispatch_k(int K, const Ctx<W> &c, int D, uint32_t nItems, uint32_t gid,
+                                                 uint32_t ngroups, Best &bst) {
+    switch (K) {
+        case 1: trace_items<W, 1, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 2: trace_items<W, 2, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 3: trace_items<W, 3, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 4: trace_items<W, 4, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 5: trace_items<W, 5, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 6: trace_items<W, 6, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 7: trace_items<W, 7, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        case 8: trace_items<W, 8, SEL>(c, D, nItems, gid, ngroups, bst); break;
+        default: break;
+    }
+}
+
+// One CTA per trace; ALLOC / RELEASE ops in order; the busy mask lives in
+// shared memory (§3.6 state management), decisions go to HBM as keys.
+template <int W, int CANON>
+__global__ void __launch_bounds__(kBlock, 1)
+esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op *__restrict__ ops, int njobs,
+          const mapa_query *__restrict__ jobs, unsigned long long *__restrict__ keys) {
+    constexpr int G = 32 / W;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int t = blockIdx.x;
+    const int xs = tb.xs;
+    load_shared(tb, xs);
+    if (tid == 0) sh().busy = 0u;
+    __syncthreads();
+    const mapa_trace_op *op = ops + (long long)t * nops;
+    const mapa_query *jb = jobs + (long long)t * njobs;
+    unsigned long long *ky = keys + (long long)t * njobs;
+    const uint32_t gid = (uint32_t)(warp * G + lane / W);
+    const uint32_t wmask = W >= 32 ? kFull : ((1u << W) - 1u);
+    for (int o = 0; o < nops; ++o) {
+        const mapa_trace_op cur = op[o];
+        const mapa_query qu = jb[cur.job];
+        const uint32_t pid = qu.pattern;
+        const bool okp = pid < (uint32_t)tb.npats && key_fits(W, tb.pat[pid < (uint32_t)tb.npats ? pid : 0]);
+        const int ep = okp ? (int)pid : 0;
+        const DevPattern &P = tb.pat[ep];
+        if (cur.op == 0) {
+            const uint32_t busy = sh().busy;
+            Ctx<W> c = make_ctx<W>(tb.topo, P, ep, xs, busy, sel_code(qu.selector, qu.sensitive));
+            Best bst{0ull, 0u, 0u, 32};
+            if (okp && P.k <= c.nF) {
+                const int D = (P.k - 1) < 2 ? (P.k - 1) : 2;
+                const uint32_t nItems = perm_count(c.nF, D);
+                switch (sel_code(qu.selector, qu.sensitive)) {
+                    case SEL_GREEDY: trace_dispatch_k<W, SEL_GREEDY | 4 * CANON>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
+                    case SEL_INSENS: trace_dispatch_k<W, SEL_INSENS | 4 * CANON>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
+                    case SEL_SENS: trace_dispatch_k<W, SEL_SENS | 4 * CANON>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
+                    default: trace_dispatch_k<W, SEL_BASE | 4 * CANON>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
+                }
+            }
+            __syncwarp();
+            unsigned long long key = bst.key, cnt = bst.cnt;
+            warp_reduce(key, cnt);
+            if (lane == 0) sh().key[warp] = key;
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long best = 0;
+                for (int w = 0; w < kWarps; ++w) best = sh().key[w] > best ? sh().key[w] : best;
+                ky[cur.job] = best;
+                if (best) sh().busy = busy | (__brev((uint32_t)(best >> P.eb) & wmask) >> (32 - W));
+            }
+        } else {
+            if (tid == 0) {
+                const unsigned long long kk = ky[cur.job];
+                sh().busy &= ~(__brev((uint32_t)(kk >> P.eb) & wmask) >> (32 - W));
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int MAXP, int LUTCAP>
+int smem_bytes(const Tables<MAXP, LUTCAP> &tb) {
+    return (int)sizeof(Shared) + tb.npats * 3 * tb.xs * tb.xs * (int)sizeof(int);
+}
+
+inline int set_smem(const void *f, int bytes) {
+    return (int)cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+}  // namespace
+}  // namespace mapa

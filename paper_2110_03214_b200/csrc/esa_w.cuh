@@ -1,0 +1,138 @@
+// esa_w.cuh — per-width entry points (included by esa_w8.cu / esa_w16.cu /
+// esa_w32.cu with MAPA_W defined): instantiates the kernels for one W.
+#include "esa_kernels.cuh"
+
+#define MAPA_CAT2(a, b) a##b
+#define MAPA_CAT(a, b) MAPA_CAT2(a, b)
+
+namespace mapa {
+namespace {
+
+template <int W, int K, int SEL>
+int do_launch_single(const SingleTables &tb, const mapa_query *dq, mapa_record *rec, int D, int rank, int world,
+                     int stripe, int grid, cudaStream_t st) {
+    const int smem = smem_bytes(tb);
+    // the attribute is always set to the fixed upper bound (see kSmemSingleMax),
+    // so the occupancy query and every launch agree
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute((const void *)esa_single<W, K, SEL>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSingleMax);
+        if (e != cudaSuccess) return (int)e;
+        configured = true;
+    }
+    if (smem > kSmemSingleMax) return (int)cudaErrorInvalidValue;
+    esa_single<W, K, SEL><<<grid, kBlock, smem, st>>>(tb, dq, rec, D, rank, world, stripe);
+    return (int)cudaGetLastError();
+}
+
+using SingleFn = int (*)(const SingleTables &, const mapa_query *, mapa_record *, int, int, int, int, int,
+                         cudaStream_t);
+
+template <int W, int SEL>
+SingleFn pick_k(int K) {
+    switch (K) {
+        case 1: return do_launch_single<W, 1, SEL>;
+        case 2: return do_launch_single<W, 2, SEL>;
+        case 3: return do_launch_single<W, 3, SEL>;
+        case 4: return do_launch_single<W, 4, SEL>;
+        case 5: return do_launch_single<W, 5, SEL>;
+        case 6: return do_launch_single<W, 6, SEL>;
+        case 7: return do_launch_single<W, 7, SEL>;
+        case 8: return do_launch_single<W, 8, SEL>;
+    }
+    return nullptr;
+}
+
+template <int W, int K, int SEL>
+const void *single_ptr() { return (const void *)esa_single<W, K, SEL>; }
+
+template <int W, int SEL>
+const void *pick_ptr(int K) {
+    switch (K) {
+        case 1: return single_ptr<W, 1, SEL>();
+        case 2: return single_ptr<W, 2, SEL>();
+        case 3: return single_ptr<W, 3, SEL>();
+        case 4: return single_ptr<W, 4, SEL>();
+        case 5: return single_ptr<W, 5, SEL>();
+        case 6: return single_ptr<W, 6, SEL>();
+        case 7: return single_ptr<W, 7, SEL>();
+        case 8: return single_ptr<W, 8, SEL>();
+    }
+    return nullptr;
+}
+
+#define MAPA_SEL_SWITCH(FN, ...)                      \
+    switch (sc & 7) {                                 \
+        case 0: return FN<MAPA_W, 0>(__VA_ARGS__);    \
+        case 1: return FN<MAPA_W, 1>(__VA_ARGS__);    \
+        case 2: return FN<MAPA_W, 2>(__VA_ARGS__);    \
+        case 3: return FN<MAPA_W, 3>(__VA_ARGS__);    \
+        case 4: return FN<MAPA_W, 4>(__VA_ARGS__);    \
+        case 5: return FN<MAPA_W, 5>(__VA_ARGS__);    \
+        case 6: return FN<MAPA_W, 6>(__VA_ARGS__);    \
+        default: return FN<MAPA_W, 7>(__VA_ARGS__);   \
+    }
+
+SingleFn pick(int K, int sc) { MAPA_SEL_SWITCH(pick_k, K) }
+const void *pick_fn(int K, int sc) { MAPA_SEL_SWITCH(pick_ptr, K) }
+
+}  // namespace
+
+// sc = selector code | 4 * canonical (SelT)
+int MAPA_CAT(launch_single_w, MAPA_W)(const SingleTables &tb, int sc, const mapa_query *dq, mapa_record *rec,
+                                      int D, int rank, int world, int stripe, int grid, void *stream) {
+    SingleFn fn = pick(tb.pat[0].k, sc);
+    if (!fn) return (int)cudaErrorInvalidValue;
+    return fn(tb, dq, rec, D, rank, world, stripe, grid, (cudaStream_t)stream);
+}
+
+int MAPA_CAT(occ_single_w, MAPA_W)(int K, int sc, int smem) {
+    const void *f = pick_fn(K, sc);
+    int nb = 0;
+    if (!f || set_smem(f, kSmemSingleMax) != 0) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kBlock, smem) != cudaSuccess) return 1;
+    return nb > 0 ? nb : 1;
+}
+
+int MAPA_CAT(launch_batch_w, MAPA_W)(const MultiTables &tb, int canon, int64_t nq, const mapa_query *d_queries,
+                                     mapa_record *d_results, uint32_t *d_ctr, int grid, void *stream) {
+    const int smem = smem_bytes(tb);
+    const void *f = canon ? (const void *)esa_batch<MAPA_W, 1> : (const void *)esa_batch<MAPA_W, 0>;
+    int err = set_smem(f, smem);
+    if (err) return err;
+    if (canon)
+        esa_batch<MAPA_W, 1><<<grid, kBlock, smem, (cudaStream_t)stream>>>(tb, (long long)nq, d_queries, d_results,
+                                                                         d_ctr);
+    else
+        esa_batch<MAPA_W, 0><<<grid, kBlock, smem, (cudaStream_t)stream>>>(tb, (long long)nq, d_queries, d_results,
+                                                                         d_ctr);
+    return (int)cudaGetLastError();
+}
+
+int MAPA_CAT(occ_batch_w, MAPA_W)(int canon, int smem) {
+    const void *f = canon ? (const void *)esa_batch<MAPA_W, 1> : (const void *)esa_batch<MAPA_W, 0>;
+    int nb = 0;
+    if (set_smem(f, smem) != 0) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kBlock, smem) != cudaSuccess) return 1;
+    return nb > 0 ? nb : 1;
+}
+
+int MAPA_CAT(launch_trace_w, MAPA_W)(const MultiTables &tb, int canon, int ntraces, int nops,
+                                     const mapa_trace_op *d_ops, int njobs, const mapa_query *d_jobs,
+                                     uint64_t *d_keys, void *stream) {
+    const int smem = smem_bytes(tb);
+    unsigned long long *k = reinterpret_cast<unsigned long long *>(d_keys);
+    const void *f = canon ? (const void *)esa_trace<MAPA_W, 1> : (const void *)esa_trace<MAPA_W, 0>;
+    int err = set_smem(f, smem);
+    if (err) return err;
+    if (canon)
+        esa_trace<MAPA_W, 1><<<ntraces, kBlock, smem, (cudaStream_t)stream>>>(tb, nops, d_ops, njobs, d_jobs, k);
+    else
+        esa_trace<MAPA_W, 0><<<ntraces, kBlock, smem, (cudaStream_t)stream>>>(tb, nops, d_ops, njobs, d_jobs, k);
+    return (int)cudaGetLastError();
+}
+
+int MAPA_CAT(smem_shared_w, MAPA_W)() { return (int)sizeof(Shared); }
+
+}  // namespace mapa

@@ -80,15 +80,16 @@ struct LaunchCfg {
 };
 
 // Kernel launchers (esa.cu).  Return cudaError_t as int.
-int launch_single(const SingleTables &tb, int selector, int sensitive, const mapa_query *d_query, mapa_record *d_record,
-                  int depth, int rank, int world, int chunk, int grid, void *stream);
-int launch_batch(const MultiTables &tb, int64_t nq, const mapa_query *d_queries,
+// sc = sel_code(...) | 4 * canonical; canon = 1 unless MAPA_F_RAW.
+int launch_single(const SingleTables &tb, int sc, const mapa_query *d_query, mapa_record *d_record, int depth,
+                  int rank, int world, int stripe, int grid, void *stream);
+int launch_batch(const MultiTables &tb, int canon, int64_t nq, const mapa_query *d_queries,
                  mapa_record *d_results, uint32_t *d_ctr, int grid, void *stream);
-int launch_trace(const MultiTables &tb, int ntraces, int nops, const mapa_trace_op *d_ops, int njobs,
+int launch_trace(const MultiTables &tb, int canon, int ntraces, int nops, const mapa_trace_op *d_ops, int njobs,
                  const mapa_query *d_jobs, uint64_t *d_keys, void *stream);
 int device_sm_count();
 int max_blocks_per_sm_single(int width, int k, int sc, int xs);
-int max_blocks_per_sm_batch(int width, int npats, int xs);
+int max_blocks_per_sm_batch(int width, int canon, int npats, int xs);
 const char *cuda_error_string(int err);
 
 }  // namespace mapa

@@ -348,6 +348,18 @@ struct Plan {
     uint64_t nlocal;
 };
 
+bool has_constraints(const DevPattern &dp) {
+    for (int j = 0; j < 8; ++j)
+        if (dp.fwd_src[j]) return true;
+    return false;
+}
+
+int multi_has_constraints(const MultiTables &tb) {
+    for (int i = 0; i < tb.npats; ++i)
+        if (has_constraints(tb.pat[i])) return 1;
+    return 0;
+}
+
 Plan plan_single(const mapa_topology *t, const mapa_pattern *p, int sensk, int nF, int world) {
     Plan pl{};
     const int W = t->width, G = 32 / W, k = p->k;
@@ -616,9 +628,6 @@ mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int
     if (selector < 0 || selector > 2) return fail(MAPA_E_INVALID_ARG, "bad selector");
     if (!key_fits(t, p)) return fail(MAPA_E_UNSUPPORTED, "key budget 15 + W + C(k,2) > 63");
     const int nF = busy_hint == 0xFFFFFFFFu ? t->n : __builtin_popcount(~busy_hint & nmask_of(t->n));
-    const int sensk = sel_code(selector, sensitive);
-    Plan pl = plan_single(t, p, sensk, nF, world);
-    if (pl.nlocal >= (1ull << 27)) return fail(MAPA_E_UNSUPPORTED, "too many work items");
     static_assert(sizeof(SingleTables) < 32000, "kernel parameter block too large");
     SingleTables tb;
     std::memset(&tb, 0, sizeof(tb));
@@ -626,10 +635,15 @@ mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int
     tb.npats = 1;
     tb.xs = pick_xs(p->m);
     fill_devpattern(p, (flags & MAPA_F_RAW) != 0, 0, tb.pat[0]);
+    // canonical instantiation only when a lex-leader constraint exists (|Aut| > 1
+    // and not RAW); otherwise the constraint-free kernel enumerates the same set
+    const int sc = sel_code(selector, sensitive) | (has_constraints(tb.pat[0]) ? 4 : 0);
+    Plan pl = plan_single(t, p, sc, nF, world);
+    if (pl.nlocal >= (1ull << 27)) return fail(MAPA_E_UNSUPPORTED, "too many work items");
     std::memcpy(tb.lut, p->lut.data(), p->lut.size() * sizeof(uint16_t));
     int err = (int)cudaMemsetAsync(d_record, 0, sizeof(mapa_record), (cudaStream_t)stream);
     if (err) return cuda_fail(err, "cudaMemsetAsync");
-    err = launch_single(tb, selector, sensitive, d_query, d_record, pl.depth, rank, world, pl.chunk, pl.grid, stream);
+    err = launch_single(tb, sc, d_query, d_record, pl.depth, rank, world, pl.chunk, pl.grid, stream);
     if (err) return cuda_fail(err, "esa_single launch");
     return MAPA_OK;
 }
@@ -713,8 +727,9 @@ mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *cons
     if ((err = (int)cudaMemsetAsync(d_scratch, 0, 64, st))) return cuda_fail(err, "memset");
     int sm = device_sm_count();
     if (sm <= 0) sm = 148;
-    const int grid = sm * max_blocks_per_sm_batch(t->width, tbp->npats, tbp->xs);
-    err = launch_batch(*tbp, nq, d_queries, d_results, (uint32_t *)d_scratch, grid, stream);
+    const int canon = multi_has_constraints(*tbp);
+    const int grid = sm * max_blocks_per_sm_batch(t->width, canon, tbp->npats, tbp->xs);
+    err = launch_batch(*tbp, canon, nq, d_queries, d_results, (uint32_t *)d_scratch, grid, stream);
     if (err) return cuda_fail(err, "esa_batch launch");
     return MAPA_OK;
 }
@@ -731,7 +746,7 @@ mapa_status mapa_trace_replay(const mapa_topology *t, const mapa_pattern *const 
     if (s != MAPA_OK) return s;
     int err = (int)cudaMemsetAsync(d_keys, 0, (size_t)ntraces * njobs * sizeof(uint64_t), (cudaStream_t)stream);
     if (err) return cuda_fail(err, "memset");
-    err = launch_trace(*tbp, ntraces, nops, d_ops, njobs, d_jobs, d_keys, stream);
+    err = launch_trace(*tbp, multi_has_constraints(*tbp), ntraces, nops, d_ops, njobs, d_jobs, d_keys, stream);
     if (err) return cuda_fail(err, "esa_trace launch");
     return MAPA_OK;
 }
