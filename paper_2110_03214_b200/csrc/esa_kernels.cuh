@@ -65,6 +65,9 @@ template <int SEL>
 struct SelT {
     static constexpr int base = SEL & 3;
     static constexpr bool canon = (SEL & 4) != 0;
+    static constexpr bool multi = (SEL & 8) != 0;      // batch / trace kernels (many patterns per block)
+    // single-query Eq. 2 scans use 16-bit packed tables and columns (pack16)
+    static constexpr bool pack16 = base == SEL_SENS && !multi;
     static constexpr bool lin = base != SEL_SENS;      // additive score (Eq. 1 / Eq. 3 / 0)
     static constexpr bool useU = base == SEL_INSENS;   // Eq. 3 sums over every placed device
     static constexpr int wt = base == SEL_BASE ? 0 : 1;
@@ -78,7 +81,7 @@ constexpr int kNeg = -(1 << 28);
 
 // Per-warp candidate lists of the innermost DFS levels (G groups x W).
 struct WarpLists {
-    int dense[32];  // level k-2: per device, increment of placing k-2 there (or a sentinel)
+    int dense[2][32];  // level k-2 (two v3 at a time): per device, increment of placing k-2 there (or a sentinel)
     int2 l3[32];    // level k-3: (v, increment of placing k-3 on v)
 };
 
@@ -101,7 +104,8 @@ struct Shared {
     unsigned long long key[kWarps], cnt[kWarps];
     uint8_t edge[kMaxPats][28];
     uint32_t busy;
-    uint32_t pad[3];
+    int one;  // = 1 (Ctx::one)
+    uint32_t pad[2];
 };
 
 // Single-query kernels: Shared + one Eq. 2 table of 3 xs^2 ints, xs <= 40.
@@ -129,6 +133,7 @@ struct Ctx {
     int pid;                        // pattern index (edge list in smem)
     uint64_t fb, fs, db;            // bytes: fwd_back, fwd_src, dback
     int clique, eb, m;
+    int one;                        // 1, read from shared memory (see scan_dense)
     int col[W];                     // lane's inner-scan column (see lane_column)
 };
 
@@ -147,6 +152,7 @@ struct Best {
     uint32_t bs;   // score of key
     uint32_t cnt;  // leaves scored
     int thr;       // (bs + 1) * 32: a scan's packed rank must reach this to matter
+    uint32_t sb;   // brev_W(device set) of key (0 while no key)
 };
 
 template <int SEL>
@@ -203,21 +209,20 @@ __device__ __noinline__ unsigned long long make_key(uint32_t S, unsigned long lo
     return ((unsigned long long)s << (W + eb)) | ((unsigned long long)sb << eb) | ecode;
 }
 
+// Called when a leaf's score s >= the lane's best score.  An equal score wins
+// only through the device-set field (brev_W(S), kept in a register), or, for
+// the same set of a non-clique pattern, through the edge code.
 template <int W, int K>
 __device__ __forceinline__ void consider(const Ctx<W> &c, Best &bst, uint32_t S, unsigned long long fpack,
                                          uint32_t s) {
-    if (s == bst.bs && bst.key) {
-        // equal score: the device-set field decides unless the sets are equal
-        const uint32_t sb_new = __brev(S) >> (32 - W);
-        const uint32_t sb_old = (uint32_t)(bst.key >> c.eb) & (W >= 32 ? kFull : ((1u << W) - 1u));
-        if (sb_new < sb_old) return;
-        if (sb_new == sb_old && c.clique) return;  // same set, clique: identical key
-    }
+    const uint32_t sbn = __brev(S) >> (32 - W);
+    if (s == bst.bs && (sbn < bst.sb || (sbn == bst.sb && c.clique))) return;
     const unsigned long long key = make_key<W, K>(S, fpack, (uint32_t)c.b, s, c.clique, c.eb, c.m, c.pid);
     if (key > bst.key) {
         bst.key = key;
         bst.bs = s;
         bst.thr = ((int)s + 1) * 32;
+        bst.sb = sbn;
     }
 }
 
@@ -273,49 +278,119 @@ __device__ __forceinline__ void leaf_k1(const Ctx<W> &c, Best &bst) {
 // compile-time indices) and keeps the max.  Within one scan a lane's leaves
 // differ only in v, and among equal scores the smaller v is the lex-smaller
 // device set (larger key), so the packed rank (score+1)*32 + (31-v) decides
-// and the full key is built once, later.  Returns < 32 when no valid leaf.
-//   LIN:  rank = base + tab[v] + col[v],     tab = 32 t2 | kNeg, col = T[v][b] + 31 - v
-//   SENS: rank = lut[base + tab[v] + col[v]] + 31 - v,  tab = t2 | kSent, col = D[v][b]
+// and the full key is built once, later.  Returns the max over v of
+//   LIN:  tab[v] + col[v] (the rank minus `base`, added by the caller after
+//         the threshold test, which keeps it off the dependency chain),
+//         tab = 32 t2 | kNeg, col = T[v][b] + 31 - v
+//   SENS: lut[base + tab[v] + col[v]] + 31 - v (the rank),  tab = t2 | kSent, col = D[v][b]
+// The rank is < 32 when no leaf is valid.
+// pack16 (single-query Eq. 2): the table holds 16-bit byte offsets and the
+// lane's column holds two 16-bit offsets per register, so one LDS.128 brings 8
+// table entries (broadcast loads cost 2 wavefronts each whatever their width)
+// and one IADD3 forms two LUT addresses (every LUT byte offset is < 3*40*40*4
+// < 2^16, so the halves never carry into each other).
 template <int W, int SEL>
-__device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2, int base) {
-    const uint32_t b = (uint32_t)c.b;
-    int *tab = sh().wl[c.warp].dense + c.g * W;
-    const bool mine = (cand >> b) & 1u;
-    __syncwarp(c.gmask);  // previous readers of the table are done
-    if constexpr (SelT<SEL>::lin) tab[b] = mine ? t2 * 32 : kNeg;
-    else tab[b] = 4 * (mine ? t2 : c.xs * c.xs);  // byte offsets into the Eq. 2 table
-    __syncwarp(c.gmask);
+__device__ __forceinline__ int *tab_ptr(const Ctx<W> &c, int which) {
+    int *t = sh().wl[c.warp].dense[which];
+    if constexpr (SelT<SEL>::pack16) return reinterpret_cast<int *>(reinterpret_cast<uint16_t *>(t) + c.g * W);
+    else return t + c.g * W;
+}
+
+template <int W, int SEL>
+__device__ __forceinline__ void tab_put(const Ctx<W> &c, int *tab, int v) {
+    if constexpr (SelT<SEL>::pack16) reinterpret_cast<uint16_t *>(tab)[c.b] = (uint16_t)v;
+    else tab[c.b] = v;
+}
+
+template <int W, int SEL>
+__device__ __forceinline__ int tab_entry(const Ctx<W> &c, uint32_t cand, int t2) {
+    const bool mine = (cand >> c.b) & 1u;
+    if constexpr (SelT<SEL>::lin) return mine ? t2 * 32 : kNeg;
+    else return 4 * (mine ? t2 : c.xs * c.xs);  // byte offsets into the Eq. 2 table
+}
+
+template <int W, int SEL>
+__device__ __forceinline__ int tab_scan(const Ctx<W> &c, const int *tab, int base) {
+    if constexpr (SelT<SEL>::pack16) {
+        const uint4 *t8 = reinterpret_cast<const uint4 *>(tab);
+        const char *lut = reinterpret_cast<const char *>(sh_lut());  // pid 0: c.lut == 0
+        const uint32_t b4 = __funnelshift_l(0u, (uint32_t)base, 2);
+        const uint32_t bp = b4 | (b4 << 16);
+        const int one = c.one;
+        int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+        for (int q = 0; q < W / 8; ++q) {
+            const uint4 e = t8[q];
+            const uint32_t s0 = bp + e.x + (uint32_t)c.col[4 * q + 0];
+            const uint32_t s1 = bp + e.y + (uint32_t)c.col[4 * q + 1];
+            const uint32_t s2 = bp + e.z + (uint32_t)c.col[4 * q + 2];
+            const uint32_t s3 = bp + e.w + (uint32_t)c.col[4 * q + 3];
+            const int v = 8 * q;
+            a0 = max(a0, max(lds_off(reinterpret_cast<const int *>(lut), s0 & 0xFFFFu) * one + (31 - v),
+                             lds_off(reinterpret_cast<const int *>(lut), __umulhi(s0, 0x10000u)) * one + (30 - v)));
+            a1 = max(a1, max(lds_off(reinterpret_cast<const int *>(lut), s1 & 0xFFFFu) * one + (29 - v),
+                             lds_off(reinterpret_cast<const int *>(lut), __umulhi(s1, 0x10000u)) * one + (28 - v)));
+            a2 = max(a2, max(lds_off(reinterpret_cast<const int *>(lut), s2 & 0xFFFFu) * one + (27 - v),
+                             lds_off(reinterpret_cast<const int *>(lut), __umulhi(s2, 0x10000u)) * one + (26 - v)));
+            a3 = max(a3, max(lds_off(reinterpret_cast<const int *>(lut), s3 & 0xFFFFu) * one + (25 - v),
+                             lds_off(reinterpret_cast<const int *>(lut), __umulhi(s3, 0x10000u)) * one + (24 - v)));
+        }
+        return max(max(a0, a1), max(a2, a3));
+    }
     const int4 *t4 = reinterpret_cast<const int4 *>(tab);
     int best = 0;
+    // Pipe balance: the integer ALU pipe (add-max, 3-input max, address adds)
+    // and the FMA pipe (IMAD) each retire a warp instruction every 2 cycles.
+    // A fused add-max costs one ALU slot per leaf; an add done as IMAD x*one+y
+    // (c.one = 1 at run time, so the compiler keeps the IMAD) followed by a
+    // 3-input max over two leaves costs one FMA slot + half an ALU slot.
     if constexpr (SelT<SEL>::lin) {
-        // four independent fused add-max chains (VIADDMNMX), base added once
-        int b0 = kNeg, b1 = kNeg, b2 = kNeg, b3 = kNeg;
+        // four independent fused add-max chains (VIADDMNMX); measured faster
+        // than moving part of the adds to the FMA pipe (the loop is latency-,
+        // not pipe-bound at 4 warps per scheduler)
+        const int4 e0 = t4[0];
+        int b0 = e0.x + c.col[0], b1 = e0.y + c.col[1], b2 = e0.z + c.col[2], b3 = e0.w + c.col[3];
 #pragma unroll
-        for (int q = 0; q < W / 4; ++q) {
+        for (int q = 1; q < W / 4; ++q) {
             const int4 e = t4[q];
             b0 = max(b0, e.x + c.col[4 * q + 0]);
             b1 = max(b1, e.y + c.col[4 * q + 1]);
             b2 = max(b2, e.z + c.col[4 * q + 2]);
             b3 = max(b3, e.w + c.col[4 * q + 3]);
         }
-        best = max(0, max(max(b0, b1), max(b2, b3)) + base);
+        best = max(max(b0, b1), max(b2, b3));
     } else {
-        // table, column and base are byte offsets: one IADD3 gives the address
-        // table, column and base are byte offsets into the Eq. 2 table
-        const int *lut = sh_lut() + c.lut;
-        const int b4 = 4 * base;
+        // table, column and base are byte offsets into the Eq. 2 table: one
+        // IADD3 per leaf gives the address.  4*base goes through a funnel shift
+        // so that the compiler does not re-split the sum into a multiply-add
+        // per leaf.
+        const int *lb = reinterpret_cast<const int *>(reinterpret_cast<const char *>(sh_lut() + c.lut) +
+                                                      (int)__funnelshift_l(0u, (uint32_t)base, 2));
+        // the (31 - v) tie-break goes in as IMAD r*one + (31-v), two leaves per 3-input max
+        int b0 = 0, b1 = 0;
+        const int one = c.one;
 #pragma unroll
         for (int q = 0; q < W / 4; ++q) {
             const int4 e = t4[q];
-            const int r0 = lds_off(lut, b4 + e.x + c.col[4 * q + 0]) + (31 - (4 * q + 0));
-            const int r1 = lds_off(lut, b4 + e.y + c.col[4 * q + 1]) + (31 - (4 * q + 1));
-            const int r2 = lds_off(lut, b4 + e.z + c.col[4 * q + 2]) + (31 - (4 * q + 2));
-            const int r3 = lds_off(lut, b4 + e.w + c.col[4 * q + 3]) + (31 - (4 * q + 3));
-            best = max(best, max(r0, r1));
-            best = max(best, max(r2, r3));
+            const int r0 = lds_off(lb, e.x + c.col[4 * q + 0]) * one + (31 - (4 * q + 0));
+            const int r1 = lds_off(lb, e.y + c.col[4 * q + 1]) * one + (31 - (4 * q + 1));
+            const int r2 = lds_off(lb, e.z + c.col[4 * q + 2]) * one + (31 - (4 * q + 2));
+            const int r3 = lds_off(lb, e.w + c.col[4 * q + 3]) * one + (31 - (4 * q + 3));
+            b0 = max(b0, max(r0, r1));
+            b1 = max(b1, max(r2, r3));
         }
+        best = max(b0, b1);
     }
     return best;
+}
+
+template <int W, int SEL>
+__device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2, int base) {
+    int *tab = tab_ptr<W, SEL>(c, 0);
+    __syncwarp(c.gmask);  // previous readers of the table are done
+    tab_put<W, SEL>(c, tab, tab_entry<W, SEL>(c, cand, t2));
+    __syncwarp(c.gmask);
+    return tab_scan<W, SEL>(c, tab, base);
 }
 
 // The two innermost levels: vertex k-2 walks the devices of `cand`, vertex
@@ -346,8 +421,11 @@ __device__ __forceinline__ void inner(const Ctx<W> &c, const St<K> &st, uint32_t
     // leaves counted: v in cand with v != b (and v < b if canonical-ordered)
     const uint32_t M = laneok ? (dep ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
     bst.cnt += (uint32_t)__popc(M & cand);
-    const int best = scan_dense<W, SEL>(c, cand, t2, base);
-    if (laneok && best >= bst.thr) {  // best >= 32 and its score >= the lane's best score
+    const int off = SelT<SEL>::lin ? base : 0;
+    const int thr = bst.thr - off;
+    const int raw = scan_dense<W, SEL>(c, cand, t2, base);
+    if (laneok && raw >= thr) {  // rank >= 32 and its score >= the lane's best score
+        const int best = raw + off;
         const uint32_t s = (uint32_t)(best >> 5) - 1u;
         {
             const uint32_t bestv = 31u - (uint32_t)(best & 31);
@@ -414,27 +492,75 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
         const uint32_t nb = ~(1u << b);
         bst.cnt += (uint32_t)(__popc(cand3 & nb) * __popc(cand2b & nb) - __popc(cand3 & cand2b & nb));
     }
-    for (uint32_t i = 0; i < n3; ++i) {
-        const int2 e3 = L3[i];
-        const uint32_t v3 = (uint32_t)e3.x;
-        const int w3 = wcol[v3 * 32];
-        const int t2 = t2b + m32 * w3;
-        const int lp = lpb + m31 * w3;
-        const uint32_t cand2 = cand2b & ~(1u << v3) & (d32 ? (0xFFFFFFFEu << v3) : kFull);
-        const bool laneok = okb && b != v3 && (!d31 || b > v3);
-        if (dep) {
-            const uint32_t M = laneok ? (d21 ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
-            bst.cnt += (uint32_t)__popc(M & cand2);
-        }
-        const int base = (SelT<SEL>::lin) ? (A + e3.y + lp + 1) * 32 : A + e3.y + lp;
-        const int best = scan_dense<W, SEL>(c, cand2, t2, base);
-        if (laneok && best >= bst.thr) {  // best >= 32 and its score >= the lane's best score
-            const uint32_t s = (uint32_t)(best >> 5) - 1u;
-            {
-                const uint32_t bestv = 31u - (uint32_t)(best & 31);
+    if constexpr (!SelT<SEL>::lin) {
+        // Eq. 2: one v3 per iteration (the scan is shared-memory bound; pairing
+        // measured slower)
+        for (uint32_t i = 0; i < n3; ++i) {
+            const int2 e3 = L3[i];
+            const uint32_t v3 = (uint32_t)e3.x;
+            const int w3 = wcol[v3 * 32];
+            const uint32_t cand2 = cand2b & ~(1u << v3) & (d32 ? (0xFFFFFFFEu << v3) : kFull);
+            const bool laneok = okb && b != v3 && (!d31 || b > v3);
+            if (dep) {
+                const uint32_t M = laneok ? (d21 ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
+                bst.cnt += (uint32_t)__popc(M & cand2);
+            }
+            const int raw = scan_dense<W, SEL>(c, cand2, t2b + m32 * w3, A + e3.y + lpb + m31 * w3);
+            if (laneok && raw >= bst.thr) {  // rank >= 32 and its score >= the lane's best score
+                const uint32_t bestv = 31u - (uint32_t)(raw & 31);
                 const unsigned long long fpack =
                     fbase | ((unsigned long long)v3 << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
-                consider<W, K>(c, bst, st.U | (1u << v3) | (1u << bestv) | (1u << b), fpack, s);
+                consider<W, K>(c, bst, st.U | (1u << v3) | (1u << bestv) | (1u << b), fpack,
+                               (uint32_t)(raw >> 5) - 1u);
+            }
+        }
+        return;
+    }
+    // two v3 per iteration (tables A and B): twice the independent work
+    // between the warp syncs and one threshold branch for both scans
+    int *tabA = tab_ptr<W, SEL>(c, 0);
+    int *tabB = tab_ptr<W, SEL>(c, 1);
+    for (uint32_t i = 0; i < n3; i += 2) {
+        const bool hasB = i + 1 < n3;
+        const int2 eA = L3[i], eB = L3[hasB ? i + 1 : i];
+        const uint32_t vA = (uint32_t)eA.x, vB = (uint32_t)eB.x;
+        const int wA = wcol[vA * 32], wB = wcol[vB * 32];
+        const uint32_t cA = cand2b & ~(1u << vA) & (d32 ? (0xFFFFFFFEu << vA) : kFull);
+        const uint32_t cB = cand2b & ~(1u << vB) & (d32 ? (0xFFFFFFFEu << vB) : kFull);
+        const bool okA = okb && b != vA && (!d31 || b > vA);
+        const bool okB = hasB && okb && b != vB && (!d31 || b > vB);
+        if (dep) {
+            const uint32_t M = d21 ? ((1u << b) - 1u) : ~(1u << b);
+            bst.cnt += (uint32_t)(okA ? __popc(M & cA) : 0) + (uint32_t)(okB ? __popc(M & cB) : 0);
+        }
+        const int lpA = lpb + m31 * wA, lpB = lpb + m31 * wB;
+        const int baseA = (SelT<SEL>::lin) ? (A + eA.y + lpA + 1) * 32 : A + eA.y + lpA;
+        const int baseB = (SelT<SEL>::lin) ? (A + eB.y + lpB + 1) * 32 : A + eB.y + lpB;
+        const int offA = SelT<SEL>::lin ? baseA : 0, offB = SelT<SEL>::lin ? baseB : 0;
+        __syncwarp(c.gmask);  // previous readers of the tables are done
+        tab_put<W, SEL>(c, tabA, tab_entry<W, SEL>(c, cA, t2b + m32 * wA));
+        tab_put<W, SEL>(c, tabB, tab_entry<W, SEL>(c, cB, t2b + m32 * wB));
+        __syncwarp(c.gmask);
+        const int rawA = tab_scan<W, SEL>(c, tabA, baseA);
+        const int rawB = tab_scan<W, SEL>(c, tabB, baseB);
+        const bool hitA = okA && rawA >= bst.thr - offA;
+        const bool hitB = okB && rawB >= bst.thr - offB;
+        if (hitA || hitB) {  // a rank >= 32 whose score >= the lane's best score
+            if (hitA) {
+                const int best = rawA + offA;
+                const uint32_t bestv = 31u - (uint32_t)(best & 31);
+                const unsigned long long fpack =
+                    fbase | ((unsigned long long)vA << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
+                consider<W, K>(c, bst, st.U | (1u << vA) | (1u << bestv) | (1u << b), fpack,
+                               (uint32_t)(best >> 5) - 1u);
+            }
+            if (hitB && rawB >= bst.thr - offB) {
+                const int best = rawB + offB;
+                const uint32_t bestv = 31u - (uint32_t)(best & 31);
+                const unsigned long long fpack =
+                    fbase | ((unsigned long long)vB << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
+                consider<W, K>(c, bst, st.U | (1u << vB) | (1u << bestv) | (1u << b), fpack,
+                               (uint32_t)(best >> 5) - 1u);
             }
         }
     }
@@ -565,7 +691,7 @@ __device__ __forceinline__ void run_range(const Ctx<W> &c, uint32_t lo, uint32_t
 // writes this warp's inc_F table.
 template <int W>
 __device__ __forceinline__ Ctx<W> make_ctx(const DevTopo &topo, const DevPattern &P, int pid, int xs, uint32_t busy,
-                                           int sc) {
+                                           int sc, bool pack16) {
     const int lane = threadIdx.x & 31;
     Ctx<W> c;
     const uint32_t nmask = topo.n >= 32 ? kFull : ((1u << topo.n) - 1u);
@@ -602,6 +728,7 @@ __device__ __forceinline__ Ctx<W> make_ctx(const DevTopo &topo, const DevPattern
     c.pid = pid;
     c.xs = xs;
     c.lut = pid * 3 * xs * xs;
+    c.one = sh().one;
     sc &= 3;
     const bool useU = sc == SEL_INSENS;
     const int w12 = sc == SEL_BASE ? 0 : 12;
@@ -620,7 +747,11 @@ __device__ __forceinline__ Ctx<W> make_ctx(const DevTopo &topo, const DevPattern
     const int *T = sens ? (eK ? (dep ? sh().tsed : sh().tse) : (dep ? sh().ts0d : sh().ts0))
                         : (eW ? (dep ? sh().twd : sh().tw) : (dep ? sh().tzd : sh().tz));
 #pragma unroll
-    for (int v = 0; v < W; ++v) c.col[v] = sens ? 4 * T[v * 32 + c.b] : T[v * 32 + c.b] + 31 - v;
+    for (int v = 0; v < W; ++v) c.col[v] = sens ? T[v * 32 + c.b] : T[v * 32 + c.b] + 31 - v;
+    if (pack16) {  // SelT::pack16: col[j] = col(2j) | col(2j+1) << 16 (byte offsets < 2^16)
+#pragma unroll
+        for (int j = 0; j < W / 2; ++j) c.col[j] = (c.col[2 * j] & 0xFFFF) | (c.col[2 * j + 1] << 16);
+    }
     __syncwarp();
     return c;
 }
@@ -643,6 +774,7 @@ __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int 
     const DevTopo &topo = tb.topo;
     const int tid = threadIdx.x;
     if (tid < kMaxN) s.cm[tid] = make_uint4(topo.cm[tid][0], topo.cm[tid][1], topo.cm[tid][2], topo.cm[tid][3]);
+    if (tid == 0) s.one = 1;
     if (tid <= kMaxN) s.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
     const int sent = xs * xs;
     for (int i = tid; i < kNN; i += blockDim.x) {
@@ -661,10 +793,10 @@ __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int 
         s.tzd[i] = badd ? kNeg : 0;
         s.twp[i] = bad ? 0 : w;
         s.tdl[i] = d;
-        s.tse[i] = d + (bad ? sent : 0);
-        s.tsed[i] = d + (badd ? sent : 0);
-        s.ts0[i] = bad ? sent : 0;
-        s.ts0d[i] = badd ? sent : 0;
+        s.tse[i] = 4 * (d + (bad ? sent : 0));  // byte offsets (see scan_dense)
+        s.tsed[i] = 4 * (d + (badd ? sent : 0));
+        s.ts0[i] = 4 * (bad ? sent : 0);
+        s.ts0d[i] = 4 * (badd ? sent : 0);
     }
     int *lut = sh_lut();
     for (int p = 0; p < tb.npats; ++p) {
@@ -697,7 +829,7 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
     const uint32_t busy = dq->busy;
     __syncthreads();
 
-    Ctx<W> c = make_ctx<W>(tb.topo, tb.pat[0], 0, xs, busy, SEL & 3);
+    Ctx<W> c = make_ctx<W>(tb.topo, tb.pat[0], 0, xs, busy, SEL & 3, SelT<SEL>::pack16);
 
     // Rank r owns the stripes s = r, r + world, ... of `stripe` consecutive
     // items; its local item space is their concatenation.  Warps grab local
@@ -710,7 +842,7 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
     const bool ownLast = nS > 0 && ((nS - 1u) % (uint32_t)world) == (uint32_t)rank;
     const uint32_t Nloc = myS == 0 ? 0u : (ownLast ? (myS - 1u) * L + (N - (nS - 1u) * L) : myS * L);
     const uint32_t P = gridDim.x * (uint32_t)kWarps;
-    Best bst{0ull, 0u, 0u, 32};
+    Best bst{0ull, 0u, 0u, 32, 0u};
     const uint32_t g = (uint32_t)(lane / W);
     for (;;) {
         uint32_t start = 0, sz = 0;
@@ -809,15 +941,15 @@ esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query
             continue;
         }
         const DevPattern &P = tb.pat[pid];
-        Ctx<W> c = make_ctx<W>(tb.topo, P, (int)pid, xs, qu.busy, sel_code(qu.selector, qu.sensitive));
+        Ctx<W> c = make_ctx<W>(tb.topo, P, (int)pid, xs, qu.busy, sel_code(qu.selector, qu.sensitive), false);
         if (P.k > c.nF) continue;
         const uint32_t j = (uint32_t)(base % W) + g;
-        Best bst{0ull, 0u, 0u, 32};
+        Best bst{0ull, 0u, 0u, 32, 0u};
         switch (sel_code(qu.selector, qu.sensitive)) {
-            case SEL_GREEDY: batch_dispatch_k<W, SEL_GREEDY | 4 * CANON>(P.k, c, j, bst); break;
-            case SEL_INSENS: batch_dispatch_k<W, SEL_INSENS | 4 * CANON>(P.k, c, j, bst); break;
-            case SEL_SENS: batch_dispatch_k<W, SEL_SENS | 4 * CANON>(P.k, c, j, bst); break;
-            default: batch_dispatch_k<W, SEL_BASE | 4 * CANON>(P.k, c, j, bst); break;
+            case SEL_GREEDY: batch_dispatch_k<W, SEL_GREEDY | 4 * CANON | 8>(P.k, c, j, bst); break;
+            case SEL_INSENS: batch_dispatch_k<W, SEL_INSENS | 4 * CANON | 8>(P.k, c, j, bst); break;
+            case SEL_SENS: batch_dispatch_k<W, SEL_SENS | 4 * CANON | 8>(P.k, c, j, bst); break;
+            default: batch_dispatch_k<W, SEL_BASE | 4 * CANON | 8>(P.k, c, j, bst); break;
         }
         __syncwarp();
         unsigned long long key = bst.key, cnt = bst.cnt;
@@ -882,16 +1014,16 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
         const DevPattern &P = tb.pat[ep];
         if (cur.op == 0) {
             const uint32_t busy = sh().busy;
-            Ctx<W> c = make_ctx<W>(tb.topo, P, ep, xs, busy, sel_code(qu.selector, qu.sensitive));
-            Best bst{0ull, 0u, 0u, 32};
+            Ctx<W> c = make_ctx<W>(tb.topo, P, ep, xs, busy, sel_code(qu.selector, qu.sensitive), false);
+            Best bst{0ull, 0u, 0u, 32, 0u};
             if (okp && P.k <= c.nF) {
                 const int D = (P.k - 1) < 2 ? (P.k - 1) : 2;
                 const uint32_t nItems = perm_count(c.nF, D);
                 switch (sel_code(qu.selector, qu.sensitive)) {
-                    case SEL_GREEDY: trace_dispatch_k<W, SEL_GREEDY | 4 * CANON>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
-                    case SEL_INSENS: trace_dispatch_k<W, SEL_INSENS | 4 * CANON>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
-                    case SEL_SENS: trace_dispatch_k<W, SEL_SENS | 4 * CANON>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
-                    default: trace_dispatch_k<W, SEL_BASE | 4 * CANON>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
+                    case SEL_GREEDY: trace_dispatch_k<W, SEL_GREEDY | 4 * CANON | 8>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
+                    case SEL_INSENS: trace_dispatch_k<W, SEL_INSENS | 4 * CANON | 8>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
+                    case SEL_SENS: trace_dispatch_k<W, SEL_SENS | 4 * CANON | 8>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
+                    default: trace_dispatch_k<W, SEL_BASE | 4 * CANON | 8>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
                 }
             }
             __syncwarp();
