@@ -32,11 +32,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         os.makedirs(objdir, exist_ok=True)
         objs = [os.path.join(objdir, os.path.basename(src) + ".o") for src in SOURCES]
 
+        hdr_t = max(os.path.getmtime(h) for h in HEADERS)
+
         def compile_one(i):
+            # incremental: an object is rebuilt when its source or any header is newer
+            if not force and os.path.exists(objs[i]) and \
+                    os.path.getmtime(objs[i]) > max(os.path.getmtime(SOURCES[i]), hdr_t):
+                return None
             return subprocess.run([NVCC] + FLAGS + ["-c", "-o", objs[i], SOURCES[i]], capture_output=True, text=True)
 
         with ThreadPoolExecutor(len(SOURCES)) as ex:
-            results = list(ex.map(compile_one, range(len(SOURCES))))
+            results = [r for r in ex.map(compile_one, range(len(SOURCES))) if r is not None]
         log = "".join(r.stderr for r in results)
         for r in results:
             if r.returncode != 0:
@@ -44,8 +50,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run([NVCC] + LINK + ["-o", LIB + ".tmp"] + objs, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
-        with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
-            f.write(log)
+        if log:
+            with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
+                f.write(log)
         os.replace(LIB + ".tmp", LIB)
         if verbose:
             print(log)

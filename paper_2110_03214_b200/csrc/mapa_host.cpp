@@ -328,13 +328,21 @@ uint64_t perm_count(int n, int d) {
 // (dx, dy) rarely hit the same shared-memory bank (32 banks of 4 B):
 // minimises #{(dx, dy) != 0, |dx|,|dy| <= 5 : 32 | xs*dx + dy}.
 int pick_xs(int m) {
-    int best = m + 1, bestc = 1 << 30;
+    // Row stride of the Eq. 2 table index x*xs + y.  The lanes of a warp read
+    // entries whose censuses differ by small (dx, dy) with few 12-links
+    // (|dx + dy| small); a pair conflicts on a shared-memory bank when
+    // xs*dx + dy == 0 (mod 32).  Score each xs by the conflicting pairs,
+    // weighted by how likely such a census difference is, and keep the
+    // cheapest (ties: the smallest table).
+    int best = m + 1;
+    double bestc = 1e30;
     for (int xs = m + 1; xs <= std::max(m + 1, 40); ++xs) {
-        int cnt = 0;
-        for (int dx = -5; dx <= 5; ++dx)
-            for (int dy = -5; dy <= 5; ++dy)
-                if ((dx || dy) && ((xs * dx + dy) % 32 + 32) % 32 == 0) ++cnt;
-        if (cnt < bestc) { bestc = cnt; best = xs; }
+        double cost = 0.0;
+        for (int dx = -6; dx <= 6; ++dx)
+            for (int dy = -6; dy <= 6; ++dy)
+                if ((dx || dy) && ((xs * dx + dy) % 32 + 32) % 32 == 0)
+                    cost += std::exp(-0.5 * (std::abs(dx) + std::abs(dy) + std::abs(dx + dy)));
+        if (cost < bestc - 1e-12) { bestc = cost; best = xs; }
     }
     return best;
 }
