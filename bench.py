@@ -179,6 +179,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="mapa", choices=["mapa", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-prune", action="store_true", help="skip the MAPA_F_PRUNE side measurement")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--config", default="c4", choices=["c4", "c1", "c2", "c3", "c5"],
                     help="c4 = the headline workload (default); c1/c2/c3/c5 measure the other SURVEY 8(d) configs")
@@ -292,6 +293,33 @@ def main():
     kern_ms = {n: sum(a.elapsed_time(b) for a, b in v) / len(v) for n, v in kev.items()}
     dev_ms = max_over_ranks(dev_ms)
 
+    # ---- MAPA_F_PRUNE (branch and bound): same decisions,
+    # fewer embeddings scored; reported beside the headline, never as it
+    prune_ms = {n: [] for _, _, n in SELECTORS}
+    prune_leaves = {}
+    if not args.no_prune:
+        precs = torch.zeros((len(SELECTORS), 4), dtype=torch.int64, device=dev)
+        for it in range(args.warmup + args.steps):
+            for i, (sel, sens, name) in enumerate(SELECTORS):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                mp.launch_query(topo, pat, sel, sens, qbuf.data_ptr(), precs[i].data_ptr(), raw=True, rank=rank,
+                                world=world, busy_hint=busy, stream=stream, prune=True)
+                b.record(stream)
+                if it >= args.warmup:
+                    prune_ms[name].append((a, b))
+            flush.zero_()
+        torch.cuda.synchronize()
+        prl = md.records_from_tensor(precs)
+        for i, (sel, sens, name) in enumerate(SELECTORS):
+            prune_leaves[name] = int(prl[i].leaves)  # rank 0's shard when world > 1
+            if world == 1:  # same decision as the exhaustive launch
+                dp = mp.decode(topo, pat, busy, sel, sens, prl[i], raw=True, prune=True)
+                de = mp.decode(topo, pat, busy, sel, sens, rlist[i], raw=True)
+                assert dp["key"] == de["key"], (name, dp["key"], de["key"])
+    prune_kms = {n: (max_over_ranks(sum(a.elapsed_time(b) for a, b in v) / len(v)) if v else None)
+                 for n, v in prune_ms.items()}
+
     sampler.stop()  # the nvidia-smi poller competes for host cores; clocks are sampled above
     # ---- e2e through the public API (host buffers, copies inside the region)
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 50))
@@ -364,6 +392,15 @@ def main():
             "gpu_launches": len(SELECTORS) * args.steps,
             "clocks": clk,
         }
+        if not args.no_prune:
+            tot = sum(prune_kms.values())
+            line["pruned"] = {
+                "mode": "MAPA_F_PRUNE branch-and-bound (exact: same decisions, asserted against the exhaustive run)",
+                "kernel_ms": prune_kms, "allocations_per_s": len(SELECTORS) / (tot / 1e3),
+                "embeddings_searched_per_s": emb_step / (tot / 1e3),
+                "leaves_scored": prune_leaves,
+                "scored_fraction": {n: v / RAW_PER_QUERY for n, v in prune_leaves.items()},
+                "note": "not the headline: skipped embeddings are not scored (SURVEY §8(f) NEXT 3)"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -27,6 +27,17 @@
  *   MAPA_F_RAW     every injective map is scored; leaves = P(|F|,k).
  * Both modes return the identical decision.
  *
+ * MAPA_F_PRUNE (single-query entry points, k >= 4):
+ *   branch-and-bound argmax.  A k-2 scan (the leaves sharing a prefix of k-2
+ *   vertices) is skipped when an upper bound of its scores is below the best
+ *   score found so far by any lane of the launch (shared through the record's
+ *   `reserved` word).  The bound is exact (Eq. 1 / Eq. 3: max table entry +
+ *   max column entry; Eq. 2: max rank reachable from the census by the edges
+ *   the scan adds) and the test strict, so the decision is identical to the
+ *   exhaustive one; only leaves_scored changes (raw_embeddings and
+ *   distinct_matches are then the closed forms P(|F|,k) and P(|F|,k)/|Aut|).
+ *   For k < 4 the flag is ignored.
+ *
  * Memory: every device pointer is caller-owned (e.g. a torch CUDA tensor);
  * streams are cudaStream_t passed as void*.  Device-side entry points are
  * asynchronous on that stream and never synchronise.
@@ -60,7 +71,8 @@ enum { MAPA_SEL_GREEDY = 0, MAPA_SEL_PRESERVE = 1, MAPA_SEL_BASELINE = 2 };
 enum {
     MAPA_F_COMMIT = 1,              /* mapa_allocate: mark the chosen devices busy (§3.6) */
     MAPA_F_RAW = 2,                 /* score every injective map (no symmetry breaking) */
-    MAPA_F_ALLOW_DISCONNECTED = 4   /* mapa_load_pattern: accept disconnected patterns */
+    MAPA_F_ALLOW_DISCONNECTED = 4,  /* mapa_load_pattern: accept disconnected patterns */
+    MAPA_F_PRUNE = 8                /* single query: branch-and-bound argmax (same decision) */
 };
 
 /* Pattern shapes of Fig. 4 as constructed by SPEC make_pattern. */
@@ -109,7 +121,7 @@ typedef struct {
     uint64_t leaves;     /* leaves scored */
     uint32_t ctr;        /* work-item counter (scratch, zeroed by the launch) */
     uint32_t status;     /* 0 ok; nonzero = device-side argument error */
-    uint64_t reserved;
+    uint64_t reserved;   /* scratch (MAPA_F_PRUNE: best score + 1 found so far), zeroed by the launch */
 } mapa_record;
 
 /* Trace op (C2 replay): op 0 = ALLOC job, 1 = RELEASE job. */

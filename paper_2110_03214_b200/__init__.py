@@ -29,7 +29,7 @@ OK, NO_CAPACITY = 0, 1
 E_INVALID_ARG, E_PARSE, E_ALREADY_BUSY, E_NOT_BUSY, E_ID_RANGE = -1, -2, -3, -4, -5
 E_UNSUPPORTED, E_CUDA, E_DISCONNECTED, E_INTERNAL = -6, -7, -8, -10
 SEL_GREEDY, SEL_PRESERVE, SEL_BASELINE = 0, 1, 2
-F_COMMIT, F_RAW, F_ALLOW_DISCONNECTED = 1, 2, 4
+F_COMMIT, F_RAW, F_ALLOW_DISCONNECTED, F_PRUNE = 1, 2, 4, 8
 SHAPES = {"ring": 0, "tree": 1, "ringtree": 2, "full": 3, "edgeless": 4}
 
 
@@ -244,12 +244,17 @@ def decision_dict(d: Decision) -> dict:
                 distinct=int(d.distinct_matches), leaves=int(d.leaves_scored), key=int(d.key))
 
 
+def _flags(raw: bool, prune: bool = False) -> int:
+    return (F_RAW if raw else 0) | (F_PRUNE if prune else 0)
+
+
 def allocate(topo: Topology, pat: Pattern, selector: int, sensitive: bool = False, raw: bool = False,
-             commit: bool = False, stream=None) -> dict:
+             commit: bool = False, stream=None, prune: bool = False) -> dict:
     """mapa_allocate: one allocation end to end from host buffers (H2D query,
-    kernel, D2H record, host decode)."""
+    kernel, D2H record, host decode).  prune = MAPA_F_PRUNE (branch and bound,
+    same decision, fewer leaves scored)."""
     d = Decision()
-    flags = (F_RAW if raw else 0) | (F_COMMIT if commit else 0)
+    flags = _flags(raw, prune) | (F_COMMIT if commit else 0)
     _check(_lib.mapa_allocate(topo.handle, pat.handle, selector, int(bool(sensitive)), flags,
                               _stream_ptr(stream), ctypes.byref(d)), allow_no_capacity=True)
     return decision_dict(d)
@@ -257,10 +262,10 @@ def allocate(topo: Topology, pat: Pattern, selector: int, sensitive: bool = Fals
 
 def launch_query(topo: Topology, pat: Pattern, selector: int, sensitive: bool, d_query_ptr: int,
                  d_record_ptr: int, raw: bool = False, rank: int = 0, world: int = 1,
-                 busy_hint: int = 0xFFFFFFFF, stream=None):
+                 busy_hint: int = 0xFFFFFFFF, stream=None, prune: bool = False):
     """mapa_launch_query: device-resident launch (asynchronous)."""
     _check(_lib.mapa_launch_query(topo.handle, pat.handle, selector, int(bool(sensitive)), d_query_ptr,
-                                  d_record_ptr, F_RAW if raw else 0, rank, world, busy_hint,
+                                  d_record_ptr, _flags(raw, prune), rank, world, busy_hint,
                                   _stream_ptr(stream)))
 
 
@@ -276,10 +281,10 @@ def reduce_records(records) -> Record:
 
 
 def decode(topo: Topology, pat: Pattern, busy: int, selector: int, sensitive: bool, record: Record,
-           raw: bool = False) -> dict:
+           raw: bool = False, prune: bool = False) -> dict:
     d = Decision()
     _check(_lib.mapa_decode(topo.handle, pat.handle, busy, selector, int(bool(sensitive)),
-                            F_RAW if raw else 0, ctypes.byref(record), ctypes.byref(d)), allow_no_capacity=True)
+                            _flags(raw, prune), ctypes.byref(record), ctypes.byref(d)), allow_no_capacity=True)
     return decision_dict(d)
 
 

@@ -64,11 +64,11 @@ int device_sm_count() {
 
 int max_blocks_per_sm_single(int width, int k, int sc, int xs) {
     // cached: (width, k, selector code with canon bit, xs) -> blocks per SM
-    static int cache[3][9][8][48] = {};
+    static int cache[3][9][24][48] = {};
     const int wi = width == 8 ? 0 : (width == 16 ? 1 : 2), xi = xs < 48 ? xs : 0;
-    int &slot = cache[wi][k >= 1 && k <= 8 ? k : 0][sc & 7][xi];
+    int &slot = cache[wi][k >= 1 && k <= 8 ? k : 0][sc & 23][xi];
     if (slot) return slot;
-    const int smem = smem_shared_w32() + 3 * xs * xs * (int)sizeof(int);
+    const int smem = smem_shared_w32() + 4 * xs * xs * (int)sizeof(int);
     int r;
     if (width == 8) r = occ_single_w8(k, sc, smem);
     else if (width == 16) r = occ_single_w16(k, sc, smem);
@@ -78,7 +78,7 @@ int max_blocks_per_sm_single(int width, int k, int sc, int xs) {
 }
 
 int max_blocks_per_sm_batch(int width, int canon, int npats, int xs) {
-    const int smem = smem_shared_w32() + npats * 3 * xs * xs * (int)sizeof(int);
+    const int smem = smem_shared_w32() + (npats * 3 + 1) * xs * xs * (int)sizeof(int);
     if (width == 8) return occ_batch_w8(canon, smem);
     if (width == 16) return occ_batch_w16(canon, smem);
     return occ_batch_w32(canon, smem);

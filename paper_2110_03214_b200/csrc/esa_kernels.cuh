@@ -66,6 +66,10 @@ struct SelT {
     static constexpr int base = SEL & 3;
     static constexpr bool canon = (SEL & 4) != 0;
     static constexpr bool multi = (SEL & 8) != 0;      // batch / trace kernels (many patterns per block)
+    // bit 4: branch-and-bound mode (MAPA_F_PRUNE, single-query kernels, k >= 4):
+    // a k-2 scan runs only if an upper bound of its leaves reaches the best
+    // score found so far by any lane of the grid (exact: the argmax is unchanged)
+    static constexpr bool prune = (SEL & 16) != 0;
     // single-query Eq. 2 scans use 16-bit packed tables and columns (pack16)
     static constexpr bool pack16 = base == SEL_SENS && !multi;
     static constexpr bool lin = base != SEL_SENS;      // additive score (Eq. 1 / Eq. 3 / 0)
@@ -108,8 +112,9 @@ struct Shared {
     uint32_t pad[2];
 };
 
-// Single-query kernels: Shared + one Eq. 2 table of 3 xs^2 ints, xs <= 40.
-constexpr int kSmemSingleMax = (int)sizeof(Shared) + 3 * 40 * 40 * (int)sizeof(int);
+// Single-query kernels: Shared + one Eq. 2 table of 3 xs^2 ints + the
+// prune-mode bound table of xs^2 ints, xs <= 40.
+constexpr int kSmemSingleMax = (int)sizeof(Shared) + 4 * 40 * 40 * (int)sizeof(int);
 
 extern __shared__ __align__(16) unsigned char g_smem[];
 __device__ __forceinline__ Shared &sh() { return *reinterpret_cast<Shared *>(g_smem); }
@@ -134,6 +139,7 @@ struct Ctx {
     uint64_t fb, fs, db;            // bytes: fwd_back, fwd_src, dback
     int clique, eb, m;
     int one;                        // 1, read from shared memory (see scan_dense)
+    int colmax;                     // additive scores: max_v col[v] (prune-mode bound)
     int col[W];                     // lane's inner-scan column (see lane_column)
 };
 
@@ -153,6 +159,8 @@ struct Best {
     uint32_t cnt;  // leaves scored
     int thr;       // (bs + 1) * 32: a scan's packed rank must reach this to matter
     uint32_t sb;   // brev_W(device set) of key (0 while no key)
+    int pthr;      // prune mode: max(thr, 32 * (grid-wide best score + 1))
+    unsigned *gb;  // prune mode: grid-wide best score + 1 (in the result record), else null
 };
 
 template <int SEL>
@@ -223,6 +231,10 @@ __device__ __forceinline__ void consider(const Ctx<W> &c, Best &bst, uint32_t S,
         bst.bs = s;
         bst.thr = ((int)s + 1) * 32;
         bst.sb = sbn;
+        if (bst.gb) {  // prune mode: publish the score to the grid
+            if (bst.thr > bst.pthr) atomicMax(bst.gb, s + 1u);
+            bst.pthr = max(bst.pthr, bst.thr);
+        }
     }
 }
 
@@ -393,6 +405,30 @@ __device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2
     return tab_scan<W, SEL>(c, tab, base);
 }
 
+template <int W>
+__device__ __forceinline__ int grp_max(const Ctx<W> &c, int x) {
+    if constexpr (W == 32) {
+        return __reduce_max_sync(kFull, x);
+    } else {
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) x = max(x, __shfl_xor_sync(c.gmask, x, o, W));
+        return x;
+    }
+}
+
+// Prune mode: does the k-2 scan with this lane's table entry / base have a leaf
+// that can still matter anywhere in the grid?  Upper bound of the lane's
+// packed ranks: additive scores max_v tab[v] + max_v col[v] + base; Eq. 2 the
+// precomputed max rank reachable from the lane's census by the edges the scan
+// adds (`ubtab`).  Group-uniform result.
+template <int W, int SEL>
+__device__ __forceinline__ bool scan_needed(const Ctx<W> &c, const Best &bst, int entry, int base, bool laneok) {
+    int ub;
+    if constexpr (SelT<SEL>::lin) ub = base + grp_max<W>(c, entry) + c.colmax;
+    else ub = sh_lut()[3 * c.xs * c.xs + base] + 31;
+    return __any_sync(c.gmask, laneok && ub >= bst.pthr);
+}
+
 // The two innermost levels: vertex k-2 walks the devices of `cand`, vertex
 // k-1 sits on the lanes.  Vertices 0..k-3 are placed.
 template <int W, int K, int SEL>
@@ -486,7 +522,34 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
     const bool okb = ((c.F & ~st.U & alw<SEL>(st.al[J1])) >> b) & 1u;
     const uint32_t cand2b = c.F & ~st.U & alw<SEL>(st.al[J2]);
     const unsigned long long fbase = pack_f<K>(st);
-    const bool dep = d32 || d31 || d21;
+    const bool dep = d32 || d31 || d21 || SelT<SEL>::prune;  // prune mode counts the scans it runs
+    if constexpr (SelT<SEL>::prune) {
+        const unsigned g = *reinterpret_cast<volatile unsigned *>(bst.gb);
+        bst.pthr = max(bst.pthr, (int)(g * 32u));
+        if constexpr (SelT<SEL>::lin) {
+            // Bound of the whole prefix subtree for this lane (vertex k-1 on b).
+            // A leaf (v3, v) ranks 32 (A + lpb + 1 + t3(v3) + m31 w(v3,b)
+            // + t2b(v) + m32 w(v3,v)) + col_b[v]; bound the v3 part and the v
+            // part separately with two dense scans (tables 32 t3 and 32 t2b
+            // over the candidates, the lane's column; col_b >= 32 w(., b)
+            // when the edge (k-2, k-1) exists, else the v3 edge takes the
+            // largest weight) and w(v3, v) by 50.
+            int *ta = tab_ptr<W, SEL>(c, 0), *tb2 = tab_ptr<W, SEL>(c, 1);
+            __syncwarp(c.gmask);
+            tab_put<W, SEL>(c, ta, ((cand3 >> b) & 1u) ? 32 * t3 : kNeg);
+            tab_put<W, SEL>(c, tb2, ((cand2b >> b) & 1u) ? 32 * t2b : kNeg);
+            __syncwarp(c.gmask);
+            // the column carries the (., b) weights unless the edge (k-2, k-1) is
+            // absent (Eq. 1), and has no order sentinels unless f(k-2) < f(k-1)
+            // is a lex-leader constraint
+            const bool colw = (SelT<SEL>::useU || e21) && !d21;
+            const int s3 = colw ? tab_scan<W, SEL>(c, ta, 0) : 32 * grp_max<W>(c, ((cand3 >> b) & 1u) ? t3 : kNeg) +
+                                                            32 * 50 * SelT<SEL>::wt * m31;
+            const int s2 = tab_scan<W, SEL>(c, tb2, 0);
+            const int ub = 32 * (A + lpb + 1 + m32 * 50 * SelT<SEL>::wt) + s3 + s2;
+            if (!__any_sync(c.gmask, okb && ub >= bst.pthr)) return;
+        }
+    }
     if (!dep && okb) {
         // leaves of this lane: every (v3, v) with v3 in cand3, v in cand2b, v3, v, b distinct
         const uint32_t nb = ~(1u << b);
@@ -501,11 +564,15 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
             const int w3 = wcol[v3 * 32];
             const uint32_t cand2 = cand2b & ~(1u << v3) & (d32 ? (0xFFFFFFFEu << v3) : kFull);
             const bool laneok = okb && b != v3 && (!d31 || b > v3);
+            const int base = A + e3.y + lpb + m31 * w3;
+            if constexpr (SelT<SEL>::prune) {
+                if (!scan_needed<W, SEL>(c, bst, 0, base, laneok)) continue;
+            }
             if (dep) {
                 const uint32_t M = laneok ? (d21 ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
                 bst.cnt += (uint32_t)__popc(M & cand2);
             }
-            const int raw = scan_dense<W, SEL>(c, cand2, t2b + m32 * w3, A + e3.y + lpb + m31 * w3);
+            const int raw = scan_dense<W, SEL>(c, cand2, t2b + m32 * w3, base);
             if (laneok && raw >= bst.thr) {  // rank >= 32 and its score >= the lane's best score
                 const uint32_t bestv = 31u - (uint32_t)(raw & 31);
                 const unsigned long long fpack =
@@ -527,22 +594,32 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
         const int wA = wcol[vA * 32], wB = wcol[vB * 32];
         const uint32_t cA = cand2b & ~(1u << vA) & (d32 ? (0xFFFFFFFEu << vA) : kFull);
         const uint32_t cB = cand2b & ~(1u << vB) & (d32 ? (0xFFFFFFFEu << vB) : kFull);
-        const bool okA = okb && b != vA && (!d31 || b > vA);
-        const bool okB = hasB && okb && b != vB && (!d31 || b > vB);
-        if (dep) {
-            const uint32_t M = d21 ? ((1u << b) - 1u) : ~(1u << b);
-            bst.cnt += (uint32_t)(okA ? __popc(M & cA) : 0) + (uint32_t)(okB ? __popc(M & cB) : 0);
-        }
+        bool okA = okb && b != vA && (!d31 || b > vA);
+        bool okB = hasB && okb && b != vB && (!d31 || b > vB);
         const int lpA = lpb + m31 * wA, lpB = lpb + m31 * wB;
         const int baseA = (SelT<SEL>::lin) ? (A + eA.y + lpA + 1) * 32 : A + eA.y + lpA;
         const int baseB = (SelT<SEL>::lin) ? (A + eB.y + lpB + 1) * 32 : A + eB.y + lpB;
         const int offA = SelT<SEL>::lin ? baseA : 0, offB = SelT<SEL>::lin ? baseB : 0;
+        const int entA = tab_entry<W, SEL>(c, cA, t2b + m32 * wA);
+        const int entB = tab_entry<W, SEL>(c, cB, t2b + m32 * wB);
+        bool runA = true, runB = true;
+        if constexpr (SelT<SEL>::prune) {
+            runA = scan_needed<W, SEL>(c, bst, entA, baseA, okA);
+            runB = scan_needed<W, SEL>(c, bst, entB, baseB, okB);
+            if (!runA && !runB) continue;
+            okA = okA && runA;  // a skipped scan counts no leaves and proposes none
+            okB = okB && runB;
+        }
+        if (dep) {
+            const uint32_t M = d21 ? ((1u << b) - 1u) : ~(1u << b);
+            bst.cnt += (uint32_t)(okA ? __popc(M & cA) : 0) + (uint32_t)(okB ? __popc(M & cB) : 0);
+        }
         __syncwarp(c.gmask);  // previous readers of the tables are done
-        tab_put<W, SEL>(c, tabA, tab_entry<W, SEL>(c, cA, t2b + m32 * wA));
-        tab_put<W, SEL>(c, tabB, tab_entry<W, SEL>(c, cB, t2b + m32 * wB));
+        tab_put<W, SEL>(c, tabA, entA);
+        tab_put<W, SEL>(c, tabB, entB);
         __syncwarp(c.gmask);
-        const int rawA = tab_scan<W, SEL>(c, tabA, baseA);
-        const int rawB = tab_scan<W, SEL>(c, tabB, baseB);
+        const int rawA = runA ? tab_scan<W, SEL>(c, tabA, baseA) : kNeg;
+        const int rawB = runB ? tab_scan<W, SEL>(c, tabB, baseB) : kNeg;
         const bool hitA = okA && rawA >= bst.thr - offA;
         const bool hitB = okB && rawB >= bst.thr - offB;
         if (hitA || hitB) {  // a rank >= 32 whose score >= the lane's best score
@@ -748,6 +825,9 @@ __device__ __forceinline__ Ctx<W> make_ctx(const DevTopo &topo, const DevPattern
                         : (eW ? (dep ? sh().twd : sh().tw) : (dep ? sh().tzd : sh().tz));
 #pragma unroll
     for (int v = 0; v < W; ++v) c.col[v] = sens ? T[v * 32 + c.b] : T[v * 32 + c.b] + 31 - v;
+    c.colmax = kNeg;
+#pragma unroll
+    for (int v = 0; v < W; ++v) c.colmax = max(c.colmax, c.col[v]);
     if (pack16) {  // SelT::pack16: col[j] = col(2j) | col(2j+1) << 16 (byte offsets < 2^16)
 #pragma unroll
         for (int j = 0; j < W / 2; ++j) c.col[j] = (c.col[2 * j] & 0xFFFF) | (c.col[2 * j + 1] << 16);
@@ -769,7 +849,7 @@ __device__ __forceinline__ void warp_reduce(unsigned long long &key, unsigned lo
 // Shared tables for Eq. 2 row stride xs + npats Eq. 2 tables + edge lists.
 // Caller syncs.
 template <int MAXP, int LUTCAP>
-__device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int xs) {
+__device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int xs, int ub_r2 = -1) {
     Shared &s = sh();
     const DevTopo &topo = tb.topo;
     const int tid = threadIdx.x;
@@ -811,6 +891,21 @@ __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int 
         }
         if (tid < 28) s.edge[p][tid] = P.edge[tid];
     }
+    if (ub_r2 >= 0) {
+        // prune mode, Eq. 2 (single pattern): ubtab[x*xs + y] = max rank entry
+        // over the censuses reachable from (x, y) by ub_r2 more edges
+        __syncthreads();
+        const int m = tb.pat[0].m;
+        int *ub = lut + 3 * xs * xs;
+        for (int i = tid; i < xs * xs; i += blockDim.x) {
+            const int x = i / xs, y = i % xs;
+            int best = 0;
+            for (int dx = 0; dx <= ub_r2; ++dx)
+                for (int dy = 0; dx + dy <= ub_r2; ++dy)
+                    if (x + dx + y + dy <= m && x + dx < xs && y + dy < xs) best = max(best, lut[(x + dx) * xs + y + dy]);
+            ub[i] = best;
+        }
+    }
 }
 
 // ---------------------------------------------------------------- single query
@@ -825,7 +920,13 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
     constexpr int DMAX = (K - 1) < kMaxDecode ? (K - 1) : kMaxDecode;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int xs = tb.xs;
-    load_shared(tb, xs);
+    int ub_r2 = -1;
+    if constexpr (SelT<SEL>::prune && SelT<SEL>::base == SEL_SENS && K >= 4) {
+        // edges a k-2 scan adds: k-2's back edges + the edge (k-2, k-1)
+        const DevPattern &P = tb.pat[0];
+        ub_r2 = (int)P.dback[K - 2] + (int)((P.fwd_back[K - 2] >> (K - 1)) & 1u);
+    }
+    load_shared(tb, xs, ub_r2);
     const uint32_t busy = dq->busy;
     __syncthreads();
 
@@ -842,7 +943,7 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
     const bool ownLast = nS > 0 && ((nS - 1u) % (uint32_t)world) == (uint32_t)rank;
     const uint32_t Nloc = myS == 0 ? 0u : (ownLast ? (myS - 1u) * L + (N - (nS - 1u) * L) : myS * L);
     const uint32_t P = gridDim.x * (uint32_t)kWarps;
-    Best bst{0ull, 0u, 0u, 32, 0u};
+    Best bst{0ull, 0u, 0u, 32, 0u, 32, SelT<SEL>::prune ? reinterpret_cast<unsigned *>(&rec->reserved) : nullptr};
     const uint32_t g = (uint32_t)(lane / W);
     for (;;) {
         uint32_t start = 0, sz = 0;
@@ -944,7 +1045,7 @@ esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query
         Ctx<W> c = make_ctx<W>(tb.topo, P, (int)pid, xs, qu.busy, sel_code(qu.selector, qu.sensitive), false);
         if (P.k > c.nF) continue;
         const uint32_t j = (uint32_t)(base % W) + g;
-        Best bst{0ull, 0u, 0u, 32, 0u};
+        Best bst{0ull, 0u, 0u, 32, 0u, 32, nullptr};
         switch (sel_code(qu.selector, qu.sensitive)) {
             case SEL_GREEDY: batch_dispatch_k<W, SEL_GREEDY | 4 * CANON | 8>(P.k, c, j, bst); break;
             case SEL_INSENS: batch_dispatch_k<W, SEL_INSENS | 4 * CANON | 8>(P.k, c, j, bst); break;
@@ -1015,7 +1116,7 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
         if (cur.op == 0) {
             const uint32_t busy = sh().busy;
             Ctx<W> c = make_ctx<W>(tb.topo, P, ep, xs, busy, sel_code(qu.selector, qu.sensitive), false);
-            Best bst{0ull, 0u, 0u, 32, 0u};
+            Best bst{0ull, 0u, 0u, 32, 0u, 32, nullptr};
             if (okp && P.k <= c.nF) {
                 const int D = (P.k - 1) < 2 ? (P.k - 1) : 2;
                 const uint32_t nItems = perm_count(c.nF, D);
@@ -1049,7 +1150,7 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
 
 template <int MAXP, int LUTCAP>
 int smem_bytes(const Tables<MAXP, LUTCAP> &tb) {
-    return (int)sizeof(Shared) + tb.npats * 3 * tb.xs * tb.xs * (int)sizeof(int);
+    return (int)sizeof(Shared) + (tb.npats * 3 + 1) * tb.xs * tb.xs * (int)sizeof(int);
 }
 
 inline int set_smem(const void *f, int bytes) {

@@ -29,12 +29,14 @@ int do_launch_single(const SingleTables &tb, const mapa_query *dq, mapa_record *
 using SingleFn = int (*)(const SingleTables &, const mapa_query *, mapa_record *, int, int, int, int, int,
                          cudaStream_t);
 
+// the prune bit (16) applies to k >= 4 only (the host never sets it below)
 template <int W, int SEL>
 SingleFn pick_k(int K) {
+    constexpr int S3 = SEL & ~16;
     switch (K) {
-        case 1: return do_launch_single<W, 1, SEL>;
-        case 2: return do_launch_single<W, 2, SEL>;
-        case 3: return do_launch_single<W, 3, SEL>;
+        case 1: return do_launch_single<W, 1, S3>;
+        case 2: return do_launch_single<W, 2, S3>;
+        case 3: return do_launch_single<W, 3, S3>;
         case 4: return do_launch_single<W, 4, SEL>;
         case 5: return do_launch_single<W, 5, SEL>;
         case 6: return do_launch_single<W, 6, SEL>;
@@ -49,10 +51,11 @@ const void *single_ptr() { return (const void *)esa_single<W, K, SEL>; }
 
 template <int W, int SEL>
 const void *pick_ptr(int K) {
+    constexpr int S3 = SEL & ~16;
     switch (K) {
-        case 1: return single_ptr<W, 1, SEL>();
-        case 2: return single_ptr<W, 2, SEL>();
-        case 3: return single_ptr<W, 3, SEL>();
+        case 1: return single_ptr<W, 1, S3>();
+        case 2: return single_ptr<W, 2, S3>();
+        case 3: return single_ptr<W, 3, S3>();
         case 4: return single_ptr<W, 4, SEL>();
         case 5: return single_ptr<W, 5, SEL>();
         case 6: return single_ptr<W, 6, SEL>();
@@ -63,7 +66,7 @@ const void *pick_ptr(int K) {
 }
 
 #define MAPA_SEL_SWITCH(FN, ...)                      \
-    switch (sc & 7) {                                 \
+    switch (sc & 23) {                                \
         case 0: return FN<MAPA_W, 0>(__VA_ARGS__);    \
         case 1: return FN<MAPA_W, 1>(__VA_ARGS__);    \
         case 2: return FN<MAPA_W, 2>(__VA_ARGS__);    \
@@ -71,7 +74,15 @@ const void *pick_ptr(int K) {
         case 4: return FN<MAPA_W, 4>(__VA_ARGS__);    \
         case 5: return FN<MAPA_W, 5>(__VA_ARGS__);    \
         case 6: return FN<MAPA_W, 6>(__VA_ARGS__);    \
-        default: return FN<MAPA_W, 7>(__VA_ARGS__);   \
+        case 7: return FN<MAPA_W, 7>(__VA_ARGS__);    \
+        case 16: return FN<MAPA_W, 16>(__VA_ARGS__);  \
+        case 17: return FN<MAPA_W, 17>(__VA_ARGS__);  \
+        case 18: return FN<MAPA_W, 18>(__VA_ARGS__);  \
+        case 19: return FN<MAPA_W, 19>(__VA_ARGS__);  \
+        case 20: return FN<MAPA_W, 20>(__VA_ARGS__);  \
+        case 21: return FN<MAPA_W, 21>(__VA_ARGS__);  \
+        case 22: return FN<MAPA_W, 22>(__VA_ARGS__);  \
+        default: return FN<MAPA_W, 23>(__VA_ARGS__);  \
     }
 
 SingleFn pick(int K, int sc) { MAPA_SEL_SWITCH(pick_k, K) }
@@ -79,7 +90,7 @@ const void *pick_fn(int K, int sc) { MAPA_SEL_SWITCH(pick_ptr, K) }
 
 }  // namespace
 
-// sc = selector code | 4 * canonical (SelT)
+// sc = selector code | 4 * canonical | 16 * prune (SelT)
 int MAPA_CAT(launch_single_w, MAPA_W)(const SingleTables &tb, int sc, const mapa_query *dq, mapa_record *rec,
                                       int D, int rank, int world, int stripe, int grid, void *stream) {
     SingleFn fn = pick(tb.pat[0].k, sc);

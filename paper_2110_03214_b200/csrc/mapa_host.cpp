@@ -406,14 +406,21 @@ mapa_status decode_record(const mapa_topology *t, const mapa_pattern *p, uint32_
     d.key = rec->key;
     d.leaves_scored = rec->leaves;
     const bool raw = (flags & MAPA_F_RAW) != 0;
-    if (raw) {
+    const uint32_t F = ~busy & nmask_of(t->n);
+    if ((flags & MAPA_F_PRUNE) && p->k >= 4) {
+        // the pruned kernel scores a subset; the totals are the closed forms
+        uint64_t perm = 1;
+        const int nf = __builtin_popcount(F);
+        for (int i = 0; i < p->k; ++i) perm *= (uint64_t)std::max(0, nf - i);
+        d.raw_embeddings = perm;
+        d.distinct_matches = perm / (uint64_t)p->aut;
+    } else if (raw) {
         d.raw_embeddings = rec->leaves;
         d.distinct_matches = rec->leaves / (uint64_t)p->aut;
     } else {
         d.distinct_matches = rec->leaves;
         d.raw_embeddings = rec->leaves * (uint64_t)p->aut;
     }
-    const uint32_t F = ~busy & nmask_of(t->n);
     if (rec->status != 0) return fail(MAPA_E_INVALID_ARG, "device reported a bad query");
     if (rec->key == 0) {
         d.status = MAPA_NO_CAPACITY;
@@ -645,7 +652,8 @@ mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int
     fill_devpattern(p, (flags & MAPA_F_RAW) != 0, 0, tb.pat[0]);
     // canonical instantiation only when a lex-leader constraint exists (|Aut| > 1
     // and not RAW); otherwise the constraint-free kernel enumerates the same set
-    const int sc = sel_code(selector, sensitive) | (has_constraints(tb.pat[0]) ? 4 : 0);
+    const int sc = sel_code(selector, sensitive) | (has_constraints(tb.pat[0]) ? 4 : 0) |
+                   ((flags & MAPA_F_PRUNE) && p->k >= 4 ? 16 : 0);
     Plan pl = plan_single(t, p, sc, nF, world);
     if (pl.nlocal >= (1ull << 27)) return fail(MAPA_E_UNSUPPORTED, "too many work items");
     std::memcpy(tb.lut, p->lut.data(), p->lut.size() * sizeof(uint16_t));
@@ -724,6 +732,7 @@ mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *cons
                                 void *d_scratch, uint32_t flags, void *stream) {
     if (!t || !pats || (nq > 0 && (!d_queries || !d_results || !d_scratch)) || nq < 0)
         return fail(MAPA_E_INVALID_ARG, "null argument");
+    if (flags & MAPA_F_PRUNE) return fail(MAPA_E_UNSUPPORTED, "MAPA_F_PRUNE is single-query only");
     static thread_local MultiTables *tbp = nullptr;  // ~10 KB: keep off the stack
     if (!tbp) tbp = new MultiTables();
     mapa_status s = build_multi(t, pats, npats, flags, tbp);
@@ -746,6 +755,7 @@ mapa_status mapa_trace_replay(const mapa_topology *t, const mapa_pattern *const 
                               int32_t ntraces, int32_t nops, const mapa_trace_op *d_ops, int32_t njobs,
                               const mapa_query *d_jobs, uint64_t *d_keys, uint32_t flags, void *stream) {
     if (!t || !pats || ntraces < 0 || nops < 0 || njobs < 0) return fail(MAPA_E_INVALID_ARG, "bad argument");
+    if (flags & MAPA_F_PRUNE) return fail(MAPA_E_UNSUPPORTED, "MAPA_F_PRUNE is single-query only");
     if (ntraces == 0) return MAPA_OK;
     if (!d_ops || !d_jobs || !d_keys) return fail(MAPA_E_INVALID_ARG, "null device buffer");
     static thread_local MultiTables *tbp = nullptr;

@@ -52,13 +52,13 @@ def record_tensor(rec: Record, device="cpu"):
 
 
 def run_query(topo: Topology, pat: Pattern, selector: int, sensitive: bool, busy: int, raw: bool = False,
-              rank: int = 0, world: int = 1, stream=None):
+              rank: int = 0, world: int = 1, stream=None, prune: bool = False):
     """Launch one (shard of a) query on the current device; returns the record
     tensor (int64[4], device) without synchronising."""
     q = query_tensor(busy, 0, selector, sensitive)
     rec = torch.empty(4, dtype=torch.int64, device="cuda")
     launch_query(topo, pat, selector, sensitive, q.data_ptr(), rec.data_ptr(), raw=raw, rank=rank, world=world,
-                 busy_hint=busy, stream=stream)
+                 busy_hint=busy, stream=stream, prune=prune)
     return rec, q
 
 
@@ -79,13 +79,13 @@ def combine_records(rec: torch.Tensor, group=None) -> Record:
 
 
 def allocate_sharded(topo: Topology, pat: Pattern, selector: int, sensitive: bool, busy: int, raw: bool = False,
-                     group=None) -> dict:
+                     group=None, prune: bool = False) -> dict:
     """Sharded single allocation over the process group (one rank per GPU)."""
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rec, _q = run_query(topo, pat, selector, sensitive, busy, raw=raw, rank=rank, world=world)
+    rec, _q = run_query(topo, pat, selector, sensitive, busy, raw=raw, rank=rank, world=world, prune=prune)
     r = combine_records(rec, group)
-    return decode(topo, pat, busy, selector, sensitive, r, raw=raw)
+    return decode(topo, pat, busy, selector, sensitive, r, raw=raw, prune=prune)
 
 
 def run_batch(topo: Topology, pats, queries, raw: bool = False, stream=None):

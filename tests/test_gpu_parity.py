@@ -210,6 +210,95 @@ def test_c4_full_size_golden(golden_dir):
             assert g["leaves"] == (652458240 if raw else 906192)
 
 
+# ---------------------------------------------------------------- MAPA_F_PRUNE
+# Branch-and-bound mode: the same decision as the
+# exhaustive search (the bound is exact and the test strict), fewer leaves
+# scored; raw / distinct are then the closed forms.
+
+
+@pytest.mark.parametrize("name", ["dgx1v", "cubemesh16", "torus2d16"])
+def test_prune_random_vs_oracle(name):
+    o = mo.builtin(name)
+    t = mp.Topology(name)
+    rng = random.Random(sum(map(ord, name)) * 11 + 5)
+    for trial in range(36):
+        shape = rng.choice(["ring", "tree", "ringtree", "full"])
+        k = rng.randint(4, 6 if o.n <= 8 else 5)
+        busy = rng.randrange(0, 1 << o.n) & rng.randrange(0, 1 << o.n)
+        if o.n > 8:
+            busy |= (1 << rng.randint(0, 3)) - 1
+        sel, sens = rng.choice(SELS)
+        raw = bool(trial & 1)
+        t.set_busy(busy)
+        g = mp.allocate(t, mp.Pattern.make(shape, k), sel, sens, raw=raw, prune=True)
+        ob = oracle(o, busy, shape, k, sel, sens, use_c=True)
+        same(ob, g, (name, trial, shape, k, hex(busy), sel, sens, raw))
+        if ob["status"] == "ok":
+            assert g["leaves"] <= (ob["raw"] if raw else ob["distinct"])
+
+
+def test_prune_text_topologies_vs_oracle():
+    rng = random.Random(4321)
+    for text in (W.rand_text(13, 4), W.rand_text(21, 5), W.het32_text(), W.rand_text(32, W.MASTER_SEED)):
+        o = mo.parse_topology(text)
+        t = mp.Topology(text=text)
+        for trial in range(10):
+            shape = rng.choice(["ring", "tree", "ringtree", "full"])
+            k = rng.randint(4, 5)
+            nb = max(0, o.n - rng.randint(k, min(o.n, 12)))
+            busy = sum(1 << d for d in rng.sample(range(o.n), nb))
+            sel, sens = rng.choice(SELS)
+            raw = bool(trial & 1)
+            t.set_busy(busy)
+            g = mp.allocate(t, mp.Pattern.make(shape, k), sel, sens, raw=raw, prune=True)
+            same(oracle(o, busy, shape, k, sel, sens, use_c=True), g, (o.name, trial, shape, k, hex(busy), sel, sens))
+
+
+def test_prune_c4_full_size_golden(golden_dir):
+    """C4 full size with MAPA_F_PRUNE: the golden decisions, raw / distinct
+    the closed forms, strictly fewer leaves scored than the exhaustive count."""
+    gold = json.load(open(os.path.join(golden_dir, "c4_expected.json")))
+    tops = {"het32": W.het32_text(), "rand32_2110": W.rand_text(32, W.MASTER_SEED)}
+    sel_of = {"greedy": (0, False), "sensitive": (1, True), "insensitive": (1, False)}
+    pat = mp.Pattern.make("full", 6)
+    for case in gold["cases"]:
+        t = mp.Topology(text=tops[case["topology"]])
+        sel, sens = sel_of[case["selector"]]
+        for raw in (True, False):
+            g = mp.allocate(t, pat, sel, sens, raw=raw, prune=True)
+            exp = dict(case)
+            exp["devices"] = tuple(exp["devices"])
+            exp["mapping"] = tuple(exp["mapping"])
+            exp["used_edges"] = [tuple(e) for e in exp["used_edges"]]
+            same(exp, g, (case["topology"], case["selector"], raw, "prune"))
+            assert g["raw"] == 652458240 and g["distinct"] == 906192
+            assert 0 < g["leaves"] < (652458240 if raw else 906192)
+
+
+def test_prune_sharded_virtual_ranks():
+    """Prune mode per shard (each rank prunes against its own best) combined
+    over 3 virtual ranks = the unsharded decision."""
+    t = mp.Topology(text=W.het32_text())
+    pat = mp.Pattern.make("tree", 5)
+    for sel, sens in SELS[:3]:
+        ref = mp.allocate(t, pat, sel, sens, raw=True)
+        recs = []
+        for r in range(3):
+            rec, _q = md.run_query(t, pat, sel, sens, 0, raw=True, rank=r, world=3, prune=True)
+            recs.append(md.records_from_tensor(rec)[0])
+        torch.cuda.synchronize()
+        d = mp.decode(t, pat, 0, sel, sens, mp.reduce_records(recs), raw=True, prune=True)
+        for f in ("devices", "mapping", "used_edges", "key"):
+            assert d[f] == ref[f], (sel, sens, f)
+
+
+def test_prune_rejected_for_batch():
+    t = mp.Topology("dgx1v")
+    with pytest.raises(mp.MapaError):
+        mp._check(mp._lib.mapa_allocate_batch(t.handle, (mp._vp * 1)(mp.Pattern.make("ring", 3).handle), 1, 0,
+                                               None, None, None, mp.F_PRUNE, None))
+
+
 def test_batch_vs_oracle_and_counts():
     """C5-shaped batch: every query's leaf count equals the closed form, a
     sample of decisions equals the oracle."""
