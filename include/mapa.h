@@ -59,7 +59,7 @@ typedef int32_t mapa_status;
 #define MAPA_E_ALREADY_BUSY (-3) /* claim of a busy device, state unchanged */
 #define MAPA_E_NOT_BUSY (-4)    /* release of a free device */
 #define MAPA_E_ID_RANGE (-5)    /* device id out of range */
-#define MAPA_E_UNSUPPORTED (-6) /* N > 32, k > 8, or key budget 15+W+C(k,2) > 63 */
+#define MAPA_E_UNSUPPORTED (-6) /* N > 32, k > 16; narrow-only entry points: k > 8 or 15+W+C(k,2) > 63 */
 #define MAPA_E_CUDA (-7)        /* CUDA runtime error (message has the CUDA string) */
 #define MAPA_E_DISCONNECTED (-8) /* disconnected pattern, k > 1 */
 #define MAPA_E_INTERNAL (-10)   /* self-check failed (decoded key inconsistent) */
@@ -72,8 +72,15 @@ enum {
     MAPA_F_COMMIT = 1,              /* mapa_allocate: mark the chosen devices busy (§3.6) */
     MAPA_F_RAW = 2,                 /* score every injective map (no symmetry breaking) */
     MAPA_F_ALLOW_DISCONNECTED = 4,  /* mapa_load_pattern: accept disconnected patterns */
-    MAPA_F_PRUNE = 8                /* single query: branch-and-bound argmax (same decision) */
+    MAPA_F_PRUNE = 8,               /* single query: branch-and-bound argmax (same decision) */
+    MAPA_F_DEEP = 16                /* mapa_allocate: use the deep (wide-key) kernel even when the
+                                       narrow 63-bit key fits (testing / comparison) */
 };
+
+/* Limits.  Narrow path (mapa_launch_query, batches, traces): k <= 8 and
+ * 15 + W + C(k,2) <= 63.  Deep path (mapa_launch_query_wide): k <= 16. */
+#define MAPA_MAX_K 16
+#define MAPA_MAX_EDGES 120
 
 /* Pattern shapes of Fig. 4 as constructed by SPEC make_pattern. */
 enum { MAPA_SHAPE_RING = 0, MAPA_SHAPE_TREE = 1, MAPA_SHAPE_RINGTREE = 2,
@@ -87,9 +94,9 @@ typedef struct {
     int32_t status;          /* MAPA_OK or MAPA_NO_CAPACITY */
     int32_t k;               /* pattern vertices */
     uint32_t device_mask;    /* bit d = device d allocated */
-    int8_t mapping[8];       /* mapping[i] = device of pattern vertex i (lex-first of the match) */
+    int8_t mapping[16];      /* mapping[i] = device of pattern vertex i (lex-first of the match) */
     int32_t m;               /* pattern edges */
-    int32_t used[28][2];     /* sorted used edges (lo, hi) = E(P) ∩ E(M) realised */
+    int32_t used[120][2];    /* sorted used edges (lo, hi) = E(P) ∩ E(M) realised */
     int32_t x, y, z;         /* link census: double / single(25|20) / PCIe used edges */
     int32_t agg_bw;          /* Eq. 1, GB/s */
     int32_t preserved_bw;    /* Eq. 3, GB/s */
@@ -98,7 +105,9 @@ typedef struct {
     uint64_t raw_embeddings;   /* P(|F|,k) injective maps (counted in RAW mode) */
     uint64_t distinct_matches; /* P(|F|,k)/|Aut(P)| (counted in canonical mode) */
     uint64_t leaves_scored;    /* leaves the kernel actually scored */
-    uint64_t key;            /* packed argmax key (see mapa_record) */
+    uint64_t key;            /* narrow path: packed argmax key (mapa_record);
+                                deep path: key word of mapa_wide_record */
+    uint64_t ecode[2];       /* deep path: 128-bit edge code {high, low} (0 on the narrow path) */
 } mapa_decision;
 
 /* Device-side query, 16 bytes (coalesced uint4 load). */
@@ -123,6 +132,29 @@ typedef struct {
     uint32_t status;     /* 0 ok; nonzero = device-side argument error */
     uint64_t reserved;   /* scratch (MAPA_F_PRUNE: best score + 1 found so far), zeroed by the launch */
 } mapa_record;
+
+/* Deep-path result record, 64 bytes (k <= 16, N <= 32).
+ * The argmax key is 192 bits, compared lexicographically as
+ * (key, ecode_hi, ecode_lo):
+ *   key   = score << 32 | brev_32(S)   (bit 31-d set for every chosen device d;
+ *           larger = lex-smaller device tuple)
+ *   ecode = 128-bit edge code: bit C(k,2)-1-p set for every used edge whose
+ *           endpoint ranks inside S form the p-th pair in lex order (larger =
+ *           lex-smaller used-edge list); ecode_hi holds bits 64..127.
+ * key 0 = no match.  The launch zeroes the record; `lock` serialises the
+ * per-CTA merges of the 192-bit maximum (order-independent, so the result is
+ * deterministic for every grid size and rank count). */
+typedef struct {
+    uint64_t key;
+    uint64_t ecode_hi;
+    uint64_t ecode_lo;
+    uint64_t leaves;     /* leaves scored */
+    uint32_t ctr;        /* work-item counter (scratch) */
+    uint32_t lock;       /* merge lock (scratch) */
+    uint32_t status;     /* 0 ok; nonzero = device-side argument error */
+    uint32_t pad;
+    uint64_t reserved[2];
+} mapa_wide_record;
 
 /* Trace op (C2 replay): op 0 = ALLOC job, 1 = RELEASE job. */
 typedef struct {
@@ -156,11 +188,14 @@ mapa_status mapa_set_busy(mapa_topology *t, uint32_t busy);
 
 /* ---------------------------------------------------------------- patterns */
 
-/* Pattern from an edge list (2*m ints, 0-based vertex ids < k).  1 <= k <= 8,
+/* Pattern from an edge list (2*m ints, 0-based vertex ids < k).  1 <= k <= 16,
  * 0 <= m <= C(k,2).  Duplicate edges and self loops: INVALID_ARG.
  * Disconnected with k > 1: DISCONNECTED unless MAPA_F_ALLOW_DISCONNECTED
- * (S:210).  Compiles Aut(P) (brute force over k!), the lex-leader symmetry
- * constraints and the Eq. 2 rank table for m. */
+ * (S:210).  Compiles the point-stabiliser chain of Aut(P) (backtracking:
+ * orbit of i under the automorphisms fixing 0..i-1), |Aut(P)| = product of
+ * the orbit sizes, the lex-leader symmetry constraints and the Eq. 2 rank
+ * table for m.  Patterns with k > 8 (or a key wider than 63 bits on the
+ * topology) run on the deep path only. */
 mapa_status mapa_load_pattern(int32_t k, int32_t m, const int32_t *edges, uint32_t flags,
                               mapa_pattern **out);
 /* SPEC make_pattern: Ring (k=2: one edge; k=1: INVALID_ARG),
@@ -170,24 +205,28 @@ void mapa_free_pattern(mapa_pattern *p);
 
 typedef struct {
     int32_t k, m;
-    int32_t aut_order;       /* |Aut(P)| */
-    uint8_t back[8];         /* back[j] bit i: edge (i,j), i < j */
-    uint8_t lex_src[8];      /* lex_src[u] bit i: canonical mode requires f(i) < f(u) */
-    int32_t edges[28][2];    /* normalised (a<b), sorted */
+    int32_t aut_order;       /* |Aut(P)|, clamped to INT32_MAX (aut_order64 is exact) */
+    uint16_t back[16];       /* back[j] bit i: edge (i,j), i < j */
+    uint16_t lex_src[16];    /* lex_src[u] bit i: canonical mode requires f(i) < f(u) */
+    int32_t edges[120][2];   /* normalised (a<b), sorted */
+    uint64_t aut_order64;    /* |Aut(P)| (16! fits) */
 } mapa_pattern_info;
 mapa_status mapa_get_pattern_info(const mapa_pattern *p, mapa_pattern_info *out);
 
 /* Eq. 2 with Table 4 theta, double. */
 double mapa_pred_effbw(int32_t x, int32_t y, int32_t z);
 /* Dense rank of Eq. 2 over the censuses with x+y+z = m: out[x*(m+1)+y]
- * (entries with x+y > m are 0).  m <= 28. */
+ * (entries with x+y > m are 0).  m <= 120 (reading A9: no ties, double order
+ * = exact order for every m <= 120). */
 mapa_status mapa_effbw_rank_table(int32_t m, uint16_t *out);
 
 /* ---------------------------------------------------------- single query */
 
 /* One allocation end to end, host buffers: stages the query (16 B) to the
  * device from pinned memory, launches the enumerate-score-argmax kernel on
- * cuda_stream (NULL = default stream), reads the 32-B record back, decodes it
+ * cuda_stream (NULL = default stream) -- the narrow kernel when the 63-bit key
+ * fits and MAPA_F_DEEP is not set, else the deep kernel
+ * (mapa_launch_query_wide) -- reads the record back, decodes it
  * on the host and, with MAPA_F_COMMIT, marks the devices busy.  Blocks until
  * the stream reaches the copy.  Returns MAPA_OK, MAPA_NO_CAPACITY (out->status
  * too) or an error. Not thread-safe per topology handle. */
@@ -218,6 +257,37 @@ mapa_status mapa_reduce_records(const mapa_record *records, int32_t n, mapa_reco
 mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint32_t busy,
                         int32_t selector, int32_t bw_sensitive, uint32_t flags,
                         const mapa_record *record, mapa_decision *out);
+
+/* ------------------------------------------------- deep patterns (k <= 16) */
+
+/* Device-resident launch of one query's shard on the deep path (SURVEY §8(f)
+ * NEXT 1: the paper's overhead study reaches "9 GPUs and above" on 16-GPU
+ * graphs).  Same contract as mapa_launch_query (busy read from
+ * d_query->busy on the device; work item i of the prefix space goes to rank
+ * i's stripe owner; asynchronous on cuda_stream) but with the 192-bit key of
+ * mapa_wide_record, so any k <= 16 on any N <= 32 fits.  Enumeration: a
+ * warp-uniform explicit-stack DFS over the first k-L pattern vertices, then
+ * the last L vertices (L = 1..4, chosen on the host) as a lane-parallel scan
+ * over a table of index tuples into the remaining free devices.  RAW and
+ * canonical modes as for the narrow path; MAPA_F_PRUNE is ignored.
+ * Errors: INVALID_ARG, UNSUPPORTED (k > 16), CUDA. */
+mapa_status mapa_launch_query_wide(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
+                                   int32_t sensitive, const mapa_query *d_query, mapa_wide_record *d_record,
+                                   uint32_t flags, int32_t rank, int32_t world, uint32_t busy_hint,
+                                   void *cuda_stream);
+
+/* Host: combine n deep shard records (lexicographic max of the 192-bit key,
+ * sum of leaves, OR of status). */
+mapa_status mapa_reduce_wide_records(const mapa_wide_record *records, int32_t n, mapa_wide_record *out);
+
+/* Host: decode a (combined) deep record.  The lex-first mapping of the
+ * winning (device set, edge set) is found by backtracking in pattern-vertex
+ * order over the devices of S in ascending order, keeping only partial maps
+ * whose placed pattern edges land on decoded edges (first complete map =
+ * lex-first).  Scores are recomputed and checked against the key. */
+mapa_status mapa_decode_wide(const mapa_topology *t, const mapa_pattern *p, uint32_t busy,
+                             int32_t selector, int32_t bw_sensitive, uint32_t flags,
+                             const mapa_wide_record *record, mapa_decision *out);
 
 /* ---------------------------------------------------------------- batches */
 

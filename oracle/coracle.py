@@ -31,6 +31,17 @@ class OracleResult(ctypes.Structure):
                 ("raw", ctypes.c_uint64), ("distinct", ctypes.c_uint64)]
 
 
+class OracleResultDeep(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("k", ctypes.c_int32),
+                ("device_mask", ctypes.c_uint32), ("mapping", ctypes.c_int8 * 16),
+                ("m", ctypes.c_int32), ("used", (ctypes.c_int32 * 2) * 120),
+                ("x", ctypes.c_int32), ("y", ctypes.c_int32), ("z", ctypes.c_int32),
+                ("agg_bw", ctypes.c_int32), ("preserved_bw", ctypes.c_int32),
+                ("pad", ctypes.c_int32),
+                ("pred_effbw", ctypes.c_double), ("score", ctypes.c_double),
+                ("raw", ctypes.c_uint64)]
+
+
 _lib = None
 
 
@@ -43,6 +54,11 @@ def lib():
             ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_uint32, ctypes.c_int,
             ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_int, ctypes.c_int,
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(OracleResult)]
+        _lib.oracle_allocate_deep.restype = ctypes.c_int
+        _lib.oracle_allocate_deep.argtypes = [
+            ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_uint32, ctypes.c_int,
+            ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_int, ctypes.c_int,
+            ctypes.c_int, ctypes.c_int, ctypes.POINTER(OracleResultDeep)]
         _lib.oracle_eq2.restype = ctypes.c_double
         _lib.oracle_eq2.argtypes = [ctypes.c_int] * 3
     return _lib
@@ -69,6 +85,29 @@ def allocate(topo: mo.Topology, busy: int, k: int, pedges, selector: int, sensit
                 used_edges=[(r.used[i][0], r.used[i][1]) for i in range(len(pedges))],
                 x=r.x, y=r.y, z=r.z, agg_bw=r.agg_bw, preserved_bw=r.preserved_bw,
                 pred_effbw=r.pred_effbw, raw=int(r.raw), distinct=int(r.distinct))
+
+
+def allocate_deep(topo: mo.Topology, busy: int, k: int, pedges, selector: int, sensitive: bool,
+                  nthreads: int | None = None, max_subsets: int = 4096) -> dict:
+    """Deep oracle (k <= 16): same decision fields as allocate(); 'distinct'
+    is not counted (None)."""
+    n = topo.n
+    w = (ctypes.c_int32 * (n * n))(*[topo.w[u][v] for u in range(n) for v in range(n)])
+    flat = [c for e in pedges for c in e]
+    pe = (ctypes.c_int32 * max(1, len(flat)))(*flat)
+    r = OracleResultDeep()
+    nt = nthreads or os.cpu_count() or 1
+    rc = lib().oracle_allocate_deep(n, w, busy, k, len(pedges), pe, selector, int(bool(sensitive)), nt,
+                                    max_subsets, ctypes.byref(r))
+    if rc != 0:
+        raise ValueError(f"oracle_allocate_deep rc={rc}")
+    if r.status == 1:
+        return dict(status="no_capacity", raw=int(r.raw), distinct=None)
+    devs = tuple(d for d in range(n) if (r.device_mask >> d) & 1)
+    return dict(status="ok", devices=devs, mapping=tuple(r.mapping[i] for i in range(k)),
+                used_edges=[(r.used[i][0], r.used[i][1]) for i in range(len(pedges))],
+                x=r.x, y=r.y, z=r.z, agg_bw=r.agg_bw, preserved_bw=r.preserved_bw,
+                pred_effbw=r.pred_effbw, raw=int(r.raw), distinct=None)
 
 
 def eq2(x: int, y: int, z: int) -> float:

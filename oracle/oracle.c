@@ -284,3 +284,186 @@ int oracle_allocate(int n, const int32_t *w, uint32_t busy, int k, int m, const 
     out->agg_bw = best.agg; out->preserved_bw = best.pres; out->pred_effbw = best.eff;
     return 0;
 }
+
+/* ------------------------------------------------------------------------
+ * Deep oracle (k <= 16).  The same definition as
+ * oracle_allocate, restated without the per-subset table of edge lists (k!
+ * entries per subset does not fit for k > 8):
+ *   for every k-subset S of F in lex order, for every permutation pi of S in
+ *   lex order: E = sorted used-edge list, score by Eq. 1 / Eq. 2 / Eq. 3;
+ *   the winner is the max score; ties go to the earlier S (lex-smaller device
+ *   tuple), then within S to the lex-smaller E, and for an equal (S, E) the
+ *   first pi is kept (the lex-first mapping) -- SPEC S:349; Alg. 1's
+ *   first-wins loop.  `distinct` is not counted here (0).
+ * Work units = (subset, index of pi[0] in S), combined in that order with the
+ * same rule, so the result does not depend on the thread count.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+    int32_t status, k;
+    uint32_t device_mask;
+    int8_t mapping[16];
+    int32_t m;
+    int32_t used[120][2];
+    int32_t x, y, z, agg_bw, preserved_bw, pad;
+    double pred_effbw, score;
+    uint64_t raw;
+} oracle_result_deep;
+
+typedef struct {
+    int found;
+    double score;
+    int S[16], pi[16];
+    uint16_t E[120];
+    int agg, x, y, z, pres;
+    double eff;
+    uint64_t raw;
+} dunit_t;
+
+typedef struct {
+    const ctx_t *c;
+    int (*subsets)[16];   /* lex-ordered k-subsets */
+    int nsub;
+    dunit_t *units;       /* nsub * k */
+    int nunits, next;
+    pthread_mutex_t mu;
+} dpool_t;
+
+static int cmp_codes(const uint16_t *a, const uint16_t *b, int m) {
+    for (int i = 0; i < m; i++)
+        if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+    return 0;
+}
+
+static void deep_unit(const ctx_t *c, const int *S, int i0, dunit_t *u) {
+    int k = c->k, m = c->m, n = c->n;
+    memset(u, 0, sizeof(*u));
+    int inS[64] = {0};
+    for (int i = 0; i < k; i++) inS[S[i]] = 1;
+    int pres = 0;                                   /* Eq. 3 (depends on S only) */
+    for (int i = 0; i < c->nf; i++) {
+        if (inS[c->F[i]]) continue;
+        for (int j = i + 1; j < c->nf; j++) {
+            if (inS[c->F[j]]) continue;
+            pres += c->w[c->F[i] * n + c->F[j]];
+        }
+    }
+    int perm[16], rest[16], nr = 0;
+    for (int i = 0; i < k; i++)
+        if (i != i0) rest[nr++] = S[i];
+    perm[0] = S[i0];
+    uint16_t E[120];
+    do {                                            /* permutations with pi[0] = S[i0], lex order */
+        for (int i = 0; i < nr; i++) perm[i + 1] = rest[i];
+        u->raw++;
+        int agg = 0, x = 0, y = 0, z = 0;
+        for (int i = 0; i < m; i++) {
+            int a = perm[c->pe[2 * i]], b = perm[c->pe[2 * i + 1]];
+            int lo = a < b ? a : b, hi = a < b ? b : a;
+            uint16_t code = (uint16_t)(lo * 64 + hi);
+            int j = i;                              /* insertion sort */
+            while (j > 0 && E[j - 1] > code) { E[j] = E[j - 1]; j--; }
+            E[j] = code;
+            int bw = c->w[lo * n + hi];
+            agg += bw;                              /* Eq. 1 */
+            if (bw == 50) x++;                      /* census */
+            else if (bw == 25 || bw == 20) y++;
+            else z++;
+        }
+        double s;
+        if (c->selector == 0) s = agg;
+        else if (c->selector == 1) s = c->sensitive ? oracle_eq2(x, y, z) : pres;
+        else s = 0.0;
+        int better = !u->found || s > u->score || (s == u->score && cmp_codes(E, u->E, m) < 0);
+        if (better) {
+            u->found = 1;
+            u->score = s;
+            for (int i = 0; i < k; i++) { u->S[i] = S[i]; u->pi[i] = perm[i]; }
+            memcpy(u->E, E, sizeof(uint16_t) * m);
+            u->agg = agg; u->x = x; u->y = y; u->z = z; u->pres = pres; u->eff = oracle_eq2(x, y, z);
+        }
+    } while (next_perm(rest, nr));
+}
+
+static void *deep_worker(void *arg) {
+    dpool_t *p = (dpool_t *)arg;
+    for (;;) {
+        pthread_mutex_lock(&p->mu);
+        int i = p->next++;
+        pthread_mutex_unlock(&p->mu);
+        if (i >= p->nunits) break;
+        deep_unit(p->c, p->subsets[i / p->c->k], i % p->c->k, &p->units[i]);
+    }
+    return NULL;
+}
+
+/* w: n*n weights; busy: bit d busy; pe: 2m pattern edges; selector as
+ * oracle_allocate.  max_subsets bounds the work (error -2 above it). */
+int oracle_allocate_deep(int n, const int32_t *w, uint32_t busy, int k, int m, const int32_t *pe,
+                         int selector, int sensitive, int nthreads, int max_subsets,
+                         oracle_result_deep *out) {
+    memset(out, 0, sizeof(*out));
+    if (n < 1 || n > 32 || k < 1 || k > 16 || m < 0 || m > 120) return -1;
+    ctx_t c;
+    c.n = n; c.k = k; c.m = m; c.selector = selector; c.sensitive = sensitive; c.w = w; c.pe = pe;
+    c.nf = 0;
+    for (int d = 0; d < n; d++)
+        if (!((busy >> d) & 1u)) c.F[c.nf++] = d;
+    out->k = k;
+    out->m = m;
+    if (k > c.nf) { out->status = 1; return 0; }
+    /* lex-ordered k-subsets of F */
+    int cap = max_subsets > 0 ? max_subsets : 1;
+    int (*subs)[16] = (int (*)[16])malloc(sizeof(int[16]) * (size_t)cap);
+    int nsub = 0, idx[16];
+    for (int i = 0; i < k; i++) idx[i] = i;
+    for (;;) {
+        if (nsub >= cap) { free(subs); return -2; }
+        for (int i = 0; i < k; i++) subs[nsub][i] = c.F[idx[i]];
+        nsub++;
+        int i = k - 1;
+        while (i >= 0 && idx[i] == c.nf - k + i) i--;
+        if (i < 0) break;
+        idx[i]++;
+        for (int j = i + 1; j < k; j++) idx[j] = idx[j - 1] + 1;
+    }
+    dpool_t p;
+    p.c = &c;
+    p.subsets = subs;
+    p.nsub = nsub;
+    p.nunits = nsub * k;
+    p.next = 0;
+    p.units = (dunit_t *)calloc((size_t)p.nunits, sizeof(dunit_t));
+    pthread_mutex_init(&p.mu, NULL);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    for (int t = 0; t < nthreads; t++) pthread_create(&th[t], NULL, deep_worker, &p);
+    for (int t = 0; t < nthreads; t++) pthread_join(th[t], NULL);
+    pthread_mutex_destroy(&p.mu);
+    dunit_t best;
+    memset(&best, 0, sizeof(best));
+    uint64_t raw = 0;
+    for (int i = 0; i < p.nunits; i++) {            /* combine in (subset, pi[0]) order */
+        dunit_t *u = &p.units[i];
+        raw += u->raw;
+        if (!u->found) continue;
+        int same_set = best.found && memcmp(u->S, best.S, sizeof(int) * k) == 0;
+        if (!best.found || u->score > best.score ||
+            (u->score == best.score && same_set && cmp_codes(u->E, best.E, m) < 0))
+            best = *u;
+    }
+    free(p.units);
+    free(subs);
+    out->raw = raw;
+    out->status = best.found ? 0 : 1;
+    if (!best.found) return 0;
+    out->score = best.score;
+    for (int i = 0; i < k; i++) {
+        out->device_mask |= 1u << best.S[i];
+        out->mapping[i] = (int8_t)best.pi[i];
+    }
+    for (int i = 0; i < m; i++) { out->used[i][0] = best.E[i] >> 6; out->used[i][1] = best.E[i] & 63; }
+    out->x = best.x; out->y = best.y; out->z = best.z;
+    out->agg_bw = best.agg; out->preserved_bw = best.pres; out->pred_effbw = best.eff;
+    return 0;
+}

@@ -29,7 +29,8 @@ OK, NO_CAPACITY = 0, 1
 E_INVALID_ARG, E_PARSE, E_ALREADY_BUSY, E_NOT_BUSY, E_ID_RANGE = -1, -2, -3, -4, -5
 E_UNSUPPORTED, E_CUDA, E_DISCONNECTED, E_INTERNAL = -6, -7, -8, -10
 SEL_GREEDY, SEL_PRESERVE, SEL_BASELINE = 0, 1, 2
-F_COMMIT, F_RAW, F_ALLOW_DISCONNECTED, F_PRUNE = 1, 2, 4, 8
+F_COMMIT, F_RAW, F_ALLOW_DISCONNECTED, F_PRUNE, F_DEEP = 1, 2, 4, 8, 16
+MAX_K = 16
 SHAPES = {"ring": 0, "tree": 1, "ringtree": 2, "full": 3, "edgeless": 4}
 
 
@@ -41,12 +42,12 @@ class MapaError(RuntimeError):
 
 class Decision(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("k", ctypes.c_int32), ("device_mask", ctypes.c_uint32),
-                ("mapping", ctypes.c_int8 * 8), ("m", ctypes.c_int32), ("used", (ctypes.c_int32 * 2) * 28),
+                ("mapping", ctypes.c_int8 * 16), ("m", ctypes.c_int32), ("used", (ctypes.c_int32 * 2) * 120),
                 ("x", ctypes.c_int32), ("y", ctypes.c_int32), ("z", ctypes.c_int32),
                 ("agg_bw", ctypes.c_int32), ("preserved_bw", ctypes.c_int32), ("score", ctypes.c_int32),
                 ("pred_effbw", ctypes.c_double), ("raw_embeddings", ctypes.c_uint64),
                 ("distinct_matches", ctypes.c_uint64), ("leaves_scored", ctypes.c_uint64),
-                ("key", ctypes.c_uint64)]
+                ("key", ctypes.c_uint64), ("ecode", ctypes.c_uint64 * 2)]
 
 
 class Query(ctypes.Structure):
@@ -59,13 +60,20 @@ class Record(ctypes.Structure):
                 ("status", ctypes.c_uint32), ("reserved", ctypes.c_uint64)]
 
 
+class WideRecord(ctypes.Structure):
+    """mapa_wide_record (deep path): 192-bit key (key, ecode_hi, ecode_lo)."""
+    _fields_ = [("key", ctypes.c_uint64), ("ecode_hi", ctypes.c_uint64), ("ecode_lo", ctypes.c_uint64),
+                ("leaves", ctypes.c_uint64), ("ctr", ctypes.c_uint32), ("lock", ctypes.c_uint32),
+                ("status", ctypes.c_uint32), ("pad", ctypes.c_uint32), ("reserved", ctypes.c_uint64 * 2)]
+
+
 class PatternInfo(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int32), ("m", ctypes.c_int32), ("aut_order", ctypes.c_int32),
-                ("back", ctypes.c_uint8 * 8), ("lex_src", ctypes.c_uint8 * 8),
-                ("edges", (ctypes.c_int32 * 2) * 28)]
+                ("back", ctypes.c_uint16 * 16), ("lex_src", ctypes.c_uint16 * 16),
+                ("edges", (ctypes.c_int32 * 2) * 120), ("aut_order64", ctypes.c_uint64)]
 
 
-assert ctypes.sizeof(Query) == 16 and ctypes.sizeof(Record) == 32
+assert ctypes.sizeof(Query) == 16 and ctypes.sizeof(Record) == 32 and ctypes.sizeof(WideRecord) == 64
 
 _vp = ctypes.c_void_p
 _S = ctypes.c_int32
@@ -89,6 +97,11 @@ _SIGS = {
     "mapa_launch_query": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.c_uint32,
                                ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, _vp]),
     "mapa_reduce_records": (_S, [ctypes.POINTER(Record), ctypes.c_int32, ctypes.POINTER(Record)]),
+    "mapa_launch_query_wide": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.c_uint32,
+                                    ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, _vp]),
+    "mapa_reduce_wide_records": (_S, [ctypes.POINTER(WideRecord), ctypes.c_int32, ctypes.POINTER(WideRecord)]),
+    "mapa_decode_wide": (_S, [_vp, _vp, ctypes.c_uint32, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
+                              ctypes.POINTER(WideRecord), ctypes.POINTER(Decision)]),
     "mapa_decode": (_S, [_vp, _vp, ctypes.c_uint32, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
                          ctypes.POINTER(Record), ctypes.POINTER(Decision)]),
     "mapa_allocate_batch": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int64, _vp, _vp, _vp,
@@ -229,7 +242,7 @@ class Pattern:
     def info(self) -> dict:
         pi = PatternInfo()
         _check(_lib.mapa_get_pattern_info(self._h, ctypes.byref(pi)))
-        return dict(k=pi.k, m=pi.m, aut=pi.aut_order, back=list(pi.back)[:pi.k],
+        return dict(k=pi.k, m=pi.m, aut=int(pi.aut_order64), back=list(pi.back)[:pi.k],
                     lex_src=list(pi.lex_src)[:pi.k], edges=[(pi.edges[i][0], pi.edges[i][1]) for i in range(pi.m)])
 
 
@@ -241,20 +254,22 @@ def decision_dict(d: Decision) -> dict:
                 used_edges=[(d.used[i][0], d.used[i][1]) for i in range(d.m)],
                 x=d.x, y=d.y, z=d.z, agg_bw=d.agg_bw, preserved_bw=d.preserved_bw,
                 pred_effbw=d.pred_effbw, score=d.score, raw=int(d.raw_embeddings),
-                distinct=int(d.distinct_matches), leaves=int(d.leaves_scored), key=int(d.key))
+                distinct=int(d.distinct_matches), leaves=int(d.leaves_scored), key=int(d.key),
+                ecode=(int(d.ecode[0]) << 64) | int(d.ecode[1]))
 
 
-def _flags(raw: bool, prune: bool = False) -> int:
-    return (F_RAW if raw else 0) | (F_PRUNE if prune else 0)
+def _flags(raw: bool, prune: bool = False, deep: bool = False) -> int:
+    return (F_RAW if raw else 0) | (F_PRUNE if prune else 0) | (F_DEEP if deep else 0)
 
 
 def allocate(topo: Topology, pat: Pattern, selector: int, sensitive: bool = False, raw: bool = False,
-             commit: bool = False, stream=None, prune: bool = False) -> dict:
+             commit: bool = False, stream=None, prune: bool = False, deep: bool = False) -> dict:
     """mapa_allocate: one allocation end to end from host buffers (H2D query,
     kernel, D2H record, host decode).  prune = MAPA_F_PRUNE (branch and bound,
-    same decision, fewer leaves scored)."""
+    same decision, fewer leaves scored); deep = MAPA_F_DEEP (the wide-key
+    kernel even when the narrow one fits; patterns with k > 8 always take it)."""
     d = Decision()
-    flags = _flags(raw, prune) | (F_COMMIT if commit else 0)
+    flags = _flags(raw, prune, deep) | (F_COMMIT if commit else 0)
     _check(_lib.mapa_allocate(topo.handle, pat.handle, selector, int(bool(sensitive)), flags,
                               _stream_ptr(stream), ctypes.byref(d)), allow_no_capacity=True)
     return decision_dict(d)
@@ -267,6 +282,29 @@ def launch_query(topo: Topology, pat: Pattern, selector: int, sensitive: bool, d
     _check(_lib.mapa_launch_query(topo.handle, pat.handle, selector, int(bool(sensitive)), d_query_ptr,
                                   d_record_ptr, _flags(raw, prune), rank, world, busy_hint,
                                   _stream_ptr(stream)))
+
+
+def launch_query_wide(topo: Topology, pat: Pattern, selector: int, sensitive: bool, d_query_ptr: int,
+                      d_record_ptr: int, busy: int, raw: bool = False, rank: int = 0, world: int = 1, stream=None):
+    """mapa_launch_query_wide: deep-path device-resident launch (asynchronous);
+    busy must equal the query's busy mask (it sizes the suffix tables)."""
+    _check(_lib.mapa_launch_query_wide(topo.handle, pat.handle, selector, int(bool(sensitive)), d_query_ptr,
+                                       d_record_ptr, _flags(raw), rank, world, busy, _stream_ptr(stream)))
+
+
+def reduce_wide_records(records) -> WideRecord:
+    arr = (WideRecord * len(records))(*records)
+    out = WideRecord()
+    _check(_lib.mapa_reduce_wide_records(arr, len(records), ctypes.byref(out)))
+    return out
+
+
+def decode_wide(topo: Topology, pat: Pattern, busy: int, selector: int, sensitive: bool, record: WideRecord,
+                raw: bool = False) -> dict:
+    d = Decision()
+    _check(_lib.mapa_decode_wide(topo.handle, pat.handle, busy, selector, int(bool(sensitive)), _flags(raw),
+                                 ctypes.byref(record), ctypes.byref(d)), allow_no_capacity=True)
+    return decision_dict(d)
 
 
 def record_from_bytes(b: bytes) -> Record:

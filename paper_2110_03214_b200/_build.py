@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmapa.so")
 # one translation unit per topology width W, compiled in parallel
-SOURCES = [os.path.join(CSRC, f) for f in ("esa_w32.cu", "esa_w16.cu", "esa_w8.cu", "esa.cu", "mapa_host.cpp")]
+SOURCES = [os.path.join(CSRC, f) for f in ("esa_w32.cu", "esa_w16.cu", "esa_w8.cu", "esa_deep.cu", "esa.cu", "mapa_host.cpp")]
 HEADERS = [os.path.join(CSRC, f) for f in ("internal.h", "esa_kernels.cuh", "esa_w.cuh")] + \
     [os.path.join(os.path.dirname(HERE), "include", "mapa.h")]
 

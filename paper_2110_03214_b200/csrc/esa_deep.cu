@@ -1,0 +1,500 @@
+// esa_deep.cu — Enumerate-Score-Argmax for deep patterns (k <= 16, N <= 32)
+// on sm_100a (the paper's overhead study reaches
+// "9 GPUs and above" on 16-GPU graphs).
+//
+// Why a second kernel: the narrow kernels (esa_kernels.cuh) put the devices
+// of the LAST pattern vertex on the lanes and keep the DFS state of every
+// level in registers, so (a) they need a packed 63-bit key (15 + W + C(k,2)
+// bits: k <= 8 at W <= 16, k <= 6 at W = 32) and (b) when k approaches the
+// free count only nF - k + 1 lanes per scan do work.  Here:
+//   * vertices 0..T-1 (T = k - L) are placed by a warp-uniform DFS whose
+//     stack is distributed over the lanes (lane j holds f(j), the candidates
+//     left at level j and the partial score after j) and read back with
+//     shuffles; the increment of placing vertex d on v is one table read per
+//     lane j < d plus a warp reduction (REDUX), the lex-leader lower bound a
+//     REDUX max;
+//   * the last L vertices (L = 1..4, chosen on the host so a node has >= ~32
+//     leaves) are a lane-parallel scan over a launch-constant table of
+//     L-tuples of indices into the r = nF - T free devices left at every
+//     node (sorted, so index order = device order and the suffix-internal
+//     lex-leader constraints are applied once, on the host, when the table
+//     is built).  Per node the lanes fill a partial table pt[l][i] (score of
+//     suffix vertex T+l on the i-th remaining device w.r.t. the placed
+//     prefix, by popc over class masks) and a pair table wt[i][i2]; a leaf is
+//     then L + (#suffix-internal scored pairs) shared-memory reads and adds;
+//   * the argmax key is 192 bits (score << 32 | brev32(S), 128-bit edge
+//     code), compared lexicographically, so any k <= 16 fits.  It is built
+//     out of line only for a leaf whose score reaches the lane's best.  CTAs
+//     merge their best under a lock in the record (max is order independent:
+//     deterministic for every grid size and rank count).
+// Scores are the narrow path's (integer): Eq. 1 AggBW, Eq. 2 as
+// the dense rank of the census (host table, reading A9 holds for
+// m <= 120), Eq. 3 PreservedBW = T_F - sum inc_F(S) + inside(S).
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace mapa {
+namespace {
+
+constexpr unsigned kFullD = 0xFFFFFFFFu;
+constexpr int kBlockD = 256;
+constexpr int kWarpsD = kBlockD / 32;
+constexpr int kMaxDecodeD = 6;
+
+struct DeepWarp {
+    int pt[4][32];   // pt[l][i]: partial of suffix vertex T+l on remaining device i
+    int wt[16 * 16]; // wt[i*16 + i2]: pair value of remaining devices i, i2 (L >= 2: r <= 16)
+    int dl[32];      // remaining free devices, ascending
+    int fw[16];      // f(j) of the placed prefix (read by the out-of-line key builder)
+};
+
+struct DeepShared {
+    uint4 cm[kMaxN];
+    int tw[kMaxN * kMaxN];  // [v*32 + b] pair value: w(v,b) (Eq. 1/3), census delta (Eq. 2), 0 if v == b
+    int incF[kMaxN];        // inc_F(v) (Eq. 3)
+    uint32_t magic[kMaxN + 4];
+    uint32_t tup[kMaxTup];
+    DeepWarp w[kWarpsD];
+    unsigned long long rk[kWarpsD][4];
+};
+
+// dynamic shared memory: DeepShared + the Eq. 2 rank table (u16, (m+1)^2 <= 121^2)
+constexpr int kDeepSmemMax = (int)sizeof(DeepShared) + 2 * (kMaxEdges + 1) * (kMaxEdges + 1) + 16;
+
+extern __shared__ __align__(16) unsigned char g_dsmem[];
+__device__ __forceinline__ DeepShared &dsh() { return *reinterpret_cast<DeepShared *>(g_dsmem); }
+__device__ __forceinline__ uint16_t *dlut() { return reinterpret_cast<uint16_t *>(g_dsmem + sizeof(DeepShared)); }
+
+struct DBest {
+    unsigned long long hi;   // score << 32 | brev32(S); 0 = none
+    unsigned long long ehi, elo;
+};
+
+__device__ __forceinline__ bool key_gt(unsigned long long a0, unsigned long long a1, unsigned long long a2,
+                                       unsigned long long b0, unsigned long long b1, unsigned long long b2) {
+    return a0 != b0 ? a0 > b0 : (a1 != b1 ? a1 > b1 : a2 > b2);
+}
+
+__device__ __forceinline__ uint32_t nth_set_d(uint32_t m, uint32_t n) {
+    uint32_t pos = 0, c;
+    c = __popc(m & 0xFFFFu); if (n >= c) { n -= c; m >>= 16; pos += 16; }
+    c = __popc(m & 0xFFu);   if (n >= c) { n -= c; m >>= 8;  pos += 8; }
+    c = __popc(m & 0xFu);    if (n >= c) { n -= c; m >>= 4;  pos += 4; }
+    c = __popc(m & 0x3u);    if (n >= c) { n -= c; m >>= 2;  pos += 2; }
+    c = m & 1u;              if (n >= c) { pos += 1; }
+    return pos;
+}
+
+// Out-of-line: a leaf whose score reached the lane's best.  Builds the device
+// set, and (unless the set alone decides) the 128-bit edge code: pattern edge
+// (a, b) -> ranks ra, rb of f(a), f(b) inside S -> pair index p of (lo, hi)
+// in lex order over C(k,2) -> bit C(k,2)-1-p.
+template <int L>
+__device__ __noinline__ void consider_deep(const DeepTables &tb, const DeepWarp &W, DBest &b, uint32_t s,
+                                           uint32_t U, uint32_t w, int T) {
+    uint32_t sdev[4];
+    uint32_t S = U;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        sdev[l] = (uint32_t)W.dl[((w >> (8 * l)) & 0xFFu) >> 2];
+        S |= 1u << sdev[l];
+    }
+    const unsigned long long hi = ((unsigned long long)s << 32) | __brev(S);
+    if (hi < b.hi) return;
+    if (hi == b.hi && tb.clique) return;  // same set of a clique: same edges
+    const int k = tb.k, eb = tb.eb;
+    unsigned long long ehi = 0, elo = 0;
+    for (int e = 0; e < tb.m; ++e) {
+        const int a = tb.edge[e] & 15, c = tb.edge[e] >> 4;
+        const uint32_t da = a < T ? (uint32_t)W.fw[a] : sdev[a - T];
+        const uint32_t dc = c < T ? (uint32_t)W.fw[c] : sdev[c - T];
+        const int ra = __popc(S & ((1u << da) - 1u)), rc = __popc(S & ((1u << dc) - 1u));
+        const int lo = min(ra, rc), hi2 = max(ra, rc);
+        const int p = lo * (2 * k - lo - 1) / 2 + (hi2 - lo - 1);
+        const int q = eb - 1 - p;
+        if (q >= 64) ehi |= 1ull << (q - 64);
+        else elo |= 1ull << q;
+    }
+    if (key_gt(hi, ehi, elo, b.hi, b.ehi, b.elo)) {
+        b.hi = hi;
+        b.ehi = ehi;
+        b.elo = elo;
+    }
+}
+
+// Increment of placing pattern vertex d on device v, given the lane-held
+// prefix f(lane) for lane < d.  Eq. 1: back-neighbours of d; Eq. 3: every
+// placed vertex, minus inc_F(v); Eq. 2: census delta; Baseline: 0.
+template <int SEL>
+__device__ __forceinline__ int place_inc(const DeepTables &tb, int d, uint32_t v, uint32_t myf, int lane) {
+    constexpr int base = SEL & 3;
+    if constexpr (base == SEL_BASE) return 0;
+    int c = 0;
+    const bool e = base == SEL_INSENS ? true : ((tb.back[d] >> lane) & 1u) != 0;
+    if (lane < d && e) c = dsh().tw[myf * 32 + v];
+    int s = __reduce_add_sync(kFullD, c);
+    if constexpr (base == SEL_INSENS) s -= dsh().incF[v];
+    return s;
+}
+
+// Canonical mode: devices allowed for vertex d by its lex-leader sources.
+template <int SEL>
+__device__ __forceinline__ uint32_t allowed(const DeepTables &tb, int d, uint32_t myf, int lane) {
+    if constexpr (!(SEL & 4)) return kFullD;
+    const int c = (lane < d && ((tb.src[d] >> lane) & 1u)) ? (int)myf : -1;
+    const int lb = __reduce_max_sync(kFullD, c);
+    return lb < 0 ? kFullD : (0xFFFFFFFEu << lb);
+}
+
+// All leaves below a node whose prefix 0..T-1 is placed (set U, score A).
+template <int L, int SEL>
+__device__ __forceinline__ void suffix(const DeepTables &tb, uint32_t F, uint32_t U, int A, uint32_t myf, int lane,
+                                       int warp, int T, DBest &bst, unsigned long long &cnt) {
+    constexpr int base = SEL & 3;
+    constexpr bool canon = (SEL & 4) != 0;
+    DeepShared &S = dsh();
+    DeepWarp &W = S.w[warp];
+    const uint32_t R = F & ~U;
+    const int r = tb.r;
+    __syncwarp();  // previous readers of dl / pt / wt are done
+    if ((R >> lane) & 1u) W.dl[__popc(R & ((1u << lane) - 1u))] = lane;
+    uint32_t X[L];
+    uint32_t MINI = 0;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+        const int u = T + l;
+        if constexpr (base == SEL_INSENS) {
+            X[l] = U;
+        } else {
+            X[l] = __reduce_or_sync(kFullD, (lane < T && ((tb.back[u] >> lane) & 1u)) ? (1u << myf) : 0u);
+        }
+        if constexpr (canon) {
+            if (tb.pcon) {
+                const int lb = __reduce_max_sync(kFullD, (lane < T && ((tb.src[u] >> lane) & 1u)) ? (int)myf : -1);
+                const uint32_t mi = lb < 0 ? 0u : (uint32_t)__popc(R & ((2u << lb) - 1u));
+                MINI |= (4u * mi) << (8 * l);
+            }
+        }
+    }
+    __syncwarp();
+    if (lane < r) {
+        const int dev = W.dl[lane];
+        const uint4 c = S.cm[dev];
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+            int v;
+            if constexpr (base == SEL_SENS) {
+                v = __popc(c.x & X[l]) * tb.xsd + __popc((c.y | c.z) & X[l]);
+            } else if constexpr (base == SEL_BASE) {
+                v = 0;
+            } else {
+                v = 12 * __popc(X[l]) + 38 * __popc(c.x & X[l]) + 13 * __popc(c.y & X[l]) + 8 * __popc(c.z & X[l]);
+                if constexpr (base == SEL_INSENS) v -= S.incF[dev];
+            }
+            W.pt[l][lane] = v;
+        }
+    }
+    if constexpr (L >= 2) {
+        if (tb.nes) {
+            for (int p = lane; p < r * 16; p += 32) {
+                const int i = p >> 4, i2 = p & 15;
+                if (i2 < r) W.wt[p] = S.tw[W.dl[i] * 32 + W.dl[i2]];
+            }
+        }
+    }
+    __syncwarp();
+    const int nt = tb.ntup;
+    const int nes = tb.nes;
+    const char *ptb = reinterpret_cast<const char *>(&W.pt[0][0]);
+    const char *wtb = reinterpret_cast<const char *>(W.wt);
+    for (int t0 = 0; t0 < nt; t0 += 32) {
+        const int t = t0 + lane;
+        bool valid = t < nt;
+        const uint32_t w = valid ? S.tup[t] : 0u;
+        if constexpr (canon) {
+            if (tb.pcon) valid = valid && ((((w | 0x80808080u) - MINI) & 0x80808080u) == 0x80808080u);
+        }
+        int s = A;
+#pragma unroll
+        for (int l = 0; l < L; ++l) s += *reinterpret_cast<const int *>(ptb + 128 * l + ((w >> (8 * l)) & 0xFFu));
+        if constexpr (L >= 2 && base != SEL_BASE) {
+#pragma unroll
+            for (int e = 0; e < (L * (L - 1)) / 2; ++e) {
+                if (e < nes) {
+                    const uint32_t oa = (w >> (8 * tb.es[e][0])) & 0xFFu, ob = (w >> (8 * tb.es[e][1])) & 0xFFu;
+                    s += *reinterpret_cast<const int *>(wtb + 16 * oa + ob);
+                }
+            }
+        }
+        if constexpr (base == SEL_SENS) s = dlut()[s];
+        if constexpr (canon) {
+            if (tb.pcon) cnt += (unsigned long long)__popc(__ballot_sync(kFullD, valid));
+            else cnt += (unsigned long long)min(32, nt - t0);
+        } else {
+            cnt += (unsigned long long)min(32, nt - t0);
+        }
+        if (valid && ((unsigned long long)(uint32_t)s << 32) >= (bst.hi & 0xFFFFFFFF00000000ull))
+            consider_deep<L>(tb, W, bst, (uint32_t)s, U, w, T);
+    }
+}
+
+__device__ __forceinline__ uint32_t perm_count_d(int n, int d) {
+    uint32_t p = 1;
+    for (int j = 0; j < d; ++j) p *= (uint32_t)(n - j);
+    return p;
+}
+
+template <int L, int SEL>
+__global__ void __launch_bounds__(kBlockD, 2)
+esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut_g, const mapa_query *__restrict__ dq,
+         mapa_wide_record *__restrict__ rec, int D, int rank, int world, int stripe) {
+    constexpr int base = SEL & 3;
+    constexpr bool canon = (SEL & 4) != 0;
+    DeepShared &S = dsh();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = tb.n;
+    const uint32_t nmask = n >= 32 ? kFullD : ((1u << n) - 1u);
+    const uint32_t F = ~dq->busy & nmask;
+    const int nF = __popc(F);
+    const int T = tb.T;
+    if (tid < kMaxN) S.cm[tid] = make_uint4(tb.cm[tid][0], tb.cm[tid][1], tb.cm[tid][2], tb.cm[tid][3]);
+    if (tid <= kMaxN) S.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
+    for (int i = tid; i < kMaxN * kMaxN; i += kBlockD) {
+        const int v = i >> 5, b = i & 31;
+        int val = 0;
+        if (v != b && v < n && b < n) {
+            const int cls = ((tb.cm[b][0] >> v) & 1u) ? 0 : ((tb.cm[b][1] >> v) & 1u) ? 1 : ((tb.cm[b][2] >> v) & 1u) ? 2 : 3;
+            if constexpr (base == SEL_SENS) val = cls == 0 ? tb.xsd : (cls == 3 ? 0 : 1);
+            else val = cls == 0 ? 50 : (cls == 1 ? 25 : (cls == 2 ? 20 : 12));  // Table 1
+        }
+        S.tw[i] = val;
+    }
+    for (int i = tid; i < tb.ntup; i += kBlockD) S.tup[i] = tb.tup[i];
+    if constexpr (base == SEL_SENS)
+        for (int i = tid; i < tb.xsd * tb.xsd; i += kBlockD) dlut()[i] = lut_g[i];
+    if (tid < kMaxN) {
+        int inc = 0;
+        if (((F >> tid) & 1u) && tid < n)
+            inc = 12 * (nF - 1) + 38 * __popc(tb.cm[tid][0] & F) + 13 * __popc(tb.cm[tid][1] & F) +
+                  8 * __popc(tb.cm[tid][2] & F);
+        S.incF[tid] = inc;
+    }
+    if (tid == 0 && nF != tb.r + T && tb.k <= nF) atomicOr(&rec->status, 2u);  // busy_hint mismatch
+    __syncthreads();
+    int acc0 = 0;
+    if constexpr (base == SEL_INSENS) acc0 = __reduce_add_sync(kFullD, S.incF[lane]) / 2;  // T_F
+
+    // Rank-local item space and guided self-scheduling, as the narrow kernel.
+    const bool okq = tb.k <= nF && nF == tb.r + T;
+    const uint32_t N = okq ? perm_count_d(nF, D) : 0u;
+    const uint32_t Ls = (uint32_t)stripe;
+    const uint32_t nS = (N + Ls - 1u) / Ls;
+    const uint32_t myS = nS > (uint32_t)rank ? (nS - (uint32_t)rank + (uint32_t)world - 1u) / (uint32_t)world : 0u;
+    const bool ownLast = nS > 0 && ((nS - 1u) % (uint32_t)world) == (uint32_t)rank;
+    const uint32_t Nloc = myS == 0 ? 0u : (ownLast ? (myS - 1u) * Ls + (N - (nS - 1u) * Ls) : myS * Ls);
+    const uint32_t P = gridDim.x * (uint32_t)kWarpsD;
+    DBest bst{0ull, 0ull, 0ull};
+    unsigned long long cnt = 0;
+    uint32_t myf = 0, mycand = 0;
+    int myacc = 0;
+    for (;;) {
+        uint32_t start = 0, sz = 0;
+        if (lane == 0) {
+            const uint32_t cur = *reinterpret_cast<volatile uint32_t *>(&rec->ctr);
+            const uint32_t rem = cur < Nloc ? Nloc - cur : 0u;
+            sz = max(1u, rem / (2u * P));
+            start = atomicAdd(&rec->ctr, sz);
+        }
+        start = __shfl_sync(kFullD, start, 0);
+        sz = __shfl_sync(kFullD, sz, 0);
+        if (start >= Nloc) break;
+        const uint32_t end = min(start + sz, Nloc);
+        for (uint32_t j = start; j < end; ++j) {
+            const uint32_t sl = j / Ls;
+            uint32_t item = (sl * (uint32_t)world + (uint32_t)rank) * Ls + (j - sl * Ls);
+            // decode the prefix of depth D (mixed radix nF - j at level j)
+            uint32_t dg[kMaxDecodeD];
+#pragma unroll
+            for (int q = kMaxDecodeD - 1; q >= 0; --q) {
+                if (q < D) {
+                    const uint32_t rr = (uint32_t)(nF - q);
+                    const uint32_t qq = __umulhi(item, S.magic[rr]);
+                    dg[q] = item - qq * rr;
+                    item = qq;
+                } else {
+                    dg[q] = 0;
+                }
+            }
+            uint32_t U = 0;
+            int acc = acc0;
+            bool ok = true;
+#pragma unroll
+            for (int q = 0; q < kMaxDecodeD; ++q) {
+                if (q < D) {
+                    const uint32_t v = nth_set_d(F & ~U, dg[q]);
+                    if (canon && !((allowed<SEL>(tb, q, myf, lane) >> v) & 1u)) { ok = false; break; }
+                    acc += place_inc<SEL>(tb, q, v, myf, lane);
+                    if (lane == q) { myf = v; myacc = acc; }
+                    if (lane == 0) S.w[warp].fw[q] = (int)v;
+                    U |= 1u << v;
+                }
+            }
+            if (!ok) continue;
+            if (D == T) {
+                suffix<L, SEL>(tb, F, U, acc, myf, lane, warp, T, bst, cnt);
+                continue;
+            }
+            // explicit-stack DFS over levels D..T-1 (lane d holds level d)
+            int d = D;
+            uint32_t cand = F & ~U & allowed<SEL>(tb, d, myf, lane);
+            for (;;) {
+                if (cand == 0) {
+                    if (d == D) break;
+                    --d;
+                    const uint32_t v = __shfl_sync(kFullD, myf, d);
+                    U &= ~(1u << v);
+                    cand = __shfl_sync(kFullD, mycand, d);
+                    continue;
+                }
+                const uint32_t v = __ffs(cand) - 1;
+                cand &= cand - 1u;
+                const int accp = d == 0 ? acc0 : __shfl_sync(kFullD, myacc, d - 1);
+                const int a = accp + place_inc<SEL>(tb, d, v, myf, lane);
+                if (lane == d) { myf = v; mycand = cand; myacc = a; }
+                if (lane == 0) S.w[warp].fw[d] = (int)v;
+                U |= 1u << v;
+                if (d + 1 == T) {
+                    suffix<L, SEL>(tb, F, U, a, myf, lane, warp, T, bst, cnt);
+                    U &= ~(1u << v);
+                } else {
+                    ++d;
+                    cand = F & ~U & allowed<SEL>(tb, d, myf, lane);
+                }
+            }
+        }
+    }
+    // warp / block / grid lexicographic max of the 192-bit key
+    unsigned long long h = bst.hi, e1 = bst.ehi, e0 = bst.elo;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long h2 = __shfl_xor_sync(kFullD, h, o);
+        const unsigned long long a2 = __shfl_xor_sync(kFullD, e1, o);
+        const unsigned long long b2 = __shfl_xor_sync(kFullD, e0, o);
+        if (key_gt(h2, a2, b2, h, e1, e0)) { h = h2; e1 = a2; e0 = b2; }
+    }
+    if (lane == 0) {
+        S.rk[warp][0] = h;
+        S.rk[warp][1] = e1;
+        S.rk[warp][2] = e0;
+        S.rk[warp][3] = cnt;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long c = 0;
+        h = 0; e1 = 0; e0 = 0;
+        for (int w = 0; w < kWarpsD; ++w) {
+            c += S.rk[w][3];
+            if (key_gt(S.rk[w][0], S.rk[w][1], S.rk[w][2], h, e1, e0)) { h = S.rk[w][0]; e1 = S.rk[w][1]; e0 = S.rk[w][2]; }
+        }
+        if (c) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->leaves), c);
+        if (h) {
+            while (atomicCAS(&rec->lock, 0u, 1u) != 0u) {
+            }
+            __threadfence();
+            volatile unsigned long long *r = reinterpret_cast<volatile unsigned long long *>(rec);
+            if (key_gt(h, e1, e0, r[0], r[1], r[2])) {
+                r[0] = h;
+                r[1] = e1;
+                r[2] = e0;
+            }
+            __threadfence();
+            atomicExch(&rec->lock, 0u);
+        }
+    }
+}
+
+template <int L, int SEL>
+int launch_t(const DeepTables &tb, const uint16_t *lut, const mapa_query *dq, mapa_wide_record *rec, int D, int rank,
+             int world, int stripe, int grid, int smem, cudaStream_t st) {
+    // the attribute is always the fixed upper bound, so occupancy queries and
+    // launches agree
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute((const void *)esa_deep<L, SEL>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmemMax);
+        if (e != cudaSuccess) return (int)e;
+        configured = true;
+    }
+    if (smem > kDeepSmemMax) return (int)cudaErrorInvalidValue;
+    esa_deep<L, SEL><<<grid, kBlockD, smem, st>>>(tb, lut, dq, rec, D, rank, world, stripe);
+    return (int)cudaGetLastError();
+}
+
+template <int L, int SEL>
+const void *fn_t() { return (const void *)esa_deep<L, SEL>; }
+
+using DeepFn = int (*)(const DeepTables &, const uint16_t *, const mapa_query *, mapa_wide_record *, int, int, int,
+                       int, int, int, cudaStream_t);
+
+template <int L>
+DeepFn pick_sel(int sc) {
+    switch (sc & 7) {
+        case 0: return launch_t<L, 0>;
+        case 1: return launch_t<L, 1>;
+        case 2: return launch_t<L, 2>;
+        case 3: return launch_t<L, 3>;
+        case 4: return launch_t<L, 4>;
+        case 5: return launch_t<L, 5>;
+        case 6: return launch_t<L, 6>;
+        default: return launch_t<L, 7>;
+    }
+}
+
+template <int L>
+const void *pick_fn_sel(int sc) {
+    switch (sc & 7) {
+        case 0: return fn_t<L, 0>();
+        case 1: return fn_t<L, 1>();
+        case 2: return fn_t<L, 2>();
+        case 3: return fn_t<L, 3>();
+        case 4: return fn_t<L, 4>();
+        case 5: return fn_t<L, 5>();
+        case 6: return fn_t<L, 6>();
+        default: return fn_t<L, 7>();
+    }
+}
+
+}  // namespace
+
+int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_query *d_query,
+                mapa_wide_record *d_record, int depth, int rank, int world, int stripe, int grid, void *stream) {
+    const int smem = (int)sizeof(DeepShared) + ((sc & 3) == SEL_SENS ? 2 * tb.xsd * tb.xsd : 0);
+    DeepFn f = nullptr;
+    switch (tb.L) {
+        case 1: f = pick_sel<1>(sc); break;
+        case 2: f = pick_sel<2>(sc); break;
+        case 3: f = pick_sel<3>(sc); break;
+        case 4: f = pick_sel<4>(sc); break;
+        default: return (int)cudaErrorInvalidValue;
+    }
+    return f(tb, d_lut, d_query, d_record, depth, rank, world, stripe, grid, smem, (cudaStream_t)stream);
+}
+
+int max_blocks_per_sm_deep(int L, int sc, int lut_bytes) {
+    const void *f = nullptr;
+    switch (L) {
+        case 1: f = pick_fn_sel<1>(sc); break;
+        case 2: f = pick_fn_sel<2>(sc); break;
+        case 3: f = pick_fn_sel<3>(sc); break;
+        case 4: f = pick_fn_sel<4>(sc); break;
+        default: return 1;
+    }
+    const int smem = (int)sizeof(DeepShared) + lut_bytes;
+    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmemMax) != cudaSuccess) return 1;
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kBlockD, smem) != cudaSuccess) return 1;
+    return nb > 0 ? nb : 1;
+}
+
+}  // namespace mapa

@@ -14,7 +14,10 @@
 
 namespace mapa {
 
-constexpr int kMaxK = 8;
+constexpr int kMaxK = 8;        // narrow path (packed 63-bit key)
+constexpr int kMaxKDeep = 16;   // deep path (192-bit key)
+constexpr int kMaxEdges = 120;  // C(16,2)
+constexpr int kMaxTup = 2048;   // deep path: suffix index tuples per launch
 constexpr int kMaxN = 32;
 constexpr int kMaxPats = 16;      // patterns per batch / trace launch
 constexpr int kLutCapSingle = 1024;  // (m+1)^2 <= 841 for m <= 28
@@ -79,6 +82,27 @@ struct LaunchCfg {
     int chunk;      // items per counter grab
 };
 
+// Deep path (k <= 16): a warp-uniform DFS places vertices 0..T-1 (T = k - L),
+// then the lanes scan a table of L-tuples of indices into the r remaining free
+// devices (sorted), one tuple per lane.  Tuple entry: byte l = 4 * i_l
+// (a byte offset into the per-node partial table of suffix vertex T+l).
+struct DeepTables {
+    uint32_t cm[kMaxN][4];   // class masks, as DevTopo
+    int32_t n;
+    int32_t k, m, L, T, r;   // r = free devices left for the suffix at every node
+    int32_t ntup;            // valid tuples (suffix-internal lex-leader constraints applied)
+    int32_t xsd;             // census index stride m+1 (Eq. 2 table [x*(m+1) + y])
+    int32_t clique;
+    int32_t nes;             // scored suffix-internal pairs (Eq. 1/2: pattern edges; Eq. 3: all pairs)
+    int32_t pcon;            // canonical: some suffix vertex has a lex-leader source in the prefix
+    int32_t eb;              // C(k,2)
+    uint8_t es[8][2];        // suffix-internal pairs (l_a, l_b), l_a < l_b
+    uint16_t back[kMaxKDeep];  // back[u] bit j: pattern edge (j, u), j < u
+    uint16_t src[kMaxKDeep];   // src[u] bit j: canonical f(j) < f(u) (0 in RAW mode)
+    uint8_t edge[kMaxEdges];   // pattern edges a | b << 4
+    uint32_t tup[kMaxTup];
+};
+
 // Kernel launchers (esa.cu).  Return cudaError_t as int.
 // sc = sel_code(...) | 4 * canonical; canon = 1 unless MAPA_F_RAW.
 int launch_single(const SingleTables &tb, int sc, const mapa_query *d_query, mapa_record *d_record, int depth,
@@ -87,6 +111,10 @@ int launch_batch(const MultiTables &tb, int canon, int64_t nq, const mapa_query 
                  mapa_record *d_results, uint32_t *d_ctr, int grid, void *stream);
 int launch_trace(const MultiTables &tb, int canon, int ntraces, int nops, const mapa_trace_op *d_ops, int njobs,
                  const mapa_query *d_jobs, uint64_t *d_keys, void *stream);
+// deep path (esa_deep.cu); sc = sel_code | 4 * canonical
+int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_query *d_query,
+                mapa_wide_record *d_record, int depth, int rank, int world, int stripe, int grid, void *stream);
+int max_blocks_per_sm_deep(int L, int sc, int lut_bytes);
 int device_sm_count();
 int max_blocks_per_sm_single(int width, int k, int sc, int xs);
 int max_blocks_per_sm_batch(int width, int canon, int npats, int xs);

@@ -34,11 +34,13 @@ struct mapa_topology {
 struct mapa_pattern {
     int k = 0, m = 0;
     std::vector<std::pair<int, int>> edges;  // a < b, sorted
-    uint8_t adj[kMaxK][kMaxK];
-    uint8_t back[kMaxK];
-    uint8_t src[kMaxK];
-    int aut = 1;
+    uint16_t adj[kMaxKDeep];   // adjacency masks
+    uint16_t back[kMaxKDeep];  // back[j] bit i: edge (i, j), i < j
+    uint16_t src[kMaxKDeep];   // src[u] bit i: lex-leader f(i) < f(u)
+    uint64_t aut = 1;          // |Aut(P)| (16! < 2^45)
     std::vector<uint16_t> lut;   // (m+1)^2
+    void *d_lut = nullptr;     // device copy of lut (deep kernel), uploaded on first use
+    int d_lut_dev = -1;
 };
 
 namespace {
@@ -234,9 +236,29 @@ std::vector<uint16_t> rank_table(int m) {
 }
 
 // ---------------------------------------------------------------- patterns
+// Does an automorphism sigma of P exist with sigma(j) = j for j < i and
+// sigma(i) = u?  Backtracking over sigma(v), v = i+1..k-1, keeping adjacency
+// AND non-adjacency with every assigned vertex (so a complete sigma is an
+// automorphism) and equal degrees.
+bool aut_extends(const mapa_pattern *p, int v, int *sig, uint32_t used) {
+    const int k = p->k;
+    if (v == k) return true;
+    for (int c = 0; c < k; ++c) {
+        if ((used >> c) & 1u) continue;
+        if (__builtin_popcount(p->adj[c]) != __builtin_popcount(p->adj[v])) continue;
+        bool ok = true;
+        for (int w = 0; w < v && ok; ++w)
+            ok = ((p->adj[v] >> w) & 1u) == ((p->adj[c] >> sig[w]) & 1u);
+        if (!ok) continue;
+        sig[v] = c;
+        if (aut_extends(p, v + 1, sig, used | (1u << c))) return true;
+    }
+    return false;
+}
+
 mapa_status compile_pattern(int k, const std::vector<std::pair<int, int>> &raw, uint32_t flags,
                             mapa_pattern **out) {
-    if (k < 1 || k > kMaxK) return fail(MAPA_E_UNSUPPORTED, "pattern: need 1 <= k <= 8");
+    if (k < 1 || k > kMaxKDeep) return fail(MAPA_E_UNSUPPORTED, "pattern: need 1 <= k <= 16");
     mapa_pattern *p = new (std::nothrow) mapa_pattern();
     if (!p) return fail(MAPA_E_INVALID_ARG, "out of memory");
     p->k = k;
@@ -246,49 +268,48 @@ mapa_status compile_pattern(int k, const std::vector<std::pair<int, int>> &raw, 
         if (a < 0 || b < 0 || a >= k || b >= k) { delete p; return fail(MAPA_E_INVALID_ARG, "pattern: vertex id out of range"); }
         if (a == b) { delete p; return fail(MAPA_E_INVALID_ARG, "pattern: self loop"); }
         if (a > b) std::swap(a, b);
-        if (p->adj[a][b]) { delete p; return fail(MAPA_E_INVALID_ARG, "pattern: duplicate edge"); }
-        p->adj[a][b] = p->adj[b][a] = 1;
+        if ((p->adj[a] >> b) & 1u) { delete p; return fail(MAPA_E_INVALID_ARG, "pattern: duplicate edge"); }
+        p->adj[a] |= (uint16_t)(1u << b);
+        p->adj[b] |= (uint16_t)(1u << a);
         p->edges.push_back({a, b});
     }
     std::sort(p->edges.begin(), p->edges.end());
     p->m = (int)p->edges.size();
     if (k > 1 && !(flags & MAPA_F_ALLOW_DISCONNECTED)) {
-        int seen = 1, stack[kMaxK], sp = 0, vis = 1;
-        stack[sp++] = 0;
-        while (sp) {
-            const int u = stack[--sp];
-            for (int v = 0; v < k; ++v)
-                if (p->adj[u][v] && !((vis >> v) & 1)) { vis |= 1 << v; ++seen; stack[sp++] = v; }
+        uint32_t vis = 1, frontier = 1;
+        while (frontier) {
+            uint32_t nxt = 0;
+            for (int u = 0; u < k; ++u)
+                if ((frontier >> u) & 1u) nxt |= p->adj[u];
+            frontier = nxt & ~vis;
+            vis |= nxt;
         }
-        if (seen != k) { delete p; return fail(MAPA_E_DISCONNECTED, "pattern: disconnected (k > 1)"); }
+        if (vis != (k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u))) {
+            delete p;
+            return fail(MAPA_E_DISCONNECTED, "pattern: disconnected (k > 1)");
+        }
     }
-    for (int j = 0; j < k; ++j) {
-        p->back[j] = 0;
-        for (int i = 0; i < j; ++i)
-            if (p->adj[i][j]) p->back[j] |= (uint8_t)(1u << i);
-    }
-    // Aut(P) by brute force (k! <= 40320), then lex-leader constraints along
-    // the point-stabiliser chain: for every vertex i, every u != i in the orbit
-    // of i under the stabiliser of 0..i-1 gets the constraint f(i) < f(u).
-    // This keeps exactly the lex-min mapping of every Aut-orbit.
-    std::vector<std::vector<int>> aut;
-    std::vector<int> s(k);
-    for (int i = 0; i < k; ++i) s[i] = i;
-    do {
-        bool ok = true;
-        for (auto &e : p->edges)
-            if (!p->adj[s[e.first]][s[e.second]]) { ok = false; break; }
-        if (ok) aut.push_back(s);
-    } while (std::next_permutation(s.begin(), s.end()));
-    p->aut = (int)aut.size();
+    for (int j = 0; j < k; ++j) p->back[j] = (uint16_t)(p->adj[j] & ((1u << j) - 1u));
+    // Point-stabiliser chain of Aut(P): the orbit of i under the automorphisms
+    // fixing 0..i-1.  Every u != i in it gets the lex-leader constraint
+    // f(i) < f(u); this keeps exactly the lex-min mapping of every Aut-orbit
+    // (DESIGN.md).  |Aut| = product of the orbit sizes (orbit-stabiliser).
     std::memset(p->src, 0, sizeof(p->src));
+    p->aut = 1;
+    int sig[kMaxKDeep];
     for (int i = 0; i < k; ++i) {
-        for (auto &a : aut) {
-            bool fixes = true;
-            for (int j = 0; j < i; ++j)
-                if (a[j] != j) { fixes = false; break; }
-            if (fixes && a[i] != i) p->src[a[i]] |= (uint8_t)(1u << i);
+        uint64_t orb = 0;
+        for (int u = i; u < k; ++u) {
+            for (int j = 0; j < i; ++j) sig[j] = j;
+            bool ok = __builtin_popcount(p->adj[u]) == __builtin_popcount(p->adj[i]);
+            for (int w = 0; w < i && ok; ++w) ok = ((p->adj[i] >> w) & 1u) == ((p->adj[u] >> w) & 1u);
+            if (!ok) continue;
+            sig[i] = u;
+            if (!aut_extends(p, i + 1, sig, ((1u << i) - 1u) | (1u << u))) continue;
+            ++orb;
+            if (u != i) p->src[u] |= (uint16_t)(1u << i);
         }
+        p->aut *= orb;
     }
     p->lut = rank_table(p->m);
     *out = p;
@@ -303,7 +324,7 @@ void fill_devpattern(const mapa_pattern *p, bool raw, uint16_t lut_off, DevPatte
     dp.clique = p->m == dp.eb;
     for (int j = 0; j < p->k; ++j) {
         for (int u = j + 1; u < p->k; ++u) {
-            if (p->adj[j][u]) dp.fwd_back[j] |= (uint8_t)(1u << u);
+            if ((p->adj[j] >> u) & 1u) dp.fwd_back[j] |= (uint8_t)(1u << u);
             if (!raw && ((p->src[u] >> j) & 1)) dp.fwd_src[j] |= (uint8_t)(1u << u);
         }
         dp.dback[j] = (uint8_t)__builtin_popcount(p->back[j]);
@@ -313,8 +334,9 @@ void fill_devpattern(const mapa_pattern *p, bool raw, uint16_t lut_off, DevPatte
     dp.aut = (uint16_t)p->aut;
 }
 
+// narrow path: k <= 8 and the packed 63-bit key fits
 bool key_fits(const mapa_topology *t, const mapa_pattern *p) {
-    return 15 + t->width + p->k * (p->k - 1) / 2 <= 63;
+    return p->k <= kMaxK && 15 + t->width + p->k * (p->k - 1) / 2 <= 63;
 }
 
 uint64_t perm_count(int n, int d) {
@@ -397,6 +419,243 @@ Plan plan_single(const mapa_topology *t, const mapa_pattern *p, int sensk, int n
     return pl;
 }
 
+// ------------------------------------------------------------------ deep path
+// Plan of one deep launch (esa_deep.cu): suffix length L, its tuple table, the
+// decoded prefix depth D, the stripe and the grid.
+struct DeepPlan {
+    int sc, depth, stripe, grid;
+    uint64_t items;
+};
+
+// Suffix-internal scored pairs for suffix length L: Eq. 3 every pair, Eq. 1 /
+// Eq. 2 the pattern edges, Baseline none.
+int suffix_pairs(const mapa_pattern *p, int L, int base, uint8_t (*es)[2]) {
+    const int T = p->k - L;
+    int n = 0;
+    for (int a = 0; a < L; ++a)
+        for (int b = a + 1; b < L; ++b) {
+            const bool e = base == SEL_INSENS || (base != SEL_BASE && ((p->adj[T + a] >> (T + b)) & 1u));
+            if (e) { es[n][0] = (uint8_t)a; es[n][1] = (uint8_t)b; ++n; }
+        }
+    return n;
+}
+
+// Valid L-tuples of distinct indices into r sorted devices (lex order); the
+// suffix-internal lex-leader constraints f(T+a) < f(T+b) become i_a < i_b.
+// Entry byte l = 4 * i_l.  Returns the count, or -1 above cap.
+int build_tuples(const mapa_pattern *p, int L, int r, bool canon, uint32_t *out, int cap) {
+    const int T = p->k - L;
+    int n = 0, idx[4] = {0, 0, 0, 0};
+    int total = 1;
+    for (int l = 0; l < L; ++l) total *= r;
+    for (int t = 0; t < total; ++t) {
+        int x = t;
+        for (int l = L - 1; l >= 0; --l) { idx[l] = x % r; x /= r; }
+        bool ok = true;
+        for (int a = 0; a < L && ok; ++a)
+            for (int b = a + 1; b < L && ok; ++b) {
+                if (idx[a] == idx[b]) ok = false;
+                else if (canon && ((p->src[T + b] >> (T + a)) & 1u) && !(idx[a] < idx[b])) ok = false;
+            }
+        if (!ok) continue;
+        if (n >= cap) return -1;
+        uint32_t w = 0;
+        for (int l = 0; l < L; ++l) w |= (uint32_t)(4 * idx[l]) << (8 * l);
+        if (out) out[n] = w;
+        ++n;
+    }
+    return n;
+}
+
+mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selector, int sens, uint32_t flags,
+                      int nF, int world, DeepTables *tb, DeepPlan *pl) {
+    const int k = p->k;
+    const bool canon = !(flags & MAPA_F_RAW) && p->aut > 1;
+    const int base = sel_code(selector, sens);
+    std::memset(tb, 0, sizeof(*tb));
+    DevTopo dt;
+    fill_devtopo(t, dt);
+    std::memcpy(tb->cm, dt.cm, sizeof(tb->cm));
+    tb->n = t->n;
+    tb->k = k;
+    tb->m = p->m;
+    tb->xsd = p->m + 1;
+    tb->eb = k * (k - 1) / 2;
+    tb->clique = p->m == tb->eb;
+    for (int u = 0; u < k; ++u) {
+        tb->back[u] = p->back[u];
+        tb->src[u] = canon ? p->src[u] : 0;
+    }
+    for (int e = 0; e < p->m; ++e) tb->edge[e] = (uint8_t)(p->edges[e].first | (p->edges[e].second << 4));
+    // suffix length L: smallest modelled cost per leaf (node overhead + rounds of 32 lanes)
+    double best = 1e30;
+    int bestL = 0;
+    for (int L = 1; L <= std::min(k, 4); ++L) {
+        const int r = nF - k + L;
+        if (r < L || r > 32 || (L >= 2 && r > 16)) continue;
+        const int nt = build_tuples(p, L, r, canon, nullptr, kMaxTup);
+        if (nt <= 0) continue;
+        uint8_t es[8][2];
+        const int nes = suffix_pairs(p, L, base, es);
+        const double node = 40.0 + 12.0 * L + (L >= 2 && nes ? 6.0 * ((r * 16 + 31) / 32) : 0.0) + 6.0 * k;
+        const double round = 12.0 + 4.0 * L + 4.0 * nes;
+        const double cost = (node + round * ((nt + 31) / 32)) / nt;
+        if (cost < best * 0.98) { best = cost; bestL = L; }
+    }
+    if (!bestL) return fail(MAPA_E_UNSUPPORTED, "deep path: no feasible suffix length");
+    const int L = bestL, T = k - L, r = nF - T;
+    tb->L = L;
+    tb->T = T;
+    tb->r = r;
+    tb->ntup = build_tuples(p, L, r, canon, tb->tup, kMaxTup);
+    tb->nes = suffix_pairs(p, L, base, tb->es);
+    tb->pcon = 0;
+    if (canon)
+        for (int l = 0; l < L; ++l)
+            if (p->src[T + l] & ((1u << T) - 1u)) tb->pcon = 1;
+    pl->sc = base | (canon ? 4 : 0);
+    // decoded prefix depth: enough items for ~8 per resident warp (x world)
+    int sm = device_sm_count();
+    if (sm <= 0) sm = 148;
+    const int occ = max_blocks_per_sm_deep(L, pl->sc, base == SEL_SENS ? 2 * tb->xsd * tb->xsd : 0);
+    const uint64_t warps = (uint64_t)sm * occ * 8;
+    const uint64_t target = 8ull * warps * (uint64_t)world;
+    int d = 0;
+    while (d < std::min(T, 6) && perm_count(nF, d) < target && perm_count(nF, d + 1) < (1ull << 27)) ++d;
+    pl->depth = d;
+    pl->items = perm_count(nF, d);
+    const uint64_t stripe = world == 1 ? std::max<uint64_t>(1, pl->items)
+                                       : std::max<uint64_t>(1, (pl->items + 64ull * world - 1) / (64ull * world));
+    pl->stripe = (int)std::min<uint64_t>(stripe, 1u << 30);
+    const uint64_t local = (pl->items + world - 1) / world;
+    pl->grid = (int)std::max<uint64_t>(1, std::min<uint64_t>((local + 7) / 8, (uint64_t)sm * occ));
+    return MAPA_OK;
+}
+
+mapa_status upload_lut(const mapa_pattern *pc) {
+    mapa_pattern *p = const_cast<mapa_pattern *>(pc);  // the device copy caches the immutable table
+    int dev = 0, err;
+    if ((err = (int)cudaGetDevice(&dev))) return cuda_fail(err, "cudaGetDevice");
+    if (p->d_lut && p->d_lut_dev == dev) return MAPA_OK;
+    if (p->d_lut) { cudaFree(p->d_lut); p->d_lut = nullptr; }
+    const size_t bytes = p->lut.size() * sizeof(uint16_t);
+    if ((err = (int)cudaMalloc(&p->d_lut, bytes))) return cuda_fail(err, "cudaMalloc (rank table)");
+    if ((err = (int)cudaMemcpy(p->d_lut, p->lut.data(), bytes, cudaMemcpyHostToDevice))) return cuda_fail(err, "H2D rank table");
+    p->d_lut_dev = dev;
+    return MAPA_OK;
+}
+
+// Lex-first bijection pi: V(P) -> S (pattern-vertex order, devices ascending)
+// with pi(E(P)) = E: keep adjacency and non-adjacency with every placed vertex
+// and equal degrees; the first complete map is the lex-first one.
+bool first_mapping(const mapa_pattern *p, const std::vector<int> &ds, const uint32_t *eadj, int v, int *pi,
+                   uint32_t used) {
+    const int k = p->k;
+    if (v == k) return true;
+    for (int c : ds) {
+        if ((used >> c) & 1u) continue;
+        if (__builtin_popcount(eadj[c]) != __builtin_popcount(p->adj[v])) continue;
+        bool ok = true;
+        for (int w = 0; w < v && ok; ++w) ok = (((p->adj[v] >> w) & 1u) != 0) == (((eadj[c] >> pi[w]) & 1u) != 0);
+        if (!ok) continue;
+        pi[v] = c;
+        if (first_mapping(p, ds, eadj, v + 1, pi, used | (1u << c))) return true;
+    }
+    return false;
+}
+
+// Decision from (S, E) (both paths): lex-first mapping, census, Eq. 1/2/3, and
+// the self-check of the key's score.
+mapa_status fill_decision(const mapa_topology *t, const mapa_pattern *p, uint32_t F, uint32_t S,
+                          std::vector<std::pair<int, int>> E, int selector, int sens, uint32_t score,
+                          mapa_decision &d) {
+    const int k = p->k;
+    if (__builtin_popcount(S) != k || (S & ~F)) return fail(MAPA_E_INTERNAL, "decoded device set inconsistent");
+    if ((int)E.size() != p->m) return fail(MAPA_E_INTERNAL, "decoded edge set has wrong size");
+    std::sort(E.begin(), E.end());
+    std::vector<int> ds;
+    for (int dv = 0; dv < t->n; ++dv)
+        if ((S >> dv) & 1u) ds.push_back(dv);
+    uint32_t eadj[kMaxN] = {0};
+    for (auto &e : E) { eadj[e.first] |= 1u << e.second; eadj[e.second] |= 1u << e.first; }
+    int pi[kMaxKDeep];
+    if (!first_mapping(p, ds, eadj, 0, pi, 0u))
+        return fail(MAPA_E_INTERNAL, "no mapping of the decoded set yields the decoded edges");
+    int agg = 0, x = 0, y = 0, z = 0;
+    for (auto &e : E) {
+        const int c = t->cls[e.first][e.second];
+        agg += kClassBw[c];
+        if (c == 0) ++x;
+        else if (c == 3) ++z;
+        else ++y;
+    }
+    int pres = 0;
+    for (int u = 0; u < t->n; ++u)
+        for (int v = u + 1; v < t->n; ++v)
+            if (((F >> u) & (F >> v) & 1u) && !((S >> u) & 1u) && !((S >> v) & 1u)) pres += bw_of(t, u, v);
+    uint32_t expect = 0;
+    if (selector == MAPA_SEL_GREEDY) expect = (uint32_t)agg;
+    else if (selector == MAPA_SEL_PRESERVE) expect = sens ? p->lut[x * (p->m + 1) + y] : (uint32_t)pres;
+    if (expect != score) return fail(MAPA_E_INTERNAL, "key score does not match the decoded match");
+    d.status = MAPA_OK;
+    d.device_mask = S;
+    for (int i = 0; i < k; ++i) d.mapping[i] = (int8_t)pi[i];
+    for (size_t i = 0; i < E.size(); ++i) { d.used[i][0] = E[i].first; d.used[i][1] = E[i].second; }
+    d.x = x; d.y = y; d.z = z;
+    d.agg_bw = agg;
+    d.preserved_bw = pres;
+    d.score = (int32_t)score;
+    d.pred_effbw = eq2(x, y, z);
+    return MAPA_OK;
+}
+
+mapa_status decode_wide(const mapa_topology *t, const mapa_pattern *p, uint32_t busy, int selector, int sens,
+                        uint32_t flags, const mapa_wide_record *rec, mapa_decision *out) {
+    mapa_decision d;
+    std::memset(&d, 0, sizeof(d));
+    d.k = p->k;
+    d.m = p->m;
+    d.key = rec->key;
+    d.ecode[0] = rec->ecode_hi;
+    d.ecode[1] = rec->ecode_lo;
+    d.leaves_scored = rec->leaves;
+    if (flags & MAPA_F_RAW) {
+        d.raw_embeddings = rec->leaves;
+        d.distinct_matches = rec->leaves / p->aut;
+    } else {
+        d.distinct_matches = rec->leaves;
+        d.raw_embeddings = rec->leaves * p->aut;
+    }
+    const uint32_t F = ~busy & nmask_of(t->n);
+    if (rec->status != 0) return fail(MAPA_E_INVALID_ARG, "device reported a bad query (busy_hint != d_query->busy?)");
+    if (rec->key == 0) {
+        d.status = MAPA_NO_CAPACITY;
+        *out = d;
+        return MAPA_NO_CAPACITY;
+    }
+    const int k = p->k, eb = k * (k - 1) / 2;
+    const uint32_t score = (uint32_t)(rec->key >> 32);
+    uint32_t S = 0;
+    for (int dv = 0; dv < 32; ++dv)
+        if ((rec->key >> (31 - dv)) & 1u) S |= 1u << dv;
+    std::vector<int> ds;
+    for (int dv = 0; dv < 32; ++dv)
+        if ((S >> dv) & 1u) ds.push_back(dv);
+    if ((int)ds.size() != k) return fail(MAPA_E_INTERNAL, "decoded device set has wrong size");
+    std::vector<std::pair<int, int>> E;
+    int pidx = 0;
+    for (int a = 0; a < k; ++a)
+        for (int b = a + 1; b < k; ++b, ++pidx) {
+            const int q = eb - 1 - pidx;
+            const uint64_t bit = q >= 64 ? (rec->ecode_hi >> (q - 64)) & 1u : (rec->ecode_lo >> q) & 1u;
+            if (bit) E.push_back({ds[a], ds[b]});
+        }
+    mapa_status st = fill_decision(t, p, F, S, E, selector, sens, score, d);
+    if (st != MAPA_OK) return st;
+    *out = d;
+    return MAPA_OK;
+}
+
 mapa_status decode_record(const mapa_topology *t, const mapa_pattern *p, uint32_t busy, int selector,
                           int sens, uint32_t flags, const mapa_record *rec, mapa_decision *out) {
     mapa_decision d;
@@ -435,56 +694,18 @@ mapa_status decode_record(const mapa_topology *t, const mapa_pattern *p, uint32_
     uint32_t S = 0;
     for (int dv = 0; dv < W; ++dv)
         if ((sb >> (W - 1 - dv)) & 1u) S |= 1u << dv;
-    if (__builtin_popcount(S) != k || (S & ~F)) return fail(MAPA_E_INTERNAL, "decoded device set inconsistent");
     std::vector<int> ds;
     for (int dv = 0; dv < t->n; ++dv)
         if ((S >> dv) & 1u) ds.push_back(dv);
+    if ((int)ds.size() != k) return fail(MAPA_E_INTERNAL, "decoded device set inconsistent");
     // used-edge set from the edge code (pair p in lex order of rank pairs)
     std::vector<std::pair<int, int>> E;
     int pidx = 0;
     for (int a = 0; a < k; ++a)
         for (int b = a + 1; b < k; ++b, ++pidx)
             if ((ecode >> (eb - 1 - pidx)) & 1u) E.push_back({ds[a], ds[b]});
-    if ((int)E.size() != p->m) return fail(MAPA_E_INTERNAL, "decoded edge set has wrong size");
-    std::sort(E.begin(), E.end());
-    // lex-first mapping of S producing E
-    std::vector<int> pi = ds;
-    bool found = false;
-    do {
-        std::vector<std::pair<int, int>> img;
-        for (auto &e : p->edges) {
-            int a = pi[e.first], b = pi[e.second];
-            img.push_back({std::min(a, b), std::max(a, b)});
-        }
-        std::sort(img.begin(), img.end());
-        if (img == E) { found = true; break; }
-    } while (std::next_permutation(pi.begin(), pi.end()));
-    if (!found) return fail(MAPA_E_INTERNAL, "no mapping of the decoded set yields the decoded edges");
-    int agg = 0, x = 0, y = 0, z = 0;
-    for (auto &e : E) {
-        const int c = t->cls[e.first][e.second];
-        agg += kClassBw[c];
-        if (c == 0) ++x;
-        else if (c == 3) ++z;
-        else ++y;
-    }
-    int pres = 0;
-    for (int u = 0; u < t->n; ++u)
-        for (int v = u + 1; v < t->n; ++v)
-            if (((F >> u) & (F >> v) & 1u) && !((S >> u) & 1u) && !((S >> v) & 1u)) pres += bw_of(t, u, v);
-    uint32_t expect = 0;
-    if (selector == MAPA_SEL_GREEDY) expect = (uint32_t)agg;
-    else if (selector == MAPA_SEL_PRESERVE) expect = sens ? p->lut[x * (p->m + 1) + y] : (uint32_t)pres;
-    if (expect != score) return fail(MAPA_E_INTERNAL, "key score does not match the decoded match");
-    d.status = MAPA_OK;
-    d.device_mask = S;
-    for (int i = 0; i < k; ++i) d.mapping[i] = (int8_t)pi[i];
-    for (size_t i = 0; i < E.size(); ++i) { d.used[i][0] = E[i].first; d.used[i][1] = E[i].second; }
-    d.x = x; d.y = y; d.z = z;
-    d.agg_bw = agg;
-    d.preserved_bw = pres;
-    d.score = (int32_t)score;
-    d.pred_effbw = eq2(x, y, z);
+    mapa_status st = fill_decision(t, p, F, S, E, selector, sens, score, d);
+    if (st != MAPA_OK) return st;
     *out = d;
     return MAPA_OK;
 }
@@ -580,7 +801,7 @@ mapa_status mapa_set_busy(mapa_topology *t, uint32_t busy) {
 
 mapa_status mapa_load_pattern(int32_t k, int32_t m, const int32_t *edges, uint32_t flags, mapa_pattern **out) {
     if (!out || m < 0 || (m > 0 && !edges)) return fail(MAPA_E_INVALID_ARG, "bad pattern arguments");
-    if (k < 1 || k > kMaxK) return fail(MAPA_E_UNSUPPORTED, "pattern: need 1 <= k <= 8");
+    if (k < 1 || k > kMaxKDeep) return fail(MAPA_E_UNSUPPORTED, "pattern: need 1 <= k <= 16");
     if (m > k * (k - 1) / 2) return fail(MAPA_E_INVALID_ARG, "pattern: more edges than vertex pairs");
     std::vector<std::pair<int, int>> e;
     for (int i = 0; i < m; ++i) e.push_back({edges[2 * i], edges[2 * i + 1]});
@@ -589,7 +810,7 @@ mapa_status mapa_load_pattern(int32_t k, int32_t m, const int32_t *edges, uint32
 
 mapa_status mapa_make_pattern(int32_t shape, int32_t k, mapa_pattern **out) {
     if (!out) return fail(MAPA_E_INVALID_ARG, "null out");
-    if (k < 1 || k > kMaxK) return fail(MAPA_E_UNSUPPORTED, "pattern: need 1 <= k <= 8");
+    if (k < 1 || k > kMaxKDeep) return fail(MAPA_E_UNSUPPORTED, "pattern: need 1 <= k <= 16");
     std::vector<std::pair<int, int>> e;
     const bool ring = shape == MAPA_SHAPE_RING || shape == MAPA_SHAPE_RINGTREE;
     const bool tree = shape == MAPA_SHAPE_TREE || shape == MAPA_SHAPE_RINGTREE;
@@ -612,14 +833,19 @@ mapa_status mapa_make_pattern(int32_t shape, int32_t k, mapa_pattern **out) {
     return compile_pattern(k, e, shape == MAPA_SHAPE_EDGELESS ? MAPA_F_ALLOW_DISCONNECTED : 0, out);
 }
 
-void mapa_free_pattern(mapa_pattern *p) { delete p; }
+void mapa_free_pattern(mapa_pattern *p) {
+    if (!p) return;
+    if (p->d_lut) cudaFree(p->d_lut);
+    delete p;
+}
 
 mapa_status mapa_get_pattern_info(const mapa_pattern *p, mapa_pattern_info *out) {
     if (!p || !out) return fail(MAPA_E_INVALID_ARG, "null argument");
     std::memset(out, 0, sizeof(*out));
     out->k = p->k;
     out->m = p->m;
-    out->aut_order = p->aut;
+    out->aut_order = (int32_t)std::min<uint64_t>(p->aut, 0x7FFFFFFFull);
+    out->aut_order64 = p->aut;
     for (int j = 0; j < p->k; ++j) { out->back[j] = p->back[j]; out->lex_src[j] = p->src[j]; }
     for (int e = 0; e < p->m; ++e) { out->edges[e][0] = p->edges[e].first; out->edges[e][1] = p->edges[e].second; }
     return MAPA_OK;
@@ -628,7 +854,7 @@ mapa_status mapa_get_pattern_info(const mapa_pattern *p, mapa_pattern_info *out)
 double mapa_pred_effbw(int32_t x, int32_t y, int32_t z) { return eq2(x, y, z); }
 
 mapa_status mapa_effbw_rank_table(int32_t m, uint16_t *out) {
-    if (m < 0 || m > 28 || !out) return fail(MAPA_E_INVALID_ARG, "m must be 0..28");
+    if (m < 0 || m > kMaxEdges || !out) return fail(MAPA_E_INVALID_ARG, "m must be 0..120");
     std::vector<uint16_t> l = rank_table(m);
     std::memcpy(out, l.data(), l.size() * sizeof(uint16_t));
     return MAPA_OK;
@@ -641,7 +867,8 @@ mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int
     if (!t || !p || !d_query || !d_record) return fail(MAPA_E_INVALID_ARG, "null argument");
     if (world < 1 || rank < 0 || rank >= world) return fail(MAPA_E_INVALID_ARG, "bad rank/world");
     if (selector < 0 || selector > 2) return fail(MAPA_E_INVALID_ARG, "bad selector");
-    if (!key_fits(t, p)) return fail(MAPA_E_UNSUPPORTED, "key budget 15 + W + C(k,2) > 63");
+    if (!key_fits(t, p))
+        return fail(MAPA_E_UNSUPPORTED, "narrow path needs k <= 8 and 15 + W + C(k,2) <= 63 (use the deep path)");
     const int nF = busy_hint == 0xFFFFFFFFu ? t->n : __builtin_popcount(~busy_hint & nmask_of(t->n));
     static_assert(sizeof(SingleTables) < 32000, "kernel parameter block too large");
     SingleTables tb;
@@ -683,11 +910,58 @@ mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint32_t 
     return decode_record(t, p, busy, selector, sens, flags, record, out);
 }
 
+mapa_status mapa_launch_query_wide(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
+                                   int32_t sensitive, const mapa_query *d_query, mapa_wide_record *d_record,
+                                   uint32_t flags, int32_t rank, int32_t world, uint32_t busy_hint, void *stream) {
+    if (!t || !p || !d_query || !d_record) return fail(MAPA_E_INVALID_ARG, "null argument");
+    if (world < 1 || rank < 0 || rank >= world) return fail(MAPA_E_INVALID_ARG, "bad rank/world");
+    if (selector < 0 || selector > 2) return fail(MAPA_E_INVALID_ARG, "bad selector");
+    if (busy_hint & ~nmask_of(t->n)) return fail(MAPA_E_INVALID_ARG, "deep path needs busy_hint = the query's busy mask");
+    const int nF = __builtin_popcount(~busy_hint & nmask_of(t->n));
+    cudaStream_t st = (cudaStream_t)stream;
+    int err = (int)cudaMemsetAsync(d_record, 0, sizeof(mapa_wide_record), st);
+    if (err) return cuda_fail(err, "cudaMemsetAsync");
+    if (p->k > nF) return MAPA_OK;  // no capacity: the zeroed record says so (key 0)
+    static_assert(sizeof(DeepTables) < 32000, "kernel parameter block too large");
+    static thread_local DeepTables *tbp = nullptr;  // ~10 KB: keep off the stack
+    if (!tbp) tbp = new DeepTables();
+    DeepPlan pl{};
+    mapa_status s = plan_deep(t, p, selector, sensitive, flags, nF, world, tbp, &pl);
+    if (s != MAPA_OK) return s;
+    if (sel_code(selector, sensitive) == SEL_SENS && (s = upload_lut(p)) != MAPA_OK) return s;
+    err = launch_deep(*tbp, pl.sc, (const uint16_t *)p->d_lut, d_query, d_record, pl.depth, rank, world,
+                      pl.stripe, pl.grid, stream);
+    if (err) return cuda_fail(err, "esa_deep launch");
+    return MAPA_OK;
+}
+
+mapa_status mapa_reduce_wide_records(const mapa_wide_record *records, int32_t n, mapa_wide_record *out) {
+    if (!records || !out || n < 1) return fail(MAPA_E_INVALID_ARG, "bad records");
+    mapa_wide_record r;
+    std::memset(&r, 0, sizeof(r));
+    for (int i = 0; i < n; ++i) {
+        const mapa_wide_record &q = records[i];
+        const bool gt = q.key != r.key ? q.key > r.key
+                                       : (q.ecode_hi != r.ecode_hi ? q.ecode_hi > r.ecode_hi : q.ecode_lo > r.ecode_lo);
+        if (gt) { r.key = q.key; r.ecode_hi = q.ecode_hi; r.ecode_lo = q.ecode_lo; }
+        r.leaves += q.leaves;
+        r.status |= q.status;
+    }
+    *out = r;
+    return MAPA_OK;
+}
+
+mapa_status mapa_decode_wide(const mapa_topology *t, const mapa_pattern *p, uint32_t busy, int32_t selector,
+                             int32_t sens, uint32_t flags, const mapa_wide_record *record, mapa_decision *out) {
+    if (!t || !p || !record || !out) return fail(MAPA_E_INVALID_ARG, "null argument");
+    return decode_wide(t, p, busy, selector, sens, flags, record, out);
+}
+
 mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selector, int32_t sens,
                           uint32_t flags, void *stream, mapa_decision *out) {
     if (!t || !p || !out) return fail(MAPA_E_INVALID_ARG, "null argument");
     if (selector < 0 || selector > 2) return fail(MAPA_E_INVALID_ARG, "bad selector");
-    if (!key_fits(t, p)) return fail(MAPA_E_UNSUPPORTED, "key budget 15 + W + C(k,2) > 63");
+    const bool deep = (flags & MAPA_F_DEEP) || !key_fits(t, p);
     const uint32_t F = ~t->busy & nmask_of(t->n);
     if (p->k > __builtin_popcount(F)) {
         std::memset(out, 0, sizeof(*out));
@@ -698,15 +972,16 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
     }
     int err;
     if (!t->d_stage) {
-        if ((err = (int)cudaMalloc(&t->d_stage, 64))) return cuda_fail(err, "cudaMalloc");
+        if ((err = (int)cudaMalloc(&t->d_stage, 128))) return cuda_fail(err, "cudaMalloc");
     }
     if (!t->h_stage) {
-        if ((err = (int)cudaMallocHost(&t->h_stage, 64))) return cuda_fail(err, "cudaMallocHost");
+        if ((err = (int)cudaMallocHost(&t->h_stage, 128))) return cuda_fail(err, "cudaMallocHost");
     }
+    // staging: query at 0 (16 B), record at 64 (32 B narrow / 64 B deep)
     mapa_query *hq = (mapa_query *)t->h_stage;
-    mapa_record *hr = (mapa_record *)((char *)t->h_stage + 32);
     mapa_query *dq = (mapa_query *)t->d_stage;
-    mapa_record *dr = (mapa_record *)((char *)t->d_stage + 32);
+    void *hr = (char *)t->h_stage + 64;
+    void *dr = (char *)t->d_stage + 64;
     hq->busy = t->busy;
     hq->pattern = 0;
     hq->selector = selector;
@@ -714,13 +989,21 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
     cudaStream_t st = (cudaStream_t)stream;
     if ((err = (int)cudaMemcpyAsync(dq, hq, sizeof(mapa_query), cudaMemcpyHostToDevice, st)))
         return cuda_fail(err, "H2D query");
-    mapa_status s = mapa_launch_query(t, p, selector, sens, dq, dr, flags, 0, 1, t->busy, stream);
+    mapa_status s;
+    const size_t rbytes = deep ? sizeof(mapa_wide_record) : sizeof(mapa_record);
+    if (deep)
+        s = mapa_launch_query_wide(t, p, selector, sens, dq, (mapa_wide_record *)dr, flags & ~MAPA_F_PRUNE, 0, 1,
+                                   t->busy, stream);
+    else
+        s = mapa_launch_query(t, p, selector, sens, dq, (mapa_record *)dr, flags, 0, 1, t->busy, stream);
     if (s != MAPA_OK) return s;
-    if ((err = (int)cudaMemcpyAsync(hr, dr, sizeof(mapa_record), cudaMemcpyDeviceToHost, st)))
-        return cuda_fail(err, "D2H record");
+    if ((err = (int)cudaMemcpyAsync(hr, dr, rbytes, cudaMemcpyDeviceToHost, st))) return cuda_fail(err, "D2H record");
     if ((err = (int)cudaStreamSynchronize(st))) return cuda_fail(err, "cudaStreamSynchronize");
     mapa_decision d;
-    s = decode_record(t, p, t->busy, selector, sens, flags, hr, &d);
+    if (deep)
+        s = decode_wide(t, p, t->busy, selector, sens, flags, (const mapa_wide_record *)hr, &d);
+    else
+        s = decode_record(t, p, t->busy, selector, sens, flags, (const mapa_record *)hr, &d);
     if (s < 0) return s;
     if (s == MAPA_OK && (flags & MAPA_F_COMMIT)) t->busy |= d.device_mask;
     *out = d;

@@ -19,8 +19,8 @@ import struct
 import torch
 import torch.distributed as dist
 
-from . import (Pattern, Record, Topology, decode, launch_query, allocate_batch, reduce_records, trace_replay,
-               SEL_PRESERVE)
+from . import (Pattern, Record, Topology, WideRecord, decode, decode_wide, launch_query, launch_query_wide,
+               allocate_batch, reduce_records, reduce_wide_records, trace_replay, SEL_PRESERVE)
 
 U32 = 0xFFFFFFFF
 
@@ -86,6 +86,53 @@ def allocate_sharded(topo: Topology, pat: Pattern, selector: int, sensitive: boo
     rec, _q = run_query(topo, pat, selector, sensitive, busy, raw=raw, rank=rank, world=world, prune=prune)
     r = combine_records(rec, group)
     return decode(topo, pat, busy, selector, sensitive, r, raw=raw, prune=prune)
+
+
+def wide_records_from_tensor(t: torch.Tensor):
+    """int64[..., 8] (64 B rows) -> list[WideRecord]."""
+    raw = t.detach().cpu().contiguous().numpy().tobytes()
+    return [WideRecord.from_buffer_copy(raw[i:i + 64]) for i in range(0, len(raw), 64)]
+
+
+def wide_record_tensor(rec: WideRecord, device="cpu"):
+    return torch.tensor(list(struct.unpack("<8q", bytes(rec))), dtype=torch.int64, device=device)
+
+
+def run_query_wide(topo: Topology, pat: Pattern, selector: int, sensitive: bool, busy: int, raw: bool = False,
+                   rank: int = 0, world: int = 1, stream=None):
+    """Deep path: launch one (shard of a) query; returns the 64-B record tensor
+    (int64[8], device) without synchronising."""
+    q = query_tensor(busy, 0, selector, sensitive)
+    rec = torch.empty(8, dtype=torch.int64, device="cuda")
+    launch_query_wide(topo, pat, selector, sensitive, q.data_ptr(), rec.data_ptr(), busy, raw=raw, rank=rank,
+                      world=world, stream=stream)
+    return rec, q
+
+
+def combine_wide_records(rec: torch.Tensor, group=None) -> WideRecord:
+    """all_gather the per-rank 64-B deep records (one collective), combine by
+    the lexicographic max of the 192-bit key and the sum of leaves."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return wide_records_from_tensor(rec)[0]
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((world, 8), dtype=torch.int64, device=rec.device)
+        dist.all_gather_into_tensor(out, rec.reshape(8), group=group)
+    else:
+        parts = [torch.empty(8, dtype=torch.int64) for _ in range(world)]
+        dist.all_gather(parts, rec.reshape(8).cpu(), group=group)
+        out = torch.stack(parts)
+    return reduce_wide_records(wide_records_from_tensor(out))
+
+
+def allocate_sharded_wide(topo: Topology, pat: Pattern, selector: int, sensitive: bool, busy: int,
+                          raw: bool = False, group=None) -> dict:
+    """Deep-path sharded single allocation over the process group."""
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rec, _q = run_query_wide(topo, pat, selector, sensitive, busy, raw=raw, rank=rank, world=world)
+    r = combine_wide_records(rec, group)
+    return decode_wide(topo, pat, busy, selector, sensitive, r, raw=raw)
 
 
 def run_batch(topo: Topology, pats, queries, raw: bool = False, stream=None):

@@ -115,8 +115,52 @@ def test_pattern_errors():
     with pytest.raises(mp.MapaError):
         mp.Pattern(3, [(0, 1), (1, 0)])
     with pytest.raises(mp.MapaError) as e:
-        mp.Pattern(9, [])
+        mp.Pattern(17, [])
     assert e.value.status == mp.E_UNSUPPORTED
+    with pytest.raises(mp.MapaError) as e:
+        mp.Pattern.make("ring", 17)
+    assert e.value.status == mp.E_UNSUPPORTED
+
+
+def _count_automorphisms(k, edges):
+    """|Aut| by exhaustive backtracking over vertex images (every complete
+    adjacency-preserving bijection is counted once; no stabiliser chain)."""
+    adj = [set() for _ in range(k)]
+    for a, b in edges:
+        adj[a].add(b)
+        adj[b].add(a)
+    img = [-1] * k
+
+    def go(v, used):
+        if v == k:
+            return 1
+        tot = 0
+        for c in range(k):
+            if c in used or len(adj[c]) != len(adj[v]):
+                continue
+            if all((w in adj[v]) == (img[w] in adj[c]) for w in range(v)):
+                img[v] = c
+                tot += go(v + 1, used | {c})
+        return tot
+
+    return go(0, frozenset())
+
+
+@pytest.mark.parametrize("shape", ["ring", "tree", "ringtree", "full", "edgeless"])
+def test_deep_patterns_aut_order(shape):
+    """k = 9..16 (deep path): |Aut| from the library's stabiliser chain equals
+    the closed forms (ring 2k, full / edgeless k!) and, for sparse shapes, an
+    exhaustive automorphism count; edges equal SPEC make_pattern's."""
+    for k in range(9, 17):
+        p = mp.Pattern.make(shape, k).info()
+        kk, e = mo.make_pattern(shape, k)
+        assert p["k"] == kk and p["edges"] == e
+        if shape == "ring":
+            assert p["aut"] == 2 * k
+        elif shape in ("full", "edgeless"):
+            assert p["aut"] == math.factorial(k)
+        else:
+            assert p["aut"] == _count_automorphisms(k, e)
 
 
 def _lex_leader_ok(f, lex_src):
