@@ -520,8 +520,13 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     const int occ = max_blocks_per_sm_deep(L, pl->sc, base == SEL_SENS ? 2 * tb->xsd * tb->xsd : 0);
     const uint64_t warps = (uint64_t)sm * occ * 8;
     const uint64_t target = 8ull * warps * (uint64_t)world;
+    // RAW items are uniform: stop at ~8 per warp.  Canonical items are not
+    // (the lex-leader bounds make prefixes with small devices first far
+    // heavier, and they are contiguous in item order), so go as deep as the
+    // 2^26-item budget allows: the heaviest item is then a small fraction of
+    // a warp's share and guided self-scheduling balances the rest.
     int d = 0;
-    while (d < std::min(T, 6) && perm_count(nF, d) < target && perm_count(nF, d + 1) < (1ull << 27)) ++d;
+    while (d < std::min(T, 6) && (canon || perm_count(nF, d) < target) && perm_count(nF, d + 1) < (1ull << 26)) ++d;
     pl->depth = d;
     pl->items = perm_count(nF, d);
     const uint64_t stripe = world == 1 ? std::max<uint64_t>(1, pl->items)
