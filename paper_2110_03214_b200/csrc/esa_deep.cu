@@ -155,8 +155,15 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, uint32_t F, uint32_
     constexpr bool canon = (SEL & 4) != 0;
     DeepShared &S = dsh();
     DeepWarp &W = S.w[warp];
-    const uint32_t R = F & ~U;
-    const int r = tb.r;
+    uint32_t R = F & ~U;
+    if constexpr (canon) {
+        // lower bound shared by every suffix vertex: drop the devices below it
+        if (tb.pcommon) {
+            const int lb = __reduce_max_sync(kFullD, (lane < T && ((tb.pcommon >> lane) & 1)) ? (int)myf : -1);
+            R &= 0xFFFFFFFEu << lb;
+        }
+    }
+    const int r = __popc(R);
     __syncwarp();  // previous readers of dl / pt / wt are done
     if ((R >> lane) & 1u) W.dl[__popc(R & ((1u << lane) - 1u))] = lane;
     uint32_t X[L];
@@ -171,7 +178,8 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, uint32_t F, uint32_
         }
         if constexpr (canon) {
             if (tb.pcon) {
-                const int lb = __reduce_max_sync(kFullD, (lane < T && ((tb.src[u] >> lane) & 1u)) ? (int)myf : -1);
+                const int lb = __reduce_max_sync(
+                    kFullD, (lane < T && ((tb.src[u] & ~tb.pcommon) >> lane) & 1u) ? (int)myf : -1);
                 const uint32_t mi = lb < 0 ? 0u : (uint32_t)__popc(R & ((2u << lb) - 1u));
                 MINI |= (4u * mi) << (8 * l);
             }
@@ -195,16 +203,27 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, uint32_t F, uint32_
             W.pt[l][lane] = v;
         }
     }
+    // Eq. 3 with L >= 2: the score depends on the set only and pt[l][i] = q[i]
+    // for every l, so sum_l q[i_l] = 1/(L-1) sum_{a<b} (q[i_a] + q[i_b]) and
+    // (L-1) s = (L-1) A + sum over the C(L,2) pairs of
+    //   wq[i][i2] = (L-1) w(i, i2) + q[i] + q[i2]
+    // (C(L,2) reads per leaf instead of L + C(L,2); the scan compares (L-1) s).
+    constexpr bool fold = base == SEL_INSENS && L >= 2;
     if constexpr (L >= 2) {
         if (tb.nes) {
+            __syncwarp();  // pt written
             for (int p = lane; p < r * 16; p += 32) {
                 const int i = p >> 4, i2 = p & 15;
-                if (i2 < r) W.wt[p] = S.tw[W.dl[i] * 32 + W.dl[i2]];
+                if (i2 < r) {
+                    int v = S.tw[W.dl[i] * 32 + W.dl[i2]];
+                    if constexpr (fold) v = (L - 1) * v + W.pt[0][i] + W.pt[0][i2];
+                    W.wt[p] = v;
+                }
             }
         }
     }
     __syncwarp();
-    const int nt = tb.ntup;
+    const int nt = tb.tcount[r];
     const int nes = tb.nes;
     const char *ptb = reinterpret_cast<const char *>(&W.pt[0][0]);
     const char *wtb = reinterpret_cast<const char *>(W.wt);
@@ -215,9 +234,12 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, uint32_t F, uint32_
         if constexpr (canon) {
             if (tb.pcon) valid = valid && ((((w | 0x80808080u) - MINI) & 0x80808080u) == 0x80808080u);
         }
-        int s = A;
+        int s = fold ? (L - 1) * A : A;
+        if constexpr (!fold) {
 #pragma unroll
-        for (int l = 0; l < L; ++l) s += *reinterpret_cast<const int *>(ptb + 128 * l + ((w >> (8 * l)) & 0xFFu));
+            for (int l = 0; l < L; ++l)
+                if ((tb.ptmask >> l) & 1) s += *reinterpret_cast<const int *>(ptb + 128 * l + ((w >> (8 * l)) & 0xFFu));
+        }
         if constexpr (L >= 2 && base != SEL_BASE) {
 #pragma unroll
             for (int e = 0; e < (L * (L - 1)) / 2; ++e) {
@@ -234,8 +256,9 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, uint32_t F, uint32_
         } else {
             cnt += (unsigned long long)min(32, nt - t0);
         }
-        if (valid && ((unsigned long long)(uint32_t)s << 32) >= (bst.hi & 0xFFFFFFFF00000000ull))
-            consider_deep<L>(tb, W, bst, (uint32_t)s, U, w, T);
+        const int bs = (int)(bst.hi >> 32);
+        if (valid && s >= (fold ? (L - 1) * bs : bs))
+            consider_deep<L>(tb, W, bst, fold ? (uint32_t)(s / (L - 1)) : (uint32_t)s, U, w, T);
     }
 }
 
@@ -313,10 +336,14 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
         for (uint32_t j = start; j < end; ++j) {
             const uint32_t sl = j / Ls;
             uint32_t item = (sl * (uint32_t)world + (uint32_t)rank) * Ls + (j - sl * Ls);
-            // decode the prefix of depth D (mixed radix nF - j at level j)
+            // decode the prefix of depth D (mixed radix nF - q at level q).
+            // Level 0 is the LEAST significant digit: under lex-leader bounds
+            // the prefixes with a small f(0) are far heavier, and this order
+            // interleaves them with light ones so that every chunk of
+            // consecutive items carries about the average work.
             uint32_t dg[kMaxDecodeD];
 #pragma unroll
-            for (int q = kMaxDecodeD - 1; q >= 0; --q) {
+            for (int q = 0; q < kMaxDecodeD; ++q) {
                 if (q < D) {
                     const uint32_t rr = (uint32_t)(nF - q);
                     const uint32_t qq = __umulhi(item, S.magic[rr]);

@@ -96,6 +96,9 @@ struct DeepTables {
     int32_t nes;             // scored suffix-internal pairs (Eq. 1/2: pattern edges; Eq. 3: all pairs)
     int32_t pcon;            // canonical: some suffix vertex has a lex-leader source in the prefix
     int32_t eb;              // C(k,2)
+    int32_t ptmask;          // bit l: suffix vertex T+l has a scored prefix neighbour (reads pt[l])
+    int32_t pcommon;         // canonical: prefix vertices that are lex-leader sources of EVERY suffix vertex
+    int32_t tcount[33];      // tcount[r']: tuples whose indices are all < r' (the table is sorted by max index)
     uint8_t es[8][2];        // suffix-internal pairs (l_a, l_b), l_a < l_b
     uint16_t back[kMaxKDeep];  // back[u] bit j: pattern edge (j, u), j < u
     uint16_t src[kMaxKDeep];   // src[u] bit j: canonical f(j) < f(u) (0 in RAW mode)

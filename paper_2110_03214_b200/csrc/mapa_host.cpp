@@ -464,6 +464,17 @@ int build_tuples(const mapa_pattern *p, int L, int r, bool canon, uint32_t *out,
         if (out) out[n] = w;
         ++n;
     }
+    if (out) {
+        // order by the largest index, so that the tuples using only the first
+        // r' devices form a prefix of the table (a node whose common lower
+        // bound leaves r' devices scans tcount[r'] entries)
+        auto mx = [L](uint32_t w) {
+            uint32_t m = 0;
+            for (int l = 0; l < L; ++l) m = std::max(m, (w >> (8 * l)) & 0xFFu);
+            return m;
+        };
+        std::stable_sort(out, out + n, [&](uint32_t a, uint32_t b) { return mx(a) < mx(b); });
+    }
     return n;
 }
 
@@ -509,10 +520,29 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     tb->r = r;
     tb->ntup = build_tuples(p, L, r, canon, tb->tup, kMaxTup);
     tb->nes = suffix_pairs(p, L, base, tb->es);
+    tb->ptmask = 0;
+    for (int l = 0; l < L; ++l)
+        if (base == SEL_INSENS || (base != SEL_BASE && (p->back[T + l] & ((1u << T) - 1u)))) tb->ptmask |= 1 << l;
+    // prefix sources common to every suffix vertex: their max is a lower bound
+    // for the whole suffix, applied by compacting the node's device list; the
+    // remaining per-vertex bounds are checked per tuple (pcon)
+    const uint32_t pmask = (1u << T) - 1u;
+    uint32_t common = canon ? pmask : 0u;
+    for (int l = 0; l < L; ++l) common &= p->src[T + l];
+    tb->pcommon = (int32_t)common;
     tb->pcon = 0;
     if (canon)
         for (int l = 0; l < L; ++l)
-            if (p->src[T + l] & ((1u << T) - 1u)) tb->pcon = 1;
+            if (p->src[T + l] & pmask & ~common) tb->pcon = 1;
+    for (int rr = 0; rr <= 32; ++rr) {
+        int c = 0;
+        for (int i = 0; i < tb->ntup; ++i) {
+            uint32_t m = 0;
+            for (int l = 0; l < L; ++l) m = std::max(m, (tb->tup[i] >> (8 * l)) & 0xFFu);
+            if ((int)(m / 4) < rr) ++c;
+        }
+        tb->tcount[rr] = c;
+    }
     pl->sc = base | (canon ? 4 : 0);
     // decoded prefix depth: enough items for ~8 per resident warp (x world)
     int sm = device_sm_count();

@@ -12,8 +12,9 @@ import workloads as W  # noqa: E402
 
 cases = [("cubemesh16", "ring", 9, False), ("cubemesh16", "ring", 12, False), ("cubemesh16", "ring", 12, True),
          ("cubemesh16", "tree", 12, False), ("cubemesh16", "ring", 14, False), ("cubemesh16", "ring", 16, False),
-         ("cubemesh16", "full", 6, True), ("het32", "full", 6, True), ("het32", "ring", 8, False),
-         ("cubemesh16", "ring", 8, True)]
+         ("het32", "full", 6, True), ("het32", "ring", 8, False), ("cubemesh16", "ring", 8, True)]
+if len(sys.argv) > 1:
+    cases = [cases[int(i)] for i in sys.argv[1].split(",")]
 for topo, shape, k, raw in cases:
     t = mp.Topology(text=W.het32_text()) if topo == "het32" else mp.Topology(topo)
     n = t.n
