@@ -41,20 +41,23 @@ constexpr unsigned kFullD = 0xFFFFFFFFu;
 constexpr int kBlockD = 256;
 constexpr int kWarpsD = kBlockD / 32;
 constexpr int kMaxDecodeD = 6;
+constexpr int kMaxL = 4;
+// per-warp term area (ints): pt[l][i] at l*32 + i, the pair table at
+// kWtOff + i*kWtStride + i2 (odd stride: fewer bank conflicts), a zero at kZeroOff
+constexpr int kWtOff = 128, kWtStride = 17, kZeroOff = 400, kAreaInts = 404;
 
 struct DeepWarp {
-    int pt[4][32];   // pt[l][i]: partial of suffix vertex T+l on remaining device i
-    int wt[16 * 16]; // wt[i*16 + i2]: pair value of remaining devices i, i2 (L >= 2: r <= 16)
+    int area[kAreaInts];
     int dl[32];      // remaining free devices, ascending
-    int fw[16];      // f(j) of the placed prefix (read by the out-of-line key builder)
+    int fw[16];      // f(j) of the placed prefix (read by the key builder)
 };
 
 struct DeepShared {
+    uint4 tup[kMaxTup];     // x: byte l = 4 i_l; y, z, w: 16-bit byte offsets of the NT terms into area
     uint4 cm[kMaxN];
     int tw[kMaxN * kMaxN];  // [v*32 + b] pair value: w(v,b) (Eq. 1/3), census delta (Eq. 2), 0 if v == b
     int incF[kMaxN];        // inc_F(v) (Eq. 3)
     uint32_t magic[kMaxN + 4];
-    uint32_t tup[kMaxTup];
     DeepWarp w[kWarpsD];
     unsigned long long rk[kWarpsD][4];
 };
@@ -86,20 +89,18 @@ __device__ __forceinline__ uint32_t nth_set_d(uint32_t m, uint32_t n) {
     return pos;
 }
 
-// Out-of-line: a leaf whose score reached the lane's best.  Builds the device
+// A leaf whose (scaled) score reached the lane's threshold.  Builds the device
 // set, and (unless the set alone decides) the 128-bit edge code: pattern edge
 // (a, b) -> ranks ra, rb of f(a), f(b) inside S -> pair index p of (lo, hi)
-// in lex order over C(k,2) -> bit C(k,2)-1-p.
-template <int L>
-__device__ __noinline__ void consider_deep(const DeepTables &tb, const DeepWarp &W, DBest &b, uint32_t s,
-                                           uint32_t U, uint32_t w, int T) {
-    uint32_t sdev[4];
+// in lex order over C(k,2) -> bit C(k,2)-1-p.  Updates the lane's best key
+// and threshold.
+__device__ __forceinline__ void consider_deep(const DeepTables &tb, const DeepWarp &W, DBest &b, int &thr,
+                                              uint32_t s, uint32_t U, uint32_t x, int T) {
+    const int L = tb.L;
     uint32_t S = U;
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
-        sdev[l] = (uint32_t)W.dl[((w >> (8 * l)) & 0xFFu) >> 2];
-        S |= 1u << sdev[l];
-    }
+    for (int l = 0; l < kMaxL; ++l)
+        if (l < L) S |= 1u << (uint32_t)W.dl[((x >> (8 * l)) & 0xFFu) >> 2];
     const unsigned long long hi = ((unsigned long long)s << 32) | __brev(S);
     if (hi < b.hi) return;
     if (hi == b.hi && tb.clique) return;  // same set of a clique: same edges
@@ -107,8 +108,8 @@ __device__ __noinline__ void consider_deep(const DeepTables &tb, const DeepWarp 
     unsigned long long ehi = 0, elo = 0;
     for (int e = 0; e < tb.m; ++e) {
         const int a = tb.edge[e] & 15, c = tb.edge[e] >> 4;
-        const uint32_t da = a < T ? (uint32_t)W.fw[a] : sdev[a - T];
-        const uint32_t dc = c < T ? (uint32_t)W.fw[c] : sdev[c - T];
+        const uint32_t da = a < T ? (uint32_t)W.fw[a] : (uint32_t)W.dl[((x >> (8 * (a - T))) & 0xFFu) >> 2];
+        const uint32_t dc = c < T ? (uint32_t)W.fw[c] : (uint32_t)W.dl[((x >> (8 * (c - T))) & 0xFFu) >> 2];
         const int ra = __popc(S & ((1u << da) - 1u)), rc = __popc(S & ((1u << dc) - 1u));
         const int lo = min(ra, rc), hi2 = max(ra, rc);
         const int p = lo * (2 * k - lo - 1) / 2 + (hi2 - lo - 1);
@@ -120,6 +121,7 @@ __device__ __noinline__ void consider_deep(const DeepTables &tb, const DeepWarp 
         b.hi = hi;
         b.ehi = ehi;
         b.elo = elo;
+        thr = (int)s * tb.scale;
     }
 }
 
@@ -148,13 +150,14 @@ __device__ __forceinline__ uint32_t allowed(const DeepTables &tb, int d, uint32_
 }
 
 // All leaves below a node whose prefix 0..T-1 is placed (set U, score A).
-template <int L, int SEL>
+template <int NT, int SEL>
 __device__ __forceinline__ void suffix(const DeepTables &tb, uint32_t F, uint32_t U, int A, uint32_t myf, int lane,
-                                       int warp, int T, DBest &bst, unsigned long long &cnt) {
+                                       int warp, int T, DBest &bst, int &thr, unsigned long long &cnt) {
     constexpr int base = SEL & 3;
     constexpr bool canon = (SEL & 4) != 0;
     DeepShared &S = dsh();
     DeepWarp &W = S.w[warp];
+    const int L = tb.L;
     uint32_t R = F & ~U;
     if constexpr (canon) {
         // lower bound shared by every suffix vertex: drop the devices below it
@@ -164,24 +167,27 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, uint32_t F, uint32_
         }
     }
     const int r = __popc(R);
-    __syncwarp();  // previous readers of dl / pt / wt are done
+    __syncwarp();  // previous readers of dl / area are done
     if ((R >> lane) & 1u) W.dl[__popc(R & ((1u << lane) - 1u))] = lane;
-    uint32_t X[L];
+    uint32_t X[kMaxL];
     uint32_t MINI = 0;
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
-        const int u = T + l;
-        if constexpr (base == SEL_INSENS) {
-            X[l] = U;
-        } else {
-            X[l] = __reduce_or_sync(kFullD, (lane < T && ((tb.back[u] >> lane) & 1u)) ? (1u << myf) : 0u);
-        }
-        if constexpr (canon) {
-            if (tb.pcon) {
-                const int lb = __reduce_max_sync(
-                    kFullD, (lane < T && ((tb.src[u] & ~tb.pcommon) >> lane) & 1u) ? (int)myf : -1);
-                const uint32_t mi = lb < 0 ? 0u : (uint32_t)__popc(R & ((2u << lb) - 1u));
-                MINI |= (4u * mi) << (8 * l);
+    for (int l = 0; l < kMaxL; ++l) {
+        X[l] = 0;
+        if (l < L) {
+            const int u = T + l;
+            if constexpr (base == SEL_INSENS) {
+                X[l] = U;
+            } else {
+                X[l] = __reduce_or_sync(kFullD, (lane < T && ((tb.back[u] >> lane) & 1u)) ? (1u << myf) : 0u);
+            }
+            if constexpr (canon) {
+                if (tb.pcon) {
+                    const int lb = __reduce_max_sync(
+                        kFullD, (lane < T && ((tb.src[u] & ~tb.pcommon) >> lane) & 1u) ? (int)myf : -1);
+                    const uint32_t mi = lb < 0 ? 0u : (uint32_t)__popc(R & ((2u << lb) - 1u));
+                    MINI |= (4u * mi) << (8 * l);
+                }
             }
         }
     }
@@ -190,76 +196,68 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, uint32_t F, uint32_
         const int dev = W.dl[lane];
         const uint4 c = S.cm[dev];
 #pragma unroll
-        for (int l = 0; l < L; ++l) {
-            int v;
-            if constexpr (base == SEL_SENS) {
-                v = __popc(c.x & X[l]) * tb.xsd + __popc((c.y | c.z) & X[l]);
-            } else if constexpr (base == SEL_BASE) {
-                v = 0;
-            } else {
-                v = 12 * __popc(X[l]) + 38 * __popc(c.x & X[l]) + 13 * __popc(c.y & X[l]) + 8 * __popc(c.z & X[l]);
-                if constexpr (base == SEL_INSENS) v -= S.incF[dev];
+        for (int l = 0; l < kMaxL; ++l) {
+            if (l < L) {
+                int v;
+                if constexpr (base == SEL_SENS) {
+                    v = __popc(c.x & X[l]) * tb.xsd + __popc((c.y | c.z) & X[l]);
+                } else if constexpr (base == SEL_BASE) {
+                    v = 0;
+                } else {
+                    v = 12 * __popc(X[l]) + 38 * __popc(c.x & X[l]) + 13 * __popc(c.y & X[l]) +
+                        8 * __popc(c.z & X[l]);
+                    if constexpr (base == SEL_INSENS) v -= S.incF[dev];
+                }
+                W.area[32 * l + lane] = v;
             }
-            W.pt[l][lane] = v;
         }
     }
-    // Eq. 3 with L >= 2: the score depends on the set only and pt[l][i] = q[i]
-    // for every l, so sum_l q[i_l] = 1/(L-1) sum_{a<b} (q[i_a] + q[i_b]) and
-    // (L-1) s = (L-1) A + sum over the C(L,2) pairs of
-    //   wq[i][i2] = (L-1) w(i, i2) + q[i] + q[i2]
-    // (C(L,2) reads per leaf instead of L + C(L,2); the scan compares (L-1) s).
-    constexpr bool fold = base == SEL_INSENS && L >= 2;
-    if constexpr (L >= 2) {
-        if (tb.nes) {
-            __syncwarp();  // pt written
-            for (int p = lane; p < r * 16; p += 32) {
-                const int i = p >> 4, i2 = p & 15;
-                if (i2 < r) {
-                    int v = S.tw[W.dl[i] * 32 + W.dl[i2]];
-                    if constexpr (fold) v = (L - 1) * v + W.pt[0][i] + W.pt[0][i2];
-                    W.wt[p] = v;
-                }
+    // Pair table.  Eq. 3 with L >= 2 (scale = L-1): the score depends on the
+    // set only and pt[l][i] = q[i] for every l, so
+    //   (L-1) s = (L-1) A + sum over the C(L,2) pairs of (L-1) w(i, i2) + q[i] + q[i2]
+    // and the tuple terms are the pairs alone.
+    if (tb.nes) {
+        __syncwarp();  // pt written
+        const int sc = tb.scale;
+        const bool fold = base == SEL_INSENS && L >= 2;
+        for (int p = lane; p < r * 16; p += 32) {
+            const int i = p >> 4, i2 = p & 15;
+            if (i2 < r) {
+                int v = S.tw[W.dl[i] * 32 + W.dl[i2]];
+                if (fold) v = sc * v + W.area[i] + W.area[i2];
+                W.area[kWtOff + i * kWtStride + i2] = v;
             }
         }
     }
     __syncwarp();
     const int nt = tb.tcount[r];
-    const int nes = tb.nes;
-    const char *ptb = reinterpret_cast<const char *>(&W.pt[0][0]);
-    const char *wtb = reinterpret_cast<const char *>(W.wt);
+    const char *ab = reinterpret_cast<const char *>(W.area);
+    const int A0 = A * tb.scale;
     for (int t0 = 0; t0 < nt; t0 += 32) {
         const int t = t0 + lane;
         bool valid = t < nt;
-        const uint32_t w = valid ? S.tup[t] : 0u;
+        const uint4 e = S.tup[valid ? t : 0];
         if constexpr (canon) {
-            if (tb.pcon) valid = valid && ((((w | 0x80808080u) - MINI) & 0x80808080u) == 0x80808080u);
+            if (tb.pcon) valid = valid && ((((e.x | 0x80808080u) - MINI) & 0x80808080u) == 0x80808080u);
         }
-        int s = fold ? (L - 1) * A : A;
-        if constexpr (!fold) {
+        int s = A0;
 #pragma unroll
-            for (int l = 0; l < L; ++l)
-                if ((tb.ptmask >> l) & 1) s += *reinterpret_cast<const int *>(ptb + 128 * l + ((w >> (8 * l)) & 0xFFu));
-        }
-        if constexpr (L >= 2 && base != SEL_BASE) {
-#pragma unroll
-            for (int e = 0; e < (L * (L - 1)) / 2; ++e) {
-                if (e < nes) {
-                    const uint32_t oa = (w >> (8 * tb.es[e][0])) & 0xFFu, ob = (w >> (8 * tb.es[e][1])) & 0xFFu;
-                    s += *reinterpret_cast<const int *>(wtb + 16 * oa + ob);
-                }
-            }
+        for (int q = 0; q < NT; ++q) {
+            const uint32_t wd = q < 2 ? e.y : (q < 4 ? e.z : e.w);
+            const uint32_t off = (q & 1) ? (wd >> 16) : (wd & 0xFFFFu);
+            s += *reinterpret_cast<const int *>(ab + off);
         }
         if constexpr (base == SEL_SENS) s = dlut()[s];
         if constexpr (canon) {
             if (tb.pcon) cnt += (unsigned long long)__popc(__ballot_sync(kFullD, valid));
-            else cnt += (unsigned long long)min(32, nt - t0);
-        } else {
-            cnt += (unsigned long long)min(32, nt - t0);
         }
-        const int bs = (int)(bst.hi >> 32);
-        if (valid && s >= (fold ? (L - 1) * bs : bs))
-            consider_deep<L>(tb, W, bst, fold ? (uint32_t)(s / (L - 1)) : (uint32_t)s, U, w, T);
+        if (valid && s >= thr) {
+            const int sc = tb.scale;
+            const uint32_t sr = sc == 1 ? (uint32_t)s : (sc == 2 ? (uint32_t)s >> 1 : (uint32_t)s / 3u);
+            consider_deep(tb, W, bst, thr, sr, U, e.x, T);
+        }
     }
+    if (!canon || !tb.pcon) cnt += (unsigned long long)nt;
 }
 
 __device__ __forceinline__ uint32_t perm_count_d(int n, int d) {
@@ -268,8 +266,8 @@ __device__ __forceinline__ uint32_t perm_count_d(int n, int d) {
     return p;
 }
 
-template <int L, int SEL>
-__global__ void __launch_bounds__(kBlockD, 2)
+template <int NT, int SEL>
+__global__ void __launch_bounds__(kBlockD, 3)
 esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut_g, const mapa_query *__restrict__ dq,
          mapa_wide_record *__restrict__ rec, int D, int rank, int world, int stripe) {
     constexpr int base = SEL & 3;
@@ -283,6 +281,7 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
     const int T = tb.T;
     if (tid < kMaxN) S.cm[tid] = make_uint4(tb.cm[tid][0], tb.cm[tid][1], tb.cm[tid][2], tb.cm[tid][3]);
     if (tid <= kMaxN) S.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
+    if (lane == 0) S.w[warp].area[kZeroOff] = 0;
     for (int i = tid; i < kMaxN * kMaxN; i += kBlockD) {
         const int v = i >> 5, b = i & 31;
         int val = 0;
@@ -293,7 +292,19 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
         }
         S.tw[i] = val;
     }
-    for (int i = tid; i < tb.ntup; i += kBlockD) S.tup[i] = tb.tup[i];
+    // tuple entries: the term offsets of every tuple (pt[a][i_a] or the pair (i_a, i_b))
+    for (int i = tid; i < tb.ntup; i += kBlockD) {
+        const uint32_t x = tb.tup[i];
+        uint32_t wd[3] = {kZeroOff * 4u * 0x10001u, kZeroOff * 4u * 0x10001u, kZeroOff * 4u * 0x10001u};
+        for (int q = 0; q < tb.nterm; ++q) {
+            const int a = tb.term[q][1], b = tb.term[q][2];
+            const uint32_t ia = ((x >> (8 * a)) & 0xFFu) >> 2, ib = ((x >> (8 * b)) & 0xFFu) >> 2;
+            const uint32_t off = 4u * (tb.term[q][0] == 0 ? (uint32_t)(32 * a) + ia : kWtOff + ia * kWtStride + ib);
+            const int sh = 16 * (q & 1);
+            wd[q >> 1] = (wd[q >> 1] & ~(0xFFFFu << sh)) | (off << sh);
+        }
+        S.tup[i] = make_uint4(x, wd[0], wd[1], wd[2]);
+    }
     if constexpr (base == SEL_SENS)
         for (int i = tid; i < tb.xsd * tb.xsd; i += kBlockD) dlut()[i] = lut_g[i];
     if (tid < kMaxN) {
@@ -318,6 +329,7 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
     const uint32_t Nloc = myS == 0 ? 0u : (ownLast ? (myS - 1u) * Ls + (N - (nS - 1u) * Ls) : myS * Ls);
     const uint32_t P = gridDim.x * (uint32_t)kWarpsD;
     DBest bst{0ull, 0ull, 0ull};
+    int thr = 0;
     unsigned long long cnt = 0;
     uint32_t myf = 0, mycand = 0;
     int myacc = 0;
@@ -369,7 +381,7 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
             }
             if (!ok) continue;
             if (D == T) {
-                suffix<L, SEL>(tb, F, U, acc, myf, lane, warp, T, bst, cnt);
+                suffix<NT, SEL>(tb, F, U, acc, myf, lane, warp, T, bst, thr, cnt);
                 continue;
             }
             // explicit-stack DFS over levels D..T-1 (lane d holds level d)
@@ -392,7 +404,7 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
                 if (lane == 0) S.w[warp].fw[d] = (int)v;
                 U |= 1u << v;
                 if (d + 1 == T) {
-                    suffix<L, SEL>(tb, F, U, a, myf, lane, warp, T, bst, cnt);
+                    suffix<NT, SEL>(tb, F, U, a, myf, lane, warp, T, bst, thr, cnt);
                     U &= ~(1u << v);
                 } else {
                     ++d;
@@ -441,81 +453,81 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
     }
 }
 
-template <int L, int SEL>
+template <int NT, int SEL>
 int launch_t(const DeepTables &tb, const uint16_t *lut, const mapa_query *dq, mapa_wide_record *rec, int D, int rank,
              int world, int stripe, int grid, int smem, cudaStream_t st) {
     // the attribute is always the fixed upper bound, so occupancy queries and
     // launches agree
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute((const void *)esa_deep<L, SEL>,
+        cudaError_t e = cudaFuncSetAttribute((const void *)esa_deep<NT, SEL>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmemMax);
         if (e != cudaSuccess) return (int)e;
         configured = true;
     }
     if (smem > kDeepSmemMax) return (int)cudaErrorInvalidValue;
-    esa_deep<L, SEL><<<grid, kBlockD, smem, st>>>(tb, lut, dq, rec, D, rank, world, stripe);
+    esa_deep<NT, SEL><<<grid, kBlockD, smem, st>>>(tb, lut, dq, rec, D, rank, world, stripe);
     return (int)cudaGetLastError();
 }
 
-template <int L, int SEL>
-const void *fn_t() { return (const void *)esa_deep<L, SEL>; }
+template <int NT, int SEL>
+const void *fn_t() { return (const void *)esa_deep<NT, SEL>; }
 
 using DeepFn = int (*)(const DeepTables &, const uint16_t *, const mapa_query *, mapa_wide_record *, int, int, int,
                        int, int, int, cudaStream_t);
 
-template <int L>
+template <int NT>
 DeepFn pick_sel(int sc) {
     switch (sc & 7) {
-        case 0: return launch_t<L, 0>;
-        case 1: return launch_t<L, 1>;
-        case 2: return launch_t<L, 2>;
-        case 3: return launch_t<L, 3>;
-        case 4: return launch_t<L, 4>;
-        case 5: return launch_t<L, 5>;
-        case 6: return launch_t<L, 6>;
-        default: return launch_t<L, 7>;
+        case 0: return launch_t<NT, 0>;
+        case 1: return launch_t<NT, 1>;
+        case 2: return launch_t<NT, 2>;
+        case 3: return launch_t<NT, 3>;
+        case 4: return launch_t<NT, 4>;
+        case 5: return launch_t<NT, 5>;
+        case 6: return launch_t<NT, 6>;
+        default: return launch_t<NT, 7>;
     }
 }
 
-template <int L>
+template <int NT>
 const void *pick_fn_sel(int sc) {
     switch (sc & 7) {
-        case 0: return fn_t<L, 0>();
-        case 1: return fn_t<L, 1>();
-        case 2: return fn_t<L, 2>();
-        case 3: return fn_t<L, 3>();
-        case 4: return fn_t<L, 4>();
-        case 5: return fn_t<L, 5>();
-        case 6: return fn_t<L, 6>();
-        default: return fn_t<L, 7>();
+        case 0: return fn_t<NT, 0>();
+        case 1: return fn_t<NT, 1>();
+        case 2: return fn_t<NT, 2>();
+        case 3: return fn_t<NT, 3>();
+        case 4: return fn_t<NT, 4>();
+        case 5: return fn_t<NT, 5>();
+        case 6: return fn_t<NT, 6>();
+        default: return fn_t<NT, 7>();
     }
 }
+
+// compile-time term count: the smallest of {2, 4, 6} >= nterm (padding terms read a zero)
+inline int nt_class(int nterm) { return nterm <= 2 ? 2 : (nterm <= 4 ? 4 : 6); }
 
 }  // namespace
 
 int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_query *d_query,
                 mapa_wide_record *d_record, int depth, int rank, int world, int stripe, int grid, void *stream) {
     const int smem = (int)sizeof(DeepShared) + ((sc & 3) == SEL_SENS ? 2 * tb.xsd * tb.xsd : 0);
+    if (tb.nterm > kDeepMaxTerms || tb.L < 1 || tb.L > kMaxL) return (int)cudaErrorInvalidValue;
     DeepFn f = nullptr;
-    switch (tb.L) {
-        case 1: f = pick_sel<1>(sc); break;
+    switch (nt_class(tb.nterm)) {
         case 2: f = pick_sel<2>(sc); break;
-        case 3: f = pick_sel<3>(sc); break;
         case 4: f = pick_sel<4>(sc); break;
-        default: return (int)cudaErrorInvalidValue;
+        default: f = pick_sel<6>(sc); break;
     }
     return f(tb, d_lut, d_query, d_record, depth, rank, world, stripe, grid, smem, (cudaStream_t)stream);
 }
 
-int max_blocks_per_sm_deep(int L, int sc, int lut_bytes) {
+int max_blocks_per_sm_deep(int nterm, int sc, int lut_bytes) {
     const void *f = nullptr;
-    switch (L) {
-        case 1: f = pick_fn_sel<1>(sc); break;
+    switch (nt_class(nterm)) {
         case 2: f = pick_fn_sel<2>(sc); break;
-        case 3: f = pick_fn_sel<3>(sc); break;
         case 4: f = pick_fn_sel<4>(sc); break;
-        default: return 1;
+        default: f = pick_fn_sel<6>(sc); break;
     }
     const int smem = (int)sizeof(DeepShared) + lut_bytes;
     if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmemMax) != cudaSuccess) return 1;

@@ -84,8 +84,11 @@ struct LaunchCfg {
 
 // Deep path (k <= 16): a warp-uniform DFS places vertices 0..T-1 (T = k - L),
 // then the lanes scan a table of L-tuples of indices into the r remaining free
-// devices (sorted), one tuple per lane.  Tuple entry: byte l = 4 * i_l
-// (a byte offset into the per-node partial table of suffix vertex T+l).
+// devices (sorted), one tuple per lane.  Tuple word: byte l = 4 * i_l.  The
+// score of a tuple is A + the sum of NT "terms", each one read of the warp's
+// per-node table: a partial pt[l][i_l] (suffix vertex T+l against the placed
+// prefix) or a pair value wt[i_a][i_b] (a scored suffix-internal pair).
+constexpr int kDeepMaxTerms = 6;
 struct DeepTables {
     uint32_t cm[kMaxN][4];   // class masks, as DevTopo
     int32_t n;
@@ -93,13 +96,15 @@ struct DeepTables {
     int32_t ntup;            // valid tuples (suffix-internal lex-leader constraints applied)
     int32_t xsd;             // census index stride m+1 (Eq. 2 table [x*(m+1) + y])
     int32_t clique;
-    int32_t nes;             // scored suffix-internal pairs (Eq. 1/2: pattern edges; Eq. 3: all pairs)
-    int32_t pcon;            // canonical: some suffix vertex has a lex-leader source in the prefix
+    int32_t nes;             // suffix-internal scored pairs (the pair table is built iff > 0)
+    int32_t pcon;            // canonical: per-vertex prefix lower bounds beyond pcommon exist
     int32_t eb;              // C(k,2)
-    int32_t ptmask;          // bit l: suffix vertex T+l has a scored prefix neighbour (reads pt[l])
     int32_t pcommon;         // canonical: prefix vertices that are lex-leader sources of EVERY suffix vertex
+    int32_t scale;           // the scan compares scale * score (Eq. 3 pair folding: L-1, else 1)
+    int32_t nterm;           // terms per tuple (<= kDeepMaxTerms)
+    uint8_t term[kDeepMaxTerms][3];  // (kind 0: pt of suffix vertex a | kind 1: pair (a, b))
+    uint8_t pad0[2];
     int32_t tcount[33];      // tcount[r']: tuples whose indices are all < r' (the table is sorted by max index)
-    uint8_t es[8][2];        // suffix-internal pairs (l_a, l_b), l_a < l_b
     uint16_t back[kMaxKDeep];  // back[u] bit j: pattern edge (j, u), j < u
     uint16_t src[kMaxKDeep];   // src[u] bit j: canonical f(j) < f(u) (0 in RAW mode)
     uint8_t edge[kMaxEdges];   // pattern edges a | b << 4
@@ -117,7 +122,7 @@ int launch_trace(const MultiTables &tb, int canon, int ntraces, int nops, const 
 // deep path (esa_deep.cu); sc = sel_code | 4 * canonical
 int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_query *d_query,
                 mapa_wide_record *d_record, int depth, int rank, int world, int stripe, int grid, void *stream);
-int max_blocks_per_sm_deep(int L, int sc, int lut_bytes);
+int max_blocks_per_sm_deep(int nt, int sc, int lut_bytes);
 int device_sm_count();
 int max_blocks_per_sm_single(int width, int k, int sc, int xs);
 int max_blocks_per_sm_batch(int width, int canon, int npats, int xs);

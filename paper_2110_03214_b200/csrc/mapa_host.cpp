@@ -440,6 +440,27 @@ int suffix_pairs(const mapa_pattern *p, int L, int base, uint8_t (*es)[2]) {
     return n;
 }
 
+// Terms of a tuple's score for suffix length L (DeepTables::term): Eq. 1 / 2
+// the partial of every suffix vertex with a scored prefix neighbour plus the
+// suffix-internal pattern edges; Eq. 3 with L >= 2 the C(L,2) pairs alone
+// (pair folding, scale L-1), with L = 1 the single partial; Baseline none.
+int suffix_terms(const mapa_pattern *p, int L, int base, uint8_t (*term)[3], int *nes, int *scale) {
+    const int T = p->k - L;
+    uint8_t es[8][2];
+    *nes = suffix_pairs(p, L, base, es);
+    const bool fold = base == SEL_INSENS && L >= 2;
+    *scale = fold ? L - 1 : 1;
+    int n = 0;
+    uint8_t tmp[16][3];
+    if (!fold && base != SEL_BASE)
+        for (int l = 0; l < L; ++l)
+            if (base == SEL_INSENS || (p->back[T + l] & ((1u << T) - 1u))) { tmp[n][0] = 0; tmp[n][1] = (uint8_t)l; tmp[n][2] = 0; ++n; }
+    for (int e = 0; e < *nes; ++e) { tmp[n][0] = 1; tmp[n][1] = es[e][0]; tmp[n][2] = es[e][1]; ++n; }
+    if (term)
+        for (int i = 0; i < n && i < kDeepMaxTerms; ++i) std::memcpy(term[i], tmp[i], 3);
+    return n;
+}
+
 // Valid L-tuples of distinct indices into r sorted devices (lex order); the
 // suffix-internal lex-leader constraints f(T+a) < f(T+b) become i_a < i_b.
 // Entry byte l = 4 * i_l.  Returns the count, or -1 above cap.
@@ -506,10 +527,12 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
         if (r < L || r > 32 || (L >= 2 && r > 16)) continue;
         const int nt = build_tuples(p, L, r, canon, nullptr, kMaxTup);
         if (nt <= 0) continue;
-        uint8_t es[8][2];
-        const int nes = suffix_pairs(p, L, base, es);
-        const double node = 40.0 + 12.0 * L + (L >= 2 && nes ? 6.0 * ((r * 16 + 31) / 32) : 0.0) + 6.0 * k;
-        const double round = 12.0 + 4.0 * L + 4.0 * nes;
+        int nes, scale;
+        const int nterm = suffix_terms(p, L, base, nullptr, &nes, &scale);
+        if (nterm > kDeepMaxTerms) continue;
+        const int NT = nterm <= 2 ? 2 : (nterm <= 4 ? 4 : 6);
+        const double node = 40.0 + 12.0 * L + (nes ? 6.0 * ((r * 16 + 31) / 32) : 0.0) + 6.0 * k;
+        const double round = 12.0 + 3.0 * NT;
         const double cost = (node + round * ((nt + 31) / 32)) / nt;
         if (cost < best * 0.98) { best = cost; bestL = L; }
     }
@@ -519,10 +542,7 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     tb->T = T;
     tb->r = r;
     tb->ntup = build_tuples(p, L, r, canon, tb->tup, kMaxTup);
-    tb->nes = suffix_pairs(p, L, base, tb->es);
-    tb->ptmask = 0;
-    for (int l = 0; l < L; ++l)
-        if (base == SEL_INSENS || (base != SEL_BASE && (p->back[T + l] & ((1u << T) - 1u)))) tb->ptmask |= 1 << l;
+    tb->nterm = suffix_terms(p, L, base, tb->term, &tb->nes, &tb->scale);
     // prefix sources common to every suffix vertex: their max is a lower bound
     // for the whole suffix, applied by compacting the node's device list; the
     // remaining per-vertex bounds are checked per tuple (pcon)
@@ -547,7 +567,7 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     // decoded prefix depth: enough items for ~8 per resident warp (x world)
     int sm = device_sm_count();
     if (sm <= 0) sm = 148;
-    const int occ = max_blocks_per_sm_deep(L, pl->sc, base == SEL_SENS ? 2 * tb->xsd * tb->xsd : 0);
+    const int occ = max_blocks_per_sm_deep(tb->nterm, pl->sc, base == SEL_SENS ? 2 * tb->xsd * tb->xsd : 0);
     const uint64_t warps = (uint64_t)sm * occ * 8;
     const uint64_t target = 8ull * warps * (uint64_t)world;
     // RAW items are uniform: stop at ~8 per warp.  Canonical items are not
