@@ -181,8 +181,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prune", action="store_true", help="skip the MAPA_F_PRUNE side measurement")
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--config", default="c4", choices=["c4", "c1", "c2", "c3", "c5"],
-                    help="c4 = the headline workload (default); c1/c2/c3/c5 measure the other SURVEY 8(d) configs")
+    ap.add_argument("--config", default="c4", choices=["c4", "c1", "c2", "c3", "c5", "deep"],
+                    help="c4 = the headline workload (default); c1/c2/c3/c5 measure the other SURVEY 8(d) configs; "
+                         "deep = the k > 8 path (SURVEY 8(f) NEXT 1)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "mapa" and not args.no_cpu_baseline:
         args.warmup = 3

@@ -259,4 +259,64 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
                                         "busy U{0..N-k}, selector U{3}), one batch launch per topology, queries "
                                         "sharded across ranks"})
         return line
+
+    if args.config == "deep":
+        topo = mp.Topology("cubemesh16")
+        busy = 0
+        sels = ((0, False, "greedy"), (1, True, "preserve_sensitive"), (1, False, "preserve_insensitive"))
+        k = 10
+        pat = mp.Pattern.make("ring", k)
+        per = math.perm(16, k)  # 29,059,430,400 embeddings per allocation
+        q = md.query_tensor(busy, device=dev)
+        recs = torch.zeros((3, 8), dtype=torch.int64, device=dev)
+        kms = {}
+        nsteps = max(3, steps // 5)
+        for i, (sel, sens, name) in enumerate(sels):
+            def fn(i=i, sel=sel, sens=sens):
+                mp.launch_query_wide(topo, pat, sel, sens, q.data_ptr(), recs[i].data_ptr(), busy, raw=True,
+                                     rank=rank, world=world, stream=stream)
+            kms[name] = max_over_ranks(_timed(torch, stream, fn, nsteps, warmup) / nsteps)
+        torch.cuda.synchronize()
+        if world == 1:
+            for i, (sel, sens, name) in enumerate(sels):
+                d = mp.decode_wide(topo, pat, busy, sel, sens, md.wide_records_from_tensor(recs[i])[0], raw=True)
+                assert d["raw"] == per, d
+        tot = sum(kms.values())
+        line = _base("deep", world, nsteps, warmup)
+        canon = {}
+        if rank == 0 and world == 1:
+            for kk in (12, 14):
+                p2 = mp.Pattern.make("ring", kk)
+                a, b = _events(torch)
+                a.record(stream)
+                d = mp.allocate(topo, p2, 0, False)
+                b.record(stream)
+                b.synchronize()
+                ms = a.elapsed_time(b)
+                canon[f"ring{kk}_greedy"] = {"ms": ms, "distinct": d["distinct"], "raw": d["raw"],
+                                             "distinct_per_s": d["distinct"] / (ms / 1e3),
+                                             "devices": list(d["devices"])}
+            from oracle import coracle as co
+            from oracle import mapa_oracle as mo
+            o = mo.builtin("cubemesh16")
+            kk_, ee = mo.make_pattern("ring", k)
+
+            def deep_cpu():
+                r = co.allocate_deep(o, 0b11111 << 11, kk_, ee, 0, False)  # 11 free devices
+                return r["raw"], 1
+            line["cpu_baseline"] = _cpu(deep_cpu, "ring-10 greedy on 11 free cubemesh16 devices (11!/1! = 39,916,800 "
+                                                  "embeddings), deep C oracle, all host threads")
+        emb_s = 3 * per / (tot / 1e3)
+        ach = 2 * emb_s / 1e9
+        line["roofline"] = {"bound": "alu", "kernel": "esa_deep<NT,SEL> (ring-10 RAW)",
+                            "achieved": ach, "peak": PEAK_GOPS, "unit": "Gop/s", "frac": ach / PEAK_GOPS,
+                            "traffic": None, "ops_per_embedding": 2,
+                            "note": "same algorithmic count as the narrow kernel (complete the score from the "
+                                    "shared prefix partial + compare)"}
+        line.update(metric="embeddings/sec (deep path: cubemesh16 ring-10 all free, RAW)", value=emb_s,
+                    unit="embeddings/s", allocations_per_s=3 / (tot / 1e3), kernel_ms=kms, scaling="strong",
+                    canonical=canon,
+                    config={"workload": "cubemesh16 x ring-10 (k > 8: 192-bit-key deep kernel), all free, RAW, "
+                                        "1 allocation per selector per step, sharded by work item"})
+        return line
     return None
