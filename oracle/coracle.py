@@ -58,7 +58,7 @@ def lib():
         _lib.oracle_allocate_deep.argtypes = [
             ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_uint32, ctypes.c_int,
             ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_int, ctypes.c_int,
-            ctypes.c_int, ctypes.c_int, ctypes.POINTER(OracleResultDeep)]
+            ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(OracleResultDeep)]
         _lib.oracle_eq2.restype = ctypes.c_double
         _lib.oracle_eq2.argtypes = [ctypes.c_int] * 3
     return _lib
@@ -88,9 +88,11 @@ def allocate(topo: mo.Topology, busy: int, k: int, pedges, selector: int, sensit
 
 
 def allocate_deep(topo: mo.Topology, busy: int, k: int, pedges, selector: int, sensitive: bool,
-                  nthreads: int | None = None, max_subsets: int = 4096) -> dict:
+                  nthreads: int | None = None, max_subsets: int = 4096, sub_lo: int = -1,
+                  sub_hi: int = -1) -> dict:
     """Deep oracle (k <= 16): same decision fields as allocate(); 'distinct'
-    is not counted (None)."""
+    is not counted (None).  [sub_lo, sub_hi): lex indices of the k-subsets
+    scored (negative = unrestricted)."""
     n = topo.n
     w = (ctypes.c_int32 * (n * n))(*[topo.w[u][v] for u in range(n) for v in range(n)])
     flat = [c for e in pedges for c in e]
@@ -98,7 +100,7 @@ def allocate_deep(topo: mo.Topology, busy: int, k: int, pedges, selector: int, s
     r = OracleResultDeep()
     nt = nthreads or os.cpu_count() or 1
     rc = lib().oracle_allocate_deep(n, w, busy, k, len(pedges), pe, selector, int(bool(sensitive)), nt,
-                                    max_subsets, ctypes.byref(r))
+                                    max_subsets, sub_lo, sub_hi, ctypes.byref(r))
     if rc != 0:
         raise ValueError(f"oracle_allocate_deep rc={rc}")
     if r.status == 1:

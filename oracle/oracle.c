@@ -397,9 +397,11 @@ static void *deep_worker(void *arg) {
 }
 
 /* w: n*n weights; busy: bit d busy; pe: 2m pattern edges; selector as
- * oracle_allocate.  max_subsets bounds the work (error -2 above it). */
+ * oracle_allocate.  max_subsets bounds the work (error -2 above it).  Only the
+ * subsets with lex index in [sub_lo, sub_hi) are scored (bounded samples and
+ * shard tests; a negative bound = unrestricted). */
 int oracle_allocate_deep(int n, const int32_t *w, uint32_t busy, int k, int m, const int32_t *pe,
-                         int selector, int sensitive, int nthreads, int max_subsets,
+                         int selector, int sensitive, int nthreads, int max_subsets, int sub_lo, int sub_hi,
                          oracle_result_deep *out) {
     memset(out, 0, sizeof(*out));
     if (n < 1 || n > 32 || k < 1 || k > 16 || m < 0 || m > 120) return -1;
@@ -426,6 +428,11 @@ int oracle_allocate_deep(int n, const int32_t *w, uint32_t busy, int k, int m, c
         idx[i]++;
         for (int j = i + 1; j < k; j++) idx[j] = idx[j - 1] + 1;
     }
+    int s_lo = sub_lo < 0 ? 0 : (sub_lo < nsub ? sub_lo : nsub);
+    int s_hi = sub_hi < 0 ? nsub : (sub_hi < nsub ? sub_hi : nsub);
+    if (s_hi < s_lo) s_hi = s_lo;
+    memmove(subs, subs + s_lo, sizeof(int[16]) * (size_t)(s_hi - s_lo));
+    nsub = s_hi - s_lo;
     dpool_t p;
     p.c = &c;
     p.subsets = subs;

@@ -86,3 +86,73 @@ def test_two_rank_combine_matches_unsharded_oracle():
             g = got[r][i]
             for f in ("devices", "mapping", "used_edges", "x", "y", "z", "agg_bw", "preserved_bw", "distinct"):
                 assert g[f] == exp[f], (name, r, f, g[f], exp[f])
+
+
+def _worker_wide(rank, port, cases, out_q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import math as _m
+
+    import torch.distributed as dist
+
+    from oracle import coracle as co
+    from oracle import mapa_oracle as mo
+    from tests.keyutil import encode_wide_key, selector_score
+    import paper_2110_03214_b200 as mp
+    from paper_2110_03214_b200 import dist as md
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=WORLD)
+    results = []
+    for name, busy, shape, k, sel, sens in cases:
+        o = mo.builtin(name)
+        kk, e = mo.make_pattern(shape, k)
+        nf = o.n - bin(busy).count("1")
+        nsub = _m.comb(nf, k)
+        half = (nsub + 1) // 2
+        lo, hi = (0, half) if rank == 0 else (half, nsub)
+        part = co.allocate_deep(o, busy, kk, e, sel, sens, nthreads=2, sub_lo=lo, sub_hi=hi)
+        t = mp.Topology(name)
+        tab = mp.effbw_rank_table(len(e))
+        if part["status"] == "ok":
+            key, eh, el = encode_wide_key(part, selector_score(part, sel, sens, tab, len(e)), k)
+        else:
+            key = eh = el = 0
+        rec = md.wide_record_tensor(mp.WideRecord(key=key, ecode_hi=eh, ecode_lo=el, leaves=part["raw"]))
+        comb = md.combine_wide_records(rec)
+        got = mp.decode_wide(t, mp.Pattern.make(shape, k), busy, sel, sens, comb, raw=True)
+        results.append(got)
+    out_q.put((rank, results))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+WIDE_CASES = [("cubemesh16", 0b0110000000100100, "ring", 10, 0, False),          # 11 free: 11 x 10!
+              ("torus2d16", 0b1000010000010010, "tree", 9, 1, True),            # 11 free: C(11,9) x 9!
+              ("cubemesh16", 0b0001000100010001, "ringtree", 9, 1, False),      # 12 free
+              ("dgx1v", 0b00100000, "full", 5, 0, False)]
+
+
+def test_two_rank_wide_combine_matches_unsharded_deep_oracle():
+    """Deep path (192-bit keys): the same exchange with 64-B wide records
+    (dist.combine_wide_records -> mapa_reduce_wide_records -> mapa_decode_wide)."""
+    from oracle import coracle as co
+    from oracle import mapa_oracle as mo
+
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_wide, args=(r, port, WIDE_CASES, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=400) for _ in range(WORLD))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for i, (name, busy, shape, k, sel, sens) in enumerate(WIDE_CASES):
+        o = mo.builtin(name)
+        kk, e = mo.make_pattern(shape, k)
+        exp = co.allocate_deep(o, busy, kk, e, sel, sens)
+        for r in range(WORLD):
+            g = got[r][i]
+            for f in ("devices", "mapping", "used_edges", "x", "y", "z", "agg_bw", "preserved_bw", "raw"):
+                assert g[f] == exp[f], (name, r, f, g[f], exp[f])
