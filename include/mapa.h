@@ -64,8 +64,16 @@ typedef int32_t mapa_status;
 #define MAPA_E_DISCONNECTED (-8) /* disconnected pattern, k > 1 */
 #define MAPA_E_INTERNAL (-10)   /* self-check failed (decoded key inconsistent) */
 
-/* Selectors (P:777 Greedy; Alg. 1 P:681-706 Preserve; P:777 Baseline). */
-enum { MAPA_SEL_GREEDY = 0, MAPA_SEL_PRESERVE = 1, MAPA_SEL_BASELINE = 2 };
+/* Selectors (P:777 Greedy; Alg. 1 P:681-706 Preserve; P:777 Baseline).
+ * MAPA_SEL_TOPO (trace replay / simulation only): the paper's Topo-aware
+ * baseline, "recursive bi-partitioning ... under the same PCIe tree (CPU
+ * socket)" (SPEC select_topo_aware S:337-344): the k lowest free
+ * ids of the smallest partition with >= k free devices, where the partitions
+ * are the socket groups of the topology recursively halved (by sorted id,
+ * first half = ceil(n/2)), ties to the partition with the lowest device id;
+ * no fitting partition -> the k lowest free ids (reading A21).  Its
+ * mapping is Baseline's: the lex-smallest used-edge list on that set. */
+enum { MAPA_SEL_GREEDY = 0, MAPA_SEL_PRESERVE = 1, MAPA_SEL_BASELINE = 2, MAPA_SEL_TOPO = 3 };
 
 /* Flags. */
 enum {
@@ -316,6 +324,58 @@ mapa_status mapa_trace_replay(const mapa_topology *t, const mapa_pattern *const 
                               int32_t npats, int32_t ntraces, int32_t nops,
                               const mapa_trace_op *d_ops, int32_t njobs, const mapa_query *d_jobs,
                               uint64_t *d_keys, uint32_t flags, void *cuda_stream);
+
+/* ------------------------------------------------------------- simulator */
+
+/* One job of a simulated stream (SPEC JobSpec / run_simulation, S:386-439;
+ * the execution framework of Fig. 13). */
+typedef struct {
+    int32_t pattern;     /* index into the pattern array of the call */
+    int32_t sensitive;   /* bandwidth sensitive (Preserve's Alg. 1 branch) */
+    double duration;     /* simulated seconds, allocation independent */
+    double arrival;      /* simulated seconds (0 = the paper's batch at t = 0) */
+} mapa_job;
+
+/* Policies of the paper's evaluation (§4; SPEC policy names). */
+enum { MAPA_POLICY_BASELINE = 0, MAPA_POLICY_TOPO = 1, MAPA_POLICY_GREEDY = 2, MAPA_POLICY_PRESERVE = 3 };
+
+/* SPEC JobLogRecord: the allocation of one job and its times. */
+typedef struct {
+    int32_t job, k;
+    uint32_t device_mask;
+    int32_t x, y, z;           /* link census of the used edges */
+    int32_t agg_bw;            /* Eq. 1 */
+    int32_t preserved_bw;      /* Eq. 3 on the free set at allocation time */
+    double pred_effbw;         /* Eq. 2 */
+    double arrival, start, end, wait;  /* simulated seconds; wait = start - arrival */
+} mapa_job_log;
+
+/* Strict-FIFO event schedule: the head job starts as soon as it
+ * has arrived and |F| >= k; finish events at equal times are processed before
+ * allocation attempts, in job order.  Because the hardware graph is complete
+ * and durations are allocation independent, the schedule depends only
+ * on the free COUNT, hence not on the policy.  Outputs (caller-owned host
+ * arrays): ops[2*njobs] = (op, job) with op 0 = ALLOC, 1 = RELEASE, and
+ * start[njobs], end[njobs].  Errors: INVALID_ARG (a job larger than the
+ * machine; negative duration / arrival). */
+mapa_status mapa_fifo_schedule(int32_t n_devices, int32_t njobs, const int32_t *k, const double *duration,
+                               const double *arrival, mapa_trace_op *ops, double *start, double *end);
+
+/* run_simulation: schedule the jobs, replay the allocations of
+ * `policy` on the device (one CTA, mapa_trace_replay's kernel: Topo-aware /
+ * Baseline / Greedy / Preserve decided and committed per ALLOC in shared
+ * memory), then decode every decision on the host into out[njobs] (job
+ * order).  The topology's own busy mask is not used or changed (the
+ * simulation starts idle).  Patterns must fit the narrow path (k <= 8).
+ * Blocks until done.  Errors: INVALID_ARG, UNSUPPORTED, CUDA, INTERNAL. */
+mapa_status mapa_simulate(const mapa_topology *t, const mapa_pattern *const *pats, int32_t npats, int32_t njobs,
+                          const mapa_job *jobs, int32_t policy, uint32_t flags, void *cuda_stream,
+                          mapa_job_log *out);
+
+/* summarize_log quantiles: min, 25th, 50th, 75th percentile, max
+ * of v[n] by linear interpolation between order statistics ("type 7":
+ * position p*(n-1)).  out[5].  Errors: INVALID_ARG for n < 1. */
+mapa_status mapa_quantiles(const double *v, int32_t n, double *out);
 
 /* Thread-local message of the last failing call on this thread. */
 const char *mapa_last_error(void);

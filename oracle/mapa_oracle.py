@@ -347,3 +347,130 @@ def replay_trace(topo: Topology, jobs, ops, patterns, policy: str, allocate_fn=N
         else:
             busy &= ~held.pop(j)
     return out
+
+
+# ---------------------------------------------------------------------------
+# Policies above the path and the simulator (§4; §5 P:871-880;
+# SPEC policies S:326-344, simulator S:386-439) -- SURVEY §8(f) NEXT 2.
+# ---------------------------------------------------------------------------
+
+def topo_partitions(topo: Topology):
+    """Reading A21 of "recursive bi-partitioning ... under the same PCIe tree
+    (CPU socket)": every socket group, then each half
+    of it (sorted ids, first half = ceil(n/2)), recursively down to single
+    devices, plus the whole machine."""
+    parts = []
+
+    def rec(g):
+        g = sorted(g)
+        parts.append(tuple(g))
+        if len(g) > 1:
+            h = (len(g) + 1) // 2
+            rec(g[:h])
+            rec(g[h:])
+
+    for g in topo.sockets:
+        rec(g)
+    parts.append(tuple(range(topo.n)))
+    return parts
+
+
+def select_topo_aware(topo: Topology, busy_mask: int, k: int):
+    """SPEC select_topo_aware: the smallest partition with >= k free devices
+    (ties: the partition holding the lowest device id), its k lowest free
+    ids; no partition fits -> the k lowest free ids (global fallback).
+    Returns the device tuple, or None without capacity."""
+    free = set(free_devices(topo, busy_mask))
+    if len(free) < k:
+        return None
+    fits = [p for p in topo_partitions(topo) if len([d for d in p if d in free]) >= k]
+    if fits:
+        best = min(fits, key=lambda p: (len(p), p[0]))
+        return tuple(sorted(d for d in best if d in free)[:k])
+    return tuple(sorted(free)[:k])
+
+
+def allocate_policy(topo: Topology, busy_mask: int, k: int, pedges, policy: str, sensitive: bool,
+                    allocate_fn=None):
+    """One decision of the evaluation's four policies.  Baseline
+    and Topo-aware choose the device set by their rule; the job's pattern is
+    then laid on it by the same tie-break as every policy (lex-smallest used
+    edge list), i.e. the Baseline allocation restricted to that set."""
+    alloc = allocate_fn or allocate
+    if policy == "greedy":
+        return alloc(topo, busy_mask, k, pedges, GREEDY, False)
+    if policy == "preserve":
+        return alloc(topo, busy_mask, k, pedges, PRESERVE, sensitive)
+    if policy == "baseline":
+        S = tuple(free_devices(topo, busy_mask)[:k]) if len(free_devices(topo, busy_mask)) >= k else None
+    elif policy == "topo":
+        S = select_topo_aware(topo, busy_mask, k)
+    else:
+        raise ValueError(policy)
+    if S is None:
+        return dict(status="no_capacity")
+    only = ((1 << topo.n) - 1) & ~device_mask(S)
+    d = alloc(topo, only, k, pedges, BASELINE, False)
+    # Eq. 3 is scored on the free set at allocation time, not on S alone
+    d = dict(d)
+    d["preserved_bw"] = preserved_bw(topo, free_devices(topo, busy_mask), S)
+    return d
+
+
+def simulate(topo: Topology, jobs, policy: str, allocate_fn=None):
+    """SPEC run_simulation, written as the paper's cycle of
+    events: all jobs wait in a FIFO queue (arrival times, default
+    0); at every event time, first the jobs whose execution time has elapsed
+    release their GPUs (job order), then the queue head is allocated while it
+    has arrived and enough GPUs are free.  jobs: dicts with k, edges
+    (pattern), sensitive, duration[, arrival].  Returns one log dict per job
+    (job order): devices, census, agg_bw, pred_effbw, preserved_bw at
+    allocation, arrival, start, end, wait."""
+    for j in jobs:
+        if j["k"] > topo.n:
+            raise ValueError("job larger than the machine")
+    busy = 0
+    t = 0.0
+    queue = list(range(len(jobs)))
+    running = {}  # job -> (end, mask)
+    log = {}
+    while queue or running:
+        for j in sorted(j for j, (e, _) in running.items() if e <= t):
+            busy &= ~running.pop(j)[1]
+        while queue:
+            j = queue[0]
+            job = jobs[j]
+            arr = job.get("arrival", 0.0)
+            if arr > t or job["k"] > topo.n - bin(busy).count("1"):
+                break
+            d = allocate_policy(topo, busy, job["k"], job["edges"], policy, bool(job["sensitive"]), allocate_fn)
+            m = device_mask(d["devices"])
+            assert d["status"] == "ok" and busy & m == 0
+            busy |= m
+            running[j] = (t + job["duration"], m)
+            log[j] = dict(job=j, k=job["k"], devices=tuple(d["devices"]), x=d["x"], y=d["y"], z=d["z"],
+                          agg_bw=d["agg_bw"], preserved_bw=d["preserved_bw"], pred_effbw=float(d["pred_effbw"]),
+                          arrival=arr, start=t, end=t + job["duration"], wait=t - arr)
+            queue.pop(0)
+        nxt = [e for e, _ in running.values()]
+        if queue and jobs[queue[0]].get("arrival", 0.0) > t:
+            nxt.append(jobs[queue[0]]["arrival"])
+        if not nxt:
+            break
+        t = min(nxt)
+    return [log[j] for j in range(len(jobs))]
+
+
+def quantiles7(values):
+    """min, 25th, 50th, 75th percentile, max by linear interpolation between
+    order statistics (SPEC summarize_log S:427-431, "type 7")."""
+    v = sorted(values)
+    if not v:
+        raise ValueError("empty")
+    out = []
+    for p in (0.0, 0.25, 0.5, 0.75, 1.0):
+        h = p * (len(v) - 1)
+        lo = int(h)
+        hi = min(lo + 1, len(v) - 1)
+        out.append(v[lo] + (h - lo) * (v[hi] - v[lo]))
+    return tuple(out)

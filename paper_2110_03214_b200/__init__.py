@@ -28,7 +28,8 @@ _lib = ctypes.CDLL(LIB_PATH)
 OK, NO_CAPACITY = 0, 1
 E_INVALID_ARG, E_PARSE, E_ALREADY_BUSY, E_NOT_BUSY, E_ID_RANGE = -1, -2, -3, -4, -5
 E_UNSUPPORTED, E_CUDA, E_DISCONNECTED, E_INTERNAL = -6, -7, -8, -10
-SEL_GREEDY, SEL_PRESERVE, SEL_BASELINE = 0, 1, 2
+SEL_GREEDY, SEL_PRESERVE, SEL_BASELINE, SEL_TOPO = 0, 1, 2, 3
+POLICIES = {"baseline": 0, "topo": 1, "greedy": 2, "preserve": 3}
 F_COMMIT, F_RAW, F_ALLOW_DISCONNECTED, F_PRUNE, F_DEEP = 1, 2, 4, 8, 16
 MAX_K = 16
 SHAPES = {"ring": 0, "tree": 1, "ringtree": 2, "full": 3, "edgeless": 4}
@@ -73,6 +74,22 @@ class PatternInfo(ctypes.Structure):
                 ("edges", (ctypes.c_int32 * 2) * 120), ("aut_order64", ctypes.c_uint64)]
 
 
+class Job(ctypes.Structure):
+    _fields_ = [("pattern", ctypes.c_int32), ("sensitive", ctypes.c_int32), ("duration", ctypes.c_double),
+                ("arrival", ctypes.c_double)]
+
+
+class JobLog(ctypes.Structure):
+    _fields_ = [("job", ctypes.c_int32), ("k", ctypes.c_int32), ("device_mask", ctypes.c_uint32),
+                ("x", ctypes.c_int32), ("y", ctypes.c_int32), ("z", ctypes.c_int32), ("agg_bw", ctypes.c_int32),
+                ("preserved_bw", ctypes.c_int32), ("pred_effbw", ctypes.c_double), ("arrival", ctypes.c_double),
+                ("start", ctypes.c_double), ("end", ctypes.c_double), ("wait", ctypes.c_double)]
+
+
+class TraceOp(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("job", ctypes.c_int32)]
+
+
 assert ctypes.sizeof(Query) == 16 and ctypes.sizeof(Record) == 32 and ctypes.sizeof(WideRecord) == 64
 
 _vp = ctypes.c_void_p
@@ -108,6 +125,13 @@ _SIGS = {
                                  ctypes.c_uint32, _vp]),
     "mapa_trace_replay": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp,
                                ctypes.c_int32, _vp, _vp, ctypes.c_uint32, _vp]),
+    "mapa_fifo_schedule": (_S, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(TraceOp), ctypes.POINTER(ctypes.c_double),
+                                ctypes.POINTER(ctypes.c_double)]),
+    "mapa_simulate": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(Job),
+                           ctypes.c_int32, ctypes.c_uint32, _vp, ctypes.POINTER(JobLog)]),
+    "mapa_quantiles": (_S, [ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
     "mapa_last_error": (ctypes.c_char_p, []),
     "mapa_version": (ctypes.c_char_p, []),
 }
@@ -351,3 +375,54 @@ def key_device_mask(key: int, topo_width: int, k: int) -> int:
     eb = k * (k - 1) // 2
     sb = (key >> eb) & ((1 << topo_width) - 1)
     return sum(1 << d for d in range(topo_width) if (sb >> (topo_width - 1 - d)) & 1)
+
+
+# ------------------------------------------------------------------ simulator
+
+def fifo_schedule(n_devices: int, ks, durations, arrivals=None):
+    """mapa_fifo_schedule: strict-FIFO (op, job) order and start / end times."""
+    n = len(ks)
+    K = (ctypes.c_int32 * max(1, n))(*ks)
+    Dd = (ctypes.c_double * max(1, n))(*durations)
+    Aa = (ctypes.c_double * max(1, n))(*(arrivals if arrivals is not None else [0.0] * n))
+    ops = (TraceOp * max(1, 2 * n))()
+    st = (ctypes.c_double * max(1, n))()
+    en = (ctypes.c_double * max(1, n))()
+    _check(_lib.mapa_fifo_schedule(n_devices, n, K, Dd, Aa, ops, st, en))
+    return [(ops[i].op, ops[i].job) for i in range(2 * n)], list(st)[:n], list(en)[:n]
+
+
+def simulate(topo: Topology, pats, jobs, policy: str, raw: bool = False, stream=None):
+    """mapa_simulate (SPEC run_simulation): jobs = [(pattern_index, sensitive,
+    duration[, arrival])]; returns one log dict per job (job order)."""
+    arr = (_vp * len(pats))(*[p.handle for p in pats])
+    js = (Job * max(1, len(jobs)))(*[Job(j[0], int(bool(j[1])), float(j[2]), float(j[3]) if len(j) > 3 else 0.0)
+                                     for j in jobs])
+    out = (JobLog * max(1, len(jobs)))()
+    _check(_lib.mapa_simulate(topo.handle, arr, len(pats), len(jobs), js, POLICIES[policy],
+                              F_RAW if raw else 0, _stream_ptr(stream), out))
+    res = []
+    for i in range(len(jobs)):
+        L = out[i]
+        res.append(dict(job=L.job, k=L.k, devices=tuple(d for d in range(32) if (L.device_mask >> d) & 1),
+                        x=L.x, y=L.y, z=L.z, agg_bw=L.agg_bw, preserved_bw=L.preserved_bw,
+                        pred_effbw=L.pred_effbw, arrival=L.arrival, start=L.start, end=L.end, wait=L.wait))
+    return res
+
+
+def quantiles(values):
+    """mapa_quantiles: (min, p25, p50, p75, max), linear interpolation (type 7)."""
+    v = (ctypes.c_double * max(1, len(values)))(*values)
+    out = (ctypes.c_double * 5)()
+    _check(_lib.mapa_quantiles(v, len(values), out))
+    return tuple(out)
+
+
+def summarize(records, group_by=None):
+    """SPEC summarize_log: per group the five quantiles of
+    pred_effbw and of wait, the makespan and the job count."""
+    groups = {}
+    for r in records:
+        groups.setdefault(r[group_by] if group_by else "all", []).append(r)
+    return {g: dict(pred_effbw=quantiles([r["pred_effbw"] for r in rs]), wait=quantiles([r["wait"] for r in rs]),
+                    makespan=max(r["end"] for r in rs), jobs=len(rs)) for g, rs in groups.items()}

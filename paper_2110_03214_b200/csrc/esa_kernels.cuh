@@ -109,7 +109,8 @@ struct Shared {
     uint8_t edge[kMaxPats][28];
     uint32_t busy;
     int one;  // = 1 (Ctx::one)
-    uint32_t pad[2];
+    uint32_t topoS;  // trace kernel: the Topo-aware device set of the current ALLOC
+    uint32_t pad;
 };
 
 // Single-query kernels: Shared + one Eq. 2 table of 3 xs^2 ints + the
@@ -1115,12 +1116,34 @@ esa_trace(const __grid_constant__ MultiTables tb, int nops, const mapa_trace_op 
         const DevPattern &P = tb.pat[ep];
         if (cur.op == 0) {
             const uint32_t busy = sh().busy;
-            Ctx<W> c = make_ctx<W>(tb.topo, P, ep, xs, busy, sel_code(qu.selector, qu.sensitive), false);
+            // Topo-aware (SPEC select_topo_aware; reading A21): the device set
+            // is the k lowest free ids of the smallest partition (recursive
+            // socket bisection, host table) with >= k free devices, else the k
+            // lowest free ids overall; its mapping is Baseline's (lex-smallest
+            // edge list), found by enumerating that set alone.
+            const bool topo = qu.selector == MAPA_SEL_TOPO;
+            uint32_t ebusy = busy;
+            if (topo) {
+                if (tid == 0) {
+                    const uint32_t nm = tb.topo.n >= 32 ? kFull : ((1u << tb.topo.n) - 1u);
+                    const uint32_t Fr = ~busy & nm;
+                    uint32_t from = Fr;
+                    for (int q = 0; q < tb.npart; ++q)
+                        if (__popc(tb.part[q] & Fr) >= (int)P.k) { from = tb.part[q] & Fr; break; }
+                    uint32_t S = 0;
+                    for (int q = 0; q < (int)P.k && from; ++q) { S |= from & (0u - from); from &= from - 1u; }
+                    sh().topoS = (__popc(S) == (int)P.k) ? S : 0u;
+                }
+                __syncthreads();
+                ebusy = ~sh().topoS;
+            }
+            const int scode = topo ? SEL_BASE : sel_code(qu.selector, qu.sensitive);
+            Ctx<W> c = make_ctx<W>(tb.topo, P, ep, xs, ebusy, scode, false);
             Best bst{0ull, 0u, 0u, 32, 0u, 32, nullptr};
             if (okp && P.k <= c.nF) {
                 const int D = (P.k - 1) < 2 ? (P.k - 1) : 2;
                 const uint32_t nItems = perm_count(c.nF, D);
-                switch (sel_code(qu.selector, qu.sensitive)) {
+                switch (scode) {
                     case SEL_GREEDY: trace_dispatch_k<W, SEL_GREEDY | 4 * CANON | 8>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
                     case SEL_INSENS: trace_dispatch_k<W, SEL_INSENS | 4 * CANON | 8>(P.k, c, D, nItems, gid, kWarps * G, bst); break;
                     case SEL_SENS: trace_dispatch_k<W, SEL_SENS | 4 * CANON | 8>(P.k, c, D, nItems, gid, kWarps * G, bst); break;

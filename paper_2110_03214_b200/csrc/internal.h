@@ -53,12 +53,15 @@ struct alignas(8) DevPattern {
 };
 static_assert(sizeof(DevPattern) == 64, "DevPattern layout");
 
+constexpr int kMaxParts = 64;
 template <int MAXP, int LUTCAP>
 struct Tables {
     DevTopo topo;
     int32_t npats;
     int32_t xs;      // row stride of the Eq. 2 tables on the device (16 if every m <= 15, else 32)
-    int32_t pad[2];
+    int32_t npart;   // Topo-aware partitions (trace kernel; SPEC select_topo_aware)
+    int32_t pad;
+    uint32_t part[kMaxParts];  // device masks, smallest first, ties by lowest device
     DevPattern pat[MAXP];
     uint16_t lut[LUTCAP];
 };

@@ -765,11 +765,47 @@ mapa_status decode_record(const mapa_topology *t, const mapa_pattern *p, uint32_
     return MAPA_OK;
 }
 
+// Topo-aware partitions (reading A21; SPEC select_topo_aware S:337-344,
+// "recursive bi-partitioning"): every socket group, recursively halved
+// by sorted id (first half = ceil(n/2)) down to single devices, plus the whole
+// machine; ordered by size, ties by lowest device id.
+void topo_partitions(const mapa_topology *t, uint32_t *part, int32_t *npart) {
+    std::vector<std::vector<int>> all;
+    std::vector<std::vector<int>> stack(t->sockets.rbegin(), t->sockets.rend());
+    while (!stack.empty()) {
+        std::vector<int> g = stack.back();
+        stack.pop_back();
+        std::sort(g.begin(), g.end());
+        all.push_back(g);
+        if (g.size() > 1) {
+            const size_t h = (g.size() + 1) / 2;
+            stack.push_back(std::vector<int>(g.begin() + h, g.end()));
+            stack.push_back(std::vector<int>(g.begin(), g.begin() + h));
+        }
+    }
+    std::vector<int> whole;
+    for (int d = 0; d < t->n; ++d) whole.push_back(d);
+    all.push_back(whole);
+    std::stable_sort(all.begin(), all.end(), [](const std::vector<int> &a, const std::vector<int> &b) {
+        return a.size() != b.size() ? a.size() < b.size() : a.front() < b.front();
+    });
+    int n = 0;
+    for (auto &g : all) {
+        if (n >= kMaxParts) break;
+        uint32_t m = 0;
+        for (int d : g) m |= 1u << d;
+        if (n > 0 && part[n - 1] == m) continue;  // a one-socket machine repeats the root
+        part[n++] = m;
+    }
+    *npart = n;
+}
+
 mapa_status build_multi(const mapa_topology *t, const mapa_pattern *const *pats, int npats, uint32_t flags,
                         MultiTables *tb) {
     if (npats < 1 || npats > kMaxPats) return fail(MAPA_E_INVALID_ARG, "npats must be 1..16");
     std::memset(tb, 0, sizeof(*tb));
     fill_devtopo(t, tb->topo);
+    topo_partitions(t, tb->part, &tb->npart);
     tb->npats = npats;
     int mmax = 0;
     for (int i = 0; i < npats; ++i)
@@ -778,6 +814,7 @@ mapa_status build_multi(const mapa_topology *t, const mapa_pattern *const *pats,
     int off = 0;
     for (int i = 0; i < npats; ++i) {
         if (!pats[i]) return fail(MAPA_E_INVALID_ARG, "null pattern");
+        if (!key_fits(t, pats[i])) return fail(MAPA_E_UNSUPPORTED, "batch / trace patterns need the narrow path (k <= 8)");
         const int n = (int)pats[i]->lut.size();
         if (off + n > kLutCapMulti) return fail(MAPA_E_UNSUPPORTED, "rank tables exceed 4096 entries");
         fill_devpattern(pats[i], (flags & MAPA_F_RAW) != 0, (uint16_t)off, tb->pat[i]);
@@ -1104,6 +1141,147 @@ mapa_status mapa_trace_replay(const mapa_topology *t, const mapa_pattern *const 
     if (err) return cuda_fail(err, "memset");
     err = launch_trace(*tbp, multi_has_constraints(*tbp), ntraces, nops, d_ops, njobs, d_jobs, d_keys, stream);
     if (err) return cuda_fail(err, "esa_trace launch");
+    return MAPA_OK;
+}
+
+mapa_status mapa_fifo_schedule(int32_t n_devices, int32_t njobs, const int32_t *k, const double *duration,
+                               const double *arrival, mapa_trace_op *ops, double *start, double *end) {
+    if (njobs < 0 || (njobs > 0 && (!k || !duration || !ops || !start || !end)) || n_devices < 1)
+        return fail(MAPA_E_INVALID_ARG, "bad schedule arguments");
+    for (int j = 0; j < njobs; ++j) {
+        if (k[j] < 1 || k[j] > n_devices) return fail(MAPA_E_INVALID_ARG, "job " + std::to_string(j) + " larger than the machine");
+        if (duration[j] < 0 || (arrival && arrival[j] < 0)) return fail(MAPA_E_INVALID_ARG, "negative time");
+    }
+    // strict FIFO event loop: finishes at time t first (job order), then the
+    // head starts while it has arrived and fits; time jumps to the next
+    // finish or the head's arrival
+    std::vector<std::pair<double, int>> running;  // (end, job)
+    int free = n_devices, q = 0, no = 0;
+    double t = 0.0;
+    while (q < njobs || !running.empty()) {
+        std::vector<int> done;
+        for (auto &r : running)
+            if (r.first <= t) done.push_back(r.second);
+        std::sort(done.begin(), done.end());
+        for (int j : done) {
+            ops[no++] = {1, j};
+            free += k[j];
+        }
+        running.erase(std::remove_if(running.begin(), running.end(),
+                                     [t](const std::pair<double, int> &r) { return r.first <= t; }),
+                      running.end());
+        while (q < njobs && (!arrival || arrival[q] <= t) && k[q] <= free) {
+            ops[no++] = {0, q};
+            start[q] = t;
+            end[q] = t + duration[q];
+            free -= k[q];
+            running.push_back({end[q], q});
+            ++q;
+        }
+        double nxt = 1e300;
+        for (auto &r : running) nxt = std::min(nxt, r.first);
+        if (q < njobs && arrival && arrival[q] > t) nxt = std::min(nxt, arrival[q]);
+        if (nxt == 1e300) break;
+        t = nxt;
+    }
+    if (q != njobs || no != 2 * njobs) return fail(MAPA_E_INTERNAL, "schedule did not drain");
+    return MAPA_OK;
+}
+
+mapa_status mapa_simulate(const mapa_topology *t, const mapa_pattern *const *pats, int32_t npats, int32_t njobs,
+                          const mapa_job *jobs, int32_t policy, uint32_t flags, void *stream, mapa_job_log *out) {
+    if (!t || !pats || njobs < 0 || (njobs > 0 && (!jobs || !out))) return fail(MAPA_E_INVALID_ARG, "null argument");
+    if (policy < MAPA_POLICY_BASELINE || policy > MAPA_POLICY_PRESERVE) return fail(MAPA_E_INVALID_ARG, "bad policy");
+    if (njobs == 0) return MAPA_OK;
+    std::vector<int32_t> kk(njobs);
+    std::vector<double> dur(njobs), arr(njobs), st(njobs), en(njobs);
+    for (int j = 0; j < njobs; ++j) {
+        if (jobs[j].pattern < 0 || jobs[j].pattern >= npats || !pats[jobs[j].pattern])
+            return fail(MAPA_E_INVALID_ARG, "job pattern index out of range");
+        kk[j] = pats[jobs[j].pattern]->k;
+        dur[j] = jobs[j].duration;
+        arr[j] = jobs[j].arrival;
+    }
+    std::vector<mapa_trace_op> ops(2 * (size_t)njobs);
+    mapa_status s = mapa_fifo_schedule(t->n, njobs, kk.data(), dur.data(), arr.data(), ops.data(), st.data(), en.data());
+    if (s != MAPA_OK) return s;
+    static const int32_t kSel[4] = {MAPA_SEL_BASELINE, MAPA_SEL_TOPO, MAPA_SEL_GREEDY, MAPA_SEL_PRESERVE};
+    std::vector<mapa_query> q(njobs);
+    for (int j = 0; j < njobs; ++j) {
+        q[j].busy = 0;
+        q[j].pattern = (uint32_t)jobs[j].pattern;
+        q[j].selector = kSel[policy];
+        q[j].sensitive = policy == MAPA_POLICY_PRESERVE ? (jobs[j].sensitive != 0) : 0;
+    }
+    cudaStream_t cs = (cudaStream_t)stream;
+    void *d_ops = nullptr, *d_jobs = nullptr, *d_keys = nullptr;
+    int err;
+    const size_t bo = ops.size() * sizeof(mapa_trace_op), bj = q.size() * sizeof(mapa_query), bk = njobs * sizeof(uint64_t);
+    if ((err = (int)cudaMalloc(&d_ops, bo + bj + bk))) return cuda_fail(err, "cudaMalloc (simulate)");
+    d_jobs = (char *)d_ops + bo;
+    d_keys = (char *)d_jobs + bj;
+    std::vector<uint64_t> keys(njobs);
+    auto cleanup = [&]() { cudaFree(d_ops); };
+    if ((err = (int)cudaMemcpyAsync(d_ops, ops.data(), bo, cudaMemcpyHostToDevice, cs)) ||
+        (err = (int)cudaMemcpyAsync(d_jobs, q.data(), bj, cudaMemcpyHostToDevice, cs))) {
+        cleanup();
+        return cuda_fail(err, "H2D (simulate)");
+    }
+    s = mapa_trace_replay(t, pats, npats, 1, 2 * njobs, (const mapa_trace_op *)d_ops, njobs,
+                          (const mapa_query *)d_jobs, (uint64_t *)d_keys, flags & MAPA_F_RAW, stream);
+    if (s != MAPA_OK) { cleanup(); return s; }
+    if ((err = (int)cudaMemcpyAsync(keys.data(), d_keys, bk, cudaMemcpyDeviceToHost, cs)) ||
+        (err = (int)cudaStreamSynchronize(cs))) {
+        cleanup();
+        return cuda_fail(err, "D2H (simulate)");
+    }
+    cleanup();
+    // host replay of the op order: the busy mask at each ALLOC decodes its key
+    uint32_t busy = 0;
+    std::vector<uint32_t> held(njobs, 0);
+    for (const mapa_trace_op &o : ops) {
+        const int j = o.job;
+        if (o.op == 1) { busy &= ~held[j]; continue; }
+        const mapa_pattern *p = pats[jobs[j].pattern];
+        mapa_record rec;
+        std::memset(&rec, 0, sizeof(rec));
+        rec.key = keys[j];
+        mapa_decision d;
+        const int sel = (policy == MAPA_POLICY_PRESERVE) ? MAPA_SEL_PRESERVE
+                      : (policy == MAPA_POLICY_GREEDY ? MAPA_SEL_GREEDY : MAPA_SEL_BASELINE);
+        s = decode_record(t, p, busy, sel, q[j].sensitive, flags & MAPA_F_RAW, &rec, &d);
+        if (s != MAPA_OK) return s == MAPA_NO_CAPACITY ? fail(MAPA_E_INTERNAL, "admitted job without a decision") : s;
+        if (d.device_mask & busy) return fail(MAPA_E_INTERNAL, "decision overlaps busy devices");
+        mapa_job_log &L = out[j];
+        std::memset(&L, 0, sizeof(L));
+        L.job = j;
+        L.k = p->k;
+        L.device_mask = d.device_mask;
+        L.x = d.x; L.y = d.y; L.z = d.z;
+        L.agg_bw = d.agg_bw;
+        L.preserved_bw = d.preserved_bw;
+        L.pred_effbw = d.pred_effbw;
+        L.arrival = arr[j];
+        L.start = st[j];
+        L.end = en[j];
+        L.wait = st[j] - arr[j];
+        held[j] = d.device_mask;
+        busy |= d.device_mask;
+    }
+    return MAPA_OK;
+}
+
+mapa_status mapa_quantiles(const double *v, int32_t n, double *out) {
+    if (!v || !out || n < 1) return fail(MAPA_E_INVALID_ARG, "quantiles of an empty set");
+    std::vector<double> a(v, v + n);
+    std::sort(a.begin(), a.end());
+    const double ps[5] = {0.0, 0.25, 0.5, 0.75, 1.0};
+    for (int i = 0; i < 5; ++i) {
+        const double h = ps[i] * (n - 1);
+        const int lo = (int)std::floor(h);
+        const int hi = std::min(lo + 1, n - 1);
+        out[i] = a[lo] + (h - lo) * (a[hi] - a[lo]);
+    }
     return MAPA_OK;
 }
 

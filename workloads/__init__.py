@@ -218,6 +218,20 @@ def c2_jobs(seed: int, count: int = 1000):
     return jobs
 
 
+def sim_jobs(seed: int, count: int = 300, kmax: int = 5):
+    """Simulator job file (§4 "Jobs configuration"): network U(6)
+    -> (sensitive, duration), requested GPUs k U{1..kmax},
+    pattern shape U{ring, tree, full} (k = 1: the singleton), all at t = 0."""
+    jobs = []
+    for j in range(count):
+        r = stream(seed ^ 0x5117, j)
+        name, sens, dur = NETWORKS[r.below(6)]
+        k = r.randint(1, kmax)
+        shape = ("ring", "tree", "full")[r.below(3)] if k > 1 else "full"
+        jobs.append(dict(job=j, network=name, sensitive=int(sens), duration=dur, k=k, shape=shape))
+    return jobs
+
+
 def fifo_ops(jobs, n_devices: int):
     """Op sequence of a strict-FIFO replay where every job arrives at t=0
     (SPEC S:404).  Admission depends only on the FREE COUNT (the
