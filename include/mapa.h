@@ -228,6 +228,23 @@ double mapa_pred_effbw(int32_t x, int32_t y, int32_t z);
  * = exact order for every m <= 120). */
 mapa_status mapa_effbw_rank_table(int32_t m, uint16_t *out);
 
+/* Eq. 2 with any 14 coefficients (theta NULL = Table 4). */
+double mapa_pred_effbw_theta(const double *theta, int32_t x, int32_t y, int32_t z);
+
+/* fit_effbw_model (§3.4.3 "non-linear polynomial regression",
+ * P:614-616): ordinary least squares of Eq. 2's 14 features (linear in
+ * theta) over n samples census[3n] = (x, y, z), bw[n] GB/s, by Householder QR.
+ * theta[14] out; diag[4] (may be NULL) = relative error ||r|| / ||bw||, RMSE,
+ * MAE, condition estimate max|R_jj| / min|R_jj| (reading A23).
+ * Errors: INVALID_ARG for n < 14 or a rank-deficient feature matrix (the
+ * message names the dependent feature). */
+mapa_status mapa_fit_effbw(int32_t n, const int32_t *census, const double *bw, double *theta, double *diag);
+
+/* Replace the pattern's Eq. 2 model (default Table 4): rebuilds its rank
+ * table; decisions and reported pred_effbw of this pattern use theta.  Not
+ * safe while a launch with this pattern is being prepared on another thread. */
+mapa_status mapa_pattern_set_effbw_model(mapa_pattern *p, const double *theta);
+
 /* ---------------------------------------------------------- single query */
 
 /* One allocation end to end, host buffers: stages the query (16 B) to the

@@ -280,7 +280,7 @@ def find_matches(topo: Topology, busy_mask: int, k: int, pedges):
     return out, raw
 
 
-def allocate(topo: Topology, busy_mask: int, k: int, pedges, selector: int, sensitive: bool):
+def allocate(topo: Topology, busy_mask: int, k: int, pedges, selector: int, sensitive: bool, theta=None):
     """Greedy (argmax AggBW), Preserve (Alg. 1: sensitive -> argmax
     predicted EffBW, insensitive -> argmax PreservedBW) or Baseline
     (constant score => lowest ids).  Strict '>' over the lex-ordered
@@ -293,7 +293,7 @@ def allocate(topo: Topology, busy_mask: int, k: int, pedges, selector: int, sens
     for S, E, pi in matches:
         agg = aggregated_bw(topo, E)
         x, y, z = link_census(topo, E)
-        eff = eq2_exact(x, y, z)
+        eff = eq2_exact(x, y, z) if theta is None else eq2_exact(x, y, z, tuple(Fraction(t) for t in theta))
         pres = preserved_bw(topo, F, S)
         if selector == GREEDY:
             s = agg
@@ -474,3 +474,29 @@ def quantiles7(values):
         hi = min(lo + 1, len(v) - 1)
         out.append(v[lo] + (h - lo) * (v[hi] - v[lo]))
     return tuple(out)
+
+
+# ---------------------------------------------------------------------------
+# Eq. 2 regression (§3.4.3; SPEC fit_effbw_model S:286-294)
+# ---------------------------------------------------------------------------
+
+def eq2_features(x: int, y: int, z: int):
+    """The 14 terms of Eq. 2 in theta order; the model is linear in theta."""
+    return [x, y, z, 1 / (x + 1), 1 / (y + 1), 1 / (z + 1), x * y, y * z, z * x,
+            1 / (x * y + 1), 1 / (y * z + 1), 1 / (z * x + 1), x * y * z, 1 / (x * y * z + 1)]
+
+
+def fit_effbw(samples):
+    """Ordinary least squares over the 14 features (numpy.linalg.lstsq as the
+    library primitive).  samples: [(x, y, z, bw)].  Returns (theta, rel_err)
+    with rel_err = ||residual|| / ||bw|| (reading A23)."""
+    import numpy as np
+    if len(samples) < 14:
+        raise ValueError("underdetermined: fewer than 14 samples")
+    A = np.array([eq2_features(*s[:3]) for s in samples], dtype=np.float64)
+    b = np.array([s[3] for s in samples], dtype=np.float64)
+    theta, _res, rank, _sv = np.linalg.lstsq(A, b, rcond=None)
+    if rank < 14:
+        raise ValueError("rank-deficient feature matrix")
+    r = A @ theta - b
+    return [float(t) for t in theta], float(np.linalg.norm(r) / np.linalg.norm(b))

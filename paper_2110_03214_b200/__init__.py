@@ -132,6 +132,10 @@ _SIGS = {
     "mapa_simulate": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(Job),
                            ctypes.c_int32, ctypes.c_uint32, _vp, ctypes.POINTER(JobLog)]),
     "mapa_quantiles": (_S, [ctypes.POINTER(ctypes.c_double), ctypes.c_int32, ctypes.POINTER(ctypes.c_double)]),
+    "mapa_pred_effbw_theta": (ctypes.c_double, [ctypes.POINTER(ctypes.c_double)] + [ctypes.c_int32] * 3),
+    "mapa_fit_effbw": (_S, [ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_double),
+                            ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "mapa_pattern_set_effbw_model": (_S, [_vp, ctypes.POINTER(ctypes.c_double)]),
     "mapa_last_error": (ctypes.c_char_p, []),
     "mapa_version": (ctypes.c_char_p, []),
 }
@@ -160,6 +164,22 @@ def version() -> str:
 def pred_effbw(x: int, y: int, z: int) -> float:
     """Eq. 2 with Table 4 theta."""
     return _lib.mapa_pred_effbw(x, y, z)
+
+
+def pred_effbw_theta(theta, x: int, y: int, z: int) -> float:
+    th = (ctypes.c_double * 14)(*theta)
+    return _lib.mapa_pred_effbw_theta(th, x, y, z)
+
+
+def fit_effbw(samples):
+    """mapa_fit_effbw: samples [(x, y, z, bw)] -> (theta[14], {rel_err, rmse, mae, cond})."""
+    n = len(samples)
+    cen = (ctypes.c_int32 * max(1, 3 * n))(*[c for s in samples for c in s[:3]])
+    bw = (ctypes.c_double * max(1, n))(*[s[3] for s in samples])
+    th = (ctypes.c_double * 14)()
+    dg = (ctypes.c_double * 4)()
+    _check(_lib.mapa_fit_effbw(n, cen, bw, th, dg))
+    return list(th), dict(rel_err=dg[0], rmse=dg[1], mae=dg[2], cond=dg[3])
 
 
 def effbw_rank_table(m: int) -> list[int]:
@@ -250,6 +270,11 @@ class Pattern:
     @classmethod
     def make(cls, shape: str, k: int) -> "Pattern":
         return cls(k, shape=shape)
+
+    def set_effbw_model(self, theta):
+        """mapa_pattern_set_effbw_model: Eq. 2 coefficients for this pattern."""
+        th = (ctypes.c_double * 14)(*theta)
+        _check(_lib.mapa_pattern_set_effbw_model(self._h, th))
 
     def __del__(self):
         try:

@@ -39,6 +39,7 @@ struct mapa_pattern {
     uint16_t src[kMaxKDeep];   // src[u] bit i: lex-leader f(i) < f(u)
     uint64_t aut = 1;          // |Aut(P)| (16! < 2^45)
     std::vector<uint16_t> lut;   // (m+1)^2
+    double theta[14];          // Eq. 2 model of this pattern (Table 4 unless mapa_pattern_set_effbw_model)
     void *d_lut = nullptr;     // device copy of lut (deep kernel), uploaded on first use
     int d_lut_dev = -1;
 };
@@ -209,22 +210,35 @@ uint32_t nmask_of(int n) { return n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u); }
 const double kTheta[14] = {16.396, 4.536, 1.556, -20.694, -9.467, 7.615, -7.973,
                            12.733, -4.195, -8.413, 62.851, 27.418, -5.114, -46.973};
 
-double eq2(int xi, int yi, int zi) {
+// The 14 features of Eq. 2 (the model is linear in theta).
+void eq2_features(int xi, int yi, int zi, double *f) {
     const double x = xi, y = yi, z = zi;
-    const double lin = kTheta[0] * x + kTheta[1] * y + kTheta[2] * z;
-    const double inv = kTheta[3] / (x + 1.0) + kTheta[4] / (y + 1.0) + kTheta[5] / (z + 1.0);
-    const double pair = kTheta[6] * x * y + kTheta[7] * y * z + kTheta[8] * z * x;
-    const double ipair = kTheta[9] / (x * y + 1.0) + kTheta[10] / (y * z + 1.0) + kTheta[11] / (z * x + 1.0);
-    const double trip = kTheta[12] * x * y * z + kTheta[13] / (x * y * z + 1.0);
+    f[0] = x; f[1] = y; f[2] = z;
+    f[3] = 1.0 / (x + 1.0); f[4] = 1.0 / (y + 1.0); f[5] = 1.0 / (z + 1.0);
+    f[6] = x * y; f[7] = y * z; f[8] = z * x;
+    f[9] = 1.0 / (x * y + 1.0); f[10] = 1.0 / (y * z + 1.0); f[11] = 1.0 / (z * x + 1.0);
+    f[12] = x * y * z; f[13] = 1.0 / (x * y * z + 1.0);
+}
+
+double eq2_theta(const double *th, int xi, int yi, int zi) {
+    const double x = xi, y = yi, z = zi;
+    const double lin = th[0] * x + th[1] * y + th[2] * z;
+    const double inv = th[3] / (x + 1.0) + th[4] / (y + 1.0) + th[5] / (z + 1.0);
+    const double pair = th[6] * x * y + th[7] * y * z + th[8] * z * x;
+    const double ipair = th[9] / (x * y + 1.0) + th[10] / (y * z + 1.0) + th[11] / (z * x + 1.0);
+    const double trip = th[12] * x * y * z + th[13] / (x * y * z + 1.0);
     return lin + inv + pair + ipair + trip;
 }
 
-// Dense rank of Eq. 2 over the censuses with x+y+z = m (reading A9: distinct
-// censuses never tie and are separated by >= 7.8e-4, so double order is exact).
-std::vector<uint16_t> rank_table(int m) {
+double eq2(int xi, int yi, int zi) { return eq2_theta(kTheta, xi, yi, zi); }
+
+// Dense rank of Eq. 2 over the censuses with x+y+z = m (reading A9/A20: with
+// Table 4 theta distinct censuses never tie and double order is exact; with a
+// fitted theta the double order defines the rank).
+std::vector<uint16_t> rank_table(int m, const double *th = kTheta) {
     std::vector<std::pair<double, int>> v;
     for (int x = 0; x <= m; ++x)
-        for (int y = 0; x + y <= m; ++y) v.push_back({eq2(x, y, m - x - y), x * (m + 1) + y});
+        for (int y = 0; x + y <= m; ++y) v.push_back({eq2_theta(th, x, y, m - x - y), x * (m + 1) + y});
     std::sort(v.begin(), v.end());
     std::vector<uint16_t> lut((size_t)(m + 1) * (m + 1), 0);
     int r = 0;
@@ -311,6 +325,7 @@ mapa_status compile_pattern(int k, const std::vector<std::pair<int, int>> &raw, 
         }
         p->aut *= orb;
     }
+    std::memcpy(p->theta, kTheta, sizeof(kTheta));
     p->lut = rank_table(p->m);
     *out = p;
     return MAPA_OK;
@@ -660,7 +675,7 @@ mapa_status fill_decision(const mapa_topology *t, const mapa_pattern *p, uint32_
     d.agg_bw = agg;
     d.preserved_bw = pres;
     d.score = (int32_t)score;
-    d.pred_effbw = eq2(x, y, z);
+    d.pred_effbw = eq2_theta(p->theta, x, y, z);
     return MAPA_OK;
 }
 
@@ -1282,6 +1297,82 @@ mapa_status mapa_quantiles(const double *v, int32_t n, double *out) {
         const int hi = std::min(lo + 1, n - 1);
         out[i] = a[lo] + (h - lo) * (a[hi] - a[lo]);
     }
+    return MAPA_OK;
+}
+
+double mapa_pred_effbw_theta(const double *theta, int32_t x, int32_t y, int32_t z) {
+    return eq2_theta(theta ? theta : kTheta, x, y, z);
+}
+
+mapa_status mapa_fit_effbw(int32_t n, const int32_t *census, const double *bw, double *theta, double *diag) {
+    if (!census || !bw || !theta) return fail(MAPA_E_INVALID_ARG, "null argument");
+    if (n < 14) return fail(MAPA_E_INVALID_ARG, "fit_effbw: " + std::to_string(n) + " samples < 14 coefficients (underdetermined)");
+    for (int i = 0; i < 3 * n; ++i)
+        if (census[i] < 0) return fail(MAPA_E_INVALID_ARG, "fit_effbw: negative census");
+    // least squares by Householder QR of the n x 14 feature matrix (column major)
+    const int c = 14;
+    std::vector<double> A((size_t)n * c), b(bw, bw + n);
+    for (int i = 0; i < n; ++i) {
+        double f[14];
+        eq2_features(census[3 * i], census[3 * i + 1], census[3 * i + 2], f);
+        for (int j = 0; j < c; ++j) A[(size_t)j * n + i] = f[j];
+    }
+    double colmax = 0.0;
+    for (double v : A) colmax = std::max(colmax, std::fabs(v));
+    std::vector<double> rdiag(c);
+    for (int j = 0; j < c; ++j) {
+        double *a = &A[(size_t)j * n];
+        double nrm = 0.0;
+        for (int i = j; i < n; ++i) nrm += a[i] * a[i];
+        nrm = std::sqrt(nrm);
+        if (nrm <= 1e-12 * std::max(1.0, colmax))
+            return fail(MAPA_E_INVALID_ARG, "fit_effbw: rank-deficient feature matrix (feature " + std::to_string(j + 1) +
+                                                " is a combination of the others on these censuses)");
+        const double alpha = a[j] > 0 ? -nrm : nrm;
+        a[j] -= alpha;
+        double vv = 0.0;
+        for (int i = j; i < n; ++i) vv += a[i] * a[i];
+        for (int k = j + 1; k < c; ++k) {
+            double *ak = &A[(size_t)k * n];
+            double d = 0.0;
+            for (int i = j; i < n; ++i) d += a[i] * ak[i];
+            const double s2 = 2.0 * d / vv;
+            for (int i = j; i < n; ++i) ak[i] -= s2 * a[i];
+        }
+        double d = 0.0;
+        for (int i = j; i < n; ++i) d += a[i] * b[i];
+        const double s2 = 2.0 * d / vv;
+        for (int i = j; i < n; ++i) b[i] -= s2 * a[i];
+        rdiag[j] = alpha;
+    }
+    double rmin = 1e300, rmax = 0.0;
+    for (int j = 0; j < c; ++j) { rmin = std::min(rmin, std::fabs(rdiag[j])); rmax = std::max(rmax, std::fabs(rdiag[j])); }
+    for (int j = c - 1; j >= 0; --j) {  // back substitution, R above the diagonal in A
+        double v = b[j];
+        for (int k = j + 1; k < c; ++k) v -= A[(size_t)k * n + j] * theta[k];
+        theta[j] = v / rdiag[j];
+    }
+    if (diag) {  // relative error ||r|| / ||bw||, RMSE, MAE, condition estimate of R
+        double r2 = 0.0, b2 = 0.0, ab = 0.0;
+        for (int i = 0; i < n; ++i) {
+            const double r = eq2_theta(theta, census[3 * i], census[3 * i + 1], census[3 * i + 2]) - bw[i];
+            r2 += r * r;
+            ab += std::fabs(r);
+            b2 += bw[i] * bw[i];
+        }
+        diag[0] = b2 > 0 ? std::sqrt(r2 / b2) : 0.0;
+        diag[1] = std::sqrt(r2 / n);
+        diag[2] = ab / n;
+        diag[3] = rmax / rmin;
+    }
+    return MAPA_OK;
+}
+
+mapa_status mapa_pattern_set_effbw_model(mapa_pattern *p, const double *theta) {
+    if (!p || !theta) return fail(MAPA_E_INVALID_ARG, "null argument");
+    std::memcpy(p->theta, theta, sizeof(p->theta));
+    p->lut = rank_table(p->m, p->theta);
+    if (p->d_lut) { cudaFree(p->d_lut); p->d_lut = nullptr; p->d_lut_dev = -1; }
     return MAPA_OK;
 }
 
