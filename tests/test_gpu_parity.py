@@ -140,10 +140,17 @@ def test_edge_cases():
 
 
 def test_unsupported_key_budget():
+    """ring-8 on 32 devices needs 15 + 32 + 28 > 63 key bits: the narrow
+    entry point refuses it; mapa_allocate routes it to the deep path."""
     t = mp.Topology(text=W.het32_text())
+    p = mp.Pattern.make("ring", 8)
+    q, rec = md.query_tensor(0), torch.zeros(4, dtype=torch.int64, device="cuda")
     with pytest.raises(mp.MapaError) as e:
-        mp.allocate(t, mp.Pattern.make("ring", 8), 0, False)
+        mp.launch_query(t, p, 0, False, q.data_ptr(), rec.data_ptr(), busy_hint=0)
     assert e.value.status == mp.E_UNSUPPORTED
+    t.set_busy(((1 << 32) - 1) & ~0x3FF)  # 10 free: P(10,8)/16 canonical leaves
+    d = mp.allocate(t, p, 0, False)
+    assert d["status"] == "ok" and d["leaves"] == 1814400 // 16
 
 
 def test_commit_and_release_roundtrip():
