@@ -267,7 +267,7 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
         k = 10
         pat = mp.Pattern.make("ring", k)
         per = math.perm(16, k)  # 29,059,430,400 embeddings per allocation
-        q = md.query_tensor(busy, device=dev)
+        q = md.query64_tensor(busy, device=dev)
         recs = torch.zeros((3, 8), dtype=torch.int64, device=dev)
         kms = {}
         nsteps = max(3, steps // 5)
@@ -316,7 +316,7 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
         line.update(metric="embeddings/sec (deep path: cubemesh16 ring-10 all free, RAW)", value=emb_s,
                     unit="embeddings/s", allocations_per_s=3 / (tot / 1e3), kernel_ms=kms, scaling="strong",
                     canonical=canon,
-                    config={"workload": "cubemesh16 x ring-10 (k > 8: 192-bit-key deep kernel), all free, RAW, "
+                    config={"workload": "cubemesh16 x ring-10 (k > 8: 256-bit-key deep kernel), all free, RAW, "
                                         "1 allocation per selector per step, sharded by work item"})
         return line
     return None

@@ -59,7 +59,7 @@ typedef int32_t mapa_status;
 #define MAPA_E_ALREADY_BUSY (-3) /* claim of a busy device, state unchanged */
 #define MAPA_E_NOT_BUSY (-4)    /* release of a free device */
 #define MAPA_E_ID_RANGE (-5)    /* device id out of range */
-#define MAPA_E_UNSUPPORTED (-6) /* N > 32, k > 16; narrow-only entry points: k > 8 or 15+W+C(k,2) > 63 */
+#define MAPA_E_UNSUPPORTED (-6) /* N > 64, k > 16; narrow-only entry points: N > 32, k > 8 or 15+W+C(k,2) > 63 */
 #define MAPA_E_CUDA (-7)        /* CUDA runtime error (message has the CUDA string) */
 #define MAPA_E_DISCONNECTED (-8) /* disconnected pattern, k > 1 */
 #define MAPA_E_INTERNAL (-10)   /* self-check failed (decoded key inconsistent) */
@@ -85,8 +85,9 @@ enum {
                                        narrow 63-bit key fits (testing / comparison) */
 };
 
-/* Limits.  Narrow path (mapa_launch_query, batches, traces): k <= 8 and
- * 15 + W + C(k,2) <= 63.  Deep path (mapa_launch_query_wide): k <= 16. */
+/* Limits.  Narrow path (mapa_launch_query, batches, traces, simulation):
+ * N <= 32, k <= 8 and 15 + W + C(k,2) <= 63.  Deep path
+ * (mapa_launch_query_wide): N <= 64, k <= 16. */
 #define MAPA_MAX_K 16
 #define MAPA_MAX_EDGES 120
 
@@ -101,7 +102,7 @@ typedef struct mapa_pattern mapa_pattern;   /* immutable compiled pattern descri
 typedef struct {
     int32_t status;          /* MAPA_OK or MAPA_NO_CAPACITY */
     int32_t k;               /* pattern vertices */
-    uint32_t device_mask;    /* bit d = device d allocated */
+    uint64_t device_mask;    /* bit d = device d allocated */
     int8_t mapping[16];      /* mapping[i] = device of pattern vertex i (lex-first of the match) */
     int32_t m;               /* pattern edges */
     int32_t used[120][2];    /* sorted used edges (lo, hi) = E(P) ∩ E(M) realised */
@@ -113,8 +114,7 @@ typedef struct {
     uint64_t raw_embeddings;   /* P(|F|,k) injective maps (counted in RAW mode) */
     uint64_t distinct_matches; /* P(|F|,k)/|Aut(P)| (counted in canonical mode) */
     uint64_t leaves_scored;    /* leaves the kernel actually scored */
-    uint64_t key;            /* narrow path: packed argmax key (mapa_record);
-                                deep path: key word of mapa_wide_record */
+    uint64_t key;            /* narrow path: packed argmax key (mapa_record); deep path: the score word */
     uint64_t ecode[2];       /* deep path: 128-bit edge code {high, low} (0 on the narrow path) */
 } mapa_decision;
 
@@ -125,6 +125,13 @@ typedef struct {
     int32_t selector;    /* MAPA_SEL_* */
     int32_t sensitive;   /* PRESERVE: 1 = bandwidth sensitive (Alg. 1) */
 } mapa_query;
+
+/* Device-side query of the deep path, 16 bytes (N <= 64). */
+typedef struct {
+    uint64_t busy;       /* bit d = device d busy */
+    int32_t selector;    /* ignored by the launch (the call's selector decides) */
+    int32_t sensitive;
+} mapa_query64;
 
 /* Device-side result record, 32 bytes.
  *   key = score << (W + C(k,2)) | brev_W(S) << C(k,2) | ecode, where W is the
@@ -141,19 +148,21 @@ typedef struct {
     uint64_t reserved;   /* scratch (MAPA_F_PRUNE: best score + 1 found so far), zeroed by the launch */
 } mapa_record;
 
-/* Deep-path result record, 64 bytes (k <= 16, N <= 32).
- * The argmax key is 192 bits, compared lexicographically as
- * (key, ecode_hi, ecode_lo):
- *   key   = score << 32 | brev_32(S)   (bit 31-d set for every chosen device d;
- *           larger = lex-smaller device tuple)
+/* Deep-path result record, 64 bytes (k <= 16, N <= 64; SURVEY §8(f) NEXT 1
+ * and NEXT 4).  The argmax key is 256 bits, compared lexicographically as
+ * (score, set, ecode_hi, ecode_lo):
+ *   score = the selector score (AggBW, Eq. 2 rank, PreservedBW, 0)
+ *   set   = brev_64(S): bit 63-d set for every chosen device d (larger =
+ *           lex-smaller device tuple)
  *   ecode = 128-bit edge code: bit C(k,2)-1-p set for every used edge whose
  *           endpoint ranks inside S form the p-th pair in lex order (larger =
  *           lex-smaller used-edge list); ecode_hi holds bits 64..127.
- * key 0 = no match.  The launch zeroes the record; `lock` serialises the
- * per-CTA merges of the 192-bit maximum (order-independent, so the result is
+ * set 0 = no match.  The launch zeroes the record; `lock` serialises the
+ * per-CTA merges of the maximum (order independent, so the result is
  * deterministic for every grid size and rank count). */
 typedef struct {
-    uint64_t key;
+    uint64_t score;
+    uint64_t set;
     uint64_t ecode_hi;
     uint64_t ecode_lo;
     uint64_t leaves;     /* leaves scored */
@@ -161,7 +170,7 @@ typedef struct {
     uint32_t lock;       /* merge lock (scratch) */
     uint32_t status;     /* 0 ok; nonzero = device-side argument error */
     uint32_t pad;
-    uint64_t reserved[2];
+    uint64_t reserved;
 } mapa_wide_record;
 
 /* Trace op (C2 replay): op 0 = ALLOC job, 1 = RELEASE job. */
@@ -175,24 +184,25 @@ typedef struct {
 /* Builtin name (dgx1v, dgx1p, summit, torus2d16, cubemesh16: S:43-51,
  * S:105-110) when is_text == 0, else the topology text format of DESIGN.md
  * (fields of S:115: name, devices, sockets, link a b class; 1-based ids;
- * unlisted pairs are PCIe).  N <= 32.  *out owned by the caller,
+ * unlisted pairs are PCIe).  N <= 64; topologies with N > 32 run on the
+ * deep path only (bigger servers).  *out owned by the caller,
  * freed with mapa_free_topology.  Errors: PARSE (message names the line),
  * ID_RANGE, UNSUPPORTED (N > 32), INVALID_ARG. */
 mapa_status mapa_load_topology(const char *builtin_or_text, int32_t is_text, mapa_topology **out);
 void mapa_free_topology(mapa_topology *t);
 
-/* N, padded width W (8, 16 or 32), link bandwidth matrix bw[N*N] (GB/s,
+/* N, padded width W (8, 16, 32 or 64), link bandwidth matrix bw[N*N] (GB/s,
  * diagonal 0; may be NULL) and the busy mask. */
 mapa_status mapa_topology_info(const mapa_topology *t, int32_t *n, int32_t *width, int32_t *bw,
-                               uint32_t *busy);
+                               uint64_t *busy);
 
 /* State management (§3.6; SPEC allocate_devices S:70-78,
  * release_devices S:79-87).  claim: ALREADY_BUSY / ID_RANGE with state
  * unchanged; release: NOT_BUSY / ID_RANGE. set_busy replaces the mask
  * (checkpoint/restore). */
-mapa_status mapa_claim(mapa_topology *t, uint32_t device_mask);
-mapa_status mapa_release(mapa_topology *t, uint32_t device_mask);
-mapa_status mapa_set_busy(mapa_topology *t, uint32_t busy);
+mapa_status mapa_claim(mapa_topology *t, uint64_t device_mask);
+mapa_status mapa_release(mapa_topology *t, uint64_t device_mask);
+mapa_status mapa_set_busy(mapa_topology *t, uint64_t busy);
 
 /* ---------------------------------------------------------------- patterns */
 
@@ -270,7 +280,7 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
  * else 0xFFFFFFFF. */
 mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
                               int32_t sensitive, const mapa_query *d_query, mapa_record *d_record,
-                              uint32_t flags, int32_t rank, int32_t world, uint32_t busy_hint,
+                              uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint,
                               void *cuda_stream);
 
 /* Host: combine n shard records (max key, sum leaves). */
@@ -279,7 +289,7 @@ mapa_status mapa_reduce_records(const mapa_record *records, int32_t n, mapa_reco
 /* Host: decode a (combined) record into a decision for (busy, selector,
  * sensitive, flags).  Recomputes census, AggBW, PreservedBW and Eq. 2 from
  * the decoded (S, mapping) and checks them against the key's score. */
-mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint32_t busy,
+mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint64_t busy,
                         int32_t selector, int32_t bw_sensitive, uint32_t flags,
                         const mapa_record *record, mapa_decision *out);
 
@@ -289,19 +299,19 @@ mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint32_t 
  * NEXT 1: the paper's overhead study reaches "9 GPUs and above" on 16-GPU
  * graphs).  Same contract as mapa_launch_query (busy read from
  * d_query->busy on the device; work item i of the prefix space goes to rank
- * i's stripe owner; asynchronous on cuda_stream) but with the 192-bit key of
- * mapa_wide_record, so any k <= 16 on any N <= 32 fits.  Enumeration: a
+ * i's stripe owner; asynchronous on cuda_stream) but with the 256-bit key of
+ * mapa_wide_record, so any k <= 16 on any N <= 64 fits.  Enumeration: a
  * warp-uniform explicit-stack DFS over the first k-L pattern vertices, then
  * the last L vertices (L = 1..4, chosen on the host) as a lane-parallel scan
  * over a table of index tuples into the remaining free devices.  RAW and
  * canonical modes as for the narrow path; MAPA_F_PRUNE is ignored.
  * Errors: INVALID_ARG, UNSUPPORTED (k > 16), CUDA. */
 mapa_status mapa_launch_query_wide(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
-                                   int32_t sensitive, const mapa_query *d_query, mapa_wide_record *d_record,
-                                   uint32_t flags, int32_t rank, int32_t world, uint32_t busy_hint,
+                                   int32_t sensitive, const mapa_query64 *d_query, mapa_wide_record *d_record,
+                                   uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint,
                                    void *cuda_stream);
 
-/* Host: combine n deep shard records (lexicographic max of the 192-bit key,
+/* Host: combine n deep shard records (lexicographic max of the 256-bit key,
  * sum of leaves, OR of status). */
 mapa_status mapa_reduce_wide_records(const mapa_wide_record *records, int32_t n, mapa_wide_record *out);
 
@@ -310,7 +320,7 @@ mapa_status mapa_reduce_wide_records(const mapa_wide_record *records, int32_t n,
  * order over the devices of S in ascending order, keeping only partial maps
  * whose placed pattern edges land on decoded edges (first complete map =
  * lex-first).  Scores are recomputed and checked against the key. */
-mapa_status mapa_decode_wide(const mapa_topology *t, const mapa_pattern *p, uint32_t busy,
+mapa_status mapa_decode_wide(const mapa_topology *t, const mapa_pattern *p, uint64_t busy,
                              int32_t selector, int32_t bw_sensitive, uint32_t flags,
                              const mapa_wide_record *record, mapa_decision *out);
 

@@ -33,7 +33,7 @@ class OracleResult(ctypes.Structure):
 
 class OracleResultDeep(ctypes.Structure):
     _fields_ = [("status", ctypes.c_int32), ("k", ctypes.c_int32),
-                ("device_mask", ctypes.c_uint32), ("mapping", ctypes.c_int8 * 16),
+                ("device_mask", ctypes.c_uint64), ("mapping", ctypes.c_int8 * 16),
                 ("m", ctypes.c_int32), ("used", (ctypes.c_int32 * 2) * 120),
                 ("x", ctypes.c_int32), ("y", ctypes.c_int32), ("z", ctypes.c_int32),
                 ("agg_bw", ctypes.c_int32), ("preserved_bw", ctypes.c_int32),
@@ -56,7 +56,7 @@ def lib():
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(OracleResult)]
         _lib.oracle_allocate_deep.restype = ctypes.c_int
         _lib.oracle_allocate_deep.argtypes = [
-            ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_uint32, ctypes.c_int,
+            ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_uint64, ctypes.c_int,
             ctypes.c_int, ctypes.POINTER(ctypes.c_int32), ctypes.c_int, ctypes.c_int,
             ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(OracleResultDeep)]
         _lib.oracle_eq2.restype = ctypes.c_double

@@ -300,7 +300,7 @@ int oracle_allocate(int n, const int32_t *w, uint32_t busy, int k, int m, const 
  * ------------------------------------------------------------------------ */
 typedef struct {
     int32_t status, k;
-    uint32_t device_mask;
+    uint64_t device_mask;
     int8_t mapping[16];
     int32_t m;
     int32_t used[120][2];
@@ -400,16 +400,16 @@ static void *deep_worker(void *arg) {
  * oracle_allocate.  max_subsets bounds the work (error -2 above it).  Only the
  * subsets with lex index in [sub_lo, sub_hi) are scored (bounded samples and
  * shard tests; a negative bound = unrestricted). */
-int oracle_allocate_deep(int n, const int32_t *w, uint32_t busy, int k, int m, const int32_t *pe,
+int oracle_allocate_deep(int n, const int32_t *w, uint64_t busy, int k, int m, const int32_t *pe,
                          int selector, int sensitive, int nthreads, int max_subsets, int sub_lo, int sub_hi,
                          oracle_result_deep *out) {
     memset(out, 0, sizeof(*out));
-    if (n < 1 || n > 32 || k < 1 || k > 16 || m < 0 || m > 120) return -1;
+    if (n < 1 || n > 64 || k < 1 || k > 16 || m < 0 || m > 120) return -1;
     ctx_t c;
     c.n = n; c.k = k; c.m = m; c.selector = selector; c.sensitive = sensitive; c.w = w; c.pe = pe;
     c.nf = 0;
     for (int d = 0; d < n; d++)
-        if (!((busy >> d) & 1u)) c.F[c.nf++] = d;
+        if (!((busy >> d) & 1ull)) c.F[c.nf++] = d;
     out->k = k;
     out->m = m;
     if (k > c.nf) { out->status = 1; return 0; }
@@ -466,7 +466,7 @@ int oracle_allocate_deep(int n, const int32_t *w, uint32_t busy, int k, int m, c
     if (!best.found) return 0;
     out->score = best.score;
     for (int i = 0; i < k; i++) {
-        out->device_mask |= 1u << best.S[i];
+        out->device_mask |= 1ull << best.S[i];
         out->mapping[i] = (int8_t)best.pi[i];
     }
     for (int i = 0; i < m; i++) { out->used[i][0] = best.E[i] >> 6; out->used[i][1] = best.E[i] & 63; }

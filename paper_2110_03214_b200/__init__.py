@@ -42,7 +42,7 @@ class MapaError(RuntimeError):
 
 
 class Decision(ctypes.Structure):
-    _fields_ = [("status", ctypes.c_int32), ("k", ctypes.c_int32), ("device_mask", ctypes.c_uint32),
+    _fields_ = [("status", ctypes.c_int32), ("k", ctypes.c_int32), ("device_mask", ctypes.c_uint64),
                 ("mapping", ctypes.c_int8 * 16), ("m", ctypes.c_int32), ("used", (ctypes.c_int32 * 2) * 120),
                 ("x", ctypes.c_int32), ("y", ctypes.c_int32), ("z", ctypes.c_int32),
                 ("agg_bw", ctypes.c_int32), ("preserved_bw", ctypes.c_int32), ("score", ctypes.c_int32),
@@ -62,10 +62,11 @@ class Record(ctypes.Structure):
 
 
 class WideRecord(ctypes.Structure):
-    """mapa_wide_record (deep path): 192-bit key (key, ecode_hi, ecode_lo)."""
-    _fields_ = [("key", ctypes.c_uint64), ("ecode_hi", ctypes.c_uint64), ("ecode_lo", ctypes.c_uint64),
-                ("leaves", ctypes.c_uint64), ("ctr", ctypes.c_uint32), ("lock", ctypes.c_uint32),
-                ("status", ctypes.c_uint32), ("pad", ctypes.c_uint32), ("reserved", ctypes.c_uint64 * 2)]
+    """mapa_wide_record (deep path): 256-bit key (score, set, ecode_hi, ecode_lo)."""
+    _fields_ = [("score", ctypes.c_uint64), ("set", ctypes.c_uint64), ("ecode_hi", ctypes.c_uint64),
+                ("ecode_lo", ctypes.c_uint64), ("leaves", ctypes.c_uint64), ("ctr", ctypes.c_uint32),
+                ("lock", ctypes.c_uint32), ("status", ctypes.c_uint32), ("pad", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint64)]
 
 
 class PatternInfo(ctypes.Structure):
@@ -98,10 +99,10 @@ _SIGS = {
     "mapa_load_topology": (_S, [ctypes.c_char_p, ctypes.c_int32, ctypes.POINTER(_vp)]),
     "mapa_free_topology": (None, [_vp]),
     "mapa_topology_info": (_S, [_vp, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
-                                ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_uint32)]),
-    "mapa_claim": (_S, [_vp, ctypes.c_uint32]),
-    "mapa_release": (_S, [_vp, ctypes.c_uint32]),
-    "mapa_set_busy": (_S, [_vp, ctypes.c_uint32]),
+                                ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_uint64)]),
+    "mapa_claim": (_S, [_vp, ctypes.c_uint64]),
+    "mapa_release": (_S, [_vp, ctypes.c_uint64]),
+    "mapa_set_busy": (_S, [_vp, ctypes.c_uint64]),
     "mapa_load_pattern": (_S, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.c_uint32,
                                ctypes.POINTER(_vp)]),
     "mapa_make_pattern": (_S, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_vp)]),
@@ -112,14 +113,14 @@ _SIGS = {
     "mapa_allocate": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, _vp,
                            ctypes.POINTER(Decision)]),
     "mapa_launch_query": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.c_uint32,
-                               ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, _vp]),
+                               ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, _vp]),
     "mapa_reduce_records": (_S, [ctypes.POINTER(Record), ctypes.c_int32, ctypes.POINTER(Record)]),
     "mapa_launch_query_wide": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.c_uint32,
-                                    ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, _vp]),
+                                    ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, _vp]),
     "mapa_reduce_wide_records": (_S, [ctypes.POINTER(WideRecord), ctypes.c_int32, ctypes.POINTER(WideRecord)]),
-    "mapa_decode_wide": (_S, [_vp, _vp, ctypes.c_uint32, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
+    "mapa_decode_wide": (_S, [_vp, _vp, ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
                               ctypes.POINTER(WideRecord), ctypes.POINTER(Decision)]),
-    "mapa_decode": (_S, [_vp, _vp, ctypes.c_uint32, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
+    "mapa_decode": (_S, [_vp, _vp, ctypes.c_uint64, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32,
                          ctypes.POINTER(Record), ctypes.POINTER(Decision)]),
     "mapa_allocate_batch": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int64, _vp, _vp, _vp,
                                  ctypes.c_uint32, _vp]),
@@ -224,7 +225,7 @@ class Topology:
         return self._h
 
     def info(self):
-        n, w, busy = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_uint32()
+        n, w, busy = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_uint64()
         _check(_lib.mapa_topology_info(self._h, ctypes.byref(n), ctypes.byref(w), None, ctypes.byref(busy)))
         bw = (ctypes.c_int32 * (n.value * n.value))()
         _check(_lib.mapa_topology_info(self._h, None, None, bw, None))
@@ -298,7 +299,7 @@ class Pattern:
 def decision_dict(d: Decision) -> dict:
     if d.status == NO_CAPACITY:
         return dict(status="no_capacity", raw=0, distinct=0, leaves=0, key=0)
-    devs = tuple(i for i in range(32) if (d.device_mask >> i) & 1)
+    devs = tuple(i for i in range(64) if (d.device_mask >> i) & 1)
     return dict(status="ok", devices=devs, mapping=tuple(d.mapping[i] for i in range(d.k)),
                 used_edges=[(d.used[i][0], d.used[i][1]) for i in range(d.m)],
                 x=d.x, y=d.y, z=d.z, agg_bw=d.agg_bw, preserved_bw=d.preserved_bw,
@@ -326,7 +327,7 @@ def allocate(topo: Topology, pat: Pattern, selector: int, sensitive: bool = Fals
 
 def launch_query(topo: Topology, pat: Pattern, selector: int, sensitive: bool, d_query_ptr: int,
                  d_record_ptr: int, raw: bool = False, rank: int = 0, world: int = 1,
-                 busy_hint: int = 0xFFFFFFFF, stream=None, prune: bool = False):
+                 busy_hint: int = (1 << 64) - 1, stream=None, prune: bool = False):
     """mapa_launch_query: device-resident launch (asynchronous)."""
     _check(_lib.mapa_launch_query(topo.handle, pat.handle, selector, int(bool(sensitive)), d_query_ptr,
                                   d_record_ptr, _flags(raw, prune), rank, world, busy_hint,
@@ -336,7 +337,8 @@ def launch_query(topo: Topology, pat: Pattern, selector: int, sensitive: bool, d
 def launch_query_wide(topo: Topology, pat: Pattern, selector: int, sensitive: bool, d_query_ptr: int,
                       d_record_ptr: int, busy: int, raw: bool = False, rank: int = 0, world: int = 1, stream=None):
     """mapa_launch_query_wide: deep-path device-resident launch (asynchronous);
-    busy must equal the query's busy mask (it sizes the suffix tables)."""
+    d_query_ptr -> mapa_query64; busy must equal its busy mask (it sizes the
+    suffix tables)."""
     _check(_lib.mapa_launch_query_wide(topo.handle, pat.handle, selector, int(bool(sensitive)), d_query_ptr,
                                        d_record_ptr, _flags(raw), rank, world, busy, _stream_ptr(stream)))
 

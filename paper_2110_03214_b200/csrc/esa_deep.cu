@@ -22,11 +22,13 @@
 //     suffix vertex T+l on the i-th remaining device w.r.t. the placed
 //     prefix, by popc over class masks) and a pair table wt[i][i2]; a leaf is
 //     then L + (#suffix-internal scored pairs) shared-memory reads and adds;
-//   * the argmax key is 192 bits (score << 32 | brev32(S), 128-bit edge
-//     code), compared lexicographically, so any k <= 16 fits.  It is built
-//     out of line only for a leaf whose score reaches the lane's best.  CTAs
-//     merge their best under a lock in the record (max is order independent:
-//     deterministic for every grid size and rank count).
+//   * the argmax key is 256 bits (score, brev64(S), 128-bit edge code),
+//     compared lexicographically, so any k <= 16 fits on any N <= 64.  It is
+//     built only for a leaf whose score reaches the lane's best.  CTAs merge
+//     their best under a lock in the record (max is order independent:
+//     deterministic for every grid size and rank count);
+//   * device masks are a template type: u32 for N <= 32, u64 for N <= 64
+//     (SURVEY §8(f) NEXT 4); only per-node work touches them.
 // Scores are the narrow path's (integer): Eq. 1 AggBW, Eq. 2 as
 // the dense rank of the census (host table, reading A9 holds for
 // m <= 120), Eq. 3 PreservedBW = T_F - sum inc_F(S) + inside(S).
@@ -42,24 +44,25 @@ constexpr int kBlockD = 256;
 constexpr int kWarpsD = kBlockD / 32;
 constexpr int kMaxDecodeD = 6;
 constexpr int kMaxL = 4;
-// per-warp term area (ints): pt[l][i] at l*32 + i, the pair table at
+constexpr int kND = kMaxNDeep;
+// per-warp term area (ints): pt[l][i] at l*64 + i, the pair table at
 // kWtOff + i*kWtStride + i2 (odd stride: fewer bank conflicts), a zero at kZeroOff
-constexpr int kWtOff = 128, kWtStride = 17, kZeroOff = 400, kAreaInts = 404;
+constexpr int kWtOff = 256, kWtStride = 17, kZeroOff = 528, kAreaInts = 532;
 
 struct DeepWarp {
     int area[kAreaInts];
-    int dl[32];      // remaining free devices, ascending
+    int dl[kND];     // remaining free devices, ascending
     int fw[16];      // f(j) of the placed prefix (read by the key builder)
 };
 
 struct DeepShared {
-    uint4 tup[kMaxTup];     // x: byte l = 4 i_l; y, z, w: 16-bit byte offsets of the NT terms into area
-    uint4 cm[kMaxN];
-    int tw[kMaxN * kMaxN];  // [v*32 + b] pair value: w(v,b) (Eq. 1/3), census delta (Eq. 2), 0 if v == b
-    int incF[kMaxN];        // inc_F(v) (Eq. 3)
-    uint32_t magic[kMaxN + 4];
+    uint4 tup[kMaxTup];        // x: byte l = i_l; y, z, w: 16-bit byte offsets of the NT terms into area
+    unsigned long long cm[kND][3];
+    int tw[kND * kND];         // [v*64 + b] pair value: w(v,b) (Eq. 1/3), census delta (Eq. 2), 0 if v == b
+    int incF[kND];             // inc_F(v) (Eq. 3)
+    uint32_t magic[kND + 4];
     DeepWarp w[kWarpsD];
-    unsigned long long rk[kWarpsD][4];
+    unsigned long long rk[kWarpsD][5];
 };
 
 // dynamic shared memory: DeepShared + the Eq. 2 rank table (u16, (m+1)^2 <= 121^2)
@@ -69,17 +72,33 @@ extern __shared__ __align__(16) unsigned char g_dsmem[];
 __device__ __forceinline__ DeepShared &dsh() { return *reinterpret_cast<DeepShared *>(g_dsmem); }
 __device__ __forceinline__ uint16_t *dlut() { return reinterpret_cast<uint16_t *>(g_dsmem + sizeof(DeepShared)); }
 
-struct DBest {
-    unsigned long long hi;   // score << 32 | brev32(S); 0 = none
-    unsigned long long ehi, elo;
-};
-
-__device__ __forceinline__ bool key_gt(unsigned long long a0, unsigned long long a1, unsigned long long a2,
-                                       unsigned long long b0, unsigned long long b1, unsigned long long b2) {
-    return a0 != b0 ? a0 > b0 : (a1 != b1 ? a1 > b1 : a2 > b2);
+// ---- mask helpers (M = uint32_t for N <= 32, unsigned long long for N <= 64)
+template <typename M> __device__ __forceinline__ int popc(M m);
+template <> __device__ __forceinline__ int popc<uint32_t>(uint32_t m) { return __popc(m); }
+template <> __device__ __forceinline__ int popc<unsigned long long>(unsigned long long m) { return __popcll(m); }
+template <typename M> __device__ __forceinline__ int lowbit(M m);
+template <> __device__ __forceinline__ int lowbit<uint32_t>(uint32_t m) { return __ffs(m) - 1; }
+template <> __device__ __forceinline__ int lowbit<unsigned long long>(unsigned long long m) { return __ffsll(m) - 1; }
+template <typename M> __device__ __forceinline__ M bit(int d) { return M(1) << d; }
+template <typename M> __device__ __forceinline__ M below(int d) { return (M(1) << d) - M(1); }  // d < width
+// devices above d (d = -1: all)
+template <typename M> __device__ __forceinline__ M above(int d) {
+    constexpr int W = 8 * (int)sizeof(M);
+    return d < 0 ? ~M(0) : (d + 1 >= W ? M(0) : (~M(0) << (d + 1)));
+}
+// devices up to and including d
+template <typename M> __device__ __forceinline__ M upto(int d) {
+    constexpr int W = 8 * (int)sizeof(M);
+    return d + 1 >= W ? ~M(0) : ((M(1) << (d + 1)) - M(1));
+}
+template <typename M> __device__ __forceinline__ M reduce_or(M v);
+template <> __device__ __forceinline__ uint32_t reduce_or<uint32_t>(uint32_t v) { return __reduce_or_sync(kFullD, v); }
+template <> __device__ __forceinline__ unsigned long long reduce_or<unsigned long long>(unsigned long long v) {
+    const uint32_t lo = __reduce_or_sync(kFullD, (uint32_t)v), hi = __reduce_or_sync(kFullD, (uint32_t)(v >> 32));
+    return ((unsigned long long)hi << 32) | lo;
 }
 
-__device__ __forceinline__ uint32_t nth_set_d(uint32_t m, uint32_t n) {
+__device__ __forceinline__ uint32_t nth_set32(uint32_t m, uint32_t n) {
     uint32_t pos = 0, c;
     c = __popc(m & 0xFFFFu); if (n >= c) { n -= c; m >>= 16; pos += 16; }
     c = __popc(m & 0xFFu);   if (n >= c) { n -= c; m >>= 8;  pos += 8; }
@@ -88,6 +107,24 @@ __device__ __forceinline__ uint32_t nth_set_d(uint32_t m, uint32_t n) {
     c = m & 1u;              if (n >= c) { pos += 1; }
     return pos;
 }
+template <typename M> __device__ __forceinline__ uint32_t nth_set(M m, uint32_t n);
+template <> __device__ __forceinline__ uint32_t nth_set<uint32_t>(uint32_t m, uint32_t n) { return nth_set32(m, n); }
+template <> __device__ __forceinline__ uint32_t nth_set<unsigned long long>(unsigned long long m, uint32_t n) {
+    const uint32_t lo = (uint32_t)m, c = (uint32_t)__popc(lo);
+    return n < c ? nth_set32(lo, n) : 32u + nth_set32((uint32_t)(m >> 32), n - c);
+}
+
+struct DBest {
+    uint32_t score;
+    unsigned long long set;  // brev64(S); 0 = none
+    unsigned long long ehi, elo;
+};
+
+__device__ __forceinline__ bool key_gt(uint32_t s0, unsigned long long a0, unsigned long long a1,
+                                       unsigned long long a2, uint32_t s1, unsigned long long b0,
+                                       unsigned long long b1, unsigned long long b2) {
+    return s0 != s1 ? s0 > s1 : (a0 != b0 ? a0 > b0 : (a1 != b1 ? a1 > b1 : a2 > b2));
+}
 
 // A leaf whose (scaled) score reached the lane's threshold.  Builds the device
 // set, and (unless the set alone decides) the 128-bit edge code: pattern edge
@@ -95,30 +132,31 @@ __device__ __forceinline__ uint32_t nth_set_d(uint32_t m, uint32_t n) {
 // in lex order over C(k,2) -> bit C(k,2)-1-p.  Updates the lane's best key
 // and threshold.
 __device__ __forceinline__ void consider_deep(const DeepTables &tb, const DeepWarp &W, DBest &b, int &thr,
-                                              uint32_t s, uint32_t U, uint32_t x, int T) {
+                                              uint32_t s, unsigned long long U, uint32_t x, int T) {
     const int L = tb.L;
-    uint32_t S = U;
+    unsigned long long S = U;
 #pragma unroll
     for (int l = 0; l < kMaxL; ++l)
-        if (l < L) S |= 1u << (uint32_t)W.dl[((x >> (8 * l)) & 0xFFu) >> 2];
-    const unsigned long long hi = ((unsigned long long)s << 32) | __brev(S);
-    if (hi < b.hi) return;
-    if (hi == b.hi && tb.clique) return;  // same set of a clique: same edges
+        if (l < L) S |= 1ull << W.dl[(x >> (8 * l)) & 0xFFu];
+    const unsigned long long set = __brevll(S);
+    if (s < b.score || (s == b.score && set < b.set)) return;
+    if (s == b.score && set == b.set && tb.clique) return;  // same set of a clique: same edges
     const int k = tb.k, eb = tb.eb;
     unsigned long long ehi = 0, elo = 0;
     for (int e = 0; e < tb.m; ++e) {
         const int a = tb.edge[e] & 15, c = tb.edge[e] >> 4;
-        const uint32_t da = a < T ? (uint32_t)W.fw[a] : (uint32_t)W.dl[((x >> (8 * (a - T))) & 0xFFu) >> 2];
-        const uint32_t dc = c < T ? (uint32_t)W.fw[c] : (uint32_t)W.dl[((x >> (8 * (c - T))) & 0xFFu) >> 2];
-        const int ra = __popc(S & ((1u << da) - 1u)), rc = __popc(S & ((1u << dc) - 1u));
+        const int da = a < T ? W.fw[a] : W.dl[(x >> (8 * (a - T))) & 0xFFu];
+        const int dc = c < T ? W.fw[c] : W.dl[(x >> (8 * (c - T))) & 0xFFu];
+        const int ra = __popcll(S & ((1ull << da) - 1ull)), rc = __popcll(S & ((1ull << dc) - 1ull));
         const int lo = min(ra, rc), hi2 = max(ra, rc);
         const int p = lo * (2 * k - lo - 1) / 2 + (hi2 - lo - 1);
         const int q = eb - 1 - p;
         if (q >= 64) ehi |= 1ull << (q - 64);
         else elo |= 1ull << q;
     }
-    if (key_gt(hi, ehi, elo, b.hi, b.ehi, b.elo)) {
-        b.hi = hi;
+    if (key_gt(s, set, ehi, elo, b.score, b.set, b.ehi, b.elo)) {
+        b.score = s;
+        b.set = set;
         b.ehi = ehi;
         b.elo = elo;
         thr = (int)s * tb.scale;
@@ -129,86 +167,81 @@ __device__ __forceinline__ void consider_deep(const DeepTables &tb, const DeepWa
 // prefix f(lane) for lane < d.  Eq. 1: back-neighbours of d; Eq. 3: every
 // placed vertex, minus inc_F(v); Eq. 2: census delta; Baseline: 0.
 template <int SEL>
-__device__ __forceinline__ int place_inc(const DeepTables &tb, int d, uint32_t v, uint32_t myf, int lane) {
+__device__ __forceinline__ int place_inc(const DeepTables &tb, int d, int v, int myf, int lane) {
     constexpr int base = SEL & 3;
     if constexpr (base == SEL_BASE) return 0;
     int c = 0;
     const bool e = base == SEL_INSENS ? true : ((tb.back[d] >> lane) & 1u) != 0;
-    if (lane < d && e) c = dsh().tw[myf * 32 + v];
+    if (lane < d && e) c = dsh().tw[myf * kND + v];
     int s = __reduce_add_sync(kFullD, c);
     if constexpr (base == SEL_INSENS) s -= dsh().incF[v];
     return s;
 }
 
 // Canonical mode: devices allowed for vertex d by its lex-leader sources.
-template <int SEL>
-__device__ __forceinline__ uint32_t allowed(const DeepTables &tb, int d, uint32_t myf, int lane) {
-    if constexpr (!(SEL & 4)) return kFullD;
-    const int c = (lane < d && ((tb.src[d] >> lane) & 1u)) ? (int)myf : -1;
-    const int lb = __reduce_max_sync(kFullD, c);
-    return lb < 0 ? kFullD : (0xFFFFFFFEu << lb);
+template <typename M, int SEL>
+__device__ __forceinline__ M allowed(const DeepTables &tb, int d, int myf, int lane) {
+    if constexpr (!(SEL & 4)) return ~M(0);
+    const int c = (lane < d && ((tb.src[d] >> lane) & 1u)) ? myf : -1;
+    return above<M>(__reduce_max_sync(kFullD, c));
 }
 
 // All leaves below a node whose prefix 0..T-1 is placed (set U, score A).
-template <int NT, int SEL>
-__device__ __forceinline__ void suffix(const DeepTables &tb, uint32_t F, uint32_t U, int A, uint32_t myf, int lane,
-                                       int warp, int T, DBest &bst, int &thr, unsigned long long &cnt) {
+template <typename M, int NT, int SEL>
+__device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, int myf, int lane, int warp, int T,
+                                       DBest &bst, int &thr, unsigned long long &cnt) {
     constexpr int base = SEL & 3;
     constexpr bool canon = (SEL & 4) != 0;
     DeepShared &S = dsh();
     DeepWarp &W = S.w[warp];
     const int L = tb.L;
-    uint32_t R = F & ~U;
+    M R = F & ~U;
     if constexpr (canon) {
         // lower bound shared by every suffix vertex: drop the devices below it
-        if (tb.pcommon) {
-            const int lb = __reduce_max_sync(kFullD, (lane < T && ((tb.pcommon >> lane) & 1)) ? (int)myf : -1);
-            R &= 0xFFFFFFFEu << lb;
-        }
+        if (tb.pcommon) R &= above<M>(__reduce_max_sync(kFullD, (lane < T && ((tb.pcommon >> lane) & 1)) ? myf : -1));
     }
-    const int r = __popc(R);
+    const int r = popc<M>(R);
     __syncwarp();  // previous readers of dl / area are done
-    if ((R >> lane) & 1u) W.dl[__popc(R & ((1u << lane) - 1u))] = lane;
-    uint32_t X[kMaxL];
+#pragma unroll
+    for (int h = 0; h < (int)sizeof(M) / 4; ++h) {
+        const int dv = lane + 32 * h;
+        if ((R >> dv) & 1u) W.dl[popc<M>(R & below<M>(dv))] = dv;
+    }
+    M X[kMaxL];
     uint32_t MINI = 0;
 #pragma unroll
     for (int l = 0; l < kMaxL; ++l) {
         X[l] = 0;
         if (l < L) {
             const int u = T + l;
-            if constexpr (base == SEL_INSENS) {
-                X[l] = U;
-            } else {
-                X[l] = __reduce_or_sync(kFullD, (lane < T && ((tb.back[u] >> lane) & 1u)) ? (1u << myf) : 0u);
-            }
+            if constexpr (base == SEL_INSENS) X[l] = U;
+            else X[l] = reduce_or<M>((lane < T && ((tb.back[u] >> lane) & 1u)) ? bit<M>(myf) : M(0));
             if constexpr (canon) {
                 if (tb.pcon) {
-                    const int lb = __reduce_max_sync(
-                        kFullD, (lane < T && ((tb.src[u] & ~tb.pcommon) >> lane) & 1u) ? (int)myf : -1);
-                    const uint32_t mi = lb < 0 ? 0u : (uint32_t)__popc(R & ((2u << lb) - 1u));
-                    MINI |= (4u * mi) << (8 * l);
+                    const int lb = __reduce_max_sync(kFullD, (lane < T && ((tb.src[u] & ~tb.pcommon) >> lane) & 1u) ? myf : -1);
+                    const uint32_t mi = lb < 0 ? 0u : (uint32_t)popc<M>(R & upto<M>(lb));
+                    MINI |= mi << (8 * l);
                 }
             }
         }
     }
     __syncwarp();
-    if (lane < r) {
-        const int dev = W.dl[lane];
-        const uint4 c = S.cm[dev];
+    for (int i = lane; i < r; i += 32) {
+        const int dev = W.dl[i];
+        const M c0 = (M)S.cm[dev][0], c1 = (M)S.cm[dev][1], c2 = (M)S.cm[dev][2];
 #pragma unroll
         for (int l = 0; l < kMaxL; ++l) {
             if (l < L) {
                 int v;
                 if constexpr (base == SEL_SENS) {
-                    v = __popc(c.x & X[l]) * tb.xsd + __popc((c.y | c.z) & X[l]);
+                    v = popc<M>(c0 & X[l]) * tb.xsd + popc<M>((c1 | c2) & X[l]);
                 } else if constexpr (base == SEL_BASE) {
                     v = 0;
                 } else {
-                    v = 12 * __popc(X[l]) + 38 * __popc(c.x & X[l]) + 13 * __popc(c.y & X[l]) +
-                        8 * __popc(c.z & X[l]);
+                    v = 12 * popc<M>(X[l]) + 38 * popc<M>(c0 & X[l]) + 13 * popc<M>(c1 & X[l]) + 8 * popc<M>(c2 & X[l]);
                     if constexpr (base == SEL_INSENS) v -= S.incF[dev];
                 }
-                W.area[32 * l + lane] = v;
+                W.area[kND * l + i] = v;
             }
         }
     }
@@ -223,7 +256,7 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, uint32_t F, uint32_
         for (int p = lane; p < r * 16; p += 32) {
             const int i = p >> 4, i2 = p & 15;
             if (i2 < r) {
-                int v = S.tw[W.dl[i] * 32 + W.dl[i2]];
+                int v = S.tw[W.dl[i] * kND + W.dl[i2]];
                 if (fold) v = sc * v + W.area[i] + W.area[i2];
                 W.area[kWtOff + i * kWtStride + i2] = v;
             }
@@ -254,7 +287,7 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, uint32_t F, uint32_
         if (valid && s >= thr) {
             const int sc = tb.scale;
             const uint32_t sr = sc == 1 ? (uint32_t)s : (sc == 2 ? (uint32_t)s >> 1 : (uint32_t)s / 3u);
-            consider_deep(tb, W, bst, thr, sr, U, e.x, T);
+            consider_deep(tb, W, bst, thr, sr, (unsigned long long)U, e.x, T);
         }
     }
     if (!canon || !tb.pcon) cnt += (unsigned long long)nt;
@@ -266,24 +299,28 @@ __device__ __forceinline__ uint32_t perm_count_d(int n, int d) {
     return p;
 }
 
-template <int NT, int SEL>
+template <typename M, int NT, int SEL>
 __global__ void __launch_bounds__(kBlockD, 3)
-esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut_g, const mapa_query *__restrict__ dq,
-         mapa_wide_record *__restrict__ rec, int D, int rank, int world, int stripe) {
+esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut_g,
+         const mapa_query64 *__restrict__ dq, mapa_wide_record *__restrict__ rec, int D, int rank, int world,
+         int stripe) {
     constexpr int base = SEL & 3;
     constexpr bool canon = (SEL & 4) != 0;
     DeepShared &S = dsh();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = tb.n;
-    const uint32_t nmask = n >= 32 ? kFullD : ((1u << n) - 1u);
-    const uint32_t F = ~dq->busy & nmask;
-    const int nF = __popc(F);
+    const M F = (M)(~dq->busy) & (n >= 8 * (int)sizeof(M) ? ~M(0) : below<M>(n));
+    const int nF = popc<M>(F);
     const int T = tb.T;
-    if (tid < kMaxN) S.cm[tid] = make_uint4(tb.cm[tid][0], tb.cm[tid][1], tb.cm[tid][2], tb.cm[tid][3]);
-    if (tid <= kMaxN) S.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
+    if (tid < kND) {
+        S.cm[tid][0] = tb.cm[tid][0];
+        S.cm[tid][1] = tb.cm[tid][1];
+        S.cm[tid][2] = tb.cm[tid][2];
+    }
+    if (tid <= kND) S.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
     if (lane == 0) S.w[warp].area[kZeroOff] = 0;
-    for (int i = tid; i < kMaxN * kMaxN; i += kBlockD) {
-        const int v = i >> 5, b = i & 31;
+    for (int i = tid; i < kND * kND; i += kBlockD) {
+        const int v = i / kND, b = i % kND;
         int val = 0;
         if (v != b && v < n && b < n) {
             const int cls = ((tb.cm[b][0] >> v) & 1u) ? 0 : ((tb.cm[b][1] >> v) & 1u) ? 1 : ((tb.cm[b][2] >> v) & 1u) ? 2 : 3;
@@ -298,8 +335,8 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
         uint32_t wd[3] = {kZeroOff * 4u * 0x10001u, kZeroOff * 4u * 0x10001u, kZeroOff * 4u * 0x10001u};
         for (int q = 0; q < tb.nterm; ++q) {
             const int a = tb.term[q][1], b = tb.term[q][2];
-            const uint32_t ia = ((x >> (8 * a)) & 0xFFu) >> 2, ib = ((x >> (8 * b)) & 0xFFu) >> 2;
-            const uint32_t off = 4u * (tb.term[q][0] == 0 ? (uint32_t)(32 * a) + ia : kWtOff + ia * kWtStride + ib);
+            const uint32_t ia = (x >> (8 * a)) & 0xFFu, ib = (x >> (8 * b)) & 0xFFu;
+            const uint32_t off = 4u * (tb.term[q][0] == 0 ? (uint32_t)(kND * a) + ia : kWtOff + ia * kWtStride + ib);
             const int sh = 16 * (q & 1);
             wd[q >> 1] = (wd[q >> 1] & ~(0xFFFFu << sh)) | (off << sh);
         }
@@ -307,17 +344,17 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
     }
     if constexpr (base == SEL_SENS)
         for (int i = tid; i < tb.xsd * tb.xsd; i += kBlockD) dlut()[i] = lut_g[i];
-    if (tid < kMaxN) {
+    if (tid < kND) {
         int inc = 0;
-        if (((F >> tid) & 1u) && tid < n)
-            inc = 12 * (nF - 1) + 38 * __popc(tb.cm[tid][0] & F) + 13 * __popc(tb.cm[tid][1] & F) +
-                  8 * __popc(tb.cm[tid][2] & F);
+        if (tid < n && ((F >> tid) & 1u))
+            inc = 12 * (nF - 1) + 38 * popc<M>((M)tb.cm[tid][0] & F) + 13 * popc<M>((M)tb.cm[tid][1] & F) +
+                  8 * popc<M>((M)tb.cm[tid][2] & F);
         S.incF[tid] = inc;
     }
     if (tid == 0 && nF != tb.r + T && tb.k <= nF) atomicOr(&rec->status, 2u);  // busy_hint mismatch
     __syncthreads();
     int acc0 = 0;
-    if constexpr (base == SEL_INSENS) acc0 = __reduce_add_sync(kFullD, S.incF[lane]) / 2;  // T_F
+    if constexpr (base == SEL_INSENS) acc0 = __reduce_add_sync(kFullD, S.incF[lane] + S.incF[lane + 32]) / 2;  // T_F
 
     // Rank-local item space and guided self-scheduling, as the narrow kernel.
     const bool okq = tb.k <= nF && nF == tb.r + T;
@@ -328,11 +365,11 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
     const bool ownLast = nS > 0 && ((nS - 1u) % (uint32_t)world) == (uint32_t)rank;
     const uint32_t Nloc = myS == 0 ? 0u : (ownLast ? (myS - 1u) * Ls + (N - (nS - 1u) * Ls) : myS * Ls);
     const uint32_t P = gridDim.x * (uint32_t)kWarpsD;
-    DBest bst{0ull, 0ull, 0ull};
+    DBest bst{0u, 0ull, 0ull, 0ull};
     int thr = 0;
     unsigned long long cnt = 0;
-    uint32_t myf = 0, mycand = 0;
-    int myacc = 0;
+    int myf = 0, myacc = 0;
+    M mycand = 0;
     for (;;) {
         uint32_t start = 0, sz = 0;
         if (lane == 0) {
@@ -365,76 +402,81 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
                     dg[q] = 0;
                 }
             }
-            uint32_t U = 0;
+            M U = 0;
             int acc = acc0;
             bool ok = true;
 #pragma unroll
             for (int q = 0; q < kMaxDecodeD; ++q) {
                 if (q < D) {
-                    const uint32_t v = nth_set_d(F & ~U, dg[q]);
-                    if (canon && !((allowed<SEL>(tb, q, myf, lane) >> v) & 1u)) { ok = false; break; }
+                    const int v = (int)nth_set<M>(F & ~U, dg[q]);
+                    if (canon && !((allowed<M, SEL>(tb, q, myf, lane) >> v) & 1u)) { ok = false; break; }
                     acc += place_inc<SEL>(tb, q, v, myf, lane);
                     if (lane == q) { myf = v; myacc = acc; }
-                    if (lane == 0) S.w[warp].fw[q] = (int)v;
-                    U |= 1u << v;
+                    if (lane == 0) S.w[warp].fw[q] = v;
+                    U |= bit<M>(v);
                 }
             }
             if (!ok) continue;
             if (D == T) {
-                suffix<NT, SEL>(tb, F, U, acc, myf, lane, warp, T, bst, thr, cnt);
+                suffix<M, NT, SEL>(tb, F, U, acc, myf, lane, warp, T, bst, thr, cnt);
                 continue;
             }
             // explicit-stack DFS over levels D..T-1 (lane d holds level d)
             int d = D;
-            uint32_t cand = F & ~U & allowed<SEL>(tb, d, myf, lane);
+            M cand = F & ~U & allowed<M, SEL>(tb, d, myf, lane);
             for (;;) {
                 if (cand == 0) {
                     if (d == D) break;
                     --d;
-                    const uint32_t v = __shfl_sync(kFullD, myf, d);
-                    U &= ~(1u << v);
+                    const int v = __shfl_sync(kFullD, myf, d);
+                    U &= ~bit<M>(v);
                     cand = __shfl_sync(kFullD, mycand, d);
                     continue;
                 }
-                const uint32_t v = __ffs(cand) - 1;
-                cand &= cand - 1u;
+                const int v = lowbit<M>(cand);
+                cand &= cand - M(1);
                 const int accp = d == 0 ? acc0 : __shfl_sync(kFullD, myacc, d - 1);
                 const int a = accp + place_inc<SEL>(tb, d, v, myf, lane);
                 if (lane == d) { myf = v; mycand = cand; myacc = a; }
-                if (lane == 0) S.w[warp].fw[d] = (int)v;
-                U |= 1u << v;
+                if (lane == 0) S.w[warp].fw[d] = v;
+                U |= bit<M>(v);
                 if (d + 1 == T) {
-                    suffix<NT, SEL>(tb, F, U, a, myf, lane, warp, T, bst, thr, cnt);
-                    U &= ~(1u << v);
+                    suffix<M, NT, SEL>(tb, F, U, a, myf, lane, warp, T, bst, thr, cnt);
+                    U &= ~bit<M>(v);
                 } else {
                     ++d;
-                    cand = F & ~U & allowed<SEL>(tb, d, myf, lane);
+                    cand = F & ~U & allowed<M, SEL>(tb, d, myf, lane);
                 }
             }
         }
     }
-    // warp / block / grid lexicographic max of the 192-bit key
-    unsigned long long h = bst.hi, e1 = bst.ehi, e0 = bst.elo;
+    // warp / block / grid lexicographic max of the 256-bit key
+    uint32_t hs = bst.score;
+    unsigned long long h = bst.set, e1 = bst.ehi, e0 = bst.elo;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t s2 = __shfl_xor_sync(kFullD, hs, o);
         const unsigned long long h2 = __shfl_xor_sync(kFullD, h, o);
         const unsigned long long a2 = __shfl_xor_sync(kFullD, e1, o);
         const unsigned long long b2 = __shfl_xor_sync(kFullD, e0, o);
-        if (key_gt(h2, a2, b2, h, e1, e0)) { h = h2; e1 = a2; e0 = b2; }
+        if (key_gt(s2, h2, a2, b2, hs, h, e1, e0)) { hs = s2; h = h2; e1 = a2; e0 = b2; }
     }
     if (lane == 0) {
-        S.rk[warp][0] = h;
-        S.rk[warp][1] = e1;
-        S.rk[warp][2] = e0;
-        S.rk[warp][3] = cnt;
+        S.rk[warp][0] = hs;
+        S.rk[warp][1] = h;
+        S.rk[warp][2] = e1;
+        S.rk[warp][3] = e0;
+        S.rk[warp][4] = cnt;
     }
     __syncthreads();
     if (tid == 0) {
         unsigned long long c = 0;
-        h = 0; e1 = 0; e0 = 0;
+        hs = 0; h = 0; e1 = 0; e0 = 0;
         for (int w = 0; w < kWarpsD; ++w) {
-            c += S.rk[w][3];
-            if (key_gt(S.rk[w][0], S.rk[w][1], S.rk[w][2], h, e1, e0)) { h = S.rk[w][0]; e1 = S.rk[w][1]; e0 = S.rk[w][2]; }
+            c += S.rk[w][4];
+            if (key_gt((uint32_t)S.rk[w][0], S.rk[w][1], S.rk[w][2], S.rk[w][3], hs, h, e1, e0)) {
+                hs = (uint32_t)S.rk[w][0]; h = S.rk[w][1]; e1 = S.rk[w][2]; e0 = S.rk[w][3];
+            }
         }
         if (c) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->leaves), c);
         if (h) {
@@ -442,10 +484,11 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
             }
             __threadfence();
             volatile unsigned long long *r = reinterpret_cast<volatile unsigned long long *>(rec);
-            if (key_gt(h, e1, e0, r[0], r[1], r[2])) {
-                r[0] = h;
-                r[1] = e1;
-                r[2] = e0;
+            if (r[1] == 0 || key_gt(hs, h, e1, e0, (uint32_t)r[0], r[1], r[2], r[3])) {
+                r[0] = hs;
+                r[1] = h;
+                r[2] = e1;
+                r[3] = e0;
             }
             __threadfence();
             atomicExch(&rec->lock, 0u);
@@ -453,82 +496,87 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
     }
 }
 
-template <int NT, int SEL>
-int launch_t(const DeepTables &tb, const uint16_t *lut, const mapa_query *dq, mapa_wide_record *rec, int D, int rank,
-             int world, int stripe, int grid, int smem, cudaStream_t st) {
+template <typename M, int NT, int SEL>
+int launch_t(const DeepTables &tb, const uint16_t *lut, const mapa_query64 *dq, mapa_wide_record *rec, int D,
+             int rank, int world, int stripe, int grid, int smem, cudaStream_t st) {
     // the attribute is always the fixed upper bound, so occupancy queries and
     // launches agree
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute((const void *)esa_deep<NT, SEL>,
+        cudaError_t e = cudaFuncSetAttribute((const void *)esa_deep<M, NT, SEL>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmemMax);
         if (e != cudaSuccess) return (int)e;
         configured = true;
     }
     if (smem > kDeepSmemMax) return (int)cudaErrorInvalidValue;
-    esa_deep<NT, SEL><<<grid, kBlockD, smem, st>>>(tb, lut, dq, rec, D, rank, world, stripe);
+    esa_deep<M, NT, SEL><<<grid, kBlockD, smem, st>>>(tb, lut, dq, rec, D, rank, world, stripe);
     return (int)cudaGetLastError();
 }
 
-template <int NT, int SEL>
-const void *fn_t() { return (const void *)esa_deep<NT, SEL>; }
+using DeepFn = int (*)(const DeepTables &, const uint16_t *, const mapa_query64 *, mapa_wide_record *, int, int,
+                       int, int, int, int, cudaStream_t);
 
-using DeepFn = int (*)(const DeepTables &, const uint16_t *, const mapa_query *, mapa_wide_record *, int, int, int,
-                       int, int, int, cudaStream_t);
-
-template <int NT>
+template <typename M, int NT>
 DeepFn pick_sel(int sc) {
     switch (sc & 7) {
-        case 0: return launch_t<NT, 0>;
-        case 1: return launch_t<NT, 1>;
-        case 2: return launch_t<NT, 2>;
-        case 3: return launch_t<NT, 3>;
-        case 4: return launch_t<NT, 4>;
-        case 5: return launch_t<NT, 5>;
-        case 6: return launch_t<NT, 6>;
-        default: return launch_t<NT, 7>;
+        case 0: return launch_t<M, NT, 0>;
+        case 1: return launch_t<M, NT, 1>;
+        case 2: return launch_t<M, NT, 2>;
+        case 3: return launch_t<M, NT, 3>;
+        case 4: return launch_t<M, NT, 4>;
+        case 5: return launch_t<M, NT, 5>;
+        case 6: return launch_t<M, NT, 6>;
+        default: return launch_t<M, NT, 7>;
     }
 }
 
-template <int NT>
+template <typename M, int NT>
 const void *pick_fn_sel(int sc) {
     switch (sc & 7) {
-        case 0: return fn_t<NT, 0>();
-        case 1: return fn_t<NT, 1>();
-        case 2: return fn_t<NT, 2>();
-        case 3: return fn_t<NT, 3>();
-        case 4: return fn_t<NT, 4>();
-        case 5: return fn_t<NT, 5>();
-        case 6: return fn_t<NT, 6>();
-        default: return fn_t<NT, 7>();
+        case 0: return (const void *)esa_deep<M, NT, 0>;
+        case 1: return (const void *)esa_deep<M, NT, 1>;
+        case 2: return (const void *)esa_deep<M, NT, 2>;
+        case 3: return (const void *)esa_deep<M, NT, 3>;
+        case 4: return (const void *)esa_deep<M, NT, 4>;
+        case 5: return (const void *)esa_deep<M, NT, 5>;
+        case 6: return (const void *)esa_deep<M, NT, 6>;
+        default: return (const void *)esa_deep<M, NT, 7>;
     }
 }
 
 // compile-time term count: the smallest of {2, 4, 6} >= nterm (padding terms read a zero)
 inline int nt_class(int nterm) { return nterm <= 2 ? 2 : (nterm <= 4 ? 4 : 6); }
 
+template <typename M>
+DeepFn pick(int nterm, int sc) {
+    switch (nt_class(nterm)) {
+        case 2: return pick_sel<M, 2>(sc);
+        case 4: return pick_sel<M, 4>(sc);
+        default: return pick_sel<M, 6>(sc);
+    }
+}
+
+template <typename M>
+const void *pick_fn(int nterm, int sc) {
+    switch (nt_class(nterm)) {
+        case 2: return pick_fn_sel<M, 2>(sc);
+        case 4: return pick_fn_sel<M, 4>(sc);
+        default: return pick_fn_sel<M, 6>(sc);
+    }
+}
+
 }  // namespace
 
-int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_query *d_query,
+int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_query64 *d_query,
                 mapa_wide_record *d_record, int depth, int rank, int world, int stripe, int grid, void *stream) {
     const int smem = (int)sizeof(DeepShared) + ((sc & 3) == SEL_SENS ? 2 * tb.xsd * tb.xsd : 0);
     if (tb.nterm > kDeepMaxTerms || tb.L < 1 || tb.L > kMaxL) return (int)cudaErrorInvalidValue;
-    DeepFn f = nullptr;
-    switch (nt_class(tb.nterm)) {
-        case 2: f = pick_sel<2>(sc); break;
-        case 4: f = pick_sel<4>(sc); break;
-        default: f = pick_sel<6>(sc); break;
-    }
+    DeepFn f = tb.n <= 32 ? pick<uint32_t>(tb.nterm, sc) : pick<unsigned long long>(tb.nterm, sc);
     return f(tb, d_lut, d_query, d_record, depth, rank, world, stripe, grid, smem, (cudaStream_t)stream);
 }
 
-int max_blocks_per_sm_deep(int nterm, int sc, int lut_bytes) {
-    const void *f = nullptr;
-    switch (nt_class(nterm)) {
-        case 2: f = pick_fn_sel<2>(sc); break;
-        case 4: f = pick_fn_sel<4>(sc); break;
-        default: f = pick_fn_sel<6>(sc); break;
-    }
+int max_blocks_per_sm_deep(int n, int nterm, int sc, int lut_bytes) {
+    const void *f = n <= 32 ? pick_fn<uint32_t>(nterm, sc) : pick_fn<unsigned long long>(nterm, sc);
     const int smem = (int)sizeof(DeepShared) + lut_bytes;
     if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmemMax) != cudaSuccess) return 1;
     int nb = 0;

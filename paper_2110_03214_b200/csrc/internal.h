@@ -15,10 +15,11 @@
 namespace mapa {
 
 constexpr int kMaxK = 8;        // narrow path (packed 63-bit key)
-constexpr int kMaxKDeep = 16;   // deep path (192-bit key)
+constexpr int kMaxKDeep = 16;   // deep path (256-bit key)
 constexpr int kMaxEdges = 120;  // C(16,2)
 constexpr int kMaxTup = 2048;   // deep path: suffix index tuples per launch
-constexpr int kMaxN = 32;
+constexpr int kMaxN = 32;        // narrow path (u32 masks)
+constexpr int kMaxNDeep = 64;   // deep path (u64 masks)
 constexpr int kMaxPats = 16;      // patterns per batch / trace launch
 constexpr int kLutCapSingle = 1024;  // (m+1)^2 <= 841 for m <= 28
 constexpr int kLutCapMulti = 4096;
@@ -87,13 +88,13 @@ struct LaunchCfg {
 
 // Deep path (k <= 16): a warp-uniform DFS places vertices 0..T-1 (T = k - L),
 // then the lanes scan a table of L-tuples of indices into the r remaining free
-// devices (sorted), one tuple per lane.  Tuple word: byte l = 4 * i_l.  The
+// devices (sorted), one tuple per lane.  Tuple word: byte l = i_l.  The
 // score of a tuple is A + the sum of NT "terms", each one read of the warp's
 // per-node table: a partial pt[l][i_l] (suffix vertex T+l against the placed
 // prefix) or a pair value wt[i_a][i_b] (a scored suffix-internal pair).
 constexpr int kDeepMaxTerms = 6;
 struct DeepTables {
-    uint32_t cm[kMaxN][4];   // class masks, as DevTopo
+    uint64_t cm[kMaxNDeep][3];  // cm[v][c] = {u != v : class(u, v) == c}, c = 0 (50), 1 (25), 2 (20)
     int32_t n;
     int32_t k, m, L, T, r;   // r = free devices left for the suffix at every node
     int32_t ntup;            // valid tuples (suffix-internal lex-leader constraints applied)
@@ -107,7 +108,7 @@ struct DeepTables {
     int32_t nterm;           // terms per tuple (<= kDeepMaxTerms)
     uint8_t term[kDeepMaxTerms][3];  // (kind 0: pt of suffix vertex a | kind 1: pair (a, b))
     uint8_t pad0[2];
-    int32_t tcount[33];      // tcount[r']: tuples whose indices are all < r' (the table is sorted by max index)
+    int32_t tcount[kMaxNDeep + 1];  // tcount[r']: tuples whose indices are all < r' (table sorted by max index)
     uint16_t back[kMaxKDeep];  // back[u] bit j: pattern edge (j, u), j < u
     uint16_t src[kMaxKDeep];   // src[u] bit j: canonical f(j) < f(u) (0 in RAW mode)
     uint8_t edge[kMaxEdges];   // pattern edges a | b << 4
@@ -123,9 +124,9 @@ int launch_batch(const MultiTables &tb, int canon, int64_t nq, const mapa_query 
 int launch_trace(const MultiTables &tb, int canon, int ntraces, int nops, const mapa_trace_op *d_ops, int njobs,
                  const mapa_query *d_jobs, uint64_t *d_keys, void *stream);
 // deep path (esa_deep.cu); sc = sel_code | 4 * canonical
-int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_query *d_query,
+int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_query64 *d_query,
                 mapa_wide_record *d_record, int depth, int rank, int world, int stripe, int grid, void *stream);
-int max_blocks_per_sm_deep(int nt, int sc, int lut_bytes);
+int max_blocks_per_sm_deep(int n, int nterm, int sc, int lut_bytes);
 int device_sm_count();
 int max_blocks_per_sm_single(int width, int k, int sc, int xs);
 int max_blocks_per_sm_batch(int width, int canon, int npats, int xs);

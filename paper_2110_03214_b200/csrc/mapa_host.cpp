@@ -24,9 +24,9 @@ struct mapa_topology {
     std::string name;
     int n = 0;
     int width = 8;
-    uint8_t cls[kMaxN][kMaxN];   // class code 0..3, diagonal 0xFF
+    uint8_t cls[kMaxNDeep][kMaxNDeep];   // class code 0..3, diagonal 0xFF
     std::vector<std::vector<int>> sockets;
-    uint32_t busy = 0;
+    uint64_t busy = 0;
     void *d_stage = nullptr;      // device: query (16 B) + record (32 B)
     void *h_stage = nullptr;      // pinned host mirror
 };
@@ -60,9 +60,9 @@ const char *kClassNames[4] = {"nv2x2", "nv2x1", "nv1x1", "pcie"};
 void topo_init(mapa_topology *t, const std::string &name, int n) {
     t->name = name;
     t->n = n;
-    t->width = n <= 8 ? 8 : (n <= 16 ? 16 : 32);
-    for (int u = 0; u < kMaxN; ++u)
-        for (int v = 0; v < kMaxN; ++v) t->cls[u][v] = (u == v) ? 0xFF : 3;  // PCIe fallback
+    t->width = n <= 8 ? 8 : (n <= 16 ? 16 : (n <= 32 ? 32 : 64));
+    for (int u = 0; u < kMaxNDeep; ++u)
+        for (int v = 0; v < kMaxNDeep; ++v) t->cls[u][v] = (u == v) ? 0xFF : 3;  // PCIe fallback
 }
 
 void topo_link(mapa_topology *t, int a1, int b1, int c) {  // 1-based ids
@@ -136,7 +136,7 @@ mapa_status parse_topology_text(const char *text, mapa_topology *t) {
             if (!(ls >> name)) return fail(MAPA_E_PARSE, "line " + std::to_string(ln) + ": name: missing value");
         } else if (f == "devices") {
             if (!(ls >> n) || n < 1) return fail(MAPA_E_PARSE, "line " + std::to_string(ln) + ": devices: bad count");
-            if (n > kMaxN) return fail(MAPA_E_UNSUPPORTED, "line " + std::to_string(ln) + ": devices > 32 unsupported");
+            if (n > kMaxNDeep) return fail(MAPA_E_UNSUPPORTED, "line " + std::to_string(ln) + ": devices > 64 unsupported");
         } else if (f == "sockets") {
             std::string grp;
             while (ls >> grp) {
@@ -166,7 +166,7 @@ mapa_status parse_topology_text(const char *text, mapa_topology *t) {
     }
     if (n < 1) return fail(MAPA_E_PARSE, "missing 'devices'");
     topo_init(t, name, n);
-    bool seen[kMaxN][kMaxN] = {};
+    bool seen[kMaxNDeep][kMaxNDeep] = {};
     for (const L &l : links) {
         if (l.a == l.b) return fail(MAPA_E_PARSE, "line " + std::to_string(l.line) + ": link: self loop");
         if (l.a < 1 || l.b < 1 || l.a > n || l.b > n)
@@ -203,7 +203,7 @@ void fill_devtopo(const mapa_topology *t, DevTopo &dt) {
 
 int bw_of(const mapa_topology *t, int u, int v) { return kClassBw[t->cls[u][v]]; }
 
-uint32_t nmask_of(int n) { return n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u); }
+uint64_t nmask_of(int n) { return n >= 64 ? ~0ull : ((1ull << n) - 1ull); }
 
 // ---------------------------------------------------------------- Eq. 2
 // Predicted effective bandwidth, Eq. 2, Table 4.
@@ -351,7 +351,7 @@ void fill_devpattern(const mapa_pattern *p, bool raw, uint16_t lut_off, DevPatte
 
 // narrow path: k <= 8 and the packed 63-bit key fits
 bool key_fits(const mapa_topology *t, const mapa_pattern *p) {
-    return p->k <= kMaxK && 15 + t->width + p->k * (p->k - 1) / 2 <= 63;
+    return t->n <= kMaxN && p->k <= kMaxK && 15 + t->width + p->k * (p->k - 1) / 2 <= 63;
 }
 
 uint64_t perm_count(int n, int d) {
@@ -478,7 +478,7 @@ int suffix_terms(const mapa_pattern *p, int L, int base, uint8_t (*term)[3], int
 
 // Valid L-tuples of distinct indices into r sorted devices (lex order); the
 // suffix-internal lex-leader constraints f(T+a) < f(T+b) become i_a < i_b.
-// Entry byte l = 4 * i_l.  Returns the count, or -1 above cap.
+// Entry byte l = i_l.  Returns the count, or -1 above cap.
 int build_tuples(const mapa_pattern *p, int L, int r, bool canon, uint32_t *out, int cap) {
     const int T = p->k - L;
     int n = 0, idx[4] = {0, 0, 0, 0};
@@ -496,7 +496,7 @@ int build_tuples(const mapa_pattern *p, int L, int r, bool canon, uint32_t *out,
         if (!ok) continue;
         if (n >= cap) return -1;
         uint32_t w = 0;
-        for (int l = 0; l < L; ++l) w |= (uint32_t)(4 * idx[l]) << (8 * l);
+        for (int l = 0; l < L; ++l) w |= (uint32_t)idx[l] << (8 * l);
         if (out) out[n] = w;
         ++n;
     }
@@ -520,9 +520,9 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     const bool canon = !(flags & MAPA_F_RAW) && p->aut > 1;
     const int base = sel_code(selector, sens);
     std::memset(tb, 0, sizeof(*tb));
-    DevTopo dt;
-    fill_devtopo(t, dt);
-    std::memcpy(tb->cm, dt.cm, sizeof(tb->cm));
+    for (int v = 0; v < t->n; ++v)
+        for (int u = 0; u < t->n; ++u)
+            if (u != v && t->cls[u][v] < 3) tb->cm[v][t->cls[u][v]] |= 1ull << u;
     tb->n = t->n;
     tb->k = k;
     tb->m = p->m;
@@ -539,7 +539,7 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     int bestL = 0;
     for (int L = 1; L <= std::min(k, 4); ++L) {
         const int r = nF - k + L;
-        if (r < L || r > 32 || (L >= 2 && r > 16)) continue;
+        if (r < L || r > kMaxNDeep || (L >= 2 && r > 16)) continue;
         const int nt = build_tuples(p, L, r, canon, nullptr, kMaxTup);
         if (nt <= 0) continue;
         int nes, scale;
@@ -569,12 +569,12 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     if (canon)
         for (int l = 0; l < L; ++l)
             if (p->src[T + l] & pmask & ~common) tb->pcon = 1;
-    for (int rr = 0; rr <= 32; ++rr) {
+    for (int rr = 0; rr <= kMaxNDeep; ++rr) {
         int c = 0;
         for (int i = 0; i < tb->ntup; ++i) {
             uint32_t m = 0;
             for (int l = 0; l < L; ++l) m = std::max(m, (tb->tup[i] >> (8 * l)) & 0xFFu);
-            if ((int)(m / 4) < rr) ++c;
+            if ((int)m < rr) ++c;
         }
         tb->tcount[rr] = c;
     }
@@ -582,7 +582,7 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     // decoded prefix depth: enough items for ~8 per resident warp (x world)
     int sm = device_sm_count();
     if (sm <= 0) sm = 148;
-    const int occ = max_blocks_per_sm_deep(tb->nterm, pl->sc, base == SEL_SENS ? 2 * tb->xsd * tb->xsd : 0);
+    const int occ = max_blocks_per_sm_deep(t->n, tb->nterm, pl->sc, base == SEL_SENS ? 2 * tb->xsd * tb->xsd : 0);
     const uint64_t warps = (uint64_t)sm * occ * 8;
     const uint64_t target = 8ull * warps * (uint64_t)world;
     // RAW items are uniform: stop at ~8 per warp.  Canonical items are not
@@ -618,38 +618,38 @@ mapa_status upload_lut(const mapa_pattern *pc) {
 // Lex-first bijection pi: V(P) -> S (pattern-vertex order, devices ascending)
 // with pi(E(P)) = E: keep adjacency and non-adjacency with every placed vertex
 // and equal degrees; the first complete map is the lex-first one.
-bool first_mapping(const mapa_pattern *p, const std::vector<int> &ds, const uint32_t *eadj, int v, int *pi,
-                   uint32_t used) {
+bool first_mapping(const mapa_pattern *p, const std::vector<int> &ds, const uint64_t *eadj, int v, int *pi,
+                   uint64_t used) {
     const int k = p->k;
     if (v == k) return true;
     for (int c : ds) {
         if ((used >> c) & 1u) continue;
-        if (__builtin_popcount(eadj[c]) != __builtin_popcount(p->adj[v])) continue;
+        if (__builtin_popcountll(eadj[c]) != __builtin_popcount(p->adj[v])) continue;
         bool ok = true;
         for (int w = 0; w < v && ok; ++w) ok = (((p->adj[v] >> w) & 1u) != 0) == (((eadj[c] >> pi[w]) & 1u) != 0);
         if (!ok) continue;
         pi[v] = c;
-        if (first_mapping(p, ds, eadj, v + 1, pi, used | (1u << c))) return true;
+        if (first_mapping(p, ds, eadj, v + 1, pi, used | (1ull << c))) return true;
     }
     return false;
 }
 
 // Decision from (S, E) (both paths): lex-first mapping, census, Eq. 1/2/3, and
 // the self-check of the key's score.
-mapa_status fill_decision(const mapa_topology *t, const mapa_pattern *p, uint32_t F, uint32_t S,
+mapa_status fill_decision(const mapa_topology *t, const mapa_pattern *p, uint64_t F, uint64_t S,
                           std::vector<std::pair<int, int>> E, int selector, int sens, uint32_t score,
                           mapa_decision &d) {
     const int k = p->k;
-    if (__builtin_popcount(S) != k || (S & ~F)) return fail(MAPA_E_INTERNAL, "decoded device set inconsistent");
+    if (__builtin_popcountll(S) != k || (S & ~F)) return fail(MAPA_E_INTERNAL, "decoded device set inconsistent");
     if ((int)E.size() != p->m) return fail(MAPA_E_INTERNAL, "decoded edge set has wrong size");
     std::sort(E.begin(), E.end());
     std::vector<int> ds;
     for (int dv = 0; dv < t->n; ++dv)
         if ((S >> dv) & 1u) ds.push_back(dv);
-    uint32_t eadj[kMaxN] = {0};
-    for (auto &e : E) { eadj[e.first] |= 1u << e.second; eadj[e.second] |= 1u << e.first; }
+    uint64_t eadj[kMaxNDeep] = {0};
+    for (auto &e : E) { eadj[e.first] |= 1ull << e.second; eadj[e.second] |= 1ull << e.first; }
     int pi[kMaxKDeep];
-    if (!first_mapping(p, ds, eadj, 0, pi, 0u))
+    if (!first_mapping(p, ds, eadj, 0, pi, 0ull))
         return fail(MAPA_E_INTERNAL, "no mapping of the decoded set yields the decoded edges");
     int agg = 0, x = 0, y = 0, z = 0;
     for (auto &e : E) {
@@ -679,13 +679,13 @@ mapa_status fill_decision(const mapa_topology *t, const mapa_pattern *p, uint32_
     return MAPA_OK;
 }
 
-mapa_status decode_wide(const mapa_topology *t, const mapa_pattern *p, uint32_t busy, int selector, int sens,
+mapa_status decode_wide(const mapa_topology *t, const mapa_pattern *p, uint64_t busy, int selector, int sens,
                         uint32_t flags, const mapa_wide_record *rec, mapa_decision *out) {
     mapa_decision d;
     std::memset(&d, 0, sizeof(d));
     d.k = p->k;
     d.m = p->m;
-    d.key = rec->key;
+    d.key = rec->score;
     d.ecode[0] = rec->ecode_hi;
     d.ecode[1] = rec->ecode_lo;
     d.leaves_scored = rec->leaves;
@@ -696,20 +696,21 @@ mapa_status decode_wide(const mapa_topology *t, const mapa_pattern *p, uint32_t 
         d.distinct_matches = rec->leaves;
         d.raw_embeddings = rec->leaves * p->aut;
     }
-    const uint32_t F = ~busy & nmask_of(t->n);
+    const uint64_t F = ~busy & nmask_of(t->n);
     if (rec->status != 0) return fail(MAPA_E_INVALID_ARG, "device reported a bad query (busy_hint != d_query->busy?)");
-    if (rec->key == 0) {
+    if (rec->set == 0) {
         d.status = MAPA_NO_CAPACITY;
         *out = d;
         return MAPA_NO_CAPACITY;
     }
     const int k = p->k, eb = k * (k - 1) / 2;
-    const uint32_t score = (uint32_t)(rec->key >> 32);
-    uint32_t S = 0;
-    for (int dv = 0; dv < 32; ++dv)
-        if ((rec->key >> (31 - dv)) & 1u) S |= 1u << dv;
+    if (rec->score > 0xFFFFFFFFull) return fail(MAPA_E_INTERNAL, "score out of range");
+    const uint32_t score = (uint32_t)rec->score;
+    uint64_t S = 0;
+    for (int dv = 0; dv < 64; ++dv)
+        if ((rec->set >> (63 - dv)) & 1u) S |= 1ull << dv;
     std::vector<int> ds;
-    for (int dv = 0; dv < 32; ++dv)
+    for (int dv = 0; dv < 64; ++dv)
         if ((S >> dv) & 1u) ds.push_back(dv);
     if ((int)ds.size() != k) return fail(MAPA_E_INTERNAL, "decoded device set has wrong size");
     std::vector<std::pair<int, int>> E;
@@ -726,7 +727,7 @@ mapa_status decode_wide(const mapa_topology *t, const mapa_pattern *p, uint32_t 
     return MAPA_OK;
 }
 
-mapa_status decode_record(const mapa_topology *t, const mapa_pattern *p, uint32_t busy, int selector,
+mapa_status decode_record(const mapa_topology *t, const mapa_pattern *p, uint64_t busy, int selector,
                           int sens, uint32_t flags, const mapa_record *rec, mapa_decision *out) {
     mapa_decision d;
     std::memset(&d, 0, sizeof(d));
@@ -735,11 +736,11 @@ mapa_status decode_record(const mapa_topology *t, const mapa_pattern *p, uint32_
     d.key = rec->key;
     d.leaves_scored = rec->leaves;
     const bool raw = (flags & MAPA_F_RAW) != 0;
-    const uint32_t F = ~busy & nmask_of(t->n);
+    const uint64_t F = ~busy & nmask_of(t->n);
     if ((flags & MAPA_F_PRUNE) && p->k >= 4) {
         // the pruned kernel scores a subset; the totals are the closed forms
         uint64_t perm = 1;
-        const int nf = __builtin_popcount(F);
+        const int nf = __builtin_popcountll(F);
         for (int i = 0; i < p->k; ++i) perm *= (uint64_t)std::max(0, nf - i);
         d.raw_embeddings = perm;
         d.distinct_matches = perm / (uint64_t)p->aut;
@@ -818,6 +819,7 @@ void topo_partitions(const mapa_topology *t, uint32_t *part, int32_t *npart) {
 mapa_status build_multi(const mapa_topology *t, const mapa_pattern *const *pats, int npats, uint32_t flags,
                         MultiTables *tb) {
     if (npats < 1 || npats > kMaxPats) return fail(MAPA_E_INVALID_ARG, "npats must be 1..16");
+    if (t->n > kMaxN) return fail(MAPA_E_UNSUPPORTED, "batch / trace / simulation need N <= 32");
     std::memset(tb, 0, sizeof(*tb));
     fill_devtopo(t, tb->topo);
     topo_partitions(t, tb->part, &tb->npart);
@@ -872,7 +874,7 @@ void mapa_free_topology(mapa_topology *t) {
     delete t;
 }
 
-mapa_status mapa_topology_info(const mapa_topology *t, int32_t *n, int32_t *width, int32_t *bw, uint32_t *busy) {
+mapa_status mapa_topology_info(const mapa_topology *t, int32_t *n, int32_t *width, int32_t *bw, uint64_t *busy) {
     if (!t) return fail(MAPA_E_INVALID_ARG, "null topology");
     if (n) *n = t->n;
     if (width) *width = t->width;
@@ -883,7 +885,7 @@ mapa_status mapa_topology_info(const mapa_topology *t, int32_t *n, int32_t *widt
     return MAPA_OK;
 }
 
-mapa_status mapa_claim(mapa_topology *t, uint32_t mask) {
+mapa_status mapa_claim(mapa_topology *t, uint64_t mask) {
     if (!t) return fail(MAPA_E_INVALID_ARG, "null topology");
     if (mask & ~nmask_of(t->n)) return fail(MAPA_E_ID_RANGE, "device id out of range");
     if (mask & t->busy) return fail(MAPA_E_ALREADY_BUSY, "device already busy");
@@ -891,7 +893,7 @@ mapa_status mapa_claim(mapa_topology *t, uint32_t mask) {
     return MAPA_OK;
 }
 
-mapa_status mapa_release(mapa_topology *t, uint32_t mask) {
+mapa_status mapa_release(mapa_topology *t, uint64_t mask) {
     if (!t) return fail(MAPA_E_INVALID_ARG, "null topology");
     if (mask & ~nmask_of(t->n)) return fail(MAPA_E_ID_RANGE, "device id out of range");
     if (mask & ~t->busy) return fail(MAPA_E_NOT_BUSY, "releasing a device that is not busy");
@@ -899,7 +901,7 @@ mapa_status mapa_release(mapa_topology *t, uint32_t mask) {
     return MAPA_OK;
 }
 
-mapa_status mapa_set_busy(mapa_topology *t, uint32_t busy) {
+mapa_status mapa_set_busy(mapa_topology *t, uint64_t busy) {
     if (!t) return fail(MAPA_E_INVALID_ARG, "null topology");
     if (busy & ~nmask_of(t->n)) return fail(MAPA_E_ID_RANGE, "device id out of range");
     t->busy = busy;
@@ -969,14 +971,15 @@ mapa_status mapa_effbw_rank_table(int32_t m, uint16_t *out) {
 
 mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
                                   int32_t sensitive, const mapa_query *d_query, mapa_record *d_record,
-                                  uint32_t flags, int32_t rank, int32_t world, uint32_t busy_hint,
+                                  uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint,
                                   void *stream) {
     if (!t || !p || !d_query || !d_record) return fail(MAPA_E_INVALID_ARG, "null argument");
+    if (t->n > kMaxN) return fail(MAPA_E_UNSUPPORTED, "narrow path needs N <= 32 (use the deep path)");
     if (world < 1 || rank < 0 || rank >= world) return fail(MAPA_E_INVALID_ARG, "bad rank/world");
     if (selector < 0 || selector > 2) return fail(MAPA_E_INVALID_ARG, "bad selector");
     if (!key_fits(t, p))
         return fail(MAPA_E_UNSUPPORTED, "narrow path needs k <= 8 and 15 + W + C(k,2) <= 63 (use the deep path)");
-    const int nF = busy_hint == 0xFFFFFFFFu ? t->n : __builtin_popcount(~busy_hint & nmask_of(t->n));
+    const int nF = busy_hint == ~0ull ? t->n : __builtin_popcountll(~busy_hint & nmask_of(t->n));
     static_assert(sizeof(SingleTables) < 32000, "kernel parameter block too large");
     SingleTables tb;
     std::memset(&tb, 0, sizeof(tb));
@@ -1011,20 +1014,20 @@ mapa_status mapa_reduce_records(const mapa_record *records, int32_t n, mapa_reco
     return MAPA_OK;
 }
 
-mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint32_t busy, int32_t selector,
+mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint64_t busy, int32_t selector,
                         int32_t sens, uint32_t flags, const mapa_record *record, mapa_decision *out) {
     if (!t || !p || !record || !out) return fail(MAPA_E_INVALID_ARG, "null argument");
     return decode_record(t, p, busy, selector, sens, flags, record, out);
 }
 
 mapa_status mapa_launch_query_wide(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
-                                   int32_t sensitive, const mapa_query *d_query, mapa_wide_record *d_record,
-                                   uint32_t flags, int32_t rank, int32_t world, uint32_t busy_hint, void *stream) {
+                                   int32_t sensitive, const mapa_query64 *d_query, mapa_wide_record *d_record,
+                                   uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint, void *stream) {
     if (!t || !p || !d_query || !d_record) return fail(MAPA_E_INVALID_ARG, "null argument");
     if (world < 1 || rank < 0 || rank >= world) return fail(MAPA_E_INVALID_ARG, "bad rank/world");
     if (selector < 0 || selector > 2) return fail(MAPA_E_INVALID_ARG, "bad selector");
     if (busy_hint & ~nmask_of(t->n)) return fail(MAPA_E_INVALID_ARG, "deep path needs busy_hint = the query's busy mask");
-    const int nF = __builtin_popcount(~busy_hint & nmask_of(t->n));
+    const int nF = __builtin_popcountll(~busy_hint & nmask_of(t->n));
     cudaStream_t st = (cudaStream_t)stream;
     int err = (int)cudaMemsetAsync(d_record, 0, sizeof(mapa_wide_record), st);
     if (err) return cuda_fail(err, "cudaMemsetAsync");
@@ -1048,9 +1051,11 @@ mapa_status mapa_reduce_wide_records(const mapa_wide_record *records, int32_t n,
     std::memset(&r, 0, sizeof(r));
     for (int i = 0; i < n; ++i) {
         const mapa_wide_record &q = records[i];
-        const bool gt = q.key != r.key ? q.key > r.key
-                                       : (q.ecode_hi != r.ecode_hi ? q.ecode_hi > r.ecode_hi : q.ecode_lo > r.ecode_lo);
-        if (gt) { r.key = q.key; r.ecode_hi = q.ecode_hi; r.ecode_lo = q.ecode_lo; }
+        const uint64_t a[4] = {q.score, q.set, q.ecode_hi, q.ecode_lo};
+        const uint64_t b[4] = {r.score, r.set, r.ecode_hi, r.ecode_lo};
+        if (q.set && std::lexicographical_compare(b, b + 4, a, a + 4)) {
+            r.score = q.score; r.set = q.set; r.ecode_hi = q.ecode_hi; r.ecode_lo = q.ecode_lo;
+        }
         r.leaves += q.leaves;
         r.status |= q.status;
     }
@@ -1058,7 +1063,7 @@ mapa_status mapa_reduce_wide_records(const mapa_wide_record *records, int32_t n,
     return MAPA_OK;
 }
 
-mapa_status mapa_decode_wide(const mapa_topology *t, const mapa_pattern *p, uint32_t busy, int32_t selector,
+mapa_status mapa_decode_wide(const mapa_topology *t, const mapa_pattern *p, uint64_t busy, int32_t selector,
                              int32_t sens, uint32_t flags, const mapa_wide_record *record, mapa_decision *out) {
     if (!t || !p || !record || !out) return fail(MAPA_E_INVALID_ARG, "null argument");
     return decode_wide(t, p, busy, selector, sens, flags, record, out);
@@ -1069,8 +1074,8 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
     if (!t || !p || !out) return fail(MAPA_E_INVALID_ARG, "null argument");
     if (selector < 0 || selector > 2) return fail(MAPA_E_INVALID_ARG, "bad selector");
     const bool deep = (flags & MAPA_F_DEEP) || !key_fits(t, p);
-    const uint32_t F = ~t->busy & nmask_of(t->n);
-    if (p->k > __builtin_popcount(F)) {
+    const uint64_t F = ~t->busy & nmask_of(t->n);
+    if (p->k > __builtin_popcountll(F)) {
         std::memset(out, 0, sizeof(*out));
         out->status = MAPA_NO_CAPACITY;
         out->k = p->k;
@@ -1084,25 +1089,32 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
     if (!t->h_stage) {
         if ((err = (int)cudaMallocHost(&t->h_stage, 128))) return cuda_fail(err, "cudaMallocHost");
     }
-    // staging: query at 0 (16 B), record at 64 (32 B narrow / 64 B deep)
-    mapa_query *hq = (mapa_query *)t->h_stage;
-    mapa_query *dq = (mapa_query *)t->d_stage;
+    // staging: query at 0 (16 B: mapa_query narrow / mapa_query64 deep), record at 64
+    void *hq = t->h_stage, *dq = t->d_stage;
     void *hr = (char *)t->h_stage + 64;
     void *dr = (char *)t->d_stage + 64;
-    hq->busy = t->busy;
-    hq->pattern = 0;
-    hq->selector = selector;
-    hq->sensitive = sens;
+    if (deep) {
+        mapa_query64 *q = (mapa_query64 *)hq;
+        q->busy = t->busy;
+        q->selector = selector;
+        q->sensitive = sens;
+    } else {
+        mapa_query *q = (mapa_query *)hq;
+        q->busy = (uint32_t)t->busy;
+        q->pattern = 0;
+        q->selector = selector;
+        q->sensitive = sens;
+    }
     cudaStream_t st = (cudaStream_t)stream;
-    if ((err = (int)cudaMemcpyAsync(dq, hq, sizeof(mapa_query), cudaMemcpyHostToDevice, st)))
-        return cuda_fail(err, "H2D query");
+    if ((err = (int)cudaMemcpyAsync(dq, hq, 16, cudaMemcpyHostToDevice, st))) return cuda_fail(err, "H2D query");
     mapa_status s;
     const size_t rbytes = deep ? sizeof(mapa_wide_record) : sizeof(mapa_record);
     if (deep)
-        s = mapa_launch_query_wide(t, p, selector, sens, dq, (mapa_wide_record *)dr, flags & ~MAPA_F_PRUNE, 0, 1,
-                                   t->busy, stream);
+        s = mapa_launch_query_wide(t, p, selector, sens, (const mapa_query64 *)dq, (mapa_wide_record *)dr,
+                                   flags & ~MAPA_F_PRUNE, 0, 1, t->busy, stream);
     else
-        s = mapa_launch_query(t, p, selector, sens, dq, (mapa_record *)dr, flags, 0, 1, t->busy, stream);
+        s = mapa_launch_query(t, p, selector, sens, (const mapa_query *)dq, (mapa_record *)dr, flags, 0, 1, t->busy,
+                              stream);
     if (s != MAPA_OK) return s;
     if ((err = (int)cudaMemcpyAsync(hr, dr, rbytes, cudaMemcpyDeviceToHost, st))) return cuda_fail(err, "D2H record");
     if ((err = (int)cudaStreamSynchronize(st))) return cuda_fail(err, "cudaStreamSynchronize");
@@ -1252,8 +1264,8 @@ mapa_status mapa_simulate(const mapa_topology *t, const mapa_pattern *const *pat
     }
     cleanup();
     // host replay of the op order: the busy mask at each ALLOC decodes its key
-    uint32_t busy = 0;
-    std::vector<uint32_t> held(njobs, 0);
+    uint64_t busy = 0;
+    std::vector<uint64_t> held(njobs, 0);
     for (const mapa_trace_op &o : ops) {
         const int j = o.job;
         if (o.op == 1) { busy &= ~held[j]; continue; }
@@ -1271,7 +1283,7 @@ mapa_status mapa_simulate(const mapa_topology *t, const mapa_pattern *const *pat
         std::memset(&L, 0, sizeof(L));
         L.job = j;
         L.k = p->k;
-        L.device_mask = d.device_mask;
+        L.device_mask = (uint32_t)d.device_mask;
         L.x = d.x; L.y = d.y; L.z = d.z;
         L.agg_bw = d.agg_bw;
         L.preserved_bw = d.preserved_bw;

@@ -98,11 +98,22 @@ def wide_record_tensor(rec: WideRecord, device="cpu"):
     return torch.tensor(list(struct.unpack("<8q", bytes(rec))), dtype=torch.int64, device=device)
 
 
+def _i64(v: int) -> int:
+    v &= (1 << 64) - 1
+    return v - (1 << 64) if v >= (1 << 63) else v
+
+
+def query64_tensor(busy: int, selector: int = 0, sensitive: bool = False, device="cuda"):
+    """One mapa_query64 (16 B: u64 busy, i32 selector, i32 sensitive) as int64[2]."""
+    return torch.tensor([_i64(busy), _i64(selector | (int(bool(sensitive)) << 32))], dtype=torch.int64,
+                        device=device)
+
+
 def run_query_wide(topo: Topology, pat: Pattern, selector: int, sensitive: bool, busy: int, raw: bool = False,
                    rank: int = 0, world: int = 1, stream=None):
     """Deep path: launch one (shard of a) query; returns the 64-B record tensor
     (int64[8], device) without synchronising."""
-    q = query_tensor(busy, 0, selector, sensitive)
+    q = query64_tensor(busy, selector, sensitive)
     rec = torch.empty(8, dtype=torch.int64, device="cuda")
     launch_query_wide(topo, pat, selector, sensitive, q.data_ptr(), rec.data_ptr(), busy, raw=raw, rank=rank,
                       world=world, stream=stream)
@@ -111,7 +122,7 @@ def run_query_wide(topo: Topology, pat: Pattern, selector: int, sensitive: bool,
 
 def combine_wide_records(rec: torch.Tensor, group=None) -> WideRecord:
     """all_gather the per-rank 64-B deep records (one collective), combine by
-    the lexicographic max of the 192-bit key and the sum of leaves."""
+    the lexicographic max of the 256-bit key and the sum of leaves."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return wide_records_from_tensor(rec)[0]

@@ -30,15 +30,15 @@ def selector_score(dec: dict, selector: int, sensitive: bool, rank_table, m: int
 
 
 def encode_wide_key(dec: dict, score: int, k: int):
-    """(key, ecode_hi, ecode_lo) of mapa_wide_record (include/mapa.h):
-    key = score << 32 | brev_32(S); ecode bit C(k,2)-1-p per used edge."""
+    """(score, set, ecode_hi, ecode_lo) of mapa_wide_record (include/mapa.h):
+    set = brev_64(S); ecode bit C(k,2)-1-p per used edge."""
     eb = k * (k - 1) // 2
     S = sorted(dec["devices"])
-    key = (score << 32) | sum(1 << (31 - d) for d in S)
+    st = sum(1 << (63 - d) for d in S)
     rank = {d: i for i, d in enumerate(S)}
     pidx = pair_index(k)
     ecode = 0
     for u, v in dec["used_edges"]:
         a, b = sorted((rank[u], rank[v]))
         ecode |= 1 << (eb - 1 - pidx[(a, b)])
-    return key, ecode >> 64, ecode & ((1 << 64) - 1)
+    return score, st, ecode >> 64, ecode & ((1 << 64) - 1)

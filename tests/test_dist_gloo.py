@@ -114,10 +114,10 @@ def _worker_wide(rank, port, cases, out_q):
         t = mp.Topology(name)
         tab = mp.effbw_rank_table(len(e))
         if part["status"] == "ok":
-            key, eh, el = encode_wide_key(part, selector_score(part, sel, sens, tab, len(e)), k)
+            sc, st, eh, el = encode_wide_key(part, selector_score(part, sel, sens, tab, len(e)), k)
         else:
-            key = eh = el = 0
-        rec = md.wide_record_tensor(mp.WideRecord(key=key, ecode_hi=eh, ecode_lo=el, leaves=part["raw"]))
+            sc = st = eh = el = 0
+        rec = md.wide_record_tensor(mp.WideRecord(score=sc, set=st, ecode_hi=eh, ecode_lo=el, leaves=part["raw"]))
         comb = md.combine_wide_records(rec)
         got = mp.decode_wide(t, mp.Pattern.make(shape, k), busy, sel, sens, comb, raw=True)
         results.append(got)
@@ -133,7 +133,7 @@ WIDE_CASES = [("cubemesh16", 0b0110000000100100, "ring", 10, 0, False),         
 
 
 def test_two_rank_wide_combine_matches_unsharded_deep_oracle():
-    """Deep path (192-bit keys): the same exchange with 64-B wide records
+    """Deep path (256-bit keys): the same exchange with 64-B wide records
     (dist.combine_wide_records -> mapa_reduce_wide_records -> mapa_decode_wide)."""
     from oracle import coracle as co
     from oracle import mapa_oracle as mo

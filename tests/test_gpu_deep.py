@@ -1,4 +1,4 @@
-"""GPU parity of the deep path (esa_deep, 192-bit key, k <= 16; SURVEY §8(f)
+"""GPU parity of the deep path (esa_deep, 256-bit key, k <= 16; SURVEY §8(f)
 NEXT 1) through the C-ABI, against the CPU oracles on the same seeded inputs:
 decision fields and counts bit-exact, Eq. 2 double within 1e-6 relative."""
 import math
@@ -166,7 +166,7 @@ def test_deep_full_clique_vs_subset_bruteforce():
 
 
 def test_deep_sharded_virtual_ranks_and_determinism():
-    """Shards r = 0..R-1 of one deep query combine (lexicographic 192-bit max,
+    """Shards r = 0..R-1 of one deep query combine (lexicographic 256-bit max,
     sum of leaves) to the unsharded record for R = 1, 2, 3, 5; repeated runs
     give identical records."""
     t = mp.Topology("cubemesh16")
@@ -183,8 +183,8 @@ def test_deep_sharded_virtual_ranks_and_determinism():
             comb = mp.reduce_wide_records(recs)
             if ref is None:
                 ref = comb
-            assert (comb.key, comb.ecode_hi, comb.ecode_lo, comb.leaves) == \
-                (ref.key, ref.ecode_hi, ref.ecode_lo, ref.leaves), (shape, k, world)
+            assert (comb.score, comb.set, comb.ecode_hi, comb.ecode_lo, comb.leaves) == \
+                (ref.score, ref.set, ref.ecode_hi, ref.ecode_lo, ref.leaves), (shape, k, world)
         d = mp.decode_wide(t, p, busy, sel, sens, ref)
         t.set_busy(busy)
         assert mp.allocate(t, p, sel, sens)["key"] == d["key"]
@@ -208,3 +208,47 @@ def test_deep_edge_cases():
         ob = co.allocate_deep(o32, busy, kk, e, sel, sens)
         t32.set_busy(busy)
         same(ob, mp.allocate(t32, mp.Pattern.make("ring", 9), sel, sens), (sel, sens))
+
+
+def test_deep_n64_vs_deep_oracle():
+    """N = 64 (het64: 8 dgx1v islands) on the deep path
+    with u64 masks and the 256-bit key: random busy masks leaving 9..11 free
+    devices spread over both halves of the id space, k = 3..9, every selector,
+    RAW and canonical, vs the deep C oracle."""
+    text = W.het64_text()
+    o = mo.parse_topology(text)
+    t = mp.Topology(text=text)
+    assert t.n == 64 and t.width == 64
+    rng = random.Random(6464)
+    for trial in range(16):
+        nf = rng.randint(9, 11)
+        free = rng.sample(range(64), nf)
+        busy = ((1 << 64) - 1) & ~sum(1 << d for d in free)
+        shape = rng.choice(["ring", "tree", "ringtree", "full"])
+        k = rng.randint(3, 9 if nf <= 10 else 8)
+        sel, sens = rng.choice(SELS)
+        kk, e = mo.make_pattern(shape, k)
+        ob = co.allocate_deep(o, busy, kk, e, sel, sens)
+        for raw in (False, True):
+            t.set_busy(busy)
+            g = mp.allocate(t, mp.Pattern.make(shape, k), sel, sens, raw=raw)
+            same(ob, g, (trial, shape, k, hex(busy), sel, sens, raw))
+            assert g["raw"] == ob["raw"] == math.perm(nf, k)
+
+
+def test_deep_n64_all_free_clique_and_narrow_refusal():
+    """het64 all free, full-4: 635,376 device sets (one orbit each), vs the
+    deep C oracle over every subset; the narrow entry point refuses N > 32."""
+    text = W.het64_text()
+    o = mo.parse_topology(text)
+    t = mp.Topology(text=text)
+    kk, e = mo.make_pattern("full", 4)
+    for sel, sens in SELS[:3]:
+        ob = co.allocate_deep(o, 0, kk, e, sel, sens, max_subsets=700000)
+        g = mp.allocate(t, mp.Pattern.make("full", 4), sel, sens)
+        same(ob, g, (sel, sens))
+        assert g["leaves"] == math.comb(64, 4)
+    q, rec = md.query_tensor(0), torch.zeros(4, dtype=torch.int64, device="cuda")
+    with pytest.raises(mp.MapaError) as ei:
+        mp.launch_query(t, mp.Pattern.make("ring", 3), 0, False, q.data_ptr(), rec.data_ptr(), busy_hint=0)
+    assert ei.value.status == mp.E_UNSUPPORTED

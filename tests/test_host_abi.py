@@ -63,7 +63,7 @@ def test_topology_parse_errors():
         mp.Topology(text="devices 4\nsockets 1,2 2,3,4\n")
     assert e.value.status == mp.E_PARSE
     with pytest.raises(mp.MapaError) as e:
-        mp.Topology(text="devices 33\n")
+        mp.Topology(text="devices 65\n")
     assert e.value.status == mp.E_UNSUPPORTED
     with pytest.raises(mp.MapaError):
         mp.Topology("dgx2")

@@ -125,6 +125,23 @@ def het32_text() -> str:
     return topology_text("het32", 32, sockets, links)
 
 
+def het64_text() -> str:
+    """het64 (servers beyond 32 accelerators): het32's
+    construction with 8 dgx1v islands, ids 8i+1..8i+8; bridges
+    (8i+j)<->(8((i+1) mod 8)+j) SingleNVLink1; sockets = the 8 islands."""
+    links = []
+    for i in range(8):
+        o = 8 * i
+        links += [(a + o, b + o, "nv2x2") for a, b in _DGX_DOUBLE]
+        links += [(a + o, b + o, "nv2x1") for a, b in _DGX_SINGLE]
+    for i in range(8):
+        for j in range(1, 9):
+            a, b = 8 * i + j, 8 * ((i + 1) % 8) + j
+            links.append((min(a, b), max(a, b), "nv1x1"))
+    sockets = [list(range(8 * i + 1, 8 * i + 9)) for i in range(8)]
+    return topology_text("het64", 64, sockets, links)
+
+
 def rand_text(n: int, seed: int, probs=(0.1, 0.1, 0.1, 0.7)) -> str:
     """randN(seed): every pair i.i.d. class with the given probabilities
     (nv2x2, nv2x1, nv1x1, pcie).  Pair (a,b), a<b, uses stream(seed, a*64+b)."""
