@@ -387,7 +387,9 @@ def main():
                                  f"(measured max SM clock)"},
             "cpu_baseline": cpu,
             "e2e": {"value": emb_step * e2e_steps / e2e_s, "unit": "embeddings/s",
-                    "h2d_bytes_per_step": 16 * len(SELECTORS),
+                    # per allocation: one 128-B H2D staging copy (16-B query + a zero record image)
+                    # and the 32-B record back (N>1: the query tensor + the all_gather'd records)
+                    "h2d_bytes_per_step": (128 if world == 1 else 16) * len(SELECTORS),
                     "d2h_bytes_per_step": 32 * len(SELECTORS) * world,
                     "allocations_per_s": len(SELECTORS) * e2e_steps / e2e_s},
             "gpu_launches": len(SELECTORS) * args.steps,

@@ -189,14 +189,25 @@ def effbw_rank_table(m: int) -> list[int]:
     return list(buf)
 
 
+_torch = None
+
+
 def _stream_ptr(stream) -> int | None:
+    """cudaStream_t of `stream`, or of torch's current stream when None
+    (without a CUDA-capable torch: the legacy default stream)."""
+    global _torch
     if stream is None:
-        try:
-            import torch
-            if torch.cuda.is_available():
-                return torch.cuda.current_stream().cuda_stream
-        except Exception:  # pragma: no cover
-            pass
+        if _torch is None:
+            try:
+                import torch
+                _torch = torch if torch.cuda.is_available() else False
+            except Exception:  # pragma: no cover
+                _torch = False
+        if _torch:
+            raw = getattr(_torch._C, "_cuda_getCurrentRawStream", None)
+            if raw is not None:  # the raw cudaStream_t without building a Stream object
+                return raw(_torch._C._cuda_getDevice())
+            return _torch.cuda.current_stream().cuda_stream
         return None
     return getattr(stream, "cuda_stream", stream)
 
@@ -299,9 +310,15 @@ class Pattern:
 def decision_dict(d: Decision) -> dict:
     if d.status == NO_CAPACITY:
         return dict(status="no_capacity", raw=0, distinct=0, leaves=0, key=0)
-    devs = tuple(i for i in range(64) if (d.device_mask >> i) & 1)
-    return dict(status="ok", devices=devs, mapping=tuple(d.mapping[i] for i in range(d.k)),
-                used_edges=[(d.used[i][0], d.used[i][1]) for i in range(d.m)],
+    devs = []
+    m = d.device_mask
+    while m:
+        low = m & -m
+        devs.append(low.bit_length() - 1)
+        m ^= low
+    k, used = d.k, d.used
+    return dict(status="ok", devices=tuple(devs), mapping=tuple(d.mapping[:k]),
+                used_edges=[(used[i][0], used[i][1]) for i in range(d.m)],
                 x=d.x, y=d.y, z=d.z, agg_bw=d.agg_bw, preserved_bw=d.preserved_bw,
                 pred_effbw=d.pred_effbw, score=d.score, raw=int(d.raw_embeddings),
                 distinct=int(d.distinct_matches), leaves=int(d.leaves_scored), key=int(d.key),
@@ -312,13 +329,24 @@ def _flags(raw: bool, prune: bool = False, deep: bool = False) -> int:
     return (F_RAW if raw else 0) | (F_PRUNE if prune else 0) | (F_DEEP if deep else 0)
 
 
+_tls = __import__("threading").local()
+
+
+def _decision_buf() -> Decision:
+    """Per-thread reusable output struct (mapa_allocate overwrites it whole)."""
+    d = getattr(_tls, "decision", None)
+    if d is None:
+        d = _tls.decision = Decision()
+    return d
+
+
 def allocate(topo: Topology, pat: Pattern, selector: int, sensitive: bool = False, raw: bool = False,
              commit: bool = False, stream=None, prune: bool = False, deep: bool = False) -> dict:
     """mapa_allocate: one allocation end to end from host buffers (H2D query,
     kernel, D2H record, host decode).  prune = MAPA_F_PRUNE (branch and bound,
     same decision, fewer leaves scored); deep = MAPA_F_DEEP (the wide-key
     kernel even when the narrow one fits; patterns with k > 8 always take it)."""
-    d = Decision()
+    d = _decision_buf()
     flags = _flags(raw, prune, deep) | (F_COMMIT if commit else 0)
     _check(_lib.mapa_allocate(topo.handle, pat.handle, selector, int(bool(sensitive)), flags,
                               _stream_ptr(stream), ctypes.byref(d)), allow_no_capacity=True)

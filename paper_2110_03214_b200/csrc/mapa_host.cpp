@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -20,6 +21,17 @@
 
 using namespace mapa;
 
+// One cached mapa_allocate sequence (H2D query, record zeroing, kernel, D2H
+// record) as an instantiated CUDA graph, keyed by (pattern uid, selector /
+// flags / path, free count, device): the kernel's parameters depend only on
+// those; the busy mask itself is read from the pinned staging buffer when the
+// graph runs.
+struct GraphEntry {
+    uint64_t key[3];
+    cudaGraphExec_t exec;
+    uint64_t tick;
+};
+
 struct mapa_topology {
     std::string name;
     int n = 0;
@@ -27,8 +39,11 @@ struct mapa_topology {
     uint8_t cls[kMaxNDeep][kMaxNDeep];   // class code 0..3, diagonal 0xFF
     std::vector<std::vector<int>> sockets;
     uint64_t busy = 0;
-    void *d_stage = nullptr;      // device: query (16 B) + record (32 B)
+    void *d_stage = nullptr;      // device: query (16 B) + record (32 / 64 B)
     void *h_stage = nullptr;      // pinned host mirror
+    cudaStream_t cap = nullptr;   // private stream for graph capture (the caller's may be the legacy stream)
+    std::vector<GraphEntry> graphs;
+    uint64_t tick = 0;
 };
 
 struct mapa_pattern {
@@ -42,6 +57,7 @@ struct mapa_pattern {
     double theta[14];          // Eq. 2 model of this pattern (Table 4 unless mapa_pattern_set_effbw_model)
     void *d_lut = nullptr;     // device copy of lut (deep kernel), uploaded on first use
     int d_lut_dev = -1;
+    uint64_t uid = 0;          // unique per compiled pattern / model (graph cache key)
 };
 
 namespace {
@@ -250,6 +266,11 @@ std::vector<uint16_t> rank_table(int m, const double *th = kTheta) {
 }
 
 // ---------------------------------------------------------------- patterns
+uint64_t next_uid() {
+    static std::atomic<uint64_t> c{1};
+    return c.fetch_add(1);
+}
+
 // Does an automorphism sigma of P exist with sigma(j) = j for j < i and
 // sigma(i) = u?  Backtracking over sigma(v), v = i+1..k-1, keeping adjacency
 // AND non-adjacency with every assigned vertex (so a complete sigma is an
@@ -327,6 +348,7 @@ mapa_status compile_pattern(int k, const std::vector<std::pair<int, int>> &raw, 
     }
     std::memcpy(p->theta, kTheta, sizeof(kTheta));
     p->lut = rank_table(p->m);
+    p->uid = next_uid();
     *out = p;
     return MAPA_OK;
 }
@@ -869,6 +891,8 @@ mapa_status mapa_load_topology(const char *spec, int32_t is_text, mapa_topology 
 
 void mapa_free_topology(mapa_topology *t) {
     if (!t) return;
+    for (auto &g : t->graphs) cudaGraphExecDestroy(g.exec);
+    if (t->cap) cudaStreamDestroy(t->cap);
     if (t->d_stage) cudaFree(t->d_stage);
     if (t->h_stage) cudaFreeHost(t->h_stage);
     delete t;
@@ -969,10 +993,25 @@ mapa_status mapa_effbw_rank_table(int32_t m, uint16_t *out) {
     return MAPA_OK;
 }
 
+static mapa_status launch_query_impl(const mapa_topology *t, const mapa_pattern *p, int32_t selector, int32_t sensitive,
+                              const mapa_query *d_query, mapa_record *d_record, uint32_t flags, int32_t rank,
+                              int32_t world, uint64_t busy_hint, void *stream, bool zero_record);
+static mapa_status launch_query_wide_impl(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
+                                   int32_t sensitive, const mapa_query64 *d_query, mapa_wide_record *d_record,
+                                   uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint, void *stream,
+                                   bool zero_record);
+
 mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
                                   int32_t sensitive, const mapa_query *d_query, mapa_record *d_record,
                                   uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint,
                                   void *stream) {
+    return launch_query_impl(t, p, selector, sensitive, d_query, d_record, flags, rank, world, busy_hint, stream,
+                             true);
+}
+
+static mapa_status launch_query_impl(const mapa_topology *t, const mapa_pattern *p, int32_t selector, int32_t sensitive,
+                              const mapa_query *d_query, mapa_record *d_record, uint32_t flags, int32_t rank,
+                              int32_t world, uint64_t busy_hint, void *stream, bool zero_record) {
     if (!t || !p || !d_query || !d_record) return fail(MAPA_E_INVALID_ARG, "null argument");
     if (t->n > kMaxN) return fail(MAPA_E_UNSUPPORTED, "narrow path needs N <= 32 (use the deep path)");
     if (world < 1 || rank < 0 || rank >= world) return fail(MAPA_E_INVALID_ARG, "bad rank/world");
@@ -994,7 +1033,7 @@ mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int
     Plan pl = plan_single(t, p, sc, nF, world);
     if (pl.nlocal >= (1ull << 27)) return fail(MAPA_E_UNSUPPORTED, "too many work items");
     std::memcpy(tb.lut, p->lut.data(), p->lut.size() * sizeof(uint16_t));
-    int err = (int)cudaMemsetAsync(d_record, 0, sizeof(mapa_record), (cudaStream_t)stream);
+    int err = zero_record ? (int)cudaMemsetAsync(d_record, 0, sizeof(mapa_record), (cudaStream_t)stream) : 0;
     if (err) return cuda_fail(err, "cudaMemsetAsync");
     err = launch_single(tb, sc, d_query, d_record, pl.depth, rank, world, pl.chunk, pl.grid, stream);
     if (err) return cuda_fail(err, "esa_single launch");
@@ -1023,13 +1062,21 @@ mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint64_t 
 mapa_status mapa_launch_query_wide(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
                                    int32_t sensitive, const mapa_query64 *d_query, mapa_wide_record *d_record,
                                    uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint, void *stream) {
+    return launch_query_wide_impl(t, p, selector, sensitive, d_query, d_record, flags, rank, world, busy_hint,
+                                  stream, true);
+}
+
+static mapa_status launch_query_wide_impl(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
+                                   int32_t sensitive, const mapa_query64 *d_query, mapa_wide_record *d_record,
+                                   uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint, void *stream,
+                                   bool zero_record) {
     if (!t || !p || !d_query || !d_record) return fail(MAPA_E_INVALID_ARG, "null argument");
     if (world < 1 || rank < 0 || rank >= world) return fail(MAPA_E_INVALID_ARG, "bad rank/world");
     if (selector < 0 || selector > 2) return fail(MAPA_E_INVALID_ARG, "bad selector");
     if (busy_hint & ~nmask_of(t->n)) return fail(MAPA_E_INVALID_ARG, "deep path needs busy_hint = the query's busy mask");
     const int nF = __builtin_popcountll(~busy_hint & nmask_of(t->n));
     cudaStream_t st = (cudaStream_t)stream;
-    int err = (int)cudaMemsetAsync(d_record, 0, sizeof(mapa_wide_record), st);
+    int err = zero_record ? (int)cudaMemsetAsync(d_record, 0, sizeof(mapa_wide_record), st) : 0;
     if (err) return cuda_fail(err, "cudaMemsetAsync");
     if (p->k > nF) return MAPA_OK;  // no capacity: the zeroed record says so (key 0)
     static_assert(sizeof(DeepTables) < 32000, "kernel parameter block too large");
@@ -1087,11 +1134,14 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
         if ((err = (int)cudaMalloc(&t->d_stage, 128))) return cuda_fail(err, "cudaMalloc");
     }
     if (!t->h_stage) {
-        if ((err = (int)cudaMallocHost(&t->h_stage, 128))) return cuda_fail(err, "cudaMallocHost");
+        if ((err = (int)cudaMallocHost(&t->h_stage, 192))) return cuda_fail(err, "cudaMallocHost");
+        std::memset(t->h_stage, 0, 192);
     }
-    // staging: query at 0 (16 B: mapa_query narrow / mapa_query64 deep), record at 64
+    // staging: host [0,16) query (mapa_query narrow / mapa_query64 deep), [64,128)
+    // a zero record (never written), [128,192) the result; ONE 128-B H2D copy
+    // stages the query and zeroes the device record (device [0,16) / [64,128))
     void *hq = t->h_stage, *dq = t->d_stage;
-    void *hr = (char *)t->h_stage + 64;
+    void *hr = (char *)t->h_stage + 128;
     void *dr = (char *)t->d_stage + 64;
     if (deep) {
         mapa_query64 *q = (mapa_query64 *)hq;
@@ -1106,17 +1156,55 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
         q->sensitive = sens;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    if ((err = (int)cudaMemcpyAsync(dq, hq, 16, cudaMemcpyHostToDevice, st))) return cuda_fail(err, "H2D query");
-    mapa_status s;
     const size_t rbytes = deep ? sizeof(mapa_wide_record) : sizeof(mapa_record);
-    if (deep)
-        s = mapa_launch_query_wide(t, p, selector, sens, (const mapa_query64 *)dq, (mapa_wide_record *)dr,
-                                   flags & ~MAPA_F_PRUNE, 0, 1, t->busy, stream);
-    else
-        s = mapa_launch_query(t, p, selector, sens, (const mapa_query *)dq, (mapa_record *)dr, flags, 0, 1, t->busy,
-                              stream);
-    if (s != MAPA_OK) return s;
-    if ((err = (int)cudaMemcpyAsync(hr, dr, rbytes, cudaMemcpyDeviceToHost, st))) return cuda_fail(err, "D2H record");
+    const uint32_t lflags = deep ? (flags & ~MAPA_F_PRUNE) : flags;
+    // the sequence issued on stream `s2`
+    auto issue = [&](cudaStream_t s2) -> mapa_status {
+        int e2;
+        if ((e2 = (int)cudaMemcpyAsync(dq, hq, 128, cudaMemcpyHostToDevice, s2))) return cuda_fail(e2, "H2D query");
+        mapa_status s3 = deep ? launch_query_wide_impl(t, p, selector, sens, (const mapa_query64 *)dq,
+                                                       (mapa_wide_record *)dr, lflags, 0, 1, t->busy, (void *)s2, false)
+                              : launch_query_impl(t, p, selector, sens, (const mapa_query *)dq, (mapa_record *)dr,
+                                                  lflags, 0, 1, t->busy, (void *)s2, false);
+        if (s3 != MAPA_OK) return s3;
+        if ((e2 = (int)cudaMemcpyAsync(hr, dr, rbytes, cudaMemcpyDeviceToHost, s2))) return cuda_fail(e2, "D2H record");
+        return MAPA_OK;
+    };
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t key[3] = {p->uid, (uint64_t)selector | ((uint64_t)(sens != 0) << 2) | ((uint64_t)deep << 3) |
+                                         ((uint64_t)lflags << 8),
+                             (uint64_t)__builtin_popcountll(F) | ((uint64_t)dev << 8)};
+    cudaGraphExec_t exec = nullptr;
+    for (auto &g : t->graphs)
+        if (g.key[0] == key[0] && g.key[1] == key[1] && g.key[2] == key[2]) { exec = g.exec; g.tick = ++t->tick; break; }
+    if (!exec) {
+        // first call for this key: capture the sequence on a private stream
+        if (deep && sel_code(selector, sens) == SEL_SENS) {
+            mapa_status su = upload_lut(p);  // synchronous: not inside the capture
+            if (su != MAPA_OK) return su;
+        }
+        if (!t->cap && (err = (int)cudaStreamCreateWithFlags(&t->cap, cudaStreamNonBlocking)))
+            return cuda_fail(err, "cudaStreamCreate");
+        if ((err = (int)cudaStreamBeginCapture(t->cap, cudaStreamCaptureModeRelaxed))) return cuda_fail(err, "capture");
+        const mapa_status sc = issue(t->cap);
+        cudaGraph_t graph = nullptr;
+        const int ec = (int)cudaStreamEndCapture(t->cap, &graph);
+        if (sc != MAPA_OK) { if (graph) cudaGraphDestroy(graph); return sc; }
+        if (ec) return cuda_fail(ec, "cudaStreamEndCapture");
+        err = (int)cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (err) return cuda_fail(err, "cudaGraphInstantiate");
+        if (t->graphs.size() >= 32) {  // evict the least recently used
+            auto lru = std::min_element(t->graphs.begin(), t->graphs.end(),
+                                        [](const GraphEntry &a2, const GraphEntry &b2) { return a2.tick < b2.tick; });
+            cudaGraphExecDestroy(lru->exec);
+            t->graphs.erase(lru);
+        }
+        t->graphs.push_back({{key[0], key[1], key[2]}, exec, ++t->tick});
+    }
+    if ((err = (int)cudaGraphLaunch(exec, st))) return cuda_fail(err, "cudaGraphLaunch");
+    mapa_status s = MAPA_OK;
     if ((err = (int)cudaStreamSynchronize(st))) return cuda_fail(err, "cudaStreamSynchronize");
     mapa_decision d;
     if (deep)
@@ -1384,6 +1472,7 @@ mapa_status mapa_pattern_set_effbw_model(mapa_pattern *p, const double *theta) {
     if (!p || !theta) return fail(MAPA_E_INVALID_ARG, "null argument");
     std::memcpy(p->theta, theta, sizeof(p->theta));
     p->lut = rank_table(p->m, p->theta);
+    p->uid = next_uid();  // cached allocate graphs baked the old table
     if (p->d_lut) { cudaFree(p->d_lut); p->d_lut = nullptr; p->d_lut_dev = -1; }
     return MAPA_OK;
 }
