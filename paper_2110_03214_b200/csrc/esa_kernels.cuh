@@ -140,6 +140,7 @@ struct Ctx {
     uint64_t fb, fs, db;            // bytes: fwd_back, fwd_src, dback
     int clique, eb, m;
     int one;                        // 1, read from shared memory (see scan_dense)
+    int negk;                       // -65536 at run time (pack16 offset split on the FMA pipe)
     int colmax;                     // additive scores: max_v col[v] (prune-mode bound)
     int col[W];                     // lane's inner-scan column (see lane_column)
 };
@@ -325,11 +326,16 @@ __device__ __forceinline__ int tab_entry(const Ctx<W> &c, uint32_t cand, int t2)
 template <int W, int SEL>
 __device__ __forceinline__ int tab_scan(const Ctx<W> &c, const int *tab, int base) {
     if constexpr (SelT<SEL>::pack16) {
+        // Each register holds two 16-bit byte offsets; the high one is s >> 16
+        // (ALU) and the low one s - (s >> 16) * 65536, an IMAD by a run-time
+        // constant (FMA pipe), so the ALU pipe -- the binding one -- spends 3
+        // ops per 2 leaves (IADD3, SHF, 3-input max); the (31 - v) tie-break
+        // goes in as IMAD r*one + (31-v) (FMA pipe).
         const uint4 *t8 = reinterpret_cast<const uint4 *>(tab);
-        const char *lut = reinterpret_cast<const char *>(sh_lut());  // pid 0: c.lut == 0
+        const int *lut = sh_lut();  // pid 0: c.lut == 0
         const uint32_t b4 = __funnelshift_l(0u, (uint32_t)base, 2);
         const uint32_t bp = b4 | (b4 << 16);
-        const int one = c.one;
+        const int one = c.one, negk = c.negk;
         int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll
         for (int q = 0; q < W / 8; ++q) {
@@ -338,15 +344,12 @@ __device__ __forceinline__ int tab_scan(const Ctx<W> &c, const int *tab, int bas
             const uint32_t s1 = bp + e.y + (uint32_t)c.col[4 * q + 1];
             const uint32_t s2 = bp + e.z + (uint32_t)c.col[4 * q + 2];
             const uint32_t s3 = bp + e.w + (uint32_t)c.col[4 * q + 3];
+            const int h0 = (int)(s0 >> 16), h1 = (int)(s1 >> 16), h2 = (int)(s2 >> 16), h3 = (int)(s3 >> 16);
             const int v = 8 * q;
-            a0 = max(a0, max(lds_off(reinterpret_cast<const int *>(lut), s0 & 0xFFFFu) * one + (31 - v),
-                             lds_off(reinterpret_cast<const int *>(lut), __umulhi(s0, 0x10000u)) * one + (30 - v)));
-            a1 = max(a1, max(lds_off(reinterpret_cast<const int *>(lut), s1 & 0xFFFFu) * one + (29 - v),
-                             lds_off(reinterpret_cast<const int *>(lut), __umulhi(s1, 0x10000u)) * one + (28 - v)));
-            a2 = max(a2, max(lds_off(reinterpret_cast<const int *>(lut), s2 & 0xFFFFu) * one + (27 - v),
-                             lds_off(reinterpret_cast<const int *>(lut), __umulhi(s2, 0x10000u)) * one + (26 - v)));
-            a3 = max(a3, max(lds_off(reinterpret_cast<const int *>(lut), s3 & 0xFFFFu) * one + (25 - v),
-                             lds_off(reinterpret_cast<const int *>(lut), __umulhi(s3, 0x10000u)) * one + (24 - v)));
+            a0 = max(a0, max(lds_off(lut, (int)s0 + h0 * negk) * one + (31 - v), lds_off(lut, h0) * one + (30 - v)));
+            a1 = max(a1, max(lds_off(lut, (int)s1 + h1 * negk) * one + (29 - v), lds_off(lut, h1) * one + (28 - v)));
+            a2 = max(a2, max(lds_off(lut, (int)s2 + h2 * negk) * one + (27 - v), lds_off(lut, h2) * one + (26 - v)));
+            a3 = max(a3, max(lds_off(lut, (int)s3 + h3 * negk) * one + (25 - v), lds_off(lut, h3) * one + (24 - v)));
         }
         return max(max(a0, a1), max(a2, a3));
     }
@@ -807,6 +810,7 @@ __device__ __forceinline__ Ctx<W> make_ctx(const DevTopo &topo, const DevPattern
     c.xs = xs;
     c.lut = pid * 3 * xs * xs;
     c.one = sh().one;
+    c.negk = c.one * -65536;
     sc &= 3;
     const bool useU = sc == SEL_INSENS;
     const int w12 = sc == SEL_BASE ? 0 : 12;
