@@ -291,6 +291,7 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, in
         }
     }
     if (!canon || !tb.pcon) cnt += (unsigned long long)nt;
+    __syncwarp();  // lanes still reading fw / dl in consider_deep are done before the next push writes them
 }
 
 __device__ __forceinline__ uint32_t perm_count_d(int n, int d) {
