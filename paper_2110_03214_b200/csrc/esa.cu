@@ -3,6 +3,8 @@
 // instantiated per W by esa_w8.cu, esa_w16.cu, esa_w32.cu.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace mapa {
@@ -12,7 +14,7 @@ namespace mapa {
                            int, void *);                                                                     \
     int occ_single_w##W(int, int, int);                                                                      \
     int launch_batch_w##W(const MultiTables &, int, int64_t, const mapa_query *, mapa_record *, uint32_t *,  \
-                          int, void *);                                                                      \
+                          const uint32_t *, int, void *);                                                    \
     int occ_batch_w##W(int, int);                                                                            \
     int launch_trace_w##W(const MultiTables &, int, int, int, const mapa_trace_op *, int, const mapa_query *, \
                           uint64_t *, void *);                                                               \
@@ -32,13 +34,77 @@ int launch_single(const SingleTables &tb, int sc, const mapa_query *d_query, map
 }
 
 int launch_batch(const MultiTables &tb, int canon, int64_t nq, const mapa_query *d_queries, mapa_record *d_results,
-                 uint32_t *d_ctr, int grid, void *stream) {
+                 uint32_t *d_ctr, const uint32_t *d_perm, int grid, void *stream) {
     switch (tb.topo.width) {
-        case 8: return launch_batch_w8(tb, canon, nq, d_queries, d_results, d_ctr, grid, stream);
-        case 16: return launch_batch_w16(tb, canon, nq, d_queries, d_results, d_ctr, grid, stream);
-        case 32: return launch_batch_w32(tb, canon, nq, d_queries, d_results, d_ctr, grid, stream);
+        case 8: return launch_batch_w8(tb, canon, nq, d_queries, d_results, d_ctr, d_perm, grid, stream);
+        case 16: return launch_batch_w16(tb, canon, nq, d_queries, d_results, d_ctr, d_perm, grid, stream);
+        case 32: return launch_batch_w32(tb, canon, nq, d_queries, d_results, d_ctr, d_perm, grid, stream);
     }
     return (int)cudaErrorInvalidValue;
+}
+
+namespace {
+
+// Code path of a batch query: (k - 1) * 4 + selector code (32 buckets; a bad
+// pattern index goes to bucket 0 and is flagged by the batch kernel).
+__device__ __forceinline__ int bucket_of(const mapa_query &q, const BucketKeys &bk) {
+    if (q.pattern >= (uint32_t)bk.npats) return 0;
+    return ((int)bk.k[q.pattern] - 1) * 4 + sel_code(q.selector, q.sensitive);
+}
+
+// Pass 1: per-bucket counts (warp-aggregated atomics).
+__global__ void bucket_count(BucketKeys bk, long long nq, const mapa_query *__restrict__ qs,
+                             unsigned int *__restrict__ cnt) {
+    const int lane = threadIdx.x & 31;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < nq; base += stride) {
+        const long long q = base + lane;
+        const int key = q < nq ? bucket_of(qs[q], bk) : 32;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
+        if (key < 32 && lane == __ffs(peers) - 1) atomicAdd(&cnt[key], (unsigned)__popc(peers));
+    }
+}
+
+// Pass 2: scatter query indices to their bucket's slice of perm (order inside
+// a bucket is arbitrary; results do not depend on it).
+__global__ void bucket_scatter(BucketKeys bk, long long nq, const mapa_query *__restrict__ qs,
+                               const unsigned int *__restrict__ cnt, unsigned int *__restrict__ cursor,
+                               uint32_t *__restrict__ perm) {
+    __shared__ unsigned int start[33];
+    if (threadIdx.x < 32) {
+        const unsigned c = cnt[threadIdx.x];
+        unsigned incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if ((int)threadIdx.x >= o) incl += v;
+        }
+        start[threadIdx.x] = incl - c;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < nq; base += stride) {
+        const long long q = base + lane;
+        const int key = q < nq ? bucket_of(qs[q], bk) : 32;
+        const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
+        const int leader = __ffs(peers) - 1;
+        unsigned off = 0;
+        if (key < 32 && lane == leader) off = atomicAdd(&cursor[key], (unsigned)__popc(peers));
+        off = __shfl_sync(0xFFFFFFFFu, off, leader);
+        if (key < 32) perm[start[key] + off + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)q;
+    }
+}
+
+}  // namespace
+
+int launch_bucket(const BucketKeys &bk, int64_t nq, const mapa_query *d_queries, unsigned int *d_cnt,
+                  unsigned int *d_cursor, uint32_t *d_perm, void *stream) {
+    const int grid = (int)std::min<int64_t>(1184, (nq + 255) / 256);
+    if (grid <= 0) return 0;
+    bucket_count<<<grid, 256, 0, (cudaStream_t)stream>>>(bk, (long long)nq, d_queries, d_cnt);
+    bucket_scatter<<<grid, 256, 0, (cudaStream_t)stream>>>(bk, (long long)nq, d_queries, d_cnt, d_cursor, d_perm);
+    return (int)cudaGetLastError();
 }
 
 int launch_trace(const MultiTables &tb, int canon, int ntraces, int nops, const mapa_trace_op *d_ops, int njobs,

@@ -1025,7 +1025,7 @@ __device__ __forceinline__ bool key_fits(int W, const DevPattern &P) { return 15
 template <int W, int CANON>
 __global__ void __launch_bounds__(kBlock, 2)
 esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query *__restrict__ qs,
-          mapa_record *__restrict__ res, uint32_t *__restrict__ ctr) {
+          mapa_record *__restrict__ res, uint32_t *__restrict__ ctr, const uint32_t *__restrict__ perm) {
     constexpr int G = 32 / W;
     const int lane = threadIdx.x & 31;
     const int xs = tb.xs;
@@ -1039,7 +1039,10 @@ esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query
         if (lane == 0) base = atomicAdd(reinterpret_cast<unsigned long long *>(ctr), (unsigned long long)G);
         base = __shfl_sync(kFull, base, 0);
         if (base >= nslots) break;
-        const unsigned long long q = base / W;  // G | W: every group of the warp has the same query
+        // G | W: every group of the warp has the same query.  Queries are taken
+        // in `perm` order (bucketed by code path: consecutive warps run the same
+        // (K, selector) instantiation, which keeps the instruction cache warm)
+        const unsigned long long q = perm ? (unsigned long long)perm[base / W] : base / W;
         const mapa_query qu = qs[q];
         const uint32_t pid = qu.pattern;
         if (pid >= (uint32_t)tb.npats || !key_fits(W, tb.pat[pid < (uint32_t)tb.npats ? pid : 0])) {

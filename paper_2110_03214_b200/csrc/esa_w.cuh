@@ -107,17 +107,18 @@ int MAPA_CAT(occ_single_w, MAPA_W)(int K, int sc, int smem) {
 }
 
 int MAPA_CAT(launch_batch_w, MAPA_W)(const MultiTables &tb, int canon, int64_t nq, const mapa_query *d_queries,
-                                     mapa_record *d_results, uint32_t *d_ctr, int grid, void *stream) {
+                                     mapa_record *d_results, uint32_t *d_ctr, const uint32_t *d_perm, int grid,
+                                     void *stream) {
     const int smem = smem_bytes(tb);
     const void *f = canon ? (const void *)esa_batch<MAPA_W, 1> : (const void *)esa_batch<MAPA_W, 0>;
     int err = set_smem(f, smem);
     if (err) return err;
     if (canon)
         esa_batch<MAPA_W, 1><<<grid, kBlock, smem, (cudaStream_t)stream>>>(tb, (long long)nq, d_queries, d_results,
-                                                                         d_ctr);
+                                                                         d_ctr, d_perm);
     else
         esa_batch<MAPA_W, 0><<<grid, kBlock, smem, (cudaStream_t)stream>>>(tb, (long long)nq, d_queries, d_results,
-                                                                         d_ctr);
+                                                                         d_ctr, d_perm);
     return (int)cudaGetLastError();
 }
 

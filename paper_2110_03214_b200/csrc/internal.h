@@ -120,7 +120,14 @@ struct DeepTables {
 int launch_single(const SingleTables &tb, int sc, const mapa_query *d_query, mapa_record *d_record, int depth,
                   int rank, int world, int stripe, int grid, void *stream);
 int launch_batch(const MultiTables &tb, int canon, int64_t nq, const mapa_query *d_queries,
-                 mapa_record *d_results, uint32_t *d_ctr, int grid, void *stream);
+                 mapa_record *d_results, uint32_t *d_ctr, const uint32_t *d_perm, int grid, void *stream);
+// Batch query order by code path (counting sort by (k, selector) bucket).
+struct BucketKeys {
+    int32_t npats;
+    uint8_t k[kMaxPats];
+};
+int launch_bucket(const BucketKeys &bk, int64_t nq, const mapa_query *d_queries, unsigned int *d_cnt,
+                  unsigned int *d_cursor, uint32_t *d_perm, void *stream);
 int launch_trace(const MultiTables &tb, int canon, int ntraces, int nops, const mapa_trace_op *d_ops, int njobs,
                  const mapa_query *d_jobs, uint64_t *d_keys, void *stream);
 // deep path (esa_deep.cu); sc = sel_code | 4 * canonical

@@ -1231,12 +1231,25 @@ mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *cons
     int err;
     if (nq == 0) return MAPA_OK;
     if ((err = (int)cudaMemsetAsync(d_results, 0, (size_t)nq * sizeof(mapa_record), st))) return cuda_fail(err, "memset");
-    if ((err = (int)cudaMemsetAsync(d_scratch, 0, 64, st))) return cuda_fail(err, "memset");
+    // scratch: [0,64) slot counter, [64,192) bucket counts, [192,320) bucket
+    // cursors, [512, 512 + 4 nq) the query order (bucketed by code path)
+    if ((err = (int)cudaMemsetAsync(d_scratch, 0, 512, st))) return cuda_fail(err, "memset");
+    uint32_t *perm = nullptr;
+    if (nq < (1ll << 32)) {
+        BucketKeys bk{};
+        bk.npats = tbp->npats;
+        for (int i = 0; i < tbp->npats; ++i) bk.k[i] = tbp->pat[i].k;
+        char *sc = (char *)d_scratch;
+        perm = (uint32_t *)(sc + 512);
+        if ((err = launch_bucket(bk, nq, d_queries, (unsigned int *)(sc + 64), (unsigned int *)(sc + 192), perm,
+                                 stream)))
+            return cuda_fail(err, "bucket launch");
+    }
     int sm = device_sm_count();
     if (sm <= 0) sm = 148;
     const int canon = multi_has_constraints(*tbp);
     const int grid = sm * max_blocks_per_sm_batch(t->width, canon, tbp->npats, tbp->xs);
-    err = launch_batch(*tbp, canon, nq, d_queries, d_results, (uint32_t *)d_scratch, grid, stream);
+    err = launch_batch(*tbp, canon, nq, d_queries, d_results, (uint32_t *)d_scratch, perm, grid, stream);
     if (err) return cuda_fail(err, "esa_batch launch");
     return MAPA_OK;
 }

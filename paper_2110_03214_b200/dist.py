@@ -150,7 +150,7 @@ def run_batch(topo: Topology, pats, queries, raw: bool = False, stream=None):
     """queries: int32[nq,4] device tensor -> int64[nq,4] device records."""
     nq = queries.shape[0]
     res = torch.empty((max(nq, 1), 4), dtype=torch.int64, device=queries.device)
-    scratch = torch.empty(8, dtype=torch.int64, device=queries.device)
+    scratch = torch.empty(64 + (nq + 1) // 2, dtype=torch.int64, device=queries.device)  # >= 512 + 4 nq bytes
     allocate_batch(topo, pats, nq, queries.data_ptr(), res.data_ptr(), scratch.data_ptr(), raw=raw, stream=stream)
     return res[:nq]
 

@@ -335,6 +335,31 @@ def test_batch_vs_oracle_and_counts():
                      (name, i, raw))
 
 
+def test_batch_mixed_code_paths_and_bad_index():
+    """Queries of every (k, selector) code path interleaved with bad pattern
+    indices: the device bucketing by code path leaves every record where its
+    query is (status 1 only for the bad ones, the rest equal to the oracle)."""
+    o, t = mo.builtin("dgx1v"), mp.Topology("dgx1v")
+    shapes = [("full", 1), ("ring", 2), ("ring", 3), ("tree", 4), ("ringtree", 5), ("full", 6), ("ring", 7)]
+    pats = [mp.Pattern.make(s, k) for s, k in shapes]
+    rng = random.Random(17)
+    rows, exp = [], []
+    for i in range(3000):
+        pi = rng.randrange(len(shapes) + 1)
+        busy = rng.randrange(0, 256) & rng.randrange(0, 256)
+        sel, sens = rng.choice(SELS)
+        rows.append((busy, pi if pi < len(shapes) else 99, sel, sens))
+        exp.append(None if pi == len(shapes) else (busy, shapes[pi], sel, sens))
+    recs = md.records_from_tensor(md.run_batch(t, pats, md.queries_tensor(rows), raw=True))
+    for i in rng.sample(range(len(rows)), 200):
+        if exp[i] is None:
+            assert recs[i].status == 1 and recs[i].key == 0
+            continue
+        busy, (shape, k), sel, sens = exp[i]
+        d = mp.decode(t, pats[rows[i][1]], busy, sel, sens, recs[i], raw=True)
+        same(oracle(o, busy, shape, k, sel, sens, use_c=True), d, (i, shape, k, hex(busy), sel, sens))
+
+
 def _trace_inputs(topo_name, seed, policy):
     jobs = W.c2_jobs(seed, 1000)
     n = mo.builtin(topo_name).n
