@@ -1,3 +1,4 @@
+import importlib.util
 import os
 import sys
 
@@ -8,9 +9,26 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+def _ensure_built():
+    """Fresh checkouts have no libmapa.so / liboracle.so (build artefacts are
+    not in git): build whichever is MISSING before collection.  An existing
+    library is used as is (a copied tree may not preserve mtimes; rebuilding
+    is `__graft_entry__.build()`'s job)."""
+    if not os.path.exists(os.path.join(ROOT, "paper_2110_03214_b200", "libmapa.so")):
+        spec = importlib.util.spec_from_file_location("_mapa_build", os.path.join(ROOT, "paper_2110_03214_b200",
+                                                                                 "_build.py"))
+        b = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(b)
+        b.build()
+    if not os.path.exists(os.path.join(ROOT, "oracle", "liboracle.so")):
+        from oracle import coracle
+        coracle.build()
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (run with -m gpu)")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+    _ensure_built()
 
 
 @pytest.fixture(scope="session")
