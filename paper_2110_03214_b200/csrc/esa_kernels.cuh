@@ -46,6 +46,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstddef>
+
 #include "internal.h"
 
 namespace mapa {
@@ -81,7 +83,7 @@ struct SelT {
 // Leaves of a k-2 scan are ranked by one int: (score + 1) * 32 + (31 - v).
 // Invalid leaves (vertex k-1 on the device of k-2, a lex-leader violation,
 // a padding lane) get kNeg added through the tables.
-constexpr int kNeg = -(1 << 28);
+constexpr int kNeg = kNegTable;
 
 // Per-warp candidate lists of the innermost DFS levels (G groups x W).
 struct WarpLists {
@@ -861,27 +863,19 @@ __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int 
     if (tid < kMaxN) s.cm[tid] = make_uint4(topo.cm[tid][0], topo.cm[tid][1], topo.cm[tid][2], topo.cm[tid][3]);
     if (tid == 0) s.one = 1;
     if (tid <= kMaxN) s.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
-    const int sent = xs * xs;
-    for (int i = tid; i < kNN; i += blockDim.x) {
-        const int v = i >> 5, b = i & 31;
-        int w = kNeg, d = 0;
-        if (v != b && v < topo.n && b < topo.n) {
-            if ((topo.cm[b][0] >> v) & 1u) { w = 50; d = xs; }
-            else if ((topo.cm[b][1] >> v) & 1u) { w = 25; d = 1; }
-            else if ((topo.cm[b][2] >> v) & 1u) { w = 20; d = 1; }
-            else w = 12;
+    static_assert(offsetof(Shared, ts0d) == offsetof(Shared, tw) + 9 * kNN * sizeof(int), "pair tables contiguous");
+    if (tb.pre) {
+        // cached image (host-built once per topology and xs): 16-B loads from L2
+        int4 *dst = reinterpret_cast<int4 *>(s.tw);
+        for (int i = tid; i < kPairTables * kNN / 4; i += blockDim.x) dst[i] = tb.pre[i];
+    } else {
+        int *pt = &s.tw[0];  // the ten tables, contiguous (asserted above)
+        for (int i = tid; i < kNN; i += blockDim.x) {
+            int e[kPairTables];
+            pair_table_entry(topo, i, xs, e);
+#pragma unroll
+            for (int t = 0; t < kPairTables; ++t) pt[t * kNN + i] = e[t];
         }
-        const bool bad = w == kNeg, badd = bad || v >= b;
-        s.tw[i] = bad ? kNeg : 32 * w;
-        s.tz[i] = bad ? kNeg : 0;
-        s.twd[i] = badd ? kNeg : 32 * w;
-        s.tzd[i] = badd ? kNeg : 0;
-        s.twp[i] = bad ? 0 : w;
-        s.tdl[i] = d;
-        s.tse[i] = 4 * (d + (bad ? sent : 0));  // byte offsets (see scan_dense)
-        s.tsed[i] = 4 * (d + (badd ? sent : 0));
-        s.ts0[i] = 4 * (bad ? sent : 0);
-        s.ts0d[i] = 4 * (badd ? sent : 0);
     }
     int *lut = sh_lut();
     for (int p = 0; p < tb.npats; ++p) {

@@ -54,6 +54,34 @@ struct alignas(8) DevPattern {
 };
 static_assert(sizeof(DevPattern) == 64, "DevPattern layout");
 
+// The ten 32x32 pair tables of the narrow kernels' shared memory (order and
+// meaning: esa_kernels.cuh `Shared`), built per CTA, or copied from a cached
+// device image built once per (topology, Eq. 2 row stride) on the host.
+constexpr int kNegTable = -(1 << 28);
+constexpr int kPairTables = 10;
+inline __host__ __device__ void pair_table_entry(const DevTopo &topo, int i, int xs, int out[kPairTables]) {
+    const int v = i >> 5, b = i & 31;
+    const int sent = xs * xs;
+    int w = kNegTable, d = 0;
+    if (v != b && v < topo.n && b < topo.n) {
+        if ((topo.cm[b][0] >> v) & 1u) { w = 50; d = xs; }
+        else if ((topo.cm[b][1] >> v) & 1u) { w = 25; d = 1; }
+        else if ((topo.cm[b][2] >> v) & 1u) { w = 20; d = 1; }
+        else w = 12;
+    }
+    const bool bad = w == kNegTable, badd = bad || v >= b;
+    out[0] = bad ? kNegTable : 32 * w;            // tw
+    out[1] = bad ? kNegTable : 0;                 // tz
+    out[2] = badd ? kNegTable : 32 * w;           // twd
+    out[3] = badd ? kNegTable : 0;                // tzd
+    out[4] = bad ? 0 : w;                         // twp
+    out[5] = d;                                   // tdl
+    out[6] = 4 * (d + (bad ? sent : 0));          // tse (byte offsets, see scan_dense)
+    out[7] = 4 * (d + (badd ? sent : 0));         // tsed
+    out[8] = 4 * (bad ? sent : 0);                // ts0
+    out[9] = 4 * (badd ? sent : 0);               // ts0d
+}
+
 constexpr int kMaxParts = 64;
 template <int MAXP, int LUTCAP>
 struct Tables {
@@ -62,6 +90,7 @@ struct Tables {
     int32_t xs;      // row stride of the Eq. 2 tables on the device (16 if every m <= 15, else 32)
     int32_t npart;   // Topo-aware partitions (trace kernel; SPEC select_topo_aware)
     int32_t pad;
+    const int4 *pre; // device image of the ten pair tables for (topo, xs), or null (built per CTA)
     uint32_t part[kMaxParts];  // device masks, smallest first, ties by lowest device
     DevPattern pat[MAXP];
     uint16_t lut[LUTCAP];

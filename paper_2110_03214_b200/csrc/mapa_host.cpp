@@ -42,6 +42,8 @@ struct mapa_topology {
     void *d_stage = nullptr;      // device: query (16 B) + record (32 / 64 B)
     void *h_stage = nullptr;      // pinned host mirror
     cudaStream_t cap = nullptr;   // private stream for graph capture (the caller's may be the legacy stream)
+    struct PairTab { int xs, dev; void *d; };
+    std::vector<PairTab> pair_tabs;  // device images of the narrow kernels' pair tables, per (xs, device)
     std::vector<GraphEntry> graphs;
     uint64_t tick = 0;
 };
@@ -410,6 +412,37 @@ mapa_status cuda_fail(int err, const char *what) {
     return fail(MAPA_E_CUDA, std::string(what) + ": " + cuda_error_string(err));
 }
 
+// Device image of the ten pair tables for (topology, Eq. 2 row stride xs) on
+// the current device, built once (the single-query kernels copy it into
+// shared memory instead of recomputing it in every CTA).  Null on failure:
+// the kernel then builds the tables itself.
+const int4 *pair_tables(const mapa_topology *tc, int xs, void *stream) {
+    mapa_topology *t = const_cast<mapa_topology *>(tc);  // a cache of immutable data
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    for (auto &pt : t->pair_tabs)
+        if (pt.xs == xs && pt.dev == dev) return (const int4 *)pt.d;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing((cudaStream_t)stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+        return nullptr;  // never allocate inside a capture (mapa_allocate warms the cache first)
+    DevTopo dt;
+    fill_devtopo(t, dt);
+    std::vector<int> img((size_t)kPairTables * kMaxN * kMaxN);
+    for (int i = 0; i < kMaxN * kMaxN; ++i) {
+        int e[kPairTables];
+        pair_table_entry(dt, i, xs, e);
+        for (int k = 0; k < kPairTables; ++k) img[(size_t)k * kMaxN * kMaxN + i] = e[k];
+    }
+    void *d = nullptr;
+    if (cudaMalloc(&d, img.size() * sizeof(int)) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, img.data(), img.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaFree(d);
+        return nullptr;
+    }
+    t->pair_tabs.push_back({xs, dev, d});
+    return (const int4 *)d;
+}
+
 struct Plan {
     int depth, chunk, grid;
     uint64_t nlocal;
@@ -437,10 +470,18 @@ Plan plan_single(const mapa_topology *t, const mapa_pattern *p, int sensk, int n
     // Items = prefixes of depth D; guided self-scheduling balances ~8 items
     // per resident W-lane group, and D = k-3 (one inner3 call per item) is
     // reached whenever that gives enough items.
+    // Going deeper than k-3 trades the lane-parallel inner3 path for more,
+    // smaller items; do it only when a rank would have fewer items than
+    // resident groups at k-3 (a sharded launch has 1/world of the items, so
+    // the balance target alone would push every multi-rank launch deeper:
+    // C4 at world 8 measured 59 us per kernel at k-2 vs ~28 us at k-3).
     const uint64_t target = 8ull * resident_warps * G * (uint64_t)world;
     int dmax = k <= 1 ? 0 : std::max(1, std::min(k - 2, 4));
     int d = k <= 1 ? 0 : 1;
-    while (d < dmax && perm_count(nF, d) < target) ++d;
+    while (d < dmax && perm_count(nF, d) < target) {
+        if (d >= k - 3 && perm_count(nF, d) >= resident_warps * G * (uint64_t)world) break;
+        ++d;
+    }
     pl.depth = d;
     const uint64_t items = nF >= k ? perm_count(nF, d) : 0;
     pl.nlocal = items;
@@ -451,7 +492,7 @@ Plan plan_single(const mapa_topology *t, const mapa_pattern *p, int sensk, int n
                                  : std::max<uint64_t>(1, (items + 64ull * world - 1) / (64ull * world));
     pl.chunk = (int)std::min<uint64_t>(stripe, 1u << 30);
     const uint64_t local = (items + world - 1) / world;
-    const uint64_t blocks = std::max<uint64_t>(1, (local + 8 * 2 * G - 1) / (8 * 2 * G));
+    const uint64_t blocks = std::max<uint64_t>(1, (local + 8 * G - 1) / (8 * G));  // >= 1 item per group
     pl.grid = (int)std::min<uint64_t>(blocks, (uint64_t)sm * occ);
     return pl;
 }
@@ -892,6 +933,7 @@ mapa_status mapa_load_topology(const char *spec, int32_t is_text, mapa_topology 
 void mapa_free_topology(mapa_topology *t) {
     if (!t) return;
     for (auto &g : t->graphs) cudaGraphExecDestroy(g.exec);
+    for (auto &pt : t->pair_tabs) cudaFree(pt.d);
     if (t->cap) cudaStreamDestroy(t->cap);
     if (t->d_stage) cudaFree(t->d_stage);
     if (t->h_stage) cudaFreeHost(t->h_stage);
@@ -1026,6 +1068,7 @@ static mapa_status launch_query_impl(const mapa_topology *t, const mapa_pattern 
     tb.npats = 1;
     tb.xs = pick_xs(p->m);
     fill_devpattern(p, (flags & MAPA_F_RAW) != 0, 0, tb.pat[0]);
+    tb.pre = pair_tables(t, tb.xs, stream);
     // canonical instantiation only when a lex-leader constraint exists (|Aut| > 1
     // and not RAW); otherwise the constraint-free kernel enumerates the same set
     const int sc = sel_code(selector, sensitive) | (has_constraints(tb.pat[0]) ? 4 : 0) |
@@ -1180,6 +1223,7 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
         if (g.key[0] == key[0] && g.key[1] == key[1] && g.key[2] == key[2]) { exec = g.exec; g.tick = ++t->tick; break; }
     if (!exec) {
         // first call for this key: capture the sequence on a private stream
+        if (!deep) pair_tables(t, pick_xs(p->m), stream);  // cudaMalloc / sync copy: not inside the capture
         if (deep && sel_code(selector, sens) == SEL_SENS) {
             mapa_status su = upload_lut(p);  // synchronous: not inside the capture
             if (su != MAPA_OK) return su;
