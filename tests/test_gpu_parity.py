@@ -360,6 +360,34 @@ def test_batch_mixed_code_paths_and_bad_index():
         same(oracle(o, busy, shape, k, sel, sens, use_c=True), d, (i, shape, k, hex(busy), sel, sens))
 
 
+def test_launch_query_inside_user_cuda_graph():
+    """mapa_launch_query is capturable into the caller's CUDA graph.  With a
+    fresh topology the cached pair-table image cannot be allocated during the
+    capture, so the kernel builds its tables itself: the replayed record must
+    equal a normal launch's (which uses the cached image)."""
+    text = W.het32_text()
+    ref_t = mp.Topology(text=text)
+    p = mp.Pattern.make("ring", 5)
+    busy = 0x00F0000F
+    for sel, sens in SELS:
+        rec0, _q0 = md.run_query(ref_t, p, sel, sens, busy, raw=True)
+        torch.cuda.synchronize()
+        ref = md.records_from_tensor(rec0)[0]
+        t = mp.Topology(text=text)  # empty cache
+        q = md.query_tensor(busy, 0, sel, sens)
+        rec = torch.zeros(4, dtype=torch.int64, device="cuda")
+        s = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                mp.launch_query(t, p, sel, sens, q.data_ptr(), rec.data_ptr(), raw=True, busy_hint=busy, stream=s)
+        for _ in range(2):
+            g.replay()
+        torch.cuda.synchronize()
+        got = md.records_from_tensor(rec)[0]
+        assert (got.key, got.leaves) == (ref.key, ref.leaves), (sel, sens)
+
+
 def _trace_inputs(topo_name, seed, policy):
     jobs = W.c2_jobs(seed, 1000)
     n = mo.builtin(topo_name).n
