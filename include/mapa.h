@@ -330,9 +330,10 @@ mapa_status mapa_decode_wide(const mapa_topology *t, const mapa_pattern *p, uint
  * d_queries[nq] -> d_results[nq] records.  pats[npats] (npats <= 16, every
  * pattern k <= 8 and sum of (m+1)^2 rank-table entries <= 4096).
  * d_scratch: >= 512 + 4*nq bytes of device memory (work counter, and the
- * query order: queries are bucketed by code path -- (k, selector) -- with a
- * device counting sort before the batch kernel, so consecutive warps run the
- * same kernel instantiation; results do not depend on the order).
+ * query order: with more than one pattern, queries are bucketed by code path
+ * -- (k, selector) -- with a device counting sort before the batch kernel, so
+ * consecutive warps run the same kernel instantiation; results do not depend
+ * on the order).
  * Asynchronous on cuda_stream.  A query with a bad pattern index or an
  * unsupported key budget gets record.status = 1 and key 0. */
 mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *const *pats,

@@ -1279,7 +1279,7 @@ mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *cons
     // cursors, [512, 512 + 4 nq) the query order (bucketed by code path)
     if ((err = (int)cudaMemsetAsync(d_scratch, 0, 512, st))) return cuda_fail(err, "memset");
     uint32_t *perm = nullptr;
-    if (nq < (1ll << 32)) {
+    if (nq < (1ll << 32) && tbp->npats > 1) {  // one pattern: <= 4 code paths, nothing to gain
         BucketKeys bk{};
         bk.npats = tbp->npats;
         for (int i = 0; i < tbp->npats; ++i) bk.k[i] = tbp->pat[i].k;
