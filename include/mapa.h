@@ -170,7 +170,7 @@ typedef struct {
     uint32_t lock;       /* merge lock (scratch) */
     uint32_t status;     /* 0 ok; nonzero = device-side argument error */
     uint32_t pad;
-    uint64_t reserved;
+    uint64_t reserved;   /* scratch: running max of (score << 32 | set >> 32), filters the merges */
 } mapa_wide_record;
 
 /* Trace op (C2 replay): op 0 = ALLOC job, 1 = RELEASE job. */
@@ -282,6 +282,19 @@ mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int
                               int32_t sensitive, const mapa_query *d_query, mapa_record *d_record,
                               uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint,
                               void *cuda_stream);
+
+/* nq independent single queries, each a full-GPU mapa_launch_query (narrow
+ * path), from ONE call: zeroes d_records[nq] once, forks `nstreams` internal
+ * streams (owned by the topology, created on first use) from cuda_stream
+ * with an event, launches query i on stream i % nstreams (its busy mask
+ * from h_queries[i] plans the grid; the kernel reads d_queries[i]), and makes
+ * cuda_stream wait for all of them: ordered like one launch on cuda_stream,
+ * with small queries' launch and drain overlapping.  pats[npats] indexed by
+ * the query's `pattern`.  Errors as mapa_launch_query (the first failing
+ * query's; earlier launches stay enqueued). */
+mapa_status mapa_launch_queries(mapa_topology *t, const mapa_pattern *const *pats, int32_t npats, int32_t nq,
+                                const mapa_query *h_queries, const mapa_query *d_queries, mapa_record *d_records,
+                                uint32_t flags, int32_t nstreams, void *cuda_stream);
 
 /* Host: combine n shard records (max key, sum leaves). */
 mapa_status mapa_reduce_records(const mapa_record *records, int32_t n, mapa_record *out);

@@ -115,6 +115,8 @@ _SIGS = {
     "mapa_launch_query": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.c_uint32,
                                ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, _vp]),
     "mapa_reduce_records": (_S, [ctypes.POINTER(Record), ctypes.c_int32, ctypes.POINTER(Record)]),
+    "mapa_launch_queries": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(Query),
+                                 _vp, _vp, ctypes.c_uint32, ctypes.c_int32, _vp]),
     "mapa_launch_query_wide": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.c_uint32,
                                     ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, _vp]),
     "mapa_reduce_wide_records": (_S, [ctypes.POINTER(WideRecord), ctypes.c_int32, ctypes.POINTER(WideRecord)]),
@@ -384,6 +386,17 @@ def decode_wide(topo: Topology, pat: Pattern, busy: int, selector: int, sensitiv
     _check(_lib.mapa_decode_wide(topo.handle, pat.handle, busy, selector, int(bool(sensitive)), _flags(raw),
                                  ctypes.byref(record), ctypes.byref(d)), allow_no_capacity=True)
     return decision_dict(d)
+
+
+def launch_queries(topo: Topology, pats, rows, d_queries_ptr: int, d_records_ptr: int, raw: bool = False,
+                   nstreams: int = 8, stream=None):
+    """mapa_launch_queries: independent full-GPU single-query launches for
+    rows [(busy, pattern index, selector, sensitive)] over `nstreams`
+    internal streams, ordered like one launch on `stream` (asynchronous)."""
+    arr = (_vp * len(pats))(*[p.handle for p in pats])
+    hq = (Query * max(1, len(rows)))(*[Query(b & 0xFFFFFFFF, pi, sel, int(bool(sens))) for b, pi, sel, sens in rows])
+    _check(_lib.mapa_launch_queries(topo.handle, arr, len(pats), len(rows), hq, d_queries_ptr, d_records_ptr,
+                                    F_RAW if raw else 0, nstreams, _stream_ptr(stream)))
 
 
 def record_from_bytes(b: bytes) -> Record:

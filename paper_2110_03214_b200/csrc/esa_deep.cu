@@ -34,6 +34,8 @@
 // m <= 120), Eq. 3 PreservedBW = T_F - sum inc_F(S) + inside(S).
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "internal.h"
 
 namespace mapa {
@@ -480,7 +482,13 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
             }
         }
         if (c) atomicAdd(reinterpret_cast<unsigned long long *>(&rec->leaves), c);
-        if (h) {
+        // Filter before the lock: (score, top 32 bits of the set word) orders
+        // keys consistently with the full 256-bit order, so a CTA whose packed
+        // value is below the running maximum cannot win and skips the
+        // serialised merge (without it every CTA took the lock: ~640 us per
+        // launch at 444 CTAs).
+        const unsigned long long packed = ((unsigned long long)hs << 32) | (h >> 32);
+        if (h && atomicMax(reinterpret_cast<unsigned long long *>(&rec->reserved), packed) <= packed) {
             while (atomicCAS(&rec->lock, 0u, 1u) != 0u) {
             }
             __threadfence();
@@ -577,12 +585,18 @@ int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_
 }
 
 int max_blocks_per_sm_deep(int n, int nterm, int sc, int lut_bytes) {
+    // cached per (mask width, term class, selector code, rank-table size)
+    static int cache[2][3][8][9] = {};
+    const int mi = n <= 32 ? 0 : 1, ti = nt_class(nterm) / 2 - 1, li = std::min(8, (lut_bytes + 4095) / 4096);
+    int &slot = cache[mi][ti][sc & 7][li];
+    if (slot) return slot;
     const void *f = n <= 32 ? pick_fn<uint32_t>(nterm, sc) : pick_fn<unsigned long long>(nterm, sc);
-    const int smem = (int)sizeof(DeepShared) + lut_bytes;
+    const int smem = (int)sizeof(DeepShared) + li * 4096;  // the bucket's upper bound
     if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmemMax) != cudaSuccess) return 1;
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kBlockD, smem) != cudaSuccess) return 1;
-    return nb > 0 ? nb : 1;
+    slot = nb > 0 ? nb : 1;
+    return slot;
 }
 
 }  // namespace mapa

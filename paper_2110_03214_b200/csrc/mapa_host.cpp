@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <new>
 #include <sstream>
 #include <string>
@@ -42,6 +43,12 @@ struct mapa_topology {
     void *d_stage = nullptr;      // device: query (16 B) + record (32 / 64 B)
     void *h_stage = nullptr;      // pinned host mirror
     cudaStream_t cap = nullptr;   // private stream for graph capture (the caller's may be the legacy stream)
+    std::vector<cudaStream_t> side;  // mapa_launch_queries' fork streams
+    // deep-path launch plans (suffix length, tuple table, terms, depth, grid)
+    // keyed by (pattern uid, selector code, |F|, N, world): planning costs
+    // far more host time than a small deep launch
+    struct DeepPlanEntry { uint64_t key[3]; DeepTables tb; int sc, depth, stripe, grid; uint64_t tick; };
+    std::vector<std::unique_ptr<DeepPlanEntry>> deep_plans;
     struct PairTab { int xs, dev; void *d; };
     std::vector<PairTab> pair_tabs;  // device images of the narrow kernels' pair tables, per (xs, device)
     std::vector<GraphEntry> graphs;
@@ -567,12 +574,17 @@ int build_tuples(const mapa_pattern *p, int L, int r, bool canon, uint32_t *out,
         // order by the largest index, so that the tuples using only the first
         // r' devices form a prefix of the table (a node whose common lower
         // bound leaves r' devices scans tcount[r'] entries)
+        // (a stable counting sort on the largest index: O(n + r))
+        std::vector<uint32_t> tmp(out, out + n);
+        std::vector<int> start(r + 1, 0);
         auto mx = [L](uint32_t w) {
             uint32_t m = 0;
             for (int l = 0; l < L; ++l) m = std::max(m, (w >> (8 * l)) & 0xFFu);
             return m;
         };
-        std::stable_sort(out, out + n, [&](uint32_t a, uint32_t b) { return mx(a) < mx(b); });
+        for (int i = 0; i < n; ++i) ++start[mx(tmp[i]) + 1];
+        for (int v = 0; v < r; ++v) start[v + 1] += start[v];
+        for (int i = 0; i < n; ++i) out[start[mx(tmp[i])]++] = tmp[i];
     }
     return n;
 }
@@ -611,7 +623,13 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
         const int NT = nterm <= 2 ? 2 : (nterm <= 4 ? 4 : 6);
         const double node = 40.0 + 12.0 * L + (nes ? 6.0 * ((r * 16 + 31) / 32) : 0.0) + 6.0 * k;
         const double round = 12.0 + 3.0 * NT;
-        const double cost = (node + round * ((nt + 31) / 32)) / nt;
+        double cost = (node + round * ((nt + 31) / 32)) / nt;
+        // parallelism: the warps can only split the prefix levels 0..k-L-1
+        // (decoded items); with fewer prefixes than ~4 per resident warp of
+        // every rank, most warps idle
+        const uint64_t want = 4ull * 148 * 3 * 8 * (uint64_t)world;
+        const uint64_t avail = perm_count(nF, std::min(k - L, 6));
+        if (avail < want) cost *= (double)want / (double)std::max<uint64_t>(1, avail);
         if (cost < best * 0.98) { best = cost; bestL = L; }
     }
     if (!bestL) return fail(MAPA_E_UNSUPPORTED, "deep path: no feasible suffix length");
@@ -632,14 +650,18 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     if (canon)
         for (int l = 0; l < L; ++l)
             if (p->src[T + l] & pmask & ~common) tb->pcon = 1;
-    for (int rr = 0; rr <= kMaxNDeep; ++rr) {
-        int c = 0;
+    {   // tcount[r'] = #tuples with largest index < r' (histogram + prefix sum)
+        int hist[kMaxNDeep + 1] = {0};
         for (int i = 0; i < tb->ntup; ++i) {
             uint32_t m = 0;
             for (int l = 0; l < L; ++l) m = std::max(m, (tb->tup[i] >> (8 * l)) & 0xFFu);
-            if ((int)m < rr) ++c;
+            ++hist[m + 1 <= (uint32_t)kMaxNDeep ? m + 1 : kMaxNDeep];
         }
-        tb->tcount[rr] = c;
+        int c = 0;
+        for (int rr = 0; rr <= kMaxNDeep; ++rr) {
+            c += hist[rr];
+            tb->tcount[rr] = c;
+        }
     }
     pl->sc = base | (canon ? 4 : 0);
     // decoded prefix depth: enough items for ~8 per resident warp (x world)
@@ -934,6 +956,7 @@ void mapa_free_topology(mapa_topology *t) {
     if (!t) return;
     for (auto &g : t->graphs) cudaGraphExecDestroy(g.exec);
     for (auto &pt : t->pair_tabs) cudaFree(pt.d);
+    for (auto s2 : t->side) cudaStreamDestroy(s2);
     if (t->cap) cudaStreamDestroy(t->cap);
     if (t->d_stage) cudaFree(t->d_stage);
     if (t->h_stage) cudaFreeHost(t->h_stage);
@@ -1083,6 +1106,47 @@ static mapa_status launch_query_impl(const mapa_topology *t, const mapa_pattern 
     return MAPA_OK;
 }
 
+mapa_status mapa_launch_queries(mapa_topology *t, const mapa_pattern *const *pats, int32_t npats, int32_t nq,
+                                const mapa_query *h_queries, const mapa_query *d_queries, mapa_record *d_records,
+                                uint32_t flags, int32_t nstreams, void *stream) {
+    if (!t || !pats || nq < 0 || (nq > 0 && (!h_queries || !d_queries || !d_records)) || nstreams < 1 || nstreams > 32)
+        return fail(MAPA_E_INVALID_ARG, "bad arguments");
+    if (nq == 0) return MAPA_OK;
+    cudaStream_t main = (cudaStream_t)stream;
+    int err;
+    while ((int)t->side.size() < nstreams) {
+        cudaStream_t s2;
+        if ((err = (int)cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking))) return cuda_fail(err, "cudaStreamCreate");
+        t->side.push_back(s2);
+    }
+    for (int i = 0; i < npats; ++i)  // warm the table cache outside the fork (it may allocate)
+        if (pats[i] && key_fits(t, pats[i])) pair_tables(t, pick_xs(pats[i]->m), stream);
+    if ((err = (int)cudaMemsetAsync(d_records, 0, (size_t)nq * sizeof(mapa_record), main))) return cuda_fail(err, "memset");
+    cudaEvent_t fork, join;
+    if ((err = (int)cudaEventCreateWithFlags(&fork, cudaEventDisableTiming))) return cuda_fail(err, "cudaEventCreate");
+    cudaEventRecord(fork, main);
+    for (int s2 = 0; s2 < nstreams; ++s2) cudaStreamWaitEvent(t->side[s2], fork, 0);
+    mapa_status st = MAPA_OK;
+    for (int i = 0; i < nq && st == MAPA_OK; ++i) {
+        const mapa_query &q = h_queries[i];
+        if ((int)q.pattern >= npats || !pats[q.pattern]) { st = fail(MAPA_E_INVALID_ARG, "query pattern index out of range"); break; }
+        if (q.selector < 0 || q.selector > 2) { st = fail(MAPA_E_INVALID_ARG, "bad selector"); break; }
+        st = launch_query_impl(t, pats[q.pattern], q.selector, q.sensitive, d_queries + i, d_records + i, flags, 0, 1,
+                               q.busy, (void *)t->side[i % nstreams], false);
+    }
+    if ((err = (int)cudaEventCreateWithFlags(&join, cudaEventDisableTiming))) {
+        cudaEventDestroy(fork);
+        return cuda_fail(err, "cudaEventCreate");
+    }
+    for (int s2 = 0; s2 < nstreams; ++s2) {  // join: every side stream's work before `main` continues
+        cudaEventRecord(join, t->side[s2]);
+        cudaStreamWaitEvent(main, join, 0);
+    }
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+    return st;
+}
+
 mapa_status mapa_reduce_records(const mapa_record *records, int32_t n, mapa_record *out) {
     if (!records || !out || n < 1) return fail(MAPA_E_INVALID_ARG, "bad records");
     mapa_record r;
@@ -1123,14 +1187,37 @@ static mapa_status launch_query_wide_impl(const mapa_topology *t, const mapa_pat
     if (err) return cuda_fail(err, "cudaMemsetAsync");
     if (p->k > nF) return MAPA_OK;  // no capacity: the zeroed record says so (key 0)
     static_assert(sizeof(DeepTables) < 32000, "kernel parameter block too large");
-    static thread_local DeepTables *tbp = nullptr;  // ~10 KB: keep off the stack
-    if (!tbp) tbp = new DeepTables();
-    DeepPlan pl{};
-    mapa_status s = plan_deep(t, p, selector, sensitive, flags, nF, world, tbp, &pl);
-    if (s != MAPA_OK) return s;
+    mapa_topology *tm = const_cast<mapa_topology *>(t);  // plan cache (immutable inputs)
+    const bool canon_req = !(flags & MAPA_F_RAW);
+    const uint64_t key[3] = {p->uid, (uint64_t)sel_code(selector, sensitive) | ((uint64_t)canon_req << 3),
+                             (uint64_t)nF | ((uint64_t)t->n << 8) | ((uint64_t)world << 16)};
+    mapa_topology::DeepPlanEntry *e = nullptr;
+    for (auto &x : tm->deep_plans)
+        if (x->key[0] == key[0] && x->key[1] == key[1] && x->key[2] == key[2]) { e = x.get(); break; }
+    mapa_status s;
+    if (!e) {
+        std::unique_ptr<mapa_topology::DeepPlanEntry> ne(new (std::nothrow) mapa_topology::DeepPlanEntry());
+        if (!ne) return fail(MAPA_E_INVALID_ARG, "out of memory");
+        DeepPlan pl{};
+        s = plan_deep(t, p, selector, sensitive, flags, nF, world, &ne->tb, &pl);
+        if (s != MAPA_OK) return s;
+        std::memcpy(ne->key, key, sizeof(key));
+        ne->sc = pl.sc; ne->depth = pl.depth; ne->stripe = pl.stripe; ne->grid = pl.grid;
+        if (tm->deep_plans.size() >= 16) {  // evict the least recently used
+            auto lru = std::min_element(tm->deep_plans.begin(), tm->deep_plans.end(),
+                                        [](const std::unique_ptr<mapa_topology::DeepPlanEntry> &a2,
+                                           const std::unique_ptr<mapa_topology::DeepPlanEntry> &b2) {
+                                            return a2->tick < b2->tick;
+                                        });
+            tm->deep_plans.erase(lru);
+        }
+        tm->deep_plans.push_back(std::move(ne));
+        e = tm->deep_plans.back().get();
+    }
+    e->tick = ++tm->tick;
     if (sel_code(selector, sensitive) == SEL_SENS && (s = upload_lut(p)) != MAPA_OK) return s;
-    err = launch_deep(*tbp, pl.sc, (const uint16_t *)p->d_lut, d_query, d_record, pl.depth, rank, world,
-                      pl.stripe, pl.grid, stream);
+    err = launch_deep(e->tb, e->sc, (const uint16_t *)p->d_lut, d_query, d_record, e->depth, rank, world,
+                      e->stripe, e->grid, stream);
     if (err) return cuda_fail(err, "esa_deep launch");
     return MAPA_OK;
 }

@@ -19,7 +19,7 @@ import struct
 import torch
 import torch.distributed as dist
 
-from . import (Pattern, Record, Topology, WideRecord, decode, decode_wide, launch_query, launch_query_wide,
+from . import (Pattern, Record, Topology, WideRecord, decode, decode_wide, launch_query, launch_queries, launch_query_wide,
                allocate_batch, reduce_records, reduce_wide_records, trace_replay, SEL_PRESERVE)
 
 U32 = 0xFFFFFFFF
@@ -60,6 +60,19 @@ def run_query(topo: Topology, pat: Pattern, selector: int, sensitive: bool, busy
     launch_query(topo, pat, selector, sensitive, q.data_ptr(), rec.data_ptr(), raw=raw, rank=rank, world=world,
                  busy_hint=busy, stream=stream, prune=prune)
     return rec, q
+
+
+def run_queries(topo: Topology, pats, rows, raw: bool = False, nstreams: int = 8, stream=None):
+    """Independent single-query launches (the full GPU per query) through ONE
+    mapa_launch_queries call: the library spreads them over `nstreams`
+    internal streams so small queries' launch / drain overlap, ordered like a
+    single launch on `stream`.  rows: [(busy, pattern index, selector,
+    sensitive)].  Returns int64[nq, 4] records (device) without synchronising."""
+    cur = stream or torch.cuda.current_stream()
+    q = queries_tensor(rows, device=cur.device)
+    recs = torch.empty((max(1, len(rows)), 4), dtype=torch.int64, device=cur.device)
+    launch_queries(topo, pats, rows, q.data_ptr(), recs.data_ptr(), raw=raw, nstreams=nstreams, stream=cur)
+    return recs[:len(rows)]
 
 
 def combine_records(rec: torch.Tensor, group=None) -> Record:

@@ -451,3 +451,25 @@ def test_c3_sampled_vs_oracle():
         if picked >= 40:
             break
     assert picked >= 20
+
+
+def test_run_queries_multistream_vs_oracle():
+    """md.run_queries (independent launches over 8 streams): every record
+    decodes to the oracle's decision, counts = closed forms."""
+    o, t = mo.builtin("cubemesh16"), mp.Topology("cubemesh16")
+    keys = [(s, k) for s in ("ring", "tree", "full") for k in (3, 4, 5)]
+    pats = [mp.Pattern.make(s, k) for s, k in keys]
+    rng = random.Random(33)
+    rows = []
+    for _ in range(120):
+        ki = rng.randrange(len(keys))
+        busy = rng.randrange(0, 1 << 16) | 0xFF
+        sel, sens = rng.choice(SELS)
+        rows.append((busy, ki, sel, sens))
+    recs = md.records_from_tensor(md.run_queries(t, pats, rows, raw=True))
+    for (busy, ki, sel, sens), r in zip(rows, recs):
+        shape, k = keys[ki]
+        nf = 16 - bin(busy).count("1")
+        assert r.leaves == (math.perm(nf, k) if k <= nf else 0)
+        d = mp.decode(t, pats[ki], busy, sel, sens, r, raw=True)
+        same(oracle(o, busy, shape, k, sel, sens, use_c=True), d, (shape, k, hex(busy), sel, sens))
