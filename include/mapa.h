@@ -317,7 +317,15 @@ mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint64_t 
  * warp-uniform explicit-stack DFS over the first k-L pattern vertices, then
  * the last L vertices (L = 1..4, chosen on the host) as a lane-parallel scan
  * over a table of index tuples into the remaining free devices.  RAW and
- * canonical modes as for the narrow path; MAPA_F_PRUNE is ignored.
+ * canonical modes as for the narrow path.  MAPA_F_PRUNE (Greedy only; the
+ * other selectors ignore it): branch and bound with exact Eq. 1 bounds -- a
+ * prefix subtree is skipped when its score so far plus, for every pattern edge
+ * from a placed vertex into the unplaced part, the best free link of that
+ * vertex's device, plus (edges inside the unplaced part) x (best free pair) is
+ * below the best score published by any lane (the record's reserved word); a
+ * node's suffix scan is skipped when the sum of its tables' maxima is below it.
+ * Strict tests: the decision equals the exhaustive one; leaves counts what was
+ * scored (the decision's raw / distinct are then the closed forms).
  * Errors: INVALID_ARG, UNSUPPORTED (k > 16), CUDA. */
 mapa_status mapa_launch_query_wide(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
                                    int32_t sensitive, const mapa_query64 *d_query, mapa_wide_record *d_record,

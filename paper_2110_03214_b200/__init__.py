@@ -365,12 +365,13 @@ def launch_query(topo: Topology, pat: Pattern, selector: int, sensitive: bool, d
 
 
 def launch_query_wide(topo: Topology, pat: Pattern, selector: int, sensitive: bool, d_query_ptr: int,
-                      d_record_ptr: int, busy: int, raw: bool = False, rank: int = 0, world: int = 1, stream=None):
+                      d_record_ptr: int, busy: int, raw: bool = False, rank: int = 0, world: int = 1, stream=None,
+                      prune: bool = False):
     """mapa_launch_query_wide: deep-path device-resident launch (asynchronous);
     d_query_ptr -> mapa_query64; busy must equal its busy mask (it sizes the
     suffix tables)."""
     _check(_lib.mapa_launch_query_wide(topo.handle, pat.handle, selector, int(bool(sensitive)), d_query_ptr,
-                                       d_record_ptr, _flags(raw), rank, world, busy, _stream_ptr(stream)))
+                                       d_record_ptr, _flags(raw, prune), rank, world, busy, _stream_ptr(stream)))
 
 
 def reduce_wide_records(records) -> WideRecord:
@@ -381,9 +382,9 @@ def reduce_wide_records(records) -> WideRecord:
 
 
 def decode_wide(topo: Topology, pat: Pattern, busy: int, selector: int, sensitive: bool, record: WideRecord,
-                raw: bool = False) -> dict:
+                raw: bool = False, prune: bool = False) -> dict:
     d = Decision()
-    _check(_lib.mapa_decode_wide(topo.handle, pat.handle, busy, selector, int(bool(sensitive)), _flags(raw),
+    _check(_lib.mapa_decode_wide(topo.handle, pat.handle, busy, selector, int(bool(sensitive)), _flags(raw, prune),
                                  ctypes.byref(record), ctypes.byref(d)), allow_no_capacity=True)
     return decision_dict(d)
 

@@ -62,6 +62,8 @@ struct DeepShared {
     unsigned long long cm[kND][3];
     int tw[kND * kND];         // [v*64 + b] pair value: w(v,b) (Eq. 1/3), census delta (Eq. 2), 0 if v == b
     int incF[kND];             // inc_F(v) (Eq. 3)
+    int maxw[kND];             // branch and bound: max_{u in F, u != v} w(u, v)
+    int gmax;                  // branch and bound: max over free pairs
     uint32_t magic[kND + 4];
     DeepWarp w[kWarpsD];
     unsigned long long rk[kWarpsD][5];
@@ -134,7 +136,8 @@ __device__ __forceinline__ bool key_gt(uint32_t s0, unsigned long long a0, unsig
 // in lex order over C(k,2) -> bit C(k,2)-1-p.  Updates the lane's best key
 // and threshold.
 __device__ __forceinline__ void consider_deep(const DeepTables &tb, const DeepWarp &W, DBest &b, int &thr,
-                                              uint32_t s, unsigned long long U, uint32_t x, int T) {
+                                              uint32_t s, unsigned long long U, uint32_t x, int T,
+                                              unsigned long long *gpub) {
     const int L = tb.L;
     unsigned long long S = U;
 #pragma unroll
@@ -157,6 +160,7 @@ __device__ __forceinline__ void consider_deep(const DeepTables &tb, const DeepWa
         else elo |= 1ull << q;
     }
     if (key_gt(s, set, ehi, elo, b.score, b.set, b.ehi, b.elo)) {
+        if (gpub && s > b.score) atomicMax(gpub, (unsigned long long)s << 32);  // branch and bound: publish
         b.score = s;
         b.set = set;
         b.ehi = ehi;
@@ -191,9 +195,10 @@ __device__ __forceinline__ M allowed(const DeepTables &tb, int d, int myf, int l
 // All leaves below a node whose prefix 0..T-1 is placed (set U, score A).
 template <typename M, int NT, int SEL>
 __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, int myf, int lane, int warp, int T,
-                                       DBest &bst, int &thr, unsigned long long &cnt) {
+                                       DBest &bst, int &thr, unsigned long long &cnt, unsigned long long *gpub) {
     constexpr int base = SEL & 3;
     constexpr bool canon = (SEL & 4) != 0;
+    constexpr bool prune = (SEL & 8) != 0;
     DeepShared &S = dsh();
     DeepWarp &W = S.w[warp];
     const int L = tb.L;
@@ -268,6 +273,26 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, in
     const int nt = tb.tcount[r];
     const char *ab = reinterpret_cast<const char *>(W.area);
     const int A0 = A * tb.scale;
+    if constexpr (prune) {
+        // table bound: every tuple's score <= A + sum over its terms of the
+        // largest entry its table can hold; strict test against the grid best
+        int ub = A0;
+        for (int q = 0; q < tb.nterm; ++q) {
+            int mx = kNegTable;
+            if (tb.term[q][0] == 0) {
+                for (int i = lane; i < r; i += 32) mx = max(mx, W.area[kND * tb.term[q][1] + i]);
+            } else {
+                for (int p = lane; p < r * 16; p += 32)
+                    if ((p & 15) < r) mx = max(mx, W.area[kWtOff + (p >> 4) * kWtStride + (p & 15)]);
+            }
+            ub += __reduce_max_sync(kFullD, mx);
+        }
+        const unsigned gb = (unsigned)(*reinterpret_cast<volatile unsigned long long *>(gpub) >> 32);
+        if (ub < (int)gb * tb.scale) {  // scaled units (Eq. 3 pair folding)
+            __syncwarp();
+            return;  // no tuple of this node can reach the best score found anywhere
+        }
+    }
     for (int t0 = 0; t0 < nt; t0 += 32) {
         const int t = t0 + lane;
         bool valid = t < nt;
@@ -289,7 +314,7 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, in
         if (valid && s >= thr) {
             const int sc = tb.scale;
             const uint32_t sr = sc == 1 ? (uint32_t)s : (sc == 2 ? (uint32_t)s >> 1 : (uint32_t)s / 3u);
-            consider_deep(tb, W, bst, thr, sr, (unsigned long long)U, e.x, T);
+            consider_deep(tb, W, bst, thr, sr, (unsigned long long)U, e.x, T, prune ? gpub : nullptr);
         }
     }
     if (!canon || !tb.pcon) cnt += (unsigned long long)nt;
@@ -354,8 +379,25 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
                   8 * popc<M>((M)tb.cm[tid][2] & F);
         S.incF[tid] = inc;
     }
+    constexpr bool prune = (SEL & 8) != 0;
     if (tid == 0 && nF != tb.r + T && tb.k <= nF) atomicOr(&rec->status, 2u);  // busy_hint mismatch
     __syncthreads();
+    if constexpr (prune) {  // per-device best free link and the best free pair (tw is complete now)
+        if (tid < kND) {
+            int mw = 0;
+            if (tid < n && ((F >> tid) & 1u))
+                for (int u = 0; u < n; ++u)
+                    if (u != tid && ((F >> u) & 1u)) mw = max(mw, S.tw[u * kND + tid]);
+            S.maxw[tid] = mw;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int g2 = __reduce_max_sync(kFullD, max(S.maxw[lane], S.maxw[lane + 32]));
+            if (lane == 0) S.gmax = g2;
+        }
+        __syncthreads();
+    }
+    unsigned long long *gpub = prune ? reinterpret_cast<unsigned long long *>(&rec->reserved) : nullptr;
     int acc0 = 0;
     if constexpr (base == SEL_INSENS) acc0 = __reduce_add_sync(kFullD, S.incF[lane] + S.incF[lane + 32]) / 2;  // T_F
 
@@ -421,7 +463,7 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
             }
             if (!ok) continue;
             if (D == T) {
-                suffix<M, NT, SEL>(tb, F, U, acc, myf, lane, warp, T, bst, thr, cnt);
+                suffix<M, NT, SEL>(tb, F, U, acc, myf, lane, warp, T, bst, thr, cnt, gpub);
                 continue;
             }
             // explicit-stack DFS over levels D..T-1 (lane d holds level d)
@@ -443,8 +485,21 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
                 if (lane == d) { myf = v; mycand = cand; myacc = a; }
                 if (lane == 0) S.w[warp].fw[d] = v;
                 U |= bit<M>(v);
+                if constexpr (prune) {
+                    // subtree bound after placing 0..d (Eq. 1): every pattern edge
+                    // from a placed vertex j to the unplaced part <= the best free
+                    // link of f(j); every edge inside the unplaced part <= gmax
+                    const int nd = d + 1;
+                    const int c = lane < nd ? __popc((uint32_t)tb.adj[lane] >> nd) * S.maxw[myf] : 0;
+                    const int ub = a + __reduce_add_sync(kFullD, c) + (int)tb.c2[nd] * S.gmax;
+                    const unsigned gb = (unsigned)(*reinterpret_cast<volatile unsigned long long *>(gpub) >> 32);
+                    if (ub < (int)gb) {
+                        U &= ~bit<M>(v);
+                        continue;  // skip the subtree: try the next candidate of level d
+                    }
+                }
                 if (d + 1 == T) {
-                    suffix<M, NT, SEL>(tb, F, U, a, myf, lane, warp, T, bst, thr, cnt);
+                    suffix<M, NT, SEL>(tb, F, U, a, myf, lane, warp, T, bst, thr, cnt, gpub);
                     U &= ~bit<M>(v);
                 } else {
                     ++d;
@@ -527,6 +582,10 @@ using DeepFn = int (*)(const DeepTables &, const uint16_t *, const mapa_query64 
 
 template <typename M, int NT>
 DeepFn pick_sel(int sc) {
+    switch (sc & 15) {  // branch and bound: Greedy (8, 12)
+        case 8: return launch_t<M, NT, 8>;
+        case 12: return launch_t<M, NT, 12>;
+    }
     switch (sc & 7) {
         case 0: return launch_t<M, NT, 0>;
         case 1: return launch_t<M, NT, 1>;
@@ -541,6 +600,10 @@ DeepFn pick_sel(int sc) {
 
 template <typename M, int NT>
 const void *pick_fn_sel(int sc) {
+    switch (sc & 15) {
+        case 8: return (const void *)esa_deep<M, NT, 8>;
+        case 12: return (const void *)esa_deep<M, NT, 12>;
+    }
     switch (sc & 7) {
         case 0: return (const void *)esa_deep<M, NT, 0>;
         case 1: return (const void *)esa_deep<M, NT, 1>;
@@ -586,9 +649,9 @@ int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_
 
 int max_blocks_per_sm_deep(int n, int nterm, int sc, int lut_bytes) {
     // cached per (mask width, term class, selector code, rank-table size)
-    static int cache[2][3][8][9] = {};
+    static int cache[2][3][16][9] = {};
     const int mi = n <= 32 ? 0 : 1, ti = nt_class(nterm) / 2 - 1, li = std::min(8, (lut_bytes + 4095) / 4096);
-    int &slot = cache[mi][ti][sc & 7][li];
+    int &slot = cache[mi][ti][sc & 15][li];
     if (slot) return slot;
     const void *f = n <= 32 ? pick_fn<uint32_t>(nterm, sc) : pick_fn<unsigned long long>(nterm, sc);
     const int smem = (int)sizeof(DeepShared) + li * 4096;  // the bucket's upper bound

@@ -141,6 +141,9 @@ struct DeepTables {
     uint16_t back[kMaxKDeep];  // back[u] bit j: pattern edge (j, u), j < u
     uint16_t src[kMaxKDeep];   // src[u] bit j: canonical f(j) < f(u) (0 in RAW mode)
     uint8_t edge[kMaxEdges];   // pattern edges a | b << 4
+    uint16_t adj[kMaxKDeep];   // pattern adjacency (branch and bound)
+    uint8_t c2[kMaxKDeep + 1]; // c2[d]: pattern edges with both endpoints >= d (branch and bound)
+    uint8_t pad1[3];
     uint32_t tup[kMaxTup];
 };
 

@@ -609,6 +609,12 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
         tb->src[u] = canon ? p->src[u] : 0;
     }
     for (int e = 0; e < p->m; ++e) tb->edge[e] = (uint8_t)(p->edges[e].first | (p->edges[e].second << 4));
+    for (int u = 0; u < k; ++u) tb->adj[u] = p->adj[u];
+    for (int d = 0; d <= k; ++d) {
+        int c = 0;
+        for (auto &e : p->edges) c += (e.first >= d && e.second >= d);
+        tb->c2[d] = (uint8_t)c;
+    }
     // suffix length L: smallest modelled cost per leaf (node overhead + rounds of 32 lanes)
     double best = 1e30;
     int bestL = 0;
@@ -663,7 +669,10 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
             tb->tcount[rr] = c;
         }
     }
-    pl->sc = base | (canon ? 4 : 0);
+    // branch and bound (MAPA_F_PRUNE): Greedy only.  (An Eq. 3 variant with
+    // the bound (k-1) maxw[v] - inc_F(v) per later vertex was exact but pruned
+    // nothing on cubemesh16 and cost 20-40 %: not dispatched.)
+    pl->sc = base | (canon ? 4 : 0) | ((flags & MAPA_F_PRUNE) && base == SEL_GREEDY ? 8 : 0);
     // decoded prefix depth: enough items for ~8 per resident warp (x world)
     int sm = device_sm_count();
     if (sm <= 0) sm = 148;
@@ -774,14 +783,21 @@ mapa_status decode_wide(const mapa_topology *t, const mapa_pattern *p, uint64_t 
     d.ecode[0] = rec->ecode_hi;
     d.ecode[1] = rec->ecode_lo;
     d.leaves_scored = rec->leaves;
-    if (flags & MAPA_F_RAW) {
+    const uint64_t F = ~busy & nmask_of(t->n);
+    if ((flags & MAPA_F_PRUNE) && selector == MAPA_SEL_GREEDY) {
+        // the pruned kernel scores a subset; the totals are the closed forms
+        uint64_t perm = 1;
+        const int nf = __builtin_popcountll(F);
+        for (int i = 0; i < p->k; ++i) perm *= (uint64_t)std::max(0, nf - i);
+        d.raw_embeddings = perm;
+        d.distinct_matches = perm / p->aut;
+    } else if (flags & MAPA_F_RAW) {
         d.raw_embeddings = rec->leaves;
         d.distinct_matches = rec->leaves / p->aut;
     } else {
         d.distinct_matches = rec->leaves;
         d.raw_embeddings = rec->leaves * p->aut;
     }
-    const uint64_t F = ~busy & nmask_of(t->n);
     if (rec->status != 0) return fail(MAPA_E_INVALID_ARG, "device reported a bad query (busy_hint != d_query->busy?)");
     if (rec->set == 0) {
         d.status = MAPA_NO_CAPACITY;
@@ -1189,7 +1205,8 @@ static mapa_status launch_query_wide_impl(const mapa_topology *t, const mapa_pat
     static_assert(sizeof(DeepTables) < 32000, "kernel parameter block too large");
     mapa_topology *tm = const_cast<mapa_topology *>(t);  // plan cache (immutable inputs)
     const bool canon_req = !(flags & MAPA_F_RAW);
-    const uint64_t key[3] = {p->uid, (uint64_t)sel_code(selector, sensitive) | ((uint64_t)canon_req << 3),
+    const uint64_t key[3] = {p->uid, (uint64_t)sel_code(selector, sensitive) | ((uint64_t)canon_req << 3) |
+                                         ((uint64_t)((flags & MAPA_F_PRUNE) != 0) << 4),
                              (uint64_t)nF | ((uint64_t)t->n << 8) | ((uint64_t)world << 16)};
     mapa_topology::DeepPlanEntry *e = nullptr;
     for (auto &x : tm->deep_plans)
@@ -1287,7 +1304,7 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
     }
     cudaStream_t st = (cudaStream_t)stream;
     const size_t rbytes = deep ? sizeof(mapa_wide_record) : sizeof(mapa_record);
-    const uint32_t lflags = deep ? (flags & ~MAPA_F_PRUNE) : flags;
+    const uint32_t lflags = flags;
     // the sequence issued on stream `s2`
     auto issue = [&](cudaStream_t s2) -> mapa_status {
         int e2;

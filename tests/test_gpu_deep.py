@@ -252,3 +252,55 @@ def test_deep_n64_all_free_clique_and_narrow_refusal():
     with pytest.raises(mp.MapaError) as ei:
         mp.launch_query(t, mp.Pattern.make("ring", 3), 0, False, q.data_ptr(), rec.data_ptr(), busy_hint=0)
     assert ei.value.status == mp.E_UNSUPPORTED
+
+
+def test_deep_prune_equals_exhaustive():
+    """Deep branch and bound (MAPA_F_PRUNE, Greedy): the decision equals the
+    exhaustive deep search's and the deep C oracle's (small cases), fewer leaves
+    are scored, and raw / distinct are the closed forms."""
+    rng = random.Random(2024)
+    for name in ("cubemesh16", "torus2d16"):
+        o = mo.builtin(name)
+        t = mp.Topology(name)
+        for shape, k in (("ring", 9), ("tree", 10), ("ringtree", 11), ("ring", 12), ("full", 9), ("ring", 5)):
+            busy = sum(1 << d for d in rng.sample(range(16), rng.randint(0, 16 - k)))
+            nf = 16 - bin(busy).count("1")
+            p = mp.Pattern.make(shape, k)
+            t.set_busy(busy)
+            for sel, sens in ((0, False), (1, False)):  # Preserve-insensitive: the flag is ignored
+                for raw in (False, True):
+                    if raw and math.perm(nf, k) > 3e10:
+                        continue
+                    ex = mp.allocate(t, p, sel, sens, raw=raw, deep=True)
+                    pr = mp.allocate(t, p, sel, sens, raw=raw, deep=True, prune=True)
+                    for f in FIELDS + ("distinct", "pred_effbw", "key", "ecode"):
+                        assert pr[f] == ex[f], (name, shape, k, hex(busy), sel, raw, f)
+                    assert pr["leaves"] <= ex["leaves"]
+                if math.perm(nf, k) <= 2e7:
+                    kk, e = mo.make_pattern(shape, k)
+                    same(co.allocate_deep(o, busy, kk, e, sel, sens, max_subsets=200000), pr,
+                         (name, shape, k, hex(busy), sel))
+
+
+def test_deep_prune_n64_and_sharded():
+    """Branch and bound on het64 (u64 masks) and across virtual ranks: the
+    combined pruned record decodes to the exhaustive decision."""
+    text = W.het64_text()
+    t = mp.Topology(text=text)
+    busy = ((1 << 64) - 1) & ~sum(1 << d for d in (1, 5, 9, 12, 20, 33, 40, 41, 47, 50, 58, 63))
+    p = mp.Pattern.make("ring", 10)
+    t.set_busy(busy)
+    ex = mp.allocate(t, p, 0, False, deep=True)
+    pr = mp.allocate(t, p, 0, False, deep=True, prune=True)
+    for f in FIELDS + ("key", "ecode"):
+        assert pr[f] == ex[f], f
+    recs = []
+    for rank in range(3):
+        q = md.query64_tensor(busy, 0, False)
+        rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+        mp.launch_query_wide(t, p, 0, False, q.data_ptr(), rec.data_ptr(), busy, rank=rank, world=3, prune=True)
+        torch.cuda.synchronize()
+        recs.append(md.wide_records_from_tensor(rec)[0])
+    d = mp.decode_wide(t, p, busy, 0, False, mp.reduce_wide_records(recs), prune=True)
+    for f in FIELDS + ("key", "ecode"):
+        assert d[f] == ex[f], f
