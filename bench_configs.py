@@ -308,19 +308,21 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
         if rank == 0 and world == 1:
             # the paper's overhead study (fig:preserve_policy_overhead): milliseconds per
             # allocation for 9+ GPU jobs on 16-GPU graphs; Greedy with MAPA_F_PRUNE (exact), end to end
+            # (Preserve-insensitive: set search over the full-k pattern + cached lex-smallest labelling)
             for tname in ("cubemesh16", "torus2d16"):
                 tt = mp.Topology(tname)
                 for shape, kk in (("ring", 9), ("ring", 12), ("ring", 14), ("ring", 16), ("tree", 12), ("tree", 14)):
                     p2 = mp.Pattern.make(shape, kk)
-                    mp.allocate(tt, p2, 0, False, prune=True)
-                    ts = []
-                    for _ in range(5):
-                        t0 = time.perf_counter()
-                        d = mp.allocate(tt, p2, 0, False, prune=True)
-                        ts.append((time.perf_counter() - t0) * 1e3)
-                    pruned[f"{tname}_{shape}{kk}_greedy"] = {"ms_median": statistics.median(ts),
-                                                             "leaves_scored": d["leaves"], "distinct": d["distinct"],
-                                                             "agg_bw": d["agg_bw"]}
+                    for sel, sname in ((0, "greedy"), (1, "preserve_insensitive")):
+                        mp.allocate(tt, p2, sel, False, prune=True)
+                        ts = []
+                        for _ in range(5):
+                            t0 = time.perf_counter()
+                            d = mp.allocate(tt, p2, sel, False, prune=True)
+                            ts.append((time.perf_counter() - t0) * 1e3)
+                        pruned[f"{tname}_{shape}{kk}_{sname}"] = {
+                            "ms_median": statistics.median(ts), "leaves_scored": d["leaves"],
+                            "distinct": d["distinct"], "agg_bw": d["agg_bw"], "preserved_bw": d["preserved_bw"]}
         emb_s = 3 * per / (tot / 1e3)
         ach = 2 * emb_s / 1e9
         line["roofline"] = {"bound": "alu", "kernel": "esa_deep<NT,SEL> (ring-10 RAW)",

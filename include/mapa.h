@@ -324,6 +324,10 @@ mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint64_t 
  * vertex's device, plus (edges inside the unplaced part) x (best free pair) is
  * below the best score published by any lane (the record's reserved word); a
  * node's suffix scan is skipped when the sum of its tables' maxima is below it.
+ * mapa_allocate with MAPA_F_PRUNE and Preserve-insensitive on the deep path
+ * searches device SETS instead (Eq. 3 depends on the set only): the full-k
+ * pattern's decision gives the set, the pattern's lex-smallest labelling
+ * (weight independent, cached per pattern) gives the edges; exact.
  * Strict tests: the decision equals the exhaustive one; leaves counts what was
  * scored (the decision's raw / distinct are then the closed forms).
  * Errors: INVALID_ARG, UNSUPPORTED (k > 16), CUDA. */

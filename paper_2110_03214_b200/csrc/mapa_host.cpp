@@ -67,6 +67,11 @@ struct mapa_pattern {
     void *d_lut = nullptr;     // device copy of lut (deep kernel), uploaded on first use
     int d_lut_dev = -1;
     uint64_t uid = 0;          // unique per compiled pattern / model (graph cache key)
+    // Eq. 3 set search (deep path, MAPA_F_PRUNE): the full-k pattern, and the
+    // pattern's lex-smallest used-edge list over rank pairs (weight independent)
+    mapa_pattern *clique = nullptr;
+    bool have_ecode_min = false;
+    uint64_t ecode_min[2] = {0, 0};
 };
 
 namespace {
@@ -1049,6 +1054,7 @@ mapa_status mapa_make_pattern(int32_t shape, int32_t k, mapa_pattern **out) {
 
 void mapa_free_pattern(mapa_pattern *p) {
     if (!p) return;
+    if (p->clique) mapa_free_pattern(p->clique);
     if (p->d_lut) cudaFree(p->d_lut);
     delete p;
 }
@@ -1263,6 +1269,133 @@ mapa_status mapa_decode_wide(const mapa_topology *t, const mapa_pattern *p, uint
     return decode_wide(t, p, busy, selector, sens, flags, record, out);
 }
 
+// Is there a bijection sigma: V(P) -> {0..k-1} with, for every decided rank
+// pair p < np (lex order), [sigma^-1 of its ranks adjacent in P] == bit p?
+// Backtracking over ranks 0..k-1: rank i takes an unused pattern vertex whose
+// adjacency to the vertices of ranks j < i matches every decided pair (j, i),
+// and every placed rank's decided 1s / 0s towards the unplaced ranks must fit
+// its unplaced neighbours / non-neighbours (counting prune).  `budget` bounds
+// the nodes visited; -1 = budget exhausted (undecided).
+int labelling_exists(const mapa_pattern *p, const std::vector<int> &pidx, const uint8_t *bit, int np, int i,
+                     int *inv, uint32_t used, long long &budget) {
+    const int k = p->k;
+    if (i == k) return 1;
+    for (int u = 0; u < k; ++u) {
+        if ((used >> u) & 1u) continue;
+        if (--budget < 0) return -1;
+        bool ok = true;
+        for (int j = 0; j < i && ok; ++j) {
+            const int q = pidx[j * k + i];
+            if (q < np) ok = (((p->adj[inv[j]] >> u) & 1u) != 0) == (bit[q] != 0);
+        }
+        if (!ok) continue;
+        inv[i] = u;
+        const uint32_t used2 = used | (1u << u);
+        const int rest = k - i - 1;
+        for (int j = 0; j <= i && ok; ++j) {  // counting prune on every placed rank
+            int need1 = 0, need0 = 0;
+            for (int x = i + 1; x < k; ++x) {
+                const int q = pidx[j * k + x];
+                if (q < np) (bit[q] ? need1 : need0)++;
+            }
+            const int nb = __builtin_popcount((uint32_t)p->adj[inv[j]] & ~used2 & ((1u << k) - 1u));
+            ok = need1 <= nb && need0 <= rest - nb;
+        }
+        if (!ok) continue;
+        const int r = labelling_exists(p, pidx, bit, np, i + 1, inv, used2, budget);
+        if (r != 0) return r;
+    }
+    return 0;
+}
+
+// The pattern's lex-smallest used-edge list over rank pairs, as the 128-bit
+// edge code (bit C(k,2)-1-p for the p-th rank pair in lex order): maximise the
+// code bit by bit -- keep bit p set iff some labelling still satisfies every
+// decided pair (the greedy is exact for a lexicographic maximum).  Weight
+// independent: the tie-break among equal-score mappings of one device set.
+// Returns false if the search budget ran out (the caller then searches
+// exhaustively).
+bool lexmin_labelling(const mapa_pattern *p, uint64_t out[2]) {
+    const int k = p->k, eb = k * (k - 1) / 2;
+    std::vector<int> pidx((size_t)k * k, 0);
+    int q = 0;
+    for (int a2 = 0; a2 < k; ++a2)
+        for (int b2 = a2 + 1; b2 < k; ++b2) pidx[a2 * k + b2] = pidx[b2 * k + a2] = q++;
+    std::vector<uint8_t> bit(eb, 0);
+    int inv[kMaxKDeep];
+    int ones = 0;
+    long long budget = 20000000;  // nodes over all feasibility checks
+    for (int p2 = 0; p2 < eb; ++p2) {
+        bit[p2] = 1;
+        if (ones < p->m) {
+            const int r = labelling_exists(p, pidx, bit.data(), p2 + 1, 0, inv, 0u, budget);
+            if (r < 0) return false;
+            if (r == 1) {
+                ++ones;
+                continue;
+            }
+        }
+        bit[p2] = 0;
+    }
+    out[0] = out[1] = 0;
+    for (int p2 = 0; p2 < eb; ++p2)
+        if (bit[p2]) {
+            const int qq = eb - 1 - p2;
+            if (qq >= 64) out[0] |= 1ull << (qq - 64);
+            else out[1] |= 1ull << qq;
+        }
+    return true;
+}
+
+// Preserve-insensitive on the deep path with MAPA_F_PRUNE: Eq. 3 depends on
+// the device set only, so (1) the best set -- max PreservedBW, ties to the
+// lex-smallest set -- is the decision of the full-k pattern (one canonical
+// leaf per k-subset), and (2) every mapping of that set scores the same, so
+// the winning used-edge list is the pattern's lex-smallest one over rank
+// pairs, which does not depend on the weights: computed once per pattern on
+// the host (lexmin_labelling) and cached.  Same decision as the exhaustive
+// search (tests); leaves = the set search's leaves.
+static mapa_status allocate_insens_sets(mapa_topology *t, const mapa_pattern *pc, uint32_t flags, void *stream,
+                                 mapa_decision *out) {
+    mapa_pattern *p = const_cast<mapa_pattern *>(pc);  // caches of immutable derived data
+    const int k = p->k;
+    mapa_status s;
+    if (!p->have_ecode_min) {
+        if (!lexmin_labelling(p, p->ecode_min))  // budget exhausted: exhaustive deep search instead
+            return mapa_allocate(t, pc, MAPA_SEL_PRESERVE, 0, flags & ~(uint32_t)MAPA_F_PRUNE, stream, out);
+        p->have_ecode_min = true;
+    }
+    if (!p->clique) {
+        std::vector<std::pair<int, int>> all;
+        for (int a = 0; a < k; ++a)
+            for (int b = a + 1; b < k; ++b) all.push_back({a, b});
+        if ((s = compile_pattern(k, all, 0, &p->clique)) != MAPA_OK) return s;
+    }
+    const uint32_t sub = flags & ~(uint32_t)(MAPA_F_COMMIT | MAPA_F_PRUNE);
+    mapa_decision dc;
+    if ((s = mapa_allocate(t, p->clique, MAPA_SEL_PRESERVE, 0, sub, stream, &dc)) != MAPA_OK) return s;
+    const uint64_t extra = 0;
+    mapa_wide_record rec;
+    std::memset(&rec, 0, sizeof(rec));
+    rec.score = (uint64_t)(uint32_t)dc.score;
+    for (int d = 0; d < 64; ++d)
+        if ((dc.device_mask >> d) & 1ull) rec.set |= 1ull << (63 - d);
+    rec.ecode_hi = p->ecode_min[0];
+    rec.ecode_lo = p->ecode_min[1];
+    rec.leaves = dc.leaves_scored + extra;
+    mapa_decision d;
+    if ((s = decode_wide(t, p, t->busy, MAPA_SEL_PRESERVE, 0, flags & ~(uint32_t)MAPA_F_PRUNE, &rec, &d)) != MAPA_OK)
+        return s;
+    uint64_t perm = 1;  // counts: the closed forms (the search scored sets, not embeddings)
+    const int nf = __builtin_popcountll(~t->busy & nmask_of(t->n));
+    for (int i = 0; i < k; ++i) perm *= (uint64_t)std::max(0, nf - i);
+    d.raw_embeddings = perm;
+    d.distinct_matches = perm / p->aut;
+    if (flags & MAPA_F_COMMIT) t->busy |= d.device_mask;
+    *out = d;
+    return MAPA_OK;
+}
+
 mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selector, int32_t sens,
                           uint32_t flags, void *stream, mapa_decision *out) {
     if (!t || !p || !out) return fail(MAPA_E_INVALID_ARG, "null argument");
@@ -1276,6 +1409,8 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
         out->m = p->m;
         return MAPA_NO_CAPACITY;
     }
+    if (deep && selector == MAPA_SEL_PRESERVE && !sens && (flags & MAPA_F_PRUNE) && p->k >= 2)
+        return allocate_insens_sets(t, p, flags, stream, out);
     int err;
     if (!t->d_stage) {
         if ((err = (int)cudaMalloc(&t->d_stage, 128))) return cuda_fail(err, "cudaMalloc");
