@@ -1371,7 +1371,9 @@ static mapa_status allocate_insens_sets(mapa_topology *t, const mapa_pattern *pc
             for (int b = a + 1; b < k; ++b) all.push_back({a, b});
         if ((s = compile_pattern(k, all, 0, &p->clique)) != MAPA_OK) return s;
     }
-    const uint32_t sub = flags & ~(uint32_t)(MAPA_F_COMMIT | MAPA_F_PRUNE);
+    // canonical even under MAPA_F_RAW: the clique has one orbit per set, so the
+    // decision is the same and RAW would enumerate k! permutations of each set
+    const uint32_t sub = flags & ~(uint32_t)(MAPA_F_COMMIT | MAPA_F_PRUNE | MAPA_F_RAW);
     mapa_decision dc;
     if ((s = mapa_allocate(t, p->clique, MAPA_SEL_PRESERVE, 0, sub, stream, &dc)) != MAPA_OK) return s;
     const uint64_t extra = 0;

@@ -321,8 +321,8 @@ def test_deep_insensitive_set_search_equals_exhaustive():
             p = mp.Pattern.make(shape, k)
             t.set_busy(busy)
             ex = mp.allocate(t, p, 1, False, deep=True)
-            for _ in range(2):  # second call: cached labelling
-                fa = mp.allocate(t, p, 1, False, deep=True, prune=True)
+            for raw in (False, True, False):  # later calls: cached labelling; RAW changes nothing
+                fa = mp.allocate(t, p, 1, False, deep=True, prune=True, raw=raw)
                 for f in FIELDS + ("distinct", "pred_effbw", "key", "ecode"):
                     assert fa[f] == ex[f], (name, shape, k, hex(busy), f, fa[f], ex[f])
             if math.perm(nf, k) <= 2e7:
