@@ -327,7 +327,9 @@ mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint64_t 
  * mapa_allocate with MAPA_F_PRUNE and Preserve-insensitive on the deep path
  * searches device SETS instead (Eq. 3 depends on the set only): the full-k
  * pattern's decision gives the set, the pattern's lex-smallest labelling
- * (weight independent, cached per pattern) gives the edges; exact.
+ * (weight independent, cached per pattern) gives the edges; exact.  Baseline
+ * with MAPA_F_PRUNE on the deep path: the k lowest free ids and that
+ * labelling, no enumeration (leaves_scored 0).
  * Strict tests: the decision equals the exhaustive one; leaves counts what was
  * scored (the decision's raw / distinct are then the closed forms).
  * Errors: INVALID_ARG, UNSUPPORTED (k > 16), CUDA. */

@@ -1355,15 +1355,40 @@ bool lexmin_labelling(const mapa_pattern *p, uint64_t out[2]) {
 // pairs, which does not depend on the weights: computed once per pattern on
 // the host (lexmin_labelling) and cached.  Same decision as the exhaustive
 // search (tests); leaves = the set search's leaves.
-static mapa_status allocate_insens_sets(mapa_topology *t, const mapa_pattern *pc, uint32_t flags, void *stream,
-                                 mapa_decision *out) {
+static mapa_status allocate_insens_sets(mapa_topology *t, const mapa_pattern *pc, int selector, uint32_t flags,
+                                        void *stream, mapa_decision *out) {
     mapa_pattern *p = const_cast<mapa_pattern *>(pc);  // caches of immutable derived data
     const int k = p->k;
     mapa_status s;
     if (!p->have_ecode_min) {
         if (!lexmin_labelling(p, p->ecode_min))  // budget exhausted: exhaustive deep search instead
-            return mapa_allocate(t, pc, MAPA_SEL_PRESERVE, 0, flags & ~(uint32_t)MAPA_F_PRUNE, stream, out);
+            return mapa_allocate(t, pc, selector, 0, flags & ~(uint32_t)MAPA_F_PRUNE, stream, out);
         p->have_ecode_min = true;
+    }
+    if (selector == MAPA_SEL_BASELINE) {
+        // constant score: the k lowest free ids, the lex-smallest labelling
+        mapa_wide_record rec;
+        std::memset(&rec, 0, sizeof(rec));
+        uint64_t free = ~t->busy & nmask_of(t->n);
+        for (int i = 0; i < k; ++i) {
+            const int d = __builtin_ctzll(free);
+            free &= free - 1;
+            rec.set |= 1ull << (63 - d);
+        }
+        rec.ecode_hi = p->ecode_min[0];
+        rec.ecode_lo = p->ecode_min[1];
+        mapa_decision d;
+        if ((s = decode_wide(t, p, t->busy, MAPA_SEL_BASELINE, 0, flags & ~(uint32_t)MAPA_F_PRUNE, &rec, &d)) != MAPA_OK)
+            return s;
+        uint64_t perm = 1;
+        const int nf = __builtin_popcountll(~t->busy & nmask_of(t->n));
+        for (int i = 0; i < k; ++i) perm *= (uint64_t)std::max(0, nf - i);
+        d.raw_embeddings = perm;
+        d.distinct_matches = perm / p->aut;
+        d.leaves_scored = 0;
+        if (flags & MAPA_F_COMMIT) t->busy |= d.device_mask;
+        *out = d;
+        return MAPA_OK;
     }
     if (!p->clique) {
         std::vector<std::pair<int, int>> all;
@@ -1411,8 +1436,9 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
         out->m = p->m;
         return MAPA_NO_CAPACITY;
     }
-    if (deep && selector == MAPA_SEL_PRESERVE && !sens && (flags & MAPA_F_PRUNE) && p->k >= 2)
-        return allocate_insens_sets(t, p, flags, stream, out);
+    if (deep && (flags & MAPA_F_PRUNE) && p->k >= 2 &&
+        ((selector == MAPA_SEL_PRESERVE && !sens) || selector == MAPA_SEL_BASELINE))
+        return allocate_insens_sets(t, p, selector, flags, stream, out);
     int err;
     if (!t->d_stage) {
         if ((err = (int)cudaMalloc(&t->d_stage, 128))) return cuda_fail(err, "cudaMalloc");

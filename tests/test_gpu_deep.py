@@ -328,3 +328,21 @@ def test_deep_insensitive_set_search_equals_exhaustive():
             if math.perm(nf, k) <= 2e7:
                 kk, e = mo.make_pattern(shape, k)
                 same(co.allocate_deep(o, busy, kk, e, 1, False, max_subsets=200000), fa, (name, shape, k, hex(busy)))
+
+
+def test_deep_baseline_set_shortcut_equals_exhaustive():
+    """Baseline with MAPA_F_PRUNE on the deep path: the k lowest free ids and
+    the pattern's lex-smallest labelling, equal to the exhaustive deep search
+    (every leaf ties there) and to the deep oracle."""
+    rng = random.Random(5)
+    o, t = mo.builtin("torus2d16"), mp.Topology("torus2d16")
+    for shape, k in (("ring", 9), ("tree", 9), ("ringtree", 10)):
+        busy = sum(1 << d for d in rng.sample(range(16), 16 - k))  # exactly k free: exhaustive stays small
+        t.set_busy(busy)
+        p = mp.Pattern.make(shape, k)
+        ex = mp.allocate(t, p, 2, False, deep=True)
+        fa = mp.allocate(t, p, 2, False, deep=True, prune=True)
+        for f in FIELDS + ("distinct", "key", "ecode"):
+            assert fa[f] == ex[f], (shape, k, f)
+        kk, e = mo.make_pattern(shape, k)
+        same(co.allocate_deep(o, busy, kk, e, 2, False), fa, (shape, k))
