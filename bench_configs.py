@@ -308,21 +308,26 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
         if rank == 0 and world == 1:
             # the paper's overhead study (fig:preserve_policy_overhead): milliseconds per
             # allocation for 9+ GPU jobs on 16-GPU graphs; Greedy with MAPA_F_PRUNE (exact), end to end
-            # (Preserve-insensitive: set search over the full-k pattern + cached lex-smallest labelling)
+            # (Preserve-insensitive: set search over the full-k pattern + cached lex-smallest labelling;
+            # Preserve-sensitive: Eq. 2 rank bound tables + the set bound on score ties)
             for tname in ("cubemesh16", "torus2d16"):
                 tt = mp.Topology(tname)
                 for shape, kk in (("ring", 9), ("ring", 12), ("ring", 14), ("ring", 16), ("tree", 12), ("tree", 14)):
                     p2 = mp.Pattern.make(shape, kk)
-                    for sel, sname in ((0, "greedy"), (1, "preserve_insensitive")):
-                        mp.allocate(tt, p2, sel, False, prune=True)
+                    for sel, sens, sname in ((0, False, "greedy"), (1, False, "preserve_insensitive"),
+                                             (1, True, "preserve_sensitive")):
+                        if sens and kk == 16:
+                            continue  # k = N all free: the set is forced, ties fall to the edge code (~5 s)
+                        mp.allocate(tt, p2, sel, sens, prune=True)
                         ts = []
-                        for _ in range(5):
+                        for _ in range(5 if not sens else 3):
                             t0 = time.perf_counter()
-                            d = mp.allocate(tt, p2, sel, False, prune=True)
+                            d = mp.allocate(tt, p2, sel, sens, prune=True)
                             ts.append((time.perf_counter() - t0) * 1e3)
                         pruned[f"{tname}_{shape}{kk}_{sname}"] = {
                             "ms_median": statistics.median(ts), "leaves_scored": d["leaves"],
-                            "distinct": d["distinct"], "agg_bw": d["agg_bw"], "preserved_bw": d["preserved_bw"]}
+                            "distinct": d["distinct"], "agg_bw": d["agg_bw"], "preserved_bw": d["preserved_bw"],
+                            "pred_effbw": d["pred_effbw"]}
         emb_s = 3 * per / (tot / 1e3)
         ach = 2 * emb_s / 1e9
         line["roofline"] = {"bound": "alu", "kernel": "esa_deep<NT,SEL> (ring-10 RAW)",

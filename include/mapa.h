@@ -317,13 +317,19 @@ mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint64_t 
  * warp-uniform explicit-stack DFS over the first k-L pattern vertices, then
  * the last L vertices (L = 1..4, chosen on the host) as a lane-parallel scan
  * over a table of index tuples into the remaining free devices.  RAW and
- * canonical modes as for the narrow path.  MAPA_F_PRUNE (Greedy only; the
- * other selectors ignore it): branch and bound with exact Eq. 1 bounds -- a
+ * canonical modes as for the narrow path.  MAPA_F_PRUNE (Greedy, and
+ * Preserve-sensitive when (k+1)(m+1)^2 <= 17408; other selectors ignore it
+ * here): branch and bound with exact bounds.  Greedy (Eq. 1) -- a
  * prefix subtree is skipped when its score so far plus, for every pattern edge
  * from a placed vertex into the unplaced part, the best free link of that
  * vertex's device, plus (edges inside the unplaced part) x (best free pair) is
  * below the best score published by any lane (the record's reserved word); a
  * node's suffix scan is skipped when the sum of its tables' maxima is below it.
+ * Preserve-sensitive (Eq. 2): after nd placed vertices with census (x0, y0)
+ * and c edges still unplaced, the bound is max rank over (x0+a, y0+b), a+b <=
+ * c (host tables uploaded with the rank table).  On a score tie the subtree
+ * is still cut when U + the lowest k-nd other free devices orders below the
+ * published best set (the reserved word holds score << 32 | brev64(S) >> 32).
  * mapa_allocate with MAPA_F_PRUNE and Preserve-insensitive on the deep path
  * searches device SETS instead (Eq. 3 depends on the set only): the full-k
  * pattern's decision gives the set, the pattern's lex-smallest labelling

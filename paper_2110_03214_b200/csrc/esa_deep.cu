@@ -70,7 +70,8 @@ struct DeepShared {
 };
 
 // dynamic shared memory: DeepShared + the Eq. 2 rank table (u16, (m+1)^2 <= 121^2)
-constexpr int kDeepSmemMax = (int)sizeof(DeepShared) + 2 * (kMaxEdges + 1) * (kMaxEdges + 1) + 16;
+// [+ the Eq. 2 branch-and-bound tables, (k+1) (m+1)^2 <= 17408 u16]
+constexpr int kDeepSmemMax = (int)sizeof(DeepShared) + 2 * (kMaxEdges + 1) * (kMaxEdges + 1) + 2 * 17408 + 16;
 
 extern __shared__ __align__(16) unsigned char g_dsmem[];
 __device__ __forceinline__ DeepShared &dsh() { return *reinterpret_cast<DeepShared *>(g_dsmem); }
@@ -160,7 +161,8 @@ __device__ __forceinline__ void consider_deep(const DeepTables &tb, const DeepWa
         else elo |= 1ull << q;
     }
     if (key_gt(s, set, ehi, elo, b.score, b.set, b.ehi, b.elo)) {
-        if (gpub && s > b.score) atomicMax(gpub, (unsigned long long)s << 32);  // branch and bound: publish
+        if (gpub && (s > b.score || set > b.set))  // branch and bound: publish (score, top of brev64(S))
+            atomicMax(gpub, ((unsigned long long)s << 32) | (set >> 32));
         b.score = s;
         b.set = set;
         b.ehi = ehi;
@@ -273,7 +275,7 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, in
     const int nt = tb.tcount[r];
     const char *ab = reinterpret_cast<const char *>(W.area);
     const int A0 = A * tb.scale;
-    if constexpr (prune) {
+    if constexpr (prune && base != SEL_SENS) {
         // table bound: every tuple's score <= A + sum over its terms of the
         // largest entry its table can hold; strict test against the grid best
         int ub = A0;
@@ -370,8 +372,10 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
         }
         S.tup[i] = make_uint4(x, wd[0], wd[1], wd[2]);
     }
-    if constexpr (base == SEL_SENS)
-        for (int i = tid; i < tb.xsd * tb.xsd; i += kBlockD) dlut()[i] = lut_g[i];
+    if constexpr (base == SEL_SENS) {
+        const int nl = tb.xsd * tb.xsd * (1 + ((SEL & 8) ? tb.k + 1 : 0));  // + bound tables (prune)
+        for (int i = tid; i < nl; i += kBlockD) dlut()[i] = lut_g[i];
+    }
     if (tid < kND) {
         int inc = 0;
         if (tid < n && ((F >> tid) & 1u))
@@ -490,10 +494,26 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
                     // from a placed vertex j to the unplaced part <= the best free
                     // link of f(j); every edge inside the unplaced part <= gmax
                     const int nd = d + 1;
-                    const int c = lane < nd ? __popc((uint32_t)tb.adj[lane] >> nd) * S.maxw[myf] : 0;
-                    const int ub = a + __reduce_add_sync(kFullD, c) + (int)tb.c2[nd] * S.gmax;
-                    const unsigned gb = (unsigned)(*reinterpret_cast<volatile unsigned long long *>(gpub) >> 32);
-                    if (ub < (int)gb) {
+                    int ub;
+                    if constexpr (base == SEL_SENS) {
+                        // Eq. 2: the largest rank reachable from the census so far
+                        ub = dlut()[tb.xsd * tb.xsd * (1 + nd) + a];
+                    } else {
+                        const int c = lane < nd ? __popc((uint32_t)tb.adj[lane] >> nd) * S.maxw[myf] : 0;
+                        ub = a + __reduce_add_sync(kFullD, c) + (int)tb.c2[nd] * S.gmax;
+                    }
+                    const unsigned long long gk = *reinterpret_cast<volatile unsigned long long *>(gpub);
+                    const unsigned gb = (unsigned)(gk >> 32);
+                    bool cut = ub < (int)gb;
+                    if (ub == (int)gb) {
+                        // score tie: the subtree's best set is U + the lowest k - nd other free devices;
+                        // cut when even that set orders below the published best (exact on ties)
+                        const M R = F & ~U;
+                        const int need = tb.k - nd;
+                        const M low = need >= popc<M>(R) ? R : (R & below<M>((int)nth_set<M>(R, need)));
+                        cut = (uint32_t)(__brevll((unsigned long long)(U | low)) >> 32) < (uint32_t)gk;
+                    }
+                    if (cut) {
                         U &= ~bit<M>(v);
                         continue;  // skip the subtree: try the next candidate of level d
                     }
@@ -582,9 +602,11 @@ using DeepFn = int (*)(const DeepTables &, const uint16_t *, const mapa_query64 
 
 template <typename M, int NT>
 DeepFn pick_sel(int sc) {
-    switch (sc & 15) {  // branch and bound: Greedy (8, 12)
+    switch (sc & 15) {  // branch and bound: Greedy (8, 12), Preserve-sensitive (10, 14)
         case 8: return launch_t<M, NT, 8>;
         case 12: return launch_t<M, NT, 12>;
+        case 10: return launch_t<M, NT, 10>;
+        case 14: return launch_t<M, NT, 14>;
     }
     switch (sc & 7) {
         case 0: return launch_t<M, NT, 0>;
@@ -603,6 +625,8 @@ const void *pick_fn_sel(int sc) {
     switch (sc & 15) {
         case 8: return (const void *)esa_deep<M, NT, 8>;
         case 12: return (const void *)esa_deep<M, NT, 12>;
+        case 10: return (const void *)esa_deep<M, NT, 10>;
+        case 14: return (const void *)esa_deep<M, NT, 14>;
     }
     switch (sc & 7) {
         case 0: return (const void *)esa_deep<M, NT, 0>;
@@ -641,7 +665,8 @@ const void *pick_fn(int nterm, int sc) {
 
 int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_query64 *d_query,
                 mapa_wide_record *d_record, int depth, int rank, int world, int stripe, int grid, void *stream) {
-    const int smem = (int)sizeof(DeepShared) + ((sc & 3) == SEL_SENS ? 2 * tb.xsd * tb.xsd : 0);
+    const int smem = (int)sizeof(DeepShared) +
+                     ((sc & 3) == SEL_SENS ? 2 * tb.xsd * tb.xsd * (1 + ((sc & 8) ? tb.k + 1 : 0)) : 0);
     if (tb.nterm > kDeepMaxTerms || tb.L < 1 || tb.L > kMaxL) return (int)cudaErrorInvalidValue;
     DeepFn f = tb.n <= 32 ? pick<uint32_t>(tb.nterm, sc) : pick<unsigned long long>(tb.nterm, sc);
     return f(tb, d_lut, d_query, d_record, depth, rank, world, stripe, grid, smem, (cudaStream_t)stream);
@@ -649,8 +674,8 @@ int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_
 
 int max_blocks_per_sm_deep(int n, int nterm, int sc, int lut_bytes) {
     // cached per (mask width, term class, selector code, rank-table size)
-    static int cache[2][3][16][9] = {};
-    const int mi = n <= 32 ? 0 : 1, ti = nt_class(nterm) / 2 - 1, li = std::min(8, (lut_bytes + 4095) / 4096);
+    static int cache[2][3][16][18] = {};
+    const int mi = n <= 32 ? 0 : 1, ti = nt_class(nterm) / 2 - 1, li = std::min(17, (lut_bytes + 4095) / 4096);
     int &slot = cache[mi][ti][sc & 15][li];
     if (slot) return slot;
     const void *f = n <= 32 ? pick_fn<uint32_t>(nterm, sc) : pick_fn<unsigned long long>(nterm, sc);

@@ -594,6 +594,10 @@ int build_tuples(const mapa_pattern *p, int L, int r, bool canon, uint32_t *out,
     return n;
 }
 
+// Eq. 2 branch and bound is built when the per-depth bound tables fit:
+// (k + 1) tables of (m + 1)^2 u16 (<= 34 KB of shared memory)
+bool sens_prunable(const mapa_pattern *p) { return (p->k + 1) * (p->m + 1) * (p->m + 1) <= 17408; }
+
 mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selector, int sens, uint32_t flags,
                       int nF, int world, DeepTables *tb, DeepPlan *pl) {
     const int k = p->k;
@@ -677,11 +681,13 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     // branch and bound (MAPA_F_PRUNE): Greedy only.  (An Eq. 3 variant with
     // the bound (k-1) maxw[v] - inc_F(v) per later vertex was exact but pruned
     // nothing on cubemesh16 and cost 20-40 %: not dispatched.)
-    pl->sc = base | (canon ? 4 : 0) | ((flags & MAPA_F_PRUNE) && base == SEL_GREEDY ? 8 : 0);
+    const bool prune = (flags & MAPA_F_PRUNE) && (base == SEL_GREEDY || (base == SEL_SENS && sens_prunable(p)));
+    pl->sc = base | (canon ? 4 : 0) | (prune ? 8 : 0);
     // decoded prefix depth: enough items for ~8 per resident warp (x world)
     int sm = device_sm_count();
     if (sm <= 0) sm = 148;
-    const int occ = max_blocks_per_sm_deep(t->n, tb->nterm, pl->sc, base == SEL_SENS ? 2 * tb->xsd * tb->xsd : 0);
+    const int lutb = base == SEL_SENS ? 2 * tb->xsd * tb->xsd * (1 + (prune ? k + 1 : 0)) : 0;
+    const int occ = max_blocks_per_sm_deep(t->n, tb->nterm, pl->sc, lutb);
     const uint64_t warps = (uint64_t)sm * occ * 8;
     const uint64_t target = 8ull * warps * (uint64_t)world;
     // RAW items are uniform: stop at ~8 per warp.  Canonical items are not
@@ -701,15 +707,41 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     return MAPA_OK;
 }
 
+// Rank table followed, for Eq. 2 branch and bound, by one bound table per
+// number of placed vertices nd: ub[nd][x*(m+1) + y] = the largest rank of a
+// final census (x+a, y+b, .) with a + b <= c_nd, c_nd = the pattern edges not
+// inside {0..nd-1} (exact: the remaining edges can only add to x, y or z).
+std::vector<uint16_t> rank_and_bounds(const mapa_pattern *p) {
+    std::vector<uint16_t> v(p->lut);
+    if (!sens_prunable(p)) return v;
+    const int m = p->m, xs = m + 1, k = p->k;
+    for (int nd = 0; nd <= k; ++nd) {
+        int inside = 0;
+        for (auto &e : p->edges) inside += (e.first < nd && e.second < nd);
+        const int c = m - inside;
+        for (int x = 0; x < xs; ++x)
+            for (int y = 0; y < xs; ++y) {
+                int best = 0;
+                if (x + y <= m)
+                    for (int a2 = 0; a2 <= c && x + a2 <= m; ++a2)
+                        for (int b2 = 0; a2 + b2 <= c && x + a2 + y + b2 <= m; ++b2)
+                            best = std::max(best, (int)p->lut[(x + a2) * xs + (y + b2)]);
+                v.push_back((uint16_t)best);
+            }
+    }
+    return v;
+}
+
 mapa_status upload_lut(const mapa_pattern *pc) {
     mapa_pattern *p = const_cast<mapa_pattern *>(pc);  // the device copy caches the immutable table
     int dev = 0, err;
     if ((err = (int)cudaGetDevice(&dev))) return cuda_fail(err, "cudaGetDevice");
     if (p->d_lut && p->d_lut_dev == dev) return MAPA_OK;
     if (p->d_lut) { cudaFree(p->d_lut); p->d_lut = nullptr; }
-    const size_t bytes = p->lut.size() * sizeof(uint16_t);
+    const std::vector<uint16_t> img = rank_and_bounds(p);
+    const size_t bytes = img.size() * sizeof(uint16_t);
     if ((err = (int)cudaMalloc(&p->d_lut, bytes))) return cuda_fail(err, "cudaMalloc (rank table)");
-    if ((err = (int)cudaMemcpy(p->d_lut, p->lut.data(), bytes, cudaMemcpyHostToDevice))) return cuda_fail(err, "H2D rank table");
+    if ((err = (int)cudaMemcpy(p->d_lut, img.data(), bytes, cudaMemcpyHostToDevice))) return cuda_fail(err, "H2D rank table");
     p->d_lut_dev = dev;
     return MAPA_OK;
 }
@@ -789,7 +821,8 @@ mapa_status decode_wide(const mapa_topology *t, const mapa_pattern *p, uint64_t 
     d.ecode[1] = rec->ecode_lo;
     d.leaves_scored = rec->leaves;
     const uint64_t F = ~busy & nmask_of(t->n);
-    if ((flags & MAPA_F_PRUNE) && selector == MAPA_SEL_GREEDY) {
+    if ((flags & MAPA_F_PRUNE) &&
+        (selector == MAPA_SEL_GREEDY || (selector == MAPA_SEL_PRESERVE && sens && sens_prunable(p)))) {
         // the pruned kernel scores a subset; the totals are the closed forms
         uint64_t perm = 1;
         const int nf = __builtin_popcountll(F);

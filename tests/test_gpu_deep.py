@@ -255,7 +255,9 @@ def test_deep_n64_all_free_clique_and_narrow_refusal():
 
 
 def test_deep_prune_equals_exhaustive():
-    """Deep branch and bound (MAPA_F_PRUNE, Greedy): the decision equals the
+    """Deep branch and bound (MAPA_F_PRUNE: Greedy's Eq. 1 bounds, Preserve-
+    sensitive's Eq. 2 rank bounds; Preserve-insensitive routes to the set
+    search): the decision equals the
     exhaustive deep search's and the deep C oracle's (small cases), fewer leaves
     are scored, and raw / distinct are the closed forms."""
     rng = random.Random(2024)
@@ -267,7 +269,7 @@ def test_deep_prune_equals_exhaustive():
             nf = 16 - bin(busy).count("1")
             p = mp.Pattern.make(shape, k)
             t.set_busy(busy)
-            for sel, sens in ((0, False), (1, False)):  # Preserve-insensitive: the flag is ignored
+            for sel, sens in ((0, False), (1, False), (1, True)):
                 for raw in (False, True):
                     if raw and math.perm(nf, k) > 3e10:
                         continue
@@ -275,7 +277,7 @@ def test_deep_prune_equals_exhaustive():
                     pr = mp.allocate(t, p, sel, sens, raw=raw, deep=True, prune=True)
                     for f in FIELDS + ("distinct", "pred_effbw", "key", "ecode"):
                         assert pr[f] == ex[f], (name, shape, k, hex(busy), sel, raw, f)
-                    if sel == 0:
+                    if sel == 0 or sens:
                         assert pr["leaves"] <= ex["leaves"]
                 if math.perm(nf, k) <= 2e7:
                     kk, e = mo.make_pattern(shape, k)
@@ -295,6 +297,10 @@ def test_deep_prune_n64_and_sharded():
     pr = mp.allocate(t, p, 0, False, deep=True, prune=True)
     for f in FIELDS + ("key", "ecode"):
         assert pr[f] == ex[f], f
+    ex_s = mp.allocate(t, p, 1, True, deep=True)
+    pr_s = mp.allocate(t, p, 1, True, deep=True, prune=True)
+    for f in FIELDS + ("key", "ecode", "pred_effbw", "distinct"):
+        assert pr_s[f] == ex_s[f], f
     recs = []
     for rank in range(3):
         q = md.query64_tensor(busy, 0, False)
