@@ -228,7 +228,15 @@ def main():
 
     if args.config != "c4":
         from bench_configs import run_config
+        sampler = ClockSampler(local)
+        if rank == 0:
+            sampler.start()
+        sampler.mark("t0")
         line = run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks)
+        sampler.mark("t1")
+        sampler.stop()
+        if line is not None and rank == 0:
+            line["clocks"] = dict(sampler.summary(), window="the whole config run (GPU legs and CPU baseline)")
         if rank == 0 and line is not None:
             print(json.dumps(line), flush=True)
         if world > 1:
