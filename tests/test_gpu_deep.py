@@ -352,3 +352,33 @@ def test_deep_baseline_set_shortcut_equals_exhaustive():
             assert fa[f] == ex[f], (shape, k, f)
         kk, e = mo.make_pattern(shape, k)
         same(co.allocate_deep(o, busy, kk, e, 2, False), fa, (shape, k))
+
+
+def test_deep_prune_forced_set_ties():
+    """Exactly k free devices (the set is forced, every top-score leaf ties on
+    it and the edge code decides): the pruned decision equals the exhaustive
+    deep search's for Greedy and Preserve-sensitive, N = 16 and 32, RAW and
+    canonical, and k = N = 16 all free."""
+    rng = random.Random(31)
+    cases = [("cubemesh16", None), ("torus2d16", None), ("het32", W.het32_text())]
+    for name, text in cases:
+        t = mp.Topology(text=text) if text else mp.Topology(name)
+        n = 32 if text else 16
+        for shape, k in (("ring", 10), ("tree", 11), ("ringtree", 12), ("ring", 12)):
+            free = rng.sample(range(n), k)
+            busy = ((1 << n) - 1) & ~sum(1 << d for d in free)
+            t.set_busy(busy)
+            p = mp.Pattern.make(shape, k)
+            for sel, sens in ((0, False), (1, True)):
+                for raw in (False, True):
+                    ex = mp.allocate(t, p, sel, sens, raw=raw, deep=True)
+                    pr = mp.allocate(t, p, sel, sens, raw=raw, deep=True, prune=True)
+                    for f in FIELDS + ("distinct", "pred_effbw", "key", "ecode"):
+                        assert pr[f] == ex[f], (name, shape, k, hex(busy), sel, raw, f)
+    t = mp.Topology("torus2d16")
+    p = mp.Pattern.make("ring", 16)
+    ex = mp.allocate(t, p, 1, True, deep=True)
+    pr = mp.allocate(t, p, 1, True, deep=True, prune=True)
+    for f in FIELDS + ("distinct", "pred_effbw", "key", "ecode"):
+        assert pr[f] == ex[f], ("ring16", f)
+    assert pr["leaves"] < ex["leaves"]
