@@ -1,6 +1,7 @@
 """Small launches of the kernels added in round 1's second half, for
 compute-sanitizer (memcheck / racecheck / synccheck): the deep kernel (u32 and
-u64 masks, every term-count class, every selector, RAW and canonical, L = 1..4),
+u64 masks, every term-count class, every selector, RAW and canonical, L = 1..4,
+exhaustive and branch and bound),
 the trace kernel's Topo-aware path (mapa_simulate), and the cached-graph
 mapa_allocate path."""
 import os
@@ -18,7 +19,8 @@ for topo, busy in ((mp.Topology("cubemesh16"), 0b0110000000100001), (mp.Topology
     for shape, k in (("ring", 9), ("tree", 8), ("full", 5), ("ringtree", 7), ("ring", 4), ("full", 1), ("edgeless", 3)):
         for sel, sens in ((0, False), (1, True), (1, False), (2, False)):
             for raw in (False, True):
-                mp.allocate(topo, mp.Pattern.make(shape, k), sel, sens, raw=raw, deep=True)
+                for prune in (False, True):  # branch and bound: Greedy / Preserve-sensitive kernels, set search
+                    mp.allocate(topo, mp.Pattern.make(shape, k), sel, sens, raw=raw, deep=True, prune=prune)
 # cached-graph replays of the narrow path
 t = mp.Topology("dgx1v")
 p = mp.Pattern.make("ring", 3)
