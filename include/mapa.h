@@ -170,7 +170,7 @@ typedef struct {
     uint32_t lock;       /* merge lock (scratch) */
     uint32_t status;     /* 0 ok; nonzero = device-side argument error */
     uint32_t pad;
-    uint64_t reserved;   /* scratch: running max of (score << 32 | set >> 32), filters the merges */
+    uint64_t reserved;   /* scratch: running max of (score << 32 | set >> 32): merge filter, branch-and-bound incumbent */
 } mapa_wide_record;
 
 /* Trace op (C2 replay): op 0 = ALLOC job, 1 = RELEASE job. */
