@@ -194,6 +194,35 @@ __device__ __forceinline__ M allowed(const DeepTables &tb, int d, int myf, int l
     return above<M>(__reduce_max_sync(kFullD, c));
 }
 
+// Branch and bound: true when no leaf below a node (pattern vertices 0..nd-1
+// placed on U, lane j < nd holding f(j), partial score a) can beat the best
+// key published in the record's reserved word (score << 32 | brev64(S) >> 32).
+// Eq. 1: every pattern edge from a placed vertex j to the unplaced part <= the
+// best free link of f(j), every edge inside the unplaced part <= the best free
+// pair.  Eq. 2: the largest rank reachable from the census so far (host table
+// per nd).  On a score tie: the subtree's best set is U + the lowest k - nd
+// other free devices; cut when even that set orders below the published one.
+template <typename M, int SEL>
+__device__ __forceinline__ bool bound_cut(const DeepTables &tb, M F, M U, int nd, int a, int myf, int lane,
+                                          const unsigned long long *gpub) {
+    constexpr int base = SEL & 3;
+    const DeepShared &S = dsh();
+    int ub;
+    if constexpr (base == SEL_SENS) {
+        ub = dlut()[tb.xsd * tb.xsd * (1 + nd) + a];
+    } else {
+        const int c = lane < nd ? __popc((uint32_t)tb.adj[lane] >> nd) * S.maxw[myf] : 0;
+        ub = a + __reduce_add_sync(kFullD, c) + (int)tb.c2[nd] * S.gmax;
+    }
+    const unsigned long long gk = *reinterpret_cast<const volatile unsigned long long *>(gpub);
+    const unsigned gb = (unsigned)(gk >> 32);
+    if (ub != (int)gb) return ub < (int)gb;
+    const M R = F & ~U;
+    const int need = tb.k - nd;
+    const M low = need >= popc<M>(R) ? R : (R & below<M>((int)nth_set<M>(R, need)));
+    return (uint32_t)(__brevll((unsigned long long)(U | low)) >> 32) < (uint32_t)gk;
+}
+
 // All leaves below a node whose prefix 0..T-1 is placed (set U, score A).
 template <typename M, int NT, int SEL>
 __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, int myf, int lane, int warp, int T,
@@ -466,6 +495,8 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
                 }
             }
             if (!ok) continue;
+            if constexpr (prune)  // the item's own subtree (prefix 0..D-1 placed)
+                if (D > 0 && bound_cut<M, SEL>(tb, F, U, D, acc, myf, lane, gpub)) continue;
             if (D == T) {
                 suffix<M, NT, SEL>(tb, F, U, acc, myf, lane, warp, T, bst, thr, cnt, gpub);
                 continue;
@@ -490,30 +521,7 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
                 if (lane == 0) S.w[warp].fw[d] = v;
                 U |= bit<M>(v);
                 if constexpr (prune) {
-                    // subtree bound after placing 0..d (Eq. 1): every pattern edge
-                    // from a placed vertex j to the unplaced part <= the best free
-                    // link of f(j); every edge inside the unplaced part <= gmax
-                    const int nd = d + 1;
-                    int ub;
-                    if constexpr (base == SEL_SENS) {
-                        // Eq. 2: the largest rank reachable from the census so far
-                        ub = dlut()[tb.xsd * tb.xsd * (1 + nd) + a];
-                    } else {
-                        const int c = lane < nd ? __popc((uint32_t)tb.adj[lane] >> nd) * S.maxw[myf] : 0;
-                        ub = a + __reduce_add_sync(kFullD, c) + (int)tb.c2[nd] * S.gmax;
-                    }
-                    const unsigned long long gk = *reinterpret_cast<volatile unsigned long long *>(gpub);
-                    const unsigned gb = (unsigned)(gk >> 32);
-                    bool cut = ub < (int)gb;
-                    if (ub == (int)gb) {
-                        // score tie: the subtree's best set is U + the lowest k - nd other free devices;
-                        // cut when even that set orders below the published best (exact on ties)
-                        const M R = F & ~U;
-                        const int need = tb.k - nd;
-                        const M low = need >= popc<M>(R) ? R : (R & below<M>((int)nth_set<M>(R, need)));
-                        cut = (uint32_t)(__brevll((unsigned long long)(U | low)) >> 32) < (uint32_t)gk;
-                    }
-                    if (cut) {
+                    if (bound_cut<M, SEL>(tb, F, U, d + 1, a, myf, lane, gpub)) {
                         U &= ~bit<M>(v);
                         continue;  // skip the subtree: try the next candidate of level d
                     }
