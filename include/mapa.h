@@ -36,7 +36,10 @@
  *   the scan adds) and the test strict, so the decision is identical to the
  *   exhaustive one; only leaves_scored changes (raw_embeddings and
  *   distinct_matches are then the closed forms P(|F|,k) and P(|F|,k)/|Aut|).
- *   For k < 4 the flag is ignored.
+ *   For k < 4 the flag is ignored.  The deep path (mapa_launch_query_wide,
+ *   mapa_allocate with k > 8 or N > 32) has its own exact bounds per DFS node
+ *   and work-item prefix (Greedy, Preserve-sensitive), a set search
+ *   (Preserve-insensitive) and a no-enumeration Baseline; see there.
  *
  * Memory: every device pointer is caller-owned (e.g. a torch CUDA tensor);
  * streams are cudaStream_t passed as void*.  Device-side entry points are
