@@ -301,16 +301,18 @@ def test_deep_prune_n64_and_sharded():
     pr_s = mp.allocate(t, p, 1, True, deep=True, prune=True)
     for f in FIELDS + ("key", "ecode", "pred_effbw", "distinct"):
         assert pr_s[f] == ex_s[f], f
-    recs = []
-    for rank in range(3):
-        q = md.query64_tensor(busy, 0, False)
-        rec = torch.zeros(8, dtype=torch.int64, device="cuda")
-        mp.launch_query_wide(t, p, 0, False, q.data_ptr(), rec.data_ptr(), busy, rank=rank, world=3, prune=True)
-        torch.cuda.synchronize()
-        recs.append(md.wide_records_from_tensor(rec)[0])
-    d = mp.decode_wide(t, p, busy, 0, False, mp.reduce_wide_records(recs), prune=True)
-    for f in FIELDS + ("key", "ecode"):
-        assert d[f] == ex[f], f
+    for sel, sens, want in ((0, False, ex), (1, True, ex_s)):
+        recs = []
+        for rank in range(3):
+            q = md.query64_tensor(busy, sel, sens)
+            rec = torch.zeros(8, dtype=torch.int64, device="cuda")
+            mp.launch_query_wide(t, p, sel, sens, q.data_ptr(), rec.data_ptr(), busy, rank=rank, world=3,
+                                 prune=True)
+            torch.cuda.synchronize()
+            recs.append(md.wide_records_from_tensor(rec)[0])
+        d = mp.decode_wide(t, p, busy, sel, sens, mp.reduce_wide_records(recs), prune=True)
+        for f in FIELDS + ("key", "ecode", "distinct"):
+            assert d[f] == want[f], (sel, f)
 
 
 def test_deep_insensitive_set_search_equals_exhaustive():
