@@ -70,8 +70,8 @@ struct DeepShared {
 };
 
 // dynamic shared memory: DeepShared + the Eq. 2 rank table (u16, (m+1)^2 <= 121^2)
-// [+ the Eq. 2 branch-and-bound tables, (k+1) (m+1)^2 <= 17408 u16]
-constexpr int kDeepSmemMax = (int)sizeof(DeepShared) + 2 * (kMaxEdges + 1) * (kMaxEdges + 1) + 2 * 17408 + 16;
+// [+ the Eq. 2 branch-and-bound tables, (k+1) (m+1)^2 <= kSensBoundMax u16]
+constexpr int kDeepSmemMax = (int)sizeof(DeepShared) + 2 * (kMaxEdges + 1) * (kMaxEdges + 1) + 2 * kSensBoundMax + 16;
 
 extern __shared__ __align__(16) unsigned char g_dsmem[];
 __device__ __forceinline__ DeepShared &dsh() { return *reinterpret_cast<DeepShared *>(g_dsmem); }

@@ -122,6 +122,10 @@ struct LaunchCfg {
 // per-node table: a partial pt[l][i_l] (suffix vertex T+l against the placed
 // prefix) or a pair value wt[i_a][i_b] (a scored suffix-internal pair).
 constexpr int kDeepMaxTerms = 6;
+// Eq. 2 deep branch and bound: (k + 1) bound tables of (m + 1)^2 u16 are built
+// when they fit in this many entries (34 KB of shared memory)
+constexpr int kSensBoundMax = 17408;
+
 struct DeepTables {
     uint64_t cm[kMaxNDeep][3];  // cm[v][c] = {u != v : class(u, v) == c}, c = 0 (50), 1 (25), 2 (20)
     int32_t n;

@@ -596,7 +596,7 @@ int build_tuples(const mapa_pattern *p, int L, int r, bool canon, uint32_t *out,
 
 // Eq. 2 branch and bound is built when the per-depth bound tables fit:
 // (k + 1) tables of (m + 1)^2 u16 (<= 34 KB of shared memory)
-bool sens_prunable(const mapa_pattern *p) { return (p->k + 1) * (p->m + 1) * (p->m + 1) <= 17408; }
+bool sens_prunable(const mapa_pattern *p) { return (p->k + 1) * (p->m + 1) * (p->m + 1) <= kSensBoundMax; }
 
 mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selector, int sens, uint32_t flags,
                       int nF, int world, DeepTables *tb, DeepPlan *pl) {
