@@ -57,8 +57,10 @@ struct DeepWarp {
     int fw[16];      // f(j) of the placed prefix (read by the key builder)
 };
 
+// The tuple table (uint4 per tuple -- x: byte l = i_l; y, z, w: 16-bit byte
+// offsets of the NT terms into area) follows the rank table, sized by ntup, so
+// that small tables do not cost occupancy.
 struct DeepShared {
-    uint4 tup[kMaxTup];        // x: byte l = i_l; y, z, w: 16-bit byte offsets of the NT terms into area
     unsigned long long cm[kND][3];
     int tw[kND * kND];         // [v*64 + b] pair value: w(v,b) (Eq. 1/3), census delta (Eq. 2), 0 if v == b
     int incF[kND];             // inc_F(v) (Eq. 3)
@@ -71,11 +73,21 @@ struct DeepShared {
 
 // dynamic shared memory: DeepShared + the Eq. 2 rank table (u16, (m+1)^2 <= 121^2)
 // [+ the Eq. 2 branch-and-bound tables, (k+1) (m+1)^2 <= kSensBoundMax u16]
-constexpr int kDeepSmemMax = (int)sizeof(DeepShared) + 2 * (kMaxEdges + 1) * (kMaxEdges + 1) + 2 * kSensBoundMax + 16;
+// [+ the tuple table, ntup <= kMaxTup uint4]
+constexpr int kDeepSmemMax =
+    (int)sizeof(DeepShared) + 2 * (kMaxEdges + 1) * (kMaxEdges + 1) + 2 * kSensBoundMax + 16 + 16 * kMaxTup;
+// byte offset of the tuple table: after DeepShared and the selector's rank (+ bound) tables
+__host__ __device__ __forceinline__ int deep_tup_off(int sc, int xsd, int k) {
+    const int lut = (sc & 3) == SEL_SENS ? 2 * xsd * xsd * (1 + ((sc & 8) ? k + 1 : 0)) : 0;
+    return ((int)sizeof(DeepShared) + lut + 15) & ~15;
+}
 
 extern __shared__ __align__(16) unsigned char g_dsmem[];
 __device__ __forceinline__ DeepShared &dsh() { return *reinterpret_cast<DeepShared *>(g_dsmem); }
 __device__ __forceinline__ uint16_t *dlut() { return reinterpret_cast<uint16_t *>(g_dsmem + sizeof(DeepShared)); }
+template <int SEL> __device__ __forceinline__ uint4 *dtup(const DeepTables &tb) {
+    return reinterpret_cast<uint4 *>(g_dsmem + deep_tup_off(SEL, tb.xsd, tb.k));
+}
 
 // ---- mask helpers (M = uint32_t for N <= 32, unsigned long long for N <= 64)
 template <typename M> __device__ __forceinline__ int popc(M m);
@@ -324,10 +336,11 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, in
             return;  // no tuple of this node can reach the best score found anywhere
         }
     }
+    const uint4 *tupl = dtup<SEL>(tb);
     for (int t0 = 0; t0 < nt; t0 += 32) {
         const int t = t0 + lane;
         bool valid = t < nt;
-        const uint4 e = S.tup[valid ? t : 0];
+        const uint4 e = tupl[valid ? t : 0];
         if constexpr (canon) {
             if (tb.pcon) valid = valid && ((((e.x | 0x80808080u) - MINI) & 0x80808080u) == 0x80808080u);
         }
@@ -399,7 +412,7 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
             const int sh = 16 * (q & 1);
             wd[q >> 1] = (wd[q >> 1] & ~(0xFFFFu << sh)) | (off << sh);
         }
-        S.tup[i] = make_uint4(x, wd[0], wd[1], wd[2]);
+        dtup<SEL>(tb)[i] = make_uint4(x, wd[0], wd[1], wd[2]);
     }
     if constexpr (base == SEL_SENS) {
         const int nl = tb.xsd * tb.xsd * (1 + ((SEL & 8) ? tb.k + 1 : 0));  // + bound tables (prune)
@@ -673,8 +686,8 @@ const void *pick_fn(int nterm, int sc) {
 
 int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_query64 *d_query,
                 mapa_wide_record *d_record, int depth, int rank, int world, int stripe, int grid, void *stream) {
-    const int smem = (int)sizeof(DeepShared) +
-                     ((sc & 3) == SEL_SENS ? 2 * tb.xsd * tb.xsd * (1 + ((sc & 8) ? tb.k + 1 : 0)) : 0);
+    if (tb.ntup < 0 || tb.ntup > kMaxTup) return (int)cudaErrorInvalidValue;
+    const int smem = deep_tup_off(sc, tb.xsd, tb.k) + 16 * tb.ntup;
     if (tb.nterm > kDeepMaxTerms || tb.L < 1 || tb.L > kMaxL) return (int)cudaErrorInvalidValue;
     DeepFn f = tb.n <= 32 ? pick<uint32_t>(tb.nterm, sc) : pick<unsigned long long>(tb.nterm, sc);
     return f(tb, d_lut, d_query, d_record, depth, rank, world, stripe, grid, smem, (cudaStream_t)stream);
@@ -682,8 +695,8 @@ int launch_deep(const DeepTables &tb, int sc, const uint16_t *d_lut, const mapa_
 
 int max_blocks_per_sm_deep(int n, int nterm, int sc, int lut_bytes) {
     // cached per (mask width, term class, selector code, rank-table size)
-    static int cache[2][3][16][18] = {};
-    const int mi = n <= 32 ? 0 : 1, ti = nt_class(nterm) / 2 - 1, li = std::min(17, (lut_bytes + 4095) / 4096);
+    static int cache[2][3][16][26] = {};
+    const int mi = n <= 32 ? 0 : 1, ti = nt_class(nterm) / 2 - 1, li = std::min(25, (lut_bytes + 4095) / 4096);
     int &slot = cache[mi][ti][sc & 15][li];
     if (slot) return slot;
     const void *f = n <= 32 ? pick_fn<uint32_t>(nterm, sc) : pick_fn<unsigned long long>(nterm, sc);

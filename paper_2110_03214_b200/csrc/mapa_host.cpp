@@ -686,7 +686,8 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     // decoded prefix depth: enough items for ~8 per resident warp (x world)
     int sm = device_sm_count();
     if (sm <= 0) sm = 148;
-    const int lutb = base == SEL_SENS ? 2 * tb->xsd * tb->xsd * (1 + (prune ? k + 1 : 0)) : 0;
+    // rank (+ bound) tables and the tuple table behind DeepShared
+    const int lutb = (base == SEL_SENS ? 2 * tb->xsd * tb->xsd * (1 + (prune ? k + 1 : 0)) : 0) + 16 + 16 * tb->ntup;
     const int occ = max_blocks_per_sm_deep(t->n, tb->nterm, pl->sc, lutb);
     const uint64_t warps = (uint64_t)sm * occ * 8;
     const uint64_t target = 8ull * warps * (uint64_t)world;
