@@ -372,7 +372,7 @@ __device__ __forceinline__ uint32_t perm_count_d(int n, int d) {
 }
 
 template <typename M, int NT, int SEL>
-__global__ void __launch_bounds__(kBlockD, sizeof(M) == 4 ? 4 : 3)  // u32: 64 registers, 4 CTAs per SM
+__global__ void __launch_bounds__(kBlockD, 4)  // 64 registers (no spills), 4 CTAs per SM
 esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut_g,
          const mapa_query64 *__restrict__ dq, mapa_wide_record *__restrict__ rec, int D, int rank, int world,
          int stripe) {
