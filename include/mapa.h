@@ -44,6 +44,16 @@
  * Memory: every device pointer is caller-owned (e.g. a torch CUDA tensor);
  * streams are cudaStream_t passed as void*.  Device-side entry points are
  * asynchronous on that stream and never synchronise.
+ *
+ * Threads and devices: a topology or pattern handle is immutable as far as
+ * the method goes, but it carries launch caches (device table images, deep
+ * launch plans, CUDA graphs, staging buffers, streams) that the launch entry
+ * points fill: a handle must not be used by two threads at once (the caller
+ * serialises).  Patterns may be used on any device (their device
+ * tables are kept per device).  A topology's mapa_allocate /
+ * mapa_launch_queries state lives on the device current at its first use;
+ * calling them on another device returns INVALID_ARG (load one handle per
+ * device, as one process per GPU does).
  */
 #ifndef MAPA_H
 #define MAPA_H
@@ -190,7 +200,7 @@ typedef struct {
  * unlisted pairs are PCIe).  N <= 64; topologies with N > 32 run on the
  * deep path only (bigger servers).  *out owned by the caller,
  * freed with mapa_free_topology.  Errors: PARSE (message names the line),
- * ID_RANGE, UNSUPPORTED (N > 32), INVALID_ARG. */
+ * ID_RANGE, UNSUPPORTED (N > 64), INVALID_ARG. */
 mapa_status mapa_load_topology(const char *builtin_or_text, int32_t is_text, mapa_topology **out);
 void mapa_free_topology(mapa_topology *t);
 
@@ -391,6 +401,24 @@ mapa_status mapa_trace_replay(const mapa_topology *t, const mapa_pattern *const 
                               int32_t npats, int32_t ntraces, int32_t nops,
                               const mapa_trace_op *d_ops, int32_t njobs, const mapa_query *d_jobs,
                               uint64_t *d_keys, uint32_t flags, void *cuda_stream);
+
+/* Host: decode ONE replayed trace (its njobs keys from mapa_trace_replay,
+ * copied to host memory) into full decisions out[njobs] (job order).  The op
+ * order is replayed on the host (§3.6 state management): ALLOC j
+ * decodes keys[j] against the busy mask of that moment -- device set, lex-first
+ * mapping, used edges, census, Eq. 1 / 2 / 3 recomputed and checked against the
+ * key's score, as mapa_decode -- then marks its devices busy; RELEASE j frees
+ * them.  jobs[njobs] = the host copy of the mapa_query array the replay used
+ * (pattern / selector / sensitive per job; MAPA_SEL_TOPO decodes as Baseline,
+ * reading A21).  The trace kernel counts no leaves, so raw_embeddings and
+ * distinct_matches are the closed forms P(|F|,k) and P(|F|,k)/|Aut| and
+ * leaves_scored is 0.  A key of 0, or a job without an ALLOC op, gives status
+ * MAPA_NO_CAPACITY in its decision (the call itself returns MAPA_OK).  Errors:
+ * INVALID_ARG (index out of range, a job allocated twice), INTERNAL (a key that
+ * overlaps the busy devices or contradicts its score), outputs untouched. */
+mapa_status mapa_decode_trace(const mapa_topology *t, const mapa_pattern *const *pats, int32_t npats,
+                              int32_t nops, const mapa_trace_op *ops, int32_t njobs, const mapa_query *jobs,
+                              const uint64_t *keys, uint32_t flags, mapa_decision *out);
 
 /* ------------------------------------------------------------- simulator */
 

@@ -128,6 +128,9 @@ _SIGS = {
                                  ctypes.c_uint32, _vp]),
     "mapa_trace_replay": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, _vp,
                                ctypes.c_int32, _vp, _vp, ctypes.c_uint32, _vp]),
+    "mapa_decode_trace": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(TraceOp),
+                               ctypes.c_int32, ctypes.POINTER(Query), ctypes.POINTER(ctypes.c_uint64), ctypes.c_uint32,
+                               ctypes.POINTER(Decision)]),
     "mapa_fifo_schedule": (_S, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                 ctypes.POINTER(TraceOp), ctypes.POINTER(ctypes.c_double),
@@ -433,17 +436,18 @@ def trace_replay(topo: Topology, pats, ntraces: int, nops: int, d_ops_ptr: int, 
                                   d_keys_ptr, F_RAW if raw else 0, _stream_ptr(stream)))
 
 
-def key_layout(topo_width: int, k: int):
-    """(score_shift, set_shift) of the packed key (include/mapa.h)."""
-    eb = k * (k - 1) // 2
-    return topo_width + eb, eb
-
-
-def key_device_mask(key: int, topo_width: int, k: int) -> int:
-    """Device set S encoded in a key (brev_W)."""
-    eb = k * (k - 1) // 2
-    sb = (key >> eb) & ((1 << topo_width) - 1)
-    return sum(1 << d for d in range(topo_width) if (sb >> (topo_width - 1 - d)) & 1)
+def decode_trace(topo: Topology, pats, ops, jobs, keys, raw: bool = False) -> list[dict]:
+    """mapa_decode_trace: one replayed trace's keys -> full decisions (job
+    order).  ops [(op, job)], jobs [(pattern index, selector, sensitive)],
+    keys = the trace's njobs keys (ints)."""
+    arr = (_vp * len(pats))(*[p.handle for p in pats])
+    o = (TraceOp * max(1, len(ops)))(*[TraceOp(a, b) for a, b in ops])
+    q = (Query * max(1, len(jobs)))(*[Query(0, pi, sel, int(bool(sens))) for pi, sel, sens in jobs])
+    ky = (ctypes.c_uint64 * max(1, len(keys)))(*[k & ((1 << 64) - 1) for k in keys])
+    out = (Decision * max(1, len(jobs)))()
+    _check(_lib.mapa_decode_trace(topo.handle, arr, len(pats), len(ops), o, len(jobs), q, ky, F_RAW if raw else 0,
+                                  out))
+    return [decision_dict(out[i]) for i in range(len(jobs))]
 
 
 # ------------------------------------------------------------------ simulator

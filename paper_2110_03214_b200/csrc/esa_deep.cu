@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "internal.h"
 
@@ -606,12 +607,15 @@ int launch_t(const DeepTables &tb, const uint16_t *lut, const mapa_query64 *dq, 
              int rank, int world, int stripe, int grid, int smem, cudaStream_t st) {
     // the attribute is always the fixed upper bound, so occupancy queries and
     // launches agree
-    static bool configured = false;
-    if (!configured) {
+    // kernel attributes are per device: one flag bit per device ordinal
+    static std::atomic<unsigned long long> configured{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return (int)cudaErrorInvalidDevice;
+    if (!((configured.load(std::memory_order_relaxed) >> dev) & 1ull)) {
         cudaError_t e = cudaFuncSetAttribute((const void *)esa_deep<M, NT, SEL>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kDeepSmemMax);
         if (e != cudaSuccess) return (int)e;
-        configured = true;
+        configured.fetch_or(1ull << dev);
     }
     if (smem > kDeepSmemMax) return (int)cudaErrorInvalidValue;
     esa_deep<M, NT, SEL><<<grid, kBlockD, smem, st>>>(tb, lut, dq, rec, D, rank, world, stripe);

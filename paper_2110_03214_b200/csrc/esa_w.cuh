@@ -1,5 +1,7 @@
 // esa_w.cuh — per-width entry points (included by esa_w8.cu / esa_w16.cu /
 // esa_w32.cu with MAPA_W defined): instantiates the kernels for one W.
+#include <atomic>
+
 #include "esa_kernels.cuh"
 
 #define MAPA_CAT2(a, b) a##b
@@ -14,12 +16,15 @@ int do_launch_single(const SingleTables &tb, const mapa_query *dq, mapa_record *
     const int smem = smem_bytes(tb);
     // the attribute is always set to the fixed upper bound (see kSmemSingleMax),
     // so the occupancy query and every launch agree
-    static bool configured = false;
-    if (!configured) {
+    // kernel attributes are per device: one flag bit per device ordinal
+    static std::atomic<unsigned long long> configured{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return (int)cudaErrorInvalidDevice;
+    if (!((configured.load(std::memory_order_relaxed) >> dev) & 1ull)) {
         cudaError_t e = cudaFuncSetAttribute((const void *)esa_single<W, K, SEL>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemSingleMax);
         if (e != cudaSuccess) return (int)e;
-        configured = true;
+        configured.fetch_or(1ull << dev);
     }
     if (smem > kSmemSingleMax) return (int)cudaErrorInvalidValue;
     esa_single<W, K, SEL><<<grid, kBlock, smem, st>>>(tb, dq, rec, D, rank, world, stripe);

@@ -40,6 +40,7 @@ struct mapa_topology {
     uint8_t cls[kMaxNDeep][kMaxNDeep];   // class code 0..3, diagonal 0xFF
     std::vector<std::vector<int>> sockets;
     uint64_t busy = 0;
+    int dev = -1;                 // device of the stream / staging state below (set on first use)
     void *d_stage = nullptr;      // device: query (16 B) + record (32 / 64 B)
     void *h_stage = nullptr;      // pinned host mirror
     cudaStream_t cap = nullptr;   // private stream for graph capture (the caller's may be the legacy stream)
@@ -64,8 +65,10 @@ struct mapa_pattern {
     uint64_t aut = 1;          // |Aut(P)| (16! < 2^45)
     std::vector<uint16_t> lut;   // (m+1)^2
     double theta[14];          // Eq. 2 model of this pattern (Table 4 unless mapa_pattern_set_effbw_model)
-    void *d_lut = nullptr;     // device copy of lut (deep kernel), uploaded on first use
-    int d_lut_dev = -1;
+    // device copies of the rank (+ bound) table for the deep kernel, one per
+    // device, uploaded on first use and kept until the model changes (cached
+    // graphs on any device may hold the pointer of theirs)
+    std::vector<std::pair<int, void *>> d_luts;
     uint64_t uid = 0;          // unique per compiled pattern / model (graph cache key)
     // Eq. 3 set search (deep path, MAPA_F_PRUNE): the full-k pattern, and the
     // pattern's lex-smallest used-edge list over rank pairs (weight independent)
@@ -447,7 +450,9 @@ const int4 *pair_tables(const mapa_topology *tc, int xs, void *stream) {
     }
     void *d = nullptr;
     if (cudaMalloc(&d, img.size() * sizeof(int)) != cudaSuccess) return nullptr;
-    if (cudaMemcpy(d, img.data(), img.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess) {
+    // pageable copy: make sure the DMA is complete before any stream reads it
+    if (cudaMemcpy(d, img.data(), img.size() * sizeof(int), cudaMemcpyHostToDevice) != cudaSuccess ||
+        cudaStreamSynchronize(cudaStreamLegacy) != cudaSuccess) {
         cudaFree(d);
         return nullptr;
     }
@@ -733,17 +738,46 @@ std::vector<uint16_t> rank_and_bounds(const mapa_pattern *p) {
     return v;
 }
 
-mapa_status upload_lut(const mapa_pattern *pc) {
+mapa_status upload_lut(const mapa_pattern *pc, const uint16_t **out) {
     mapa_pattern *p = const_cast<mapa_pattern *>(pc);  // the device copy caches the immutable table
     int dev = 0, err;
     if ((err = (int)cudaGetDevice(&dev))) return cuda_fail(err, "cudaGetDevice");
-    if (p->d_lut && p->d_lut_dev == dev) return MAPA_OK;
-    if (p->d_lut) { cudaFree(p->d_lut); p->d_lut = nullptr; }
+    for (auto &e : p->d_luts)
+        if (e.first == dev) {
+            *out = (const uint16_t *)e.second;
+            return MAPA_OK;
+        }
     const std::vector<uint16_t> img = rank_and_bounds(p);
     const size_t bytes = img.size() * sizeof(uint16_t);
-    if ((err = (int)cudaMalloc(&p->d_lut, bytes))) return cuda_fail(err, "cudaMalloc (rank table)");
-    if ((err = (int)cudaMemcpy(p->d_lut, img.data(), bytes, cudaMemcpyHostToDevice))) return cuda_fail(err, "H2D rank table");
-    p->d_lut_dev = dev;
+    void *d = nullptr;
+    if ((err = (int)cudaMalloc(&d, bytes))) return cuda_fail(err, "cudaMalloc (rank table)");
+    // a pageable copy may still be in flight when cudaMemcpy returns: finish it
+    // before any stream (non-blocking ones included) can read the table
+    if ((err = (int)cudaMemcpy(d, img.data(), bytes, cudaMemcpyHostToDevice)) ||
+        (err = (int)cudaStreamSynchronize(cudaStreamLegacy))) {
+        cudaFree(d);
+        return cuda_fail(err, "H2D rank table");
+    }
+    p->d_luts.push_back({dev, d});
+    *out = (const uint16_t *)d;
+    return MAPA_OK;
+}
+
+void free_luts(mapa_pattern *p) {
+    for (auto &e : p->d_luts) cudaFree(e.second);
+    p->d_luts.clear();
+}
+
+// The topology's staging buffers, capture / side streams and cached graphs
+// belong to the device current at their first use: mapa_allocate and
+// mapa_launch_queries refuse a handle used from another device.
+mapa_status bind_device(mapa_topology *t) {
+    int dev = 0, err;
+    if ((err = (int)cudaGetDevice(&dev))) return cuda_fail(err, "cudaGetDevice");
+    if (t->dev < 0) t->dev = dev;
+    if (t->dev != dev)
+        return fail(MAPA_E_INVALID_ARG, "topology handle is bound to device " + std::to_string(t->dev) +
+                                            " (current device " + std::to_string(dev) + "): use one handle per device");
     return MAPA_OK;
 }
 
@@ -1089,7 +1123,7 @@ mapa_status mapa_make_pattern(int32_t shape, int32_t k, mapa_pattern **out) {
 void mapa_free_pattern(mapa_pattern *p) {
     if (!p) return;
     if (p->clique) mapa_free_pattern(p->clique);
-    if (p->d_lut) cudaFree(p->d_lut);
+    free_luts(p);
     delete p;
 }
 
@@ -1170,6 +1204,8 @@ mapa_status mapa_launch_queries(mapa_topology *t, const mapa_pattern *const *pat
     if (nq == 0) return MAPA_OK;
     cudaStream_t main = (cudaStream_t)stream;
     int err;
+    mapa_status sb = bind_device(t);
+    if (sb != MAPA_OK) return sb;
     while ((int)t->side.size() < nstreams) {
         cudaStream_t s2;
         if ((err = (int)cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking))) return cuda_fail(err, "cudaStreamCreate");
@@ -1180,19 +1216,19 @@ mapa_status mapa_launch_queries(mapa_topology *t, const mapa_pattern *const *pat
     if ((err = (int)cudaMemsetAsync(d_records, 0, (size_t)nq * sizeof(mapa_record), main))) return cuda_fail(err, "memset");
     cudaEvent_t fork, join;
     if ((err = (int)cudaEventCreateWithFlags(&fork, cudaEventDisableTiming))) return cuda_fail(err, "cudaEventCreate");
+    if ((err = (int)cudaEventCreateWithFlags(&join, cudaEventDisableTiming))) {  // both before the fork
+        cudaEventDestroy(fork);
+        return cuda_fail(err, "cudaEventCreate");
+    }
     cudaEventRecord(fork, main);
     for (int s2 = 0; s2 < nstreams; ++s2) cudaStreamWaitEvent(t->side[s2], fork, 0);
     mapa_status st = MAPA_OK;
     for (int i = 0; i < nq && st == MAPA_OK; ++i) {
         const mapa_query &q = h_queries[i];
-        if ((int)q.pattern >= npats || !pats[q.pattern]) { st = fail(MAPA_E_INVALID_ARG, "query pattern index out of range"); break; }
+        if (q.pattern >= (uint32_t)npats || !pats[q.pattern]) { st = fail(MAPA_E_INVALID_ARG, "query pattern index out of range"); break; }
         if (q.selector < 0 || q.selector > 2) { st = fail(MAPA_E_INVALID_ARG, "bad selector"); break; }
         st = launch_query_impl(t, pats[q.pattern], q.selector, q.sensitive, d_queries + i, d_records + i, flags, 0, 1,
                                q.busy, (void *)t->side[i % nstreams], false);
-    }
-    if ((err = (int)cudaEventCreateWithFlags(&join, cudaEventDisableTiming))) {
-        cudaEventDestroy(fork);
-        return cuda_fail(err, "cudaEventCreate");
     }
     for (int s2 = 0; s2 < nstreams; ++s2) {  // join: every side stream's work before `main` continues
         cudaEventRecord(join, t->side[s2]);
@@ -1272,8 +1308,9 @@ static mapa_status launch_query_wide_impl(const mapa_topology *t, const mapa_pat
         e = tm->deep_plans.back().get();
     }
     e->tick = ++tm->tick;
-    if (sel_code(selector, sensitive) == SEL_SENS && (s = upload_lut(p)) != MAPA_OK) return s;
-    err = launch_deep(e->tb, e->sc, (const uint16_t *)p->d_lut, d_query, d_record, e->depth, rank, world,
+    const uint16_t *d_lut = nullptr;
+    if (sel_code(selector, sensitive) == SEL_SENS && (s = upload_lut(p, &d_lut)) != MAPA_OK) return s;
+    err = launch_deep(e->tb, e->sc, d_lut, d_query, d_record, e->depth, rank, world,
                       e->stripe, e->grid, stream);
     if (err) return cuda_fail(err, "esa_deep launch");
     return MAPA_OK;
@@ -1474,6 +1511,8 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
         ((selector == MAPA_SEL_PRESERVE && !sens) || selector == MAPA_SEL_BASELINE))
         return allocate_insens_sets(t, p, selector, flags, stream, out);
     int err;
+    mapa_status sb = bind_device(t);
+    if (sb != MAPA_OK) return sb;
     if (!t->d_stage) {
         if ((err = (int)cudaMalloc(&t->d_stage, 128))) return cuda_fail(err, "cudaMalloc");
     }
@@ -1526,7 +1565,8 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
         // first call for this key: capture the sequence on a private stream
         if (!deep) pair_tables(t, pick_xs(p->m), stream);  // cudaMalloc / sync copy: not inside the capture
         if (deep && sel_code(selector, sens) == SEL_SENS) {
-            mapa_status su = upload_lut(p);  // synchronous: not inside the capture
+            const uint16_t *d_lut = nullptr;
+            mapa_status su = upload_lut(p, &d_lut);  // synchronous: not inside the capture
             if (su != MAPA_OK) return su;
         }
         if (!t->cap && (err = (int)cudaStreamCreateWithFlags(&t->cap, cudaStreamNonBlocking)))
@@ -1710,21 +1750,14 @@ mapa_status mapa_simulate(const mapa_topology *t, const mapa_pattern *const *pat
     }
     cleanup();
     // host replay of the op order: the busy mask at each ALLOC decodes its key
-    uint64_t busy = 0;
-    std::vector<uint64_t> held(njobs, 0);
-    for (const mapa_trace_op &o : ops) {
-        const int j = o.job;
-        if (o.op == 1) { busy &= ~held[j]; continue; }
+    std::vector<mapa_decision> dec(njobs);
+    s = mapa_decode_trace(t, pats, npats, 2 * njobs, ops.data(), njobs, q.data(), keys.data(), flags & MAPA_F_RAW,
+                          dec.data());
+    if (s != MAPA_OK) return s;
+    for (int j = 0; j < njobs; ++j) {
+        const mapa_decision &d = dec[j];
+        if (d.status != MAPA_OK) return fail(MAPA_E_INTERNAL, "admitted job without a decision");
         const mapa_pattern *p = pats[jobs[j].pattern];
-        mapa_record rec;
-        std::memset(&rec, 0, sizeof(rec));
-        rec.key = keys[j];
-        mapa_decision d;
-        const int sel = (policy == MAPA_POLICY_PRESERVE) ? MAPA_SEL_PRESERVE
-                      : (policy == MAPA_POLICY_GREEDY ? MAPA_SEL_GREEDY : MAPA_SEL_BASELINE);
-        s = decode_record(t, p, busy, sel, q[j].sensitive, flags & MAPA_F_RAW, &rec, &d);
-        if (s != MAPA_OK) return s == MAPA_NO_CAPACITY ? fail(MAPA_E_INTERNAL, "admitted job without a decision") : s;
-        if (d.device_mask & busy) return fail(MAPA_E_INTERNAL, "decision overlaps busy devices");
         mapa_job_log &L = out[j];
         std::memset(&L, 0, sizeof(L));
         L.job = j;
@@ -1738,9 +1771,62 @@ mapa_status mapa_simulate(const mapa_topology *t, const mapa_pattern *const *pat
         L.start = st[j];
         L.end = en[j];
         L.wait = st[j] - arr[j];
+    }
+    return MAPA_OK;
+}
+
+mapa_status mapa_decode_trace(const mapa_topology *t, const mapa_pattern *const *pats, int32_t npats, int32_t nops,
+                              const mapa_trace_op *ops, int32_t njobs, const mapa_query *jobs, const uint64_t *keys,
+                              uint32_t flags, mapa_decision *out) {
+    if (!t || !pats || npats < 1 || nops < 0 || njobs < 0 || (nops > 0 && !ops) ||
+        (njobs > 0 && (!jobs || !keys || !out)))
+        return fail(MAPA_E_INVALID_ARG, "bad decode_trace arguments");
+    for (int j = 0; j < njobs; ++j)
+        if (jobs[j].pattern >= (uint32_t)npats || !pats[jobs[j].pattern])
+            return fail(MAPA_E_INVALID_ARG, "job " + std::to_string(j) + ": pattern index out of range");
+    std::vector<mapa_decision> dec(njobs);
+    for (auto &d : dec) {
+        std::memset(&d, 0, sizeof(d));
+        d.status = MAPA_NO_CAPACITY;
+    }
+    // replay the op order (§3.6): an ALLOC decodes its key on the
+    // busy mask of that moment, then claims the devices; RELEASE frees them
+    uint64_t busy = 0;
+    std::vector<uint64_t> held(njobs, 0);
+    std::vector<char> seen(njobs, 0);
+    for (int i = 0; i < nops; ++i) {
+        const int j = ops[i].job;
+        if (j < 0 || j >= njobs || (ops[i].op != 0 && ops[i].op != 1))
+            return fail(MAPA_E_INVALID_ARG, "op " + std::to_string(i) + " out of range");
+        if (ops[i].op == 1) {
+            busy &= ~held[j];
+            held[j] = 0;
+            continue;
+        }
+        if (seen[j]) return fail(MAPA_E_INVALID_ARG, "job " + std::to_string(j) + " allocated twice");
+        seen[j] = 1;
+        const mapa_pattern *p = pats[jobs[j].pattern];
+        const int nf = __builtin_popcountll(~busy & nmask_of(t->n));
+        mapa_decision &d = dec[j];
+        d.k = p->k;
+        d.m = p->m;
+        if (keys[j] == 0) continue;  // no capacity: state unchanged
+        // Topo-aware lays the pattern on its set like Baseline (reading A21)
+        const int sel = jobs[j].selector == MAPA_SEL_TOPO ? MAPA_SEL_BASELINE : jobs[j].selector;
+        mapa_record rec;
+        std::memset(&rec, 0, sizeof(rec));
+        rec.key = keys[j];
+        mapa_status s = decode_record(t, p, busy, sel, jobs[j].sensitive, flags & MAPA_F_RAW, &rec, &d);
+        if (s != MAPA_OK) return s == MAPA_NO_CAPACITY ? fail(MAPA_E_INTERNAL, "nonzero key decoded as no capacity") : s;
+        if (d.device_mask & busy) return fail(MAPA_E_INTERNAL, "job " + std::to_string(j) + ": decision overlaps busy devices");
+        // the trace kernel does not count leaves: the totals are the closed forms
+        d.raw_embeddings = perm_count(nf, p->k);
+        d.distinct_matches = d.raw_embeddings / (uint64_t)p->aut;
+        d.leaves_scored = 0;
         held[j] = d.device_mask;
         busy |= d.device_mask;
     }
+    std::memcpy(out, dec.data(), sizeof(mapa_decision) * (size_t)njobs);
     return MAPA_OK;
 }
 
@@ -1831,7 +1917,7 @@ mapa_status mapa_pattern_set_effbw_model(mapa_pattern *p, const double *theta) {
     std::memcpy(p->theta, theta, sizeof(p->theta));
     p->lut = rank_table(p->m, p->theta);
     p->uid = next_uid();  // cached allocate graphs baked the old table
-    if (p->d_lut) { cudaFree(p->d_lut); p->d_lut = nullptr; p->d_lut_dev = -1; }
+    free_luts(p);
     return MAPA_OK;
 }
 

@@ -123,13 +123,13 @@ def query64_tensor(busy: int, selector: int = 0, sensitive: bool = False, device
 
 
 def run_query_wide(topo: Topology, pat: Pattern, selector: int, sensitive: bool, busy: int, raw: bool = False,
-                   rank: int = 0, world: int = 1, stream=None):
+                   rank: int = 0, world: int = 1, stream=None, prune: bool = False):
     """Deep path: launch one (shard of a) query; returns the 64-B record tensor
     (int64[8], device) without synchronising."""
     q = query64_tensor(busy, selector, sensitive)
     rec = torch.empty(8, dtype=torch.int64, device="cuda")
     launch_query_wide(topo, pat, selector, sensitive, q.data_ptr(), rec.data_ptr(), busy, raw=raw, rank=rank,
-                      world=world, stream=stream)
+                      world=world, stream=stream, prune=prune)
     return rec, q
 
 
@@ -150,13 +150,14 @@ def combine_wide_records(rec: torch.Tensor, group=None) -> WideRecord:
 
 
 def allocate_sharded_wide(topo: Topology, pat: Pattern, selector: int, sensitive: bool, busy: int,
-                          raw: bool = False, group=None) -> dict:
-    """Deep-path sharded single allocation over the process group."""
+                          raw: bool = False, group=None, prune: bool = False) -> dict:
+    """Deep-path sharded single allocation over the process group (prune =
+    MAPA_F_PRUNE: each rank's branch and bound, same combined decision)."""
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rec, _q = run_query_wide(topo, pat, selector, sensitive, busy, raw=raw, rank=rank, world=world)
+    rec, _q = run_query_wide(topo, pat, selector, sensitive, busy, raw=raw, rank=rank, world=world, prune=prune)
     r = combine_wide_records(rec, group)
-    return decode_wide(topo, pat, busy, selector, sensitive, r, raw=raw)
+    return decode_wide(topo, pat, busy, selector, sensitive, r, raw=raw, prune=prune)
 
 
 def run_batch(topo: Topology, pats, queries, raw: bool = False, stream=None):

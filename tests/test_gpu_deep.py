@@ -168,11 +168,23 @@ def test_deep_full_clique_vs_subset_bruteforce():
 def test_deep_sharded_virtual_ranks_and_determinism():
     """Shards r = 0..R-1 of one deep query combine (lexicographic 256-bit max,
     sum of leaves) to the unsharded record for R = 1, 2, 3, 5; repeated runs
-    give identical records."""
+    give identical records; on 11 free devices the combined 3-rank record
+    decodes to the deep C oracle's decision."""
     t = mp.Topology("cubemesh16")
+    o = mo.builtin("cubemesh16")
     busy = 0b0000000000100001
     for shape, k, sel, sens in (("ring", 10, 0, False), ("tree", 11, 1, True), ("ringtree", 9, 1, False)):
         p = mp.Pattern.make(shape, k)
+        # 11 free devices for the oracle comparison of the combined shards
+        ob = 0b1000110000100001
+        kk, ee = mo.make_pattern(shape, k)
+        exp = co.allocate_deep(o, ob, kk, ee, sel, sens)
+        recs = []
+        for rank in range(3):
+            rec, _q = md.run_query_wide(t, p, sel, sens, ob, rank=rank, world=3)
+            torch.cuda.synchronize()
+            recs.append(md.wide_records_from_tensor(rec)[0])
+        same(exp, mp.decode_wide(t, p, ob, sel, sens, mp.reduce_wide_records(recs)), (shape, k, "world 3 vs oracle"))
         ref = None
         for world in (1, 2, 3, 5):
             recs = []

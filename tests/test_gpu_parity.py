@@ -166,12 +166,16 @@ def test_commit_and_release_roundtrip():
 
 def test_sharded_virtual_ranks_equal_unsharded():
     """Sharding by work item (rank = i % world) + max/sum combine gives the
-    unsharded record for every world size (S:369 determinism)."""
+    unsharded record for every world size (S:369 determinism), and the
+    combined record decodes to the C oracle's decision."""
     text = W.rand_text(32, W.MASTER_SEED)
     t = mp.Topology(text=text)
+    o = mo.parse_topology(text)
     for shape, k, busy in (("full", 5, 0), ("ring", 5, 0x0000FF00), ("tree", 6, 0xF0F0F0F0)):
         pat = mp.Pattern.make(shape, k)
+        kk, ee = mo.make_pattern(shape, k)
         for sel, sens in SELS[:3]:
+            exp = co.allocate(o, busy, kk, ee, sel, sens)
             for raw in (True, False):
                 ref, _ = md.run_query(t, pat, sel, sens, busy, raw=raw)
                 torch.cuda.synchronize()
@@ -184,6 +188,8 @@ def test_sharded_virtual_ranks_equal_unsharded():
                         recs.append(md.records_from_tensor(rt)[0])
                     comb = mp.reduce_records(recs)
                     assert comb.key == ref.key and comb.leaves == ref.leaves, (shape, k, world, raw)
+                    # the combined shards decode to the oracle's decision
+                    same(exp, mp.decode(t, pat, busy, sel, sens, comb, raw=raw), (shape, k, world, raw))
                 d = mp.decode(t, pat, busy, sel, sens, ref, raw=raw)
                 nf = 32 - bin(busy).count("1")
                 assert d["raw"] == math.perm(nf, k)
@@ -424,11 +430,11 @@ def test_c2_trace_replay_vs_oracle(topo_name, policy):
             return co.allocate(topo, busy, k, pe, sel, sens, nthreads=1)
 
         exp = mo.replay_trace(o, jobs, ops, patd, policy, allocate_fn=alloc)
-        W8 = t.width
+        # every key decoded through the C-ABI (mapa_decode_trace replays the
+        # busy state) and compared field by field with the oracle's replay
+        got = mp.decode_trace(t, pats, ops, [(r[1], r[2], r[3]) for r in jrows], keys, raw=raw)
         for j, d in exp.items():
-            k = jobs[j]["k"]
-            got = mp.key_device_mask(keys[j] & ((1 << 64) - 1), W8, k)
-            assert got == mo.device_mask(d["devices"]), (topo_name, policy, j)
+            same(d, got[j], (topo_name, policy, j, raw))
 
 
 def test_c3_sampled_vs_oracle():

@@ -258,3 +258,39 @@ def test_reduce_records_max_and_sum():
     recs = [mp.Record(key=5, leaves=10), mp.Record(key=9, leaves=1), mp.Record(key=7, leaves=100)]
     r = mp.reduce_records(recs)
     assert r.key == 9 and r.leaves == 111
+
+
+def test_decode_trace_recovers_oracle_replay():
+    """mapa_decode_trace on keys encoded (test side) from the oracle's replay
+    of a 120-job FIFO trace on summit: every decision is decoded against the
+    busy mask of its moment and equals the oracle's field by field; raw /
+    distinct are the closed forms (§3.6)."""
+    jobs = W.c2_jobs(7, 120)
+    o = mo.builtin("summit")
+    ops = W.fifo_ops(jobs, o.n)
+    shapes = sorted({(j["shape"], j["k"]) for j in jobs})
+    patd = {sk: mo.make_pattern(*sk) for sk in shapes}
+    exp = mo.replay_trace(o, jobs, ops, patd, "preserve")
+    t = mp.Topology("summit")
+    pats = [mp.Pattern.make(s, k) for s, k in shapes]
+    rows = [(shapes.index((j["shape"], j["k"])), 1, j["sensitive"]) for j in jobs]
+    keys = []
+    for j, job in enumerate(jobs):
+        d, m = exp[j], len(patd[(job["shape"], job["k"])][1])
+        score = selector_score(d, 1, job["sensitive"], mp.effbw_rank_table(m), m)
+        keys.append(encode_key(d, score, t.width, job["k"]))
+    got = mp.decode_trace(t, pats, ops, rows, keys)
+    for j, d in exp.items():
+        for f in ("devices", "mapping", "used_edges", "x", "y", "z", "agg_bw", "preserved_bw", "raw", "distinct"):
+            assert got[j][f] == d[f], (j, f, got[j][f], d[f])
+        assert abs(got[j]["pred_effbw"] - d["pred_effbw"]) <= 1e-6 * max(1, abs(d["pred_effbw"]))
+    # a key that overlaps a running job is rejected; a zero key is no capacity
+    first = [j for op, j in ops if op == 0][:2]
+    bad = list(keys)
+    bad[first[1]] = keys[first[0]]
+    with pytest.raises(mp.MapaError) as e:
+        mp.decode_trace(t, pats, ops, rows, bad)
+    assert e.value.status == mp.E_INTERNAL
+    zero = list(keys)
+    zero[first[1]] = 0
+    assert mp.decode_trace(t, pats, ops, rows, zero)[first[1]]["status"] == "no_capacity"
