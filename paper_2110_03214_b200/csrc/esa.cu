@@ -130,9 +130,9 @@ int device_sm_count() {
 
 int max_blocks_per_sm_single(int width, int k, int sc, int xs) {
     // cached: (width, k, selector code with canon bit, xs) -> blocks per SM
-    static int cache[3][9][24][48] = {};
+    static int cache[3][9][56][48] = {};
     const int wi = width == 8 ? 0 : (width == 16 ? 1 : 2), xi = xs < 48 ? xs : 0;
-    int &slot = cache[wi][k >= 1 && k <= 8 ? k : 0][sc & 23][xi];
+    int &slot = cache[wi][k >= 1 && k <= 8 ? k : 0][sc & 55][xi];
     if (slot) return slot;
     const int smem = smem_shared_w32() + 4 * xs * xs * (int)sizeof(int);
     int r;

@@ -236,6 +236,68 @@ __device__ __forceinline__ bool bound_cut(const DeepTables &tb, M F, M U, int nd
     return (uint32_t)(__brevll((unsigned long long)(U | low)) >> 32) < (uint32_t)gk;
 }
 
+// L = 2 without a tuple table (tb.lanes2; the host picks it when r is large,
+// e.g. N = 64 topologies, where the 16x16 pair table of the tuple scan caps L
+// at 1 and a node would hold only r leaves): vertex T walks the r remaining
+// devices i (uniform loop, pt[0][i] and dl[i] broadcast from shared memory),
+// vertex T+1 sits on the lanes j = lane, lane + 32 (pt[1][j] and dl[j] in
+// registers); a leaf costs one gather of the pair value w(dl[i], dl[j]) from
+// the 64x64 table, one add and the threshold test.  pt[l][i] is already in
+// the area (scale 1: Eq. 3 is pt0 + pt1 + w, every pair scored).
+template <typename M, int SEL>
+__device__ __forceinline__ void suffix_lanes2(const DeepTables &tb, const DeepWarp &W, int r, int A, uint32_t MINI, M U,
+                                              unsigned long long nbest, int lane, int T, DBest &bst, int &thr,
+                                              unsigned long long &cnt, unsigned long long *gpub) {
+    constexpr int base = SEL & 3;
+    constexpr bool canon = (SEL & 4) != 0;
+    constexpr bool prune = (SEL & 8) != 0;
+    const DeepShared &S = dsh();
+    const int mi0 = canon ? (int)(MINI & 0xFFu) : 0, mi1 = canon ? (int)((MINI >> 8) & 0xFFu) : 0;
+    const bool dep = canon && tb.l2dep;
+    const int e = tb.l2e;
+    const int two = r > 32;
+    __syncwarp();  // pt[l][i] and dl written by the other lanes
+    int pj0 = 0, pj1 = 0, dj0 = 0, dj1 = 0;
+    if (lane < r) { pj0 = W.area[kND + lane]; dj0 = W.dl[lane]; }
+    if (two && lane + 32 < r) { pj1 = W.area[kND + lane + 32]; dj1 = W.dl[lane + 32]; }
+    // leaves of this node (closed form): i in [mi0, r), j in [mi1, r), j != i (dep: j > i)
+    {
+        int c = 0;
+        for (int i = mi0 + lane; i < r; i += 32) c += r - max(mi1, dep ? i + 1 : 0) - (!dep && i >= mi1 ? 1 : 0);
+        cnt += (unsigned long long)__reduce_add_sync(kFullD, c);
+    }
+    if constexpr (prune && base != SEL_SENS) {
+        // every leaf <= A + max pt0 + max pt1 + e * (best free pair)
+        int m0 = kNegTable, m1 = kNegTable;
+        if (lane >= mi0 && lane < r) m0 = W.area[lane];
+        if (lane + 32 >= mi0 && lane + 32 < r) m0 = max(m0, W.area[lane + 32]);
+        if (lane >= mi1 && lane < r) m1 = pj0;
+        if (lane + 32 >= mi1 && lane + 32 < r) m1 = max(m1, pj1);
+        const int ub = A + __reduce_max_sync(kFullD, m0) + __reduce_max_sync(kFullD, m1) + e * S.gmax;
+        const unsigned gb = (unsigned)(*reinterpret_cast<volatile unsigned long long *>(gpub) >> 32);
+        if (ub < (int)gb) return;
+    }
+    int tie = nbest >= bst.set ? 0 : 1;  // score ties (see suffix)
+    for (int i = mi0; i < r; ++i) {
+        const int a = A + W.area[i];
+        const int *row = S.tw + W.dl[i] * kND;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !two) break;
+            const int j = lane + 32 * h;
+            const bool valid = j < r && j >= mi1 && (dep ? j > i : j != i);
+            int s = a + (h ? pj1 : pj0) + (e ? row[h ? dj1 : dj0] : 0);
+            if constexpr (base == SEL_SENS) s = dlut()[valid ? s : 0];
+            if (valid && s >= thr + tie) {
+                consider_deep(tb, W, bst, thr, (uint32_t)s, (unsigned long long)U, (uint32_t)i | ((uint32_t)j << 8), T,
+                              prune ? gpub : nullptr);
+                tie = nbest >= bst.set ? 0 : 1;
+            }
+        }
+    }
+    __syncwarp();
+}
+
 // All leaves below a node whose prefix 0..T-1 is placed (set U, score A).
 template <typename M, int NT, int SEL>
 __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, int myf, int lane, int warp, int T,
@@ -252,6 +314,15 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, in
         if (tb.pcommon) R &= above<M>(__reduce_max_sync(kFullD, (lane < T && ((tb.pcommon >> lane) & 1)) ? myf : -1));
     }
     const int r = popc<M>(R);
+    // Score ties: a leaf of this node holds U plus L devices of R, so the best
+    // device set any of them can have is U + the L lowest devices of R.  When
+    // that set orders below the lane's best set, a leaf that only TIES the
+    // lane's best score cannot win the tie-break: the threshold is strict
+    // (scores are multiples of `scale`), and such leaves -- every automorphic
+    // copy of a winner in RAW mode, and equal-weight labellings on topologies
+    // with many equal links -- never reach the out-of-line key builder.
+    const M lowL = L >= r ? R : (R & below<M>((int)nth_set<M>(R, (uint32_t)L)));
+    const unsigned long long nbest = __brevll((unsigned long long)(U | lowL));
     __syncwarp();  // previous readers of dl / area are done
 #pragma unroll
     for (int h = 0; h < (int)sizeof(M) / 4; ++h) {
@@ -296,6 +367,10 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, in
             }
         }
     }
+    if (tb.lanes2) {
+        suffix_lanes2<M, SEL>(tb, W, r, A, MINI, U, nbest, lane, T, bst, thr, cnt, gpub);
+        return;
+    }
     // Pair table.  Eq. 3 with L >= 2 (scale = L-1): the score depends on the
     // set only and pt[l][i] = q[i] for every l, so
     //   (L-1) s = (L-1) A + sum over the C(L,2) pairs of (L-1) w(i, i2) + q[i] + q[i2]
@@ -337,6 +412,7 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, in
             return;  // no tuple of this node can reach the best score found anywhere
         }
     }
+    int tie = nbest >= bst.set ? 0 : 1;
     const uint4 *tupl = dtup<SEL>(tb);
     for (int t0 = 0; t0 < nt; t0 += 32) {
         const int t = t0 + lane;
@@ -356,10 +432,11 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, in
         if constexpr (canon) {
             if (tb.pcon) cnt += (unsigned long long)__popc(__ballot_sync(kFullD, valid));
         }
-        if (valid && s >= thr) {
+        if (valid && s >= thr + tie) {
             const int sc = tb.scale;
             const uint32_t sr = sc == 1 ? (uint32_t)s : (sc == 2 ? (uint32_t)s >> 1 : (uint32_t)s / 3u);
             consider_deep(tb, W, bst, thr, sr, (unsigned long long)U, e.x, T, prune ? gpub : nullptr);
+            tie = nbest >= bst.set ? 0 : 1;
         }
     }
     if (!canon || !tb.pcon) cnt += (unsigned long long)nt;

@@ -75,6 +75,11 @@ struct SelT {
     // single-query Eq. 2 scans use 16-bit packed tables and columns (pack16)
     static constexpr bool pack16 = base == SEL_SENS && !multi;
     static constexpr bool lin = base != SEL_SENS;      // additive score (Eq. 1 / Eq. 3 / 0)
+    // bit 5: single-query Eq. 1 / Eq. 3 scans on 16-bit lanes (two leaves per
+    // VIADDMNMX.S16x2); the host sets it only when every scan value fits s16
+    // (lin16_fits in mapa_host.cpp)
+    static constexpr bool lin16 = (SEL & 32) != 0 && lin && !multi;
+    static constexpr bool half = pack16 || lin16;      // 16-bit table entries
     static constexpr bool useU = base == SEL_INSENS;   // Eq. 3 sums over every placed device
     static constexpr int wt = base == SEL_BASE ? 0 : 1;
     static constexpr int w0 = 38 * wt, w1 = 13 * wt, w2 = 8 * wt, w12 = 12 * wt;
@@ -144,6 +149,8 @@ struct Ctx {
     int one;                        // 1, read from shared memory (see scan_dense)
     int negk;                       // -65536 at run time (pack16 offset split on the FMA pipe)
     int colmax;                     // additive scores: max_v col[v] (prune-mode bound)
+    int ishift;                     // lin16 Eq. 3: max_{v in F} inc_F(v), added to table entries (0 otherwise)
+    int irange;                     // lin16 Eq. 3: ishift - min_{v in F} inc_F(v)
     int col[W];                     // lane's inner-scan column (see lane_column)
 };
 
@@ -308,20 +315,34 @@ __device__ __forceinline__ void leaf_k1(const Ctx<W> &c, Best &bst) {
 template <int W, int SEL>
 __device__ __forceinline__ int *tab_ptr(const Ctx<W> &c, int which) {
     int *t = sh().wl[c.warp].dense[which];
-    if constexpr (SelT<SEL>::pack16) return reinterpret_cast<int *>(reinterpret_cast<uint16_t *>(t) + c.g * W);
+    if constexpr (SelT<SEL>::half) return reinterpret_cast<int *>(reinterpret_cast<uint16_t *>(t) + c.g * W);
     else return t + c.g * W;
 }
 
 template <int W, int SEL>
 __device__ __forceinline__ void tab_put(const Ctx<W> &c, int *tab, int v) {
-    if constexpr (SelT<SEL>::pack16) reinterpret_cast<uint16_t *>(tab)[c.b] = (uint16_t)v;
+    if constexpr (SelT<SEL>::half) reinterpret_cast<uint16_t *>(tab)[c.b] = (uint16_t)v;
     else tab[c.b] = v;
+}
+
+// lin16 sentinels.  Valid table entries are 32 (t2 + ishift) in [0, 31135]
+// (the host's lin16_fits), valid column entries 32 w + 31 - v in [0, 1631], so
+// every valid leaf sums to [0, 32766].  An invalid table entry is -1632 and an
+// invalid column entry -31136: any sum with a sentinel is negative and >= -32768
+// (no s16 wrap).
+constexpr int kNeg16T = -1632;
+constexpr int kNeg16C = -31136;
+
+template <int W, int SEL>
+__device__ __forceinline__ int lin_entry(const Ctx<W> &c, bool ok, int t) {
+    if constexpr (SelT<SEL>::lin16) return ok ? (t + c.ishift) * 32 : kNeg16T;
+    else return ok ? t * 32 : kNeg;
 }
 
 template <int W, int SEL>
 __device__ __forceinline__ int tab_entry(const Ctx<W> &c, uint32_t cand, int t2) {
     const bool mine = (cand >> c.b) & 1u;
-    if constexpr (SelT<SEL>::lin) return mine ? t2 * 32 : kNeg;
+    if constexpr (SelT<SEL>::lin) return lin_entry<W, SEL>(c, mine, t2);
     else return 4 * (mine ? t2 : c.xs * c.xs);  // byte offsets into the Eq. 2 table
 }
 
@@ -354,6 +375,23 @@ __device__ __forceinline__ int tab_scan(const Ctx<W> &c, const int *tab, int bas
             a3 = max(a3, max(lds_off(lut, (int)s3 + h3 * negk) * one + (25 - v), lds_off(lut, h3) * one + (24 - v)));
         }
         return max(max(a0, a1), max(a2, a3));
+    }
+    if constexpr (SelT<SEL>::lin16) {
+        // two leaves per VIADDMNMX.S16x2: table word q holds entries 2q / 2q+1,
+        // column register q the lane's matching pair; four independent chains
+        const uint4 *t8 = reinterpret_cast<const uint4 *>(tab);
+        unsigned a0 = 0x80008000u, a1 = 0x80008000u, a2 = 0x80008000u, a3 = 0x80008000u;
+#pragma unroll
+        for (int q = 0; q < W / 8; ++q) {
+            const uint4 e = t8[q];
+            a0 = __viaddmax_s16x2(e.x, (unsigned)c.col[4 * q + 0], a0);
+            a1 = __viaddmax_s16x2(e.y, (unsigned)c.col[4 * q + 1], a1);
+            a2 = __viaddmax_s16x2(e.z, (unsigned)c.col[4 * q + 2], a2);
+            a3 = __viaddmax_s16x2(e.w, (unsigned)c.col[4 * q + 3], a3);
+        }
+        const unsigned m2 = __vmaxs2(__vmaxs2(a0, a1), __vmaxs2(a2, a3));
+        const int r = max((int)(short)(m2 & 0xFFFFu), (int)m2 >> 16);
+        return r < 0 ? kNeg : r;  // no valid leaf
     }
     const int4 *t4 = reinterpret_cast<const int4 *>(tab);
     int best = 0;
@@ -453,7 +491,7 @@ __device__ __forceinline__ void inner(const Ctx<W> &c, const St<K> &st, uint32_t
              SelT<SEL>::w2 * __popc(c.cm2 & X2);
         const int lp = c.laneC + SelT<SEL>::w12 * __popc(X1) + SelT<SEL>::w0 * __popc(c.cm0 & X1) + SelT<SEL>::w1 * __popc(c.cm1 & X1) +
                        SelT<SEL>::w2 * __popc(c.cm2 & X1);
-        base = (st.acc + lp + 1) * 32;
+        base = (st.acc + lp + 1 - c.ishift) * 32;
     } else {
         const uint32_t X2 = st.bm[J], X1 = st.bm[K - 1];
         t2 = __popc(c.cm0 & X2) * c.xs + __popc(c.cm12 & X2);
@@ -542,8 +580,8 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
             // largest weight) and w(v3, v) by 50.
             int *ta = tab_ptr<W, SEL>(c, 0), *tb2 = tab_ptr<W, SEL>(c, 1);
             __syncwarp(c.gmask);
-            tab_put<W, SEL>(c, ta, ((cand3 >> b) & 1u) ? 32 * t3 : kNeg);
-            tab_put<W, SEL>(c, tb2, ((cand2b >> b) & 1u) ? 32 * t2b : kNeg);
+            tab_put<W, SEL>(c, ta, lin_entry<W, SEL>(c, (cand3 >> b) & 1u, t3));
+            tab_put<W, SEL>(c, tb2, lin_entry<W, SEL>(c, (cand2b >> b) & 1u, t2b));
             __syncwarp(c.gmask);
             // the column carries the (., b) weights unless the edge (k-2, k-1) is
             // absent (Eq. 1), and has no order sentinels unless f(k-2) < f(k-1)
@@ -552,7 +590,8 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
             const int s3 = colw ? tab_scan<W, SEL>(c, ta, 0) : 32 * grp_max<W>(c, ((cand3 >> b) & 1u) ? t3 : kNeg) +
                                                             32 * 50 * SelT<SEL>::wt * m31;
             const int s2 = tab_scan<W, SEL>(c, tb2, 0);
-            const int ub = 32 * (A + lpb + 1 + m32 * 50 * SelT<SEL>::wt) + s3 + s2;
+            // lin16: the scanned entries carry + 32 ishift each
+            const int ub = 32 * (A + lpb + 1 + m32 * 50 * SelT<SEL>::wt) + s3 + s2 - (colw ? 64 : 32) * c.ishift;
             if (!__any_sync(c.gmask, okb && ub >= bst.pthr)) return;
         }
     }
@@ -603,8 +642,8 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
         bool okA = okb && b != vA && (!d31 || b > vA);
         bool okB = hasB && okb && b != vB && (!d31 || b > vB);
         const int lpA = lpb + m31 * wA, lpB = lpb + m31 * wB;
-        const int baseA = (SelT<SEL>::lin) ? (A + eA.y + lpA + 1) * 32 : A + eA.y + lpA;
-        const int baseB = (SelT<SEL>::lin) ? (A + eB.y + lpB + 1) * 32 : A + eB.y + lpB;
+        const int baseA = (SelT<SEL>::lin) ? (A + eA.y + lpA + 1 - c.ishift) * 32 : A + eA.y + lpA;
+        const int baseB = (SelT<SEL>::lin) ? (A + eB.y + lpB + 1 - c.ishift) * 32 : A + eB.y + lpB;
         const int offA = SelT<SEL>::lin ? baseA : 0, offB = SelT<SEL>::lin ? baseB : 0;
         const int entA = tab_entry<W, SEL>(c, cA, t2b + m32 * wA);
         const int entB = tab_entry<W, SEL>(c, cB, t2b + m32 * wB);
@@ -774,7 +813,7 @@ __device__ __forceinline__ void run_range(const Ctx<W> &c, uint32_t lo, uint32_t
 // writes this warp's inc_F table.
 template <int W>
 __device__ __forceinline__ Ctx<W> make_ctx(const DevTopo &topo, const DevPattern &P, int pid, int xs, uint32_t busy,
-                                           int sc, bool pack16) {
+                                           int sc, bool pack16, bool lin16 = false) {
     const int lane = threadIdx.x & 31;
     Ctx<W> c;
     const uint32_t nmask = topo.n >= 32 ? kFull : ((1u << topo.n) - 1u);
@@ -835,6 +874,26 @@ __device__ __forceinline__ Ctx<W> make_ctx(const DevTopo &topo, const DevPattern
     c.colmax = kNeg;
 #pragma unroll
     for (int v = 0; v < W; ++v) c.colmax = max(c.colmax, c.col[v]);
+    c.ishift = 0;
+    c.irange = 0;
+    if (lin16) {
+        // Eq. 3 table entries t2(v) = sum_U w(u, v) - inc_F(v) are shifted by
+        // max_{v in F} inc_F(v) to be >= 0 (the caller's base subtracts it)
+        int im = useU && inFb ? incb : 0, imn = useU && inFb ? incb : 0x7FFFFFFF;
+#pragma unroll
+        for (int o = W / 2; o > 0; o >>= 1) {
+            im = max(im, __shfl_xor_sync(kFull, im, o, W));
+            imn = min(imn, __shfl_xor_sync(kFull, imn, o, W));
+        }
+        c.ishift = im;
+        c.irange = useU ? im - min(imn, im) : 0;
+#pragma unroll
+        for (int j = 0; j < W / 2; ++j) {
+            const int lo = c.col[2 * j] < 0 ? kNeg16C : c.col[2 * j];
+            const int hi = c.col[2 * j + 1] < 0 ? kNeg16C : c.col[2 * j + 1];
+            c.col[j] = (lo & 0xFFFF) | (hi << 16);
+        }
+    }
     if (pack16) {  // SelT::pack16: col[j] = col(2j) | col(2j+1) << 16 (byte offsets < 2^16)
 #pragma unroll
         for (int j = 0; j < W / 2; ++j) c.col[j] = (c.col[2 * j] & 0xFFFF) | (c.col[2 * j + 1] << 16);
@@ -929,7 +988,15 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
     const uint32_t busy = dq->busy;
     __syncthreads();
 
-    Ctx<W> c = make_ctx<W>(tb.topo, tb.pat[0], 0, xs, busy, SEL & 3, SelT<SEL>::pack16);
+    Ctx<W> c = make_ctx<W>(tb.topo, tb.pat[0], 0, xs, busy, SEL & 3, SelT<SEL>::pack16, SelT<SEL>::lin16);
+    if constexpr (SelT<SEL>::lin16) {
+        // the host chose 16-bit scans from busy_hint; a query whose free set
+        // breaks the range (lin16_fits) is refused loudly, never mis-scored
+        if (32 * (50 * (K - 2) + c.irange) > 31135) {
+            if (tid == 0) atomicExch(&rec->status, 1u);
+            return;
+        }
+    }
 
     // Rank r owns the stripes s = r, r + world, ... of `stripe` consecutive
     // items; its local item space is their concatenation.  Warps grab local
@@ -944,17 +1011,33 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
     const uint32_t P = gridDim.x * (uint32_t)kWarps;
     Best bst{0ull, 0u, 0u, 32, 0u, 32, SelT<SEL>::prune ? reinterpret_cast<unsigned *>(&rec->reserved) : nullptr};
     const uint32_t g = (uint32_t)(lane / W);
+    // The first chunk of every warp is static (warp w takes [w s0, (w+1) s0)),
+    // so a launch starts without P same-address atomics; the counter then
+    // hands out [off0, Nloc), and a warp that reads it exhausted leaves
+    // without an atomic.
+    const uint32_t s0 = (max(2u * G, Nloc / (2u * P)) + G - 1u) / G * G;
+    const uint32_t off0 = (uint32_t)min((unsigned long long)P * s0, (unsigned long long)Nloc);
+    const uint32_t gw = blockIdx.x * (uint32_t)kWarps + (uint32_t)warp;
+    bool first = true;
     for (;;) {
-        uint32_t start = 0, sz = 0;
-        if (lane == 0) {
-            const uint32_t cur = *reinterpret_cast<volatile uint32_t *>(&rec->ctr);
-            const uint32_t rem = cur < Nloc ? Nloc - cur : 0u;
-            sz = max(2u * G, rem / (2u * P));
-            sz = (sz + G - 1u) / G * G;
-            start = atomicAdd(&rec->ctr, sz);
+        uint32_t start = Nloc, sz = 0;
+        if (first) {
+            first = false;
+            if (gw * s0 >= off0) continue;  // no static chunk: straight to the counter
+            start = gw * s0;
+            sz = s0;
+        } else {
+            if (lane == 0) {
+                const uint32_t cur = off0 + *reinterpret_cast<volatile uint32_t *>(&rec->ctr);
+                if (cur < Nloc) {
+                    sz = max(2u * G, (Nloc - cur) / (2u * P));
+                    sz = (sz + G - 1u) / G * G;
+                    start = off0 + atomicAdd(&rec->ctr, sz);
+                }
+            }
+            start = __shfl_sync(kFull, start, 0);
+            sz = __shfl_sync(kFull, sz, 0);
         }
-        start = __shfl_sync(kFull, start, 0);
-        sz = __shfl_sync(kFull, sz, 0);
         if (start >= Nloc) break;
         const uint32_t end = min(start + sz, Nloc);
         const uint32_t per = (end - start + G - 1u) / G;

@@ -37,10 +37,10 @@ using SingleFn = int (*)(const SingleTables &, const mapa_query *, mapa_record *
 // the prune bit (16) applies to k >= 4 only (the host never sets it below)
 template <int W, int SEL>
 SingleFn pick_k(int K) {
-    constexpr int S3 = SEL & ~16;
+    constexpr int S3 = SEL & ~16, S2 = SEL & ~(16 | 32);  // lin16 from k = 3, prune from k = 4
     switch (K) {
-        case 1: return do_launch_single<W, 1, S3>;
-        case 2: return do_launch_single<W, 2, S3>;
+        case 1: return do_launch_single<W, 1, S2>;
+        case 2: return do_launch_single<W, 2, S2>;
         case 3: return do_launch_single<W, 3, S3>;
         case 4: return do_launch_single<W, 4, SEL>;
         case 5: return do_launch_single<W, 5, SEL>;
@@ -56,10 +56,10 @@ const void *single_ptr() { return (const void *)esa_single<W, K, SEL>; }
 
 template <int W, int SEL>
 const void *pick_ptr(int K) {
-    constexpr int S3 = SEL & ~16;
+    constexpr int S3 = SEL & ~16, S2 = SEL & ~(16 | 32);
     switch (K) {
-        case 1: return single_ptr<W, 1, S3>();
-        case 2: return single_ptr<W, 2, S3>();
+        case 1: return single_ptr<W, 1, S2>();
+        case 2: return single_ptr<W, 2, S2>();
         case 3: return single_ptr<W, 3, S3>();
         case 4: return single_ptr<W, 4, SEL>();
         case 5: return single_ptr<W, 5, SEL>();
@@ -70,8 +70,18 @@ const void *pick_ptr(int K) {
     return nullptr;
 }
 
+// lin16 (bit 5) exists for W = 16 / 32 and the additive selectors only
 #define MAPA_SEL_SWITCH(FN, ...)                      \
-    switch (sc & 23) {                                \
+    if (MAPA_W == 8 || (sc & 3) >= SEL_SENS) sc &= ~32; \
+    switch (sc & 55) {                                \
+        case 32: return FN<MAPA_W, 32 * (MAPA_W > 8) + 0>(__VA_ARGS__);   \
+        case 33: return FN<MAPA_W, 32 * (MAPA_W > 8) + 1>(__VA_ARGS__);   \
+        case 36: return FN<MAPA_W, 32 * (MAPA_W > 8) + 4>(__VA_ARGS__);   \
+        case 37: return FN<MAPA_W, 32 * (MAPA_W > 8) + 5>(__VA_ARGS__);   \
+        case 48: return FN<MAPA_W, 32 * (MAPA_W > 8) + 16>(__VA_ARGS__);  \
+        case 49: return FN<MAPA_W, 32 * (MAPA_W > 8) + 17>(__VA_ARGS__);  \
+        case 52: return FN<MAPA_W, 32 * (MAPA_W > 8) + 20>(__VA_ARGS__);  \
+        case 53: return FN<MAPA_W, 32 * (MAPA_W > 8) + 21>(__VA_ARGS__);  \
         case 0: return FN<MAPA_W, 0>(__VA_ARGS__);    \
         case 1: return FN<MAPA_W, 1>(__VA_ARGS__);    \
         case 2: return FN<MAPA_W, 2>(__VA_ARGS__);    \

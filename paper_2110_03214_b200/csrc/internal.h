@@ -139,6 +139,11 @@ struct DeepTables {
     int32_t pcommon;         // canonical: prefix vertices that are lex-leader sources of EVERY suffix vertex
     int32_t scale;           // the scan compares scale * score (Eq. 3 pair folding: L-1, else 1)
     int32_t nterm;           // terms per tuple (<= kDeepMaxTerms)
+    // lanes2 (L = 2 for any r <= 64, no tuple table): vertex T walks the r
+    // remaining devices i, vertex T+1 sits on the lanes j (two rounds when r > 32)
+    int32_t lanes2;
+    int32_t l2e;             // lanes2: the pair (T, T+1) is scored (Eq. 1 / 2 pattern edge, Eq. 3 always)
+    int32_t l2dep;           // lanes2, canonical: lex-leader f(T) < f(T+1)
     uint8_t term[kDeepMaxTerms][3];  // (kind 0: pt of suffix vertex a | kind 1: pair (a, b))
     uint8_t pad0[2];
     int32_t tcount[kMaxNDeep + 1];  // tcount[r']: tuples whose indices are all < r' (table sorted by max index)

@@ -460,6 +460,32 @@ const int4 *pair_tables(const mapa_topology *tc, int xs, void *stream) {
     return (const int4 *)d;
 }
 
+// Can the single-query Eq. 1 / Eq. 3 scans run on 16-bit lanes (SelT::lin16,
+// esa_kernels.cuh)?  Their table entries are 32 (t2 + ishift) with t2 <= 50 (k-2)
+// (the vertex k-2 has at most k-2 placed neighbours) for Eq. 1, and t2 =
+// sum_U w(u, v) - inc_F(v), ishift = max_{v in F} inc_F(v) for Eq. 3, so
+// t2 + ishift <= 50 (k-2) + spread, spread = max - min of inc_F over F
+// (unknown F: spread <= max_v inc over all devices); entries must stay <= 31135.
+bool lin16_fits(const mapa_topology *t, const mapa_pattern *p, int selcode, uint64_t busy_hint) {
+    if (t->width < 16 || p->k < 3 || (selcode != SEL_GREEDY && selcode != SEL_INSENS)) return false;
+    int spread = 0;
+    if (selcode == SEL_INSENS) {
+        const uint64_t all = nmask_of(t->n);
+        const uint64_t F = busy_hint == ~0ull ? all : (~busy_hint & all);
+        int lo = 1 << 30, hi = 0;
+        for (int v = 0; v < t->n; ++v) {
+            if (!((F >> v) & 1u)) continue;
+            int inc = 0;
+            for (int u = 0; u < t->n; ++u)
+                if (u != v && ((F >> u) & 1u)) inc += bw_of(t, u, v);
+            lo = std::min(lo, inc);
+            hi = std::max(hi, inc);
+        }
+        spread = busy_hint == ~0ull ? hi : hi - (lo > hi ? hi : lo);
+    }
+    return 32 * (50 * (p->k - 2) + spread) <= 31135;
+}
+
 struct Plan {
     int depth, chunk, grid;
     uint64_t nlocal;
@@ -632,9 +658,29 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
     // suffix length L: smallest modelled cost per leaf (node overhead + rounds of 32 lanes)
     double best = 1e30;
     int bestL = 0;
+    bool bestLanes2 = false;
+    // parallelism: the warps can only split the prefix levels 0..k-L-1
+    // (decoded items); with fewer prefixes than ~4 per resident warp of every
+    // rank, most warps idle
+    auto par = [&](int L) {
+        const uint64_t want = 4ull * 148 * 3 * 8 * (uint64_t)world;
+        const uint64_t avail = perm_count(nF, std::min(k - L, 6));
+        return avail < want ? (double)want / (double)std::max<uint64_t>(1, avail) : 1.0;
+    };
     for (int L = 1; L <= std::min(k, 4); ++L) {
         const int r = nF - k + L;
-        if (r < L || r > kMaxNDeep || (L >= 2 && r > 16)) continue;
+        if (r < L || r > kMaxNDeep) continue;
+        if (L == 2) {
+            // lanes2: vertex T loops over r devices, T+1 on the lanes (one or two
+            // rounds of 32); no tuple table, so r is not capped at 16
+            const bool dep = canon && ((p->src[k - 1] >> (k - 2)) & 1u);
+            const double leaves = dep ? 0.5 * r * (r - 1) : (double)r * (r - 1);
+            const double node = 40.0 + 24.0 + 6.0 * k + 10.0;
+            const double per_i = ((r + 31) / 32) * (base == SEL_SENS ? 10.0 : 8.0) + 4.0;
+            const double cost = (node + per_i * r) / std::max(1.0, leaves) * par(L);
+            if (cost < best * 0.98) { best = cost; bestL = L; bestLanes2 = true; }
+        }
+        if (L >= 2 && r > 16) continue;
         const int nt = build_tuples(p, L, r, canon, nullptr, kMaxTup);
         if (nt <= 0) continue;
         int nes, scale;
@@ -643,22 +689,26 @@ mapa_status plan_deep(const mapa_topology *t, const mapa_pattern *p, int selecto
         const int NT = nterm <= 2 ? 2 : (nterm <= 4 ? 4 : 6);
         const double node = 40.0 + 12.0 * L + (nes ? 6.0 * ((r * 16 + 31) / 32) : 0.0) + 6.0 * k;
         const double round = 12.0 + 3.0 * NT;
-        double cost = (node + round * ((nt + 31) / 32)) / nt;
-        // parallelism: the warps can only split the prefix levels 0..k-L-1
-        // (decoded items); with fewer prefixes than ~4 per resident warp of
-        // every rank, most warps idle
-        const uint64_t want = 4ull * 148 * 3 * 8 * (uint64_t)world;
-        const uint64_t avail = perm_count(nF, std::min(k - L, 6));
-        if (avail < want) cost *= (double)want / (double)std::max<uint64_t>(1, avail);
-        if (cost < best * 0.98) { best = cost; bestL = L; }
+        const double cost = (node + round * ((nt + 31) / 32)) / nt * par(L);
+        if (cost < best * 0.98) { best = cost; bestL = L; bestLanes2 = false; }
     }
     if (!bestL) return fail(MAPA_E_UNSUPPORTED, "deep path: no feasible suffix length");
     const int L = bestL, T = k - L, r = nF - T;
     tb->L = L;
     tb->T = T;
     tb->r = r;
-    tb->ntup = build_tuples(p, L, r, canon, tb->tup, kMaxTup);
-    tb->nterm = suffix_terms(p, L, base, tb->term, &tb->nes, &tb->scale);
+    if (bestLanes2) {
+        tb->lanes2 = 1;
+        tb->l2e = base == SEL_INSENS || ((base == SEL_GREEDY || base == SEL_SENS) && ((p->adj[T] >> (T + 1)) & 1u));
+        tb->l2dep = canon && ((p->src[T + 1] >> T) & 1u);
+        tb->ntup = 0;
+        tb->nterm = 2;  // the NT = 2 instantiation (no tuple terms are read)
+        tb->nes = 0;
+        tb->scale = 1;
+    } else {
+        tb->ntup = build_tuples(p, L, r, canon, tb->tup, kMaxTup);
+        tb->nterm = suffix_terms(p, L, base, tb->term, &tb->nes, &tb->scale);
+    }
     // prefix sources common to every suffix vertex: their max is a lower bound
     // for the whole suffix, applied by compacting the node's device list; the
     // remaining per-vertex bounds are checked per tuple (pcon)
@@ -1185,7 +1235,8 @@ static mapa_status launch_query_impl(const mapa_topology *t, const mapa_pattern 
     // canonical instantiation only when a lex-leader constraint exists (|Aut| > 1
     // and not RAW); otherwise the constraint-free kernel enumerates the same set
     const int sc = sel_code(selector, sensitive) | (has_constraints(tb.pat[0]) ? 4 : 0) |
-                   ((flags & MAPA_F_PRUNE) && p->k >= 4 ? 16 : 0);
+                   ((flags & MAPA_F_PRUNE) && p->k >= 4 ? 16 : 0) |
+                   (lin16_fits(t, p, sel_code(selector, sensitive), busy_hint) ? 32 : 0);
     Plan pl = plan_single(t, p, sc, nF, world);
     if (pl.nlocal >= (1ull << 27)) return fail(MAPA_E_UNSUPPORTED, "too many work items");
     std::memcpy(tb.lut, p->lut.data(), p->lut.size() * sizeof(uint16_t));
