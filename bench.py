@@ -181,6 +181,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-prune", action="store_true", help="skip the MAPA_F_PRUNE side measurement")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--streams", type=int, default=0,
+                    help="C4: streams for the three selector launches of a step (default 1 at N=1, 3 at N>1)")
     ap.add_argument("--config", default="c4", choices=["c4", "c1", "c2", "c3", "c5", "deep"],
                     help="c4 = the headline workload (default); c1/c2/c3/c5 measure the other SURVEY 8(d) configs; "
                          "deep = the k > 8 path (SURVEY 8(f) NEXT 1)")
@@ -253,17 +255,36 @@ def main():
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     kev = {name: [] for _, _, name in SELECTORS}
+    # One memset zeroes the three records (MAPA_F_ZEROED launches: no memset node
+    # per launch).  With N > 1 ranks each rank's three shards are small, so the
+    # three launches go to three streams and their prologues / tails overlap;
+    # at N = 1 they stay on one stream, so the per-kernel CUDA events of the
+    # timed region give each kernel's own duration (the roofline's input).
+    nstreams = args.streams or (len(SELECTORS) if world > 1 else 1)
+    lstreams = [stream] if nstreams == 1 else [torch.cuda.Stream(device=dev) for _ in range(nstreams)]
 
     def step(timed):
+        recs.zero_()
+        if nstreams > 1:
+            fork = torch.cuda.Event()
+            fork.record(stream)
         for i, (sel, sens, name) in enumerate(SELECTORS):
+            ls = lstreams[i % nstreams]
+            if nstreams > 1:
+                ls.wait_event(fork)
             if timed:
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
+                a.record(ls)
             mp.launch_query(topo, pat, sel, sens, qbuf.data_ptr(), recs[i].data_ptr(), raw=True, rank=rank,
-                            world=world, busy_hint=busy, stream=stream)
+                            world=world, busy_hint=busy, stream=ls, zeroed=True)
             if timed:
-                b.record(stream)
+                b.record(ls)
                 kev[name].append((a, b))
+        if nstreams > 1:
+            for ls in lstreams:
+                j = torch.cuda.Event()
+                j.record(ls)
+                stream.wait_event(j)
         if world > 1:
             all_gather_dev(gath.view(world, -1), recs.view(-1))
 
@@ -383,7 +404,8 @@ def main():
                                    "RAW mode, 1 allocation per selector per step",
                        "embeddings_per_step": emb_step, "allocations_per_step": len(SELECTORS),
                        "parallelism": f"shard-by-work-item x{world} + 1 NCCL all_gather/step" if world > 1
-                       else "1 GPU", "l2": "flushed between steps (256 MiB memset outside step events)"},
+                       else "1 GPU", "launch_streams": nstreams,
+                       "l2": "flushed between steps (256 MiB memset outside step events)"},
             "allocations_per_s": allocs,
             "kernel_ms": kern_ms,
             "roofline": {"bound": "alu", "kernel": f"esa_single<32,6,{'SENS' if dom == 'preserve_sensitive' else 'LIN'}> ({dom})",

@@ -94,8 +94,11 @@ enum {
     MAPA_F_RAW = 2,                 /* score every injective map (no symmetry breaking) */
     MAPA_F_ALLOW_DISCONNECTED = 4,  /* mapa_load_pattern: accept disconnected patterns */
     MAPA_F_PRUNE = 8,               /* single query: branch-and-bound argmax (same decision) */
-    MAPA_F_DEEP = 16                /* mapa_allocate: use the deep (wide-key) kernel even when the
+    MAPA_F_DEEP = 16,               /* mapa_allocate: use the deep (wide-key) kernel even when the
                                        narrow 63-bit key fits (testing / comparison) */
+    MAPA_F_ZEROED = 32              /* mapa_launch_query(_wide): the caller has zeroed d_record on the
+                                       stream already (e.g. one memset for several records): no
+                                       per-launch memset node */
 };
 
 /* Limits.  Narrow path (mapa_launch_query, batches, traces, simulation):
@@ -282,7 +285,8 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
                           int32_t bw_sensitive, uint32_t flags, void *cuda_stream,
                           mapa_decision *out);
 
-/* Device-resident launch of one query's shard: zeroes d_record and
+/* Device-resident launch of one query's shard: zeroes d_record (unless
+ * MAPA_F_ZEROED: the caller zeroed it on cuda_stream) and
  * enumerates the work items i with i % world == rank of the query whose busy
  * mask is read from d_query->busy on the device (the other d_query fields are
  * ignored; p, selector and sensitive choose the kernel).  rank = 0, world = 1

@@ -30,7 +30,7 @@ E_INVALID_ARG, E_PARSE, E_ALREADY_BUSY, E_NOT_BUSY, E_ID_RANGE = -1, -2, -3, -4,
 E_UNSUPPORTED, E_CUDA, E_DISCONNECTED, E_INTERNAL = -6, -7, -8, -10
 SEL_GREEDY, SEL_PRESERVE, SEL_BASELINE, SEL_TOPO = 0, 1, 2, 3
 POLICIES = {"baseline": 0, "topo": 1, "greedy": 2, "preserve": 3}
-F_COMMIT, F_RAW, F_ALLOW_DISCONNECTED, F_PRUNE, F_DEEP = 1, 2, 4, 8, 16
+F_COMMIT, F_RAW, F_ALLOW_DISCONNECTED, F_PRUNE, F_DEEP, F_ZEROED = 1, 2, 4, 8, 16, 32
 MAX_K = 16
 SHAPES = {"ring": 0, "tree": 1, "ringtree": 2, "full": 3, "edgeless": 4}
 
@@ -360,11 +360,12 @@ def allocate(topo: Topology, pat: Pattern, selector: int, sensitive: bool = Fals
 
 def launch_query(topo: Topology, pat: Pattern, selector: int, sensitive: bool, d_query_ptr: int,
                  d_record_ptr: int, raw: bool = False, rank: int = 0, world: int = 1,
-                 busy_hint: int = (1 << 64) - 1, stream=None, prune: bool = False):
-    """mapa_launch_query: device-resident launch (asynchronous)."""
+                 busy_hint: int = (1 << 64) - 1, stream=None, prune: bool = False, zeroed: bool = False):
+    """mapa_launch_query: device-resident launch (asynchronous); zeroed =
+    MAPA_F_ZEROED (the caller already zeroed the record on `stream`)."""
     _check(_lib.mapa_launch_query(topo.handle, pat.handle, selector, int(bool(sensitive)), d_query_ptr,
-                                  d_record_ptr, _flags(raw, prune), rank, world, busy_hint,
-                                  _stream_ptr(stream)))
+                                  d_record_ptr, _flags(raw, prune) | (F_ZEROED if zeroed else 0), rank, world,
+                                  busy_hint, _stream_ptr(stream)))
 
 
 def launch_query_wide(topo: Topology, pat: Pattern, selector: int, sensitive: bool, d_query_ptr: int,

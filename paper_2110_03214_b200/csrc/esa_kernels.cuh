@@ -311,7 +311,12 @@ __device__ __forceinline__ void leaf_k1(const Ctx<W> &c, Best &bst) {
 // lane's column holds two 16-bit offsets per register, so one LDS.128 brings 8
 // table entries (broadcast loads cost 2 wavefronts each whatever their width)
 // and one IADD3 forms two LUT addresses (every LUT byte offset is < 3*40*40*4
-// < 2^16, so the halves never carry into each other).
+// < 2^16, so the halves never carry into each other).  (Measured against a
+// u16 rank table with one IADD3 per leaf and VIADDMNMX.U16x2 over IMAD-packed
+// pairs: 3 % slower, ALU-pipe bound.)
+// lin16 (single-query Eq. 1 / 3, when the host proves the range fits): table
+// entries and the lane's column are s16 pairs, two leaves per
+// VIADDMNMX.S16x2 (see kNeg16T / kNeg16C).
 template <int W, int SEL>
 __device__ __forceinline__ int *tab_ptr(const Ctx<W> &c, int which) {
     int *t = sh().wl[c.warp].dense[which];
@@ -914,8 +919,21 @@ __device__ __forceinline__ void warp_reduce(unsigned long long &key, unsigned lo
 
 // Shared tables for Eq. 2 row stride xs + npats Eq. 2 tables + edge lists.
 // Caller syncs.
+// Pair tables a single-query kernel reads (indices into the ten of Shared,
+// order tw tz twd tzd twp tdl tse tsed ts0 ts0d): the lane column's table
+// (make_ctx) and the k-3 weight / census-delta table (inner3).
+__device__ __forceinline__ int col_table(int sc, const DevPattern &P) {
+    const int K = P.k, base = sc & 3;
+    const int sh2 = K >= 2 ? 8 * (K - 2) : 0;
+    const bool eK = K >= 2 && ((P.fwd_back[K - 2] >> (K - 1)) & 1u);
+    const bool dep = K >= 2 && (((*reinterpret_cast<const uint64_t *>(P.fwd_src) >> sh2) >> (K - 1)) & 1u);
+    if (base == SEL_SENS) return eK ? (dep ? 7 : 6) : (dep ? 9 : 8);
+    const bool eW = base != SEL_BASE && (base == SEL_INSENS || eK);
+    return eW ? (dep ? 2 : 0) : (dep ? 3 : 1);
+}
+
 template <int MAXP, int LUTCAP>
-__device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int xs, int ub_r2 = -1) {
+__device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int xs, int ub_r2 = -1, int only_sc = -1) {
     Shared &s = sh();
     const DevTopo &topo = tb.topo;
     const int tid = threadIdx.x;
@@ -923,7 +941,16 @@ __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int 
     if (tid == 0) s.one = 1;
     if (tid <= kMaxN) s.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
     static_assert(offsetof(Shared, ts0d) == offsetof(Shared, tw) + 9 * kNN * sizeof(int), "pair tables contiguous");
-    if (tb.pre) {
+    if (tb.pre && only_sc >= 0) {
+        // single query: only the two tables this selector / pattern reads (8 KB
+        // of the 40-KB image; the prologue is the fixed cost of every launch)
+        const int t0 = col_table(only_sc, tb.pat[0]), t1 = (only_sc & 3) == SEL_SENS ? 5 : 4;
+        int4 *dst = reinterpret_cast<int4 *>(s.tw);
+        for (int i = tid; i < 2 * kNN / 4; i += blockDim.x) {
+            const int t = i < kNN / 4 ? t0 : t1, j = i & (kNN / 4 - 1);
+            dst[t * (kNN / 4) + j] = tb.pre[t * (kNN / 4) + j];
+        }
+    } else if (tb.pre) {
         // cached image (host-built once per topology and xs): 16-B loads from L2
         int4 *dst = reinterpret_cast<int4 *>(s.tw);
         for (int i = tid; i < kPairTables * kNN / 4; i += blockDim.x) dst[i] = tb.pre[i];
@@ -984,8 +1011,9 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
         const DevPattern &P = tb.pat[0];
         ub_r2 = (int)P.dback[K - 2] + (int)((P.fwd_back[K - 2] >> (K - 1)) & 1u);
     }
-    load_shared(tb, xs, ub_r2);
-    const uint32_t busy = dq->busy;
+    // the query load is issued first: its latency overlaps the table copy
+    const uint32_t busy = *reinterpret_cast<const volatile uint32_t *>(&dq->busy);
+    load_shared(tb, xs, ub_r2, SEL & 3);
     __syncthreads();
 
     Ctx<W> c = make_ctx<W>(tb.topo, tb.pat[0], 0, xs, busy, SEL & 3, SelT<SEL>::pack16, SelT<SEL>::lin16);
@@ -1027,6 +1055,7 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
             start = gw * s0;
             sz = s0;
         } else {
+            if (off0 >= Nloc) break;  // the static chunks covered every item: no counter round trip
             if (lane == 0) {
                 const uint32_t cur = off0 + *reinterpret_cast<volatile uint32_t *>(&rec->ctr);
                 if (cur < Nloc) {

@@ -1211,7 +1211,7 @@ mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int
                                   uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint,
                                   void *stream) {
     return launch_query_impl(t, p, selector, sensitive, d_query, d_record, flags, rank, world, busy_hint, stream,
-                             true);
+                             !(flags & MAPA_F_ZEROED));
 }
 
 static mapa_status launch_query_impl(const mapa_topology *t, const mapa_pattern *p, int32_t selector, int32_t sensitive,
@@ -1313,7 +1313,7 @@ mapa_status mapa_launch_query_wide(const mapa_topology *t, const mapa_pattern *p
                                    int32_t sensitive, const mapa_query64 *d_query, mapa_wide_record *d_record,
                                    uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint, void *stream) {
     return launch_query_wide_impl(t, p, selector, sensitive, d_query, d_record, flags, rank, world, busy_hint,
-                                  stream, true);
+                                  stream, !(flags & MAPA_F_ZEROED));
 }
 
 static mapa_status launch_query_wide_impl(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
