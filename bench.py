@@ -65,11 +65,28 @@ def peaks():
         return {}
 
 
+def int_peaks():
+    """The integer issue / pipe microbenchmark (scripts/int_ubench.cu, run on a
+    B200 of this pool): lane-ops per SM per clock of each instruction class."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02_int_peaks.json")))
+        return {r["op"]: r["lane_ops_per_sm_per_clk"] for r in d["results"]}
+    except Exception:
+        return {}
+
+
+def issue_lanes_per_sm_clk() -> float:
+    """Issue roofline in lane-instructions per SM per clock: MEASURED with an
+    independent IADD3 (ALU pipe) + IMAD (FMA pipe) 1:1 mix, 128.06 (one
+    warp-instruction per SMSP per clock; each pipe alone 64,
+    profiles/r02_int_peaks.json).  Fallback: the nominal 128 (B300_MICROARCH)."""
+    return int_peaks().get("IADD3+IMAD (1:1)", 128.0)
+
+
 def alu_peak_gops(clock_mhz: float) -> float:
-    """Integer issue roofline: 148 SMs x 4 SMSPs x 32 lanes = 128 lane-ops/clk/SM
-    (B300_MICROARCH: 1 warp-instr/clk/SMSP; ALU pipe 16 lanes + FMA pipe (IMAD)
-    16 lanes per SMSP per clk), at the measured max SM clock."""
-    return 148 * 128 * clock_mhz * 1e6 / 1e9
+    """Integer issue roofline: 148 SMs x the measured lane-instructions per SM
+    per clock (issue_lanes_per_sm_clk) at the measured max SM clock."""
+    return 148 * issue_lanes_per_sm_clk() * clock_mhz * 1e6 / 1e9
 
 
 class ClockSampler:
@@ -134,13 +151,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def cpu_oracle_sample():
-    """Oracle (oracle/oracle.c) on the bounded sample, all host threads."""
+def cpu_model() -> str:
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_oracle_sample(nthreads=None):
+    """Oracle (oracle/oracle.c) on the bounded sample, all host threads (or nthreads)."""
     from oracle import coracle as co
     from oracle import mapa_oracle as mo
     t = mo.parse_topology(W.het32_text())
     k, e = mo.make_pattern("full", K_PAT)
-    nthreads = os.cpu_count() or 1
+    nthreads = nthreads or os.cpu_count() or 1
     t0 = time.perf_counter()
     r = co.allocate(t, 0, k, e, 0, False, nthreads=nthreads, **SAMPLE)
     dt = time.perf_counter() - t0
@@ -385,17 +412,24 @@ def main():
         dom = max(kern_ms, key=kern_ms.get)
         leaves_per_launch = RAW_PER_QUERY / world
         achieved = ALG_OPS[dom] * leaves_per_launch / (kern_ms[dom] / 1e3) / 1e9
-        traffic = None
+        traffic, lipe = None, None
         try:
             prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
             traffic = prof.get("dram_bytes_per_launch", {}).get(dom)
+            lipe = prof.get("lane_instr_per_embedding", {}).get(dom)
         except Exception:
             pass
+        # issue_frac: the kernel's executed lane-instructions per embedding (ncu,
+        # profiles/ncu_summary.json) x embeddings/s / the measured issue peak
+        emb_s = leaves_per_launch / (kern_ms[dom] / 1e3)
+        issue_frac = lipe * emb_s / (peak * 1e9) if lipe else None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             raw, dt, cores = cpu_oracle_sample()
+            raw1, dt1, _ = cpu_oracle_sample(1)
             cpu = {"value": raw / dt, "unit": "embeddings/s", "cores": cores, "kind": "oracle",
-                   "sample": SAMPLE_DESC}
+                   "sample": SAMPLE_DESC, "cpu_model": cpu_model(), "host_cpus": os.cpu_count(),
+                   "value_1thread": raw1 / dt1, "seconds": dt, "seconds_1thread": dt1}
         line = {
             "metric": METRIC, "value": value, "unit": "embeddings/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
@@ -412,9 +446,15 @@ def main():
                          "achieved": achieved, "peak": peak, "unit": "Gop/s", "frac": achieved / peak,
                          "traffic": traffic,
                          "ops_per_embedding": ALG_OPS[dom], "ops_unamortised": ALG_OPS_UNAMORTISED[dom],
-                         "note": f"{ALG_OPS[dom]} int ops per embedding (complete score from shared partials + compare; "
-                                 f"DESIGN.md Roofline); peak = 148 SM x 128 int32 lane-ops/clk (issue) x {max_mhz:.0f} MHz "
-                                 f"(measured max SM clock)"},
+                         "frac_unamortised": ALG_OPS_UNAMORTISED[dom] * emb_s / (peak * 1e9),
+                         "lane_instr_per_embedding": lipe, "issue_frac": issue_frac,
+                         "note": f"frac = {ALG_OPS[dom]} algorithmic int ops per embedding (complete the score from two "
+                                 f"shared partials + compare; DESIGN.md Roofline) x embeddings/s / peak; peak = 148 SM x "
+                                 f"{issue_lanes_per_sm_clk():.2f} lane-ops/SM/clk (measured issue rate, "
+                                 f"profiles/r02_int_peaks.json) x {max_mhz:.0f} MHz (measured max SM clock); issue_frac = "
+                                 f"ncu lane-instructions per embedding (profiles/ncu_summary.json) x embeddings/s / peak; "
+                                 f"frac_unamortised = SURVEY 8(d)'s per-embedding count (every weight re-read) over the "
+                                 f"same peak, > 1 because the enumeration tree shares prefix work"},
             "cpu_baseline": cpu,
             "e2e": {"value": emb_step * e2e_steps / e2e_s, "unit": "embeddings/s",
                     # per allocation: one 128-B H2D staging copy (16-B query + a zero record image)

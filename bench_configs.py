@@ -41,14 +41,45 @@ def _timed(torch, stream, fn, steps, warmup):
     return tot  # ms
 
 
-PEAK_GOPS = 148 * 128 * 1965e6 / 1e9   # int32 issue roofline, measured max SM clock
+def _peak_gops():
+    """148 SMs x the measured issue rate (lane-instructions per SM per clock,
+    profiles/r02_int_peaks.json: IADD3 + IMAD 1:1) x the measured max SM clock."""
+    import json
+    import os
+    root = os.path.dirname(os.path.abspath(__file__))
+    lanes, mhz = 128.0, 1965.0
+    try:
+        d = json.load(open(os.path.join(root, "profiles", "r02_int_peaks.json")))
+        lanes = {r["op"]: r["lane_ops_per_sm_per_clk"] for r in d["results"]}["IADD3+IMAD (1:1)"]
+    except Exception:
+        pass
+    try:
+        mhz = json.load(open(os.path.join(root, "MEASURED_PEAKS.json"))).get("sm_max_mhz") or mhz
+    except Exception:
+        pass
+    return 148 * lanes * mhz * 1e6 / 1e9
+
+
+def _traffic(cfg):
+    """DRAM bytes per launch of the config's dominant kernel from one ncu
+    --set full capture (profiles/ncu_summary.json "config_traffic"), or None."""
+    import json
+    import os
+    try:
+        d = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_summary.json")))
+        return d.get("config_traffic", {}).get(cfg)
+    except Exception:
+        return None
+
+
+PEAK_GOPS = _peak_gops()               # int32 issue roofline (DESIGN.md)
 OPS_MIX = (2 + 3 + 2) / 3              # ops/embedding, selectors U{Greedy, Sensitive, Insensitive}
 
 
-def _roof(emb_per_s, kernel, note=""):
+def _roof(emb_per_s, kernel, note="", cfg=None):
     ach = OPS_MIX * emb_per_s / 1e9
     return {"bound": "alu", "kernel": kernel, "achieved": ach, "peak": PEAK_GOPS, "unit": "Gop/s",
-            "frac": ach / PEAK_GOPS, "traffic": None, "ops_per_embedding": OPS_MIX, "note": note}
+            "frac": ach / PEAK_GOPS, "traffic": _traffic(cfg), "ops_per_embedding": OPS_MIX, "note": note}
 
 
 def _cpu(fn, what):
@@ -101,7 +132,7 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
                     co.allocate(o, 0, kk, ee, [0, 1, 1][i % 3], [0, 1, 0][i % 3], nthreads=1)
                 return 600 * 336, 600
             line["cpu_baseline"] = _cpu(c1_cpu, "600 C1 allocations, C oracle, 1 thread each")
-        line["roofline"] = _roof(allocs * 336, "esa_batch<8> (C1 queries)")
+        line["roofline"] = _roof(allocs * 336, "esa_batch<8> (C1 queries)", cfg="c1")
         line.update(metric="allocations/sec (C1: dgx1v ring-3, all free)", value=allocs, unit="allocations/s",
                     embeddings_per_s=allocs * 336, batch=B, e2e_latency_us_median=lat,
                     config={"workload": "C1 dgx1v ring-3 all free; 1e5 identical queries per batch launch "
@@ -165,7 +196,7 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
                 return emb, 1000
             line["cpu_baseline"] = _cpu(c2_cpu, "one dgx1p Preserve 1000-job trace replayed by the C oracle")
         line["roofline"] = _roof(total_emb * world / (total_ms / 1e3), "esa_trace<8> / esa_trace<8> (summit)",
-                                 "dependent ALLOC/RELEASE chain per CTA: latency-bound, not issue-bound")
+                                 "dependent ALLOC/RELEASE chain per CTA: latency-bound, not issue-bound", cfg="c2")
         line.update(metric="allocations/sec (C2: 1000-job FIFO traces replayed on device)",
                     value=total_allocs * world / (total_ms / 1e3), unit="allocations/s",
                     embeddings_per_s=total_emb * world / (total_ms / 1e3), per_case=res, replicas_per_case=R,
@@ -205,7 +236,7 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
                     emb_ += r["raw"]
                 return emb_, len(sample)
             line["cpu_baseline"] = _cpu(c3_cpu, f"{len(sample)} C3 queries with k <= 6, C oracle, all host threads")
-        line["roofline"] = _roof(emb * world / (ms / 1e3), "esa_single<16,K,*> (C3 queries)")
+        line["roofline"] = _roof(emb * world / (ms / 1e3), "esa_single<16,K,*> (C3 queries)", cfg="c3")
         line.update(metric="embeddings/sec (C3: cubemesh16, k in {4,6,8}, random busy)", value=emb * world / (ms / 1e3),
                     unit="embeddings/s", allocations_per_s=len(qs) * world / (ms / 1e3), queries=len(qs) * world,
                     scaling="weak",
@@ -249,7 +280,7 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
                     emb_ += r["raw"]
                 return emb_, len(sample)
             line["cpu_baseline"] = _cpu(c5_cpu, "first 40 het32 C5 queries, C oracle, all host threads")
-        line["roofline"] = _roof(tot_emb * world / (tot_ms / 1e3), "esa_batch<32> + esa_batch<16>")
+        line["roofline"] = _roof(tot_emb * world / (tot_ms / 1e3), "esa_batch<32> + esa_batch<16>", cfg="c5")
         line.update(metric="embeddings/sec (C5: 1e5 batched random queries per topology)",
                     value=tot_emb * world / (tot_ms / 1e3), unit="embeddings/s",
                     allocations_per_s=tot_q * world / (tot_ms / 1e3), per_topology=res, scaling="weak",
@@ -332,7 +363,7 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
         ach = 2 * emb_s / 1e9
         line["roofline"] = {"bound": "alu", "kernel": "esa_deep<NT,SEL> (ring-10 RAW)",
                             "achieved": ach, "peak": PEAK_GOPS, "unit": "Gop/s", "frac": ach / PEAK_GOPS,
-                            "traffic": None, "ops_per_embedding": 2,
+                            "traffic": _traffic("deep"), "ops_per_embedding": 2,
                             "note": "same algorithmic count as the narrow kernel (complete the score from the "
                                     "shared prefix partial + compare)"}
         line.update(metric="embeddings/sec (deep path: cubemesh16 ring-10 all free, RAW)", value=emb_s,

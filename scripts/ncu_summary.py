@@ -50,6 +50,10 @@ def raw_rows(rep):
     return res
 
 
+def _us(v, unit):
+    return v / 1e3 if unit in ("nsecond", "ns") else (v * 1e3 if unit in ("msecond", "ms") else v)
+
+
 def launches(path):
     rows = [r for r in csv.reader(open(path)) if r]
     i = next(k for k, r in enumerate(rows) if "Kernel Name" in r)
@@ -75,10 +79,32 @@ def main():
     ap.add_argument("--rep")
     ap.add_argument("--launches")
     ap.add_argument("--tag", required=True)
+    ap.add_argument("--configs", action="store_true",
+                    help="the report is scripts/prof_configs.py's: also write profiles/ncu_summary.json "
+                         "(per-launch DRAM bytes and C4 lane-instructions per embedding)")
     a = ap.parse_args()
     out = {"tag": a.tag}
     if a.rep:
         out["full"] = raw_rows(a.rep)
+        if a.configs:
+            sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+            from prof_configs import KERNELS  # noqa: E402  (index -> config)
+            full = [k for k in out["full"] if "esa_" in k["kernel"]]
+            assert len(full) == len(KERNELS), (len(full), len(KERNELS))
+            byk = dict(zip(KERNELS, full))
+            dram = {n: k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"] for n, k in byk.items()}
+            emb = 652458240  # P(32,6): one C4 RAW launch
+            summ = {"source": f"profiles/{a.tag}_ncu.json (ncu --set full, scripts/prof_configs.py: one launch of "
+                              f"each config's dominant kernel)",
+                    "dram_bytes_per_launch": {n[3:]: dram[n] for n in KERNELS[:3]},
+                    "lane_instr_per_embedding": {n[3:]: byk[n]["smsp__inst_executed.sum"] * 32 / emb
+                                                 for n in KERNELS[:3]},
+                    "kernel_us_ncu": {n: _us(byk[n]["gpu__time_duration.sum"], byk[n]["gpu__time_duration.sum.unit"])
+                                      for n in KERNELS},
+                    "config_traffic": {n: dram[n] for n in KERNELS[3:]}}
+            summ["config_traffic"]["c4"] = dram["c4_preserve_sensitive"]
+            with open("profiles/ncu_summary.json", "w") as f:
+                json.dump(summ, f, indent=1)
     if a.launches:
         out["launch_list"] = launches(a.launches)
     os.makedirs("profiles", exist_ok=True)

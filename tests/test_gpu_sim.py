@@ -54,20 +54,61 @@ def test_simulate_vs_oracle(name, count, kmax, policy):
         assert abs(g["pred_effbw"] - e["pred_effbw"]) <= 1e-6 * max(1.0, abs(e["pred_effbw"]))
 
 
-def test_preserve_lifts_lower_tail_300_jobs():
-    """300-job dgx1v run (§4): for bandwidth-sensitive jobs the 25th
-    percentile of predicted EffBW under Preserve is >= Baseline's (SPEC S:435;
-    Fig. 12c direction); summaries come from mapa_quantiles."""
-    out = {}
-    for pol in POLICIES:
-        js = W.sim_jobs(2110, 300, 5)
-        shapes = sorted({(j["shape"], j["k"]) for j in js})
-        pid = {sk: i for i, sk in enumerate(shapes)}
-        t = mp.Topology("dgx1v")
-        pats = [mp.Pattern.make(s, k) for s, k in shapes]
-        log = mp.simulate(t, pats, [(pid[(j["shape"], j["k"])], j["sensitive"], j["duration"]) for j in js], pol)
-        for r, j in zip(log, js):
-            r["sensitive"] = j["sensitive"]
-        out[pol] = mp.summarize(log, "sensitive")
-    assert out["preserve"][1]["pred_effbw"][1] >= out["baseline"][1]["pred_effbw"][1]
-    assert out["preserve"][1]["makespan"] == out["baseline"][1]["makespan"]  # schedule is policy independent
+def _sim_spec(name, seed, count, policy, kmin=1, kmax=5):
+    """mapa_simulate on SPEC's generated job mix (workloads.spec_jobs)."""
+    js = W.spec_jobs(seed, count, kmin, kmax)
+    shapes = sorted({(j["shape"], j["k"]) for j in js})
+    pid = {sk: i for i, sk in enumerate(shapes)}
+    pats = [mp.Pattern.make(s, k) for s, k in shapes]
+    log = mp.simulate(mp.Topology(name), pats, [(pid[(j["shape"], j["k"])], j["sensitive"], j["duration"]) for j in js],
+                      policy)
+    return js, log
+
+
+@pytest.mark.parametrize("seed", [2110, 2111, 2112])
+def test_spec_criterion6_baseline_fragmentation(seed):
+    """SPEC acceptance 6 (Fig. 9 analogue, "75% of jobs experience
+    allocations with 20% less bandwidth availability or worse"): 100 seeded
+    jobs of 2-5 GPUs on dgx1v under Baseline; agg_bw / ideal agg_bw of the
+    3-GPU jobs has p25 <= 0.8.  Ideal = the best ring-3 AggBW on the idle
+    machine (the oracle's; 125, the C1 answer)."""
+    o = mo.builtin("dgx1v")
+    ideal = mo.allocate(o, 0, *mo.make_pattern("ring", 3), 0, False)["agg_bw"]
+    assert ideal == 125
+    js, log = _sim_spec("dgx1v", seed, 100, "baseline", 2, 5)
+    r3 = [r["agg_bw"] / ideal for r, j in zip(log, js) if j["k"] == 3]
+    assert len(r3) >= 10
+    assert mp.quantiles(r3)[1] <= 0.8, mp.quantiles(r3)
+
+
+@pytest.mark.parametrize("name", ["dgx1v", "cubemesh16"])
+def test_spec_criterion7_preserve_lifts_p25(name):
+    """SPEC acceptance 7 (Fig. 12c / fig:16-GPU_simulation): on
+    seeded 300-job mixes, for bandwidth-sensitive multi-GPU jobs the 25th
+    percentile of predicted EffBW (Eq. 2) under Preserve is >= Baseline's and
+    >= Topo-aware's.  Quantiles over k >= 2 (reading A24: a 1-GPU
+    job has no link, census (0,0,0), 12.337 under every policy)."""
+    for seed in (2110, 2111, 2112):
+        q = {}
+        for pol in ("baseline", "topo", "preserve"):
+            js, log = _sim_spec(name, seed, 300, pol)
+            q[pol] = mp.quantiles([r["pred_effbw"] for r, j in zip(log, js) if j["sensitive"] and j["k"] >= 2])
+        assert q["preserve"][1] >= q["baseline"][1], (name, seed, q)
+        assert q["preserve"][1] >= q["topo"][1], (name, seed, q)
+        assert q["preserve"][1] > q["baseline"][1], (name, seed, q)  # not a tie: the lift is real
+
+
+@pytest.mark.xfail(strict=True, reason="SPEC criterion 7's cubemesh16 min clause does not hold for this job mix: "
+                   "Preserve min 9.03 / 3.21 / 3.21 vs Baseline p25 11.38 / 10.45 / 16.84 (seeds 2110-2112; "
+                   "strict FIFO on a fragmented 16-GPU graph forces 5-GPU rings onto PCIe-heavy sets); "
+                   "recorded in DESIGN.md, not weakened")
+def test_spec_criterion7_cubemesh16_min_clause():
+    """SPEC acceptance 7, last clause ("equivalent to the 25th
+    percentile"): on cubemesh16, min predicted EffBW of Preserve >= p25 of
+    Baseline for sensitive multi-GPU jobs."""
+    for seed in (2110, 2111, 2112):
+        q = {}
+        for pol in ("baseline", "preserve"):
+            js, log = _sim_spec("cubemesh16", seed, 300, pol)
+            q[pol] = mp.quantiles([r["pred_effbw"] for r, j in zip(log, js) if j["sensitive"] and j["k"] >= 2])
+        assert q["preserve"][0] >= q["baseline"][1], (seed, q)

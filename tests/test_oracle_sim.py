@@ -101,3 +101,21 @@ def test_host_quantiles_equal_oracle():
     assert mp.quantiles([10, 20, 30, 40]) == (10, 17.5, 25, 32.5, 40)
     with pytest.raises(mp.MapaError):
         mp.quantiles([])
+
+
+def test_spec_generate_jobs_mix():
+    """SPEC generate_jobs examples: deterministic for a seed; 300
+    jobs of U{1..5} GPUs -> every gpu_count class within the binomial 99 %
+    bounds of 60 (60 +- 2.576 sqrt(300 * 0.2 * 0.8) = [42, 78]); 6 networks ->
+    each within those of 50 ([34, 66]); Ring for k >= 2, the singleton for k = 1."""
+    a, b = W.spec_jobs(2110, 300), W.spec_jobs(2110, 300)
+    assert a == b
+    for seed in (2110, 2111, 2112):
+        js = W.spec_jobs(seed, 300)
+        for k in range(1, 6):
+            assert 42 <= sum(j["k"] == k for j in js) <= 78, (seed, k)
+        for name, _, _ in W.NETWORKS:
+            assert 34 <= sum(j["network"] == name for j in js) <= 66, (seed, name)
+        assert all(j["shape"] == ("ring" if j["k"] >= 2 else "full") for j in js)
+        assert all(bool(j["sensitive"]) == (j["network"] in ("alexnet", "vgg16", "resnet50", "inceptionv3"))
+                   for j in js)

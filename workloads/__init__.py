@@ -249,6 +249,21 @@ def sim_jobs(seed: int, count: int = 300, kmax: int = 5):
     return jobs
 
 
+def spec_jobs(seed: int, count: int = 300, kmin: int = 1, kmax: int = 5):
+    """SPEC generate_jobs (§4 "Jobs configuration"):
+    network U(6) -> (sensitive, duration), requested GPUs
+    U{kmin..kmax}, shape Ring for k >= 2 (NCCL's all-reduce ring) and the
+    singleton for k = 1, all at t = 0.  The job mix of the directional
+    simulator checks (SPEC acceptance criteria 6-7)."""
+    jobs = []
+    for j in range(count):
+        r = stream(seed ^ 0x5EC, j)
+        name, sens, dur = NETWORKS[r.below(6)]
+        k = r.randint(kmin, kmax)
+        jobs.append(dict(job=j, network=name, sensitive=int(sens), duration=dur, k=k, shape="ring" if k >= 2 else "full"))
+    return jobs
+
+
 def fifo_ops(jobs, n_devices: int):
     """Op sequence of a strict-FIFO replay where every job arrives at t=0
     (SPEC S:404).  Admission depends only on the FREE COUNT (the
