@@ -50,6 +50,10 @@ def raw_rows(rep):
     return res
 
 
+def _bytes(v, unit):
+    return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Kibyte": 1024, "Mibyte": 1 << 20}.get(unit, 1)
+
+
 def _us(v, unit):
     return v / 1e3 if unit in ("nsecond", "ns") else (v * 1e3 if unit in ("msecond", "ms") else v)
 
@@ -92,7 +96,8 @@ def main():
             full = [k for k in out["full"] if "esa_" in k["kernel"]]
             assert len(full) == len(KERNELS), (len(full), len(KERNELS))
             byk = dict(zip(KERNELS, full))
-            dram = {n: k["dram__bytes_read.sum"] + k["dram__bytes_write.sum"] for n, k in byk.items()}
+            dram = {n: _bytes(k["dram__bytes_read.sum"], k["dram__bytes_read.sum.unit"]) +
+                    _bytes(k["dram__bytes_write.sum"], k["dram__bytes_write.sum.unit"]) for n, k in byk.items()}
             emb = 652458240  # P(32,6): one C4 RAW launch
             summ = {"source": f"profiles/{a.tag}_ncu.json (ncu --set full, scripts/prof_configs.py: one launch of "
                               f"each config's dominant kernel)",
