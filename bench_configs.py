@@ -251,11 +251,15 @@ def run_config(args, mp, md, torch, dev, stream, rank, world, max_over_ranks):
         for tname in ("cubemesh16", "het32"):
             n = 16 if tname == "cubemesh16" else 32
             topo = mp.Topology(tname) if tname == "cubemesh16" else mp.Topology(text=W.het32_text())
-            qs = W.c5_queries(n, count=100_000)[rank::world]
+            allq = W.c5_queries(n, count=100_000)
             pats = [mp.Pattern.make(s, k) for s, k in SHAPE_K]
             pid = {sk: i for i, sk in enumerate(SHAPE_K)}
-            qt = md.queries_tensor([(q["busy"], pid[(q["shape"], q["k"])], q["selector"], q["sensitive"])
-                                    for q in qs], device=dev)
+            rows = [(q["busy"], pid[(q["shape"], q["k"])], q["selector"], q["sensitive"]) for q in allq]
+            # the library's LPT deal (mapa_shard_queries): heaviest queries first, each to the
+            # least-loaded rank; no data-path collective
+            idx, myrows = md.shard_rows(topo, pats, rows, raw=True)
+            qs = [allq[i] for i in idx]
+            qt = md.queries_tensor(myrows, device=dev)
             emb = sum(math.perm(n - bin(q["busy"]).count("1"), q["k"]) for q in qs)
             ms = _timed(torch, stream, lambda: md.run_batch(topo, pats, qt, raw=True, stream=stream),
                         max(1, steps // 10), warmup) / max(1, steps // 10)

@@ -391,6 +391,19 @@ mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *cons
                                 mapa_record *d_results, void *d_scratch, uint32_t flags,
                                 void *cuda_stream);
 
+/* Host: deal nq independent queries (host copies, as for the batch) over
+ * `world` ranks for a multi-GPU batch (batches shard by query,
+ * no data-path collective).  A query's work is the number of leaves its launch
+ * scores, P(|F|,k) with MAPA_F_RAW, else P(|F|,k)/|Aut(P)| (0 without
+ * capacity); queries are taken heaviest first (ties by index) and each goes
+ * to the least-loaded rank (ties by rank): longest-processing-time-first,
+ * deterministic, every rank's load <= mean + the largest query.  owner[nq]
+ * out (rank of each query); load[world] (may be NULL) out, in leaves.
+ * Errors: INVALID_ARG (a pattern index out of range). */
+mapa_status mapa_shard_queries(const mapa_topology *t, const mapa_pattern *const *pats, int32_t npats, int64_t nq,
+                               const mapa_query *queries, uint32_t flags, int32_t world, int32_t *owner,
+                               double *load);
+
 /* ----------------------------------------------------------- trace replay */
 
 /* C2: ntraces independent FIFO traces replayed entirely on the device, one

@@ -131,6 +131,9 @@ _SIGS = {
     "mapa_decode_trace": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(TraceOp),
                                ctypes.c_int32, ctypes.POINTER(Query), ctypes.POINTER(ctypes.c_uint64), ctypes.c_uint32,
                                ctypes.POINTER(Decision)]),
+    "mapa_shard_queries": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(Query),
+                                ctypes.c_uint32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                ctypes.POINTER(ctypes.c_double)]),
     "mapa_fifo_schedule": (_S, [ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
                                 ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                 ctypes.POINTER(TraceOp), ctypes.POINTER(ctypes.c_double),
@@ -428,6 +431,18 @@ def allocate_batch(topo: Topology, pats, nq: int, d_queries_ptr: int, d_results_
     arr = (_vp * len(pats))(*[p.handle for p in pats])
     _check(_lib.mapa_allocate_batch(topo.handle, arr, len(pats), nq, d_queries_ptr, d_results_ptr,
                                     d_scratch_ptr, F_RAW if raw else 0, _stream_ptr(stream)))
+
+
+def shard_queries(topo: Topology, pats, rows, world: int, raw: bool = False):
+    """mapa_shard_queries: LPT deal of batch queries rows [(busy, pattern
+    index, selector, sensitive)] over `world` ranks -> (owner per query, load
+    per rank in leaves)."""
+    arr = (_vp * len(pats))(*[p.handle for p in pats])
+    hq = (Query * max(1, len(rows)))(*[Query(b & 0xFFFFFFFF, pi, sel, int(bool(sens))) for b, pi, sel, sens in rows])
+    own = (ctypes.c_int32 * max(1, len(rows)))()
+    ld = (ctypes.c_double * world)()
+    _check(_lib.mapa_shard_queries(topo.handle, arr, len(pats), len(rows), hq, F_RAW if raw else 0, world, own, ld))
+    return list(own)[:len(rows)], list(ld)
 
 
 def trace_replay(topo: Topology, pats, ntraces: int, nops: int, d_ops_ptr: int, njobs: int, d_jobs_ptr: int,

@@ -1881,6 +1881,46 @@ mapa_status mapa_decode_trace(const mapa_topology *t, const mapa_pattern *const 
     return MAPA_OK;
 }
 
+mapa_status mapa_shard_queries(const mapa_topology *t, const mapa_pattern *const *pats, int32_t npats, int64_t nq,
+                               const mapa_query *queries, uint32_t flags, int32_t world, int32_t *owner,
+                               double *load) {
+    if (!t || !pats || npats < 1 || nq < 0 || world < 1 || (nq > 0 && (!queries || !owner)))
+        return fail(MAPA_E_INVALID_ARG, "bad shard arguments");
+    // work of a query = the leaves its launch scores: P(|F|, k) in RAW mode,
+    // P(|F|, k) / |Aut(P)| canonical (orbit theorem); 0 without capacity
+    std::vector<std::pair<double, int64_t>> wq((size_t)nq);
+    for (int64_t i = 0; i < nq; ++i) {
+        const mapa_query &q = queries[i];
+        if (q.pattern >= (uint32_t)npats || !pats[q.pattern])
+            return fail(MAPA_E_INVALID_ARG, "query " + std::to_string(i) + ": pattern index out of range");
+        const mapa_pattern *p = pats[q.pattern];
+        const int nf = __builtin_popcountll(~(uint64_t)q.busy & nmask_of(t->n));
+        double w = 0.0;
+        if (p->k <= nf) {
+            w = 1.0;
+            for (int j = 0; j < p->k; ++j) w *= (double)(nf - j);
+            if (!(flags & MAPA_F_RAW)) w /= (double)p->aut;
+        }
+        wq[(size_t)i] = {w, i};
+    }
+    // LPT: heaviest first (ties by query index), each to the least-loaded rank
+    // (ties by rank id): deterministic, max load <= mean + the largest query
+    std::stable_sort(wq.begin(), wq.end(), [](const std::pair<double, int64_t> &a, const std::pair<double, int64_t> &b) {
+        return a.first > b.first;
+    });
+    std::vector<double> ld((size_t)world, 0.0);
+    for (const auto &x : wq) {
+        int r = 0;
+        for (int j = 1; j < world; ++j)
+            if (ld[(size_t)j] < ld[(size_t)r]) r = j;
+        owner[x.second] = r;
+        ld[(size_t)r] += x.first;
+    }
+    if (load)
+        for (int j = 0; j < world; ++j) load[j] = ld[(size_t)j];
+    return MAPA_OK;
+}
+
 mapa_status mapa_quantiles(const double *v, int32_t n, double *out) {
     if (!v || !out || n < 1) return fail(MAPA_E_INVALID_ARG, "quantiles of an empty set");
     std::vector<double> a(v, v + n);

@@ -20,7 +20,7 @@ import torch
 import torch.distributed as dist
 
 from . import (Pattern, Record, Topology, WideRecord, decode, decode_wide, launch_query, launch_queries, launch_query_wide,
-               allocate_batch, reduce_records, reduce_wide_records, trace_replay, SEL_PRESERVE)
+               allocate_batch, reduce_records, reduce_wide_records, shard_queries, trace_replay, SEL_PRESERVE)
 
 U32 = 0xFFFFFFFF
 
@@ -158,6 +158,17 @@ def allocate_sharded_wide(topo: Topology, pat: Pattern, selector: int, sensitive
     rec, _q = run_query_wide(topo, pat, selector, sensitive, busy, raw=raw, rank=rank, world=world, prune=prune)
     r = combine_wide_records(rec, group)
     return decode_wide(topo, pat, busy, selector, sensitive, r, raw=raw, prune=prune)
+
+
+def shard_rows(topo: Topology, pats, rows, raw: bool = False, group=None):
+    """This rank's share of a multi-GPU batch: the library's LPT deal
+    (mapa_shard_queries, identical on every rank) -> (indices, rows) owned by
+    this rank.  No collective: each rank runs its own queries."""
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    owner, _ = shard_queries(topo, pats, rows, world, raw=raw)
+    idx = [i for i, o in enumerate(owner) if o == rank]
+    return idx, [rows[i] for i in idx]
 
 
 def run_batch(topo: Topology, pats, queries, raw: bool = False, stream=None):

@@ -156,3 +156,52 @@ def test_two_rank_wide_combine_matches_unsharded_deep_oracle():
             g = got[r][i]
             for f in ("devices", "mapping", "used_edges", "x", "y", "z", "agg_bw", "preserved_bw", "raw"):
                 assert g[f] == exp[f], (name, r, f, g[f], exp[f])
+
+
+def _worker_shard(rank, port, out_q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    import workloads as W
+    import paper_2110_03214_b200 as mp
+    from paper_2110_03214_b200 import dist as md
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=WORLD)
+    t = mp.Topology(text=W.het32_text())
+    shapes = [(s, k) for s in ("ring", "tree", "full") for k in range(2, 6)]
+    pats = [mp.Pattern.make(s, k) for s, k in shapes]
+    pid = {sk: i for i, sk in enumerate(shapes)}
+    rows = [(q["busy"], pid[(q["shape"], q["k"])], q["selector"], q["sensitive"])
+            for q in W.c5_queries(32, count=3000, seed=11)]
+    idx, mine = md.shard_rows(t, pats, rows, raw=True)
+    assert mine == [rows[i] for i in idx]
+    out_q.put((rank, idx))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_batch_lpt_deal_partitions_the_queries():
+    """Multi-GPU batches: every rank calls dist.shard_rows (the
+    library's LPT deal, no collective) on the same rows; the two ranks' query
+    sets are disjoint, cover the batch, and their work differs by at most the
+    largest query."""
+    import math
+
+    import workloads as W
+
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_shard, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=240) for _ in range(WORLD))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a, b = set(got[0]), set(got[1])
+    assert not a & b and a | b == set(range(3000))
+    qs = W.c5_queries(32, count=3000, seed=11)
+    work = [math.perm(32 - bin(x["busy"]).count("1"), x["k"]) for x in qs]
+    assert abs(sum(work[i] for i in a) - sum(work[i] for i in b)) <= max(work)

@@ -396,3 +396,32 @@ def test_deep_prune_forced_set_ties():
     for f in FIELDS + ("distinct", "pred_effbw", "key", "ecode"):
         assert pr[f] == ex[f], ("ring16", f)
     assert pr["leaves"] < ex["leaves"]
+
+
+def test_deep_k12_13_vs_oracle_golden(golden_dir):
+    """k = 12 and 13 NON-clique patterns (ring / tree / ringtree) on the
+    16-GPU graphs with exactly k or k+1 free devices: every decision field of
+    the deep path (RAW and canonical) equals the deep C oracle's, stored in
+    tests/golden/deep_k12_13.json by tests/golden/make_golden_deep.py (oracle/
+    only; 12! = 4.8e8 and 13! = 6.2e9 permutations per case); canonical
+    leaves = raw / |Aut| (orbit theorem)."""
+    import json
+    import os
+    path = os.path.join(golden_dir, "deep_k12_13.json")
+    if not os.path.exists(path):
+        pytest.skip("deep golden not generated")
+    cases = json.load(open(path))["cases"]
+    assert len(cases) == 16
+    tops = {n: mp.Topology(n) for n in ("cubemesh16", "torus2d16")}
+    for c in cases:
+        t = tops[c["topology"]]
+        p = mp.Pattern.make(c["shape"], c["k"])
+        exp = dict(c, devices=tuple(c["devices"]), mapping=tuple(c["mapping"]),
+                   used_edges=[tuple(e) for e in c["used_edges"]])
+        nf = 16 - bin(c["busy"]).count("1")
+        assert exp["raw"] == math.perm(nf, c["k"])
+        t.set_busy(c["busy"])
+        for raw in (False, True):
+            g = mp.allocate(t, p, c["selector"], bool(c["sensitive"]), raw=raw)
+            same(exp, g, (c["topology"], c["shape"], c["k"], nf, c["selector"], c["sensitive"], raw))
+            assert g["leaves"] == (exp["raw"] if raw else exp["raw"] // p.info()["aut"])

@@ -294,3 +294,35 @@ def test_decode_trace_recovers_oracle_replay():
     zero = list(keys)
     zero[first[1]] = 0
     assert mp.decode_trace(t, pats, ops, rows, zero)[first[1]]["status"] == "no_capacity"
+
+
+def test_shard_queries_lpt():
+    """mapa_shard_queries (SURVEY §8(e) batches): every query owned by one rank
+    in [0, world); loads = the per-rank sums of P(|F|,k) (RAW) or
+    P(|F|,k)/|Aut| (canonical); LPT bound max load <= mean + largest query;
+    deterministic; world 1 owns everything."""
+    t = mp.Topology("cubemesh16")
+    shapes = [(s, k) for s in ("ring", "tree", "full") for k in range(2, 6)]
+    pats = [mp.Pattern.make(s, k) for s, k in shapes]
+    qs = W.c5_queries(16, count=2000, seed=5)
+    pid = {sk: i for i, sk in enumerate(shapes)}
+    rows = [(q["busy"], pid[(q["shape"], q["k"])], q["selector"], q["sensitive"]) for q in qs]
+    for raw in (True, False):
+        work = []
+        for q in qs:
+            nf = 16 - bin(q["busy"]).count("1")
+            w = math.perm(nf, q["k"]) if q["k"] <= nf else 0
+            if not raw:
+                w //= mo.automorphism_count(*mo.make_pattern(q["shape"], q["k"]))
+            work.append(w)
+        for world in (1, 2, 3, 8):
+            own, load = mp.shard_queries(t, pats, rows, world, raw=raw)
+            assert own == mp.shard_queries(t, pats, rows, world, raw=raw)[0]
+            assert all(0 <= o < world for o in own)
+            exp = [sum(w for w, o in zip(work, own) if o == r) for r in range(world)]
+            assert [round(x) for x in load] == exp
+            assert max(exp) <= sum(work) / world + max(work)
+            if world == 1:
+                assert set(own) == {0}
+    with pytest.raises(mp.MapaError):
+        mp.shard_queries(t, pats, [(0, 99, 0, 0)], 2)
