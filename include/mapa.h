@@ -300,15 +300,20 @@ mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int
                               uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint,
                               void *cuda_stream);
 
-/* nq independent single queries, each a full-GPU mapa_launch_query (narrow
- * path), from ONE call: zeroes d_records[nq] once, forks `nstreams` internal
- * streams (owned by the topology, created on first use) from cuda_stream
- * with an event, launches query i on stream i % nstreams (its busy mask
- * from h_queries[i] plans the grid; the kernel reads d_queries[i]), and makes
- * cuda_stream wait for all of them: ordered like one launch on cuda_stream,
- * with small queries' launch and drain overlapping.  pats[npats] indexed by
- * the query's `pattern`.  Errors as mapa_launch_query (the first failing
- * query's; earlier launches stay enqueued). */
+/* nq independent single queries (narrow path) from ONE call: zeroes
+ * d_records[nq] once, forks `nstreams` internal streams (owned by the
+ * topology, created on first use) from cuda_stream with an event and makes
+ * cuda_stream wait for all of them: ordered like one launch on cuda_stream.
+ * Queries that score fewer than 2^22 leaves (P(|F|,k), /|Aut| canonical) run
+ * together in ONE batch launch (the mapa_allocate_batch kernel over a
+ * host-built order of those queries, grouped by (k, selector)) on the first
+ * stream, when every pattern fits the batch kernel (npats <= 16, k <= 8) and
+ * MAPA_F_PRUNE is not set; every other query gets a full-GPU mapa_launch_query
+ * (its busy mask from h_queries[i] plans the grid; the kernel reads
+ * d_queries[i]) round-robin over the streams.  The records are the same
+ * either way.  pats[npats] indexed by the query's `pattern`.  Errors as
+ * mapa_launch_query (the first failing query's; earlier launches stay
+ * enqueued). */
 mapa_status mapa_launch_queries(mapa_topology *t, const mapa_pattern *const *pats, int32_t npats, int32_t nq,
                                 const mapa_query *h_queries, const mapa_query *d_queries, mapa_record *d_records,
                                 uint32_t flags, int32_t nstreams, void *cuda_stream);

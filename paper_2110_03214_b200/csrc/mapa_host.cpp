@@ -45,6 +45,11 @@ struct mapa_topology {
     void *h_stage = nullptr;      // pinned host mirror
     cudaStream_t cap = nullptr;   // private stream for graph capture (the caller's may be the legacy stream)
     std::vector<cudaStream_t> side;  // mapa_launch_queries' fork streams
+    // mapa_launch_queries' small-query batch: device [counter (64 B) | order],
+    // its pinned host staging, and the event guarding the staging's reuse
+    void *d_mix = nullptr, *h_mix = nullptr;
+    size_t mix_cap = 0;
+    cudaEvent_t ev_mix = nullptr;
     // deep-path launch plans (suffix length, tuple table, terms, depth, grid)
     // keyed by (pattern uid, selector code, |F|, N, world): planning costs
     // far more host time than a small deep launch
@@ -1099,6 +1104,9 @@ void mapa_free_topology(mapa_topology *t) {
     if (t->cap) cudaStreamDestroy(t->cap);
     if (t->d_stage) cudaFree(t->d_stage);
     if (t->h_stage) cudaFreeHost(t->h_stage);
+    if (t->ev_mix) cudaEventSynchronize(t->ev_mix), cudaEventDestroy(t->ev_mix);
+    if (t->d_mix) cudaFree(t->d_mix);
+    if (t->h_mix) cudaFreeHost(t->h_mix);
     delete t;
 }
 
@@ -1271,15 +1279,86 @@ mapa_status mapa_launch_queries(mapa_topology *t, const mapa_pattern *const *pat
         cudaEventDestroy(fork);
         return cuda_fail(err, "cudaEventCreate");
     }
+    // Small queries (fewer than kMixLeaves leaves) go to ONE batch launch on
+    // side stream 0, ordered by code path (k, selector); the others keep a
+    // full-GPU single-query launch each, round-robin over the side streams.
+    // A single launch costs ~10 us of fixed time (prologue, ramp, drain), more
+    // than a small query's work.  Same records either way (max / sum).
+    constexpr double kMixLeaves = 4194304.0;
+    std::vector<uint32_t> small;
+    bool can_batch = npats <= kMaxPats && !(flags & MAPA_F_PRUNE) && t->n <= kMaxN;
+    for (int i = 0; i < npats && can_batch; ++i) can_batch = pats[i] && key_fits(t, pats[i]);
+    std::vector<char> is_small((size_t)nq, 0);
+    for (int i = 0; i < nq; ++i) {
+        const mapa_query &q = h_queries[i];
+        if (q.pattern >= (uint32_t)npats || !pats[q.pattern]) {
+            cudaEventDestroy(fork);
+            cudaEventDestroy(join);
+            return fail(MAPA_E_INVALID_ARG, "query pattern index out of range");
+        }
+        if (!can_batch) continue;
+        const mapa_pattern *p = pats[q.pattern];
+        const int nf = __builtin_popcountll(~(uint64_t)q.busy & nmask_of(t->n));
+        double w = 1.0;
+        for (int j = 0; j < p->k; ++j) w *= (double)std::max(0, nf - j);
+        if (!(flags & MAPA_F_RAW)) w /= (double)p->aut;
+        if (w < kMixLeaves && q.selector >= 0 && q.selector <= 2) { is_small[(size_t)i] = 1; small.push_back((uint32_t)i); }
+    }
+    if (small.size() < 2) {
+        small.clear();
+        std::fill(is_small.begin(), is_small.end(), 0);
+    }
     cudaEventRecord(fork, main);
     for (int s2 = 0; s2 < nstreams; ++s2) cudaStreamWaitEvent(t->side[s2], fork, 0);
     mapa_status st = MAPA_OK;
+    if (!small.empty()) {
+        static thread_local MultiTables *tbp = nullptr;
+        if (!tbp) tbp = new MultiTables();
+        st = build_multi(t, pats, npats, flags, tbp);
+        const size_t bytes = 64 + 4 * small.size();
+        if (st == MAPA_OK && bytes > t->mix_cap) {
+            if (t->ev_mix) cudaEventSynchronize(t->ev_mix);
+            if (t->d_mix) cudaFree(t->d_mix);
+            if (t->h_mix) cudaFreeHost(t->h_mix);
+            t->d_mix = t->h_mix = nullptr;
+            t->mix_cap = 0;
+            if ((err = (int)cudaMalloc(&t->d_mix, bytes)) || (err = (int)cudaMallocHost(&t->h_mix, bytes)))
+                st = cuda_fail(err, "cudaMalloc (query batch)");
+            else
+                t->mix_cap = bytes;
+        }
+        if (st == MAPA_OK && !t->ev_mix && (err = (int)cudaEventCreateWithFlags(&t->ev_mix, cudaEventDisableTiming)))
+            st = cuda_fail(err, "cudaEventCreate");
+        if (st == MAPA_OK) {
+            cudaEventSynchronize(t->ev_mix);  // the previous call's copy out of h_mix is done
+            std::stable_sort(small.begin(), small.end(), [&](uint32_t a, uint32_t b) {
+                const mapa_query &qa = h_queries[a], &qb = h_queries[b];
+                const int ka = pats[qa.pattern]->k * 4 + sel_code(qa.selector, qa.sensitive);
+                const int kb = pats[qb.pattern]->k * 4 + sel_code(qb.selector, qb.sensitive);
+                return ka < kb;
+            });
+            std::memcpy((char *)t->h_mix + 64, small.data(), 4 * small.size());
+            cudaStream_t s0 = t->side[0];
+            int sm = device_sm_count();
+            if (sm <= 0) sm = 148;
+            const int canon = multi_has_constraints(*tbp);
+            const int grid = sm * max_blocks_per_sm_batch(t->width, canon, tbp->npats, tbp->xs);
+            if ((err = (int)cudaMemsetAsync(t->d_mix, 0, 64, s0)) ||
+                (err = (int)cudaMemcpyAsync((char *)t->d_mix + 64, (char *)t->h_mix + 64, 4 * small.size(),
+                                            cudaMemcpyHostToDevice, s0)) ||
+                (err = (int)cudaEventRecord(t->ev_mix, s0)) ||
+                (err = launch_batch(*tbp, canon, (int64_t)small.size(), d_queries, d_records, (uint32_t *)t->d_mix,
+                                    (const uint32_t *)((char *)t->d_mix + 64), grid, (void *)s0)))
+                st = cuda_fail(err, "query batch launch");
+        }
+    }
+    int nb = 0;
     for (int i = 0; i < nq && st == MAPA_OK; ++i) {
+        if (is_small[(size_t)i]) continue;
         const mapa_query &q = h_queries[i];
-        if (q.pattern >= (uint32_t)npats || !pats[q.pattern]) { st = fail(MAPA_E_INVALID_ARG, "query pattern index out of range"); break; }
         if (q.selector < 0 || q.selector > 2) { st = fail(MAPA_E_INVALID_ARG, "bad selector"); break; }
         st = launch_query_impl(t, pats[q.pattern], q.selector, q.sensitive, d_queries + i, d_records + i, flags, 0, 1,
-                               q.busy, (void *)t->side[i % nstreams], false);
+                               q.busy, (void *)t->side[(nb++ + (small.empty() ? 0 : 1)) % nstreams], false);
     }
     for (int s2 = 0; s2 < nstreams; ++s2) {  // join: every side stream's work before `main` continues
         cudaEventRecord(join, t->side[s2]);
