@@ -2,20 +2,23 @@
 # One GPU-box pass that regenerates the round's measurement evidence into gpurun_out/
 # (copied into profiles/ by hand after review):
 #   bench lines (C4 headline + C1/C2/C3/C5 + the deep path), the ncu launch list of the
-#   bench command, one `ncu --set full` capture of the three C4 kernels and of the deep
-#   kernel, and the simulator report.
+#   headline bench command, kernel-only probes (per-kernel times, strong-scaling shards,
+#   three-stream overlap, deep-path rates) and the simulator report.
+# The ncu --set full captures are separate (scripts/prof_configs.py + ncu_summary.py
+# --configs, run on the box: the report itself exceeds gpurun's 64 MiB return limit).
 set -u
-TAG=${1:-r01}
+TAG=${1:-r02}
 mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${TAG}_smi.txt
 python bench.py > gpurun_out/${TAG}_bench_c4_n1.json 2> gpurun_out/${TAG}_bench_c4.err
 for c in c1 c2 c3 c5 deep; do
   python bench.py --config $c > gpurun_out/${TAG}_bench_$c.json 2> gpurun_out/${TAG}_bench_$c.err
 done
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
-    python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_bench.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:esa_single -c 3 -o gpurun_out/${TAG}_full \
-    python scripts/prof_one.py > gpurun_out/${TAG}_ncu_full.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:esa_deep -s 2 -c 2 -o gpurun_out/${TAG}_deep \
-    python scripts/prof_deep.py > gpurun_out/${TAG}_ncu_deep.log 2>&1
+    python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-prune > gpurun_out/${TAG}_ncu_bench.log 2>&1
+python scripts/kern_time.py > gpurun_out/${TAG}_kern_time.txt 2>&1
+python scripts/shard_probe.py > gpurun_out/${TAG}_shard_probe.txt 2>&1
+python scripts/stream_probe.py > gpurun_out/${TAG}_stream_probe.txt 2>&1
+python scripts/deep_rate.py > gpurun_out/${TAG}_deep_rate.txt 2>&1
 python scripts/sim_report.py > gpurun_out/${TAG}_sim_report.json 2> gpurun_out/${TAG}_sim_report.err
-tail -c 600 gpurun_out/${TAG}_bench_c4_n1.json
+tail -c 400 gpurun_out/${TAG}_bench_c4_n1.json
