@@ -479,3 +479,48 @@ def test_run_queries_multistream_vs_oracle():
         assert r.leaves == (math.perm(nf, k) if k <= nf else 0)
         d = mp.decode(t, pats[ki], busy, sel, sens, r, raw=True)
         same(oracle(o, busy, shape, k, sel, sens, use_c=True), d, (shape, k, hex(busy), sel, sens))
+
+
+def _hub_text(n=32):
+    """Device 1 has a double NVLink to every other device; all other pairs
+    are PCIe: inc_F(hub) = 50 (n-1) while inc_F(other) = 50 + 12 (n-2), an
+    Eq. 3 spread far beyond the 16-bit scan's range (lin16_fits)."""
+    lines = [f"name hub{n}", f"devices {n}", "sockets " + ",".join(str(i) for i in range(1, n // 2 + 1)) + " "
+             + ",".join(str(i) for i in range(n // 2 + 1, n + 1))]
+    lines += [f"link 1 {b} nv2x2" for b in range(2, n + 1)]
+    return "\n".join(lines) + "\n"
+
+
+def test_lin16_range_fallback_and_refusal():
+    """Eq. 3 on a hub topology (spread 1140 > the s16 budget): with the hub
+    free the host keeps the 32-bit scan and decisions equal the oracle's; with
+    the hub busy the 16-bit scan is used and decisions still equal the
+    oracle's; a launch whose busy_hint claims the hub busy while the device
+    query has it free is refused by the kernel (record status -> decode
+    error), never mis-scored."""
+    text = _hub_text()
+    o, t = mo.parse_topology(text), mp.Topology(text=text)
+    rng = random.Random(5)
+    for trial in range(6):
+        # hub free with 24 others: spread 38 nf - 76 = 874 > 972 - 50 (k-2) -> 32-bit scan;
+        # hub busy (or few free): spread small -> 16-bit scan
+        hub_busy = trial % 2 == 1
+        free = rng.sample(range(1, 32), 24 if not hub_busy else 10) + ([] if hub_busy else [0])
+        busy = ((1 << 32) - 1) & ~sum(1 << d for d in free)
+        shape = rng.choice(["ring", "tree", "full"])
+        k = rng.randint(4, 5)
+        for raw in (True, False):
+            same(oracle(o, busy, shape, k, 1, False, use_c=True), gpu(t, busy, shape, k, 1, False, raw),
+                 ("hub", trial, hub_busy, shape, k, raw))
+    pat = mp.Pattern.make("full", 5)
+    busy_true = 0                                 # all 32 free: spread 1140
+    hint = 1                                      # claims the hub busy: spread 0 -> 16-bit scan chosen
+    q = md.query_tensor(busy_true)
+    rec = torch.zeros(4, dtype=torch.int64, device="cuda")
+    mp.launch_query(t, pat, 1, False, q.data_ptr(), rec.data_ptr(), raw=True, busy_hint=hint)
+    torch.cuda.synchronize()
+    r = md.records_from_tensor(rec)[0]
+    assert r.status != 0
+    with pytest.raises(mp.MapaError) as e:
+        mp.decode(t, pat, busy_true, 1, False, r, raw=True)
+    assert e.value.status == mp.E_INVALID_ARG
