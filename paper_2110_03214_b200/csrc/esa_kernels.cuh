@@ -80,6 +80,10 @@ struct SelT {
     // (lin16_fits in mapa_host.cpp)
     static constexpr bool lin16 = (SEL & 32) != 0 && lin && !multi;
     static constexpr bool half = pack16 || lin16;      // 16-bit table entries
+    // single-query additive kernels share the CTA's best score as the hit
+    // threshold (Shared::cthr; measured: Eq. 1 / 3 -5 % instructions, while the
+    // Eq. 2 kernel, already at the 128-register cap, lost 16 % with it)
+    static constexpr bool cta = lin && !multi;
     static constexpr bool useU = base == SEL_INSENS;   // Eq. 3 sums over every placed device
     static constexpr int wt = base == SEL_BASE ? 0 : 1;
     static constexpr int w0 = 38 * wt, w1 = 13 * wt, w2 = 8 * wt, w12 = 12 * wt;
@@ -117,7 +121,7 @@ struct Shared {
     uint32_t busy;
     int one;  // = 1 (Ctx::one)
     uint32_t topoS;  // trace kernel: the Topo-aware device set of the current ALLOC
-    uint32_t pad;
+    int cthr;        // single-query kernels: the CTA's best packed threshold (score + 1) * 32 so far
 };
 
 // Single-query kernels: Shared + one Eq. 2 table of 3 xs^2 ints + the
@@ -231,7 +235,7 @@ __device__ __noinline__ unsigned long long make_key(uint32_t S, unsigned long lo
 // Called when a leaf's score s >= the lane's best score.  An equal score wins
 // only through the device-set field (brev_W(S), kept in a register), or, for
 // the same set of a non-clique pattern, through the edge code.
-template <int W, int K>
+template <int W, int K, bool CTA = false>
 __device__ __forceinline__ void consider(const Ctx<W> &c, Best &bst, uint32_t S, unsigned long long fpack,
                                          uint32_t s) {
     const uint32_t sbn = __brev(S) >> (32 - W);
@@ -242,6 +246,7 @@ __device__ __forceinline__ void consider(const Ctx<W> &c, Best &bst, uint32_t S,
         bst.bs = s;
         bst.thr = ((int)s + 1) * 32;
         bst.sb = sbn;
+        if constexpr (CTA) atomicMax(&sh().cthr, bst.thr);  // the CTA's threshold (see inner3)
         if (bst.gb) {  // prune mode: publish the score to the grid
             if (bst.thr > bst.pthr) atomicMax(bst.gb, s + 1u);
             bst.pthr = max(bst.pthr, bst.thr);
@@ -507,7 +512,8 @@ __device__ __forceinline__ void inner(const Ctx<W> &c, const St<K> &st, uint32_t
     const uint32_t M = laneok ? (dep ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
     bst.cnt += (uint32_t)__popc(M & cand);
     const int off = SelT<SEL>::lin ? base : 0;
-    const int thr = bst.thr - off;
+    // a leaf below the CTA's best score cannot win anywhere (max is global)
+    const int thr = (SelT<SEL>::cta ? max(bst.thr, sh().cthr) : bst.thr) - off;
     const int raw = scan_dense<W, SEL>(c, cand, t2, base);
     if (laneok && raw >= thr) {  // rank >= 32 and its score >= the lane's best score
         const int best = raw + off;
@@ -516,7 +522,7 @@ __device__ __forceinline__ void inner(const Ctx<W> &c, const St<K> &st, uint32_t
             const uint32_t bestv = 31u - (uint32_t)(best & 31);
             unsigned long long fpack = pack_f<K>(st);
             fpack |= (unsigned long long)bestv << (8 * J);
-            consider<W, K>(c, bst, st.U | (1u << bestv) | (1u << b), fpack, s);
+            consider<W, K, SelT<SEL>::cta>(c, bst, st.U | (1u << bestv) | (1u << b), fpack, s);
         }
     }
 }
@@ -572,6 +578,12 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
     const uint32_t cand2b = c.F & ~st.U & alw<SEL>(st.al[J2]);
     const unsigned long long fbase = pack_f<K>(st);
     const bool dep = d32 || d31 || d21 || SelT<SEL>::prune;  // prune mode counts the scans it runs
+    // Hit threshold: a leaf matters only if its score reaches both the lane's
+    // best and the best any lane of this CTA has found (a lower score loses
+    // to that key in the final max; ties still reach the key builder for the
+    // tie-break).  Sharing the CTA's best keeps most lanes out of the
+    // divergent key-building path early in the search.
+    int thrE = SelT<SEL>::cta ? max(bst.thr, sh().cthr) : bst.thr;
     if constexpr (SelT<SEL>::prune) {
         const unsigned g = *reinterpret_cast<volatile unsigned *>(bst.gb);
         bst.pthr = max(bst.pthr, (int)(g * 32u));
@@ -627,7 +639,7 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
                 const uint32_t bestv = 31u - (uint32_t)(raw & 31);
                 const unsigned long long fpack =
                     fbase | ((unsigned long long)v3 << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
-                consider<W, K>(c, bst, st.U | (1u << v3) | (1u << bestv) | (1u << b), fpack,
+                consider<W, K, SelT<SEL>::cta>(c, bst, st.U | (1u << v3) | (1u << bestv) | (1u << b), fpack,
                                (uint32_t)(raw >> 5) - 1u);
             }
         }
@@ -670,25 +682,26 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
         __syncwarp(c.gmask);
         const int rawA = runA ? tab_scan<W, SEL>(c, tabA, baseA) : kNeg;
         const int rawB = runB ? tab_scan<W, SEL>(c, tabB, baseB) : kNeg;
-        const bool hitA = okA && rawA >= bst.thr - offA;
-        const bool hitB = okB && rawB >= bst.thr - offB;
-        if (hitA || hitB) {  // a rank >= 32 whose score >= the lane's best score
+        const bool hitA = okA && rawA >= thrE - offA;
+        const bool hitB = okB && rawB >= thrE - offB;
+        if (hitA || hitB) {  // a rank >= 32 whose score >= the lane's / CTA's best score
             if (hitA) {
                 const int best = rawA + offA;
                 const uint32_t bestv = 31u - (uint32_t)(best & 31);
                 const unsigned long long fpack =
                     fbase | ((unsigned long long)vA << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
-                consider<W, K>(c, bst, st.U | (1u << vA) | (1u << bestv) | (1u << b), fpack,
+                consider<W, K, SelT<SEL>::cta>(c, bst, st.U | (1u << vA) | (1u << bestv) | (1u << b), fpack,
                                (uint32_t)(best >> 5) - 1u);
             }
-            if (hitB && rawB >= bst.thr - offB) {
+            if (hitB && rawB >= max(thrE, bst.thr) - offB) {
                 const int best = rawB + offB;
                 const uint32_t bestv = 31u - (uint32_t)(best & 31);
                 const unsigned long long fpack =
                     fbase | ((unsigned long long)vB << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
-                consider<W, K>(c, bst, st.U | (1u << vB) | (1u << bestv) | (1u << b), fpack,
+                consider<W, K, SelT<SEL>::cta>(c, bst, st.U | (1u << vB) | (1u << bestv) | (1u << b), fpack,
                                (uint32_t)(best >> 5) - 1u);
             }
+            thrE = max(thrE, bst.thr);
         }
     }
 }
@@ -938,7 +951,10 @@ __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int 
     const DevTopo &topo = tb.topo;
     const int tid = threadIdx.x;
     if (tid < kMaxN) s.cm[tid] = make_uint4(topo.cm[tid][0], topo.cm[tid][1], topo.cm[tid][2], topo.cm[tid][3]);
-    if (tid == 0) s.one = 1;
+    if (tid == 0) {
+        s.one = 1;
+        s.cthr = 32;
+    }
     if (tid <= kMaxN) s.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
     static_assert(offsetof(Shared, ts0d) == offsetof(Shared, tw) + 9 * kNN * sizeof(int), "pair tables contiguous");
     if (tb.pre && only_sc >= 0) {
