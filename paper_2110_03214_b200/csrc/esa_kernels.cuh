@@ -81,8 +81,10 @@ struct SelT {
     static constexpr bool lin16 = (SEL & 32) != 0 && lin && !multi;
     static constexpr bool half = pack16 || lin16;      // 16-bit table entries
     // single-query additive kernels share the CTA's best score as the hit
-    // threshold (Shared::cthr; measured: Eq. 1 / 3 -5 % instructions, while the
-    // Eq. 2 kernel, already at the 128-register cap, lost 16 % with it)
+    // threshold (Shared::cthr, folded into the lane's Best::thr at each inner3
+    // call; measured: Eq. 1 / 3 -6 % instructions; the Eq. 2 kernel, at the
+    // 128-register cap, compiled to +15 % instructions with it, so it keeps
+    // the lane's own threshold)
     static constexpr bool cta = lin && !multi;
     static constexpr bool useU = base == SEL_INSENS;   // Eq. 3 sums over every placed device
     static constexpr int wt = base == SEL_BASE ? 0 : 1;
@@ -513,7 +515,8 @@ __device__ __forceinline__ void inner(const Ctx<W> &c, const St<K> &st, uint32_t
     bst.cnt += (uint32_t)__popc(M & cand);
     const int off = SelT<SEL>::lin ? base : 0;
     // a leaf below the CTA's best score cannot win anywhere (max is global)
-    const int thr = (SelT<SEL>::cta ? max(bst.thr, sh().cthr) : bst.thr) - off;
+    if constexpr (SelT<SEL>::cta) bst.thr = max(bst.thr, sh().cthr);
+    const int thr = bst.thr - off;
     const int raw = scan_dense<W, SEL>(c, cand, t2, base);
     if (laneok && raw >= thr) {  // rank >= 32 and its score >= the lane's best score
         const int best = raw + off;
@@ -583,7 +586,9 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
     // to that key in the final max; ties still reach the key builder for the
     // tie-break).  Sharing the CTA's best keeps most lanes out of the
     // divergent key-building path early in the search.
-    int thrE = SelT<SEL>::cta ? max(bst.thr, sh().cthr) : bst.thr;
+    // (a lower score loses to the CTA's best key in the final max, so the
+    // lane's threshold may be raised to it; ties still reach the key builder)
+    if constexpr (SelT<SEL>::cta) bst.thr = max(bst.thr, sh().cthr);
     if constexpr (SelT<SEL>::prune) {
         const unsigned g = *reinterpret_cast<volatile unsigned *>(bst.gb);
         bst.pthr = max(bst.pthr, (int)(g * 32u));
@@ -682,8 +687,8 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
         __syncwarp(c.gmask);
         const int rawA = runA ? tab_scan<W, SEL>(c, tabA, baseA) : kNeg;
         const int rawB = runB ? tab_scan<W, SEL>(c, tabB, baseB) : kNeg;
-        const bool hitA = okA && rawA >= thrE - offA;
-        const bool hitB = okB && rawB >= thrE - offB;
+        const bool hitA = okA && rawA >= bst.thr - offA;
+        const bool hitB = okB && rawB >= bst.thr - offB;
         if (hitA || hitB) {  // a rank >= 32 whose score >= the lane's / CTA's best score
             if (hitA) {
                 const int best = rawA + offA;
@@ -693,7 +698,7 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
                 consider<W, K, SelT<SEL>::cta>(c, bst, st.U | (1u << vA) | (1u << bestv) | (1u << b), fpack,
                                (uint32_t)(best >> 5) - 1u);
             }
-            if (hitB && rawB >= max(thrE, bst.thr) - offB) {
+            if (hitB && rawB >= bst.thr - offB) {
                 const int best = rawB + offB;
                 const uint32_t bestv = 31u - (uint32_t)(best & 31);
                 const unsigned long long fpack =
@@ -701,7 +706,6 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
                 consider<W, K, SelT<SEL>::cta>(c, bst, st.U | (1u << vB) | (1u << bestv) | (1u << b), fpack,
                                (uint32_t)(best >> 5) - 1u);
             }
-            thrE = max(thrE, bst.thr);
         }
     }
 }
