@@ -380,21 +380,25 @@ def main():
     sampler.stop()  # the nvidia-smi poller competes for host cores; clocks are sampled above
     # ---- e2e through the public API (host buffers, copies inside the region)
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 50))
-    for _ in range(args.warmup):  # untimed: first call allocates the pinned/device staging buffers
-        for sel, sens, _name in SELECTORS:
-            if world == 1:
-                mp.allocate(topo, pat, sel, sens, raw=True)
-            else:
+    many = [(pat, sel, sens) for sel, sens, _name in SELECTORS]
+    for _ in range(args.warmup):  # untimed: first call allocates the staging buffers and captures the graph
+        if world == 1:
+            mp.allocate_many(topo, many, raw=True)
+        else:
+            for sel, sens, _name in SELECTORS:
                 md.allocate_sharded(topo, pat, sel, sens, busy, raw=True)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     w0 = time.perf_counter()
     for _ in range(e2e_steps):
-        for sel, sens, _name in SELECTORS:
-            if world == 1:
-                d = mp.allocate(topo, pat, sel, sens, raw=True)          # H2D 16 B, kernel, D2H 32 B, decode
-            else:
+        if world == 1:
+            # mapa_allocate_many: one H2D copy of the three queries (+ zero records), the three
+            # launches as parallel graph branches, one D2H copy of the records, host decode
+            ds = mp.allocate_many(topo, many, raw=True)
+            assert ds[0]["raw"] == RAW_PER_QUERY
+        else:
+            for sel, sens, _name in SELECTORS:
                 d = md.allocate_sharded(topo, pat, sel, sens, busy, raw=True)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - w0
@@ -457,10 +461,12 @@ def main():
                                  f"same peak, > 1 because the enumeration tree shares prefix work"},
             "cpu_baseline": cpu,
             "e2e": {"value": emb_step * e2e_steps / e2e_s, "unit": "embeddings/s",
-                    # per allocation: one 128-B H2D staging copy (16-B query + a zero record image)
-                    # and the 32-B record back (N>1: the query tensor + the all_gather'd records)
+                    # N=1: mapa_allocate_many -- one H2D staging copy of 128 B per query (16-B query +
+                    # a zero record image) and one D2H copy of the 64-B record slots; N>1: per
+                    # allocation the query tensor + the all_gather'd records
+                    "api": "mapa_allocate_many (3 queries per call)" if world == 1 else "dist.allocate_sharded",
                     "h2d_bytes_per_step": (128 if world == 1 else 16) * len(SELECTORS),
-                    "d2h_bytes_per_step": 32 * len(SELECTORS) * world,
+                    "d2h_bytes_per_step": (64 if world == 1 else 32 * world) * len(SELECTORS),
                     "allocations_per_s": len(SELECTORS) * e2e_steps / e2e_s},
             "gpu_launches": len(SELECTORS) * args.steps,
             "clocks": clk,

@@ -285,6 +285,19 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
                           int32_t bw_sensitive, uint32_t flags, void *cuda_stream,
                           mapa_decision *out);
 
+/* nq (1..32) independent allocations on the topology's current busy mask,
+ * end to end from host buffers in ONE call: one H2D copy stages every query
+ * (and zeroes every device record), the nq enumerate-score-argmax launches
+ * run as parallel branches of one cached CUDA graph (their prologues and
+ * tails overlap), one D2H copy brings the records back, and each is decoded
+ * on the host exactly as mapa_allocate would (pats[i], selector[i],
+ * sensitive[i]; narrow or deep path per query).  Never commits
+ * (MAPA_F_COMMIT: INVALID_ARG): the queries see the same state.  out[nq]; a
+ * query without capacity gets status MAPA_NO_CAPACITY in its decision.
+ * Blocks until the stream reaches the copy.  Errors as mapa_allocate. */
+mapa_status mapa_allocate_many(mapa_topology *t, const mapa_pattern *const *pats, int32_t nq, const int32_t *selector,
+                               const int32_t *sensitive, uint32_t flags, void *cuda_stream, mapa_decision *out);
+
 /* Device-resident launch of one query's shard: zeroes d_record (unless
  * MAPA_F_ZEROED: the caller zeroed it on cuda_stream) and
  * enumerates the work items i with i % world == rank of the query whose busy

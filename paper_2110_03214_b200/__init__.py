@@ -112,6 +112,8 @@ _SIGS = {
     "mapa_effbw_rank_table": (_S, [ctypes.c_int32, ctypes.POINTER(ctypes.c_uint16)]),
     "mapa_allocate": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_uint32, _vp,
                            ctypes.POINTER(Decision)]),
+    "mapa_allocate_many": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32, ctypes.POINTER(ctypes.c_int32),
+                                ctypes.POINTER(ctypes.c_int32), ctypes.c_uint32, _vp, ctypes.POINTER(Decision)]),
     "mapa_launch_query": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.c_uint32,
                                ctypes.c_int32, ctypes.c_int32, ctypes.c_uint64, _vp]),
     "mapa_reduce_records": (_S, [ctypes.POINTER(Record), ctypes.c_int32, ctypes.POINTER(Record)]),
@@ -359,6 +361,20 @@ def allocate(topo: Topology, pat: Pattern, selector: int, sensitive: bool = Fals
     _check(_lib.mapa_allocate(topo.handle, pat.handle, selector, int(bool(sensitive)), flags,
                               _stream_ptr(stream), ctypes.byref(d)), allow_no_capacity=True)
     return decision_dict(d)
+
+
+def allocate_many(topo: Topology, queries, raw: bool = False, stream=None, prune: bool = False,
+                  deep: bool = False) -> list[dict]:
+    """mapa_allocate_many: independent allocations [(pattern, selector,
+    sensitive)] on the topology's current state in one call (one graph: one
+    H2D copy, parallel launches, one D2H copy, host decode); never commits."""
+    n = len(queries)
+    arr = (_vp * n)(*[q[0].handle for q in queries])
+    sel = (ctypes.c_int32 * n)(*[q[1] for q in queries])
+    sen = (ctypes.c_int32 * n)(*[int(bool(q[2])) for q in queries])
+    out = (Decision * n)()
+    _check(_lib.mapa_allocate_many(topo.handle, arr, n, sel, sen, _flags(raw, prune, deep), _stream_ptr(stream), out))
+    return [decision_dict(out[i]) for i in range(n)]
 
 
 def launch_query(topo: Topology, pat: Pattern, selector: int, sensitive: bool, d_query_ptr: int,

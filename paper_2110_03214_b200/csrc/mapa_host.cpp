@@ -33,6 +33,13 @@ struct GraphEntry {
     uint64_t tick;
 };
 
+// mapa_allocate_many: one cached graph per (patterns, selectors, flags, |F|, device)
+struct ManyEntry {
+    std::vector<uint64_t> key;
+    cudaGraphExec_t exec;
+    uint64_t tick;
+};
+
 struct mapa_topology {
     std::string name;
     int n = 0;
@@ -58,6 +65,9 @@ struct mapa_topology {
     struct PairTab { int xs, dev; void *d; };
     std::vector<PairTab> pair_tabs;  // device images of the narrow kernels' pair tables, per (xs, device)
     std::vector<GraphEntry> graphs;
+    std::vector<ManyEntry> many_graphs;
+    void *d_many = nullptr, *h_many = nullptr;  // mapa_allocate_many staging: 128 B per query
+    int many_cap = 0;
     uint64_t tick = 0;
 };
 
@@ -1099,6 +1109,9 @@ mapa_status mapa_load_topology(const char *spec, int32_t is_text, mapa_topology 
 void mapa_free_topology(mapa_topology *t) {
     if (!t) return;
     for (auto &g : t->graphs) cudaGraphExecDestroy(g.exec);
+    for (auto &g : t->many_graphs) cudaGraphExecDestroy(g.exec);
+    if (t->d_many) cudaFree(t->d_many);
+    if (t->h_many) cudaFreeHost(t->h_many);
     for (auto &pt : t->pair_tabs) cudaFree(pt.d);
     for (auto s2 : t->side) cudaStreamDestroy(s2);
     if (t->cap) cudaStreamDestroy(t->cap);
@@ -1730,6 +1743,143 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
     if (s == MAPA_OK && (flags & MAPA_F_COMMIT)) t->busy |= d.device_mask;
     *out = d;
     return s;
+}
+
+mapa_status mapa_allocate_many(mapa_topology *t, const mapa_pattern *const *pats, int32_t nq, const int32_t *selector,
+                               const int32_t *sensitive, uint32_t flags, void *stream, mapa_decision *out) {
+    if (!t || nq < 1 || nq > 32 || !pats || !selector || !sensitive || !out)
+        return fail(MAPA_E_INVALID_ARG, "bad allocate_many arguments (1 <= nq <= 32)");
+    if (flags & MAPA_F_COMMIT) return fail(MAPA_E_INVALID_ARG, "allocate_many never commits (independent queries)");
+    for (int i = 0; i < nq; ++i)
+        if (!pats[i] || selector[i] < 0 || selector[i] > 2) return fail(MAPA_E_INVALID_ARG, "bad query " + std::to_string(i));
+    mapa_status sb = bind_device(t);
+    if (sb != MAPA_OK) return sb;
+    const uint64_t F = ~t->busy & nmask_of(t->n);
+    const int nf = __builtin_popcountll(F);
+    int err;
+    if (nq > t->many_cap) {
+        if (t->d_many) cudaFree(t->d_many);
+        if (t->h_many) cudaFreeHost(t->h_many);
+        t->d_many = t->h_many = nullptr;
+        t->many_cap = 0;
+        for (auto &g : t->many_graphs) cudaGraphExecDestroy(g.exec);
+        t->many_graphs.clear();  // they hold the old staging pointers
+        if ((err = (int)cudaMalloc(&t->d_many, 128 * (size_t)32)) || (err = (int)cudaMallocHost(&t->h_many, 256 * (size_t)32)))
+            return cuda_fail(err, "cudaMalloc (allocate_many)");
+        std::memset(t->h_many, 0, 256 * 32);
+        t->many_cap = 32;
+    }
+    // staging: host [128 i, 128 i + 16) query i, [128 i + 64, 128 i + 128) a zero
+    // record; ONE H2D copy of nq x 128 B stages every query and zeroes every
+    // device record; the records come back in one D2H copy into [128 nq, ...)
+    std::vector<char> deep(nq);
+    for (int i = 0; i < nq; ++i) {
+        deep[i] = (flags & MAPA_F_DEEP) || !key_fits(t, pats[i]);
+        char *h = (char *)t->h_many + 128 * i;
+        std::memset(h, 0, 128);
+        if (deep[i]) {
+            mapa_query64 *q = (mapa_query64 *)h;
+            q->busy = t->busy;
+            q->selector = selector[i];
+            q->sensitive = sensitive[i];
+        } else {
+            mapa_query *q = (mapa_query *)h;
+            q->busy = (uint32_t)t->busy;
+            q->selector = selector[i];
+            q->sensitive = sensitive[i];
+        }
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::vector<uint64_t> key;
+    key.push_back((uint64_t)nq | ((uint64_t)flags << 8) | ((uint64_t)nf << 40) | ((uint64_t)dev << 48));
+    for (int i = 0; i < nq; ++i) {
+        key.push_back(pats[i]->uid);
+        key.push_back((uint64_t)selector[i] | ((uint64_t)(sensitive[i] != 0) << 2) | ((uint64_t)deep[i] << 3));
+    }
+    cudaGraphExec_t exec = nullptr;
+    for (auto &g : t->many_graphs)
+        if (g.key == key) { exec = g.exec; g.tick = ++t->tick; break; }
+    if (!exec) {
+        // warm every cache that allocates or copies synchronously, outside the capture
+        for (int i = 0; i < nq; ++i) {
+            if (!deep[i]) pair_tables(t, pick_xs(pats[i]->m), stream);
+            if (deep[i] && sel_code(selector[i], sensitive[i]) == SEL_SENS) {
+                const uint16_t *d_lut = nullptr;
+                mapa_status su = upload_lut(pats[i], &d_lut);
+                if (su != MAPA_OK) return su;
+            }
+        }
+        if (!t->cap && (err = (int)cudaStreamCreateWithFlags(&t->cap, cudaStreamNonBlocking)))
+            return cuda_fail(err, "cudaStreamCreate");
+        while ((int)t->side.size() < nq) {
+            cudaStream_t s2;
+            if ((err = (int)cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking))) return cuda_fail(err, "cudaStreamCreate");
+            t->side.push_back(s2);
+        }
+        cudaEvent_t ev[2];
+        if ((err = (int)cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming))) return cuda_fail(err, "cudaEventCreate");
+        if ((err = (int)cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming))) {
+            cudaEventDestroy(ev[0]);
+            return cuda_fail(err, "cudaEventCreate");
+        }
+        if ((err = (int)cudaStreamBeginCapture(t->cap, cudaStreamCaptureModeRelaxed))) {
+            cudaEventDestroy(ev[0]);
+            cudaEventDestroy(ev[1]);
+            return cuda_fail(err, "capture");
+        }
+        // one H2D copy, then the nq launches as parallel branches (their
+        // prologues and tails overlap), then one D2H copy
+        mapa_status sc = MAPA_OK;
+        if ((err = (int)cudaMemcpyAsync(t->d_many, t->h_many, 128 * (size_t)nq, cudaMemcpyHostToDevice, t->cap)))
+            sc = cuda_fail(err, "H2D queries");
+        cudaEventRecord(ev[0], t->cap);
+        for (int i = 0; i < nq && sc == MAPA_OK; ++i) {
+            cudaStream_t s2 = t->side[i];
+            cudaStreamWaitEvent(s2, ev[0], 0);
+            char *dq = (char *)t->d_many + 128 * i, *dr = dq + 64;
+            sc = deep[i] ? launch_query_wide_impl(t, pats[i], selector[i], sensitive[i], (const mapa_query64 *)dq,
+                                                  (mapa_wide_record *)dr, flags, 0, 1, t->busy, (void *)s2, false)
+                         : launch_query_impl(t, pats[i], selector[i], sensitive[i], (const mapa_query *)dq,
+                                             (mapa_record *)dr, flags, 0, 1, t->busy, (void *)s2, false);
+            cudaEventRecord(ev[1], s2);
+            cudaStreamWaitEvent(t->cap, ev[1], 0);
+        }
+        // the nq records (64 B each, pitch 128 on the device) back in one 2-D copy
+        if (sc == MAPA_OK && (err = (int)cudaMemcpy2DAsync((char *)t->h_many + 128 * 32, 64, (char *)t->d_many + 64, 128,
+                                                           64, (size_t)nq, cudaMemcpyDeviceToHost, t->cap)))
+            sc = cuda_fail(err, "D2H records");
+        cudaGraph_t graph = nullptr;
+        const int ec = (int)cudaStreamEndCapture(t->cap, &graph);
+        cudaEventDestroy(ev[0]);
+        cudaEventDestroy(ev[1]);
+        if (sc != MAPA_OK) { if (graph) cudaGraphDestroy(graph); return sc; }
+        if (ec) return cuda_fail(ec, "cudaStreamEndCapture");
+        err = (int)cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (err) return cuda_fail(err, "cudaGraphInstantiate");
+        if (t->many_graphs.size() >= 16) {
+            auto lru = std::min_element(t->many_graphs.begin(), t->many_graphs.end(),
+                                        [](const ManyEntry &a2, const ManyEntry &b2) { return a2.tick < b2.tick; });
+            cudaGraphExecDestroy(lru->exec);
+            t->many_graphs.erase(lru);
+        }
+        t->many_graphs.push_back({key, exec, ++t->tick});
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((err = (int)cudaGraphLaunch(exec, st))) return cuda_fail(err, "cudaGraphLaunch");
+    if ((err = (int)cudaStreamSynchronize(st))) return cuda_fail(err, "cudaStreamSynchronize");
+    std::vector<mapa_decision> dec(nq);
+    for (int i = 0; i < nq; ++i) {
+        const char *hr = (const char *)t->h_many + 128 * 32 + 64 * i;
+        mapa_status s = deep[i] ? decode_wide(t, pats[i], t->busy, selector[i], sensitive[i], flags,
+                                              (const mapa_wide_record *)hr, &dec[i])
+                                : decode_record(t, pats[i], t->busy, selector[i], sensitive[i], flags,
+                                                (const mapa_record *)hr, &dec[i]);
+        if (s < 0) return s;
+    }
+    std::memcpy(out, dec.data(), sizeof(mapa_decision) * (size_t)nq);
+    return MAPA_OK;
 }
 
 mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *const *pats, int32_t npats,

@@ -524,3 +524,29 @@ def test_lin16_range_fallback_and_refusal():
     with pytest.raises(mp.MapaError) as e:
         mp.decode(t, pat, busy_true, 1, False, r, raw=True)
     assert e.value.status == mp.E_INVALID_ARG
+
+
+def test_allocate_many_equals_single_allocations_and_oracle():
+    """mapa_allocate_many (one graph: one H2D copy, parallel launches, one D2H
+    copy, host decode): every decision equals mapa_allocate's for the same
+    query and the oracle's; narrow and deep queries and a no-capacity query in
+    one call; the cached graph is reused when only the busy mask changes."""
+    o, t = mo.builtin("cubemesh16"), mp.Topology("cubemesh16")
+    qs = [("ring", 4, 0, False), ("tree", 5, 1, True), ("full", 4, 1, False), ("ring", 9, 0, False),
+          ("tree", 13, 1, True)]
+    pats = {(s, k): mp.Pattern.make(s, k) for s, k, _, _ in qs}
+    for busy in (0b1010000000000001, 0b0000000100100110, 0b1111111100000000):
+        t.set_busy(busy)
+        for raw in (True, False):
+            got = mp.allocate_many(t, [(pats[(s, k)], sel, sens) for s, k, sel, sens in qs], raw=raw)
+            for (s, k, sel, sens), g in zip(qs, got):
+                one = mp.allocate(t, pats[(s, k)], sel, sens, raw=raw)
+                assert g["status"] == one["status"]
+                if g["status"] == "ok":
+                    for f in FIELDS + ("leaves", "key", "pred_effbw"):
+                        assert g[f] == one[f], (s, k, hex(busy), raw, f)
+                if k <= 5:
+                    same(oracle(o, busy, s, k, sel, sens, use_c=True), g, (s, k, hex(busy), raw))
+    assert t.busy == 0b1111111100000000  # never commits
+    with pytest.raises(mp.MapaError):
+        mp._check(mp._lib.mapa_allocate_many(t.handle, None, 0, None, None, 0, None, None))
