@@ -8,8 +8,10 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libmapa.so")
-# one translation unit per topology width W, compiled in parallel
-SOURCES = [os.path.join(CSRC, f) for f in ("esa_w32.cu", "esa_w16.cu", "esa_w8.cu", "esa_deep.cu", "esa.cu", "mapa_host.cpp")]
+# translation units compiled in parallel
+# (the per-width kernels in five parts each: see csrc/esa_w.cuh)
+SOURCES = [os.path.join(CSRC, f"esa_w{w}_p{p}.cu") for w in (32, 16, 8) for p in range(5)] + \
+    [os.path.join(CSRC, f) for f in ("esa_deep.cu", "esa.cu", "mapa_host.cpp")]
 HEADERS = [os.path.join(CSRC, f) for f in ("internal.h", "esa_kernels.cuh", "esa_w.cuh")] + \
     [os.path.join(os.path.dirname(HERE), "include", "mapa.h")]
 
@@ -41,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 return None
             return subprocess.run([NVCC] + FLAGS + ["-c", "-o", objs[i], SOURCES[i]], capture_output=True, text=True)
 
-        with ThreadPoolExecutor(len(SOURCES)) as ex:
+        with ThreadPoolExecutor(min(len(SOURCES), max(2, os.cpu_count() or 2))) as ex:
             results = [r for r in ex.map(compile_one, range(len(SOURCES))) if r is not None]
         log = "".join(r.stderr for r in results)
         for r in results:

@@ -1,6 +1,6 @@
 // esa.cu — host dispatch of the Enumerate-Score-Argmax kernels by topology
 // width W (8 / 16 / 32); the kernels themselves are in esa_kernels.cuh and are
-// instantiated per W by esa_w8.cu, esa_w16.cu, esa_w32.cu.
+// instantiated per W and part by esa_w{8,16,32}_p{0..4}.cu (see esa_w.cuh).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -9,10 +9,12 @@
 
 namespace mapa {
 
+#define MAPA_DECL_P(W, P)                                                                                       \
+    int launch_single_w##W##_p##P(const SingleTables &, int, const mapa_query *, mapa_record *, int, int, int, int, \
+                                  int, void *);                                                                     \
+    int occ_single_w##W##_p##P(int, int, int);
 #define MAPA_DECL_W(W)                                                                                       \
-    int launch_single_w##W(const SingleTables &, int, const mapa_query *, mapa_record *, int, int, int, int, \
-                           int, void *);                                                                     \
-    int occ_single_w##W(int, int, int);                                                                      \
+    MAPA_DECL_P(W, 0) MAPA_DECL_P(W, 1) MAPA_DECL_P(W, 2) MAPA_DECL_P(W, 3)                                   \
     int launch_batch_w##W(const MultiTables &, int, int64_t, const mapa_query *, mapa_record *, uint32_t *,  \
                           const uint32_t *, int, void *);                                                    \
     int occ_batch_w##W(int, int);                                                                            \
@@ -23,12 +25,21 @@ MAPA_DECL_W(8)
 MAPA_DECL_W(16)
 MAPA_DECL_W(32)
 
+// single-query kernels live in per-selector parts (esa_w*_p<sc & 3>.cu)
+#define MAPA_SINGLE_PARTS(W, FN, ...)                      \
+    switch (sc & 3) {                                      \
+        case 0: return FN##_w##W##_p0(__VA_ARGS__);        \
+        case 1: return FN##_w##W##_p1(__VA_ARGS__);        \
+        case 2: return FN##_w##W##_p2(__VA_ARGS__);        \
+        default: return FN##_w##W##_p3(__VA_ARGS__);       \
+    }
+
 int launch_single(const SingleTables &tb, int sc, const mapa_query *d_query, mapa_record *d_record, int depth,
                   int rank, int world, int stripe, int grid, void *stream) {
     switch (tb.topo.width) {
-        case 8: return launch_single_w8(tb, sc, d_query, d_record, depth, rank, world, stripe, grid, stream);
-        case 16: return launch_single_w16(tb, sc, d_query, d_record, depth, rank, world, stripe, grid, stream);
-        case 32: return launch_single_w32(tb, sc, d_query, d_record, depth, rank, world, stripe, grid, stream);
+        case 8: MAPA_SINGLE_PARTS(8, launch_single, tb, sc, d_query, d_record, depth, rank, world, stripe, grid, stream)
+        case 16: MAPA_SINGLE_PARTS(16, launch_single, tb, sc, d_query, d_record, depth, rank, world, stripe, grid, stream)
+        case 32: MAPA_SINGLE_PARTS(32, launch_single, tb, sc, d_query, d_record, depth, rank, world, stripe, grid, stream)
     }
     return (int)cudaErrorInvalidValue;
 }
@@ -128,6 +139,12 @@ int device_sm_count() {
     return n;
 }
 
+static int occ_single_parts(int width, int k, int sc, int smem) {
+    if (width == 8) { MAPA_SINGLE_PARTS(8, occ_single, k, sc, smem) }
+    if (width == 16) { MAPA_SINGLE_PARTS(16, occ_single, k, sc, smem) }
+    MAPA_SINGLE_PARTS(32, occ_single, k, sc, smem)
+}
+
 int max_blocks_per_sm_single(int width, int k, int sc, int xs) {
     // cached: (width, k, selector code with canon bit, xs) -> blocks per SM
     static int cache[3][9][56][48] = {};
@@ -136,9 +153,7 @@ int max_blocks_per_sm_single(int width, int k, int sc, int xs) {
     if (slot) return slot;
     const int smem = smem_shared_w32() + 4 * xs * xs * (int)sizeof(int);
     int r;
-    if (width == 8) r = occ_single_w8(k, sc, smem);
-    else if (width == 16) r = occ_single_w16(k, sc, smem);
-    else r = occ_single_w32(k, sc, smem);
+    r = occ_single_parts(width, k, sc, smem);
     slot = r;
     return r;
 }

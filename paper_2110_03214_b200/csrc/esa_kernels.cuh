@@ -124,6 +124,7 @@ struct Shared {
     int one;  // = 1 (Ctx::one)
     uint32_t topoS;  // trace kernel: the Topo-aware device set of the current ALLOC
     int cthr;        // single-query kernels: the CTA's best packed threshold (score + 1) * 32 so far
+    unsigned long long ckey;  // single-query Eq. 2 kernels: the CTA's best key so far (sens_hit)
 };
 
 // Single-query kernels: Shared + one Eq. 2 table of 3 xs^2 ints + the
@@ -133,6 +134,27 @@ constexpr int kSmemSingleMax = (int)sizeof(Shared) + 4 * 40 * 40 * (int)sizeof(i
 extern __shared__ __align__(16) unsigned char g_smem[];
 __device__ __forceinline__ Shared &sh() { return *reinterpret_cast<Shared *>(g_smem); }
 __device__ __forceinline__ int *sh_lut() { return reinterpret_cast<int *>(g_smem + sizeof(Shared)); }
+
+// Single-query Eq. 2 kernels (SelT::pack16) keep their one Eq. 2 table (and
+// the prune-mode bound table) in STATIC shared memory: the first static
+// variable of a kernel sits at the bottom of the CTA's shared window, shared
+// address kLut1Addr, so the hot gathers address it as LDS [R + kLut1Addr]
+// with the byte offset alone in R -- no per-leaf add of the window base, which
+// the compiler otherwise keeps in a vector register under the 128-register
+// cap (33 extra IMADs per scan, measured).  esa_single checks the address at
+// run time and refuses the query (status 2) if it ever differs.
+constexpr int kLut1Ints = 4 * 40 * 40;
+constexpr uint32_t kLut1Addr = 0x400;
+__shared__ __align__(16) int g_lut1[kLut1Ints];
+
+// gather at byte offset `off` of g_lut1 (volatile: never merged with another
+// load, so no gathered value is kept live across the hit branch)
+__device__ __forceinline__ int lds_lut1(uint32_t off) {
+    int v;
+    asm volatile("ld.shared.b32 %0, [%1+1024];" : "=r"(v) : "r"(off));
+    return v;
+}
+static_assert(kLut1Addr == 1024, "lds_lut1 immediate");
 
 template <int W>
 struct Ctx {
@@ -191,6 +213,15 @@ __device__ __forceinline__ int lds_off(const int *base, int byte_off) {
     return *reinterpret_cast<const int *>(reinterpret_cast<const char *>(base) + byte_off);
 }
 
+// a * b + c that the compiler may not re-associate (the pack16 low-half
+// offset: re-associated, the shared-window base costs one add per leaf
+// instead of riding in the uniform operand of LDS [R+UR+imm])
+__device__ __forceinline__ int mad_lo(int a, int b, int c) {
+    int r;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t nth_set(uint32_t m, uint32_t n) {
     // position of the n-th (0-based) set bit of m (popc binary search)
     uint32_t pos = 0, c;
@@ -237,7 +268,7 @@ __device__ __noinline__ unsigned long long make_key(uint32_t S, unsigned long lo
 // Called when a leaf's score s >= the lane's best score.  An equal score wins
 // only through the device-set field (brev_W(S), kept in a register), or, for
 // the same set of a non-clique pattern, through the edge code.
-template <int W, int K, bool CTA = false>
+template <int W, int K, bool CTA = false, bool CKEY = false>
 __device__ __forceinline__ void consider(const Ctx<W> &c, Best &bst, uint32_t S, unsigned long long fpack,
                                          uint32_t s) {
     const uint32_t sbn = __brev(S) >> (32 - W);
@@ -249,6 +280,7 @@ __device__ __forceinline__ void consider(const Ctx<W> &c, Best &bst, uint32_t S,
         bst.thr = ((int)s + 1) * 32;
         bst.sb = sbn;
         if constexpr (CTA) atomicMax(&sh().cthr, bst.thr);  // the CTA's threshold (see inner3)
+        if constexpr (CKEY) atomicMax(&sh().ckey, key);     // the CTA's best key (see sens_hit)
         if (bst.gb) {  // prune mode: publish the score to the grid
             if (bst.thr > bst.pthr) atomicMax(bst.gb, s + 1u);
             bst.pthr = max(bst.pthr, bst.thr);
@@ -358,16 +390,41 @@ __device__ __forceinline__ int tab_entry(const Ctx<W> &c, uint32_t cand, int t2)
     else return 4 * (mine ? t2 : c.xs * c.xs);  // byte offsets into the Eq. 2 table
 }
 
-template <int W, int SEL>
+template <int W, int SEL, bool TIE = true>
 __device__ __forceinline__ int tab_scan(const Ctx<W> &c, const int *tab, int base) {
-    if constexpr (SelT<SEL>::pack16) {
+    if constexpr (SelT<SEL>::pack16 && !TIE) {
+        // Hot scan of the single-query Eq. 2 kernels: the max LUT entry
+        // (rank + 1) * 32 only, no tie-break -- per 2 leaves one IADD3, one SHF,
+        // one IMAD (offset split), two gathers and one 3-input max.  The lane
+        // with a hit (rank >= its best score, rare) rescans with TIE = true to
+        // find the smallest v of that rank (sens_hit).  0 when no leaf is valid.
+        const uint4 *t8 = reinterpret_cast<const uint4 *>(tab);
+        const uint32_t b4 = __funnelshift_l(0u, (uint32_t)base, 2);
+        const uint32_t bp = b4 | (b4 << 16);
+        const int negk = c.negk;
+        int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+        for (int q = 0; q < W / 8; ++q) {
+            const uint4 e = t8[q];
+            const uint32_t s0 = bp + e.x + (uint32_t)c.col[4 * q + 0];
+            const uint32_t s1 = bp + e.y + (uint32_t)c.col[4 * q + 1];
+            const uint32_t s2 = bp + e.z + (uint32_t)c.col[4 * q + 2];
+            const uint32_t s3 = bp + e.w + (uint32_t)c.col[4 * q + 3];
+            const int h0 = (int)(s0 >> 16), h1 = (int)(s1 >> 16), h2 = (int)(s2 >> 16), h3 = (int)(s3 >> 16);
+            a0 = max(a0, max(lds_lut1((uint32_t)mad_lo(h0, negk, (int)s0)), lds_lut1((uint32_t)h0)));
+            a1 = max(a1, max(lds_lut1((uint32_t)mad_lo(h1, negk, (int)s1)), lds_lut1((uint32_t)h1)));
+            a2 = max(a2, max(lds_lut1((uint32_t)mad_lo(h2, negk, (int)s2)), lds_lut1((uint32_t)h2)));
+            a3 = max(a3, max(lds_lut1((uint32_t)mad_lo(h3, negk, (int)s3)), lds_lut1((uint32_t)h3)));
+        }
+        return max(max(a0, a1), max(a2, a3));
+    } else if constexpr (SelT<SEL>::pack16) {
         // Each register holds two 16-bit byte offsets; the high one is s >> 16
         // (ALU) and the low one s - (s >> 16) * 65536, an IMAD by a run-time
         // constant (FMA pipe), so the ALU pipe -- the binding one -- spends 3
         // ops per 2 leaves (IADD3, SHF, 3-input max); the (31 - v) tie-break
         // goes in as IMAD r*one + (31-v) (FMA pipe).
         const uint4 *t8 = reinterpret_cast<const uint4 *>(tab);
-        const int *lut = sh_lut();  // pid 0: c.lut == 0
+        const int *lut = g_lut1;
         const uint32_t b4 = __funnelshift_l(0u, (uint32_t)base, 2);
         const uint32_t bp = b4 | (b4 << 16);
         const int one = c.one, negk = c.negk;
@@ -452,13 +509,59 @@ __device__ __forceinline__ int tab_scan(const Ctx<W> &c, const int *tab, int bas
     return best;
 }
 
+// lin16 hot scan against the lane's threshold t (= thr - off): the four s16x2
+// chains start at clamp(t - 1, -1, 32766) in both halves, so the scan has a
+// hit iff their max differs from that start (valid leaf sums are >= 0, invalid
+// ones < 0, none above 32766); only a hit unpacks the halves (s16_best).
+// Returns the s16x2 max; `i0` gets the start value.
+template <int W, int SEL>
+__device__ __forceinline__ unsigned tab_scan_thr(const Ctx<W> &c, const int *tab, int t, unsigned &i0) {
+    static_assert(SelT<SEL>::lin16, "lin16 only");
+    const uint4 *t8 = reinterpret_cast<const uint4 *>(tab);
+    const int t0 = min(max(t - 1, -1), 32766);
+    i0 = __byte_perm((unsigned)t0, 0u, 0x1010);
+    unsigned a0 = i0, a1 = i0, a2 = i0, a3 = i0;
+#pragma unroll
+    for (int q = 0; q < W / 8; ++q) {
+        const uint4 e = t8[q];
+        a0 = __viaddmax_s16x2(e.x, (unsigned)c.col[4 * q + 0], a0);
+        a1 = __viaddmax_s16x2(e.y, (unsigned)c.col[4 * q + 1], a1);
+        a2 = __viaddmax_s16x2(e.z, (unsigned)c.col[4 * q + 2], a2);
+        a3 = __viaddmax_s16x2(e.w, (unsigned)c.col[4 * q + 3], a3);
+    }
+    return __vmaxs2(__vmaxs2(a0, a1), __vmaxs2(a2, a3));
+}
+
+__device__ __forceinline__ int s16_best(unsigned m2) { return max((int)(short)(m2 & 0xFFFFu), (int)m2 >> 16); }
+
 template <int W, int SEL>
 __device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2, int base) {
     int *tab = tab_ptr<W, SEL>(c, 0);
     __syncwarp(c.gmask);  // previous readers of the table are done
     tab_put<W, SEL>(c, tab, tab_entry<W, SEL>(c, cand, t2));
     __syncwarp(c.gmask);
-    return tab_scan<W, SEL>(c, tab, base);
+    return tab_scan<W, SEL, !SelT<SEL>::pack16>(c, tab, base);
+}
+
+// pack16 hit (scan max `raw` = (rank + 1) * 32 >= the lane's threshold): the
+// packed rank with the (31 - v) tie-break, or -1 when the hit cannot change
+// the result.  Hits are frequent (Eq. 2 ranks saturate: ~40 % of the C4 scans
+// reach the lane's best score), so they are filtered against the CTA's best
+// key (Shared::ckey, raised by every lane's improvement) before the rescan:
+// a leaf of this scan has score s = raw / 32 - 1 and a device set no smaller
+// than Ufix + the smallest valid v (`vm` = the lane's valid v), so if
+// (s, that set) does not beat the CTA key's (score, set) no leaf of the scan
+// can win anywhere (the final result is a max).  The lane's threshold is
+// raised to the CTA's score on the way.
+template <int W, int SEL>
+__device__ __forceinline__ int sens_hit(const Ctx<W> &c, Best &bst, int raw, uint32_t Ufix, uint32_t vm, int base) {
+    const unsigned long long chi = *reinterpret_cast<volatile unsigned long long *>(&sh().ckey) >> c.eb;
+    bst.thr = max(bst.thr, ((int)(uint32_t)(chi >> W) + 1) * 32);
+    if (raw < bst.thr) return -1;
+    const uint32_t sbmax = __brev(Ufix | (vm & (0u - vm))) >> (32 - W);
+    const unsigned long long hi = ((unsigned long long)((uint32_t)raw >> 5) - 1ull) << W | sbmax;
+    if (hi < chi || (hi == chi && c.clique)) return -1;
+    return tab_scan<W, SEL, true>(c, tab_ptr<W, SEL>(c, 0), base);
 }
 
 template <int W>
@@ -481,7 +584,7 @@ template <int W, int SEL>
 __device__ __forceinline__ bool scan_needed(const Ctx<W> &c, const Best &bst, int entry, int base, bool laneok) {
     int ub;
     if constexpr (SelT<SEL>::lin) ub = base + grp_max<W>(c, entry) + c.colmax;
-    else ub = sh_lut()[3 * c.xs * c.xs + base] + 31;
+    else ub = g_lut1[3 * c.xs * c.xs + base] + 31;  // prune mode: single-query only
     return __any_sync(c.gmask, laneok && ub >= bst.pthr);
 }
 
@@ -517,15 +620,19 @@ __device__ __forceinline__ void inner(const Ctx<W> &c, const St<K> &st, uint32_t
     // a leaf below the CTA's best score cannot win anywhere (max is global)
     if constexpr (SelT<SEL>::cta) bst.thr = max(bst.thr, sh().cthr);
     const int thr = bst.thr - off;
-    const int raw = scan_dense<W, SEL>(c, cand, t2, base);
+    int raw = scan_dense<W, SEL>(c, cand, t2, base);
     if (laneok && raw >= thr) {  // rank >= 32 and its score >= the lane's best score
+        if constexpr (SelT<SEL>::pack16) {
+            raw = sens_hit<W, SEL>(c, bst, raw, st.U | (1u << b), M & cand, base);
+            if (raw < 0) return;
+        }
         const int best = raw + off;
         const uint32_t s = (uint32_t)(best >> 5) - 1u;
         {
             const uint32_t bestv = 31u - (uint32_t)(best & 31);
             unsigned long long fpack = pack_f<K>(st);
             fpack |= (unsigned long long)bestv << (8 * J);
-            consider<W, K, SelT<SEL>::cta>(c, bst, st.U | (1u << bestv) | (1u << b), fpack, s);
+            consider<W, K, SelT<SEL>::cta, SelT<SEL>::pack16>(c, bst, st.U | (1u << bestv) | (1u << b), fpack, s);
         }
     }
 }
@@ -639,12 +746,17 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
                 const uint32_t M = laneok ? (d21 ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
                 bst.cnt += (uint32_t)__popc(M & cand2);
             }
-            const int raw = scan_dense<W, SEL>(c, cand2, t2b + m32 * w3, base);
+            int raw = scan_dense<W, SEL>(c, cand2, t2b + m32 * w3, base);
             if (laneok && raw >= bst.thr) {  // rank >= 32 and its score >= the lane's best score
+                if constexpr (SelT<SEL>::pack16) {
+                    const uint32_t vm = cand2 & (d21 ? ((1u << b) - 1u) : ~(1u << b));
+                    raw = sens_hit<W, SEL>(c, bst, raw, st.U | (1u << v3) | (1u << b), vm, base);
+                    if (raw < 0) continue;
+                }
                 const uint32_t bestv = 31u - (uint32_t)(raw & 31);
                 const unsigned long long fpack =
                     fbase | ((unsigned long long)v3 << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
-                consider<W, K, SelT<SEL>::cta>(c, bst, st.U | (1u << v3) | (1u << bestv) | (1u << b), fpack,
+                consider<W, K, SelT<SEL>::cta, SelT<SEL>::pack16>(c, bst, st.U | (1u << v3) | (1u << bestv) | (1u << b), fpack,
                                (uint32_t)(raw >> 5) - 1u);
             }
         }
@@ -685,17 +797,32 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
         tab_put<W, SEL>(c, tabA, entA);
         tab_put<W, SEL>(c, tabB, entB);
         __syncwarp(c.gmask);
-        const int rawA = runA ? tab_scan<W, SEL>(c, tabA, baseA) : kNeg;
-        const int rawB = runB ? tab_scan<W, SEL>(c, tabB, baseB) : kNeg;
-        const bool hitA = okA && rawA >= bst.thr - offA;
-        const bool hitB = okB && rawB >= bst.thr - offB;
+        int rawA, rawB;
+        bool hitA, hitB;
+        unsigned mA = 0, mB = 0;
+        if constexpr (SelT<SEL>::lin16) {
+            unsigned iA = 0, iB = 0;
+            if (runA) mA = tab_scan_thr<W, SEL>(c, tabA, bst.thr - offA, iA);
+            if (runB) mB = tab_scan_thr<W, SEL>(c, tabB, bst.thr - offB, iB);
+            hitA = okA && runA && mA != iA;
+            hitB = okB && runB && mB != iB;
+        } else {
+            rawA = runA ? tab_scan<W, SEL>(c, tabA, baseA) : kNeg;
+            rawB = runB ? tab_scan<W, SEL>(c, tabB, baseB) : kNeg;
+            hitA = okA && rawA >= bst.thr - offA;
+            hitB = okB && rawB >= bst.thr - offB;
+        }
         if (hitA || hitB) {  // a rank >= 32 whose score >= the lane's / CTA's best score
+            if constexpr (SelT<SEL>::lin16) {
+                rawA = s16_best(mA);
+                rawB = s16_best(mB);
+            }
             if (hitA) {
                 const int best = rawA + offA;
                 const uint32_t bestv = 31u - (uint32_t)(best & 31);
                 const unsigned long long fpack =
                     fbase | ((unsigned long long)vA << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
-                consider<W, K, SelT<SEL>::cta>(c, bst, st.U | (1u << vA) | (1u << bestv) | (1u << b), fpack,
+                consider<W, K, SelT<SEL>::cta, SelT<SEL>::pack16>(c, bst, st.U | (1u << vA) | (1u << bestv) | (1u << b), fpack,
                                (uint32_t)(best >> 5) - 1u);
             }
             if (hitB && rawB >= bst.thr - offB) {
@@ -703,7 +830,7 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
                 const uint32_t bestv = 31u - (uint32_t)(best & 31);
                 const unsigned long long fpack =
                     fbase | ((unsigned long long)vB << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
-                consider<W, K, SelT<SEL>::cta>(c, bst, st.U | (1u << vB) | (1u << bestv) | (1u << b), fpack,
+                consider<W, K, SelT<SEL>::cta, SelT<SEL>::pack16>(c, bst, st.U | (1u << vB) | (1u << bestv) | (1u << b), fpack,
                                (uint32_t)(best >> 5) - 1u);
             }
         }
@@ -950,7 +1077,8 @@ __device__ __forceinline__ int col_table(int sc, const DevPattern &P) {
 }
 
 template <int MAXP, int LUTCAP>
-__device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int xs, int ub_r2 = -1, int only_sc = -1) {
+__device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int xs, int ub_r2 = -1, int only_sc = -1,
+                                            int *lut = nullptr) {
     Shared &s = sh();
     const DevTopo &topo = tb.topo;
     const int tid = threadIdx.x;
@@ -958,6 +1086,7 @@ __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int 
     if (tid == 0) {
         s.one = 1;
         s.cthr = 32;
+        s.ckey = 0ull;
     }
     if (tid <= kMaxN) s.magic[tid] = tid >= 2 ? (0xFFFFFFFFu / (uint32_t)tid + 1u) : 0u;
     static_assert(offsetof(Shared, ts0d) == offsetof(Shared, tw) + 9 * kNN * sizeof(int), "pair tables contiguous");
@@ -983,7 +1112,7 @@ __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int 
             for (int t = 0; t < kPairTables; ++t) pt[t * kNN + i] = e[t];
         }
     }
-    int *lut = sh_lut();
+    if (!lut) lut = sh_lut();  // single-query Eq. 2 kernels pass g_lut1
     for (int p = 0; p < tb.npats; ++p) {
         const DevPattern &P = tb.pat[p];
         const uint16_t *rank = tb.lut + P.lut_off;
@@ -1033,7 +1162,16 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
     }
     // the query load is issued first: its latency overlaps the table copy
     const uint32_t busy = *reinterpret_cast<const volatile uint32_t *>(&dq->busy);
-    load_shared(tb, xs, ub_r2, SEL & 3);
+    if constexpr (SelT<SEL>::pack16) {
+        // g_lut1 must sit where lds_lut1's immediate points (see kLut1Addr)
+        if ((uint32_t)__cvta_generic_to_shared(g_lut1) != kLut1Addr) {
+            if (tid == 0) atomicExch(&rec->status, 2u);
+            return;
+        }
+        load_shared(tb, xs, ub_r2, SEL & 3, g_lut1);
+    } else {
+        load_shared(tb, xs, ub_r2, SEL & 3);
+    }
     __syncthreads();
 
     Ctx<W> c = make_ctx<W>(tb.topo, tb.pat[0], 0, xs, busy, SEL & 3, SelT<SEL>::pack16, SelT<SEL>::lin16);

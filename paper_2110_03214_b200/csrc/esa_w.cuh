@@ -1,5 +1,8 @@
-// esa_w.cuh — per-width entry points (included by esa_w8.cu / esa_w16.cu /
-// esa_w32.cu with MAPA_W defined): instantiates the kernels for one W.
+// esa_w.cuh — per-width entry points, included by esa_w{8,16,32}_p{0..4}.cu
+// with MAPA_W and MAPA_PART defined: part p < 4 instantiates the single-query
+// kernels of base selector p (Greedy / Preserve-insensitive / Preserve-
+// sensitive / Baseline), part 4 the batch and trace kernels, so the ~100
+// kernel instantiations per width compile as parallel translation units.
 #include <atomic>
 
 #include "esa_kernels.cuh"
@@ -100,26 +103,43 @@ const void *pick_ptr(int K) {
         default: return FN<MAPA_W, 23>(__VA_ARGS__);  \
     }
 
-SingleFn pick(int K, int sc) { MAPA_SEL_SWITCH(pick_k, K) }
-const void *pick_fn(int K, int sc) { MAPA_SEL_SWITCH(pick_ptr, K) }
+// single-query selector codes compiled into this part (the dispatcher in
+// esa.cu routes by sc & 3, so a code outside the part is never asked for)
+constexpr bool owns_sel(int sel) { return MAPA_PART < 4 && (sel & 3) == MAPA_PART; }
+template <int W, int SEL>
+SingleFn pick_k_part(int K) {
+    if constexpr (owns_sel(SEL)) return pick_k<W, SEL>(K);
+    else return nullptr;
+}
+template <int W, int SEL>
+const void *pick_ptr_part(int K) {
+    if constexpr (owns_sel(SEL)) return pick_ptr<W, SEL>(K);
+    else return nullptr;
+}
+
+SingleFn pick(int K, int sc) { MAPA_SEL_SWITCH(pick_k_part, K) }
+const void *pick_fn(int K, int sc) { MAPA_SEL_SWITCH(pick_ptr_part, K) }
 
 }  // namespace
 
+#if MAPA_PART < 4
+#define MAPA_PNAME(f) MAPA_CAT(MAPA_CAT(f, MAPA_W), MAPA_CAT(_p, MAPA_PART))
 // sc = selector code | 4 * canonical | 16 * prune (SelT)
-int MAPA_CAT(launch_single_w, MAPA_W)(const SingleTables &tb, int sc, const mapa_query *dq, mapa_record *rec,
+int MAPA_PNAME(launch_single_w)(const SingleTables &tb, int sc, const mapa_query *dq, mapa_record *rec,
                                       int D, int rank, int world, int stripe, int grid, void *stream) {
     SingleFn fn = pick(tb.pat[0].k, sc);
     if (!fn) return (int)cudaErrorInvalidValue;
     return fn(tb, dq, rec, D, rank, world, stripe, grid, (cudaStream_t)stream);
 }
 
-int MAPA_CAT(occ_single_w, MAPA_W)(int K, int sc, int smem) {
+int MAPA_PNAME(occ_single_w)(int K, int sc, int smem) {
     const void *f = pick_fn(K, sc);
     int nb = 0;
     if (!f || set_smem(f, kSmemSingleMax) != 0) return 1;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kBlock, smem) != cudaSuccess) return 1;
     return nb > 0 ? nb : 1;
 }
+#else
 
 int MAPA_CAT(launch_batch_w, MAPA_W)(const MultiTables &tb, int canon, int64_t nq, const mapa_query *d_queries,
                                      mapa_record *d_results, uint32_t *d_ctr, const uint32_t *d_perm, int grid,
@@ -161,5 +181,6 @@ int MAPA_CAT(launch_trace_w, MAPA_W)(const MultiTables &tb, int canon, int ntrac
 }
 
 int MAPA_CAT(smem_shared_w, MAPA_W)() { return (int)sizeof(Shared); }
+#endif
 
 }  // namespace mapa
