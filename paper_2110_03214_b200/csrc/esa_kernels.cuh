@@ -86,6 +86,11 @@ struct SelT {
     // 128-register cap, compiled to +15 % instructions with it, so it keeps
     // the lane's own threshold)
     static constexpr bool cta = lin && !multi;
+    // single-query 16-bit kernels outside prune mode walk the two innermost
+    // levels on static tables (inner3s / inners): per v3 the scan reads the
+    // k-3 -> k-2 edge row of a table built once per CTA, and the lane's
+    // column is re-based once per k-3 prefix, so no per-v3 table is built
+    static constexpr bool stat = (pack16 || lin16) && !prune;
     static constexpr bool useU = base == SEL_INSENS;   // Eq. 3 sums over every placed device
     static constexpr int wt = base == SEL_BASE ? 0 : 1;
     static constexpr int w0 = 38 * wt, w1 = 13 * wt, w2 = 8 * wt, w12 = 12 * wt;
@@ -145,7 +150,39 @@ __device__ __forceinline__ int *sh_lut() { return reinterpret_cast<int *>(g_smem
 // run time and refuses the query (status 2) if it ever differs.
 constexpr int kLut1Ints = 4 * 40 * 40;
 constexpr uint32_t kLut1Addr = 0x400;
-__shared__ __align__(16) int g_lut1[kLut1Ints];
+// Static tables of the SelT::stat kernels (W <= 32, pairs packed per word):
+//   row[v3 * W/2 + q]: the entries of placing vertex k-2 on v = 2q / 2q+1 that
+//     depend on v3 alone -- the (k-3, k-2) edge term and the sentinels of
+//     v == v3 and of the lex-leader bound f(k-3) < f(k-2); row W is all zero
+//     (the k-2-level scan of inners)
+//   col[q * W + b]: lane b's column (edge (k-2, k-1) term, 31 - v tie-break for
+//     additive scores, sentinels of v == b and of f(k-2) < f(k-1))
+struct StatShared {
+    int lut[kLut1Ints];  // first: at kLut1Addr
+    uint32_t row[(32 + 1) * 16];
+    uint32_t col[16 * 32];
+};
+__shared__ __align__(16) StatShared g_st;
+#define g_lut1 (g_st.lut)
+// 16-byte load of g_st.row at byte offset `off` (immediate window address, as
+// lds_lut1: a run-time window base would be rebuilt every iteration)
+constexpr int kRowAddr = (int)kLut1Addr + (int)offsetof(StatShared, row);
+__device__ __forceinline__ uint4 lds_row(uint32_t off) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+%5];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(off), "n"(kRowAddr));
+    return v;
+}
+// lin16 sentinels of the static path: T2B (per prefix) / row / column.  Valid
+// T2B entries are 32 (t2 + ishift) <= kStTmax, valid row entries 32 w <= 1600,
+// valid column entries 32 w + 31 - v <= 1631: a valid leaf sums to
+// [0, kStTmax + 3231]; any sentinel makes the sum negative (each dominates the
+// other two's valid maximum) and the three together stay >= -32768.
+constexpr int kStX = -3232, kStY = -14768, kStZ = -14768;
+constexpr int kStTmax = kLin16StatMax;
+static_assert(kStTmax == -kStY - 1632 && kStTmax == -kStZ - 1632, "see kLin16StatMax");
+static_assert(-(kStX + kStY + kStZ) <= 32768, "s16 range");
 
 // gather at byte offset `off` of g_lut1 (volatile: never merged with another
 // load, so no gathered value is kept live across the hit branch)
@@ -534,6 +571,73 @@ __device__ __forceinline__ unsigned tab_scan_thr(const Ctx<W> &c, const int *tab
 
 __device__ __forceinline__ int s16_best(unsigned m2) { return max((int)(short)(m2 & 0xFFFFu), (int)m2 >> 16); }
 
+// ---------------------------------------------------------------- static-table scans (SelT::stat)
+// lin16: as tab_scan_thr, the leaf pair sums being row[q] + colT[q] (s16x2)
+template <int W>
+__device__ __forceinline__ unsigned scan_row_thr(uint32_t row, const uint32_t (&colT)[W / 2], int t,
+                                                 unsigned &i0) {
+    const int t0 = min(max(t - 1, -1), 32766);
+    i0 = __byte_perm((unsigned)t0, 0u, 0x1010);
+    unsigned a0 = i0, a1 = i0, a2 = i0, a3 = i0;
+#pragma unroll
+    for (int q = 0; q < W / 8; ++q) {
+        const uint4 e = lds_row(row + 16u * q);
+        a0 = __viaddmax_s16x2(e.x, colT[4 * q + 0], a0);
+        a1 = __viaddmax_s16x2(e.y, colT[4 * q + 1], a1);
+        a2 = __viaddmax_s16x2(e.z, colT[4 * q + 2], a2);
+        a3 = __viaddmax_s16x2(e.w, colT[4 * q + 3], a3);
+    }
+    return __vmaxs2(__vmaxs2(a0, a1), __vmaxs2(a2, a3));
+}
+
+// Eq. 2: max LUT entry over the leaves, byte offsets bp + row[q] + colT[q]
+// (the pack16 scan of tab_scan<.., false>)
+template <int W>
+__device__ __forceinline__ int scan_row_max(uint32_t row, const uint32_t (&colT)[W / 2], int base, int negk) {
+    const uint32_t b4 = __funnelshift_l(0u, (uint32_t)base, 2);
+    const uint32_t bp = b4 | (b4 << 16);
+    int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+    for (int q = 0; q < W / 8; ++q) {
+        const uint4 e = lds_row(row + 16u * q);
+        const uint32_t s0 = bp + e.x + colT[4 * q + 0];
+        const uint32_t s1 = bp + e.y + colT[4 * q + 1];
+        const uint32_t s2 = bp + e.z + colT[4 * q + 2];
+        const uint32_t s3 = bp + e.w + colT[4 * q + 3];
+        const int h0 = (int)(s0 >> 16), h1 = (int)(s1 >> 16), h2 = (int)(s2 >> 16), h3 = (int)(s3 >> 16);
+        a0 = max(a0, max(lds_lut1((uint32_t)mad_lo(h0, negk, (int)s0)), lds_lut1((uint32_t)h0)));
+        a1 = max(a1, max(lds_lut1((uint32_t)mad_lo(h1, negk, (int)s1)), lds_lut1((uint32_t)h1)));
+        a2 = max(a2, max(lds_lut1((uint32_t)mad_lo(h2, negk, (int)s2)), lds_lut1((uint32_t)h2)));
+        a3 = max(a3, max(lds_lut1((uint32_t)mad_lo(h3, negk, (int)s3)), lds_lut1((uint32_t)h3)));
+    }
+    return max(max(a0, a1), max(a2, a3));
+}
+
+// Eq. 2 rescan of a hit: the packed rank (rank + 1) * 32 + 31 - v
+template <int W>
+__device__ __forceinline__ int scan_row_tie(uint32_t row, const uint32_t (&colT)[W / 2], int base, int one,
+                                            int negk) {
+    const int *lut = g_lut1;
+    const uint32_t b4 = __funnelshift_l(0u, (uint32_t)base, 2);
+    const uint32_t bp = b4 | (b4 << 16);
+    int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+    for (int q = 0; q < W / 8; ++q) {
+        const uint4 e = lds_row(row + 16u * q);
+        const uint32_t s0 = bp + e.x + colT[4 * q + 0];
+        const uint32_t s1 = bp + e.y + colT[4 * q + 1];
+        const uint32_t s2 = bp + e.z + colT[4 * q + 2];
+        const uint32_t s3 = bp + e.w + colT[4 * q + 3];
+        const int h0 = (int)(s0 >> 16), h1 = (int)(s1 >> 16), h2 = (int)(s2 >> 16), h3 = (int)(s3 >> 16);
+        const int v = 8 * q;
+        a0 = max(a0, max(lds_off(lut, (int)s0 + h0 * negk) * one + (31 - v), lds_off(lut, h0) * one + (30 - v)));
+        a1 = max(a1, max(lds_off(lut, (int)s1 + h1 * negk) * one + (29 - v), lds_off(lut, h1) * one + (28 - v)));
+        a2 = max(a2, max(lds_off(lut, (int)s2 + h2 * negk) * one + (27 - v), lds_off(lut, h2) * one + (26 - v)));
+        a3 = max(a3, max(lds_off(lut, (int)s3 + h3 * negk) * one + (25 - v), lds_off(lut, h3) * one + (24 - v)));
+    }
+    return max(max(a0, a1), max(a2, a3));
+}
+
 template <int W, int SEL>
 __device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2, int base) {
     int *tab = tab_ptr<W, SEL>(c, 0);
@@ -553,14 +657,19 @@ __device__ __forceinline__ int scan_dense(const Ctx<W> &c, uint32_t cand, int t2
 // (s, that set) does not beat the CTA key's (score, set) no leaf of the scan
 // can win anywhere (the final result is a max).  The lane's threshold is
 // raised to the CTA's score on the way.
-template <int W, int SEL>
-__device__ __forceinline__ int sens_hit(const Ctx<W> &c, Best &bst, int raw, uint32_t Ufix, uint32_t vm, int base) {
+template <int W>
+__device__ __forceinline__ bool sens_may_win(const Ctx<W> &c, Best &bst, int raw, uint32_t Ufix, uint32_t vm) {
     const unsigned long long chi = *reinterpret_cast<volatile unsigned long long *>(&sh().ckey) >> c.eb;
     bst.thr = max(bst.thr, ((int)(uint32_t)(chi >> W) + 1) * 32);
-    if (raw < bst.thr) return -1;
+    if (raw < bst.thr) return false;
     const uint32_t sbmax = __brev(Ufix | (vm & (0u - vm))) >> (32 - W);
     const unsigned long long hi = ((unsigned long long)((uint32_t)raw >> 5) - 1ull) << W | sbmax;
-    if (hi < chi || (hi == chi && c.clique)) return -1;
+    return !(hi < chi || (hi == chi && c.clique));
+}
+
+template <int W, int SEL>
+__device__ __forceinline__ int sens_hit(const Ctx<W> &c, Best &bst, int raw, uint32_t Ufix, uint32_t vm, int base) {
+    if (!sens_may_win<W>(c, bst, raw, Ufix, vm)) return -1;
     return tab_scan<W, SEL, true>(c, tab_ptr<W, SEL>(c, 0), base);
 }
 
@@ -837,14 +946,217 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
     }
 }
 
+// ---------------------------------------------------------------- static-table inner levels
+// The lane's column re-based on this prefix: colT[q] = column pair q + the
+// pair (2q, 2q+1) of the lanes' T2 entries (`entry` = this lane's entry as the
+// device of vertex k-2).  The caller has synced the group since the last
+// reader of dense[0]; this syncs after the write.
+template <int W, int SEL>
+__device__ __forceinline__ void stat_col(const Ctx<W> &c, int entry, uint32_t (&colT)[W / 2]) {
+    uint16_t *t = reinterpret_cast<uint16_t *>(sh().wl[c.warp].dense[0]) + c.g * W;
+    t[c.b] = (uint16_t)entry;
+    __syncwarp(c.gmask);
+    const uint4 *t8 = reinterpret_cast<const uint4 *>(t);
+    const uint32_t *cs = g_st.col + c.b;
+#pragma unroll
+    for (int q = 0; q < W / 8; ++q) {
+        const uint4 e = t8[q];
+        const uint32_t ev[4] = {e.x, e.y, e.z, e.w};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t cv = cs[(4 * q + j) * W];
+            if constexpr (SelT<SEL>::lin16) colT[4 * q + j] = __viaddmax_s16x2(cv, ev[j], 0x80008000u);  // s16x2 add
+            else colT[4 * q + j] = cv + ev[j];  // byte offsets, no carry between the halves
+        }
+    }
+}
+
+// T2 entry of this lane as the device of vertex k-2 (`ok`: a candidate)
+template <int W, int SEL>
+__device__ __forceinline__ int stat_entry(const Ctx<W> &c, bool ok, int t2) {
+    if constexpr (SelT<SEL>::lin16) return ok ? (t2 + c.ishift) * 32 : kStX;
+    else return 4 * (ok ? t2 : c.xs * c.xs);
+}
+
+// inner() on the static tables: the k-2 scan reads the all-zero row W.
+template <int W, int K, int SEL>
+__device__ __forceinline__ void inners(const Ctx<W> &c, const St<K> &st, uint32_t cand, Best &bst) {
+    constexpr int J = K - 2;
+    const uint32_t b = (uint32_t)c.b;
+    const uint32_t fsJ = (uint32_t)(SelT<SEL>::canon ? c.fs >> (8 * J) : 0ull) & 0xFFu;
+    const bool dep = (fsJ >> (K - 1)) & 1u;  // lex-leader f(k-2) < f(k-1)
+    int t2, base;
+    if constexpr (SelT<SEL>::lin) {
+        const uint32_t X2 = SelT<SEL>::useU ? st.U : st.bm[J];
+        const uint32_t X1 = SelT<SEL>::useU ? st.U : st.bm[K - 1];
+        t2 = SelT<SEL>::w12 * __popc(X2) - (SelT<SEL>::useU ? c.incb : 0) + SelT<SEL>::w0 * __popc(c.cm0 & X2) +
+             SelT<SEL>::w1 * __popc(c.cm1 & X2) + SelT<SEL>::w2 * __popc(c.cm2 & X2);
+        const int lp = c.laneC + SelT<SEL>::w12 * __popc(X1) + SelT<SEL>::w0 * __popc(c.cm0 & X1) +
+                       SelT<SEL>::w1 * __popc(c.cm1 & X1) + SelT<SEL>::w2 * __popc(c.cm2 & X1);
+        base = (st.acc + lp + 1 - c.ishift) * 32;
+    } else {
+        const uint32_t X2 = st.bm[J], X1 = st.bm[K - 1];
+        t2 = __popc(c.cm0 & X2) * c.xs + __popc(c.cm12 & X2);
+        base = (st.acc + __popc(c.cm0 & X1)) * c.xs + st.acc2 + __popc(c.cm12 & X1);  // census index
+    }
+    const bool laneok = ((c.F & ~st.U & alw<SEL>(st.al[K - 1])) >> b) & 1u;
+    const uint32_t M = laneok ? (dep ? ((1u << b) - 1u) : ~(1u << b)) : 0u;
+    bst.cnt += (uint32_t)__popc(M & cand);
+    if constexpr (SelT<SEL>::cta) bst.thr = max(bst.thr, sh().cthr);
+    uint32_t colT[W / 2];
+    __syncwarp(c.gmask);  // previous readers of dense[0] are done
+    stat_col<W, SEL>(c, stat_entry<W, SEL>(c, (cand >> b) & 1u, t2), colT);
+    const uint32_t row = 4u * W * (W / 2);  // byte offset of row W
+    int raw;
+    if constexpr (SelT<SEL>::lin16) {
+        unsigned i0;
+        const unsigned m2 = scan_row_thr<W>(row, colT, bst.thr - base, i0);
+        if (!(laneok && m2 != i0)) return;
+        raw = s16_best(m2) + base;
+    } else {
+        raw = scan_row_max<W>(row, colT, base, c.negk);
+        if (!(laneok && raw >= bst.thr)) return;
+        if (!sens_may_win<W>(c, bst, raw, st.U | (1u << b), M & cand)) return;
+        raw = scan_row_tie<W>(row, colT, base, c.one, c.negk);
+    }
+    const uint32_t bestv = 31u - (uint32_t)(raw & 31);
+    const unsigned long long fpack = pack_f<K>(st) | ((unsigned long long)bestv << (8 * J));
+    consider<W, K, SelT<SEL>::cta, SelT<SEL>::pack16>(c, bst, st.U | (1u << bestv) | (1u << b), fpack,
+                                                      (uint32_t)(raw >> 5) - 1u);
+}
+
+// inner3() on the static tables (see SelT::stat): per v3 no table is built and
+// no warp sync runs; the scan reads row v3 and the prefix-based column colT.
+template <int W, int K, int SEL>
+__device__ __forceinline__ void inner3s(const Ctx<W> &c, const St<K> &st, uint32_t cand3, Best &bst) {
+    constexpr int J3 = K - 3, J2 = K - 2, J1 = K - 1;
+    const uint32_t b = (uint32_t)c.b;
+    const uint32_t fs3 = (uint32_t)(SelT<SEL>::canon ? c.fs >> (8 * J3) : 0ull) & 0xFFu;
+    const uint32_t fb3 = (uint32_t)(c.fb >> (8 * J3)) & 0xFFu;
+    const uint32_t fs2 = (uint32_t)(SelT<SEL>::canon ? c.fs >> (8 * J2) : 0ull) & 0xFFu;
+    const bool e31 = (fb3 >> J1) & 1u;
+    const bool d32 = (fs3 >> J2) & 1u, d31 = (fs3 >> J1) & 1u, d21 = (fs2 >> J1) & 1u;
+    // lane values over the placed vertices 0..k-4 (see inner3); the (k-3, k-2)
+    // edge term lives in the static row, the (k-3, k-1) term is m31 w3
+    int t3, t2b, lpb, m31, A;
+    const int *wcol;
+    if constexpr (SelT<SEL>::lin) {
+        const uint32_t X3 = SelT<SEL>::useU ? st.U : st.bm[J3];
+        const uint32_t X2 = SelT<SEL>::useU ? st.U : st.bm[J2];
+        const uint32_t X1 = SelT<SEL>::useU ? st.U : st.bm[J1];
+        const int inc = SelT<SEL>::useU ? c.incb : 0;
+        t3 = SelT<SEL>::w12 * __popc(X3) - inc + SelT<SEL>::w0 * __popc(c.cm0 & X3) + SelT<SEL>::w1 * __popc(c.cm1 & X3) +
+             SelT<SEL>::w2 * __popc(c.cm2 & X3);
+        t2b = SelT<SEL>::w12 * __popc(X2) - inc + SelT<SEL>::w0 * __popc(c.cm0 & X2) + SelT<SEL>::w1 * __popc(c.cm1 & X2) +
+              SelT<SEL>::w2 * __popc(c.cm2 & X2);
+        lpb = c.laneC + SelT<SEL>::w12 * __popc(X1) + SelT<SEL>::w0 * __popc(c.cm0 & X1) + SelT<SEL>::w1 * __popc(c.cm1 & X1) +
+              SelT<SEL>::w2 * __popc(c.cm2 & X1);
+        m31 = (SelT<SEL>::w12 != 0 && (SelT<SEL>::useU || e31)) ? 1 : 0;
+        A = st.acc;
+        wcol = sh().twp + b;
+    } else {
+        const uint32_t X3 = st.bm[J3], X2 = st.bm[J2], X1 = st.bm[J1];
+        t3 = __popc(c.cm0 & X3) * c.xs + __popc(c.cm12 & X3);
+        t2b = __popc(c.cm0 & X2) * c.xs + __popc(c.cm12 & X2);
+        lpb = __popc(c.cm0 & X1) * c.xs + __popc(c.cm12 & X1);
+        m31 = e31 ? 1 : 0;
+        A = st.acc * c.xs + st.acc2;
+        wcol = sh().tdl + b;
+    }
+    int2 *L3 = sh().wl[c.warp].l3 + c.g * W;
+    const uint32_t n3 = (uint32_t)__popc(cand3);
+    const bool okb = ((c.F & ~st.U & alw<SEL>(st.al[J1])) >> b) & 1u;
+    const uint32_t cand2b = c.F & ~st.U & alw<SEL>(st.al[J2]);
+    __syncwarp(c.gmask);  // previous readers of the k-3 list and of dense[0] are done
+    if ((cand3 >> b) & 1u) L3[__popc(cand3 & ((1u << b) - 1u))] = make_int2((int)b, t3);
+    uint32_t colT[W / 2];
+    stat_col<W, SEL>(c, stat_entry<W, SEL>(c, (cand2b >> b) & 1u, t2b), colT);  // syncs the group
+    const unsigned long long fbase = pack_f<K>(st);
+    const bool dep = d32 || d31 || d21;
+    if constexpr (SelT<SEL>::cta) bst.thr = max(bst.thr, sh().cthr);
+    const uint32_t Mb = d21 ? ((1u << b) - 1u) : ~(1u << b);  // valid v of this lane given f(k-1) = b
+    if (!dep && okb) {
+        const uint32_t nb = ~(1u << b);
+        bst.cnt += (uint32_t)(__popc(cand3 & nb) * __popc(cand2b & nb) - __popc(cand3 & cand2b & nb));
+    }
+    if constexpr (!SelT<SEL>::lin) {
+        for (uint32_t i = 0; i < n3; ++i) {
+            const int2 e3 = L3[i];
+            const uint32_t v3 = (uint32_t)e3.x;
+            const int w3 = wcol[v3 * 32];
+            const bool laneok = okb && b != v3 && (!d31 || b > v3);
+            const int base = A + e3.y + lpb + m31 * w3;
+            const uint32_t row = v3 * (2u * W);  // byte offset of row v3
+            if (dep) {
+                const uint32_t cand2 = cand2b & ~(1u << v3) & (d32 ? (0xFFFFFFFEu << v3) : kFull);
+                bst.cnt += laneok ? (uint32_t)__popc(Mb & cand2) : 0u;
+            }
+            int raw = scan_row_max<W>(row, colT, base, c.negk);
+            if (laneok && raw >= bst.thr) {  // rank >= the lane's best score: filter, then rescan for the v
+                const uint32_t cand2 = cand2b & ~(1u << v3) & (d32 ? (0xFFFFFFFEu << v3) : kFull);
+                if (!sens_may_win<W>(c, bst, raw, st.U | (1u << v3) | (1u << b), cand2 & Mb)) continue;
+                raw = scan_row_tie<W>(row, colT, base, c.one, c.negk);
+                const uint32_t bestv = 31u - (uint32_t)(raw & 31);
+                const unsigned long long fpack =
+                    fbase | ((unsigned long long)v3 << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
+                consider<W, K, false, true>(c, bst, st.U | (1u << v3) | (1u << bestv) | (1u << b), fpack,
+                                            (uint32_t)(raw >> 5) - 1u);
+            }
+        }
+        return;
+    } else {
+        for (uint32_t i = 0; i < n3; i += 2) {
+            const bool hasB = i + 1 < n3;
+            const int2 eA = L3[i], eB = L3[hasB ? i + 1 : i];
+            const uint32_t vA = (uint32_t)eA.x, vB = (uint32_t)eB.x;
+            const int wA = wcol[vA * 32], wB = wcol[vB * 32];
+            const bool okA = okb && b != vA && (!d31 || b > vA);
+            const bool okB = hasB && okb && b != vB && (!d31 || b > vB);
+            const int offA = (A + eA.y + lpb + m31 * wA + 1 - c.ishift) * 32;
+            const int offB = (A + eB.y + lpb + m31 * wB + 1 - c.ishift) * 32;
+            if (dep) {
+                const uint32_t cA = cand2b & ~(1u << vA) & (d32 ? (0xFFFFFFFEu << vA) : kFull);
+                const uint32_t cB = cand2b & ~(1u << vB) & (d32 ? (0xFFFFFFFEu << vB) : kFull);
+                bst.cnt += (uint32_t)(okA ? __popc(Mb & cA) : 0) + (uint32_t)(okB ? __popc(Mb & cB) : 0);
+            }
+            unsigned iA, iB;
+            const unsigned mA = scan_row_thr<W>(vA * (2u * W), colT, bst.thr - offA, iA);
+            const unsigned mB = scan_row_thr<W>(vB * (2u * W), colT, bst.thr - offB, iB);
+            const bool hitA = okA && mA != iA, hitB = okB && mB != iB;
+            if (hitA || hitB) {  // a leaf whose score reaches the lane's / CTA's best score
+                if (hitA) {
+                    const int best = s16_best(mA) + offA;
+                    const uint32_t bestv = 31u - (uint32_t)(best & 31);
+                    const unsigned long long fpack =
+                        fbase | ((unsigned long long)vA << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
+                    consider<W, K, SelT<SEL>::cta, false>(c, bst, st.U | (1u << vA) | (1u << bestv) | (1u << b), fpack,
+                                                          (uint32_t)(best >> 5) - 1u);
+                }
+                if (hitB) {
+                    const int best = s16_best(mB) + offB;
+                    if (best >= bst.thr) {
+                        const uint32_t bestv = 31u - (uint32_t)(best & 31);
+                        const unsigned long long fpack =
+                            fbase | ((unsigned long long)vB << (8 * J3)) | ((unsigned long long)bestv << (8 * J2));
+                        consider<W, K, SelT<SEL>::cta, false>(c, bst, st.U | (1u << vB) | (1u << bestv) | (1u << b),
+                                                              fpack, (uint32_t)(best >> 5) - 1u);
+                    }
+                }
+            }
+        }
+    }
+}
+
 template <int W, int K, int SEL, int J>
 __device__ __forceinline__ void level(const Ctx<W> &c, const St<K> &st, Best &bst) {
     if constexpr (K == 1) {
         leaf_k1<W, SEL>(c, bst);
     } else if constexpr (J == K - 2) {
-        inner<W, K, SEL>(c, st, c.F & ~st.U & alw<SEL>(st.al[J]), bst);
+        if constexpr (SelT<SEL>::stat) inners<W, K, SEL>(c, st, c.F & ~st.U & alw<SEL>(st.al[J]), bst);
+        else inner<W, K, SEL>(c, st, c.F & ~st.U & alw<SEL>(st.al[J]), bst);
     } else if constexpr (J == K - 3) {
-        inner3<W, K, SEL>(c, st, c.F & ~st.U & alw<SEL>(st.al[J]), bst);
+        if constexpr (SelT<SEL>::stat) inner3s<W, K, SEL>(c, st, c.F & ~st.U & alw<SEL>(st.al[J]), bst);
+        else inner3<W, K, SEL>(c, st, c.F & ~st.U & alw<SEL>(st.al[J]), bst);
     } else {
         uint32_t cand = c.F & ~st.U & alw<SEL>(st.al[J]);
         while (cand) {
@@ -928,9 +1240,11 @@ __device__ __forceinline__ uint32_t descend_range(const Ctx<W> &c, const St<K> &
             }
             cand &= alw<SEL>(st.al[J]);
             if constexpr (J == K - 2) {
-                inner<W, K, SEL>(c, st, cand, bst);
+                if constexpr (SelT<SEL>::stat) inners<W, K, SEL>(c, st, cand, bst);
+                else inner<W, K, SEL>(c, st, cand, bst);
             } else if constexpr (J == K - 3) {
-                inner3<W, K, SEL>(c, st, cand, bst);
+                if constexpr (SelT<SEL>::stat) inner3s<W, K, SEL>(c, st, cand, bst);
+                else inner3<W, K, SEL>(c, st, cand, bst);
             } else {
                 while (cand) {
                     const uint32_t v = __ffs(cand) - 1;
@@ -1078,7 +1392,7 @@ __device__ __forceinline__ int col_table(int sc, const DevPattern &P) {
 
 template <int MAXP, int LUTCAP>
 __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int xs, int ub_r2 = -1, int only_sc = -1,
-                                            int *lut = nullptr) {
+                                            int *lut = nullptr, int regions = 3) {
     Shared &s = sh();
     const DevTopo &topo = tb.topo;
     const int tid = threadIdx.x;
@@ -1117,11 +1431,11 @@ __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int 
         const DevPattern &P = tb.pat[p];
         const uint16_t *rank = tb.lut + P.lut_off;
         const int m = P.m;
-        for (int i = tid; i < 3 * xs * xs; i += blockDim.x) {
+        for (int i = tid; i < regions * xs * xs; i += blockDim.x) {
             const int x = i / xs, y = i % xs;
             int v = kNeg;
             if (i < xs * xs) v = (x + y <= m) ? ((int)rank[x * (m + 1) + y] + 1) * 32 : 0;
-            lut[p * 3 * xs * xs + i] = v;
+            lut[p * regions * xs * xs + i] = v;
         }
         if (tid < 28) s.edge[p][tid] = P.edge[tid];
     }
@@ -1139,6 +1453,50 @@ __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int 
                     if (x + dx + y + dy <= m && x + dx < xs && y + dy < xs) best = max(best, lut[(x + dx) * xs + y + dy]);
             ub[i] = best;
         }
+    }
+}
+
+// Static tables of the SelT::stat kernels (StatShared), from the pair tables
+// load_shared put in shared memory (the lane column's table and twp / tdl).
+// Caller syncs before (tables loaded) and after.
+template <int W, int SEL>
+__device__ __forceinline__ void build_stat(const DevPattern &P, int xs) {
+    const int K = P.k, tid = threadIdx.x;
+    const bool e32 = K >= 3 && ((P.fwd_back[K - 3] >> (K - 2)) & 1u);
+    const bool d32 = SelT<SEL>::canon && K >= 3 && ((P.fwd_src[K - 3] >> (K - 2)) & 1u);
+    const int *ct = &sh().tw[0] + col_table(SEL & 3, P) * kNN;
+    const int *dt = SelT<SEL>::lin ? sh().twp : sh().tdl;
+    const bool m32 = SelT<SEL>::lin ? (SelT<SEL>::w12 != 0 && (SelT<SEL>::useU || e32)) : e32;
+    constexpr int H = W / 2;
+    for (int i = tid; i < (W + 1) * H; i += blockDim.x) {
+        const int v3 = i / H, q = i % H;
+        uint32_t pr = 0;
+        if (v3 < W) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int v = 2 * q + h;
+                const bool bad = v == v3 || (d32 && v <= v3);
+                int e;
+                if constexpr (SelT<SEL>::lin16) e = bad ? kStY : (m32 ? 32 * dt[v3 * 32 + v] : 0);
+                else e = 4 * ((m32 ? dt[v3 * 32 + v] : 0) + (bad ? xs * xs : 0));
+                pr |= ((uint32_t)e & 0xFFFFu) << (16 * h);
+            }
+        }
+        g_st.row[i] = pr;
+    }
+    for (int i = tid; i < H * W; i += blockDim.x) {
+        const int q = i / W, b = i % W;
+        uint32_t pr = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int v = 2 * q + h;
+            const int t = ct[v * 32 + b];
+            int e;
+            if constexpr (SelT<SEL>::lin16) e = t == kNegTable ? kStZ : t + 31 - v;
+            else e = t;
+            pr |= ((uint32_t)e & 0xFFFFu) << (16 * h);
+        }
+        g_st.col[i] = pr;
     }
 }
 
@@ -1168,17 +1526,22 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
             if (tid == 0) atomicExch(&rec->status, 2u);
             return;
         }
-        load_shared(tb, xs, ub_r2, SEL & 3, g_lut1);
+        // (static path: an index carries up to three sentinels -> 4 regions)
+        load_shared(tb, xs, ub_r2, SEL & 3, g_lut1, SelT<SEL>::stat ? 4 : 3);
     } else {
         load_shared(tb, xs, ub_r2, SEL & 3);
     }
     __syncthreads();
+    if constexpr (SelT<SEL>::stat) {
+        build_stat<W, SEL>(tb.pat[0], xs);
+        __syncthreads();
+    }
 
     Ctx<W> c = make_ctx<W>(tb.topo, tb.pat[0], 0, xs, busy, SEL & 3, SelT<SEL>::pack16, SelT<SEL>::lin16);
     if constexpr (SelT<SEL>::lin16) {
         // the host chose 16-bit scans from busy_hint; a query whose free set
         // breaks the range (lin16_fits) is refused loudly, never mis-scored
-        if (32 * (50 * (K - 2) + c.irange) > 31135) {
+        if (32 * (50 * (K - 2) + c.irange) > (SelT<SEL>::stat ? kStTmax : kLin16Max)) {
             if (tid == 0) atomicExch(&rec->status, 1u);
             return;
         }

@@ -58,6 +58,11 @@ static_assert(sizeof(DevPattern) == 64, "DevPattern layout");
 // meaning: esa_kernels.cuh `Shared`), built per CTA, or copied from a cached
 // device image built once per (topology, Eq. 2 row stride) on the host.
 constexpr int kNegTable = -(1 << 28);
+// lin16 single-query scans (16-bit Eq. 1 / Eq. 3): the largest 32 (50 (k-2) +
+// inc_F spread) the kernels accept -- the per-v3-table path (prune mode) and
+// the static-table path (esa_kernels.cuh, kStX / kStY / kStZ)
+constexpr int kLin16Max = 31135;
+constexpr int kLin16StatMax = 14768 - 1632;
 constexpr int kPairTables = 10;
 inline __host__ __device__ void pair_table_entry(const DevTopo &topo, int i, int xs, int out[kPairTables]) {
     const int v = i >> 5, b = i & 31;

@@ -481,7 +481,8 @@ const int4 *pair_tables(const mapa_topology *tc, int xs, void *stream) {
 // sum_U w(u, v) - inc_F(v), ishift = max_{v in F} inc_F(v) for Eq. 3, so
 // t2 + ishift <= 50 (k-2) + spread, spread = max - min of inc_F over F
 // (unknown F: spread <= max_v inc over all devices); entries must stay <= 31135.
-bool lin16_fits(const mapa_topology *t, const mapa_pattern *p, int selcode, uint64_t busy_hint) {
+// `bound`: kLin16Max (prune-mode kernels) or kLin16StatMax (the others)
+bool lin16_fits(const mapa_topology *t, const mapa_pattern *p, int selcode, uint64_t busy_hint, int bound) {
     if (t->width < 16 || p->k < 3 || (selcode != SEL_GREEDY && selcode != SEL_INSENS)) return false;
     int spread = 0;
     if (selcode == SEL_INSENS) {
@@ -498,7 +499,7 @@ bool lin16_fits(const mapa_topology *t, const mapa_pattern *p, int selcode, uint
         }
         spread = busy_hint == ~0ull ? hi : hi - (lo > hi ? hi : lo);
     }
-    return 32 * (50 * (p->k - 2) + spread) <= 31135;
+    return 32 * (50 * (p->k - 2) + spread) <= bound;
 }
 
 struct Plan {
@@ -1255,9 +1256,10 @@ static mapa_status launch_query_impl(const mapa_topology *t, const mapa_pattern 
     tb.pre = pair_tables(t, tb.xs, stream);
     // canonical instantiation only when a lex-leader constraint exists (|Aut| > 1
     // and not RAW); otherwise the constraint-free kernel enumerates the same set
-    const int sc = sel_code(selector, sensitive) | (has_constraints(tb.pat[0]) ? 4 : 0) |
-                   ((flags & MAPA_F_PRUNE) && p->k >= 4 ? 16 : 0) |
-                   (lin16_fits(t, p, sel_code(selector, sensitive), busy_hint) ? 32 : 0);
+    const bool prune = (flags & MAPA_F_PRUNE) && p->k >= 4;
+    const int sc = sel_code(selector, sensitive) | (has_constraints(tb.pat[0]) ? 4 : 0) | (prune ? 16 : 0) |
+                   (lin16_fits(t, p, sel_code(selector, sensitive), busy_hint, prune ? kLin16Max : kLin16StatMax)
+                        ? 32 : 0);
     Plan pl = plan_single(t, p, sc, nF, world);
     if (pl.nlocal >= (1ull << 27)) return fail(MAPA_E_UNSUPPORTED, "too many work items");
     std::memcpy(tb.lut, p->lut.data(), p->lut.size() * sizeof(uint16_t));
