@@ -157,21 +157,39 @@ constexpr uint32_t kLut1Addr = 0x400;
 //     (the k-2-level scan of inners)
 //   col[q * W + b]: lane b's column (edge (k-2, k-1) term, 31 - v tie-break for
 //     additive scores, sentinels of v == b and of f(k-2) < f(k-1))
-struct StatShared {
-    int lut[kLut1Ints];  // first: at kLut1Addr
+// The Eq. 2 kernels keep the LUT in front (StatSharedL, g_stL), the additive
+// ones only the row / column tables (g_stN, no LUT: 4 KB, so three CTAs fit an
+// SM); a kernel references one of the two, which sits at kLut1Addr.
+struct StatTabs {
     uint32_t row[(32 + 1) * 16];
     uint32_t col[16 * 32];
 };
-__shared__ __align__(16) StatShared g_st;
-#define g_lut1 (g_st.lut)
-// 16-byte load of g_st.row at byte offset `off` (immediate window address, as
-// lds_lut1: a run-time window base would be rebuilt every iteration)
-constexpr int kRowAddr = (int)kLut1Addr + (int)offsetof(StatShared, row);
+struct StatSharedL {
+    int lut[kLut1Ints];  // first: at kLut1Addr
+    StatTabs t;
+};
+__shared__ __align__(16) StatSharedL g_stL;
+__shared__ __align__(16) StatTabs g_stN;
+#define g_lut1 (g_stL.lut)
+template <bool L>
+__device__ __forceinline__ StatTabs &stt() {
+    if constexpr (L) return g_stL.t;
+    else return g_stN;
+}
+template <bool L>
+__device__ __forceinline__ const void *stat_base() {
+    if constexpr (L) return &g_stL;
+    else return &g_stN;
+}
+// 16-byte load of the static row table at byte offset `off` (immediate window
+// address, as lds_lut1: a run-time window base would be rebuilt every iteration)
+template <bool L>
 __device__ __forceinline__ uint4 lds_row(uint32_t off) {
+    constexpr int addr = (int)kLut1Addr + (L ? (int)offsetof(StatSharedL, t) : 0) + (int)offsetof(StatTabs, row);
     uint4 v;
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4+%5];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "r"(off), "n"(kRowAddr));
+                 : "r"(off), "n"(addr));
     return v;
 }
 // lin16 sentinels of the static path: T2B (per prefix) / row / column.  Valid
@@ -581,7 +599,7 @@ __device__ __forceinline__ unsigned scan_row_thr(uint32_t row, const uint32_t (&
     unsigned a0 = i0, a1 = i0, a2 = i0, a3 = i0;
 #pragma unroll
     for (int q = 0; q < W / 8; ++q) {
-        const uint4 e = lds_row(row + 16u * q);
+        const uint4 e = lds_row<false>(row + 16u * q);
         a0 = __viaddmax_s16x2(e.x, colT[4 * q + 0], a0);
         a1 = __viaddmax_s16x2(e.y, colT[4 * q + 1], a1);
         a2 = __viaddmax_s16x2(e.z, colT[4 * q + 2], a2);
@@ -599,7 +617,7 @@ __device__ __forceinline__ int scan_row_max(uint32_t row, const uint32_t (&colT)
     int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll
     for (int q = 0; q < W / 8; ++q) {
-        const uint4 e = lds_row(row + 16u * q);
+        const uint4 e = lds_row<true>(row + 16u * q);
         const uint32_t s0 = bp + e.x + colT[4 * q + 0];
         const uint32_t s1 = bp + e.y + colT[4 * q + 1];
         const uint32_t s2 = bp + e.z + colT[4 * q + 2];
@@ -623,7 +641,7 @@ __device__ __forceinline__ int scan_row_tie(uint32_t row, const uint32_t (&colT)
     int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll
     for (int q = 0; q < W / 8; ++q) {
-        const uint4 e = lds_row(row + 16u * q);
+        const uint4 e = lds_row<true>(row + 16u * q);
         const uint32_t s0 = bp + e.x + colT[4 * q + 0];
         const uint32_t s1 = bp + e.y + colT[4 * q + 1];
         const uint32_t s2 = bp + e.z + colT[4 * q + 2];
@@ -957,7 +975,7 @@ __device__ __forceinline__ void stat_col(const Ctx<W> &c, int entry, uint32_t (&
     t[c.b] = (uint16_t)entry;
     __syncwarp(c.gmask);
     const uint4 *t8 = reinterpret_cast<const uint4 *>(t);
-    const uint32_t *cs = g_st.col + c.b;
+    const uint32_t *cs = stt<SelT<SEL>::pack16>().col + c.b;
 #pragma unroll
     for (int q = 0; q < W / 8; ++q) {
         const uint4 e = t8[q];
@@ -1427,11 +1445,14 @@ __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int 
         }
     }
     if (!lut) lut = sh_lut();  // single-query Eq. 2 kernels pass g_lut1
+    // single-query additive kernels read no Eq. 2 table (and get no dynamic
+    // shared memory for it: smem_single)
+    const int nlut = only_sc >= 0 && (only_sc & 3) != SEL_SENS ? 0 : tb.npats;
     for (int p = 0; p < tb.npats; ++p) {
         const DevPattern &P = tb.pat[p];
         const uint16_t *rank = tb.lut + P.lut_off;
         const int m = P.m;
-        for (int i = tid; i < regions * xs * xs; i += blockDim.x) {
+        for (int i = tid; p < nlut && i < regions * xs * xs; i += blockDim.x) {
             const int x = i / xs, y = i % xs;
             int v = kNeg;
             if (i < xs * xs) v = (x + y <= m) ? ((int)rank[x * (m + 1) + y] + 1) * 32 : 0;
@@ -1482,7 +1503,7 @@ __device__ __forceinline__ void build_stat(const DevPattern &P, int xs) {
                 pr |= ((uint32_t)e & 0xFFFFu) << (16 * h);
             }
         }
-        g_st.row[i] = pr;
+        stt<SelT<SEL>::pack16>().row[i] = pr;
     }
     for (int i = tid; i < H * W; i += blockDim.x) {
         const int q = i / W, b = i % W;
@@ -1496,16 +1517,23 @@ __device__ __forceinline__ void build_stat(const DevPattern &P, int xs) {
             else e = t;
             pr |= ((uint32_t)e & 0xFFFFu) << (16 * h);
         }
-        g_st.col[i] = pr;
+        stt<SelT<SEL>::pack16>().col[i] = pr;
     }
 }
+
+// CTAs per SM the single-query kernels are compiled for: three for the static
+// lin16 Greedy kernels (80 registers, a few spills outside the hot loop; C4
+// 84.8 -> 82.9 us), two otherwise (the Eq. 3 kernel spilled more at 80
+// registers and ran 3 % slower)
+template <int SEL>
+constexpr int kCtasPerSm = SelT<SEL>::stat && SelT<SEL>::lin16 && SelT<SEL>::base == SEL_GREEDY ? 3 : 2;
 
 // ---------------------------------------------------------------- single query
 // Items = prefixes of depth D, in chunks of `chunk` consecutive items; local
 // chunk q of rank r is global chunk q*world + r.  Group g of a warp walks the
 // g-th slice of the chunk.
 template <int W, int K, int SEL>
-__global__ void __launch_bounds__(kBlock, 2)
+__global__ void __launch_bounds__(kBlock, kCtasPerSm<SEL>)
 esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict__ dq,
            mapa_record *__restrict__ rec, int D, int rank, int world, int stripe) {
     constexpr int G = 32 / W;
@@ -1520,12 +1548,14 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
     }
     // the query load is issued first: its latency overlaps the table copy
     const uint32_t busy = *reinterpret_cast<const volatile uint32_t *>(&dq->busy);
-    if constexpr (SelT<SEL>::pack16) {
-        // g_lut1 must sit where lds_lut1's immediate points (see kLut1Addr)
-        if ((uint32_t)__cvta_generic_to_shared(g_lut1) != kLut1Addr) {
+    if constexpr (SelT<SEL>::pack16 || SelT<SEL>::stat) {
+        // the static tables must sit where the immediates point (see kLut1Addr)
+        if ((uint32_t)__cvta_generic_to_shared(stat_base<SelT<SEL>::pack16>()) != kLut1Addr) {
             if (tid == 0) atomicExch(&rec->status, 2u);
             return;
         }
+    }
+    if constexpr (SelT<SEL>::pack16) {
         // (static path: an index carries up to three sentinels -> 4 regions)
         load_shared(tb, xs, ub_r2, SEL & 3, g_lut1, SelT<SEL>::stat ? 4 : 3);
     } else {
@@ -1809,6 +1839,10 @@ template <int MAXP, int LUTCAP>
 int smem_bytes(const Tables<MAXP, LUTCAP> &tb) {
     return (int)sizeof(Shared) + (tb.npats * 3 + 1) * tb.xs * tb.xs * (int)sizeof(int);
 }
+
+// dynamic shared memory of a single-query kernel: the additive selectors read
+// no Eq. 2 table, the Eq. 2 kernels keep theirs in static memory (g_stL)
+inline int smem_single(int sc, int smem) { return (sc & 3) == SEL_SENS ? smem : (int)sizeof(Shared); }
 
 inline int set_smem(const void *f, int bytes) {
     return (int)cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);

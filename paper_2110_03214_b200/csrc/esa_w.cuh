@@ -16,7 +16,7 @@ namespace {
 template <int W, int K, int SEL>
 int do_launch_single(const SingleTables &tb, const mapa_query *dq, mapa_record *rec, int D, int rank, int world,
                      int stripe, int grid, cudaStream_t st) {
-    const int smem = smem_bytes(tb);
+    const int smem = smem_single(SEL, smem_bytes(tb));
     // the attribute is always set to the fixed upper bound (see kSmemSingleMax),
     // so the occupancy query and every launch agree
     // kernel attributes are per device: one flag bit per device ordinal
@@ -136,7 +136,7 @@ int MAPA_PNAME(occ_single_w)(int K, int sc, int smem) {
     const void *f = pick_fn(K, sc);
     int nb = 0;
     if (!f || set_smem(f, kSmemSingleMax) != 0) return 1;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kBlock, smem) != cudaSuccess) return 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kBlock, smem_single(sc, smem)) != cudaSuccess) return 1;
     return nb > 0 ? nb : 1;
 }
 #else
