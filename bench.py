@@ -416,17 +416,22 @@ def main():
         dom = max(kern_ms, key=kern_ms.get)
         leaves_per_launch = RAW_PER_QUERY / world
         achieved = ALG_OPS[dom] * leaves_per_launch / (kern_ms[dom] / 1e3) / 1e9
-        traffic, lipe = None, None
+        traffic, lipe, swpe = None, None, None
         try:
             prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
             traffic = prof.get("dram_bytes_per_launch", {}).get(dom)
             lipe = prof.get("lane_instr_per_embedding", {}).get(dom)
+            swpe = prof.get("smem_wavefronts_per_embedding", {}).get(dom)
         except Exception:
             pass
         # issue_frac: the kernel's executed lane-instructions per embedding (ncu,
         # profiles/ncu_summary.json) x embeddings/s / the measured issue peak
         emb_s = leaves_per_launch / (kern_ms[dom] / 1e3)
         issue_frac = lipe * emb_s / (peak * 1e9) if lipe else None
+        # lsu_frac: shared-memory data-pipe wavefronts per embedding (ncu) x embeddings/s
+        # / (148 SMs x 1 wavefront per SM per clock x the max SM clock) -- the Eq. 2
+        # kernel's gathers make this its binding resource
+        lsu_frac = swpe * emb_s / (148 * max_mhz * 1e6) if swpe else None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             raw, dt, cores = cpu_oracle_sample()
@@ -452,11 +457,14 @@ def main():
                          "ops_per_embedding": ALG_OPS[dom], "ops_unamortised": ALG_OPS_UNAMORTISED[dom],
                          "frac_unamortised": ALG_OPS_UNAMORTISED[dom] * emb_s / (peak * 1e9),
                          "lane_instr_per_embedding": lipe, "issue_frac": issue_frac,
+                         "smem_wavefronts_per_embedding": swpe, "lsu_frac": lsu_frac,
                          "note": f"frac = {ALG_OPS[dom]} algorithmic int ops per embedding (complete the score from two "
                                  f"shared partials + compare; DESIGN.md Roofline) x embeddings/s / peak; peak = 148 SM x "
                                  f"{issue_lanes_per_sm_clk():.2f} lane-ops/SM/clk (measured issue rate, "
                                  f"profiles/r02_int_peaks.json) x {max_mhz:.0f} MHz (measured max SM clock); issue_frac = "
                                  f"ncu lane-instructions per embedding (profiles/ncu_summary.json) x embeddings/s / peak; "
+                                 f"lsu_frac = ncu shared-memory wavefronts per embedding x embeddings/s / (148 SM x 1 "
+                                 f"wavefront/SM/clk x the max SM clock) -- the Eq. 2 gathers' binding pipe; "
                                  f"frac_unamortised = SURVEY 8(d)'s per-embedding count (every weight re-read) over the "
                                  f"same peak, > 1 because the enumeration tree shares prefix work"},
             "cpu_baseline": cpu,

@@ -227,7 +227,7 @@ __device__ __forceinline__ bool bound_cut(const DeepTables &tb, M F, M U, int nd
         const int c = lane < nd ? __popc((uint32_t)tb.adj[lane] >> nd) * S.maxw[myf] : 0;
         ub = a + __reduce_add_sync(kFullD, c) + (int)tb.c2[nd] * S.gmax;
     }
-    const unsigned long long gk = *reinterpret_cast<const volatile unsigned long long *>(gpub);
+    const unsigned long long gk = ld_relaxed(gpub);
     const unsigned gb = (unsigned)(gk >> 32);
     if (ub != (int)gb) return ub < (int)gb;
     const M R = F & ~U;
@@ -274,7 +274,7 @@ __device__ __forceinline__ void suffix_lanes2(const DeepTables &tb, const DeepWa
         if (lane >= mi1 && lane < r) m1 = pj0;
         if (lane + 32 >= mi1 && lane + 32 < r) m1 = max(m1, pj1);
         const int ub = A + __reduce_max_sync(kFullD, m0) + __reduce_max_sync(kFullD, m1) + e * S.gmax;
-        const unsigned gb = (unsigned)(*reinterpret_cast<volatile unsigned long long *>(gpub) >> 32);
+        const unsigned gb = (unsigned)(ld_relaxed(gpub) >> 32);
         if (ub < (int)gb) return;
     }
     int tie = nbest >= bst.set ? 0 : 1;  // score ties (see suffix)
@@ -406,7 +406,7 @@ __device__ __forceinline__ void suffix(const DeepTables &tb, M F, M U, int A, in
             }
             ub += __reduce_max_sync(kFullD, mx);
         }
-        const unsigned gb = (unsigned)(*reinterpret_cast<volatile unsigned long long *>(gpub) >> 32);
+        const unsigned gb = (unsigned)(ld_relaxed(gpub) >> 32);
         if (ub < (int)gb * tb.scale) {  // scaled units (Eq. 3 pair folding)
             __syncwarp();
             return;  // no tuple of this node can reach the best score found anywhere
@@ -542,7 +542,7 @@ esa_deep(const __grid_constant__ DeepTables tb, const uint16_t *__restrict__ lut
     for (;;) {
         uint32_t start = 0, sz = 0;
         if (lane == 0) {
-            const uint32_t cur = *reinterpret_cast<volatile uint32_t *>(&rec->ctr);
+            const uint32_t cur = ld_relaxed(&rec->ctr);
             const uint32_t rem = cur < Nloc ? Nloc - cur : 0u;
             sz = max(1u, rem / (2u * P));
             start = atomicAdd(&rec->ctr, sz);

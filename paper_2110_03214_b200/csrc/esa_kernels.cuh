@@ -824,7 +824,7 @@ __device__ __forceinline__ void inner3(const Ctx<W> &c, const St<K> &st, uint32_
     // lane's threshold may be raised to it; ties still reach the key builder)
     if constexpr (SelT<SEL>::cta) bst.thr = max(bst.thr, sh().cthr);
     if constexpr (SelT<SEL>::prune) {
-        const unsigned g = *reinterpret_cast<volatile unsigned *>(bst.gb);
+        const unsigned g = ld_relaxed(bst.gb);
         bst.pthr = max(bst.pthr, (int)(g * 32u));
         if constexpr (SelT<SEL>::lin) {
             // Bound of the whole prefix subtree for this lane (vertex k-1 on b).
@@ -1608,7 +1608,7 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
         } else {
             if (off0 >= Nloc) break;  // the static chunks covered every item: no counter round trip
             if (lane == 0) {
-                const uint32_t cur = off0 + *reinterpret_cast<volatile uint32_t *>(&rec->ctr);
+                const uint32_t cur = off0 + ld_relaxed(&rec->ctr);
                 if (cur < Nloc) {
                     sz = max(2u * G, (Nloc - cur) / (2u * P));
                     sz = (sz + G - 1u) / G * G;

@@ -58,6 +58,23 @@ static_assert(sizeof(DevPattern) == 64, "DevPattern layout");
 // meaning: esa_kernels.cuh `Shared`), built per CTA, or copied from a cached
 // device image built once per (topology, Eq. 2 row stride) on the host.
 constexpr int kNegTable = -(1 << 28);
+
+#ifdef __CUDACC__
+// Relaxed GPU-scope reads of words other CTAs update with atomics (work
+// counters, published bounds).  A `volatile` read compiles to a system-scope
+// strong load (LDG.E.STRONG.SYS), which is slower and serialises under
+// contention; these are only hints or are re-checked by the atomic that follows.
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+#endif
 // lin16 single-query scans (16-bit Eq. 1 / Eq. 3): the largest 32 (50 (k-2) +
 // inc_F spread) the kernels accept -- the per-v3-table path (prune mode) and
 // the static-table path (esa_kernels.cuh, kStX / kStY / kStZ)

@@ -104,6 +104,9 @@ def main():
                     "dram_bytes_per_launch": {n[3:]: dram[n] for n in KERNELS[:3]},
                     "lane_instr_per_embedding": {n[3:]: byk[n]["smsp__inst_executed.sum"] * 32 / emb
                                                  for n in KERNELS[:3]},
+                    # shared-memory data-pipe wavefronts (1 per SM per clock at most) per embedding
+                    "smem_wavefronts_per_embedding": {
+                        n[3:]: byk[n]["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"] / emb for n in KERNELS[:3]},
                     "kernel_us_ncu": {n: _us(byk[n]["gpu__time_duration.sum"], byk[n]["gpu__time_duration.sum.unit"])
                                       for n in KERNELS},
                     "config_traffic": {n: dram[n] for n in KERNELS[3:]}}

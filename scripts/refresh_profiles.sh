@@ -8,6 +8,8 @@
 # --configs, run on the box: the report itself exceeds gpurun's 64 MiB return limit).
 set -u
 TAG=${1:-r02}
+# (the full ncu pass: ncu --set full --import-source on --clock-control none -k regex:esa_ \
+#   -o gpurun_out/${TAG}_cfg python scripts/prof_configs.py, then ncu_summary.py --configs)
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${TAG}_smi.txt
 python bench.py > gpurun_out/${TAG}_bench_c4_n1.json 2> gpurun_out/${TAG}_bench_c4.err
@@ -19,6 +21,9 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 python scripts/kern_time.py > gpurun_out/${TAG}_kern_time.txt 2>&1
 python scripts/shard_probe.py > gpurun_out/${TAG}_shard_probe.txt 2>&1
 python scripts/stream_probe.py > gpurun_out/${TAG}_stream_probe.txt 2>&1
+python scripts/graph_probe.py > gpurun_out/${TAG}_graph_probe.txt 2>&1
+ncu --metrics gpu__time_duration.sum,sm__cycles_active.avg,launch__grid_size --clock-control none --csv \
+    --log-file gpurun_out/${TAG}_fixed_cost.csv python scripts/fixed_probe.py > /dev/null 2>&1
 python scripts/deep_rate.py > gpurun_out/${TAG}_deep_rate.txt 2>&1
 python scripts/sim_report.py > gpurun_out/${TAG}_sim_report.json 2> gpurun_out/${TAG}_sim_report.err
 tail -c 400 gpurun_out/${TAG}_bench_c4_n1.json
