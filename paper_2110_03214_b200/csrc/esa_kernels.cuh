@@ -1098,10 +1098,17 @@ __device__ __forceinline__ void inner3s(const Ctx<W> &c, const St<K> &st, uint32
         bst.cnt += (uint32_t)(__popc(cand3 & nb) * __popc(cand2b & nb) - __popc(cand3 & cand2b & nb));
     }
     if constexpr (!SelT<SEL>::lin) {
+        // the next v3's list entry and w(v3, b) are loaded one iteration
+        // ahead (the LDS -> LDS -> base chain is off the scan's critical path;
+        // `& 31` keeps the read in bounds when the list is empty)
+        int2 e3n = L3[0];
+        int w3n = wcol[((uint32_t)e3n.x & 31u) * 32];
         for (uint32_t i = 0; i < n3; ++i) {
-            const int2 e3 = L3[i];
+            const int2 e3 = e3n;
+            const int w3 = w3n;
+            e3n = L3[min(i + 1u, n3 - 1u)];
+            w3n = wcol[((uint32_t)e3n.x & 31u) * 32];
             const uint32_t v3 = (uint32_t)e3.x;
-            const int w3 = wcol[v3 * 32];
             const bool laneok = okb && b != v3 && (!d31 || b > v3);
             const int base = A + e3.y + lpb + m31 * w3;
             const uint32_t row = v3 * (2u * W);  // byte offset of row v3
@@ -1126,8 +1133,8 @@ __device__ __forceinline__ void inner3s(const Ctx<W> &c, const St<K> &st, uint32
         for (uint32_t i = 0; i < n3; i += 2) {
             const bool hasB = i + 1 < n3;
             const int2 eA = L3[i], eB = L3[hasB ? i + 1 : i];
+            const int wA = wcol[(uint32_t)eA.x * 32], wB = wcol[(uint32_t)eB.x * 32];
             const uint32_t vA = (uint32_t)eA.x, vB = (uint32_t)eB.x;
-            const int wA = wcol[vA * 32], wB = wcol[vB * 32];
             const bool okA = okb && b != vA && (!d31 || b > vA);
             const bool okB = hasB && okb && b != vB && (!d31 || b > vB);
             const int offA = (A + eA.y + lpb + m31 * wA + 1 - c.ishift) * 32;
