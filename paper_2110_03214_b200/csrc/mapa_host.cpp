@@ -20,6 +20,8 @@
 
 #include "internal.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 using namespace mapa;
 
 // One cached mapa_allocate sequence (H2D query, record zeroing, kernel, D2H
@@ -93,6 +95,15 @@ struct mapa_pattern {
 };
 
 namespace {
+
+// NVTX range over a C-ABI entry point (SURVEY §5 tracing; header-only NVTX v3:
+// a no-op unless a profiler injects itself)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 thread_local std::string g_err;
 
@@ -1232,6 +1243,7 @@ mapa_status mapa_launch_query(const mapa_topology *t, const mapa_pattern *p, int
                                   int32_t sensitive, const mapa_query *d_query, mapa_record *d_record,
                                   uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint,
                                   void *stream) {
+    const NvtxRange nvtx_range_("mapa_launch_query");
     return launch_query_impl(t, p, selector, sensitive, d_query, d_record, flags, rank, world, busy_hint, stream,
                              !(flags & MAPA_F_ZEROED));
 }
@@ -1273,6 +1285,7 @@ static mapa_status launch_query_impl(const mapa_topology *t, const mapa_pattern 
 mapa_status mapa_launch_queries(mapa_topology *t, const mapa_pattern *const *pats, int32_t npats, int32_t nq,
                                 const mapa_query *h_queries, const mapa_query *d_queries, mapa_record *d_records,
                                 uint32_t flags, int32_t nstreams, void *stream) {
+    const NvtxRange nvtx_range_("mapa_launch_queries");
     if (!t || !pats || nq < 0 || (nq > 0 && (!h_queries || !d_queries || !d_records)) || nstreams < 1 || nstreams > 32)
         return fail(MAPA_E_INVALID_ARG, "bad arguments");
     if (nq == 0) return MAPA_OK;
@@ -1406,6 +1419,7 @@ mapa_status mapa_decode(const mapa_topology *t, const mapa_pattern *p, uint64_t 
 mapa_status mapa_launch_query_wide(const mapa_topology *t, const mapa_pattern *p, int32_t selector,
                                    int32_t sensitive, const mapa_query64 *d_query, mapa_wide_record *d_record,
                                    uint32_t flags, int32_t rank, int32_t world, uint64_t busy_hint, void *stream) {
+    const NvtxRange nvtx_range_("mapa_launch_query_wide");
     return launch_query_wide_impl(t, p, selector, sensitive, d_query, d_record, flags, rank, world, busy_hint,
                                   stream, !(flags & MAPA_F_ZEROED));
 }
@@ -1641,6 +1655,7 @@ static mapa_status allocate_insens_sets(mapa_topology *t, const mapa_pattern *pc
 
 mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selector, int32_t sens,
                           uint32_t flags, void *stream, mapa_decision *out) {
+    const NvtxRange nvtx_range_("mapa_allocate");
     if (!t || !p || !out) return fail(MAPA_E_INVALID_ARG, "null argument");
     if (selector < 0 || selector > 2) return fail(MAPA_E_INVALID_ARG, "bad selector");
     const bool deep = (flags & MAPA_F_DEEP) || !key_fits(t, p);
@@ -1749,6 +1764,7 @@ mapa_status mapa_allocate(mapa_topology *t, const mapa_pattern *p, int32_t selec
 
 mapa_status mapa_allocate_many(mapa_topology *t, const mapa_pattern *const *pats, int32_t nq, const int32_t *selector,
                                const int32_t *sensitive, uint32_t flags, void *stream, mapa_decision *out) {
+    const NvtxRange nvtx_range_("mapa_allocate_many");
     if (!t || nq < 1 || nq > 32 || !pats || !selector || !sensitive || !out)
         return fail(MAPA_E_INVALID_ARG, "bad allocate_many arguments (1 <= nq <= 32)");
     if (flags & MAPA_F_COMMIT) return fail(MAPA_E_INVALID_ARG, "allocate_many never commits (independent queries)");
@@ -1887,6 +1903,7 @@ mapa_status mapa_allocate_many(mapa_topology *t, const mapa_pattern *const *pats
 mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *const *pats, int32_t npats,
                                 int64_t nq, const mapa_query *d_queries, mapa_record *d_results,
                                 void *d_scratch, uint32_t flags, void *stream) {
+    const NvtxRange nvtx_range_("mapa_allocate_batch");
     if (!t || !pats || (nq > 0 && (!d_queries || !d_results || !d_scratch)) || nq < 0)
         return fail(MAPA_E_INVALID_ARG, "null argument");
     if (flags & MAPA_F_PRUNE) return fail(MAPA_E_UNSUPPORTED, "MAPA_F_PRUNE is single-query only");
@@ -1924,6 +1941,7 @@ mapa_status mapa_allocate_batch(const mapa_topology *t, const mapa_pattern *cons
 mapa_status mapa_trace_replay(const mapa_topology *t, const mapa_pattern *const *pats, int32_t npats,
                               int32_t ntraces, int32_t nops, const mapa_trace_op *d_ops, int32_t njobs,
                               const mapa_query *d_jobs, uint64_t *d_keys, uint32_t flags, void *stream) {
+    const NvtxRange nvtx_range_("mapa_trace_replay");
     if (!t || !pats || ntraces < 0 || nops < 0 || njobs < 0) return fail(MAPA_E_INVALID_ARG, "bad argument");
     if (flags & MAPA_F_PRUNE) return fail(MAPA_E_UNSUPPORTED, "MAPA_F_PRUNE is single-query only");
     if (ntraces == 0) return MAPA_OK;
@@ -1985,6 +2003,7 @@ mapa_status mapa_fifo_schedule(int32_t n_devices, int32_t njobs, const int32_t *
 
 mapa_status mapa_simulate(const mapa_topology *t, const mapa_pattern *const *pats, int32_t npats, int32_t njobs,
                           const mapa_job *jobs, int32_t policy, uint32_t flags, void *stream, mapa_job_log *out) {
+    const NvtxRange nvtx_range_("mapa_simulate");
     if (!t || !pats || njobs < 0 || (njobs > 0 && (!jobs || !out))) return fail(MAPA_E_INVALID_ARG, "null argument");
     if (policy < MAPA_POLICY_BASELINE || policy > MAPA_POLICY_PRESERVE) return fail(MAPA_E_INVALID_ARG, "bad policy");
     if (njobs == 0) return MAPA_OK;

@@ -75,20 +75,28 @@ def run_queries(topo: Topology, pats, rows, raw: bool = False, nstreams: int = 8
     return recs[:len(rows)]
 
 
+def gather_records(rec: torch.Tensor, width: int, group=None) -> torch.Tensor:
+    """The one collective of a sharded allocation: all_gather every rank's
+    record (`width` int64 words: 4 narrow, 8 deep) -> int64[world, width].
+    NCCL: device tensors, all_gather_into_tensor (NVLink / NVSwitch); gloo (the
+    CPU tests of the multi-rank path): host tensors."""
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((world, width), dtype=torch.int64, device=rec.device)
+        dist.all_gather_into_tensor(out, rec.reshape(width), group=group)
+        return out
+    parts = [torch.empty(width, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(parts, rec.reshape(width).cpu(), group=group)
+    return torch.stack(parts)
+
+
 def combine_records(rec: torch.Tensor, group=None) -> Record:
     """all_gather the per-rank 32-B records (one collective) and combine them
     by max(key), sum(leaves) on the host."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return records_from_tensor(rec)[0]
-    if dist.get_backend(group) == "nccl":
-        out = torch.empty((world, 4), dtype=torch.int64, device=rec.device)
-        dist.all_gather_into_tensor(out, rec.reshape(4), group=group)
-    else:  # gloo (CPU tests of the multi-rank path): host tensors
-        parts = [torch.empty(4, dtype=torch.int64) for _ in range(world)]
-        dist.all_gather(parts, rec.reshape(4).cpu(), group=group)
-        out = torch.stack(parts)
-    return reduce_records(records_from_tensor(out))
+    return reduce_records(records_from_tensor(gather_records(rec, 4, group)))
 
 
 def allocate_sharded(topo: Topology, pat: Pattern, selector: int, sensitive: bool, busy: int, raw: bool = False,
@@ -139,14 +147,7 @@ def combine_wide_records(rec: torch.Tensor, group=None) -> WideRecord:
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return wide_records_from_tensor(rec)[0]
-    if dist.get_backend(group) == "nccl":
-        out = torch.empty((world, 8), dtype=torch.int64, device=rec.device)
-        dist.all_gather_into_tensor(out, rec.reshape(8), group=group)
-    else:
-        parts = [torch.empty(8, dtype=torch.int64) for _ in range(world)]
-        dist.all_gather(parts, rec.reshape(8).cpu(), group=group)
-        out = torch.stack(parts)
-    return reduce_wide_records(wide_records_from_tensor(out))
+    return reduce_wide_records(wide_records_from_tensor(gather_records(rec, 8, group)))
 
 
 def allocate_sharded_wide(topo: Topology, pat: Pattern, selector: int, sensitive: bool, busy: int,
