@@ -160,7 +160,12 @@ typedef struct {
     uint64_t key;
     uint64_t leaves;     /* leaves scored */
     uint32_t ctr;        /* work-item counter (scratch, zeroed by the launch) */
-    uint32_t status;     /* 0 ok; nonzero = device-side argument error */
+    uint32_t status;     /* 0 ok; nonzero = the launch refused the query and scored nothing:
+                            1 = the 16-bit scan's range does not fit this free set (a busy_hint
+                            that lied: see mapa_launch_query), 2 = the single-query kernel's
+                            static shared tables are not at the window address its code
+                            addresses them by (never seen; a guard, not a mode) -- mapa_decode
+                            reports MAPA_E_INVALID_ARG for both */
     uint64_t reserved;   /* scratch (MAPA_F_PRUNE: best score + 1 found so far), zeroed by the launch */
 } mapa_record;
 

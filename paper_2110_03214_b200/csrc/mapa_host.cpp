@@ -948,7 +948,9 @@ mapa_status decode_wide(const mapa_topology *t, const mapa_pattern *p, uint64_t 
         d.distinct_matches = rec->leaves;
         d.raw_embeddings = rec->leaves * p->aut;
     }
-    if (rec->status != 0) return fail(MAPA_E_INVALID_ARG, "device reported a bad query (busy_hint != d_query->busy?)");
+    if (rec->status != 0)
+        return fail(MAPA_E_INVALID_ARG, rec->status == 2 ? "device refused the query: static shared tables misplaced"
+                                                          : "device reported a bad query (busy_hint != d_query->busy?)");
     if (rec->set == 0) {
         d.status = MAPA_NO_CAPACITY;
         *out = d;
@@ -1002,7 +1004,9 @@ mapa_status decode_record(const mapa_topology *t, const mapa_pattern *p, uint64_
         d.distinct_matches = rec->leaves;
         d.raw_embeddings = rec->leaves * (uint64_t)p->aut;
     }
-    if (rec->status != 0) return fail(MAPA_E_INVALID_ARG, "device reported a bad query");
+    if (rec->status != 0)
+        return fail(MAPA_E_INVALID_ARG, rec->status == 2 ? "device refused the query: static shared tables misplaced"
+                                                          : "device reported a bad query");
     if (rec->key == 0) {
         d.status = MAPA_NO_CAPACITY;
         *out = d;
