@@ -78,7 +78,9 @@ struct SelT {
     // bit 5: single-query Eq. 1 / Eq. 3 scans on 16-bit lanes (two leaves per
     // VIADDMNMX.S16x2); the host sets it only when every scan value fits s16
     // (lin16_fits in mapa_host.cpp)
-    static constexpr bool lin16 = (SEL & 32) != 0 && lin && !multi;
+    // (batch kernels too: esa_batch picks it per query, from the query's own
+    // free set; the trace kernel never sets bit 5)
+    static constexpr bool lin16 = (SEL & 32) != 0 && lin;
     static constexpr bool half = pack16 || lin16;      // 16-bit table entries
     // single-query additive kernels share the CTA's best score as the hit
     // threshold (Shared::cthr, folded into the lane's Best::thr at each inner3
@@ -90,7 +92,7 @@ struct SelT {
     // levels on static tables (inner3s / inners): per v3 the scan reads the
     // k-3 -> k-2 edge row of a table built once per CTA, and the lane's
     // column is re-based once per k-3 prefix, so no per-v3 table is built
-    static constexpr bool stat = (pack16 || lin16) && !prune;
+    static constexpr bool stat = (pack16 || lin16) && !prune && !multi;
     static constexpr bool useU = base == SEL_INSENS;   // Eq. 3 sums over every placed device
     static constexpr int wt = base == SEL_BASE ? 0 : 1;
     static constexpr int w0 = 38 * wt, w1 = 13 * wt, w2 = 8 * wt, w12 = 12 * wt;
@@ -1662,7 +1664,9 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
 // K = 1 queries use slot 0 only (depth 0).
 template <int W, int K, int SEL>
 __device__ __forceinline__ void batch_item(const Ctx<W> &c, uint32_t j, Best &bst) {
-    if constexpr (K == 1) {
+    if constexpr (SelT<SEL>::lin16 && K < 3) {
+        return;  // never dispatched (lin16 from k = 3)
+    } else if constexpr (K == 1) {
         if (j == 0) leaf_k1<W, SEL>(c, bst);
     } else {
         if (j < (uint32_t)c.nF) run_range<W, K, SEL, 1>(c, j, j + 1, 1, bst);
@@ -1714,13 +1718,28 @@ esa_batch(const __grid_constant__ MultiTables tb, long long nq, const mapa_query
             continue;
         }
         const DevPattern &P = tb.pat[pid];
-        Ctx<W> c = make_ctx<W>(tb.topo, P, (int)pid, xs, qu.busy, sel_code(qu.selector, qu.sensitive), false);
+        const int scq = sel_code(qu.selector, qu.sensitive);
+        // 16-bit scans (two leaves per VIADDMNMX.S16x2) for the additive
+        // selectors when this query's free set keeps every sum in range (the
+        // single-query kernels' lin16, decided here per query, exactly)
+        bool l16 = W >= 16 && P.k >= 3 && (scq == SEL_GREEDY || scq == SEL_INSENS);
+        Ctx<W> c = make_ctx<W>(tb.topo, P, (int)pid, xs, qu.busy, scq, false, l16);
+        if (l16 && 32 * (50 * (P.k - 2) + c.irange) > kLin16Max) {
+            l16 = false;
+            c = make_ctx<W>(tb.topo, P, (int)pid, xs, qu.busy, scq, false, false);
+        }
         if (P.k > c.nF) continue;
         const uint32_t j = (uint32_t)(base % W) + g;
         Best bst{0ull, 0u, 0u, 32, 0u, 32, nullptr};
-        switch (sel_code(qu.selector, qu.sensitive)) {
-            case SEL_GREEDY: batch_dispatch_k<W, SEL_GREEDY | 4 * CANON | 8>(P.k, c, j, bst); break;
-            case SEL_INSENS: batch_dispatch_k<W, SEL_INSENS | 4 * CANON | 8>(P.k, c, j, bst); break;
+        switch (scq) {
+            case SEL_GREEDY:
+                if (W >= 16 && l16) batch_dispatch_k<W, SEL_GREEDY | 4 * CANON | 8 | 32 * (W >= 16)>(P.k, c, j, bst);
+                else batch_dispatch_k<W, SEL_GREEDY | 4 * CANON | 8>(P.k, c, j, bst);
+                break;
+            case SEL_INSENS:
+                if (W >= 16 && l16) batch_dispatch_k<W, SEL_INSENS | 4 * CANON | 8 | 32 * (W >= 16)>(P.k, c, j, bst);
+                else batch_dispatch_k<W, SEL_INSENS | 4 * CANON | 8>(P.k, c, j, bst);
+                break;
             case SEL_SENS: batch_dispatch_k<W, SEL_SENS | 4 * CANON | 8>(P.k, c, j, bst); break;
             default: batch_dispatch_k<W, SEL_BASE | 4 * CANON | 8>(P.k, c, j, bst); break;
         }
