@@ -172,7 +172,8 @@ struct StatSharedL {
 };
 __shared__ __align__(16) StatSharedL g_stL;
 __shared__ __align__(16) StatTabs g_stN;
-#define g_lut1 (g_stL.lut)
+// the Eq. 2 kernels' LUT (at kLut1Addr)
+__device__ __forceinline__ int *lut1() { return g_stL.lut; }
 template <bool L>
 __device__ __forceinline__ StatTabs &stt() {
     if constexpr (L) return g_stL.t;
@@ -204,7 +205,7 @@ constexpr int kStTmax = kLin16StatMax;
 static_assert(kStTmax == -kStY - 1632 && kStTmax == -kStZ - 1632, "see kLin16StatMax");
 static_assert(-(kStX + kStY + kStZ) <= 32768, "s16 range");
 
-// gather at byte offset `off` of g_lut1 (volatile: never merged with another
+// gather at byte offset `off` of lut1() (volatile: never merged with another
 // load, so no gathered value is kept live across the hit branch)
 __device__ __forceinline__ int lds_lut1(uint32_t off) {
     int v;
@@ -481,7 +482,7 @@ __device__ __forceinline__ int tab_scan(const Ctx<W> &c, const int *tab, int bas
         // ops per 2 leaves (IADD3, SHF, 3-input max); the (31 - v) tie-break
         // goes in as IMAD r*one + (31-v) (FMA pipe).
         const uint4 *t8 = reinterpret_cast<const uint4 *>(tab);
-        const int *lut = g_lut1;
+        const int *lut = lut1();
         const uint32_t b4 = __funnelshift_l(0u, (uint32_t)base, 2);
         const uint32_t bp = b4 | (b4 << 16);
         const int one = c.one, negk = c.negk;
@@ -637,7 +638,7 @@ __device__ __forceinline__ int scan_row_max(uint32_t row, const uint32_t (&colT)
 template <int W>
 __device__ __forceinline__ int scan_row_tie(uint32_t row, const uint32_t (&colT)[W / 2], int base, int one,
                                             int negk) {
-    const int *lut = g_lut1;
+    const int *lut = lut1();
     const uint32_t b4 = __funnelshift_l(0u, (uint32_t)base, 2);
     const uint32_t bp = b4 | (b4 << 16);
     int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
@@ -713,7 +714,7 @@ template <int W, int SEL>
 __device__ __forceinline__ bool scan_needed(const Ctx<W> &c, const Best &bst, int entry, int base, bool laneok) {
     int ub;
     if constexpr (SelT<SEL>::lin) ub = base + grp_max<W>(c, entry) + c.colmax;
-    else ub = g_lut1[3 * c.xs * c.xs + base] + 31;  // prune mode: single-query only
+    else ub = lut1()[3 * c.xs * c.xs + base] + 31;  // prune mode: single-query only
     return __any_sync(c.gmask, laneok && ub >= bst.pthr);
 }
 
@@ -1453,7 +1454,7 @@ __device__ __forceinline__ void load_shared(const Tables<MAXP, LUTCAP> &tb, int 
             for (int t = 0; t < kPairTables; ++t) pt[t * kNN + i] = e[t];
         }
     }
-    if (!lut) lut = sh_lut();  // single-query Eq. 2 kernels pass g_lut1
+    if (!lut) lut = sh_lut();  // single-query Eq. 2 kernels pass lut1()
     // single-query additive kernels read no Eq. 2 table (and get no dynamic
     // shared memory for it: smem_single)
     const int nlut = only_sc >= 0 && (only_sc & 3) != SEL_SENS ? 0 : tb.npats;
@@ -1566,7 +1567,7 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
     }
     if constexpr (SelT<SEL>::pack16) {
         // (static path: an index carries up to three sentinels -> 4 regions)
-        load_shared(tb, xs, ub_r2, SEL & 3, g_lut1, SelT<SEL>::stat ? 4 : 3);
+        load_shared(tb, xs, ub_r2, SEL & 3, lut1(), SelT<SEL>::stat ? 4 : 3);
     } else {
         load_shared(tb, xs, ub_r2, SEL & 3);
     }
