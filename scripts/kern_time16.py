@@ -37,4 +37,4 @@ for nfree in (16, 14, 12):
             row.append(statistics.median(ts))
         n = math.perm(nfree, 8)
         print(f"free {nfree} {shape}-8: greedy {row[0]:.1f} sens {row[1]:.1f} insens {row[2]:.1f} us "
-              f"({n / row[0] / 1e6:.3g} / {n / row[1] / 1e6:.3g} / {n / row[2] / 1e6:.3g} M emb/s... x1e6)", flush=True)
+              f"({n / row[0] / 1e6:.3g} / {n / row[1] / 1e6:.3g} / {n / row[2] / 1e6:.3g} e12 embeddings/s)", flush=True)
