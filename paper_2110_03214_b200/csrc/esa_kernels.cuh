@@ -1604,7 +1604,12 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
     // so a launch starts without P same-address atomics; the counter then
     // hands out [off0, Nloc), and a warp that reads it exhausted leaves
     // without an atomic.
-    const uint32_t s0 = (max(2u * G, Nloc / (2u * P)) + G - 1u) / G * G;
+    // (chunks of at least one item per group and two per warp: a minimum of
+    // two items per GROUP left warps of the W <= 16 kernels idle on queries
+    // with few prefixes -- cubemesh16 k = 8 at 12 free: 62 -> 51 us; W = 32
+    // keeps two per warp, measured no better with one)
+    const uint32_t cmin = max(2u, (uint32_t)G);
+    const uint32_t s0 = (max(cmin, Nloc / (2u * P)) + G - 1u) / G * G;
     const uint32_t off0 = (uint32_t)min((unsigned long long)P * s0, (unsigned long long)Nloc);
     const uint32_t gw = blockIdx.x * (uint32_t)kWarps + (uint32_t)warp;
     bool first = true;
@@ -1620,7 +1625,7 @@ esa_single(const __grid_constant__ SingleTables tb, const mapa_query *__restrict
             if (lane == 0) {
                 const uint32_t cur = off0 + ld_relaxed(&rec->ctr);
                 if (cur < Nloc) {
-                    sz = max(2u * G, (Nloc - cur) / (2u * P));
+                    sz = max(cmin, (Nloc - cur) / (2u * P));
                     sz = (sz + G - 1u) / G * G;
                     start = off0 + atomicAdd(&rec->ctr, sz);
                 }
